@@ -1,0 +1,472 @@
+"""Benchmark of the seriesinv B200 hot path (BASELINE.json metric).
+
+Default workload = BASELINE config 4: dense SPD n=16384 (Householder-product
+eigenbasis, lambda log-uniform in [1, 1e6]), 64 right-hand sides; one step =
+one plain Richardson update with P_k + one composite Newton-Schulz
+step with rates (2,3,4,5), order_n=2 (newton_schulz.py:177-228) -- the
+reference GEMM DAG, 22 n^3 products + 2 n^2 r products, recomputed every step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c1|c2|c3|c4|c5] [--n N]
+
+Prints ONE JSON line on rank 0.  Timing: CUDA events on the launching stream,
+barrier + synchronize on both sides, max over ranks; inputs (2.1 GB per matrix)
+are far larger than the 126 MB L2, so no flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "iters/s and FP64 TFLOP/s (% of peak) of composite Newton-Schulz at n=16384"
+
+
+# --------------------------------------------------------------------------- helpers
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[6]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+            "power_w_median": statistics.median(power) if power else None,
+        }
+
+
+def dist_setup(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------------------- workloads
+
+
+class Workload:
+    """One config: device state + one step function + algorithmic FLOPs per step."""
+
+    def __init__(self, cfg: str, n: int | None):
+        self.cfg = cfg
+        self.n = n
+
+    # FLOPs of the executed reference DAG per step (2 M N K summed)
+    def flops(self) -> float:
+        n = self.n
+        if self.cfg == "c4":
+            return 22 * 2.0 * n**3 + 2 * 2.0 * n * n * self.r
+        if self.cfg == "c3":
+            return 6 * 2.0 * n**3 + 2 * 2.0 * n * n
+        if self.cfg == "c1":
+            return 3 * 2.0 * n**3 + 2 * 2.0 * n * n
+        if self.cfg == "c5":
+            return self.mmm_per_step * 2.0 * n**3 + 2 * 2.0 * n * n * self.r
+        if self.cfg == "c2":
+            return self.batch * (10 * 2.0 * 32**3 + 2 * 2.0 * 32 * 32)
+        raise ValueError(self.cfg)
+
+    def setup(self):
+        import torch
+
+        import paper_2008_11480_b200 as P
+        from paper_2008_11480_b200 import configs
+
+        self.P = P
+        cfg = self.cfg
+        if cfg == "c4":
+            self.n = self.n or 16384
+            self.r = 64
+            if self.n >= 4096:
+                a, b = configs.c4_householder_device(n=self.n, rhs=self.r)
+            else:
+                a, b = (P.as_device(x) for x in configs.c4_householder(n=self.n, rhs=self.r))
+            self.workload = f"c4: dense SPD n={self.n}, Householder(64) eigenbasis, kappa 1e6, {self.r} RHS; composite NS rates (2,3,4,5) order_n=2 + plain Richardson"
+        elif cfg == "c3":
+            self.n = self.n or 4096
+            self.r = 1
+            a_np, b_np = configs.c3_gram(n=self.n)
+            a, b = P.as_device(a_np), P.as_device(b_np)
+            self.workload = f"c3: Gram n={self.n}; order-8 factorised NS (h8) + plain Richardson"
+        elif cfg == "c1":
+            self.n = self.n or 64
+            self.r = 1
+            a_np, b_np = configs.c1_dense_small(n=self.n)
+            a, b = P.as_device(a_np), P.as_device(b_np)
+            self.workload = f"c1: dense SPD n={self.n}; NS order 3 + plain Richardson"
+        elif cfg == "c5":
+            self.n = self.n or 32768
+            self.r = 256
+            a, b = configs.c5_gram_device(n=self.n, m=int(self.n * 40000 / 32768), rhs=self.r)
+            self.workload = f"c5: Gram n={self.n}, {self.r} RHS; recursive Richardson/NS order 16"
+        elif cfg == "c2":
+            self.batch = self.n or 16384
+            a_np, b_np = configs.c2_batched(batch=self.batch)
+            self.a2, self.b2 = P.as_device(a_np), P.as_device(b_np)
+            self.pre2, self.res2 = P.batched_scalar_split(self.a2)
+            self.p2, self.f2 = self.pre2.clone(), self.res2.clone()
+            self.t2 = torch.zeros_like(self.b2)
+            self.workload = f"c2: {self.batch} systems 32x32; composite (2,3) order_n=2 + plain Richardson"
+            self.n = 32
+            return
+        else:
+            raise ValueError(cfg)
+        self.a = a
+        self.b = b
+        self.sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False, verify=False)
+        if cfg == "c5":
+            self.st = P.initial_richardson(self.sp, b, 0, 1, order=16, q=16)
+            self.plan16 = P.plan_order(16)
+            self.st = P.richardson_recursive_step(self.st, self.sp.matrix, b,
+                                                  factor_plan=self.plan16, doubling_sum=True)
+            self.mmm_per_step = 18
+        else:
+            order = {"c4": 2, "c3": 8, "c1": 3}[cfg]
+            self.st = P.initial_series(self.sp, 0, 1, order=order)
+            self.theta = torch.zeros_like(b)
+        self.spec = P.CompositeSpec((2, 3, 4, 5))
+        self.plan8 = P.table_plans()[8][0]
+
+    def step(self):
+        P = self.P
+        cfg = self.cfg
+        if cfg == "c2":
+            self.p2, self.f2, self.t2 = P.batched_composite_richardson(
+                self.a2, self.b2, self.pre2, self.res2, self.p2, self.f2, self.t2, (2, 3), 2, 1)
+            return
+        if cfg == "c5":
+            self.st = P.richardson_recursive_step(self.st, self.sp.matrix, self.b,
+                                                  factor_plan=self.plan16, doubling_sum=True)
+            return
+        self.theta = P.plain_richardson(self.theta, self.st.estimate, self.sp.matrix, self.b, self.st.ctr)
+        if cfg == "c4":
+            self.st = P.composite_step(self.st, self.sp.matrix, self.sp, self.spec, 2)
+        elif cfg == "c3":
+            self.st = P.ns_step(self.st, self.sp.matrix, plan=self.plan8)
+        else:
+            self.st = P.ns_step(self.st, self.sp.matrix)
+
+    def e2e_step(self, host):
+        """The public API called with HOST inputs: H2D of the step's inputs from pinned
+        memory, the step, D2H of its result; returns (h2d_bytes, d2h_bytes)."""
+        import torch
+
+        P = self.P
+        dev = self.a.device
+        d = {k: v.to(dev, non_blocking=True) for k, v in host["in"].items()}
+        sp = P.Splitting(precond=d["precond"], residual=d["residual"], matrix=d["a"], kind="scalar",
+                         verify=False)
+        st = P.NsState(estimate=d["g"], residual=d["f"], step=0, order=self.st.order,
+                       series_order=1, ctr=P.MulCounter())
+        theta = P.plain_richardson(d["theta"], st.estimate, sp.matrix, d["b"], st.ctr)
+        if self.cfg == "c4":
+            st = P.composite_step(st, sp.matrix, sp, self.spec, 2)
+        elif self.cfg == "c3":
+            st = P.ns_step(st, sp.matrix, plan=self.plan8)
+        else:
+            st = P.ns_step(st, sp.matrix)
+        host["out"]["g"].copy_(st.estimate, non_blocking=True)
+        host["out"]["f"].copy_(st.residual, non_blocking=True)
+        host["out"]["theta"].copy_(theta, non_blocking=True)
+        h2d = sum(v.numel() * 8 for v in host["in"].values())
+        d2h = sum(v.numel() * 8 for v in host["out"].values())
+        del d, st, theta, sp
+        return h2d, d2h
+
+    def pinned_inputs(self):
+        import torch
+
+        def pin(t):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            return h
+
+        host = {"in": {"a": pin(self.sp.matrix), "precond": pin(self.sp.precond),
+                       "residual": pin(self.sp.residual), "g": pin(self.st.estimate),
+                       "f": pin(self.st.residual), "b": pin(self.b), "theta": pin(self.theta)},
+                "out": {}}
+        host["out"] = {"g": torch.empty_like(host["in"]["g"], pin_memory=True),
+                       "f": torch.empty_like(host["in"]["f"], pin_memory=True),
+                       "theta": torch.empty_like(host["in"]["theta"], pin_memory=True)}
+        return host
+
+
+def cpu_sample(n: int, flops_step: float, reps: int = 1):
+    """Oracle (numpy, all host threads) on a bounded sample: one full-size n x n x n
+    product of the step's DAG (oracle.mm), extrapolated by the DAG's FLOP ratio."""
+    import numpy as np
+
+    from oracle import seriesinv_oracle as O
+
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((n, n))
+    y = rng.standard_normal((n, n))
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.mm(x, y, O.Counter())
+        ts.append(time.perf_counter() - t0)
+    t = min(ts)
+    step_s = t * flops_step / (2.0 * n**3)
+    return step_s, t
+
+
+# --------------------------------------------------------------------------- arms
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = args.config
+    n = args.n or {"c4": 16384, "c3": 4096, "c1": 64, "c5": 32768, "c2": 32}[cfg]
+    w = Workload(cfg, n)
+    w.r = {"c4": 64, "c5": 256}.get(cfg, 1)
+    w.mmm_per_step = 34
+    w.batch = args.n or 16384
+    flops = w.flops()
+    cores = host_cores()
+    sample_n = n if cfg not in ("c5",) else 16384
+    # each step: a bounded full-size sample, extrapolated to one step of the workload
+    step_times = []
+    for i in range(args.warmup + args.steps):
+        s, t = cpu_sample(sample_n, flops * (sample_n / n) ** 3 if cfg == "c5" else flops)
+        if cfg == "c5":
+            s *= (n / sample_n) ** 3
+        if i >= args.warmup:
+            step_times.append(s)
+    step_s = statistics.mean(step_times)
+    value = 1.0 / step_s
+    sample = (f"one {sample_n}^3 FP64 GEMM through oracle.mm (numpy/OpenBLAS, {cores} threads) "
+              f"per step, extrapolated by the step DAG's FLOP ratio ({flops:.4e} FLOP/step)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg, "n": n, "sample": "extrapolated"},
+        "tflops": flops / step_s / 1e12,
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    world, rank, local = dist_setup(args)
+    from paper_2008_11480_b200 import _lib
+
+    w = Workload(args.config, args.n)
+    w.setup()
+    flops = w.flops()
+    h = _lib.handle()
+    for _ in range(args.warmup):
+        w.step()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    _lib.call("si_profile_begin", h)
+    stream = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        w.step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    import ctypes
+
+    g_ms, g_fl = ctypes.c_double(), ctypes.c_double()
+    g_n, launches = ctypes.c_int64(), ctypes.c_int64()
+    _lib.call("si_profile_end", h, ctypes.byref(g_ms), ctypes.byref(g_fl), ctypes.byref(g_n),
+              ctypes.byref(launches))
+    clocks = sampler.stop()
+    barrier(world)
+    ms = e0.elapsed_time(e1)
+    ms_max = max_over_ranks(ms, world)
+    step_s = ms_max / 1e3 / args.steps
+    value = world * args.steps / (ms_max / 1e3)
+    tflops = flops / step_s / 1e12
+
+    peak = ctypes.c_double()
+    _lib.call("si_dmma_peak", h, 20000, ctypes.byref(peak))
+    achieved = (g_fl.value / (g_ms.value / 1e3) / 1e12) if g_ms.value > 0 else None
+
+    e2e = None
+    if not args.no_e2e and args.config in ("c4", "c3", "c1"):
+        host = w.pinned_inputs()
+        h2d = d2h = 0
+        ksteps = max(1, min(args.steps, 3))
+        w.e2e_step(host)  # warm
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(ksteps):
+            h2d, d2h = w.e2e_step(host)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks(f0.elapsed_time(f1), world)
+        e2e = {"value": world * ksteps / (e_ms / 1e3), "unit": "iters/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": ksteps}
+        del host
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and args.config in ("c4", "c3"):
+        s, t = cpu_sample(w.n, flops)
+        cpu = {"value": 1.0 / s, "unit": "iters/s", "cores": host_cores(), "kind": "port",
+               "sample": f"one {w.n}^3 FP64 GEMM through oracle.mm (numpy/OpenBLAS, all host "
+                         f"threads) in {t:.2f} s, extrapolated by the step's FLOP ratio"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded PCG64 draws, SURVEY Appendix A recipe)",
+            "config": {"workload": w.workload, "n": w.n,
+                       "parallelism": "replicas" if world > 1 else "single-gpu",
+                       "l2": "inputs larger than L2 (2.1 GB per matrix), no flush"},
+            "tflops": tflops,
+            "tflops_frac_of_dmma_peak": tflops / peak.value,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak.value,
+                         "unit": "TFLOP/s", "frac": (achieved / peak.value) if achieved else None,
+                         "traffic": None, "kernel": "gemm_f64_tma_kernel",
+                         "launches": g_n.value,
+                         "peak_source": "measured live: DMMA m8n8k4 register-only probe (si_dmma_peak); MEASURED_PEAKS.json has no FP64 entry"},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches.value,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c4")
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

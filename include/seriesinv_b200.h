@@ -1,0 +1,209 @@
+/*
+ * seriesinv_b200.h -- C ABI of the B200-native seriesinv hot path.
+ *
+ * Drop-in boundary for the FP64 matrix-product chains of arXiv 2008.11480's
+ * reference package `seriesinv` (/root/reference/pkg/src/seriesinv).  The
+ * reference has no FFI of its own (pure Python + numpy); its seams are
+ *   - the GEMM seam  mat_mul / mat_vec           (matrix_core.py:101-114), and
+ *   - the step seam  ns_step, composite_step, ...  (newton_schulz.py:127-325,
+ *                    richardson.py:61-189, series_toolkit.py:279-457).
+ * Each entry point below names the reference function it replaces.
+ *
+ * Conventions
+ *   - All matrix/vector pointers are DEVICE pointers to FP64 row-major data.
+ *     Step-level functions take contiguous n x n matrices (ld = n) and
+ *     contiguous n x nrhs right-hand sides (nrhs = 1 for a vector).
+ *   - Output buffers are caller-owned and must not alias inputs; inputs are
+ *     never written (the reference's states are immutable, matrix_core.py:52).
+ *     Temporaries come from a handle-owned stream-ordered memory pool.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *     asynchronous unless documented otherwise.
+ *   - `counters` (may be NULL) points at int64_t[2] = {mmm, mvm}; each call ADDS
+ *     the number of matrix-matrix / matrix-vector products it executed, which
+ *     equals the reference MulCounter delta for the same call
+ *     (matrix_core.py:71-98).
+ *   - Plans (series_toolkit.py FactorPlan trees) are passed as an int32 preorder
+ *     code plus a double constant pool; see INTEGRATION.md for the encoding.
+ *   - Every function returns SI_OK (0) or a negative status; it never throws
+ *     across the boundary.  si_last_error() returns a thread-local message.
+ *   - `concurrent` != 0 maps the reference's `executor` argument
+ *     (newton_schulz.py:254, richardson.py:111) to side CUDA streams joined by
+ *     events; results are bitwise identical to the serial path.
+ */
+#ifndef SERIESINV_B200_H
+#define SERIESINV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SI_OK 0
+#define SI_EINVAL (-1) /* bad argument: maps to ValueError */
+#define SI_ECUDA (-2)  /* CUDA launch / runtime failure: RuntimeError */
+#define SI_ENOMEM (-3) /* device allocation failure: MemoryError */
+
+#if defined(__GNUC__)
+#define SI_API __attribute__((visibility("default")))
+#else
+#define SI_API
+#endif
+
+typedef struct si_handle_s* si_handle;
+
+SI_API int si_version(void);
+SI_API const char* si_last_error(void);
+SI_API int si_create(int device, si_handle* out);
+SI_API int si_destroy(si_handle h);
+/* Release cached pool memory back to the device. */
+SI_API int si_trim(si_handle h);
+
+/* ---------------- GEMM seam (matrix_core.py:101-114) ---------------- */
+
+/* D = alpha*(A@B) + beta*C + diag*I with A m x k, B k x n, C/D m x n.
+ * One counted product (mvm if is_mv, else mmm).  Replaces mat_mul / mat_vec
+ * plus the element-wise op that follows it at the reference call site
+ * (e.g. `eye - mat_mul(x, a)` = alpha -1, diag 1; `mat_mul(y, z) + x` = beta 1). */
+SI_API int si_gemm(si_handle h, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+            int64_t lda, const double* B, int64_t ldb, double beta, const double* C, int64_t ldc,
+            double diag, double* D, int64_t ldd, int is_mv, int64_t* counters, void* stream);
+
+/* D = cdiag*I + sum_i coefs[i]*X[i] (nterms <= 6), one rounding per term in
+ * order: the `Lin` instruction (series_toolkit.py:375-378). */
+SI_API int si_lincomb(si_handle h, int64_t m, int64_t n, double cdiag, int nterms, const double* coefs,
+               const double* const* X, const int64_t* ldx, double* D, int64_t ldd, void* stream);
+
+/* Host-returning reductions (synchronise `stream`): matrix_core.py:154-172. */
+SI_API int si_fro_norm(si_handle h, int64_t m, int64_t n, const double* X, int64_t ldx, double* out,
+                void* stream);
+SI_API int si_inf_norm(si_handle h, int64_t m, int64_t n, const double* X, int64_t ldx, double* out,
+                void* stream);
+
+/* ---------------- splittings (splitting.py:101-146) ---------------- */
+
+/* precond = I/alpha, residual = I - A/alpha  (split_scalar, splitting.py:138-140) */
+SI_API int si_split_scalar(si_handle h, int64_t n, const double* A, double alpha, double* precond,
+                    double* residual, void* stream);
+/* precond = diag(1/d), residual = I - A/d[:,None]  (split_diagonal, splitting.py:113-114) */
+SI_API int si_split_diagonal(si_handle h, int64_t n, const double* A, double* precond, double* residual,
+                      void* stream);
+/* out = (A + A^T)/2  (splitting.py:73) */
+SI_API int si_symmetrize(si_handle h, int64_t n, const double* A, double* out, void* stream);
+
+/* ---------------- evaluators (series_toolkit.py:279-457) ---------------- */
+
+/* horner_eval (series_toolkit.py:279-302).  y may be NULL iff form_y; with
+ * form_y the effective Y = I - X A is formed (one product) and, when y is
+ * given, checked against it (SI_EINVAL on mismatch; synchronises). */
+SI_API int si_horner_eval(si_handle h, int64_t n, const double* y, const double* x, int order,
+                   const double* a, int form_y, double* out, int64_t* counters, void* stream);
+/* factored_eval (series_toolkit.py:326-356) */
+SI_API int si_factored_eval(si_handle h, int64_t n, const double* y, const double* x, const double* a,
+                     int p, int w, int form_y, double* out, int64_t* counters, void* stream);
+/* nested_eval (series_toolkit.py:408-429) */
+SI_API int si_nested_eval(si_handle h, int64_t n, const double* y, const double* x, const double* a,
+                   const int32_t* plan, int64_t plan_len, const double* consts, int64_t nconsts,
+                   int form_y, double* out, int64_t* counters, void* stream);
+/* geometric_apply (series_toolkit.py:432-457); base_plan = plan_order(b) for the
+ * order b <= 64 reached from `order` by repeated halving (unused when b == 1). */
+SI_API int si_geometric_apply(si_handle h, int64_t n, const double* y, const double* x, int order,
+                       const double* a, const int32_t* base_plan, int64_t plan_len,
+                       const double* consts, int64_t nconsts, double* out, int64_t* counters,
+                       void* stream);
+/* mat_pow_counted (matrix_core.py:137-151) */
+SI_API int si_mat_pow_counted(si_handle h, int64_t n, const double* y, int e, double* out,
+                       int64_t* counters, void* stream);
+
+/* ---------------- Newton-Schulz steps (newton_schulz.py) ---------------- */
+
+/* initial_series (newton_schulz.py:127-147) */
+SI_API int si_initial_series(si_handle h, int64_t n, const double* precond, const double* residual,
+                      const double* a, int p, int w, double* g_out, double* f_out,
+                      int64_t* counters, void* stream);
+/* ns_step (newton_schulz.py:150-174); plan may be NULL (Horner). */
+SI_API int si_ns_step(si_handle h, int64_t n, const double* a, const double* g, const double* f,
+               int order, const int32_t* plan, int64_t plan_len, const double* consts,
+               int64_t nconsts, double* g_out, double* f_out, int64_t* counters, void* stream);
+/* composite_step (newton_schulz.py:177-228).  plans/plan_offsets[nrates+1]
+ * hold, per rate, the geometric_apply base plan (empty for rate 1). */
+SI_API int si_composite_step(si_handle h, int64_t n, const double* a, const double* g, const double* f,
+                      const double* precond, const double* residual, const double* split_matrix,
+                      int nrates, const int32_t* rates, const int32_t* plans,
+                      const int64_t* plan_offsets, const double* consts, int64_t nconsts,
+                      int order_n, int concurrent, double* g_out, double* f_out,
+                      int64_t* counters, void* stream);
+/* initial_double (newton_schulz.py:231-251) */
+SI_API int si_initial_double(si_handle h, int64_t n, const double* precond, const double* residual,
+                      const double* a, int p, int w, int order, double* g_out, double* f_out,
+                      double* l_out, double* r_out, int64_t* counters, void* stream);
+/* double_ns_step (newton_schulz.py:254-298) */
+SI_API int si_double_ns_step(si_handle h, int64_t n, const double* a, const double* g, const double* f,
+                      const double* l, const double* r, int order, int concurrent, double* g_out,
+                      double* f_out, double* l_out, double* r_out, int64_t* counters,
+                      void* stream);
+/* additive_correction_step (newton_schulz.py:301-325) */
+SI_API int si_additive_correction_step(si_handle h, int64_t n, const double* a, const double* z,
+                                const double* g, int p, double* z_out, double* g_out,
+                                int64_t* counters, void* stream);
+
+/* ---------------- Richardson (richardson.py) ---------------- */
+
+/* richardson_step (richardson.py:81-98): b, theta, theta_out are n x nrhs. */
+SI_API int si_richardson_step(si_handle h, int64_t n, int64_t nrhs, const double* a, const double* b,
+                       const double* theta, const double* g, const double* f, const double* l,
+                       const double* r, int order, int q, double* g_out, double* f_out,
+                       double* l_out, double* r_out, double* theta_out, int64_t* counters,
+                       void* stream);
+/* richardson_recursive_step (richardson.py:111-189).  omega/ns_part may be NULL
+ * (first call).  Opt-in factorised variant (not in the reference): a non-NULL
+ * factor_plan of order `order` evaluates N' and doubling_sum != 0 builds
+ * S = prod_j (I + Gamma^(2^j)) (order must be a power of two). */
+SI_API int si_richardson_recursive_step(si_handle h, int64_t n, int64_t nrhs, const double* a,
+                                 const double* b, const double* theta, const double* g,
+                                 const double* f, const double* l, const double* r,
+                                 const double* omega, const double* ns_part, int order,
+                                 const int32_t* factor_plan, int64_t plan_len,
+                                 const double* consts, int64_t nconsts, int doubling_sum,
+                                 int concurrent, double* g_out, double* f_out, double* l_out,
+                                 double* r_out, double* omega_out, double* ns_out,
+                                 double* theta_out, int64_t* counters, void* stream);
+/* Plain update theta' = theta - P (A theta - b)  (ordering as
+ * richardson.py:88-89). */
+SI_API int si_plain_richardson(si_handle h, int64_t n, int64_t nrhs, const double* a, const double* b,
+                        const double* theta, const double* p, double* theta_out,
+                        int64_t* counters, void* stream);
+
+/* ---------------- measurement ---------------- */
+
+/* Start recording CUDA events around every large (TMA) GEMM launch and
+ * counting kernel launches made through this handle. */
+SI_API int si_profile_begin(si_handle h);
+/* Stop recording; synchronises and returns the summed device time (ms) and
+ * algorithmic FLOPs of the recorded TMA GEMM launches, their count, and the
+ * total number of kernels this handle launched since si_profile_begin. */
+SI_API int si_profile_end(si_handle h, double* gemm_ms, double* gemm_flops,
+                          int64_t* gemm_launches, int64_t* total_launches);
+/* FP64 DMMA (m8n8k4) register-only throughput of this device in TFLOP/s:
+ * the roofline denominator (MEASURED_PEAKS.json has no FP64 entry). */
+SI_API int si_dmma_peak(si_handle h, int iters, double* tflops);
+
+/* ---------------- batched small systems (BASELINE config 2) ---------------- */
+
+/* `iters` x { plain Richardson with P_k; composite_step(rates, order_n) } for
+ * `batch` independent n x n systems (n <= 32), everything resident on chip.
+ * A, P (in/out), F (in/out): batch x n x n; b, theta (in/out): batch x n.
+ * precond/residual: batch x n x n splitting of each A; plans as in
+ * si_composite_step.  Counters are per system (identical for all systems). */
+SI_API int si_batched_composite_richardson(si_handle h, int64_t batch, int64_t n, const double* a,
+                                    const double* b, const double* precond,
+                                    const double* residual, int nrates, const int32_t* rates,
+                                    const int32_t* plans, const int64_t* plan_offsets,
+                                    const double* consts, int64_t nconsts, int order_n,
+                                    int iters, double* p_io, double* f_io, double* theta_io,
+                                    int64_t* counters, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SERIESINV_B200_H */

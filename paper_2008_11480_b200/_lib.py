@@ -1,0 +1,153 @@
+"""ctypes binding of ``libseriesinv_b200.so`` (the C ABI in include/seriesinv_b200.h).
+
+The product path has no fallback: if the shared library is missing or no CUDA
+device is visible, every entry point raises.  Device memory and streams come
+from PyTorch (plumbing only); all arithmetic runs in the library's kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from ctypes import POINTER, c_double, c_int, c_int32, c_int64, c_void_p
+
+import torch
+
+LIB_NAME = "libseriesinv_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+SI_OK, SI_EINVAL, SI_ECUDA, SI_ENOMEM = 0, -1, -2, -3
+
+_P = c_void_p
+_I64 = c_int64
+_I = c_int
+_D = c_double
+_PI64 = POINTER(c_int64)
+
+# name -> argtypes (all return int status)
+SIGNATURES: dict[str, list] = {
+    "si_create": [_I, POINTER(c_void_p)],
+    "si_destroy": [_P],
+    "si_trim": [_P],
+    "si_gemm": [_P, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _D, _P, _I64, _I, _PI64, _P],
+    "si_lincomb": [_P, _I64, _I64, _D, _I, _P, _P, _P, _P, _I64, _P],
+    "si_fro_norm": [_P, _I64, _I64, _P, _I64, POINTER(c_double), _P],
+    "si_inf_norm": [_P, _I64, _I64, _P, _I64, POINTER(c_double), _P],
+    "si_split_scalar": [_P, _I64, _P, _D, _P, _P, _P],
+    "si_split_diagonal": [_P, _I64, _P, _P, _P, _P],
+    "si_symmetrize": [_P, _I64, _P, _P, _P],
+    "si_horner_eval": [_P, _I64, _P, _P, _I, _P, _I, _P, _PI64, _P],
+    "si_factored_eval": [_P, _I64, _P, _P, _P, _I, _I, _I, _P, _PI64, _P],
+    "si_nested_eval": [_P, _I64, _P, _P, _P, _P, _I64, _P, _I64, _I, _P, _PI64, _P],
+    "si_geometric_apply": [_P, _I64, _P, _P, _I, _P, _P, _I64, _P, _I64, _P, _PI64, _P],
+    "si_mat_pow_counted": [_P, _I64, _P, _I, _P, _PI64, _P],
+    "si_initial_series": [_P, _I64, _P, _P, _P, _I, _I, _P, _P, _PI64, _P],
+    "si_ns_step": [_P, _I64, _P, _P, _P, _I, _P, _I64, _P, _I64, _P, _P, _PI64, _P],
+    "si_composite_step": [_P, _I64, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _P, _P, _PI64, _P],
+    "si_initial_double": [_P, _I64, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _PI64, _P],
+    "si_double_ns_step": [_P, _I64, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _PI64, _P],
+    "si_additive_correction_step": [_P, _I64, _P, _P, _P, _I, _P, _P, _PI64, _P],
+    "si_richardson_step": [_P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _PI64, _P],
+    "si_richardson_recursive_step": [
+        _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I64, _P, _I64, _I, _I,
+        _P, _P, _P, _P, _P, _P, _P, _PI64, _P,
+    ],
+    "si_plain_richardson": [_P, _I64, _I64, _P, _P, _P, _P, _P, _PI64, _P],
+    "si_profile_begin": [_P],
+    "si_profile_end": [_P, POINTER(c_double), POINTER(c_double), _PI64, _PI64],
+    "si_dmma_peak": [_P, _I, POINTER(c_double)],
+    "si_batched_composite_richardson": [
+        _P, _I64, _I64, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _PI64, _P,
+    ],
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+_handles: dict[int, int] = {}
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA extension is not built or no CUDA device is visible."""
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load the shared library and declare every prototype (no GPU needed)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        lib = ctypes.CDLL(path)
+        for name, argtypes in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = argtypes
+            fn.restype = c_int
+        lib.si_last_error.restype = ctypes.c_char_p
+        lib.si_last_error.argtypes = []
+        lib.si_version.restype = c_int
+        lib.si_version.argtypes = []
+        _lib = lib
+        return lib
+
+
+def _raise(status: int, name: str):
+    msg = _lib.si_last_error().decode(errors="replace") if _lib is not None else ""
+    if status == SI_EINVAL:
+        raise ValueError(msg or f"{name}: invalid argument")
+    if status == SI_ENOMEM:
+        raise MemoryError(f"{name}: {msg}")
+    raise RuntimeError(f"{name} failed ({status}): {msg}")
+
+
+def handle(device: int | None = None) -> int:
+    """Per-device library handle (workspace pool, side streams, events)."""
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device visible: the seriesinv B200 path has no CPU fallback")
+    lib = load_library()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    h = _handles.get(dev)
+    if h is None:
+        out = c_void_p()
+        st = lib.si_create(dev, ctypes.byref(out))
+        if st != SI_OK:
+            _raise(st, "si_create")
+        h = out.value
+        _handles[dev] = h
+    return h
+
+
+def call(name: str, *args) -> None:
+    lib = load_library()
+    st = getattr(lib, name)(*args)
+    if st != SI_OK:
+        _raise(st, name)
+
+
+def stream_ptr(device: torch.device | None = None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def i32_array(values) -> ctypes.Array:
+    return (c_int32 * max(len(values), 1))(*values)
+
+
+def i64_array(values) -> ctypes.Array:
+    return (c_int64 * max(len(values), 1))(*values)
+
+
+def f64_array(values) -> ctypes.Array:
+    return (c_double * max(len(values), 1))(*values)
+
+
+def counter_buf() -> ctypes.Array:
+    return (c_int64 * 2)(0, 0)

@@ -1,0 +1,64 @@
+"""Batched small systems (BASELINE config 2) on the device.
+
+``batched_composite_richardson`` advances ``batch`` independent n x n systems
+(n <= 32) through ``iters`` x { plain Richardson with P_k;
+``composite_step(rates, order_n)`` (newton_schulz.py:177-228) } in ONE kernel
+launch: one CTA per system, the whole state resident in shared memory, DMMA
+products.  Per system it executes exactly the reference GEMM DAG, so the
+returned counter is the per-system MulCounter delta.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .matrix_core import MulCounter, as_device
+from .series_toolkit import encode_many, geometric_base_plan
+
+__all__ = ["batched_composite_richardson", "batched_scalar_split"]
+
+
+def batched_scalar_split(a: torch.Tensor, eps_factor: float = 0.5):
+    """Per-system split_scalar(A_i, eps = eps_factor*||A_i||_inf) (splitting.py:124-146):
+    alpha_i = ||A_i||_inf (1/2 + eps_factor); P_i = I/alpha_i, B_i = I - A_i/alpha_i.
+    ``eps_factor=0.5`` gives P0 = I/||A||_inf."""
+    a = as_device(a)
+    n = a.shape[-1]
+    norm = a.abs().sum(dim=-1).amax(dim=-1)
+    alpha = norm / 2.0 + eps_factor * norm
+    eye = torch.eye(n, dtype=torch.float64, device=a.device)
+    precond = eye / alpha[:, None, None]
+    residual = eye - a / alpha[:, None, None]
+    return precond, residual
+
+
+def batched_composite_richardson(a, b, precond, residual, p, f, theta, rates, order_n: int,
+                                 iters: int, ctr: MulCounter | None = None):
+    """Returns new (P, F, theta) after ``iters`` fused iterations; inputs untouched."""
+    a, b = as_device(a), as_device(b)
+    precond, residual = as_device(precond), as_device(residual)
+    batch, n, n2 = a.shape
+    if n != n2 or n > 32:
+        raise ValueError("batched path expects batch x n x n with n <= 32")
+    if b.shape != (batch, n):
+        raise ValueError("dimension mismatch")
+    rates = tuple(int(x) for x in rates)
+    if not rates or any(x < 1 for x in rates):
+        raise ValueError("rates must be positive integers")
+    if order_n < 1:
+        raise ValueError("order_n must be >= 1")
+    p_io = as_device(p).clone()
+    f_io = as_device(f).clone()
+    th_io = as_device(theta).clone()
+    plans = [geometric_base_plan(x) if x > 1 else None for x in rates]
+    code, offsets, consts = encode_many(plans)
+    buf = _lib.counter_buf()
+    _lib.call("si_batched_composite_richardson", _lib.handle(a.device.index), batch, n,
+              a.data_ptr(), b.data_ptr(), precond.data_ptr(), residual.data_ptr(), len(rates),
+              _lib.i32_array(list(rates)), _lib.i32_array(code), _lib.i64_array(offsets),
+              _lib.f64_array(consts), len(consts), order_n, iters, p_io.data_ptr(), f_io.data_ptr(),
+              th_io.data_ptr(), buf, _lib.stream_ptr(a.device))
+    if ctr is not None:
+        ctr.absorb(buf)
+    return p_io, f_io, th_io

@@ -1,0 +1,21 @@
+#pragma once
+#include <vector>
+
+#include "engine.hpp"
+
+namespace si {
+
+constexpr int kBatchMaxN = 32;
+constexpr int kBatchMaxRates = 4;
+
+// BASELINE config 2: `iters` x { plain Richardson with P_k;
+// composite_step(rates, order_n) (newton_schulz.py:177-228) } for `batch`
+// independent n x n systems, one CTA per system, state resident in shared
+// memory across iterations.  Returns the per-system counter delta.
+Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const double* a,
+                                      const double* b, const double* precond,
+                                      const double* residual, const std::vector<int>& rates,
+                                      const std::vector<const PlanNode*>& plans, int order_n,
+                                      int iters, double* p_io, double* f_io, double* theta_io);
+
+}  // namespace si

@@ -1,0 +1,522 @@
+// extern "C" boundary (include/seriesinv_b200.h).  Validates arguments, maps
+// exceptions to status codes, never throws across the ABI.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "../../include/seriesinv_b200.h"
+#include "batched.hpp"
+#include "steps.hpp"
+
+using namespace si;
+
+struct si_handle_s {
+  Handle h;
+};
+
+namespace {
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return SI_OK;
+  } catch (const Error& e) {
+    set_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return SI_ENOMEM;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return SI_ECUDA;
+  }
+}
+
+void need(bool ok, const char* msg) {
+  if (!ok) throw Error(kEInval, msg);
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+MV sq(const double* p, int64_t n) { return view(const_cast<double*>(p), n, n, n); }
+MV rect(const double* p, int64_t n, int64_t r) { return view(const_cast<double*>(p), n, r, r); }
+
+void add_counters(int64_t* counters, const Ctx& c) {
+  if (counters) {
+    counters[0] += c.ctr.mmm;
+    counters[1] += c.ctr.mvm;
+  }
+}
+
+struct Call {
+  Ctx c;
+  int64_t* counters;
+  Call(si_handle h, void* stream, int64_t* ctrs) : c(&h->h, as_stream(stream)), counters(ctrs) {
+    check(cudaSetDevice(h->h.device), "cudaSetDevice");
+  }
+  ~Call() { add_counters(counters, c); }
+};
+
+PlanPtr opt_plan(const int32_t* code, int64_t len, const double* consts, int64_t nconsts) {
+  if (!code || len == 0) return nullptr;
+  return decode_plan(code, len, consts, nconsts);
+}
+
+double host_fro(Ctx& c, const MV& x) {
+  Handle* h = c.h;
+  const size_t need_elems = reduce_work_elems(x.v);
+  if (h->red_elems < need_elems) {
+    if (h->red_work) cudaFree(h->red_work);
+    h->red_work = nullptr;
+    check(cudaMalloc(&h->red_work, need_elems * sizeof(double)), "cudaMalloc");
+    h->red_elems = need_elems;
+  }
+  check(launch_sumsq(x.v, h->scalar, h->red_work, c.s), "sumsq");
+  double v = 0.0;
+  check(cudaMemcpyAsync(&v, h->scalar, sizeof(double), cudaMemcpyDeviceToHost, c.s), "memcpy");
+  check(cudaStreamSynchronize(c.s), "sync");
+  return std::sqrt(v);
+}
+
+// series_toolkit.py:270-276 -- Y = I - X A, checked against a supplied Y.
+MV formed_y(Ctx& c, const double* y, const MV& x, const MV& a) {
+  MV ye = residual(c, x, a);
+  if (y) {
+    MV yv = sq(y, x.v.rows);
+    MV diff = lincomb(c, 0.0, {{1.0, &ye}, {-1.0, &yv}}, x.v.rows, x.v.cols);
+    const double gap = host_fro(c, diff);
+    const double ny = host_fro(c, yv);
+    if (gap > 1e-10 * (1.0 + ny)) throw Error(kEInval, "supplied Y does not match I - X A");
+  }
+  return ye;
+}
+
+}  // namespace
+
+extern "C" {
+
+int si_version(void) { return 1; }
+const char* si_last_error(void) { return get_error(); }
+
+int si_create(int device, si_handle* out) {
+  return guard([&] {
+    need(out != nullptr, "null handle pointer");
+    check(cudaSetDevice(device), "cudaSetDevice");
+    auto* hs = new si_handle_s();
+    hs->h.device = device;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    check(cudaMemPoolCreate(&hs->h.pool, &props), "cudaMemPoolCreate");
+    uint64_t thresh = UINT64_MAX;
+    check(cudaMemPoolSetAttribute(hs->h.pool, cudaMemPoolAttrReleaseThreshold, &thresh),
+          "cudaMemPoolSetAttribute");
+    for (int i = 0; i < Handle::kSide; ++i)
+      check(cudaStreamCreateWithFlags(&hs->h.side[i], cudaStreamNonBlocking), "cudaStreamCreate");
+    check(cudaMalloc(&hs->h.scalar, sizeof(double)), "cudaMalloc");
+    *out = hs;
+  });
+}
+
+int si_destroy(si_handle h) {
+  return guard([&] {
+    if (!h) return;
+    cudaSetDevice(h->h.device);
+    cudaDeviceSynchronize();
+    for (auto e : h->h.events) cudaEventDestroy(e);
+    for (int i = 0; i < Handle::kSide; ++i)
+      if (h->h.side[i]) cudaStreamDestroy(h->h.side[i]);
+    if (h->h.red_work) cudaFree(h->h.red_work);
+    if (h->h.scalar) cudaFree(h->h.scalar);
+    if (h->h.pool) cudaMemPoolDestroy(h->h.pool);
+    delete h;
+  });
+}
+
+int si_trim(si_handle h) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    check(cudaDeviceSynchronize(), "sync");
+    check(cudaMemPoolTrimTo(h->h.pool, 0), "cudaMemPoolTrimTo");
+  });
+}
+
+int si_gemm(si_handle h, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+            int64_t lda, const double* B, int64_t ldb, double beta, const double* C, int64_t ldc,
+            double diag, double* D, int64_t ldd, int is_mv, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && A && B && D, "null pointer");
+    need(m >= 0 && n >= 0 && k >= 0, "negative dimension");
+    need(lda >= k && ldb >= n && ldd >= n, "leading dimension too small");
+    need(beta == 0.0 || (C && ldc >= n), "beta != 0 needs C");
+    Call call(h, stream, counters);
+    MV a = view(const_cast<double*>(A), m, k, lda), b = view(const_cast<double*>(B), k, n, ldb);
+    MV d = view(D, m, n, ldd);
+    MV cm = view(const_cast<double*>(C), m, n, ldc);
+    gemm(call.c, d, a, b, alpha, C ? &cm : nullptr, beta, diag, is_mv != 0);
+  });
+}
+
+int si_lincomb(si_handle h, int64_t m, int64_t n, double cdiag, int nterms, const double* coefs,
+               const double* const* X, const int64_t* ldx, double* D, int64_t ldd, void* stream) {
+  return guard([&] {
+    need(h && D, "null pointer");
+    need(nterms >= 0 && nterms <= kMaxLinTerms, "nterms out of range");
+    need(nterms == 0 || (coefs && X && ldx), "null term arrays");
+    Call call(h, stream, nullptr);
+    Mat xs[kMaxLinTerms];
+    for (int i = 0; i < nterms; ++i) {
+      need(X[i] != nullptr && ldx[i] >= n, "bad term");
+      xs[i] = view(const_cast<double*>(X[i]), m, n, ldx[i]).v;
+    }
+    Mat d = view(D, m, n, ldd).v;
+    check(launch_lincomb(d, cdiag, nterms, coefs, xs, call.c.s), "lincomb");
+  });
+}
+
+int si_fro_norm(si_handle h, int64_t m, int64_t n, const double* X, int64_t ldx, double* out,
+                void* stream) {
+  return guard([&] {
+    need(h && X && out, "null pointer");
+    Call call(h, stream, nullptr);
+    *out = host_fro(call.c, view(const_cast<double*>(X), m, n, ldx));
+  });
+}
+
+int si_inf_norm(si_handle h, int64_t m, int64_t n, const double* X, int64_t ldx, double* out,
+                void* stream) {
+  return guard([&] {
+    need(h && X && out, "null pointer");
+    Call call(h, stream, nullptr);
+    Handle* hh = &h->h;
+    Mat x = view(const_cast<double*>(X), m, n, ldx).v;
+    const size_t ne = reduce_work_elems(x);
+    if (hh->red_elems < ne) {
+      if (hh->red_work) cudaFree(hh->red_work);
+      hh->red_work = nullptr;
+      check(cudaMalloc(&hh->red_work, ne * sizeof(double)), "cudaMalloc");
+      hh->red_elems = ne;
+    }
+    check(launch_inf_norm(x, hh->scalar, hh->red_work, call.c.s), "inf_norm");
+    check(cudaMemcpyAsync(out, hh->scalar, sizeof(double), cudaMemcpyDeviceToHost, call.c.s),
+          "memcpy");
+    check(cudaStreamSynchronize(call.c.s), "sync");
+  });
+}
+
+int si_split_scalar(si_handle h, int64_t n, const double* A, double alpha, double* precond,
+                    double* residual, void* stream) {
+  return guard([&] {
+    need(h && A && residual, "null pointer");
+    need(n >= 1 && alpha > 0.0, "bad splitting arguments");
+    Call call(h, stream, nullptr);
+    Mat p = view(precond, n, n, n).v, b = view(residual, n, n, n).v;
+    check(launch_scalar_split(p, b, sq(A, n).v, alpha, call.c.s), "split_scalar");
+  });
+}
+
+int si_split_diagonal(si_handle h, int64_t n, const double* A, double* precond, double* residual,
+                      void* stream) {
+  return guard([&] {
+    need(h && A && residual, "null pointer");
+    Call call(h, stream, nullptr);
+    Mat p = view(precond, n, n, n).v, b = view(residual, n, n, n).v;
+    check(launch_diag_split(p, b, sq(A, n).v, call.c.s), "split_diagonal");
+  });
+}
+
+int si_symmetrize(si_handle h, int64_t n, const double* A, double* out, void* stream) {
+  return guard([&] {
+    need(h && A && out && A != out, "bad pointer");
+    Call call(h, stream, nullptr);
+    Mat d = view(out, n, n, n).v;
+    check(launch_symmetrize(d, sq(A, n).v, call.c.s), "symmetrize");
+  });
+}
+
+int si_horner_eval(si_handle h, int64_t n, const double* y, const double* x, int order,
+                   const double* a, int form_y, double* out, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && x && out, "null pointer");
+    need(order >= 1, "order h must be >= 1");
+    need(!form_y || a, "form_y=True requires the matrix a");
+    need(form_y || y, "y is required unless form_y=True");
+    Call call(h, stream, counters);
+    MV xv = sq(x, n);
+    MV yv = form_y ? formed_y(call.c, y, xv, sq(a, n)) : sq(y, n);
+    copy_into(call.c, sq(out, n), horner(call.c, yv, xv, order));
+  });
+}
+
+int si_factored_eval(si_handle h, int64_t n, const double* y, const double* x, const double* a,
+                     int p, int w, int form_y, double* out, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && x && a && out, "null pointer");
+    need(p >= 0 && w >= 1, "requires p >= 0 and w >= 1");
+    need(form_y || y, "y is required unless form_y=True");
+    Call call(h, stream, counters);
+    MV xv = sq(x, n), av = sq(a, n);
+    MV yv = form_y ? formed_y(call.c, y, xv, av) : sq(y, n);
+    copy_into(call.c, sq(out, n), factored(call.c, yv, xv, av, p, w));
+  });
+}
+
+int si_nested_eval(si_handle h, int64_t n, const double* y, const double* x, const double* a,
+                   const int32_t* plan, int64_t plan_len, const double* consts, int64_t nconsts,
+                   int form_y, double* out, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && x && a && out, "null pointer");
+    need(form_y || y, "y is required unless form_y=True");
+    PlanPtr pl = decode_plan(plan, plan_len, consts, nconsts);
+    Call call(h, stream, counters);
+    MV xv = sq(x, n), av = sq(a, n);
+    MV yv = form_y ? formed_y(call.c, y, xv, av) : sq(y, n);
+    copy_into(call.c, sq(out, n), eval_node(call.c, *pl, yv, xv, av));
+  });
+}
+
+int si_geometric_apply(si_handle h, int64_t n, const double* y, const double* x, int order,
+                       const double* a, const int32_t* base_plan, int64_t plan_len,
+                       const double* consts, int64_t nconsts, double* out, int64_t* counters,
+                       void* stream) {
+  return guard([&] {
+    need(h && y && x && a && out, "null pointer");
+    need(order >= 1, "order must be >= 1");
+    PlanPtr pl = opt_plan(base_plan, plan_len, consts, nconsts);
+    Call call(h, stream, counters);
+    copy_into(call.c, sq(out, n), geometric(call.c, sq(y, n), sq(x, n), order, sq(a, n), pl.get()));
+  });
+}
+
+int si_mat_pow_counted(si_handle h, int64_t n, const double* y, int e, double* out,
+                       int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && y && out, "null pointer");
+    need(e >= 0, "exponent must be non-negative");
+    Call call(h, stream, counters);
+    copy_into(call.c, sq(out, n), mat_pow_counted(call.c, sq(y, n), e));
+  });
+}
+
+int si_initial_series(si_handle h, int64_t n, const double* precond, const double* residual,
+                      const double* a, int p, int w, double* g_out, double* f_out,
+                      int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && precond && residual && a && g_out && f_out, "null pointer");
+    Call call(h, stream, counters);
+    initial_series(call.c, sq(precond, n), sq(residual, n), sq(a, n), p, w, sq(g_out, n),
+                   sq(f_out, n));
+  });
+}
+
+int si_ns_step(si_handle h, int64_t n, const double* a, const double* g, const double* f,
+               int order, const int32_t* plan, int64_t plan_len, const double* consts,
+               int64_t nconsts, double* g_out, double* f_out, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && g && f && g_out && f_out, "null pointer");
+    PlanPtr pl = opt_plan(plan, plan_len, consts, nconsts);
+    Call call(h, stream, counters);
+    ns_step(call.c, sq(a, n), sq(g, n), sq(f, n), order, pl.get(), sq(g_out, n), sq(f_out, n));
+  });
+}
+
+int si_composite_step(si_handle h, int64_t n, const double* a, const double* g, const double* f,
+                      const double* precond, const double* residual, const double* split_matrix,
+                      int nrates, const int32_t* rates, const int32_t* plans,
+                      const int64_t* plan_offsets, const double* consts, int64_t nconsts,
+                      int order_n, int concurrent, double* g_out, double* f_out,
+                      int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && g && f && precond && residual && split_matrix && g_out && f_out,
+         "null pointer");
+    need(nrates >= 1 && rates, "composite spec needs at least one rate");
+    need(order_n >= 1, "order_n must be >= 1");
+    std::vector<int> rv(rates, rates + nrates);
+    std::vector<PlanPtr> owned(nrates);
+    std::vector<const PlanNode*> pv(nrates, nullptr);
+    for (int i = 0; i < nrates; ++i) {
+      need(rv[i] >= 1, "rates must be positive integers");
+      if (plans && plan_offsets && plan_offsets[i + 1] > plan_offsets[i]) {
+        owned[i] = decode_plan(plans + plan_offsets[i], plan_offsets[i + 1] - plan_offsets[i],
+                               consts, nconsts);
+        pv[i] = owned[i].get();
+      }
+    }
+    Call call(h, stream, counters);
+    composite_step(call.c, sq(a, n), sq(g, n), sq(f, n), sq(precond, n), sq(residual, n),
+                   sq(split_matrix, n), rv, pv, order_n, concurrent != 0, sq(g_out, n),
+                   sq(f_out, n));
+  });
+}
+
+int si_initial_double(si_handle h, int64_t n, const double* precond, const double* residual,
+                      const double* a, int p, int w, int order, double* g_out, double* f_out,
+                      double* l_out, double* r_out, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && precond && residual && a && g_out && f_out && l_out && r_out, "null pointer");
+    need(order >= 1, "order must be >= 1");
+    Call call(h, stream, counters);
+    initial_double(call.c, sq(precond, n), sq(residual, n), sq(a, n), p, w, order, sq(g_out, n),
+                   sq(f_out, n), sq(l_out, n), sq(r_out, n));
+  });
+}
+
+int si_double_ns_step(si_handle h, int64_t n, const double* a, const double* g, const double* f,
+                      const double* l, const double* r, int order, int concurrent, double* g_out,
+                      double* f_out, double* l_out, double* r_out, int64_t* counters,
+                      void* stream) {
+  return guard([&] {
+    need(h && a && g && f && l && r && g_out && f_out && l_out && r_out, "null pointer");
+    Call call(h, stream, counters);
+    double_ns_step(call.c, sq(a, n), sq(g, n), sq(f, n), sq(l, n), sq(r, n), order,
+                   concurrent != 0, sq(g_out, n), sq(f_out, n), sq(l_out, n), sq(r_out, n));
+  });
+}
+
+int si_additive_correction_step(si_handle h, int64_t n, const double* a, const double* z,
+                                const double* g, int p, double* z_out, double* g_out,
+                                int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && z && g && z_out && g_out, "null pointer");
+    Call call(h, stream, counters);
+    additive_correction_step(call.c, sq(a, n), sq(z, n), sq(g, n), p, sq(z_out, n),
+                             sq(g_out, n));
+  });
+}
+
+int si_richardson_step(si_handle h, int64_t n, int64_t nrhs, const double* a, const double* b,
+                       const double* theta, const double* g, const double* f, const double* l,
+                       const double* r, int order, int q, double* g_out, double* f_out,
+                       double* l_out, double* r_out, double* theta_out, int64_t* counters,
+                       void* stream) {
+  return guard([&] {
+    need(h && a && b && theta && g && f && l && r && g_out && f_out && l_out && r_out &&
+             theta_out,
+         "null pointer");
+    need(nrhs >= 1, "nrhs must be >= 1");
+    Call call(h, stream, counters);
+    richardson_step(call.c, sq(a, n), rect(b, n, nrhs), rect(theta, n, nrhs), sq(g, n), sq(f, n),
+                    sq(l, n), sq(r, n), order, q, sq(g_out, n), sq(f_out, n), sq(l_out, n),
+                    sq(r_out, n), rect(theta_out, n, nrhs));
+  });
+}
+
+int si_richardson_recursive_step(si_handle h, int64_t n, int64_t nrhs, const double* a,
+                                 const double* b, const double* theta, const double* g,
+                                 const double* f, const double* l, const double* r,
+                                 const double* omega, const double* ns_part, int order,
+                                 const int32_t* factor_plan, int64_t plan_len,
+                                 const double* consts, int64_t nconsts, int doubling_sum,
+                                 int concurrent, double* g_out, double* f_out, double* l_out,
+                                 double* r_out, double* omega_out, double* ns_out,
+                                 double* theta_out, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && b && theta && g && f && l && r && g_out && f_out && l_out && r_out &&
+             omega_out && ns_out && theta_out,
+         "null pointer");
+    need(nrhs >= 1, "nrhs must be >= 1");
+    PlanPtr pl = opt_plan(factor_plan, plan_len, consts, nconsts);
+    if (pl) need(plan_order_of(*pl) == order, "factor plan order != iteration order");
+    Call call(h, stream, counters);
+    MV om = omega ? sq(omega, n) : MV{}, nsp = ns_part ? sq(ns_part, n) : MV{};
+    richardson_recursive_step(call.c, sq(a, n), rect(b, n, nrhs), rect(theta, n, nrhs), sq(g, n),
+                              sq(f, n), sq(l, n), sq(r, n), omega ? &om : nullptr,
+                              ns_part ? &nsp : nullptr, order, concurrent != 0, pl.get(),
+                              doubling_sum != 0, sq(g_out, n), sq(f_out, n), sq(l_out, n),
+                              sq(r_out, n), sq(omega_out, n), sq(ns_out, n),
+                              rect(theta_out, n, nrhs));
+  });
+}
+
+int si_plain_richardson(si_handle h, int64_t n, int64_t nrhs, const double* a, const double* b,
+                        const double* theta, const double* p, double* theta_out,
+                        int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && b && theta && p && theta_out, "null pointer");
+    need(nrhs >= 1, "nrhs must be >= 1");
+    Call call(h, stream, counters);
+    plain_richardson(call.c, sq(a, n), rect(b, n, nrhs), rect(theta, n, nrhs), sq(p, n),
+                     rect(theta_out, n, nrhs));
+  });
+}
+
+int si_profile_begin(si_handle h) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    Handle& hh = h->h;
+    for (auto& r : hh.prof) {
+      hh.prof_pool.push_back(r.start);
+      hh.prof_pool.push_back(r.stop);
+    }
+    hh.prof.clear();
+    hh.launches = 0;
+    hh.profiling = true;
+  });
+}
+
+int si_profile_end(si_handle h, double* gemm_ms, double* gemm_flops, int64_t* gemm_launches,
+                   int64_t* total_launches) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    Handle& hh = h->h;
+    hh.profiling = false;
+    double ms = 0.0, fl = 0.0;
+    for (auto& r : hh.prof) {
+      check(cudaEventSynchronize(r.stop), "cudaEventSynchronize");
+      float t = 0.f;
+      check(cudaEventElapsedTime(&t, r.start, r.stop), "cudaEventElapsedTime");
+      ms += t;
+      fl += r.flops;
+    }
+    if (gemm_ms) *gemm_ms = ms;
+    if (gemm_flops) *gemm_flops = fl;
+    if (gemm_launches) *gemm_launches = (int64_t)hh.prof.size();
+    if (total_launches) *total_launches = hh.launches;
+  });
+}
+
+int si_dmma_peak(si_handle h, int iters, double* tflops) {
+  return guard([&] {
+    need(h && tflops && iters > 0, "bad arguments");
+    check(cudaSetDevice(h->h.device), "cudaSetDevice");
+    check(dmma_peak_tflops(iters, tflops), "dmma peak");
+  });
+}
+
+int si_batched_composite_richardson(si_handle h, int64_t batch, int64_t n, const double* a,
+                                    const double* b, const double* precond,
+                                    const double* residual, int nrates, const int32_t* rates,
+                                    const int32_t* plans, const int64_t* plan_offsets,
+                                    const double* consts, int64_t nconsts, int order_n,
+                                    int iters, double* p_io, double* f_io, double* theta_io,
+                                    int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && b && precond && residual && rates && p_io && f_io && theta_io,
+         "null pointer");
+    need(batch >= 0 && n >= 1 && n <= kBatchMaxN, "batched path supports 1 <= n <= 32");
+    need(nrates >= 1 && nrates <= kBatchMaxRates, "batched path supports 1..4 rates");
+    need(order_n >= 1 && iters >= 0, "bad order_n / iters");
+    std::vector<int> rv(rates, rates + nrates);
+    std::vector<PlanPtr> owned(nrates);
+    std::vector<const PlanNode*> pv(nrates, nullptr);
+    for (int i = 0; i < nrates; ++i) {
+      need(rv[i] >= 1, "rates must be positive integers");
+      if (plans && plan_offsets && plan_offsets[i + 1] > plan_offsets[i]) {
+        owned[i] = decode_plan(plans + plan_offsets[i], plan_offsets[i + 1] - plan_offsets[i],
+                               consts, nconsts);
+        pv[i] = owned[i].get();
+      }
+    }
+    Call call(h, stream, nullptr);
+    Counters per = batched_composite_richardson(call.c, batch, n, a, b, precond, residual, rv, pv,
+                                                order_n, iters, p_io, f_io, theta_io);
+    if (counters) {
+      counters[0] += per.mmm;
+      counters[1] += per.mvm;
+    }
+  });
+}
+
+}  // extern "C"

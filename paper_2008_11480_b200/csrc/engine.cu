@@ -1,0 +1,419 @@
+// Native step engine.  Every function cites the reference code it mirrors; the
+// GEMM DAG (which products, in which order, with which element-wise op after
+// each) is the reference's, so the mmm/mvm counters match matrix_core.py:71-98
+// tick for tick, while the element-wise ops are fused into the GEMM epilogues.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace si {
+
+thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+const char* get_error() { return g_err.c_str(); }
+
+void check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();
+  if (e == cudaErrorMemoryAllocation)
+    throw Error(kENoMem, std::string(what) + ": " + cudaGetErrorString(e));
+  throw Error(kECuda, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+Buf::~Buf() {
+  if (p) cudaFreeAsync(p, free_stream);
+}
+
+MV view(double* p, int64_t rows, int64_t cols, int64_t ld) {
+  MV m;
+  m.v.p = p;
+  m.v.rows = rows;
+  m.v.cols = cols;
+  m.v.ld = ld;
+  return m;
+}
+
+MV alloc(Ctx& c, int64_t rows, int64_t cols) {
+  auto b = std::make_shared<Buf>();
+  b->free_stream = c.root;
+  void* p = nullptr;
+  const size_t bytes = sizeof(double) * (size_t)std::max<int64_t>(rows * cols, 1);
+  check(cudaMallocFromPoolAsync(&p, bytes, c.h->pool, c.s), "cudaMallocFromPoolAsync");
+  b->p = static_cast<double*>(p);
+  MV m = view(b->p, rows, cols, cols);
+  m.own = b;
+  return m;
+}
+
+// ---------------------------------------------------------------------------
+// products
+// ---------------------------------------------------------------------------
+
+void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV* C, double beta,
+          double diag, bool mv) {
+  if (A.v.cols != B.v.rows || D.v.rows != A.v.rows || D.v.cols != B.v.cols)
+    throw Error(kEInval, "dimension mismatch in product");
+  if (C && (C->v.rows != D.v.rows || C->v.cols != D.v.cols))
+    throw Error(kEInval, "dimension mismatch in epilogue operand");
+  Epilogue e;
+  e.alpha = alpha;
+  e.beta = C ? beta : 0.0;
+  e.diag = diag;
+  e.c = C ? C->v.p : nullptr;
+  e.ldc = C ? C->v.ld : 0;
+  Mat d = D.v;
+  cudaError_t err;
+  Handle* h = c.h;
+  if (d.rows == 0 || d.cols == 0) {
+    err = cudaSuccess;
+  } else if (d.cols <= 4) {
+    err = launch_gemv(A.v, B.v, d, e, c.s);
+    h->launches += 1;
+  } else if (std::max(d.rows, d.cols) >= 128 && tma_eligible(A.v, B.v, d, e)) {
+    Handle::ProfRec rec{};
+    if (h->profiling) {
+      for (cudaEvent_t* ev : {&rec.start, &rec.stop}) {
+        if (h->prof_pool.empty()) {
+          check(cudaEventCreate(ev), "cudaEventCreate");
+        } else {
+          *ev = h->prof_pool.back();
+          h->prof_pool.pop_back();
+        }
+      }
+      rec.flops = 2.0 * (double)d.rows * (double)d.cols * (double)A.v.cols;
+      check(cudaEventRecord(rec.start, c.s), "cudaEventRecord");
+    }
+    err = launch_gemm_tma(A.v, B.v, d, e, c.s);
+    h->launches += 1;
+    if (h->profiling && err == cudaSuccess) {
+      check(cudaEventRecord(rec.stop, c.s), "cudaEventRecord");
+      h->prof.push_back(rec);
+    }
+  } else {
+    err = launch_gemm_generic(A.v, B.v, d, e, c.s);
+    h->launches += 1;
+  }
+  check(err, "gemm launch");
+  if (mv)
+    c.ctr.mvm += 1;
+  else
+    c.ctr.mmm += 1;
+}
+
+MV gemm_new(Ctx& c, const MV& A, const MV& B, double alpha, const MV* C, double beta, double diag,
+            bool mv) {
+  MV D = alloc(c, A.v.rows, B.v.cols);
+  gemm(c, D, A, B, alpha, C, beta, diag, mv);
+  return D;
+}
+
+// identity(n) - mat_mul(X, A)  (the residual form)
+MV residual(Ctx& c, const MV& X, const MV& A) { return gemm_new(c, X, A, -1.0, nullptr, 0.0, 1.0); }
+void residual_into(Ctx& c, const MV& D, const MV& X, const MV& A) {
+  gemm(c, D, X, A, -1.0, nullptr, 0.0, 1.0);
+}
+
+void copy_into(Ctx& c, const MV& D, const MV& X) {
+  if (D.v.p == X.v.p) return;
+  Mat d = D.v;
+  check(launch_copy(d, X.v, c.s), "copy");
+  c.h->launches += 1;
+}
+
+MV lincomb(Ctx& c, double cdiag, const std::vector<std::pair<double, const MV*>>& terms,
+           int64_t rows, int64_t cols) {
+  MV D = alloc(c, rows, cols);
+  if ((int)terms.size() > kMaxLinTerms) throw Error(kEInval, "too many lin terms");
+  double coef[kMaxLinTerms];
+  Mat xs[kMaxLinTerms];
+  for (size_t i = 0; i < terms.size(); ++i) {
+    coef[i] = terms[i].first;
+    xs[i] = terms[i].second->v;
+  }
+  check(launch_lincomb(D.v, cdiag, (int)terms.size(), coef, xs, c.s), "lincomb");
+  c.h->launches += 1;
+  return D;
+}
+
+// ---------------------------------------------------------------------------
+// plans
+// ---------------------------------------------------------------------------
+
+namespace {
+struct Decoder {
+  const int32_t* code;
+  int64_t len, pos = 0;
+  const double* consts;
+  int64_t nconsts;
+  int32_t next() {
+    if (pos >= len) throw Error(kEInval, "malformed plan: truncated");
+    return code[pos++];
+  }
+  double cst(int32_t slot) {
+    if (slot < 0 || slot >= nconsts) throw Error(kEInval, "malformed plan: const slot");
+    return consts[slot];
+  }
+  PlanPtr node(int depth) {
+    if (depth > 16) throw Error(kEInval, "malformed plan: too deep");
+    auto n = std::make_shared<PlanNode>();
+    n->kind = next();
+    switch (n->kind) {
+      case 0:
+        n->h = next();
+        if (n->h < 1) throw Error(kEInval, "Horner order must be >= 1");
+        break;
+      case 1:
+        n->p = next();
+        n->w = next();
+        if (n->p < 0 || n->w < 1) throw Error(kEInval, "Split requires p >= 0 and w >= 1");
+        if (next()) n->inner = node(depth + 1);
+        if (next()) n->outer = node(depth + 1);
+        if (n->p >= 1 && !n->inner) throw Error(kEInval, "Split with p >= 1 needs an inner node");
+        if (n->w >= 2 && !n->outer) throw Error(kEInval, "Split with w >= 2 needs an outer node");
+        break;
+      case 2:
+        n->inner = node(depth + 1);
+        break;
+      case 3: {
+        n->order = next();
+        n->nregs = next();
+        const int ninstr = next();
+        if (n->nregs < 2 || ninstr < 0) throw Error(kEInval, "malformed table form");
+        for (int i = 0; i < ninstr; ++i) {
+          Instr ins;
+          ins.op = next();
+          ins.dst = next();
+          ins.a = ins.b = -1;
+          ins.cconst = 0.0;
+          if (ins.op == 0) {
+            ins.a = next();
+            ins.b = next();
+          } else if (ins.op == 1) {
+            ins.a = next();
+          } else if (ins.op == 2) {
+            ins.cconst = cst(next());
+            const int nt = next();
+            for (int t = 0; t < nt; ++t) {
+              const double cf = cst(next());
+              ins.terms.emplace_back(cf, next());
+            }
+          } else {
+            throw Error(kEInval, "malformed table form: opcode");
+          }
+          auto okreg = [&](int r) { return r >= 0 && r < n->nregs; };
+          if (!okreg(ins.dst) || (ins.op <= 1 && !okreg(ins.a)) || (ins.op == 0 && !okreg(ins.b)))
+            throw Error(kEInval, "malformed table form: register");
+          for (auto& t : ins.terms)
+            if (!okreg(t.second)) throw Error(kEInval, "malformed table form: register");
+          n->prog.push_back(std::move(ins));
+        }
+        break;
+      }
+      default:
+        throw Error(kEInval, "malformed plan: node kind");
+    }
+    return n;
+  }
+};
+}  // namespace
+
+int plan_order_of(const PlanNode& n) {
+  switch (n.kind) {
+    case 0:
+      return n.h;
+    case 1: {
+      if (n.p >= 1 && plan_order_of(*n.inner) != n.p + 1)
+        throw Error(kEInval, "Split inner order != p + 1");
+      if (n.w >= 2 && plan_order_of(*n.outer) != n.w) throw Error(kEInval, "Split outer order != w");
+      return n.w * (n.p + 1);
+    }
+    case 2:
+      return plan_order_of(*n.inner) + 1;
+    default:
+      return n.order;
+  }
+}
+
+PlanPtr decode_plan(const int32_t* code, int64_t len, const double* consts, int64_t nconsts) {
+  if (!code || len <= 0) throw Error(kEInval, "empty plan");
+  Decoder d{code, len, 0, consts, nconsts};
+  PlanPtr p = d.node(0);
+  if (d.pos != len) throw Error(kEInval, "malformed plan: trailing data");
+  plan_order_of(*p);
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// evaluators
+// ---------------------------------------------------------------------------
+
+// st:263-267  z <- y z + x, h-1 times (each product + add fused in one GEMM)
+MV horner(Ctx& c, const MV& y, const MV& x, int h) {
+  MV z = x;
+  for (int i = 0; i < h - 1; ++i) z = gemm_new(c, y, z, 1.0, &x, 1.0);
+  return z;
+}
+
+// st:326-356 with the supplied Y (form_y handled by the caller)
+MV factored(Ctx& c, const MV& y, const MV& x, const MV& a, int p, int w) {
+  MV u = (p == 0) ? x : horner(c, y, x, p + 1);
+  if (w == 1) return u;
+  MV q = (p == 0) ? y : residual(c, u, a);
+  return horner(c, q, u, w);
+}
+
+// st:359-382  straight-line program; a Mul whose only use is the very next
+// Lin "0*I + 1*X + 1*mul" is fused into that GEMM's epilogue (identical
+// rounding: numpy computes fl(X + fl(Y@Z)), the epilogue fl(acc + X)).
+static MV run_program(Ctx& c, const PlanNode& node, const MV& y, const MV& x, const MV& a) {
+  const auto& prog = node.prog;
+  const int nr = node.nregs;
+  std::vector<MV> env(nr);
+  std::vector<int> last_use(nr, -1);
+  for (int i = 0; i < (int)prog.size(); ++i) {
+    const Instr& in = prog[i];
+    if (in.a >= 0) last_use[in.a] = i;
+    if (in.b >= 0) last_use[in.b] = i;
+    for (auto& t : in.terms) last_use[t.second] = i;
+  }
+  env[0] = y;
+  env[1] = x;
+  int result = prog.empty() ? 1 : prog.back().dst;
+  auto need = [&](int r) -> const MV& {
+    if (!env[r].v.p && env[r].v.rows == 0) throw Error(kEInval, "malformed table form: unset register");
+    return env[r];
+  };
+  for (int i = 0; i < (int)prog.size(); ++i) {
+    const Instr& in = prog[i];
+    if (in.op == 0) {
+      // fusion candidate: next is lin(dst2, 0, [(1, other), (1, in.dst)]) or reversed,
+      // and in.dst is not used after it.
+      bool fused = false;
+      if (i + 1 < (int)prog.size()) {
+        const Instr& nx = prog[i + 1];
+        if (nx.op == 2 && nx.cconst == 0.0 && nx.terms.size() == 2 && nx.terms[0].first == 1.0 &&
+            nx.terms[1].first == 1.0 && last_use[in.dst] == i + 1 && in.dst != nx.dst) {
+          int other = -1;
+          if (nx.terms[1].second == in.dst && nx.terms[0].second != in.dst) other = nx.terms[0].second;
+          if (nx.terms[0].second == in.dst && nx.terms[1].second != in.dst) other = nx.terms[1].second;
+          if (other >= 0) {
+            env[nx.dst] = gemm_new(c, need(in.a), need(in.b), 1.0, &need(other), 1.0);
+            ++i;
+            fused = true;
+          }
+        }
+      }
+      if (!fused) env[in.dst] = gemm_new(c, need(in.a), need(in.b));
+    } else if (in.op == 1) {
+      env[in.dst] = residual(c, need(in.a), a);
+    } else {
+      std::vector<std::pair<double, const MV*>> terms;
+      for (auto& t : in.terms) terms.emplace_back(t.first, &need(t.second));
+      env[in.dst] = lincomb(c, in.cconst, terms, x.v.rows, x.v.cols);
+    }
+    // release dead temporaries (never Y/X or the result)
+    for (int r = 2; r < nr; ++r)
+      if (r != result && last_use[r] >= 0 && last_use[r] <= i && env[r].own) env[r] = MV{};
+  }
+  return env[result];
+}
+
+// st:385-405
+MV eval_node(Ctx& c, const PlanNode& node, const MV& y, const MV& x, const MV& a) {
+  switch (node.kind) {
+    case 0:
+      return horner(c, y, x, node.h);
+    case 1: {
+      MV u = (node.p == 0) ? x : eval_node(c, *node.inner, y, x, a);
+      if (node.w == 1) return u;
+      MV q = (node.p == 0) ? y : residual(c, u, a);
+      return eval_node(c, *node.outer, q, u, a);
+    }
+    case 2: {
+      MV z = eval_node(c, *node.inner, y, x, a);
+      return gemm_new(c, y, z, 1.0, &x, 1.0);  // x + y z
+    }
+    default:
+      return run_program(c, node, y, x, a);
+  }
+}
+
+// mc:137-151
+MV mat_pow_counted(Ctx& c, const MV& y, int e) {
+  if (e == 0) {
+    MV d = alloc(c, y.v.rows, y.v.cols);
+    check(launch_fill_identity(d.v, 1.0, c.s), "identity");
+    c.h->launches += 1;
+    return d;
+  }
+  MV base = y, result;
+  bool have = false;
+  while (e > 0) {
+    if (e & 1) {
+      result = have ? gemm_new(c, result, base) : base;
+      have = true;
+    }
+    e >>= 1;
+    if (e) base = gemm_new(c, base, base);
+  }
+  return result;
+}
+
+// st:432-457
+MV geometric(Ctx& c, const MV& y, const MV& x, int order, const MV& a, const PlanNode* base) {
+  if (order < 1) throw Error(kEInval, "order must be >= 1");
+  if (order == 1) {
+    MV d = alloc(c, x.v.rows, x.v.cols);
+    copy_into(c, d, x);
+    return d;
+  }
+  if (order <= 64) {
+    if (!base || plan_order_of(*base) != order) throw Error(kEInval, "missing plan for geometric order");
+    return eval_node(c, *base, y, x, a);
+  }
+  const int half = order / 2;
+  MV t = geometric(c, y, x, half, a, base);
+  MV yh = mat_pow_counted(c, y, half);
+  MV z = gemm_new(c, yh, t, 1.0, &t, 1.0);  // t + y^half t
+  if (order % 2) z = gemm_new(c, y, z, 1.0, &x, 1.0);
+  return z;
+}
+
+// ---------------------------------------------------------------------------
+// fork / join (executor hook: newton_schulz.py:275-285, richardson.py:556-566)
+// ---------------------------------------------------------------------------
+
+static cudaEvent_t get_event(Handle* h, size_t i) {
+  while (h->events.size() <= i) {
+    cudaEvent_t e;
+    check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    h->events.push_back(e);
+  }
+  return h->events[i];
+}
+
+Fork::Fork(Ctx& c) : parent(c) {
+  cudaEvent_t e = get_event(c.h, 0);
+  check(cudaEventRecord(e, c.s), "cudaEventRecord");
+  evs.push_back(e);
+}
+
+Ctx Fork::branch(int i) {
+  if (i < 0 || i >= Handle::kSide) throw Error(kEInval, "too many branches");
+  Ctx ch(parent.h, parent.root);
+  ch.s = parent.h->side[i];
+  check(cudaStreamWaitEvent(ch.s, evs[0], 0), "cudaStreamWaitEvent");
+  return ch;
+}
+
+void Fork::join(Ctx& child) {
+  cudaEvent_t e = get_event(parent.h, 1 + evs.size());
+  check(cudaEventRecord(e, child.s), "cudaEventRecord");
+  check(cudaStreamWaitEvent(parent.s, e, 0), "cudaStreamWaitEvent");
+  evs.push_back(e);
+  parent.ctr.mmm += child.ctr.mmm;
+  parent.ctr.mvm += child.ctr.mvm;
+}
+
+}  // namespace si

@@ -1,0 +1,121 @@
+// Native step engine: the seriesinv hot path (series_toolkit.py evaluators,
+// newton_schulz.py steps, richardson.py steps) as stream-ordered sequences of
+// fused FP64 GEMMs on device-resident matrices.
+#pragma once
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace si {
+
+enum Status : int { kOk = 0, kEInval = -1, kECuda = -2, kENoMem = -3 };
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+struct Handle {
+  int device = 0;
+  cudaMemPool_t pool = nullptr;
+  static constexpr int kSide = 5;
+  cudaStream_t side[kSide] = {};
+  std::vector<cudaEvent_t> events;
+  double* red_work = nullptr;  // reduction scratch
+  size_t red_elems = 0;
+  double* scalar = nullptr;    // one device double
+  // live profiling of the dominant kernel (bench.py roofline): CUDA events
+  // around every TMA GEMM launch, on the stream it is launched on.
+  struct ProfRec {
+    cudaEvent_t start, stop;
+    double flops;
+  };
+  bool profiling = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> prof_pool;
+  int64_t launches = 0;  // kernels launched by this handle
+};
+
+// Owning device buffer, released stream-ordered on its root stream.
+struct Buf {
+  double* p = nullptr;
+  cudaStream_t free_stream = nullptr;
+  ~Buf();
+};
+
+// A matrix value: a view plus (optional) shared ownership of its storage.
+struct MV {
+  Mat v;
+  std::shared_ptr<Buf> own;
+  int64_t n() const { return v.rows; }
+};
+
+struct Counters {
+  int64_t mmm = 0, mvm = 0;
+};
+
+// Execution context for one C-ABI call: root stream + current stream.
+struct Ctx {
+  Handle* h;
+  cudaStream_t root;
+  cudaStream_t s;
+  Counters ctr;
+  Ctx(Handle* hh, cudaStream_t st) : h(hh), root(st), s(st) {}
+};
+
+void check(cudaError_t e, const char* what);
+MV view(double* p, int64_t rows, int64_t cols, int64_t ld);
+MV alloc(Ctx& c, int64_t rows, int64_t cols);
+
+// D = alpha * A @ B + beta * C + diag * I  (one counted product; mv=true ticks mvm)
+void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha = 1.0,
+          const MV* C = nullptr, double beta = 0.0, double diag = 0.0, bool mv = false);
+MV gemm_new(Ctx& c, const MV& A, const MV& B, double alpha = 1.0, const MV* C = nullptr,
+            double beta = 0.0, double diag = 0.0, bool mv = false);
+// I - X @ A
+MV residual(Ctx& c, const MV& X, const MV& A);
+void residual_into(Ctx& c, const MV& D, const MV& X, const MV& A);
+void copy_into(Ctx& c, const MV& D, const MV& X);
+MV lincomb(Ctx& c, double cdiag, const std::vector<std::pair<double, const MV*>>& terms,
+           int64_t rows, int64_t cols);
+
+// ---- plans (series_toolkit.py:71-157), decoded from the int32 preorder form ----
+struct PlanNode;
+using PlanPtr = std::shared_ptr<const PlanNode>;
+struct Instr {
+  int op;  // 0 mul, 1 residual, 2 lin
+  int dst, a, b;
+  double cconst;
+  std::vector<std::pair<double, int>> terms;
+};
+struct PlanNode {
+  int kind;  // 0 horner, 1 split, 2 wrap, 3 table
+  int h = 0, p = 0, w = 0, order = 0, nregs = 0;
+  PlanPtr inner, outer;
+  std::vector<Instr> prog;
+};
+PlanPtr decode_plan(const int32_t* code, int64_t len, const double* consts, int64_t nconsts);
+int plan_order_of(const PlanNode& n);
+
+// ---- evaluators (series_toolkit.py:263-457) ----
+MV horner(Ctx& c, const MV& y, const MV& x, int h);
+MV factored(Ctx& c, const MV& y, const MV& x, const MV& a, int p, int w);
+MV eval_node(Ctx& c, const PlanNode& node, const MV& y, const MV& x, const MV& a);
+// geometric_apply (st:432-457): `base` is plan_order(b) for the order b <= 64
+// reached by repeated halving (null when that order is 1).
+MV geometric(Ctx& c, const MV& y, const MV& x, int order, const MV& a, const PlanNode* base);
+MV mat_pow_counted(Ctx& c, const MV& y, int e);
+
+// ---- fork/join helpers for the executor mapping ----
+struct Fork {
+  Ctx& parent;
+  std::vector<cudaEvent_t> evs;
+  explicit Fork(Ctx& c);
+  Ctx branch(int i);                 // a child ctx on side stream i, ordered after parent
+  void join(Ctx& child);             // parent waits for child; counters merged
+};
+
+}  // namespace si

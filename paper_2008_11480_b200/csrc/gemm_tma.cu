@@ -1,0 +1,336 @@
+// FP64 GEMM for sm_100a: TMA-staged, mbarrier-pipelined, warp-specialised,
+// persistent, on the FP64 DMMA tensor path (mma.sync m8n8k4 -> SASS DMMA.8x8x4),
+// with the seriesinv epilogue D = alpha*(A@B) + beta*C + diag*I fused.
+//
+// This is the kernel behind every n x n product of the hot path
+// (matrix_core.py:101-106 mat_mul, and the element-wise op that follows each
+// product at its call site: series_toolkit.py:265-266, :273, :375-378;
+// newton_schulz.py:144,166,210,215-220,268-270,287-288; richardson.py:148-154,168).
+//
+// Design (B200, 148 SMs, DMMA peak measured at 37.0 TFLOP/s = 64 FMA/clk/SM):
+//  * CTA tile 128x128, BK=16 doubles per stage, 6-stage ring (32 KB/stage).
+//  * 1 producer warp: one lane issues cp.async.bulk.tensor (TMA) for the A box
+//    (16 x 128, 128B swizzle) and up to 8 B boxes (16 x 16, 128B swizzle).
+//  * 8 consumer warps (2 x 4), warp tile 64 x 32 = 8 x 4 DMMA tiles, 128 FP64
+//    accumulator registers per thread.
+//  * Bank-conflict-free fragment loads: the 4 k-lanes of each DMMA read k rows
+//    {0,1,4,5} / {2,3,6,7} (+8) of the swizzled slab, so every 256 B warp load is
+//    exactly 2 shared-memory wavefronts for both operands.  The permutation is
+//    fixed, so the K accumulation order is deterministic (serial == concurrent
+//    bitwise, newton_schulz.py:259-261).
+//  * Persistent grid (<= #SMs CTAs), grouped tile rasterisation for L2 reuse;
+//    the producer runs ahead into the next tile while consumers drain the
+//    epilogue.
+#include "common.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+namespace si {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16;
+constexpr int STAGES = 6;
+constexpr int NUM_CONSUMER_WARPS = 8;
+constexpr int THREADS = (NUM_CONSUMER_WARPS + 1) * 32;
+constexpr int A_STAGE_BYTES = BM * BK * 8;  // 16 KB
+constexpr int B_BOX_BYTES = 16 * BK * 8;    // 2 KB (16 cols x 16 rows)
+constexpr int B_STAGE_BYTES = BK * BN * 8;  // 16 KB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
+constexpr int GROUP_M = 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double lds(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+// k index supplied by k-lane t (0..3) of k-step s (0..3) inside a 16-deep slab.
+__device__ __forceinline__ int kperm(int s, int t) {
+  return (s >> 1) * 8 + (s & 1) * 2 + (t >> 1) * 4 + (t & 1);
+}
+
+__device__ __forceinline__ double apply_epi(double acc, double alpha, double beta, double cval) {
+  double v = (alpha == 1.0) ? acc : (alpha == -1.0 ? -acc : __dmul_rn(alpha, acc));
+  if (beta != 0.0) v = __dadd_rn(v, beta == 1.0 ? cval : __dmul_rn(beta, cval));
+  return v;
+}
+
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& tm, int& tn) {
+  const int per_group = GROUP_M * num_n;
+  const int group = tile / per_group;
+  const int first_m = group * GROUP_M;
+  const int gsize = min(num_m - first_m, GROUP_M);
+  const int r = tile % per_group;
+  tm = first_m + r % gsize;
+  tn = r / gsize;
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, double* __restrict__ D,
+                        int64_t ldd, const double* __restrict__ C, int64_t ldc, int M, int N,
+                        int K, double alpha, double beta, double diag) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bars = base + STAGES * STAGE_BYTES;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int kblocks = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), NUM_CONSUMER_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == NUM_CONSUMER_WARPS) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int tm, tn;
+        tile_coords(tile, num_m, num_n, tm, tn);
+        const int n0 = tn * BN;
+        const int nboxes = min(8, (N - n0 + 15) / 16);
+        const uint32_t bytes = A_STAGE_BYTES + nboxes * B_BOX_BYTES;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1u);
+          const uint32_t sa = base + stage * STAGE_BYTES;
+          const uint32_t sb = sa + A_STAGE_BYTES;
+          mbar_expect_tx(full_bar(stage), bytes);
+          tma_load_2d(sa, &tmA, full_bar(stage), kb * BK, tm * BM);
+          for (int j = 0; j < nboxes; ++j)
+            tma_load_2d(sb + j * B_BOX_BYTES, &tmB, full_bar(stage), n0 + j * 16, kb * BK);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- DMMA consumers ----------------
+  const int wm = warp >> 2;  // 0..1 -> 64-row half
+  const int wn = warp & 3;   // 0..3 -> 32-col quarter
+  const int g = lane >> 2;   // fragment row / col group
+  const int t = lane & 3;    // k-lane
+
+  uint32_t a_off[4], b_off[4][2];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int k = kperm(s, t);
+    a_off[s] = (wm * 64 + g) * 128 + ((((k >> 1) ^ g) & 7) << 4) + ((k & 1) << 3);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int nl = h * 8 + g;  // column inside a 16-wide box
+      b_off[s][h] = wn * 2 * B_BOX_BYTES + k * 128 + ((((nl >> 1) ^ (k & 7)) & 7) << 4) +
+                    ((nl & 1) << 3);
+    }
+  }
+
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    int tm, tn;
+    tile_coords(tile, num_m, num_n, tm, tn);
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int kb = 0; kb < kblocks; ++kb) {
+      mbar_wait(full_bar(stage), phase);
+      const uint32_t sa = base + stage * STAGE_BYTES;
+      const uint32_t sb = sa + A_STAGE_BYTES;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        double af[8], bf[4];
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi) af[mi] = lds(sa + a_off[s] + mi * 1024);
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) bf[ni] = lds(sb + b_off[s][ni & 1] + (ni >> 1) * B_BOX_BYTES);
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_bar(stage));
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+
+    // ---------------- fused epilogue ----------------
+    const int row0 = tm * BM + wm * 64 + g;
+    const int col0 = tn * BN + wn * 32 + 2 * t;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int row = row0 + mi * 8;
+      if (row >= M) continue;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int col = col0 + ni * 8;
+        if (col >= N) continue;
+        double c0 = 0.0, c1 = 0.0;
+        const bool two = (col + 1 < N);
+        if (beta != 0.0) {
+          if (two) {
+            const double2 cv = *reinterpret_cast<const double2*>(C + (int64_t)row * ldc + col);
+            c0 = cv.x;
+            c1 = cv.y;
+          } else {
+            c0 = C[(int64_t)row * ldc + col];
+          }
+        }
+        double v0 = apply_epi(acc[mi][ni][0], alpha, beta, c0);
+        double v1 = apply_epi(acc[mi][ni][1], alpha, beta, c1);
+        if (diag != 0.0) {
+          if (row == col) v0 = __dadd_rn(v0, diag);
+          if (row == col + 1) v1 = __dadd_rn(v1, diag);
+        }
+        if (two) {
+          *reinterpret_cast<double2*>(D + (int64_t)row * ldd + col) = make_double2(v0, v1);
+        } else {
+          D[(int64_t)row * ldd + col] = v0;
+        }
+      }
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* map, const double* ptr, int64_t rows, int64_t cols, int64_t ld,
+              uint32_t box_cols, uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+}  // namespace
+
+bool tma_eligible(const Mat& A, const Mat& B, const Mat& D, const Epilogue& e) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  if (!al16(A.p) || !al16(B.p) || !al16(D.p)) return false;
+  if ((A.ld & 1) || (B.ld & 1) || (D.ld & 1)) return false;
+  if (e.beta != 0.0 && (!al16(e.c) || (e.ldc & 1))) return false;
+  if (A.rows > INT32_MAX || A.cols > INT32_MAX || B.cols > INT32_MAX) return false;
+  return get_encode() != nullptr;
+}
+
+cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& e,
+                            cudaStream_t s) {
+  CUtensorMap ta, tb;
+  if (!make_map(&ta, A.p, A.rows, A.cols, A.ld, BK, BM) ||
+      !make_map(&tb, B.p, B.rows, B.cols, B.ld, 16, BK)) {
+    set_error("cuTensorMapEncodeTiled failed");
+    return cudaErrorInvalidValue;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t err = cudaFuncSetAttribute(gemm_f64_tma_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    attr_set = true;
+  }
+  const int M = (int)D.rows, N = (int)D.cols, K = (int)A.cols;
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  gemm_f64_tma_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, D.p, D.ld, e.c, e.ldc, M, N, K,
+                                                        e.alpha, e.beta, e.diag);
+  return cudaGetLastError();
+}
+
+}  // namespace si

@@ -1,0 +1,228 @@
+// Step bodies of newton_schulz.py and richardson.py on the native engine.
+// Outputs are caller-owned device buffers; inputs are never written (the
+// reference's purity contract: states are immutable, matrix_core.py:52).
+#include "steps.hpp"
+
+namespace si {
+
+// ns:127-147
+void initial_series(Ctx& c, const MV& P, const MV& B, const MV& A, int p, int w, const MV& Gout,
+                    const MV& Fout) {
+  if (p < 0 || w < 1) throw Error(kEInval, "requires p >= 0 and w >= 1");
+  const int h = w * (p + 1);
+  if (h == 1) {
+    copy_into(c, Gout, P);
+    copy_into(c, Fout, B);
+    return;
+  }
+  MV g = factored(c, B, P, A, p, w);
+  copy_into(c, Gout, g);
+  residual_into(c, Fout, Gout, A);
+}
+
+// ns:150-174
+void ns_step(Ctx& c, const MV& A, const MV& G, const MV& F, int order, const PlanNode* plan,
+             const MV& Gout, const MV& Fout) {
+  if (order < 1) throw Error(kEInval, "order must be >= 1");
+  MV g;
+  if (plan) {
+    if (plan_order_of(*plan) != order) throw Error(kEInval, "plan order != iteration order");
+    g = eval_node(c, *plan, F, G, A);
+  } else {
+    g = horner(c, F, G, order);
+  }
+  copy_into(c, Gout, g);
+  residual_into(c, Fout, Gout, A);
+}
+
+// ns:177-228 -- parts (T_i, Gamma_i) are independent of each other and of the
+// state; with `concurrent` each part (and the NS part) runs on its own stream.
+void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, const MV& B,
+                    const MV& Sm, const std::vector<int>& rates,
+                    const std::vector<const PlanNode*>& plans, int order_n, bool concurrent,
+                    const MV& Gout, const MV& Fout) {
+  if (order_n < 1) throw Error(kEInval, "order_n must be >= 1");
+  if (rates.empty()) throw Error(kEInval, "composite spec needs at least one rate");
+  const size_t k = rates.size();
+  std::vector<MV> ts(k), gs(k);
+  MV nsp;
+  auto part = [&](Ctx& cc, size_t i) {
+    if (rates[i] < 1) throw Error(kEInval, "rates must be positive integers");
+    if (rates[i] == 1) {
+      ts[i] = alloc(cc, P.v.rows, P.v.cols);
+      copy_into(cc, ts[i], P);
+    } else {
+      ts[i] = geometric(cc, B, P, rates[i], Sm, plans[i]);
+    }
+    gs[i] = residual(cc, ts[i], A);
+  };
+  if (concurrent) {
+    Fork fk(c);
+    std::vector<Ctx> kids;
+    const int nstreams = Handle::kSide - 1;
+    for (int s = 0; s < nstreams && s < (int)k; ++s) kids.push_back(fk.branch(s));
+    for (size_t i = 0; i < k; ++i) part(kids[i % kids.size()], i);
+    Ctx nsc = fk.branch(Handle::kSide - 1);
+    nsp = horner(nsc, F, G, order_n);
+    for (auto& kd : kids) fk.join(kd);
+    fk.join(nsc);
+  } else {
+    for (size_t i = 0; i < k; ++i) part(c, i);
+  }
+  MV t = ts[0], r = gs[0];
+  for (size_t i = 1; i < k; ++i) {
+    t = gemm_new(c, r, ts[i], 1.0, &t, 1.0);  // t + r T_i
+    r = gemm_new(c, r, gs[i]);                // r Gamma_i
+  }
+  if (!concurrent) nsp = horner(c, F, G, order_n);
+  gemm(c, Gout, r, nsp, 1.0, &t, 1.0);  // G = t + r ns
+  residual_into(c, Fout, Gout, A);
+}
+
+// ns:231-251
+void initial_double(Ctx& c, const MV& P, const MV& B, const MV& A, int p, int w, int order,
+                    const MV& Gout, const MV& Fout, const MV& Lout, const MV& Rout) {
+  initial_series(c, P, B, A, p, w, Gout, Fout);
+  MV l0 = horner(c, Fout, Gout, order);
+  copy_into(c, Lout, l0);
+  residual_into(c, Rout, Lout, A);
+}
+
+// ns:254-298
+void double_ns_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& L, const MV& R,
+                    int order, bool concurrent, const MV& Gout, const MV& Fout, const MV& Lout,
+                    const MV& Rout) {
+  if (order < 1) throw Error(kEInval, "order must be >= 1");
+  MV nsp;
+  auto accel = [&](Ctx& cc) {
+    MV gamma = residual(cc, L, A);
+    MV l = horner(cc, gamma, L, order);
+    copy_into(cc, Lout, l);
+    residual_into(cc, Rout, Lout, A);
+  };
+  if (concurrent) {
+    Fork fk(c);
+    Ctx c1 = fk.branch(0), c2 = fk.branch(1);
+    accel(c1);
+    nsp = horner(c2, F, G, order);
+    fk.join(c1);
+    fk.join(c2);
+  } else {
+    accel(c);
+    nsp = horner(c, F, G, order);
+  }
+  gemm(c, Gout, Rout, nsp, 1.0, &Lout, 1.0);  // L' + R' ns
+  residual_into(c, Fout, Gout, A);
+}
+
+// ns:301-325
+void additive_correction_step(Ctx& c, const MV& A, const MV& Z, const MV& G, int p,
+                              const MV& Zout, const MV& Gout) {
+  if (p < 2) throw Error(kEInval, "order p must be >= 2");
+  MV lprev = residual(c, Z, A);
+  MV zn = horner(c, lprev, Z, p);
+  copy_into(c, Zout, zn);
+  MV fprev = residual(c, G, A);
+  gemm(c, Gout, fprev, Zout, 1.0, &G, 1.0);
+}
+
+// ri:81-98
+void richardson_step(Ctx& c, const MV& A, const MV& b, const MV& theta, const MV& G, const MV& F,
+                     const MV& L, const MV& R, int order, int q, const MV& Gout, const MV& Fout,
+                     const MV& Lout, const MV& Rout, const MV& theta_out) {
+  if (q < 1) throw Error(kEInval, "q must be >= 1");
+  double_ns_step(c, A, G, F, L, R, order, false, Gout, Fout, Lout, Rout);
+  MV s = horner(c, Fout, Gout, q);
+  MV wgt = gemm_new(c, Rout, s, 1.0, &Lout, 1.0);
+  MV resid = gemm_new(c, A, theta, 1.0, &b, -1.0, 0.0, true);   // A theta - b
+  gemm(c, theta_out, wgt, resid, -1.0, &theta, 1.0, 0.0, true);  // theta - W resid
+}
+
+// ri:101-108  I + gamma + ... + gamma^(n-1)
+MV power_sum(Ctx& c, const MV& gamma, int n) {
+  MV acc = alloc(c, gamma.v.rows, gamma.v.cols);
+  check(launch_fill_identity(acc.v, 1.0, c.s), "identity");
+  c.h->launches += 1;
+  MV cur;
+  bool have = false;
+  for (int i = 0; i < n - 1; ++i) {
+    cur = have ? gemm_new(c, cur, gamma) : gamma;
+    have = true;
+    acc = lincomb(c, 0.0, {{1.0, &acc}, {1.0, &cur}}, gamma.v.rows, gamma.v.cols);
+  }
+  return acc;
+}
+
+// Opt-in (not in the reference): S_n(gamma) for n = 2^m as the product of the
+// factors (I + gamma^(2^j)), i.e. S_2t = S_t + gamma^t S_t: 2(m-1) products
+// instead of the n-2 of power_sum.
+MV power_sum_doubling(Ctx& c, const MV& gamma, int n) {
+  if (n < 2 || (n & (n - 1))) throw Error(kEInval, "doubling power sum needs n = 2^m >= 2");
+  MV eye = alloc(c, gamma.v.rows, gamma.v.cols);
+  check(launch_fill_identity(eye.v, 1.0, c.s), "identity");
+  c.h->launches += 1;
+  MV s = lincomb(c, 0.0, {{1.0, &eye}, {1.0, &gamma}}, gamma.v.rows, gamma.v.cols);  // I + gamma
+  MV pw = gamma;
+  for (int t = 2; t < n; t *= 2) {
+    pw = gemm_new(c, pw, pw);               // gamma^t
+    s = gemm_new(c, pw, s, 1.0, &s, 1.0);   // S_2t = S_t + gamma^t S_t
+  }
+  return s;
+}
+
+// ri:111-189.  Opt-in factorised variant (not in the reference): `factor_plan`
+// evaluates N' = S_n(F) G through a plan of order n and `doubling_sum` builds
+// S_n(gamma) by power_sum_doubling (order 16: 18 products instead of 34).
+void richardson_recursive_step(Ctx& c, const MV& A, const MV& b, const MV& theta, const MV& G,
+                               const MV& F, const MV& L, const MV& R, const MV* omega,
+                               const MV* ns_part, int order, bool concurrent,
+                               const PlanNode* factor_plan, bool doubling_sum,
+                               const MV& Gout, const MV& Fout, const MV& Lout, const MV& Rout,
+                               const MV& omega_out, const MV& ns_out, const MV& theta_out) {
+  const int n = order;
+  if (n < 1) throw Error(kEInval, "order must be >= 1");
+  MV ns_prev, om_prev;
+  if (!omega || !ns_part) {
+    ns_prev = horner(c, F, G, n);
+    om_prev = gemm_new(c, R, ns_prev, 1.0, &L, 1.0);
+  } else {
+    ns_prev = *ns_part;
+    om_prev = *omega;
+  }
+  MV s = doubling_sum ? power_sum_doubling(c, R, n) : power_sum(c, R, n);
+  MV nsn;
+  auto estimate = [&](Ctx& cc) {
+    MV diff = lincomb(cc, 0.0, {{1.0, &om_prev}, {-1.0, &ns_prev}}, G.v.rows, G.v.cols);
+    gemm(cc, Gout, s, diff, 1.0, &ns_prev, 1.0);  // S (om - ns) + ns
+    residual_into(cc, Fout, Gout, A);
+    nsn = factor_plan ? eval_node(cc, *factor_plan, Fout, Gout, A) : horner(cc, Fout, Gout, n);
+  };
+  auto accel = [&](Ctx& cc) {
+    gemm(cc, Lout, s, L);
+    residual_into(cc, Rout, Lout, A);
+  };
+  if (concurrent) {
+    Fork fk(c);
+    Ctx c1 = fk.branch(0), c2 = fk.branch(1);
+    estimate(c1);
+    accel(c2);
+    fk.join(c1);
+    fk.join(c2);
+  } else {
+    estimate(c);
+    accel(c);
+  }
+  copy_into(c, ns_out, nsn);
+  gemm(c, omega_out, Rout, ns_out, 1.0, &Lout, 1.0);              // L' + R' N'
+  MV resid = gemm_new(c, A, theta, 1.0, &b, -1.0, 0.0, true);     // A theta - b
+  gemm(c, theta_out, omega_out, resid, -1.0, &theta, 1.0, 0.0, true);
+}
+
+// theta + P (b - A theta), evaluated as ri:88-89 does.
+void plain_richardson(Ctx& c, const MV& A, const MV& b, const MV& theta, const MV& P,
+                      const MV& theta_out) {
+  MV resid = gemm_new(c, A, theta, 1.0, &b, -1.0, 0.0, true);
+  gemm(c, theta_out, P, resid, -1.0, &theta, 1.0, 0.0, true);
+}
+
+}  // namespace si

@@ -1,0 +1,37 @@
+#pragma once
+#include <vector>
+
+#include "engine.hpp"
+
+namespace si {
+
+void initial_series(Ctx& c, const MV& P, const MV& B, const MV& A, int p, int w, const MV& Gout,
+                    const MV& Fout);
+void ns_step(Ctx& c, const MV& A, const MV& G, const MV& F, int order, const PlanNode* plan,
+             const MV& Gout, const MV& Fout);
+void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, const MV& B,
+                    const MV& Sm, const std::vector<int>& rates,
+                    const std::vector<const PlanNode*>& plans, int order_n, bool concurrent,
+                    const MV& Gout, const MV& Fout);
+void initial_double(Ctx& c, const MV& P, const MV& B, const MV& A, int p, int w, int order,
+                    const MV& Gout, const MV& Fout, const MV& Lout, const MV& Rout);
+void double_ns_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& L, const MV& R,
+                    int order, bool concurrent, const MV& Gout, const MV& Fout, const MV& Lout,
+                    const MV& Rout);
+void additive_correction_step(Ctx& c, const MV& A, const MV& Z, const MV& G, int p,
+                              const MV& Zout, const MV& Gout);
+void richardson_step(Ctx& c, const MV& A, const MV& b, const MV& theta, const MV& G, const MV& F,
+                     const MV& L, const MV& R, int order, int q, const MV& Gout, const MV& Fout,
+                     const MV& Lout, const MV& Rout, const MV& theta_out);
+MV power_sum(Ctx& c, const MV& gamma, int n);
+MV power_sum_doubling(Ctx& c, const MV& gamma, int n);
+void richardson_recursive_step(Ctx& c, const MV& A, const MV& b, const MV& theta, const MV& G,
+                               const MV& F, const MV& L, const MV& R, const MV* omega,
+                               const MV* ns_part, int order, bool concurrent,
+                               const PlanNode* factor_plan, bool doubling_sum,
+                               const MV& Gout, const MV& Fout, const MV& Lout, const MV& Rout,
+                               const MV& omega_out, const MV& ns_out, const MV& theta_out);
+void plain_richardson(Ctx& c, const MV& A, const MV& b, const MV& theta, const MV& P,
+                      const MV& theta_out);
+
+}  // namespace si

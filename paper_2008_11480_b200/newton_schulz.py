@@ -1,0 +1,284 @@
+"""High-order Newton-Schulz family on the device (newton_schulz.py).
+
+Same signatures, state fields and errors as ``seriesinv.newton_schulz``; the
+states hold device tensors and every step body is one C-ABI call that runs the
+reference's GEMM DAG on the DMMA kernels.  ``executor`` arguments map to
+concurrent CUDA streams (bitwise identical to the serial path).  The integer
+exponent laws (newton_schulz.py:343-400) are host arithmetic and are restated
+here unchanged in meaning.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from math import sqrt
+
+import torch
+
+from . import _lib
+from .matrix_core import MulCounter, as_device, fro_norm
+from .series_toolkit import FactorPlan, encode_many, encode_plan, geometric_base_plan
+from .splitting import Splitting
+
+__all__ = [
+    "CompositeSpec",
+    "DoubleNsState",
+    "NsState",
+    "additive_correction_step",
+    "additive_exponents",
+    "classical_exponent",
+    "composite_exponent",
+    "composite_step",
+    "constant_rates",
+    "converged",
+    "double_exponent",
+    "double_ns_step",
+    "initial_double",
+    "initial_series",
+    "ns_step",
+    "power_rates",
+    "residual_exponent",
+    "run_until_converged",
+]
+
+DEFAULT_MAX_STEPS = 30
+
+
+@dataclass
+class NsState:
+    """G_k (estimate), F_k = I - G_k A (residual) (newton_schulz.py:58-72)."""
+
+    estimate: torch.Tensor
+    residual: torch.Tensor
+    step: int
+    order: int
+    series_order: int
+    ctr: MulCounter
+
+
+@dataclass
+class DoubleNsState:
+    """Two-loop state with accelerator L_k and its residual (newton_schulz.py:75-91)."""
+
+    estimate: torch.Tensor
+    residual: torch.Tensor
+    accel_estimate: torch.Tensor
+    accel_residual: torch.Tensor
+    step: int
+    order: int
+    series_order: int
+    ctr: MulCounter
+
+
+@dataclass(frozen=True)
+class CompositeSpec:
+    """Expansion rates x_i, one per parallel unit (newton_schulz.py:94-108)."""
+
+    rates: tuple[int, ...]
+
+    def __post_init__(self):
+        if not self.rates:
+            raise ValueError("composite spec needs at least one rate")
+        if any(x < 1 for x in self.rates):
+            raise ValueError("rates must be positive integers")
+
+    @property
+    def width(self) -> int:
+        return len(self.rates)
+
+
+def constant_rates(rate: int, width: int) -> CompositeSpec:
+    return CompositeSpec(rates=(rate,) * width)
+
+
+def power_rates(base: int, width: int):
+    """At step k every unit expands at rate base**k (newton_schulz.py:116-124)."""
+    if base < 2:
+        raise ValueError("base must be >= 2")
+
+    def spec_for_step(k: int) -> CompositeSpec:
+        return CompositeSpec(rates=(base**k,) * width)
+
+    return spec_for_step
+
+
+def _ctx(t: torch.Tensor):
+    return _lib.handle(t.device.index), _lib.stream_ptr(t.device)
+
+
+def initial_series(split: Splitting, p: int, w: int, order: int = 2) -> NsState:
+    """G_0 = S_h(B) S^-1 with h = w(p+1) (newton_schulz.py:127-147)."""
+    if order < 1:
+        raise ValueError("order must be >= 1")
+    if p < 0 or w < 1:
+        raise ValueError("requires p >= 0 and w >= 1")
+    ctr = MulCounter()
+    n = split.matrix.shape[0]
+    g = torch.empty_like(split.matrix)
+    f = torch.empty_like(split.matrix)
+    h, s = _ctx(g)
+    buf = _lib.counter_buf()
+    _lib.call("si_initial_series", h, n, split.precond.data_ptr(), split.residual.data_ptr(),
+              split.matrix.data_ptr(), p, w, g.data_ptr(), f.data_ptr(), buf, s)
+    ctr.absorb(buf)
+    return NsState(estimate=g, residual=f, step=0, order=order, series_order=w * (p + 1), ctr=ctr)
+
+
+def ns_step(st: NsState, a, plan: FactorPlan | None = None) -> NsState:
+    """G_k = S_n(F) G (Horner or ``plan``), F_k = I - G_k A (newton_schulz.py:150-174)."""
+    n = st.order
+    a = as_device(a)
+    if a.shape != st.estimate.shape:
+        raise ValueError("dimension mismatch between state and matrix")
+    code: list[int] = []
+    consts: list[float] = []
+    if plan is not None:
+        if plan.order_h != n:
+            raise ValueError(f"plan order {plan.order_h} != iteration order {n}")
+        code, consts = encode_plan(plan)
+    g = torch.empty_like(st.estimate)
+    f = torch.empty_like(st.estimate)
+    h, s = _ctx(g)
+    buf = _lib.counter_buf()
+    _lib.call("si_ns_step", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
+              st.residual.data_ptr(), n, _lib.i32_array(code) if code else None, len(code),
+              _lib.f64_array(consts) if consts else None, len(consts), g.data_ptr(), f.data_ptr(),
+              buf, s)
+    st.ctr.absorb(buf)
+    return NsState(estimate=g, residual=f, step=st.step + 1, order=n,
+                   series_order=st.series_order, ctr=st.ctr)
+
+
+def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_n: int,
+                   executor=None) -> NsState:
+    """G_k = T_comp + R_comp S_n(F) G, F_k = I - G_k A (newton_schulz.py:177-228).
+
+    ``executor`` (not in the reference signature, whose parts run serially)
+    evaluates the independent parts on concurrent streams."""
+    if order_n < 1:
+        raise ValueError("order_n must be >= 1")
+    a = as_device(a)
+    if a.shape != st.estimate.shape:
+        raise ValueError("dimension mismatch between state and matrix")
+    plans = [geometric_base_plan(x) if x > 1 else None for x in spec.rates]
+    code, offsets, consts = encode_many(plans)
+    g = torch.empty_like(st.estimate)
+    f = torch.empty_like(st.estimate)
+    h, s = _ctx(g)
+    buf = _lib.counter_buf()
+    _lib.call("si_composite_step", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
+              st.residual.data_ptr(), split.precond.data_ptr(), split.residual.data_ptr(),
+              split.matrix.data_ptr(), len(spec.rates), _lib.i32_array(list(spec.rates)),
+              _lib.i32_array(code), _lib.i64_array(offsets), _lib.f64_array(consts), len(consts),
+              order_n, int(executor is not None), g.data_ptr(), f.data_ptr(), buf, s)
+    st.ctr.absorb(buf)
+    return NsState(estimate=g, residual=f, step=st.step + 1, order=order_n,
+                   series_order=st.series_order, ctr=st.ctr)
+
+
+def initial_double(split: Splitting, p: int, w: int, order: int = 2) -> DoubleNsState:
+    """Two-loop init: L_0 = S_n(F_0) G_0 (newton_schulz.py:231-251)."""
+    if order < 1:
+        raise ValueError("order must be >= 1")
+    if p < 0 or w < 1:
+        raise ValueError("requires p >= 0 and w >= 1")
+    ctr = MulCounter()
+    m = split.matrix
+    g, f, l, r = (torch.empty_like(m) for _ in range(4))
+    h, s = _ctx(m)
+    buf = _lib.counter_buf()
+    _lib.call("si_initial_double", h, m.shape[0], split.precond.data_ptr(), split.residual.data_ptr(),
+              m.data_ptr(), p, w, order, g.data_ptr(), f.data_ptr(), l.data_ptr(), r.data_ptr(),
+              buf, s)
+    ctr.absorb(buf)
+    return DoubleNsState(estimate=g, residual=f, accel_estimate=l, accel_residual=r, step=0,
+                         order=order, series_order=w * (p + 1), ctr=ctr)
+
+
+def double_ns_step(st: DoubleNsState, a, executor=None) -> DoubleNsState:
+    """F_k = (I - L_k A) F_(k-1)^n (newton_schulz.py:254-298); ``executor`` -> two streams."""
+    a = as_device(a)
+    if a.shape != st.estimate.shape:
+        raise ValueError("dimension mismatch between state and matrix")
+    g, f, l, r = (torch.empty_like(st.estimate) for _ in range(4))
+    h, s = _ctx(g)
+    buf = _lib.counter_buf()
+    _lib.call("si_double_ns_step", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
+              st.residual.data_ptr(), st.accel_estimate.data_ptr(), st.accel_residual.data_ptr(),
+              st.order, int(executor is not None), g.data_ptr(), f.data_ptr(), l.data_ptr(),
+              r.data_ptr(), buf, s)
+    st.ctr.absorb(buf)
+    return DoubleNsState(estimate=g, residual=f, accel_estimate=l, accel_residual=r,
+                         step=st.step + 1, order=st.order, series_order=st.series_order, ctr=st.ctr)
+
+
+def additive_correction_step(z, g, a, p: int, ctr: MulCounter):
+    """Two-estimate additive scheme (newton_schulz.py:301-325)."""
+    if p < 2:
+        raise ValueError("order p must be >= 2")
+    z, g, a = as_device(z), as_device(g), as_device(a)
+    zn = torch.empty_like(z)
+    gn = torch.empty_like(g)
+    h, s = _ctx(z)
+    buf = _lib.counter_buf()
+    _lib.call("si_additive_correction_step", h, a.shape[0], a.data_ptr(), z.data_ptr(),
+              g.data_ptr(), p, zn.data_ptr(), gn.data_ptr(), buf, s)
+    ctr.absorb(buf)
+    return zn, gn
+
+
+def converged(st) -> bool:
+    """||F_k||_F <= 1e-13 sqrt(n) (newton_schulz.py:328-331)."""
+    dim = st.residual.shape[0]
+    return fro_norm(st.residual) <= 1e-13 * sqrt(dim)
+
+
+def run_until_converged(st: NsState, a, max_steps: int = DEFAULT_MAX_STEPS) -> NsState:
+    """Classical steps until converged or the cap (newton_schulz.py:334-340)."""
+    while st.step < max_steps and not converged(st):
+        st = ns_step(st, a)
+    return st
+
+
+# ---------------------------------------------------------------------------
+# Integer exponent laws: F_k = B**e (newton_schulz.py:343-400)
+# ---------------------------------------------------------------------------
+
+
+def classical_exponent(k: int, n: int, h: int) -> int:
+    return h * n**k
+
+
+def double_exponent(k: int, n: int, h: int) -> int:
+    return h * (k * n ** (k + 1) + n**k)
+
+
+def composite_exponent(k: int, n: int, h: int, rates: tuple[int, ...]) -> int:
+    e, total = h, sum(rates)
+    for _ in range(k):
+        e = total + n * e
+    return e
+
+
+def additive_exponents(k: int, p: int, h: int) -> tuple[int, int]:
+    e_l = e_f = h
+    for _ in range(k):
+        e_f += p * e_l
+        e_l *= p
+    return e_l, e_f
+
+
+def residual_exponent(kind: str, k: int, n: int, h: int, rates=None) -> int:
+    if k < 0:
+        raise ValueError("step index must be >= 0")
+    if kind == "classical":
+        return classical_exponent(k, n, h)
+    if kind == "double":
+        return double_exponent(k, n, h)
+    if kind == "composite":
+        if not rates:
+            raise ValueError("composite kind needs rates")
+        return composite_exponent(k, n, h, tuple(rates))
+    if kind == "additive":
+        return additive_exponents(k, n, h)[1]
+    raise ValueError(f"unknown iteration kind: {kind!r}")

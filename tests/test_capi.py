@@ -1,0 +1,79 @@
+"""The C-ABI library: loads without a GPU and exports every symbol the header declares."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "seriesinv_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"SI_API\s+(?:const\s+)?\w+\*?\s+(si_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_step_seam():
+    syms = declared_symbols()
+    for name in ("si_gemm", "si_ns_step", "si_composite_step", "si_double_ns_step",
+                 "si_richardson_step", "si_richardson_recursive_step", "si_plain_richardson",
+                 "si_batched_composite_richardson", "si_nested_eval", "si_geometric_apply"):
+        assert name in syms
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2008_11480_b200 import _lib
+
+    lib = _lib.load_library()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert lib.si_version() == 1
+
+
+def test_python_prototypes_cover_the_header():
+    from paper_2008_11480_b200 import _lib
+
+    declared = set(declared_symbols()) - {"si_version", "si_last_error"}
+    assert declared == set(_lib.SIGNATURES)
+
+
+def test_prototype_arity_matches_header():
+    from paper_2008_11480_b200 import _lib
+
+    text = open(HEADER).read()
+    for name, argtypes in _lib.SIGNATURES.items():
+        m = re.search(rf"{name}\s*\(([^;]*)\);", text, re.S)
+        assert m, name
+        params = [p for p in m.group(1).split(",") if p.strip() and p.strip() != "void"]
+        assert len(params) == len(argtypes), name
+
+
+def test_no_silent_cpu_fallback():
+    """Without a CUDA device the product path raises instead of computing on the host."""
+    import torch
+
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import _lib
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    with pytest.raises(_lib.NativeUnavailable):
+        P.mat_mul([[1.0]], [[1.0]], P.MulCounter())
+    with pytest.raises(_lib.NativeUnavailable):
+        _lib.handle()
+
+
+def test_abi_rejects_bad_arguments_without_gpu():
+    """Argument validation happens before any device work and maps to SI_EINVAL."""
+    from paper_2008_11480_b200 import _lib
+
+    lib = _lib.load_library()
+    assert lib.si_create(0, None) == _lib.SI_EINVAL
+    assert b"null" in lib.si_last_error()
+    buf = ctypes.c_void_p()
+    assert lib.si_gemm(None, 1, 1, 1, 1.0, None, 1, None, 1, 0.0, None, 1, 0.0, None, 1, 0, None,
+                       None) == _lib.SI_EINVAL
+    del buf
