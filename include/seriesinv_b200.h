@@ -69,10 +69,22 @@ SI_API int si_gemm(si_handle h, int64_t m, int64_t n, int64_t k, double alpha, c
             int64_t lda, const double* B, int64_t ldb, double beta, const double* C, int64_t ldc,
             double diag, double* D, int64_t ldd, int is_mv, int64_t* counters, void* stream);
 
+/* si_gemm with the diag*I term placed at (i, i + diag_offset): used on row
+ * blocks [r0, r0+m) of a block-row sharded matrix (diag_offset = r0). */
+SI_API int si_gemm_ex(si_handle h, int64_t m, int64_t n, int64_t k, double alpha,
+                      const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                      const double* C, int64_t ldc, double diag, int64_t diag_offset, double* D,
+                      int64_t ldd, int is_mv, int64_t* counters, void* stream);
+
 /* D = cdiag*I + sum_i coefs[i]*X[i] (nterms <= 6), one rounding per term in
  * order: the `Lin` instruction (series_toolkit.py:375-378). */
 SI_API int si_lincomb(si_handle h, int64_t m, int64_t n, double cdiag, int nterms, const double* coefs,
                const double* const* X, const int64_t* ldx, double* D, int64_t ldd, void* stream);
+
+/* si_lincomb with cdiag*I placed at (i, i + diag_offset) (row blocks). */
+SI_API int si_lincomb_ex(si_handle h, int64_t m, int64_t n, double cdiag, int64_t diag_offset,
+                         int nterms, const double* coefs, const double* const* X,
+                         const int64_t* ldx, double* D, int64_t ldd, void* stream);
 
 /* Host-returning reductions (synchronise `stream`): matrix_core.py:154-172. */
 SI_API int si_fro_norm(si_handle h, int64_t m, int64_t n, const double* X, int64_t ldx, double* out,

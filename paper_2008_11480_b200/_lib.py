@@ -31,7 +31,9 @@ SIGNATURES: dict[str, list] = {
     "si_destroy": [_P],
     "si_trim": [_P],
     "si_gemm": [_P, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _D, _P, _I64, _I, _PI64, _P],
+    "si_gemm_ex": [_P, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _D, _I64, _P, _I64, _I, _PI64, _P],
     "si_lincomb": [_P, _I64, _I64, _D, _I, _P, _P, _P, _P, _I64, _P],
+    "si_lincomb_ex": [_P, _I64, _I64, _D, _I64, _I, _P, _P, _P, _P, _I64, _P],
     "si_fro_norm": [_P, _I64, _I64, _P, _I64, POINTER(c_double), _P],
     "si_inf_norm": [_P, _I64, _I64, _P, _I64, POINTER(c_double), _P],
     "si_split_scalar": [_P, _I64, _P, _D, _P, _P, _P],

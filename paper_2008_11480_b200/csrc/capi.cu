@@ -146,6 +146,14 @@ int si_trim(si_handle h) {
 int si_gemm(si_handle h, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
             int64_t lda, const double* B, int64_t ldb, double beta, const double* C, int64_t ldc,
             double diag, double* D, int64_t ldd, int is_mv, int64_t* counters, void* stream) {
+  return si_gemm_ex(h, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, diag, 0, D, ldd, is_mv,
+                    counters, stream);
+}
+
+int si_gemm_ex(si_handle h, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+               int64_t lda, const double* B, int64_t ldb, double beta, const double* C,
+               int64_t ldc, double diag, int64_t diag_offset, double* D, int64_t ldd, int is_mv,
+               int64_t* counters, void* stream) {
   return guard([&] {
     need(h && A && B && D, "null pointer");
     need(m >= 0 && n >= 0 && k >= 0, "negative dimension");
@@ -155,12 +163,18 @@ int si_gemm(si_handle h, int64_t m, int64_t n, int64_t k, double alpha, const do
     MV a = view(const_cast<double*>(A), m, k, lda), b = view(const_cast<double*>(B), k, n, ldb);
     MV d = view(D, m, n, ldd);
     MV cm = view(const_cast<double*>(C), m, n, ldc);
-    gemm(call.c, d, a, b, alpha, C ? &cm : nullptr, beta, diag, is_mv != 0);
+    gemm(call.c, d, a, b, alpha, C ? &cm : nullptr, beta, diag, is_mv != 0, diag_offset);
   });
 }
 
 int si_lincomb(si_handle h, int64_t m, int64_t n, double cdiag, int nterms, const double* coefs,
                const double* const* X, const int64_t* ldx, double* D, int64_t ldd, void* stream) {
+  return si_lincomb_ex(h, m, n, cdiag, 0, nterms, coefs, X, ldx, D, ldd, stream);
+}
+
+int si_lincomb_ex(si_handle h, int64_t m, int64_t n, double cdiag, int64_t diag_offset,
+                  int nterms, const double* coefs, const double* const* X, const int64_t* ldx,
+                  double* D, int64_t ldd, void* stream) {
   return guard([&] {
     need(h && D, "null pointer");
     need(nterms >= 0 && nterms <= kMaxLinTerms, "nterms out of range");
@@ -172,7 +186,8 @@ int si_lincomb(si_handle h, int64_t m, int64_t n, double cdiag, int nterms, cons
       xs[i] = view(const_cast<double*>(X[i]), m, n, ldx[i]).v;
     }
     Mat d = view(D, m, n, ldd).v;
-    check(launch_lincomb(d, cdiag, nterms, coefs, xs, call.c.s), "lincomb");
+    check(launch_lincomb(d, cdiag, diag_offset, nterms, coefs, xs, call.c.s), "lincomb");
+    h->h.launches += 1;
   });
 }
 

@@ -21,6 +21,7 @@ struct Epilogue {
   double alpha = 1.0;
   double beta = 0.0;
   double diag = 0.0;
+  int64_t doff = 0;  // diag*I sits at (i, i + doff): row blocks of a sharded matrix
   const double* c = nullptr;
   int64_t ldc = 0;
 };
@@ -37,7 +38,7 @@ bool tma_eligible(const Mat& A, const Mat& B, const Mat& D, const Epilogue& e);
 // D = cdiag * I + sum_i coef[i] * X[i], accumulated in argument order with one
 // rounding per term (series_toolkit.py:375-378, numpy temporaries).
 constexpr int kMaxLinTerms = 6;
-cudaError_t launch_lincomb(Mat& D, double cdiag, int nterms, const double* coef, const Mat* X,
+cudaError_t launch_lincomb(Mat& D, double cdiag, int64_t doff, int nterms, const double* coef, const Mat* X,
                            cudaStream_t s);
 // D = scale * I  (scale=0 -> zeros)
 cudaError_t launch_fill_identity(Mat& D, double scale, cudaStream_t s);

@@ -51,7 +51,7 @@ MV alloc(Ctx& c, int64_t rows, int64_t cols) {
 // ---------------------------------------------------------------------------
 
 void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV* C, double beta,
-          double diag, bool mv) {
+          double diag, bool mv, int64_t doff) {
   if (A.v.cols != B.v.rows || D.v.rows != A.v.rows || D.v.cols != B.v.cols)
     throw Error(kEInval, "dimension mismatch in product");
   if (C && (C->v.rows != D.v.rows || C->v.cols != D.v.cols))
@@ -60,6 +60,7 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
   e.alpha = alpha;
   e.beta = C ? beta : 0.0;
   e.diag = diag;
+  e.doff = doff;
   e.c = C ? C->v.p : nullptr;
   e.ldc = C ? C->v.ld : 0;
   Mat d = D.v;
@@ -131,7 +132,7 @@ MV lincomb(Ctx& c, double cdiag, const std::vector<std::pair<double, const MV*>>
     coef[i] = terms[i].first;
     xs[i] = terms[i].second->v;
   }
-  check(launch_lincomb(D.v, cdiag, (int)terms.size(), coef, xs, c.s), "lincomb");
+  check(launch_lincomb(D.v, cdiag, 0, (int)terms.size(), coef, xs, c.s), "lincomb");
   c.h->launches += 1;
   return D;
 }

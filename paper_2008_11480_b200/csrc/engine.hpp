@@ -72,7 +72,8 @@ MV alloc(Ctx& c, int64_t rows, int64_t cols);
 
 // D = alpha * A @ B + beta * C + diag * I  (one counted product; mv=true ticks mvm)
 void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha = 1.0,
-          const MV* C = nullptr, double beta = 0.0, double diag = 0.0, bool mv = false);
+          const MV* C = nullptr, double beta = 0.0, double diag = 0.0, bool mv = false,
+          int64_t doff = 0);
 MV gemm_new(Ctx& c, const MV& A, const MV& B, double alpha = 1.0, const MV* C = nullptr,
             double beta = 0.0, double diag = 0.0, bool mv = false);
 // I - X @ A

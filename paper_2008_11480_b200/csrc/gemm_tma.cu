@@ -13,9 +13,10 @@
 //    (16 x 128, 128B swizzle) and up to 8 B boxes (16 x 16, 128B swizzle).
 //  * 8 consumer warps (2 x 4), warp tile 64 x 32 = 8 x 4 DMMA tiles, 128 FP64
 //    accumulator registers per thread.
-//  * Bank-conflict-free fragment loads: the 4 k-lanes of each DMMA read k rows
-//    {0,1,4,5} / {2,3,6,7} (+8) of the swizzled slab, so every 256 B warp load is
-//    exactly 2 shared-memory wavefronts for both operands.  The permutation is
+//  * Bank-conflict-free fragment loads: the 4 k-lanes of each DMMA read the k
+//    rows {0,3,12,15} / {8,11,4,7} / {1,2,13,14} / {9,10,5,6} of the swizzled
+//    slab, so every 256 B warp load is exactly 2 shared-memory wavefronts for
+//    both operands (see kperm).  The permutation is
 //    fixed, so the K accumulation order is deterministic (serial == concurrent
 //    bitwise, newton_schulz.py:259-261).
 //  * Persistent grid (<= #SMs CTAs), grouped tile rasterisation for L2 reuse;
@@ -33,8 +34,13 @@ namespace {
 
 constexpr int BM = 128, BN = 128, BK = 16;
 constexpr int STAGES = 6;
-constexpr int NUM_CONSUMER_WARPS = 8;
-constexpr int THREADS = (NUM_CONSUMER_WARPS + 1) * 32;
+constexpr int NUM_CONSUMER_WARPS = 8;  // two consumer warpgroups
+// + one producer warpgroup (only one lane issues TMA).  Register budget is
+// moved with setmaxnreg: producers drop to 40, consumers rise to 232, which the
+// 128 FP64 accumulators plus two buffered fragment sets need.
+constexpr int THREADS = (NUM_CONSUMER_WARPS + 4) * 32;
+constexpr int PRODUCER_REGS = 40;
+constexpr int CONSUMER_REGS = 232;
 constexpr int A_STAGE_BYTES = BM * BK * 8;  // 16 KB
 constexpr int B_BOX_BYTES = 16 * BK * 8;    // 2 KB (16 cols x 16 rows)
 constexpr int B_STAGE_BYTES = BK * BN * 8;  // 16 KB
@@ -90,8 +96,16 @@ __device__ __forceinline__ double lds(uint32_t addr) {
 }
 
 // k index supplied by k-lane t (0..3) of k-step s (0..3) inside a 16-deep slab.
+// Shared memory serves an 8-byte warp load in two half-warp phases of 128 B;
+// with the 128B TMA swizzle (16-B chunk ^= row & 7) a phase is conflict-free
+// iff its 16 (chunk, 8-byte half) slots are distinct.  For the A fragment
+// (rows g, k = K[t]) that needs K>>1 to differ by 4 between the two k-lanes
+// that share K&1; for the B fragment (rows K[t], columns g) it needs (K&7)>>1
+// distinct over the four k-lanes.  These four k-sets satisfy both, so every
+// fragment load costs the minimum 2 wavefronts.
 __device__ __forceinline__ int kperm(int s, int t) {
-  return (s >> 1) * 8 + (s & 1) * 2 + (t >> 1) * 4 + (t & 1);
+  // = {0,3,12,15, 8,11,4,7, 1,2,13,14, 9,10,5,6}[4 s + t], computed (no local array)
+  return 8 * ((t >> 1) ^ (s & 1)) + (t >> 1) * 4 + ((s >> 1) ? 1 + (t & 1) : 3 * (t & 1));
 }
 
 __device__ __forceinline__ double apply_epi(double acc, double alpha, double beta, double cval) {
@@ -114,7 +128,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, double* __restrict__ D,
                         int64_t ldd, const double* __restrict__ C, int64_t ldc, int M, int N,
-                        int K, double alpha, double beta, double diag) {
+                        int K, double alpha, double beta, double diag, int64_t doff) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -138,9 +152,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __syncthreads();
 
-  if (warp == NUM_CONSUMER_WARPS) {
+  if (warp >= NUM_CONSUMER_WARPS) {
     // ---------------- TMA producer ----------------
-    if (lane == 0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PRODUCER_REGS));
+    if (warp == NUM_CONSUMER_WARPS && lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
       int stage = 0;
@@ -170,6 +185,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 
   // ---------------- DMMA consumers ----------------
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CONSUMER_REGS));
   const int wm = warp >> 2;  // 0..1 -> 64-row half
   const int wn = warp & 3;   // 0..3 -> 32-col quarter
   const int g = lane >> 2;   // fragment row / col group
@@ -199,28 +215,49 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+    // Fragments are double-buffered one k-step ahead: the loads of step s+1
+    // (and of the next slab's step 0) are in flight while the 32 DMMAs of step s
+    // issue, so no DMMA waits on shared-memory latency.
+    double fa[2][8], fb[2][4];
+    auto load_frags = [&](int buf, uint32_t sa, uint32_t sb, int s) {
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi) fa[buf][mi] = lds(sa + a_off[s] + mi * 1024);
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+        fb[buf][ni] = lds(sb + b_off[s][ni & 1] + (ni >> 1) * B_BOX_BYTES);
+    };
+    auto mma_step = [&](int buf) {
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+          dmma(acc[mi][ni][0], acc[mi][ni][1], fa[buf][mi], fb[buf][ni]);
+    };
+    mbar_wait(full_bar(stage), phase);
+    uint32_t sa = base + stage * STAGE_BYTES;
+    uint32_t sb = sa + A_STAGE_BYTES;
+    load_frags(0, sa, sb, 0);
     for (int kb = 0; kb < kblocks; ++kb) {
-      mbar_wait(full_bar(stage), phase);
-      const uint32_t sa = base + stage * STAGE_BYTES;
-      const uint32_t sb = sa + A_STAGE_BYTES;
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        double af[8], bf[4];
-#pragma unroll
-        for (int mi = 0; mi < 8; ++mi) af[mi] = lds(sa + a_off[s] + mi * 1024);
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) bf[ni] = lds(sb + b_off[s][ni & 1] + (ni >> 1) * B_BOX_BYTES);
-#pragma unroll
-        for (int mi = 0; mi < 8; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
-      }
+      load_frags(1, sa, sb, 1);
+      mma_step(0);
+      load_frags(0, sa, sb, 2);
+      mma_step(1);
+      load_frags(1, sa, sb, 3);
+      mma_step(0);
+      // every load of this slab has been issued: hand the stage back to TMA
       __syncwarp();
       if (lane == 0) mbar_arrive(empty_bar(stage));
       if (++stage == STAGES) {
         stage = 0;
         phase ^= 1u;
       }
+      if (kb + 1 < kblocks) {
+        mbar_wait(full_bar(stage), phase);
+        sa = base + stage * STAGE_BYTES;
+        sb = sa + A_STAGE_BYTES;
+        load_frags(0, sa, sb, 0);
+      }
+      mma_step(1);
     }
 
     // ---------------- fused epilogue ----------------
@@ -248,8 +285,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         double v0 = apply_epi(acc[mi][ni][0], alpha, beta, c0);
         double v1 = apply_epi(acc[mi][ni][1], alpha, beta, c1);
         if (diag != 0.0) {
-          if (row == col) v0 = __dadd_rn(v0, diag);
-          if (row == col + 1) v1 = __dadd_rn(v1, diag);
+          if (row + doff == col) v0 = __dadd_rn(v0, diag);
+          if (row + doff == col + 1) v1 = __dadd_rn(v1, diag);
         }
         if (two) {
           *reinterpret_cast<double2*>(D + (int64_t)row * ldd + col) = make_double2(v0, v1);
@@ -329,7 +366,7 @@ cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& 
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   gemm_f64_tma_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, D.p, D.ld, e.c, e.ldc, M, N, K,
-                                                        e.alpha, e.beta, e.diag);
+                                                        e.alpha, e.beta, e.diag, e.doff);
   return cudaGetLastError();
 }
 

@@ -33,7 +33,7 @@ constexpr int GPAD = 4;  // row padding (doubles)
 __global__ void __launch_bounds__(128) gemm_generic_kernel(
     const double* __restrict__ A, int64_t lda, const double* __restrict__ B, int64_t ldb,
     double* __restrict__ D, int64_t ldd, const double* __restrict__ C, int64_t ldc, int64_t M,
-    int64_t N, int64_t K, double alpha, double beta, double diag) {
+    int64_t N, int64_t K, double alpha, double beta, double diag, int64_t doff) {
   __shared__ double As[GB][GK + GPAD];
   __shared__ double Bs[GK][GB + GPAD];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(128) gemm_generic_kernel(
         if (col >= N) continue;
         double cv = (beta != 0.0) ? C[row * ldc + col] : 0.0;
         double v = apply_epi(acc[mi][ni][h], alpha, beta, cv);
-        if (diag != 0.0 && row == col) v = __dadd_rn(v, diag);
+        if (diag != 0.0 && row + doff == col) v = __dadd_rn(v, diag);
         D[row * ldd + col] = v;
       }
     }
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(256) gemv_kernel(const double* __restrict__ A,
                                                    double* __restrict__ D, int64_t ldd,
                                                    const double* __restrict__ C, int64_t ldc,
                                                    int64_t M, int64_t K, double alpha,
-                                                   double beta, double diag) {
+                                                   double beta, double diag, int64_t doff) {
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= M) return;
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) gemv_kernel(const double* __restrict__ A,
       if (lane == j) v = s[j];
     const double cv = (beta != 0.0) ? C[row * ldc + lane] : 0.0;
     v = apply_epi(v, alpha, beta, cv);
-    if (diag != 0.0 && row == lane) v = __dadd_rn(v, diag);
+    if (diag != 0.0 && row + doff == lane) v = __dadd_rn(v, diag);
     D[row * ldd + lane] = v;
   }
 }
@@ -137,12 +137,12 @@ struct LinArgs {
 };
 
 __global__ void lincomb_kernel(double* __restrict__ D, int64_t ldd, int64_t M, int64_t N,
-                               double cdiag, int nterms, LinArgs args) {
+                               double cdiag, int64_t doff, int nterms, LinArgs args) {
   const int64_t total = M * N;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / N, c = i % N;
-    double acc = (r == c) ? cdiag : 0.0;
+    double acc = (r + doff == c) ? cdiag : 0.0;
     for (int j = 0; j < nterms; ++j) {
       const double xv = args.x[j][r * args.ldx[j] + c];
       const double term = (args.coef[j] == 1.0) ? xv : __dmul_rn(args.coef[j], xv);
@@ -309,7 +309,7 @@ cudaError_t launch_gemm_generic(const Mat& A, const Mat& B, Mat& D, const Epilog
                                 cudaStream_t s) {
   dim3 grid((unsigned)((D.cols + GB - 1) / GB), (unsigned)((D.rows + GB - 1) / GB));
   gemm_generic_kernel<<<grid, 128, 0, s>>>(A.p, A.ld, B.p, B.ld, D.p, D.ld, e.c, e.ldc, D.rows,
-                                           D.cols, A.cols, e.alpha, e.beta, e.diag);
+                                           D.cols, A.cols, e.alpha, e.beta, e.diag, e.doff);
   return cudaGetLastError();
 }
 
@@ -318,25 +318,25 @@ cudaError_t launch_gemv(const Mat& A, const Mat& X, Mat& D, const Epilogue& e, c
   switch (D.cols) {
     case 1:
       gemv_kernel<1><<<grid, 256, 0, s>>>(A.p, A.ld, X.p, X.ld, D.p, D.ld, e.c, e.ldc, D.rows,
-                                          A.cols, e.alpha, e.beta, e.diag);
+                                          A.cols, e.alpha, e.beta, e.diag, e.doff);
       break;
     case 2:
       gemv_kernel<2><<<grid, 256, 0, s>>>(A.p, A.ld, X.p, X.ld, D.p, D.ld, e.c, e.ldc, D.rows,
-                                          A.cols, e.alpha, e.beta, e.diag);
+                                          A.cols, e.alpha, e.beta, e.diag, e.doff);
       break;
     case 3:
       gemv_kernel<3><<<grid, 256, 0, s>>>(A.p, A.ld, X.p, X.ld, D.p, D.ld, e.c, e.ldc, D.rows,
-                                          A.cols, e.alpha, e.beta, e.diag);
+                                          A.cols, e.alpha, e.beta, e.diag, e.doff);
       break;
     default:
       gemv_kernel<4><<<grid, 256, 0, s>>>(A.p, A.ld, X.p, X.ld, D.p, D.ld, e.c, e.ldc, D.rows,
-                                          A.cols, e.alpha, e.beta, e.diag);
+                                          A.cols, e.alpha, e.beta, e.diag, e.doff);
       break;
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_lincomb(Mat& D, double cdiag, int nterms, const double* coef, const Mat* X,
+cudaError_t launch_lincomb(Mat& D, double cdiag, int64_t doff, int nterms, const double* coef, const Mat* X,
                            cudaStream_t s) {
   if (nterms > kMaxLinTerms) return cudaErrorInvalidValue;
   LinArgs args{};
@@ -345,7 +345,7 @@ cudaError_t launch_lincomb(Mat& D, double cdiag, int nterms, const double* coef,
     args.ldx[i] = X[i].ld;
     args.coef[i] = coef[i];
   }
-  lincomb_kernel<<<ew_grid(D.rows * D.cols), 256, 0, s>>>(D.p, D.ld, D.rows, D.cols, cdiag, nterms,
+  lincomb_kernel<<<ew_grid(D.rows * D.cols), 256, 0, s>>>(D.p, D.ld, D.rows, D.cols, cdiag, doff, nterms,
                                                           args);
   return cudaGetLastError();
 }

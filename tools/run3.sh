@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+python tools/gemm_bench.py 1024 2048 4096 8192 16384 2>&1 | tee gpurun_out/r3_gemm_bench.txt
+timeout 600 python -m pytest tests -m gpu -x -q -k "gemm or fixtures" 2>&1 | tail -3
+python tools/profile_gemm.py 8192 3 > gpurun_out/r3_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:gemm_f64_tma -s 1 -c 1 -o gpurun_out/gemm_full_r01b python tools/profile_gemm.py 8192 3 > gpurun_out/r3_ncu_full.log 2>&1
+tail -2 gpurun_out/r3_ncu_full.log
