@@ -131,6 +131,19 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def ncu_traffic(w) -> float | None:
+    """DRAM bytes per launch of the dominant kernel at this workload's n, from the
+    committed ncu --set full capture (profiles/ncu_traffic.json), else None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            data = json.load(fh)
+        rec = data.get("gemm_f64_tma_kernel", {}).get(str(w.n))
+        return float(rec["dram_bytes_per_launch"]) if rec else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -144,9 +157,11 @@ def host_cores() -> int:
 class Workload:
     """One config: device state + one step function + algorithmic FLOPs per step."""
 
-    def __init__(self, cfg: str, n: int | None):
+    def __init__(self, cfg: str, n: int | None, world: int = 1):
         self.cfg = cfg
         self.n = n
+        self.world = world
+        self.sharded = None
 
     # FLOPs of the executed reference DAG per step (2 M N K summed)
     def flops(self) -> float:
@@ -211,6 +226,27 @@ class Workload:
         self.a = a
         self.b = b
         self.sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False, verify=False)
+        self.sharded = None
+        if self.world > 1 and cfg in ("c4", "c3"):
+            # block-row sharding over the ranks (sharded.py): A, S^-1, B replicated,
+            # G / F row blocks, one NCCL all-gather per product with a sharded right operand
+            from paper_2008_11480_b200.sharded import RowComm, ShardedEngine
+
+            comm = RowComm(self.n)
+            eng = ShardedEngine(comm)
+            st = P.initial_series(self.sp, 0, 1, order={"c4": 2, "c3": 8}[cfg])
+            self.sharded = {
+                "eng": eng, "comm": comm,
+                "A": eng.replicated(self.sp.matrix), "P": eng.replicated(self.sp.precond),
+                "B": eng.replicated(self.sp.residual), "b": eng.replicated(b),
+                "g": eng.local(st.estimate[comm.r0:comm.r1].clone()),
+                "f": eng.local(st.residual[comm.r0:comm.r1].clone()),
+                "theta": eng.replicated(torch.zeros_like(b)),
+            }
+            del st
+            self.spec = P.CompositeSpec((2, 3, 4, 5))
+            self.plan8 = P.table_plans()[8][0]
+            return
         if cfg == "c5":
             self.st = P.initial_richardson(self.sp, b, 0, 1, order=16, q=16)
             self.plan16 = P.plan_order(16)
@@ -234,6 +270,16 @@ class Workload:
         if cfg == "c5":
             self.st = P.richardson_recursive_step(self.st, self.sp.matrix, self.b,
                                                   factor_plan=self.plan16, doubling_sum=True)
+            return
+        if self.sharded is not None:
+            s = self.sharded
+            eng = s["eng"]
+            s["theta"] = eng.plain_richardson(s["theta"], s["g"], s["A"], s["b"])
+            if cfg == "c4":
+                s["g"], s["f"] = eng.composite_step(s["g"], s["f"], s["A"], s["P"], s["B"],
+                                                    (2, 3, 4, 5), 2)
+            else:
+                s["g"], s["f"] = eng.ns_step(s["g"], s["f"], s["A"], 8, plan=self.plan8)
             return
         self.theta = P.plain_richardson(self.theta, self.st.estimate, self.sp.matrix, self.b, self.st.ctr)
         if cfg == "c4":
@@ -358,7 +404,7 @@ def run_ours(args):
     world, rank, local = dist_setup(args)
     from paper_2008_11480_b200 import _lib
 
-    w = Workload(args.config, args.n)
+    w = Workload(args.config, args.n, world)
     w.setup()
     flops = w.flops()
     h = _lib.handle()
@@ -390,15 +436,20 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     ms_max = max_over_ranks(ms, world)
     step_s = ms_max / 1e3 / args.steps
-    value = world * args.steps / (ms_max / 1e3)
-    tflops = flops / step_s / 1e12
+    # sharded (c3/c4 at N > 1): every rank works on the same job -> strong scaling;
+    # otherwise N independent replicas each complete `steps` iterations -> weak
+    strong = w.sharded is not None
+    value = (1 if strong else world) * args.steps / (ms_max / 1e3)
+    tflops = (1 if strong else world) * flops / step_s / 1e12
+    if strong:
+        flops = flops / world  # per-rank share, for the per-GPU fraction below
 
     peak = ctypes.c_double()
     _lib.call("si_dmma_peak", h, 20000, ctypes.byref(peak))
     achieved = (g_fl.value / (g_ms.value / 1e3) / 1e12) if g_ms.value > 0 else None
 
     e2e = None
-    if not args.no_e2e and args.config in ("c4", "c3", "c1"):
+    if not args.no_e2e and args.config in ("c4", "c3", "c1") and w.sharded is None:
         host = w.pinned_inputs()
         h2d = d2h = 0
         ksteps = max(1, min(args.steps, 3))
@@ -427,16 +478,18 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded PCG64 draws, SURVEY Appendix A recipe)",
             "config": {"workload": w.workload, "n": w.n,
-                       "parallelism": "replicas" if world > 1 else "single-gpu",
+                       "parallelism": (f"block-row x{world} (NCCL all-gather)" if strong
+                                       else (f"replicas x{world}" if world > 1 else "single-gpu")),
                        "l2": "inputs larger than L2 (2.1 GB per matrix), no flush"},
             "tflops": tflops,
-            "tflops_frac_of_dmma_peak": tflops / peak.value,
+            "tflops_frac_of_dmma_peak": tflops / (world * peak.value),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak.value,
                          "unit": "TFLOP/s", "frac": (achieved / peak.value) if achieved else None,
-                         "traffic": None, "kernel": "gemm_f64_tma_kernel",
+                         "traffic": ncu_traffic(w), "kernel": "gemm_f64_tma_kernel",
                          "launches": g_n.value,
                          "peak_source": "measured live: DMMA m8n8k4 register-only probe (si_dmma_peak); MEASURED_PEAKS.json has no FP64 entry"},
             "e2e": e2e,

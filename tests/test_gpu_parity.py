@@ -174,6 +174,32 @@ def test_concurrent_bitwise_at_size():
     assert s1.ctr.mmm == s2.ctr.mmm == 22
 
 
+def test_sharded_engine_single_rank_bitwise_equals_native():
+    """The block-row engine at world size 1 runs the same kernels on the same operands as
+    the native composite step: results must be bitwise identical, counters equal."""
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import configs
+    from paper_2008_11480_b200.sharded import RowComm, ShardedEngine
+
+    a, b = configs.c4_householder(n=512, rhs=8)
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False)
+    st = P.initial_series(sp, 0, 1, order=2)
+    bd = P.as_device(b)
+    theta = torch.zeros_like(bd)
+    eng = ShardedEngine(RowComm(512))
+    g, f = eng.local(st.estimate.clone()), eng.local(st.residual.clone())
+    th = eng.replicated(theta.clone())
+    A, Pc, B, bv = (eng.replicated(x) for x in (sp.matrix, sp.precond, sp.residual, bd))
+    for _ in range(2):
+        theta = P.plain_richardson(theta, st.estimate, sp.matrix, bd, st.ctr)
+        st = P.composite_step(st, sp.matrix, sp, P.CompositeSpec((2, 3, 4, 5)), 2)
+        th = eng.plain_richardson(th, g, A, bv)
+        g, f = eng.composite_step(g, f, A, Pc, B, (2, 3, 4, 5), 2)
+    assert torch.equal(g.t, st.estimate) and torch.equal(f.t, st.residual)
+    assert torch.equal(th.t, theta)
+    assert (eng.ctr.mmm, eng.ctr.mvm) == (st.ctr.mmm - 0, st.ctr.mvm)
+
+
 # ---------------------------------------------------------------- batched (config 2)
 
 

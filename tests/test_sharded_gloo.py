@@ -1,0 +1,134 @@
+"""Multi-rank block-row sharded steps on CPU: world_size 2 over gloo.
+
+The orchestration (row splits, all-gathers of sharded right operands, shifted
+diagonals, the composite fold) is the product code in
+paper_2008_11480_b200/sharded.py; only the local-ops layer is swapped for a
+CPU torch implementation here.  Results are compared with the oracle on the
+same inputs, and the GEMM count with the reference DAG.
+"""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+
+class CpuOps:
+    """Test-only local ops (CPU float64 torch)."""
+
+    def gemm(self, a, b, alpha, c, beta, diag, doff, is_mv, ctr):
+        out = alpha * (a @ b)
+        if c is not None:
+            out = out + beta * c
+        if diag:
+            rows = torch.arange(out.shape[0])
+            cols = rows + doff
+            ok = cols < out.shape[1]
+            out[rows[ok], cols[ok]] += diag
+        if is_mv:
+            ctr.mvm += 1
+        else:
+            ctr.mmm += 1
+        return out
+
+    def lin(self, cdiag, doff, terms, rows, cols, like):
+        out = torch.zeros((rows, cols), dtype=torch.float64)
+        if cdiag:
+            r = torch.arange(rows)
+            ok = r + doff < cols
+            out[r[ok], (r + doff)[ok]] = cdiag
+        for coef, t in terms:
+            out = out + coef * t
+        return out
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, outdir, n, steps):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from paper_2008_11480_b200 import configs
+    from paper_2008_11480_b200.sharded import RowComm, ShardedEngine
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    a_np, b_np = configs.c4_householder(n=n, rhs=3)
+    alpha = np.max(np.sum(np.abs(a_np), axis=1))
+    comm = RowComm(n)
+    eng = ShardedEngine(comm, ops=CpuOps())
+    A = eng.replicated(torch.as_tensor(a_np))
+    P = eng.replicated(torch.eye(n, dtype=torch.float64) / alpha)
+    B = eng.replicated(torch.eye(n, dtype=torch.float64) - torch.as_tensor(a_np) / alpha)
+    b = eng.replicated(torch.as_tensor(b_np))
+    g = eng.local(P.t[comm.r0:comm.r1].clone())
+    f = eng.local(B.t[comm.r0:comm.r1].clone())
+    theta = eng.replicated(torch.zeros_like(b.t))
+    for _ in range(steps):
+        theta = eng.plain_richardson(theta, g, A, b)
+        g, f = eng.composite_step(g, f, A, P, B, (2, 3, 4, 5), 2)
+    g_full = comm.all_gather_rows(g.t)
+    h_full = eng.ns_step(g, f, A, 8, plan=None)[0]
+    h_full = comm.all_gather_rows(h_full.t)
+    if rank == 0:
+        np.save(os.path.join(outdir, "g.npy"), g_full.numpy())
+        np.save(os.path.join(outdir, "theta.npy"), theta.t.numpy())
+        np.save(os.path.join(outdir, "h.npy"), h_full.numpy())
+        np.save(os.path.join(outdir, "ctr.npy"), np.array([eng.ctr.mmm, eng.ctr.mvm]))
+        np.save(os.path.join(outdir, "gathered.npy"), np.array([comm.bytes_gathered]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 41), (3, 24)])
+def test_sharded_composite_matches_oracle(world, n):
+    from oracle import seriesinv_oracle as O
+    from paper_2008_11480_b200 import configs
+
+    steps = 2
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(world, _free_port(), d, n, steps), nprocs=world, join=True)
+        g = np.load(os.path.join(d, "g.npy"))
+        theta = np.load(os.path.join(d, "theta.npy"))
+        h = np.load(os.path.join(d, "h.npy"))
+        ctr = np.load(os.path.join(d, "ctr.npy"))
+        gathered = int(np.load(os.path.join(d, "gathered.npy"))[0])
+    a, b = configs.c4_householder(n=n, rhs=3)
+    sp = O.split_scalar(a, O.inf_norm(a) / 2.0)
+    st = O.initial_series(sp, 0, 1, 2)
+    th = np.zeros_like(b)
+    for _ in range(steps):
+        th = O.plain_richardson(th, st.estimate, sp.matrix, b, st.ctr)
+        st = O.composite_step(st, sp.matrix, sp, (2, 3, 4, 5), 2)
+    mmm_ref, mvm_ref = st.ctr.mmm, st.ctr.mvm
+    # ns_step with order 8 on the final state (Horner)
+    st8 = O.NS(st.estimate, st.residual, st.step, 8, 1, O.Counter())
+    h_ref = O.ns_step(st8, sp.matrix).estimate
+    rel = lambda x, y: np.linalg.norm(x - y) / np.linalg.norm(y)  # noqa: E731
+    assert rel(g, st.estimate) <= 1e-11
+    assert rel(theta, th) <= 1e-11
+    assert rel(h, h_ref) <= 1e-11
+    # same DAG as the reference: 22 products + 2 per composite step, then 8 for ns_step(8)
+    assert int(ctr[0]) == mmm_ref + 8 and int(ctr[1]) == mvm_ref
+    assert gathered > 0
+
+
+def test_row_splits_cover():
+    from paper_2008_11480_b200.sharded import row_splits
+
+    for n in (1, 7, 64, 1000):
+        for w in (1, 2, 3, 8):
+            s = row_splits(n, w)
+            assert s[0][0] == 0 and s[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(s, s[1:]))
+            assert max(r1 - r0 for r0, r1 in s) - min(r1 - r0 for r0, r1 in s) <= 1
