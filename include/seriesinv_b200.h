@@ -33,6 +33,7 @@
 #ifndef SERIESINV_B200_H
 #define SERIESINV_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -56,6 +57,13 @@ SI_API int si_version(void);
 SI_API const char* si_last_error(void);
 SI_API int si_create(int device, si_handle* out);
 SI_API int si_destroy(si_handle h);
+/* Route the library's temporaries through a caller allocator (e.g. the host
+ * framework's caching allocator) instead of the handle's stream-ordered pool.
+ * alloc_fn(ctx, bytes, stream) returns device memory usable in `stream` order
+ * (NULL on failure); free_fn(ctx, ptr, stream) releases it in `stream` order.
+ * Pass NULL, NULL to restore the internal pool. */
+SI_API int si_set_allocator(si_handle h, void* (*alloc_fn)(void* ctx, size_t bytes, void* stream),
+                            void (*free_fn)(void* ctx, void* ptr, void* stream), void* ctx);
 /* Release cached pool memory back to the device. */
 SI_API int si_trim(si_handle h);
 
@@ -203,7 +211,7 @@ SI_API int si_dmma_peak(si_handle h, int iters, double* tflops);
 /* ---------------- batched small systems (BASELINE config 2) ---------------- */
 
 /* `iters` x { plain Richardson with P_k; composite_step(rates, order_n) } for
- * `batch` independent n x n systems (n <= 32), everything resident on chip.
+ * `batch` independent n x n systems (n <= 64), everything resident on chip.
  * A, P (in/out), F (in/out): batch x n x n; b, theta (in/out): batch x n.
  * precond/residual: batch x n x n splitting of each A; plans as in
  * si_composite_step.  Counters are per system (identical for all systems). */
@@ -212,6 +220,16 @@ SI_API int si_batched_composite_richardson(si_handle h, int64_t batch, int64_t n
                                     const double* residual, int nrates, const int32_t* rates,
                                     const int32_t* plans, const int64_t* plan_offsets,
                                     const double* consts, int64_t nconsts, int order_n,
+                                    int iters, double* p_io, double* f_io, double* theta_io,
+                                    int64_t* counters, void* stream);
+
+/* BASELINE config 1 shape (batch = 1, n <= 64) and batches of it: `iters` x
+ * { plain Richardson with P_k; ns_step(order, plan) } with the state resident
+ * in shared memory (one launch for the whole run).  A: batch x n x n; P, F
+ * (in/out): batch x n x n; b, theta (in/out): batch x n; plan may be NULL. */
+SI_API int si_batched_ns_richardson(si_handle h, int64_t batch, int64_t n, const double* a,
+                                    const double* b, int order, const int32_t* plan,
+                                    int64_t plan_len, const double* consts, int64_t nconsts,
                                     int iters, double* p_io, double* f_io, double* theta_io,
                                     int64_t* counters, void* stream);
 

@@ -30,6 +30,7 @@ SIGNATURES: dict[str, list] = {
     "si_create": [_I, POINTER(c_void_p)],
     "si_destroy": [_P],
     "si_trim": [_P],
+    "si_set_allocator": [_P, _P, _P, _P],
     "si_gemm": [_P, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _D, _P, _I64, _I, _PI64, _P],
     "si_gemm_ex": [_P, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _D, _I64, _P, _I64, _I, _PI64, _P],
     "si_lincomb": [_P, _I64, _I64, _D, _I, _P, _P, _P, _P, _I64, _P],
@@ -59,6 +60,7 @@ SIGNATURES: dict[str, list] = {
     "si_profile_begin": [_P],
     "si_profile_end": [_P, POINTER(c_double), POINTER(c_double), _PI64, _PI64],
     "si_dmma_peak": [_P, _I, POINTER(c_double)],
+    "si_batched_ns_richardson": [_P, _I64, _I64, _P, _P, _I, _P, _I64, _P, _I64, _I, _P, _P, _P, _PI64, _P],
     "si_batched_composite_richardson": [
         _P, _I64, _I64, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _PI64, _P,
     ],
@@ -105,8 +107,31 @@ def _raise(status: int, name: str):
     raise RuntimeError(f"{name} failed ({status}): {msg}")
 
 
+_ALLOC_FN = ctypes.CFUNCTYPE(c_void_p, c_void_p, ctypes.c_size_t, c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, c_void_p, c_void_p, c_void_p)
+
+
+def _torch_alloc(ctx, nbytes, stream):
+    try:
+        return torch.cuda.caching_allocator_alloc(int(nbytes), device=int(ctx or 0),
+                                                  stream=int(stream or 0))
+    except Exception:  # noqa: BLE001 -- reported to C as NULL (SI_ENOMEM)
+        return None
+
+
+def _torch_free(ctx, ptr, stream):
+    torch.cuda.caching_allocator_delete(int(ptr))
+
+
+# kept alive for the lifetime of the process (C holds the raw pointers)
+_ALLOC_CB = _ALLOC_FN(_torch_alloc)
+_FREE_CB = _FREE_FN(_torch_free)
+
+
 def handle(device: int | None = None) -> int:
-    """Per-device library handle (workspace pool, side streams, events)."""
+    """Per-device library handle (side streams, events); the library's
+    temporaries are allocated from PyTorch's caching allocator so one allocator
+    owns all device memory."""
     if not torch.cuda.is_available():
         raise NativeUnavailable("no CUDA device visible: the seriesinv B200 path has no CPU fallback")
     lib = load_library()
@@ -118,6 +143,10 @@ def handle(device: int | None = None) -> int:
         if st != SI_OK:
             _raise(st, "si_create")
         h = out.value
+        st = lib.si_set_allocator(h, ctypes.cast(_ALLOC_CB, c_void_p),
+                                  ctypes.cast(_FREE_CB, c_void_p), c_void_p(dev))
+        if st != SI_OK:
+            _raise(st, "si_set_allocator")
         _handles[dev] = h
     return h
 

@@ -16,7 +16,7 @@ from . import _lib
 from .matrix_core import MulCounter, as_device
 from .series_toolkit import encode_many, geometric_base_plan
 
-__all__ = ["batched_composite_richardson", "batched_scalar_split"]
+__all__ = ["batched_composite_richardson", "batched_ns_richardson", "batched_scalar_split"]
 
 
 def batched_scalar_split(a: torch.Tensor, eps_factor: float = 0.5):
@@ -61,4 +61,40 @@ def batched_composite_richardson(a, b, precond, residual, p, f, theta, rates, or
               th_io.data_ptr(), buf, _lib.stream_ptr(a.device))
     if ctr is not None:
         ctr.absorb(buf)
+    return p_io, f_io, th_io
+
+
+def batched_ns_richardson(a, b, p, f, theta, order: int, iters: int, plan=None,
+                          ctr: MulCounter | None = None):
+    """``iters`` x { plain Richardson with P_k; ns_step(order, plan) } for a batch of
+    n x n systems (n <= 64) in one launch; BASELINE config 1 is batch = 1, n = 64,
+    order 3.  Returns new (P, F, theta); inputs untouched."""
+    from .series_toolkit import encode_plan
+
+    a, b = as_device(a), as_device(b)
+    squeeze = a.ndim == 2
+    if squeeze:
+        a, b = a[None], b.reshape(1, -1)
+    batch, n, n2 = a.shape
+    if n != n2 or n > 64:
+        raise ValueError("batched path expects batch x n x n with n <= 64")
+    if b.shape != (batch, n):
+        raise ValueError("dimension mismatch")
+    if order < 1:
+        raise ValueError("order must be >= 1")
+    if plan is not None and plan.order_h != order:
+        raise ValueError(f"plan order {plan.order_h} != iteration order {order}")
+    p_io = as_device(p).reshape(batch, n, n).clone()
+    f_io = as_device(f).reshape(batch, n, n).clone()
+    th_io = as_device(theta).reshape(batch, n).clone()
+    code, consts = encode_plan(plan) if plan is not None else ([], [])
+    buf = _lib.counter_buf()
+    _lib.call("si_batched_ns_richardson", _lib.handle(a.device.index), batch, n, a.data_ptr(),
+              b.contiguous().data_ptr(), order, _lib.i32_array(code) if code else None, len(code),
+              _lib.f64_array(consts) if consts else None, len(consts), iters, p_io.data_ptr(),
+              f_io.data_ptr(), th_io.data_ptr(), buf, _lib.stream_ptr(a.device))
+    if ctr is not None:
+        ctr.absorb(buf)
+    if squeeze:
+        return p_io[0], f_io[0], th_io[0]
     return p_io, f_io, th_io

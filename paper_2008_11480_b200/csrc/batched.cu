@@ -1,32 +1,27 @@
-// Batched small systems (BASELINE config 2): thousands of independent n <= 32
-// SPD systems, each advanced by `iters` x { plain Richardson update (SURVEY
-// a12, ordered as richardson.py:88-89), composite_step (newton_schulz.py:
-// 177-228) }.
+// Resident small systems: BASELINE config 2 (16384 independent 32 x 32
+// systems, composite step + plain Richardson) and config 1 (one 64 x 64
+// system, Newton-Schulz step + plain Richardson).
 //
-// The per-iteration GEMM DAG is recorded once on the host by the same
-// evaluator structure as the dense engine (series_toolkit.py:263-457 over the
-// decoded plans), register-allocated onto shared-memory matrix slots, and then
-// interpreted by one CTA per system: every matrix stays resident in shared
-// memory for all iterations, products run on DMMA (m8n8k4), and HBM is touched
-// once per system on entry (coalesced double2 loads) and once on exit.
+// One iteration of the reference GEMM DAG (series_toolkit.py:263-457 over the
+// decoded plans, newton_schulz.py:150-228, plain Richardson as
+// richardson.py:88-89) is recorded once on the host, register-allocated onto
+// shared-memory matrix slots, and interpreted by one CTA per system for all
+// `iters` iterations: the state never leaves shared memory, products run on
+// DMMA (m8n8k4), and HBM is touched once per system on entry (coalesced
+// double2 loads) and once on exit.  Per system this executes exactly the
+// reference's products, so MulCounter deltas match tick for tick.
 #include <algorithm>
-#include <map>
 
 #include "batched.hpp"
 
 namespace si {
 namespace {
 
-constexpr int NPAD = 32;   // systems are zero-padded to 32 x 32
-constexpr int LDS = 36;    // shared row stride (doubles): conflict-free fragments
-constexpr int MSLOT = NPAD * LDS;
-constexpr int BTHREADS = 128;
-
 enum : int8_t { OP_GEMM = 0, OP_GEMV = 1, OP_LIN = 2 };
 
 struct BOp {
   int8_t kind;
-  int8_t vec;     // lin over vectors
+  int8_t vec;  // lin over vectors
   int8_t nterms;
   int8_t pad_;
   int16_t dst, a, b, c;
@@ -34,6 +29,7 @@ struct BOp {
   int16_t t[kMaxLinTerms];
   double coef[kMaxLinTerms];
 };
+constexpr int kMaxOps = 96;
 
 // ------------------------------------------------------------------ recorder
 struct Rec {
@@ -151,13 +147,14 @@ struct Rec {
   }
 };
 
-// Linear-scan assignment of virtual registers to physical slots.
+// Linear-scan assignment of virtual registers to physical slots; pinned
+// registers (inputs and the carried results) keep their slots for the run.
 struct Alloc {
   std::vector<int16_t> phys;
   int nmat = 0, nvec = 0;
 };
 
-Alloc assign(const Rec& r, const std::vector<int>& pinned, int nops_iter) {
+Alloc assign(const Rec& r, const std::vector<int>& pinned) {
   const int nv = (int)r.is_vec.size();
   std::vector<int> last(nv, -1);
   auto use = [&](int v, int i) {
@@ -172,7 +169,6 @@ Alloc assign(const Rec& r, const std::vector<int>& pinned, int nops_iter) {
       for (int j = 0; j < o.nterms; ++j) use(o.t[j], i);
   }
   for (int p : pinned) last[p] = INT32_MAX;
-  (void)nops_iter;
   Alloc al;
   al.phys.assign(nv, -1);
   std::vector<int> free_m, free_v;
@@ -192,7 +188,7 @@ Alloc assign(const Rec& r, const std::vector<int>& pinned, int nops_iter) {
     auto release = [&](int v) {
       if (v >= 0 && last[v] == i && al.phys[v] >= 0) {
         (r.is_vec[v] ? free_v : free_m).push_back(al.phys[v]);
-        last[v] = -2;  // released once
+        last[v] = -2;
       }
     };
     release(o.a);
@@ -200,9 +196,7 @@ Alloc assign(const Rec& r, const std::vector<int>& pinned, int nops_iter) {
     release(o.c);
     if (o.kind == OP_LIN)
       for (int j = 0; j < o.nterms; ++j) release(o.t[j]);
-    if (last[o.dst] == -1) {  // never read: free immediately
-      (r.is_vec[o.dst] ? free_v : free_m).push_back(al.phys[o.dst]);
-    }
+    if (last[o.dst] == -1) (r.is_vec[o.dst] ? free_v : free_m).push_back(al.phys[o.dst]);
   }
   return al;
 }
@@ -233,144 +227,170 @@ struct BatchArgs {
   int n;
   int iters;
   int64_t batch;
-  // slots of the pinned registers
-  int sA, sP, sB, sG, sF, sT, sb;
-  // per-iteration result slots copied back into sG/sF/sT
-  int rG, rF, rT;
+  int sA, sP, sB, sG, sF, sT, sb;  // pinned slots (sP/sB < 0 when unused)
+  int rG, rF, rT;                  // per-iteration results carried into sG/sF/sT
 };
 
-__device__ __forceinline__ double* mslot(double* sm, int s) { return sm + (size_t)s * MSLOT; }
-__device__ __forceinline__ double* vslot(double* sm, int nmat, int s) {
-  return sm + (size_t)nmat * MSLOT + (size_t)s * NPAD;
-}
+// NP: padded order (32 or 64); the row stride NP+4 doubles makes every DMMA
+// fragment load conflict-free (row starts advance 8 banks).
+template <int NP>
+struct Geo {
+  static constexpr int LD = NP + 4;
+  static constexpr int SLOT = NP * LD;
+  static constexpr int WARPS = NP == 32 ? 4 : 8;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int WROWS = NP / (WARPS / 2);  // warp tile rows (16)
+  static constexpr int WCOLS = NP / 2;             // warp tile cols (16 or 32)
+  static constexpr int MT = WROWS / 8, NT = WCOLS / 8;
+};
 
+template <int NP>
 __device__ void load_mat(double* dst, const double* src, int n) {
-  if (n == NPAD) {
+  using G = Geo<NP>;
+  if (n == NP) {
     const double2* s2 = reinterpret_cast<const double2*>(src);
-    for (int i = threadIdx.x; i < NPAD * NPAD / 2; i += BTHREADS) {
+    for (int i = threadIdx.x; i < NP * NP / 2; i += G::THREADS) {
       const double2 v = __ldg(s2 + i);
-      const int r = (2 * i) / NPAD, c = (2 * i) % NPAD;
-      dst[r * LDS + c] = v.x;
-      dst[r * LDS + c + 1] = v.y;
+      const int r = (2 * i) / NP, c = (2 * i) % NP;
+      dst[r * G::LD + c] = v.x;
+      dst[r * G::LD + c + 1] = v.y;
     }
   } else {
-    for (int i = threadIdx.x; i < NPAD * NPAD; i += BTHREADS) {
-      const int r = i / NPAD, c = i % NPAD;
-      dst[r * LDS + c] = (r < n && c < n) ? src[r * n + c] : 0.0;
+    for (int i = threadIdx.x; i < NP * NP; i += G::THREADS) {
+      const int r = i / NP, c = i % NP;
+      dst[r * G::LD + c] = (r < n && c < n) ? src[r * n + c] : 0.0;
     }
-  }
-}
-__device__ void store_mat(double* dst, const double* src, int n) {
-  if (n == NPAD) {
-    double2* d2 = reinterpret_cast<double2*>(dst);
-    for (int i = threadIdx.x; i < NPAD * NPAD / 2; i += BTHREADS) {
-      const int r = (2 * i) / NPAD, c = (2 * i) % NPAD;
-      d2[i] = make_double2(src[r * LDS + c], src[r * LDS + c + 1]);
-    }
-  } else {
-    for (int i = threadIdx.x; i < n * n; i += BTHREADS) dst[i] = src[(i / n) * LDS + (i % n)];
   }
 }
 
-__global__ void __launch_bounds__(BTHREADS) batched_kernel(BatchArgs p) {
+template <int NP>
+__device__ void store_mat(double* dst, const double* src, int n) {
+  using G = Geo<NP>;
+  if (n == NP) {
+    double2* d2 = reinterpret_cast<double2*>(dst);
+    for (int i = threadIdx.x; i < NP * NP / 2; i += G::THREADS) {
+      const int r = (2 * i) / NP, c = (2 * i) % NP;
+      d2[i] = make_double2(src[r * G::LD + c], src[r * G::LD + c + 1]);
+    }
+  } else {
+    for (int i = threadIdx.x; i < n * n; i += G::THREADS) dst[i] = src[(i / n) * G::LD + (i % n)];
+  }
+}
+
+template <int NP>
+__global__ void __launch_bounds__(Geo<NP>::THREADS) resident_kernel(BatchArgs p) {
+  using G = Geo<NP>;
   extern __shared__ double sm[];
+  __shared__ BOp prog[kMaxOps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int n = p.n;
   const int64_t nn = (int64_t)n * n;
+  auto mslot = [&](int s) { return sm + (size_t)s * G::SLOT; };
+  auto vslot = [&](int s) { return sm + (size_t)p.nmat * G::SLOT + (size_t)s * NP; };
+  // the program is read by every thread for every op: stage it in shared memory
+  for (int i = threadIdx.x; i < p.nops * (int)sizeof(BOp) / 4; i += G::THREADS)
+    reinterpret_cast<int*>(prog)[i] = reinterpret_cast<const int*>(p.ops)[i];
+  __syncthreads();
+
   for (int64_t sys = blockIdx.x; sys < p.batch; sys += gridDim.x) {
-    load_mat(mslot(sm, p.sA), p.a + sys * nn, n);
-    load_mat(mslot(sm, p.sP), p.precond + sys * nn, n);
-    load_mat(mslot(sm, p.sB), p.residual + sys * nn, n);
-    load_mat(mslot(sm, p.sG), p.p_io + sys * nn, n);
-    load_mat(mslot(sm, p.sF), p.f_io + sys * nn, n);
-    if (threadIdx.x < NPAD) {
-      vslot(sm, p.nmat, p.sT)[threadIdx.x] = threadIdx.x < n ? p.theta_io[sys * n + threadIdx.x] : 0.0;
-      vslot(sm, p.nmat, p.sb)[threadIdx.x] = threadIdx.x < n ? p.b[sys * n + threadIdx.x] : 0.0;
+    load_mat<NP>(mslot(p.sA), p.a + sys * nn, n);
+    if (p.sP >= 0) load_mat<NP>(mslot(p.sP), p.precond + sys * nn, n);
+    if (p.sB >= 0) load_mat<NP>(mslot(p.sB), p.residual + sys * nn, n);
+    load_mat<NP>(mslot(p.sG), p.p_io + sys * nn, n);
+    load_mat<NP>(mslot(p.sF), p.f_io + sys * nn, n);
+    if (threadIdx.x < NP) {
+      vslot(p.sT)[threadIdx.x] = threadIdx.x < n ? p.theta_io[sys * n + threadIdx.x] : 0.0;
+      vslot(p.sb)[threadIdx.x] = threadIdx.x < n ? p.b[sys * n + threadIdx.x] : 0.0;
     }
     __syncthreads();
     for (int it = 0; it < p.iters; ++it) {
       for (int k = 0; k < p.nops; ++k) {
-        const BOp& o = p.ops[k];
+        const BOp& o = prog[k];
         if (o.kind == OP_GEMM) {
-          const double* A = mslot(sm, o.a);
-          const double* B = mslot(sm, o.b);
-          const double* C = o.c >= 0 ? mslot(sm, o.c) : nullptr;
-          double* D = mslot(sm, o.dst);
-          const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 16;
-          double acc[2][2][2] = {};
+          const double* A = mslot(o.a);
+          const double* B = mslot(o.b);
+          const double* C = o.c >= 0 ? mslot(o.c) : nullptr;
+          double* D = mslot(o.dst);
+          const int r0 = (warp >> 1) * G::WROWS, c0 = (warp & 1) * G::WCOLS;
+          double acc[G::MT][G::NT][2] = {};
 #pragma unroll
-          for (int kk = 0; kk < NPAD; kk += 4) {
-            double af[2], bf[2];
+          for (int kk = 0; kk < NP; kk += 4) {
+            double af[G::MT], bf[G::NT];
 #pragma unroll
-            for (int mi = 0; mi < 2; ++mi) af[mi] = A[(r0 + mi * 8 + g) * LDS + kk + t];
+            for (int mi = 0; mi < G::MT; ++mi) af[mi] = A[(r0 + mi * 8 + g) * G::LD + kk + t];
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) bf[ni] = B[(kk + t) * LDS + c0 + ni * 8 + g];
+            for (int ni = 0; ni < G::NT; ++ni) bf[ni] = B[(kk + t) * G::LD + c0 + ni * 8 + g];
 #pragma unroll
-            for (int mi = 0; mi < 2; ++mi)
+            for (int mi = 0; mi < G::MT; ++mi)
 #pragma unroll
-              for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+              for (int ni = 0; ni < G::NT; ++ni)
+                dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
           }
 #pragma unroll
-          for (int mi = 0; mi < 2; ++mi)
+          for (int mi = 0; mi < G::MT; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni)
+            for (int ni = 0; ni < G::NT; ++ni)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int row = r0 + mi * 8 + g, col = c0 + ni * 8 + 2 * t + h;
-                double v = epi(acc[mi][ni][h], o.alpha, o.beta, C ? C[row * LDS + col] : 0.0);
+                double v = epi(acc[mi][ni][h], o.alpha, o.beta, C ? C[row * G::LD + col] : 0.0);
                 if (o.diag != 0.0 && row == col && row < n) v = __dadd_rn(v, o.diag);
-                D[row * LDS + col] = v;
+                D[row * G::LD + col] = v;
               }
         } else if (o.kind == OP_GEMV) {
-          if (warp == 0) {
-            const double* A = mslot(sm, o.a);
-            const double* x = vslot(sm, p.nmat, o.b);
+          // every warp takes NP / WARPS rows; lanes split k, fixed-order shuffle sum
+          const double* A = mslot(o.a);
+          const double* x = vslot(o.b);
+          constexpr int RPW = NP / G::WARPS;
+#pragma unroll
+          for (int rr = 0; rr < RPW; ++rr) {
+            const int row = warp * RPW + rr;
             double s = 0.0;
-            for (int j = 0; j < NPAD; ++j) {
-              const int k2 = (j + lane) & (NPAD - 1);  // rotated: conflict-free
-              s = fma(A[lane * LDS + k2], x[k2], s);
+#pragma unroll
+            for (int kk = lane; kk < NP; kk += 32) s = fma(A[row * G::LD + kk], x[kk], s);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            if (lane == 0) {
+              const double cv = o.c >= 0 ? vslot(o.c)[row] : 0.0;
+              vslot(o.dst)[row] = epi(s, o.alpha, o.beta, cv);
             }
-            const double cv = o.c >= 0 ? vslot(sm, p.nmat, o.c)[lane] : 0.0;
-            vslot(sm, p.nmat, o.dst)[lane] = epi(s, o.alpha, o.beta, cv);
+          }
+        } else if (o.vec) {
+          if (threadIdx.x < NP) {
+            double acc = 0.0;
+            for (int j = 0; j < o.nterms; ++j) {
+              const double xv = vslot(o.t[j])[threadIdx.x];
+              acc = __dadd_rn(acc, o.coef[j] == 1.0 ? xv : __dmul_rn(o.coef[j], xv));
+            }
+            vslot(o.dst)[threadIdx.x] = acc;
           }
         } else {
-          if (o.vec) {
-            if (threadIdx.x < NPAD) {
-              double acc = 0.0;
-              for (int j = 0; j < o.nterms; ++j) {
-                const double xv = vslot(sm, p.nmat, o.t[j])[threadIdx.x];
-                acc = __dadd_rn(acc, o.coef[j] == 1.0 ? xv : __dmul_rn(o.coef[j], xv));
-              }
-              vslot(sm, p.nmat, o.dst)[threadIdx.x] = acc;
+          double* D = mslot(o.dst);
+          for (int i = threadIdx.x; i < NP * NP; i += G::THREADS) {
+            const int r = i / NP, c = i % NP;
+            double acc = (r == c && r < n) ? o.diag : 0.0;
+            for (int j = 0; j < o.nterms; ++j) {
+              const double xv = mslot(o.t[j])[r * G::LD + c];
+              acc = __dadd_rn(acc, o.coef[j] == 1.0 ? xv : __dmul_rn(o.coef[j], xv));
             }
-          } else {
-            double* D = mslot(sm, o.dst);
-            for (int i = threadIdx.x; i < NPAD * NPAD; i += BTHREADS) {
-              const int r = i / NPAD, c = i % NPAD;
-              double acc = (r == c && r < n) ? o.diag : 0.0;
-              for (int j = 0; j < o.nterms; ++j) {
-                const double xv = mslot(sm, o.t[j])[r * LDS + c];
-                acc = __dadd_rn(acc, o.coef[j] == 1.0 ? xv : __dmul_rn(o.coef[j], xv));
-              }
-              D[r * LDS + c] = acc;
-            }
+            D[r * G::LD + c] = acc;
           }
         }
         __syncthreads();
       }
       // carry the state: G <- G', F <- F', theta <- theta'
-      for (int i = threadIdx.x; i < NPAD * NPAD; i += BTHREADS) {
-        const int r = i / NPAD, c = i % NPAD;
-        mslot(sm, p.sG)[r * LDS + c] = mslot(sm, p.rG)[r * LDS + c];
-        mslot(sm, p.sF)[r * LDS + c] = mslot(sm, p.rF)[r * LDS + c];
+      for (int i = threadIdx.x; i < NP * NP; i += G::THREADS) {
+        const int r = i / NP, c = i % NP;
+        mslot(p.sG)[r * G::LD + c] = mslot(p.rG)[r * G::LD + c];
+        mslot(p.sF)[r * G::LD + c] = mslot(p.rF)[r * G::LD + c];
       }
-      if (threadIdx.x < NPAD) vslot(sm, p.nmat, p.sT)[threadIdx.x] = vslot(sm, p.nmat, p.rT)[threadIdx.x];
+      if (threadIdx.x < NP) vslot(p.sT)[threadIdx.x] = vslot(p.rT)[threadIdx.x];
       __syncthreads();
     }
-    store_mat(p.p_io + sys * nn, mslot(sm, p.sG), n);
-    store_mat(p.f_io + sys * nn, mslot(sm, p.sF), n);
-    if (threadIdx.x < n) p.theta_io[sys * n + threadIdx.x] = vslot(sm, p.nmat, p.sT)[threadIdx.x];
+    store_mat<NP>(p.p_io + sys * nn, mslot(p.sG), n);
+    store_mat<NP>(p.f_io + sys * nn, mslot(p.sF), n);
+    if (threadIdx.x < n) p.theta_io[sys * n + threadIdx.x] = vslot(p.sT)[threadIdx.x];
     __syncthreads();
   }
 }
@@ -385,46 +405,41 @@ int num_sms_b() {
   return n;
 }
 
-}  // namespace
-
-Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const double* a,
-                                      const double* b, const double* precond,
-                                      const double* residual, const std::vector<int>& rates,
-                                      const std::vector<const PlanNode*>& plans, int order_n,
-                                      int iters, double* p_io, double* f_io, double* theta_io) {
+// Registers of a recorded iteration.
+struct Recipe {
   Rec r;
-  const int A = r.fresh(false), P = r.fresh(false), B = r.fresh(false), G = r.fresh(false),
-            F = r.fresh(false), T = r.fresh(true), bv = r.fresh(true);
-  // plain Richardson with P_k (before the inversion update)
-  const int res = r.gemv(A, T, 1.0, bv, -1.0);    // A theta - b
-  const int tn = r.gemv(G, res, -1.0, T, 1.0);    // theta - P resid
-  // composite_step (ns:177-228)
-  std::vector<int> ts, gs;
-  for (size_t i = 0; i < rates.size(); ++i) {
-    const int ti = r.geometric(B, P, rates[i], A, plans[i]);
-    ts.push_back(ti);
-    gs.push_back(r.residual(ti, A));
-  }
-  int tc = ts[0], rc = gs[0];
-  for (size_t i = 1; i < ts.size(); ++i) {
-    tc = r.gemm(rc, ts[i], 1.0, tc, 1.0);
-    rc = r.gemm(rc, gs[i]);
-  }
-  const int nsp = r.horner(F, G, order_n);
-  const int gn = r.gemm(rc, nsp, 1.0, tc, 1.0);
-  const int fn = r.residual(gn, A);
+  int A, P, B, G, F, T, bv;
+  int gn, fn, tn;
+};
 
+// plain Richardson with P_k = G (before the inversion update)
+void record_plain(Recipe& q) {
+  const int res = q.r.gemv(q.A, q.T, 1.0, q.bv, -1.0);  // A theta - b
+  q.tn = q.r.gemv(q.G, res, -1.0, q.T, 1.0);            // theta - P resid
+}
+
+template <int NP>
+Counters launch(Ctx& c, Recipe& q, bool uses_split, int64_t batch, int64_t n, const double* a,
+                const double* b, const double* precond, const double* residual, int iters,
+                double* p_io, double* f_io, double* theta_io) {
+  using Gm = Geo<NP>;
   Counters per;
-  for (const BOp& o : r.ops) {
+  for (const BOp& o : q.r.ops) {
     if (o.kind == OP_GEMM) per.mmm += 1;
     if (o.kind == OP_GEMV) per.mvm += 1;
   }
   per.mmm *= iters;
   per.mvm *= iters;
   if (batch == 0 || iters == 0) return per;
+  if ((int)q.r.ops.size() > kMaxOps) throw Error(kEInval, "resident program too long");
 
-  Alloc al = assign(r, {A, P, B, G, F, T, bv, gn, fn, tn}, (int)r.ops.size());
-  std::vector<BOp> ops = r.ops;
+  std::vector<int> pinned = {q.A, q.G, q.F, q.T, q.bv, q.gn, q.fn, q.tn};
+  if (uses_split) {
+    pinned.push_back(q.P);
+    pinned.push_back(q.B);
+  }
+  Alloc al = assign(q.r, pinned);
+  std::vector<BOp> ops = q.r.ops;
   auto ph = [&](int v) -> int16_t { return v >= 0 ? al.phys[v] : (int16_t)-1; };
   for (BOp& o : ops) {
     o.dst = ph(o.dst);
@@ -434,13 +449,16 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
     if (o.kind == OP_LIN)
       for (int j = 0; j < o.nterms; ++j) o.t[j] = ph(o.t[j]);
   }
-  const size_t smem = (size_t)al.nmat * MSLOT * sizeof(double) + (size_t)al.nvec * NPAD * sizeof(double);
-  if (smem > 227 * 1024) throw Error(kEInval, "batched program needs too much shared memory");
+  const size_t smem =
+      (size_t)al.nmat * Gm::SLOT * sizeof(double) + (size_t)al.nvec * NP * sizeof(double);
+  if (smem + sizeof(BOp) * kMaxOps > 227 * 1024)
+    throw Error(kEInval, "resident program needs too much shared memory");
 
   MV dops = alloc(c, (int64_t)((ops.size() * sizeof(BOp) + 7) / 8), 1);
-  check(cudaMemcpyAsync(dops.v.p, ops.data(), ops.size() * sizeof(BOp), cudaMemcpyHostToDevice, c.s),
+  check(cudaMemcpyAsync(dops.v.p, ops.data(), ops.size() * sizeof(BOp), cudaMemcpyHostToDevice,
+                        c.s),
         "memcpy program");
-  BatchArgs args;
+  BatchArgs args{};
   args.a = a;
   args.b = b;
   args.precond = precond;
@@ -454,26 +472,84 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
   args.n = (int)n;
   args.iters = iters;
   args.batch = batch;
-  args.sA = al.phys[A];
-  args.sP = al.phys[P];
-  args.sB = al.phys[B];
-  args.sG = al.phys[G];
-  args.sF = al.phys[F];
-  args.sT = al.phys[T];
-  args.sb = al.phys[bv];
-  args.rG = al.phys[gn];
-  args.rF = al.phys[fn];
-  args.rT = al.phys[tn];
-  check(cudaFuncSetAttribute(batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+  args.sA = al.phys[q.A];
+  args.sP = uses_split ? al.phys[q.P] : -1;
+  args.sB = uses_split ? al.phys[q.B] : -1;
+  args.sG = al.phys[q.G];
+  args.sF = al.phys[q.F];
+  args.sT = al.phys[q.T];
+  args.sb = al.phys[q.bv];
+  args.rG = al.phys[q.gn];
+  args.rF = al.phys[q.fn];
+  args.rT = al.phys[q.tn];
+  check(cudaFuncSetAttribute(resident_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem),
         "cudaFuncSetAttribute");
   int per_sm = 0;
-  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batched_kernel, BTHREADS, smem),
+  check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, resident_kernel<NP>,
+                                                      Gm::THREADS, smem),
         "occupancy");
-  if (per_sm < 1) per_sm = 1;
+  if (per_sm < 1) throw Error(kEInval, "resident kernel does not fit on an SM");
   const int64_t grid = std::min<int64_t>(batch, (int64_t)num_sms_b() * per_sm);
-  batched_kernel<<<(unsigned)grid, BTHREADS, smem, c.s>>>(args);
-  check(cudaGetLastError(), "batched kernel launch");
+  resident_kernel<NP><<<(unsigned)grid, Gm::THREADS, smem, c.s>>>(args);
+  check(cudaGetLastError(), "resident kernel launch");
+  c.h->launches += 1;
   return per;
+}
+
+Recipe new_recipe() {
+  Recipe q;
+  q.A = q.r.fresh(false);
+  q.P = q.r.fresh(false);
+  q.B = q.r.fresh(false);
+  q.G = q.r.fresh(false);
+  q.F = q.r.fresh(false);
+  q.T = q.r.fresh(true);
+  q.bv = q.r.fresh(true);
+  return q;
+}
+
+}  // namespace
+
+Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const double* a,
+                                      const double* b, const double* precond,
+                                      const double* residual, const std::vector<int>& rates,
+                                      const std::vector<const PlanNode*>& plans, int order_n,
+                                      int iters, double* p_io, double* f_io, double* theta_io) {
+  Recipe q = new_recipe();
+  record_plain(q);
+  // composite_step (newton_schulz.py:177-228)
+  std::vector<int> ts, gs;
+  for (size_t i = 0; i < rates.size(); ++i) {
+    const int ti = q.r.geometric(q.B, q.P, rates[i], q.A, plans[i]);
+    ts.push_back(ti);
+    gs.push_back(q.r.residual(ti, q.A));
+  }
+  int tc = ts[0], rc = gs[0];
+  for (size_t i = 1; i < ts.size(); ++i) {
+    tc = q.r.gemm(rc, ts[i], 1.0, tc, 1.0);
+    rc = q.r.gemm(rc, gs[i]);
+  }
+  const int nsp = q.r.horner(q.F, q.G, order_n);
+  q.gn = q.r.gemm(rc, nsp, 1.0, tc, 1.0);
+  q.fn = q.r.residual(q.gn, q.A);
+  if (n <= 32)
+    return launch<32>(c, q, true, batch, n, a, b, precond, residual, iters, p_io, f_io, theta_io);
+  return launch<64>(c, q, true, batch, n, a, b, precond, residual, iters, p_io, f_io, theta_io);
+}
+
+Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a, const double* b,
+                               int order, const PlanNode* plan, int iters, double* p_io,
+                               double* f_io, double* theta_io) {
+  Recipe q = new_recipe();
+  record_plain(q);
+  // ns_step (newton_schulz.py:150-174)
+  const int gnew = plan ? q.r.eval(*plan, q.F, q.G, q.A) : q.r.horner(q.F, q.G, order);
+  q.gn = gnew == q.G ? q.r.copy(q.G) : gnew;
+  q.fn = q.r.residual(q.gn, q.A);
+  if (n <= 32)
+    return launch<32>(c, q, false, batch, n, a, b, nullptr, nullptr, iters, p_io, f_io, theta_io);
+  return launch<64>(c, q, false, batch, n, a, b, nullptr, nullptr, iters, p_io, f_io, theta_io);
 }
 
 }  // namespace si

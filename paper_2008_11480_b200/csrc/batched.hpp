@@ -5,7 +5,7 @@
 
 namespace si {
 
-constexpr int kBatchMaxN = 32;
+constexpr int kBatchMaxN = 64;
 constexpr int kBatchMaxRates = 4;
 
 // BASELINE config 2: `iters` x { plain Richardson with P_k;
@@ -17,5 +17,11 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
                                       const double* residual, const std::vector<int>& rates,
                                       const std::vector<const PlanNode*>& plans, int order_n,
                                       int iters, double* p_io, double* f_io, double* theta_io);
+
+// BASELINE config 1 (batch = 1) and batches of it: `iters` x { plain
+// Richardson with P_k; ns_step(order, plan) (newton_schulz.py:150-174) }.
+Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a, const double* b,
+                               int order, const PlanNode* plan, int iters, double* p_io,
+                               double* f_io, double* theta_io);
 
 }  // namespace si

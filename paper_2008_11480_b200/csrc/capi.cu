@@ -135,6 +135,17 @@ int si_destroy(si_handle h) {
   });
 }
 
+int si_set_allocator(si_handle h, void* (*alloc_fn)(void*, size_t, void*),
+                     void (*free_fn)(void*, void*, void*), void* ctx) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need((alloc_fn == nullptr) == (free_fn == nullptr), "alloc_fn and free_fn go together");
+    h->h.alloc_fn = alloc_fn;
+    h->h.free_fn = free_fn;
+    h->h.alloc_ctx = ctx;
+  });
+}
+
 int si_trim(si_handle h) {
   return guard([&] {
     need(h != nullptr, "null handle");
@@ -510,7 +521,7 @@ int si_batched_composite_richardson(si_handle h, int64_t batch, int64_t n, const
   return guard([&] {
     need(h && a && b && precond && residual && rates && p_io && f_io && theta_io,
          "null pointer");
-    need(batch >= 0 && n >= 1 && n <= kBatchMaxN, "batched path supports 1 <= n <= 32");
+    need(batch >= 0 && n >= 1 && n <= kBatchMaxN, "batched path supports 1 <= n <= 64");
     need(nrates >= 1 && nrates <= kBatchMaxRates, "batched path supports 1..4 rates");
     need(order_n >= 1 && iters >= 0, "bad order_n / iters");
     std::vector<int> rv(rates, rates + nrates);
@@ -527,6 +538,26 @@ int si_batched_composite_richardson(si_handle h, int64_t batch, int64_t n, const
     Call call(h, stream, nullptr);
     Counters per = batched_composite_richardson(call.c, batch, n, a, b, precond, residual, rv, pv,
                                                 order_n, iters, p_io, f_io, theta_io);
+    if (counters) {
+      counters[0] += per.mmm;
+      counters[1] += per.mvm;
+    }
+  });
+}
+
+int si_batched_ns_richardson(si_handle h, int64_t batch, int64_t n, const double* a,
+                             const double* b, int order, const int32_t* plan, int64_t plan_len,
+                             const double* consts, int64_t nconsts, int iters, double* p_io,
+                             double* f_io, double* theta_io, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && b && p_io && f_io && theta_io, "null pointer");
+    need(batch >= 0 && n >= 1 && n <= kBatchMaxN, "batched path supports 1 <= n <= 64");
+    need(order >= 1 && iters >= 0, "bad order / iters");
+    PlanPtr pl = opt_plan(plan, plan_len, consts, nconsts);
+    if (pl) need(plan_order_of(*pl) == order, "plan order != iteration order");
+    Call call(h, stream, nullptr);
+    Counters per = batched_ns_richardson(call.c, batch, n, a, b, order, pl.get(), iters, p_io,
+                                         f_io, theta_io);
     if (counters) {
       counters[0] += per.mmm;
       counters[1] += per.mvm;

@@ -22,7 +22,11 @@ void check(cudaError_t e, const char* what) {
 }
 
 Buf::~Buf() {
-  if (p) cudaFreeAsync(p, free_stream);
+  if (!p) return;
+  if (external)
+    h->free_fn(h->alloc_ctx, p, free_stream);
+  else
+    cudaFreeAsync(p, free_stream);
 }
 
 MV view(double* p, int64_t rows, int64_t cols, int64_t ld) {
@@ -37,10 +41,27 @@ MV view(double* p, int64_t rows, int64_t cols, int64_t ld) {
 MV alloc(Ctx& c, int64_t rows, int64_t cols) {
   auto b = std::make_shared<Buf>();
   b->free_stream = c.root;
+  b->h = c.h;
   void* p = nullptr;
   const size_t bytes = sizeof(double) * (size_t)std::max<int64_t>(rows * cols, 1);
-  check(cudaMallocFromPoolAsync(&p, bytes, c.h->pool, c.s), "cudaMallocFromPoolAsync");
+  if (c.h->alloc_fn) {
+    // external allocator, always associated with the root stream
+    p = c.h->alloc_fn(c.h->alloc_ctx, bytes, c.root);
+    if (!p) throw Error(kENoMem, "external allocator returned NULL");
+    b->external = true;
+    if (c.s != c.root) {
+      // a branch stream uses memory handed out in root-stream order
+      cudaEvent_t e;
+      check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      check(cudaEventRecord(e, c.root), "cudaEventRecord");
+      check(cudaStreamWaitEvent(c.s, e, 0), "cudaStreamWaitEvent");
+      cudaEventDestroy(e);
+    }
+  } else {
+    check(cudaMallocFromPoolAsync(&p, bytes, c.h->pool, c.s), "cudaMallocFromPoolAsync");
+  }
   b->p = static_cast<double*>(p);
+  if (c.keep) c.keep->push_back(b);
   MV m = view(b->p, rows, cols, cols);
   m.own = b;
   return m;
@@ -404,6 +425,7 @@ Ctx Fork::branch(int i) {
   if (i < 0 || i >= Handle::kSide) throw Error(kEInval, "too many branches");
   Ctx ch(parent.h, parent.root);
   ch.s = parent.h->side[i];
+  ch.keep = std::make_shared<std::vector<std::shared_ptr<Buf>>>();
   check(cudaStreamWaitEvent(ch.s, evs[0], 0), "cudaStreamWaitEvent");
   return ch;
 }
@@ -415,6 +437,8 @@ void Fork::join(Ctx& child) {
   evs.push_back(e);
   parent.ctr.mmm += child.ctr.mmm;
   parent.ctr.mvm += child.ctr.mvm;
+  // the root stream now follows every use in the branch: its temporaries may go
+  if (child.keep) child.keep->clear();
 }
 
 }  // namespace si

@@ -37,12 +37,23 @@ struct Handle {
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> prof_pool;
   int64_t launches = 0;  // kernels launched by this handle
+  // Optional external allocator (si_set_allocator): the Python layer routes
+  // temporaries through PyTorch's caching allocator so that one allocator owns
+  // all device memory (at n=32768 a matrix is 8.6 GB; two caches do not fit).
+  void* (*alloc_fn)(void* ctx, size_t bytes, void* stream) = nullptr;
+  void (*free_fn)(void* ctx, void* ptr, void* stream) = nullptr;
+  void* alloc_ctx = nullptr;
 };
 
-// Owning device buffer, released stream-ordered on its root stream.
+// Owning device buffer, released stream-ordered on its root stream (the
+// stream of the C-ABI call).  Buffers created inside a concurrent branch are
+// kept alive by the branch until it is joined, so their release is ordered
+// after every use on the side stream.
 struct Buf {
   double* p = nullptr;
   cudaStream_t free_stream = nullptr;
+  Handle* h = nullptr;
+  bool external = false;
   ~Buf();
 };
 
@@ -63,6 +74,8 @@ struct Ctx {
   cudaStream_t root;
   cudaStream_t s;
   Counters ctr;
+  // set on branch contexts: buffers allocated in the branch, released at join
+  std::shared_ptr<std::vector<std::shared_ptr<Buf>>> keep;
   Ctx(Handle* hh, cudaStream_t st) : h(hh), root(st), s(st) {}
 };
 

@@ -47,7 +47,8 @@ def test_prototype_arity_matches_header():
     for name, argtypes in _lib.SIGNATURES.items():
         m = re.search(rf"{name}\s*\(([^;]*)\);", text, re.S)
         assert m, name
-        params = [p for p in m.group(1).split(",") if p.strip() and p.strip() != "void"]
+        body = re.sub(r"\(\*(\w+)\)\s*\([^()]*\)", r"(*\1)", m.group(1))  # fn-pointer params
+        params = [p for p in body.split(",") if p.strip() and p.strip() != "void"]
         assert len(params) == len(argtypes), name
 
 

@@ -363,3 +363,51 @@ def test_c3_full_size_properties():
         norms.append(float(torch.linalg.norm(sp.matrix @ theta - b)))
     assert all(n2 < n1 for n1, n2 in zip(norms, norms[1:]) if n1 > 1e-9)
     assert P.converged(st)
+
+
+def test_resident_c1_matches_reference_per_iteration():
+    """BASELINE config 1 through the resident kernel (state in shared memory)."""
+    import paper_2008_11480_b200 as P
+
+    g = golden("c1.npz")
+    a = torch.as_tensor(g["a"], device="cuda")
+    b = torch.as_tensor(g["b"], device="cuda")
+    alpha = float(np.max(np.sum(np.abs(g["a"]), axis=1)))
+    eye = torch.eye(64, dtype=torch.float64, device="cuda")
+    p, f = eye / alpha, eye - a / alpha
+    theta = torch.zeros_like(b)
+    ctr = P.MulCounter()
+    for k in range(1, 31):
+        p, f, theta = P.batched_ns_richardson(a, b, p, f, theta, 3, 1, ctr=ctr)
+        assert np.linalg.norm(theta.cpu().numpy() - g[f"theta_{k}"]) <= TOL * np.linalg.norm(g[f"theta_{k}"])
+        assert np.linalg.norm(p.cpu().numpy() - g[f"p_{k}"]) <= TOL * np.linalg.norm(g[f"p_{k}"])
+    assert (ctr.mmm, ctr.mvm) == (int(g["mmm"]), int(g["mvm"]))
+    # one fused launch of all 30 iterations is bitwise the stepwise result
+    p30, f30, t30 = P.batched_ns_richardson(a, b, eye / alpha, eye - a / alpha,
+                                            torch.zeros_like(b), 3, 30)
+    assert torch.equal(p30, p) and torch.equal(t30, theta)
+
+
+def test_resident_ns_plan_and_batch_vs_oracle():
+    import paper_2008_11480_b200 as P
+    from oracle import seriesinv_oracle as o
+
+    rng = np.random.default_rng(11)
+    batch, n = 5, 48
+    g = rng.standard_normal((batch, 2 * n, n))
+    a_np = np.einsum("bki,bkj->bij", g, g) / (2 * n) + 0.2 * np.eye(n)
+    b_np = rng.standard_normal((batch, n))
+    a = torch.as_tensor(a_np, device="cuda")
+    b = torch.as_tensor(b_np, device="cuda")
+    pre, res = P.batched_scalar_split(a)
+    plan = P.table_plans()[8][0]
+    p, f, th = P.batched_ns_richardson(a, b, pre, res, torch.zeros_like(b), 8, 4, plan=plan)
+    for i in range(batch):
+        sp = o.split_scalar(a_np[i], o.inf_norm(a_np[i]) / 2.0)
+        st = o.initial_series(sp, 0, 1, 8)
+        theta = np.zeros(n)
+        for _ in range(4):
+            theta = o.plain_richardson(theta, st.estimate, sp.matrix, b_np[i], st.ctr)
+            st = o.ns_step(st, sp.matrix, o.TABLE_ROOTS[8][0][1])
+        assert np.linalg.norm(p[i].cpu().numpy() - st.estimate) <= TOL * np.linalg.norm(st.estimate)
+        assert np.linalg.norm(th[i].cpu().numpy() - theta) <= TOL * np.linalg.norm(theta)
