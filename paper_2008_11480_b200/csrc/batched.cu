@@ -7,9 +7,15 @@
 // richardson.py:88-89) is recorded once on the host, register-allocated onto
 // shared-memory matrix slots, and interpreted by one CTA per system for all
 // `iters` iterations: the state never leaves shared memory, products run on
-// DMMA (m8n8k4), and HBM is touched once per system on entry (coalesced
-// double2 loads) and once on exit.  Per system this executes exactly the
-// reference's products, so MulCounter deltas match tick for tick.
+// DMMA (m8n8k4), and HBM is touched once per system on entry and exit (plus
+// the splitting S^-1 / B, streamed in when a product needs them so they do
+// not occupy slots).  Per system this executes exactly the reference's
+// products, so MulCounter deltas match tick for tick.
+//
+// Shared-memory layout: a slot is an unpadded NP x NP row-major matrix whose
+// 16-byte chunks are XOR-swizzled by 2*(row & 3); every DMMA fragment load is
+// then the minimum 2 wavefronts, and slots are 8 KB (NP=32) / 32 KB (NP=64),
+// so three 32 x 32 systems fit per SM.
 #include <algorithm>
 
 #include "batched.hpp"
@@ -17,11 +23,11 @@
 namespace si {
 namespace {
 
-enum : int8_t { OP_GEMM = 0, OP_GEMV = 1, OP_LIN = 2 };
+enum : int8_t { OP_GEMM = 0, OP_GEMV = 1, OP_LIN = 2, OP_LOAD = 3 };
 
 struct BOp {
   int8_t kind;
-  int8_t vec;  // lin over vectors
+  int8_t vec;  // lin over vectors; for OP_LOAD: 0 = S^-1, 1 = B
   int8_t nterms;
   int8_t pad_;
   int16_t dst, a, b, c;
@@ -38,6 +44,15 @@ struct Rec {
   int fresh(bool vec) {
     is_vec.push_back(vec);
     return (int)is_vec.size() - 1;
+  }
+  int load(int which) {
+    BOp o{};
+    o.kind = OP_LOAD;
+    o.vec = (int8_t)which;
+    o.a = o.b = o.c = -1;
+    o.dst = fresh(false);
+    ops.push_back(o);
+    return o.dst;
   }
   int gemm(int a, int b, double alpha = 1.0, int c = -1, double beta = 0.0, double diag = 0.0) {
     BOp o{};
@@ -91,7 +106,30 @@ struct Rec {
     env[0] = y;
     env[1] = x;
     int res = x;
-    for (const Instr& in : node.prog) {
+    const auto& prog = node.prog;
+    for (size_t i = 0; i < prog.size(); ++i) {
+      const Instr& in = prog[i];
+      if (in.op == 0 && i + 1 < prog.size()) {
+        // Mul followed by "0*I + 1*other + 1*mul" with the product used nowhere
+        // else: one GEMM with the add in its epilogue (same rounding).
+        const Instr& nx = prog[i + 1];
+        bool dead_after = true;
+        for (size_t j = i + 2; j < prog.size(); ++j) {
+          const Instr& u = prog[j];
+          if (u.a == in.dst || u.b == in.dst) dead_after = false;
+          for (auto& tt : u.terms)
+            if (tt.second == in.dst) dead_after = false;
+        }
+        if (nx.op == 2 && nx.cconst == 0.0 && nx.terms.size() == 2 && nx.terms[0].first == 1.0 &&
+            nx.terms[1].first == 1.0 && dead_after && nx.dst != in.dst &&
+            (nx.terms[0].second == in.dst) != (nx.terms[1].second == in.dst)) {
+          const int other = nx.terms[0].second == in.dst ? nx.terms[1].second : nx.terms[0].second;
+          env[nx.dst] = gemm(env[in.a], env[in.b], 1.0, env[other], 1.0);
+          res = env[nx.dst];
+          ++i;
+          continue;
+        }
+      }
       if (in.op == 0)
         env[in.dst] = gemm(env[in.a], env[in.b]);
       else if (in.op == 1)
@@ -147,14 +185,18 @@ struct Rec {
   }
 };
 
-// Linear-scan assignment of virtual registers to physical slots; pinned
-// registers (inputs and the carried results) keep their slots for the run.
+// Linear-scan assignment of virtual registers to shared-memory slots.
+//  * pinned: live for the whole run (A, b);
+//  * carried (in, out): `in` holds the state at the start of an iteration and
+//    dies at its last use; `out` (its next value) is live from its definition to
+//    the end and takes `in`'s slot when that is free -- no copy needed.
 struct Alloc {
   std::vector<int16_t> phys;
   int nmat = 0, nvec = 0;
 };
 
-Alloc assign(const Rec& r, const std::vector<int>& pinned) {
+Alloc assign(const Rec& r, const std::vector<int>& pinned,
+             const std::vector<std::pair<int, int>>& carried) {
   const int nv = (int)r.is_vec.size();
   std::vector<int> last(nv, -1);
   auto use = [&](int v, int i) {
@@ -169,6 +211,11 @@ Alloc assign(const Rec& r, const std::vector<int>& pinned) {
       for (int j = 0; j < o.nterms; ++j) use(o.t[j], i);
   }
   for (int p : pinned) last[p] = INT32_MAX;
+  std::vector<int> out_of(nv, -1);  // out -> in
+  for (auto& pr : carried) {
+    last[pr.second] = INT32_MAX;
+    out_of[pr.second] = pr.first;
+  }
   Alloc al;
   al.phys.assign(nv, -1);
   std::vector<int> free_m, free_v;
@@ -181,22 +228,39 @@ Alloc assign(const Rec& r, const std::vector<int>& pinned) {
     }
     return vec ? al.nvec++ : al.nmat++;
   };
+  auto release = [&](int v) {
+    if (v >= 0 && al.phys[v] >= 0 && last[v] != INT32_MAX && last[v] != -2) {
+      (r.is_vec[v] ? free_v : free_m).push_back(al.phys[v]);
+      last[v] = -2;
+    }
+  };
   for (int p : pinned) al.phys[p] = (int16_t)take(r.is_vec[p]);
+  for (auto& pr : carried) al.phys[pr.first] = (int16_t)take(r.is_vec[pr.first]);
+  for (auto& pr : carried)  // a carried input never read this iteration is free at once
+    if (last[pr.first] == -1) release(pr.first);
   for (int i = 0; i < (int)r.ops.size(); ++i) {
     const BOp& o = r.ops[i];
-    al.phys[o.dst] = (int16_t)take(r.is_vec[o.dst]);
-    auto release = [&](int v) {
-      if (v >= 0 && last[v] == i && al.phys[v] >= 0) {
-        (r.is_vec[v] ? free_v : free_m).push_back(al.phys[v]);
-        last[v] = -2;
+    const bool vec = r.is_vec[o.dst];
+    if (al.phys[o.dst] < 0) {
+      const int in = out_of[o.dst];
+      auto& fl = vec ? free_v : free_m;
+      auto it = in >= 0 ? std::find(fl.begin(), fl.end(), (int)al.phys[in]) : fl.end();
+      if (it != fl.end()) {
+        al.phys[o.dst] = (int16_t)*it;
+        fl.erase(it);
+      } else {
+        al.phys[o.dst] = (int16_t)take(vec);
       }
+    }
+    auto rel_if_last = [&](int v) {
+      if (v >= 0 && last[v] == i) release(v);
     };
-    release(o.a);
-    release(o.b);
-    release(o.c);
+    rel_if_last(o.a);
+    rel_if_last(o.b);
+    rel_if_last(o.c);
     if (o.kind == OP_LIN)
-      for (int j = 0; j < o.nterms; ++j) release(o.t[j]);
-    if (last[o.dst] == -1) (r.is_vec[o.dst] ? free_v : free_m).push_back(al.phys[o.dst]);
+      for (int j = 0; j < o.nterms; ++j) rel_if_last(o.t[j]);
+    if (last[o.dst] == -1) release(o.dst);  // never read
   }
   return al;
 }
@@ -224,56 +288,61 @@ struct BatchArgs {
   const BOp* ops;
   int nops;
   int nmat;
+  int nvec;
   int n;
   int iters;
   int64_t batch;
-  int sA, sP, sB, sG, sF, sT, sb;  // pinned slots (sP/sB < 0 when unused)
-  int rG, rF, rT;                  // per-iteration results carried into sG/sF/sT
+  int sA, sG, sF, sT, sb;  // slots of A, the carried inputs, b
+  int rG, rF, rT;          // slots of the carried outputs (copied back when different)
 };
 
-// NP: padded order (32 or 64); the row stride NP+4 doubles makes every DMMA
-// fragment load conflict-free (row starts advance 8 banks).
 template <int NP>
 struct Geo {
-  static constexpr int LD = NP + 4;
-  static constexpr int SLOT = NP * LD;
+  static constexpr int SLOT = NP * NP;
   static constexpr int WARPS = NP == 32 ? 4 : 8;
   static constexpr int THREADS = WARPS * 32;
   static constexpr int WROWS = NP / (WARPS / 2);  // warp tile rows (16)
   static constexpr int WCOLS = NP / 2;             // warp tile cols (16 or 32)
   static constexpr int MT = WROWS / 8, NT = WCOLS / 8;
+  // element (r, c) of a slot: 16-byte chunks XOR-swizzled by 2*(r & 3)
+  __device__ static __forceinline__ int idx(int r, int c) {
+    return r * NP + ((((c >> 1) ^ ((r & 3) << 1))) << 1) + (c & 1);
+  }
+  // logical column of the element stored at position (r, p)
+  __device__ static __forceinline__ int col_at(int r, int p) {
+    return ((((p >> 1) ^ ((r & 3) << 1))) << 1) + (p & 1);
+  }
 };
 
 template <int NP>
-__device__ void load_mat(double* dst, const double* src, int n) {
+__device__ void load_mat(double* dst, const double* __restrict__ src, int n) {
   using G = Geo<NP>;
   if (n == NP) {
     const double2* s2 = reinterpret_cast<const double2*>(src);
     for (int i = threadIdx.x; i < NP * NP / 2; i += G::THREADS) {
       const double2 v = __ldg(s2 + i);
-      const int r = (2 * i) / NP, c = (2 * i) % NP;
-      dst[r * G::LD + c] = v.x;
-      dst[r * G::LD + c + 1] = v.y;
+      const int r = (2 * i) / NP, c = (2 * i) % NP;  // c even: one swizzled chunk
+      *reinterpret_cast<double2*>(dst + G::idx(r, c)) = v;
     }
   } else {
     for (int i = threadIdx.x; i < NP * NP; i += G::THREADS) {
       const int r = i / NP, c = i % NP;
-      dst[r * G::LD + c] = (r < n && c < n) ? src[r * n + c] : 0.0;
+      dst[G::idx(r, c)] = (r < n && c < n) ? src[r * n + c] : 0.0;
     }
   }
 }
 
 template <int NP>
-__device__ void store_mat(double* dst, const double* src, int n) {
+__device__ void store_mat(double* __restrict__ dst, const double* src, int n) {
   using G = Geo<NP>;
   if (n == NP) {
     double2* d2 = reinterpret_cast<double2*>(dst);
     for (int i = threadIdx.x; i < NP * NP / 2; i += G::THREADS) {
       const int r = (2 * i) / NP, c = (2 * i) % NP;
-      d2[i] = make_double2(src[r * G::LD + c], src[r * G::LD + c + 1]);
+      d2[i] = *reinterpret_cast<const double2*>(src + G::idx(r, c));
     }
   } else {
-    for (int i = threadIdx.x; i < n * n; i += G::THREADS) dst[i] = src[(i / n) * G::LD + (i % n)];
+    for (int i = threadIdx.x; i < n * n; i += G::THREADS) dst[i] = src[G::idx(i / n, i % n)];
   }
 }
 
@@ -281,22 +350,20 @@ template <int NP>
 __global__ void __launch_bounds__(Geo<NP>::THREADS) resident_kernel(BatchArgs p) {
   using G = Geo<NP>;
   extern __shared__ double sm[];
-  __shared__ BOp prog[kMaxOps];
+  // dynamic shared memory: [matrix slots][vector slots][program]
+  BOp* prog = reinterpret_cast<BOp*>(sm + (size_t)p.nmat * G::SLOT + (size_t)p.nvec * NP);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int n = p.n;
   const int64_t nn = (int64_t)n * n;
   auto mslot = [&](int s) { return sm + (size_t)s * G::SLOT; };
   auto vslot = [&](int s) { return sm + (size_t)p.nmat * G::SLOT + (size_t)s * NP; };
-  // the program is read by every thread for every op: stage it in shared memory
   for (int i = threadIdx.x; i < p.nops * (int)sizeof(BOp) / 4; i += G::THREADS)
     reinterpret_cast<int*>(prog)[i] = reinterpret_cast<const int*>(p.ops)[i];
   __syncthreads();
 
   for (int64_t sys = blockIdx.x; sys < p.batch; sys += gridDim.x) {
     load_mat<NP>(mslot(p.sA), p.a + sys * nn, n);
-    if (p.sP >= 0) load_mat<NP>(mslot(p.sP), p.precond + sys * nn, n);
-    if (p.sB >= 0) load_mat<NP>(mslot(p.sB), p.residual + sys * nn, n);
     load_mat<NP>(mslot(p.sG), p.p_io + sys * nn, n);
     load_mat<NP>(mslot(p.sF), p.f_io + sys * nn, n);
     if (threadIdx.x < NP) {
@@ -313,31 +380,38 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS) resident_kernel(BatchArgs p)
           const double* C = o.c >= 0 ? mslot(o.c) : nullptr;
           double* D = mslot(o.dst);
           const int r0 = (warp >> 1) * G::WROWS, c0 = (warp & 1) * G::WCOLS;
-          double acc[G::MT][G::NT][2] = {};
+          // two accumulator sets (even / odd k-steps): dependent DMMA chains of
+          // NP/8 instead of NP/4, combined once in a fixed order
+          double acc[2][G::MT][G::NT][2] = {};
 #pragma unroll
           for (int kk = 0; kk < NP; kk += 4) {
             double af[G::MT], bf[G::NT];
 #pragma unroll
-            for (int mi = 0; mi < G::MT; ++mi) af[mi] = A[(r0 + mi * 8 + g) * G::LD + kk + t];
+            for (int mi = 0; mi < G::MT; ++mi) af[mi] = A[G::idx(r0 + mi * 8 + g, kk + t)];
 #pragma unroll
-            for (int ni = 0; ni < G::NT; ++ni) bf[ni] = B[(kk + t) * G::LD + c0 + ni * 8 + g];
+            for (int ni = 0; ni < G::NT; ++ni) bf[ni] = B[G::idx(kk + t, c0 + ni * 8 + g)];
+            const int h = (kk >> 2) & 1;
 #pragma unroll
             for (int mi = 0; mi < G::MT; ++mi)
 #pragma unroll
               for (int ni = 0; ni < G::NT; ++ni)
-                dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+                dmma(acc[h][mi][ni][0], acc[h][mi][ni][1], af[mi], bf[ni]);
           }
 #pragma unroll
           for (int mi = 0; mi < G::MT; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < G::NT; ++ni)
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const int row = r0 + mi * 8 + g, col = c0 + ni * 8 + 2 * t + h;
-                double v = epi(acc[mi][ni][h], o.alpha, o.beta, C ? C[row * G::LD + col] : 0.0);
-                if (o.diag != 0.0 && row == col && row < n) v = __dadd_rn(v, o.diag);
-                D[row * G::LD + col] = v;
+            for (int ni = 0; ni < G::NT; ++ni) {
+              const int row = r0 + mi * 8 + g, col = c0 + ni * 8 + 2 * t;
+              double2 cv = make_double2(0.0, 0.0);
+              if (C) cv = *reinterpret_cast<const double2*>(C + G::idx(row, col));
+              double v0 = epi(__dadd_rn(acc[0][mi][ni][0], acc[1][mi][ni][0]), o.alpha, o.beta, cv.x);
+              double v1 = epi(__dadd_rn(acc[0][mi][ni][1], acc[1][mi][ni][1]), o.alpha, o.beta, cv.y);
+              if (o.diag != 0.0 && row < n) {
+                if (row == col) v0 = __dadd_rn(v0, o.diag);
+                if (row == col + 1) v1 = __dadd_rn(v1, o.diag);
               }
+              *reinterpret_cast<double2*>(D + G::idx(row, col)) = make_double2(v0, v1);
+            }
         } else if (o.kind == OP_GEMV) {
           // every warp takes NP / WARPS rows; lanes split k, fixed-order shuffle sum
           const double* A = mslot(o.a);
@@ -348,7 +422,7 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS) resident_kernel(BatchArgs p)
             const int row = warp * RPW + rr;
             double s = 0.0;
 #pragma unroll
-            for (int kk = lane; kk < NP; kk += 32) s = fma(A[row * G::LD + kk], x[kk], s);
+            for (int kk = lane; kk < NP; kk += 32) s = fma(A[G::idx(row, kk)], x[kk], s);
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
             if (lane == 0) {
@@ -356,6 +430,8 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS) resident_kernel(BatchArgs p)
               vslot(o.dst)[row] = epi(s, o.alpha, o.beta, cv);
             }
           }
+        } else if (o.kind == OP_LOAD) {
+          load_mat<NP>(mslot(o.dst), (o.vec ? p.residual : p.precond) + sys * nn, n);
         } else if (o.vec) {
           if (threadIdx.x < NP) {
             double acc = 0.0;
@@ -368,24 +444,26 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS) resident_kernel(BatchArgs p)
         } else {
           double* D = mslot(o.dst);
           for (int i = threadIdx.x; i < NP * NP; i += G::THREADS) {
-            const int r = i / NP, c = i % NP;
+            const int r = i / NP;
+            const int c = G::col_at(r, i % NP);
             double acc = (r == c && r < n) ? o.diag : 0.0;
             for (int j = 0; j < o.nterms; ++j) {
-              const double xv = mslot(o.t[j])[r * G::LD + c];
+              const double xv = mslot(o.t[j])[i];
               acc = __dadd_rn(acc, o.coef[j] == 1.0 ? xv : __dmul_rn(o.coef[j], xv));
             }
-            D[r * G::LD + c] = acc;
+            D[i] = acc;
           }
         }
         __syncthreads();
       }
-      // carry the state: G <- G', F <- F', theta <- theta'
-      for (int i = threadIdx.x; i < NP * NP; i += G::THREADS) {
-        const int r = i / NP, c = i % NP;
-        mslot(p.sG)[r * G::LD + c] = mslot(p.rG)[r * G::LD + c];
-        mslot(p.sF)[r * G::LD + c] = mslot(p.rF)[r * G::LD + c];
+      // carry the state where the allocator could not place it in place
+      if (p.rG != p.sG || p.rF != p.sF) {
+        for (int i = threadIdx.x; i < NP * NP; i += G::THREADS) {
+          if (p.rG != p.sG) mslot(p.sG)[i] = mslot(p.rG)[i];
+          if (p.rF != p.sF) mslot(p.sF)[i] = mslot(p.rF)[i];
+        }
       }
-      if (threadIdx.x < NP) vslot(p.sT)[threadIdx.x] = vslot(p.rT)[threadIdx.x];
+      if (p.rT != p.sT && threadIdx.x < NP) vslot(p.sT)[threadIdx.x] = vslot(p.rT)[threadIdx.x];
       __syncthreads();
     }
     store_mat<NP>(p.p_io + sys * nn, mslot(p.sG), n);
@@ -408,9 +486,19 @@ int num_sms_b() {
 // Registers of a recorded iteration.
 struct Recipe {
   Rec r;
-  int A, P, B, G, F, T, bv;
-  int gn, fn, tn;
+  int A, G, F, T, bv;
+  int gn = -1, fn = -1, tn = -1;
 };
+
+Recipe new_recipe() {
+  Recipe q;
+  q.A = q.r.fresh(false);
+  q.G = q.r.fresh(false);
+  q.F = q.r.fresh(false);
+  q.T = q.r.fresh(true);
+  q.bv = q.r.fresh(true);
+  return q;
+}
 
 // plain Richardson with P_k = G (before the inversion update)
 void record_plain(Recipe& q) {
@@ -419,9 +507,9 @@ void record_plain(Recipe& q) {
 }
 
 template <int NP>
-Counters launch(Ctx& c, Recipe& q, bool uses_split, int64_t batch, int64_t n, const double* a,
-                const double* b, const double* precond, const double* residual, int iters,
-                double* p_io, double* f_io, double* theta_io) {
+Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, const double* b,
+                const double* precond, const double* residual, int iters, double* p_io,
+                double* f_io, double* theta_io) {
   using Gm = Geo<NP>;
   Counters per;
   for (const BOp& o : q.r.ops) {
@@ -433,12 +521,7 @@ Counters launch(Ctx& c, Recipe& q, bool uses_split, int64_t batch, int64_t n, co
   if (batch == 0 || iters == 0) return per;
   if ((int)q.r.ops.size() > kMaxOps) throw Error(kEInval, "resident program too long");
 
-  std::vector<int> pinned = {q.A, q.G, q.F, q.T, q.bv, q.gn, q.fn, q.tn};
-  if (uses_split) {
-    pinned.push_back(q.P);
-    pinned.push_back(q.B);
-  }
-  Alloc al = assign(q.r, pinned);
+  Alloc al = assign(q.r, {q.A, q.bv}, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}});
   std::vector<BOp> ops = q.r.ops;
   auto ph = [&](int v) -> int16_t { return v >= 0 ? al.phys[v] : (int16_t)-1; };
   for (BOp& o : ops) {
@@ -449,10 +532,9 @@ Counters launch(Ctx& c, Recipe& q, bool uses_split, int64_t batch, int64_t n, co
     if (o.kind == OP_LIN)
       for (int j = 0; j < o.nterms; ++j) o.t[j] = ph(o.t[j]);
   }
-  const size_t smem =
-      (size_t)al.nmat * Gm::SLOT * sizeof(double) + (size_t)al.nvec * NP * sizeof(double);
-  if (smem + sizeof(BOp) * kMaxOps > 227 * 1024)
-    throw Error(kEInval, "resident program needs too much shared memory");
+  const size_t smem = (size_t)al.nmat * Gm::SLOT * sizeof(double) +
+                      (size_t)al.nvec * NP * sizeof(double) + ops.size() * sizeof(BOp);
+  if (smem > 227 * 1024) throw Error(kEInval, "resident program needs too much shared memory");
 
   MV dops = alloc(c, (int64_t)((ops.size() * sizeof(BOp) + 7) / 8), 1);
   check(cudaMemcpyAsync(dops.v.p, ops.data(), ops.size() * sizeof(BOp), cudaMemcpyHostToDevice,
@@ -469,12 +551,11 @@ Counters launch(Ctx& c, Recipe& q, bool uses_split, int64_t batch, int64_t n, co
   args.ops = reinterpret_cast<const BOp*>(dops.v.p);
   args.nops = (int)ops.size();
   args.nmat = al.nmat;
+  args.nvec = al.nvec;
   args.n = (int)n;
   args.iters = iters;
   args.batch = batch;
   args.sA = al.phys[q.A];
-  args.sP = uses_split ? al.phys[q.P] : -1;
-  args.sB = uses_split ? al.phys[q.B] : -1;
   args.sG = al.phys[q.G];
   args.sF = al.phys[q.F];
   args.sT = al.phys[q.T];
@@ -497,18 +578,6 @@ Counters launch(Ctx& c, Recipe& q, bool uses_split, int64_t batch, int64_t n, co
   return per;
 }
 
-Recipe new_recipe() {
-  Recipe q;
-  q.A = q.r.fresh(false);
-  q.P = q.r.fresh(false);
-  q.B = q.r.fresh(false);
-  q.G = q.r.fresh(false);
-  q.F = q.r.fresh(false);
-  q.T = q.r.fresh(true);
-  q.bv = q.r.fresh(true);
-  return q;
-}
-
 }  // namespace
 
 Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const double* a,
@@ -518,10 +587,14 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
                                       int iters, double* p_io, double* f_io, double* theta_io) {
   Recipe q = new_recipe();
   record_plain(q);
-  // composite_step (newton_schulz.py:177-228)
+  // composite_step (newton_schulz.py:177-228).  The NS part S_n(F) G is
+  // evaluated first (the parts are independent of it) so G and F die early;
+  // S^-1 and B are streamed in for the parts and die after the last one.
+  const int nsp = q.r.horner(q.F, q.G, order_n);
+  const int P = q.r.load(0), B = q.r.load(1);
   std::vector<int> ts, gs;
   for (size_t i = 0; i < rates.size(); ++i) {
-    const int ti = q.r.geometric(q.B, q.P, rates[i], q.A, plans[i]);
+    const int ti = q.r.geometric(B, P, rates[i], q.A, plans[i]);
     ts.push_back(ti);
     gs.push_back(q.r.residual(ti, q.A));
   }
@@ -530,12 +603,11 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
     tc = q.r.gemm(rc, ts[i], 1.0, tc, 1.0);
     rc = q.r.gemm(rc, gs[i]);
   }
-  const int nsp = q.r.horner(q.F, q.G, order_n);
   q.gn = q.r.gemm(rc, nsp, 1.0, tc, 1.0);
   q.fn = q.r.residual(q.gn, q.A);
   if (n <= 32)
-    return launch<32>(c, q, true, batch, n, a, b, precond, residual, iters, p_io, f_io, theta_io);
-  return launch<64>(c, q, true, batch, n, a, b, precond, residual, iters, p_io, f_io, theta_io);
+    return launch<32>(c, q, batch, n, a, b, precond, residual, iters, p_io, f_io, theta_io);
+  return launch<64>(c, q, batch, n, a, b, precond, residual, iters, p_io, f_io, theta_io);
 }
 
 Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a, const double* b,
@@ -548,8 +620,8 @@ Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a
   q.gn = gnew == q.G ? q.r.copy(q.G) : gnew;
   q.fn = q.r.residual(q.gn, q.A);
   if (n <= 32)
-    return launch<32>(c, q, false, batch, n, a, b, nullptr, nullptr, iters, p_io, f_io, theta_io);
-  return launch<64>(c, q, false, batch, n, a, b, nullptr, nullptr, iters, p_io, f_io, theta_io);
+    return launch<32>(c, q, batch, n, a, b, nullptr, nullptr, iters, p_io, f_io, theta_io);
+  return launch<64>(c, q, batch, n, a, b, nullptr, nullptr, iters, p_io, f_io, theta_io);
 }
 
 }  // namespace si
