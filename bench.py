@@ -399,7 +399,7 @@ def run_reference(args):
     # each step: a bounded full-size sample, extrapolated to one step of the workload
     step_times = []
     for i in range(args.warmup + args.steps):
-        s, t = cpu_sample(sample_n, flops * (sample_n / n) ** 3 if cfg == "c5" else flops)
+        s, t = cpu_sample(sample_n, flops * (sample_n / n) ** 3 if cfg == "c5" else flops, reps=2)
         if cfg == "c5":
             s *= (n / sample_n) ** 3
         if i >= args.warmup:

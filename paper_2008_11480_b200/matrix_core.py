@@ -25,11 +25,15 @@ __all__ = [
     "fro_norm",
     "identity",
     "inf_norm",
+    "load_matrix",
+    "load_vector",
     "mat_mul",
     "mat_pow",
     "mat_pow_counted",
     "mat_vec",
     "norms",
+    "save_matrix",
+    "save_vector",
     "spectral_radius",
     "square_matrix",
     "to_host",
@@ -184,6 +188,83 @@ def inf_norm(a) -> float:
 def norms(a) -> Norms:
     """Frobenius and infinity norms (matrix_core.py:154-172)."""
     return Norms(frobenius=fro_norm(a), inf_norm=inf_norm(a))
+
+
+# ---------------------------------------------------------------------------
+# On-disk formats: the reference's text format (matrix_core.py:242-310: a "dim"
+# line, then rows, '#' comment lines, 17 significant digits) and a binary .npy
+# path for the sizes where text is unusable (25 GB of text at n=32768).
+# ---------------------------------------------------------------------------
+
+
+def _data_lines(text: str) -> list[str]:
+    return [ln.strip() for ln in text.splitlines() if ln.strip() and not ln.strip().startswith("#")]
+
+
+def load_matrix(path, device: torch.device | None = None) -> torch.Tensor:
+    """Square matrix from ``.npy`` or the reference text format, placed on the device."""
+    if str(path).endswith(".npy"):
+        return square_matrix(np.load(path, allow_pickle=False))
+    with open(path, "r", encoding="utf-8") as fh:
+        lines = _data_lines(fh.read())
+    if not lines:
+        raise ValueError(f"{path}: empty matrix file")
+    dim = int(lines[0])
+    if dim < 1:
+        raise ValueError(f"{path}: dimension must be positive, got {dim}")
+    if len(lines) != 1 + dim:
+        raise ValueError(f"{path}: expected {dim} data rows, got {len(lines) - 1}")
+    rows = []
+    for i, line in enumerate(lines[1:]):
+        row = [float(tok) for tok in line.split()]
+        if len(row) != dim:
+            raise ValueError(f"{path}: row {i} has {len(row)} entries, expected {dim}")
+        rows.append(row)
+    return square_matrix(np.array(rows))
+
+
+def save_matrix(path, a, comment: str | None = None) -> None:
+    """Write ``.npy`` (binary) or the reference text format (17 significant digits)."""
+    host = to_host(a) if isinstance(a, torch.Tensor) else np.asarray(a, dtype=np.float64)
+    if host.ndim != 2 or host.shape[0] != host.shape[1]:
+        raise ValueError(f"expected a square matrix, got shape {host.shape}")
+    if str(path).endswith(".npy"):
+        np.save(path, host)
+        return
+    with open(path, "w", encoding="utf-8") as fh:
+        for line in (comment or "").splitlines():
+            fh.write(f"# {line}\n")
+        fh.write(f"{host.shape[0]}\n")
+        for row in host:
+            fh.write(" ".join(format(x, ".17g") for x in row) + "\n")
+
+
+def load_vector(path) -> torch.Tensor:
+    if str(path).endswith(".npy"):
+        return vector(np.load(path, allow_pickle=False))
+    with open(path, "r", encoding="utf-8") as fh:
+        lines = _data_lines(fh.read())
+    if not lines:
+        raise ValueError(f"{path}: empty vector file")
+    dim = int(lines[0])
+    values = [float(tok) for line in lines[1:] for tok in line.split()]
+    if len(values) != dim:
+        raise ValueError(f"{path}: expected {dim} entries, got {len(values)}")
+    return vector(values)
+
+
+def save_vector(path, v, comment: str | None = None) -> None:
+    host = to_host(v) if isinstance(v, torch.Tensor) else np.asarray(v, dtype=np.float64)
+    host = host.reshape(-1)
+    if str(path).endswith(".npy"):
+        np.save(path, host)
+        return
+    with open(path, "w", encoding="utf-8") as fh:
+        for line in (comment or "").splitlines():
+            fh.write(f"# {line}\n")
+        fh.write(f"{host.size}\n")
+        for x in host:
+            fh.write(format(x, ".17g") + "\n")
 
 
 class SpectralRadiusError(RuntimeError):

@@ -340,6 +340,36 @@ def test_full_size_gemm_row_sampled(n):
     assert ctr.mmm == 1
 
 
+def test_c4_full_size_step():
+    """BASELINE config 4 at its full size (n=16384, 64 RHS): one composite step through
+    the native engine equals the block-row engine bitwise (two independent
+    orchestrations of the same DAG), F' = I - G' A holds on sampled rows, and the
+    counters follow the reference DAG (22 mmm + 2 mvm)."""
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import configs
+    from paper_2008_11480_b200.sharded import RowComm, ShardedEngine
+
+    n = 16384
+    a, b = configs.c4_householder_device(n=n, rhs=64)
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False, verify=False)
+    del a
+    st = P.initial_series(sp, 0, 1, order=2)
+    theta = torch.zeros_like(b)
+    c0 = st.ctr.copy()
+    theta1 = P.plain_richardson(theta, st.estimate, sp.matrix, b, st.ctr)
+    st1 = P.composite_step(st, sp.matrix, sp, P.CompositeSpec((2, 3, 4, 5)), 2)
+    assert (st1.ctr.mmm - c0.mmm, st1.ctr.mvm - c0.mvm) == (22, 2)
+    eng = ShardedEngine(RowComm(n))
+    A, Pc, B = (eng.replicated(x) for x in (sp.matrix, sp.precond, sp.residual))
+    g, f = eng.composite_step(eng.local(st.estimate), eng.local(st.residual), A, Pc, B,
+                              (2, 3, 4, 5), 2)
+    th = eng.plain_richardson(eng.replicated(theta), eng.local(st.estimate), A, eng.replicated(b))
+    assert torch.equal(g.t, st1.estimate) and torch.equal(f.t, st1.residual)
+    assert torch.equal(th.t, theta1)
+    rows = np.random.default_rng(4).choice(n, 8, replace=False)
+    _row_sample_check(st1.residual, st1.estimate, sp.matrix, rows, alpha=-1.0, diag=1.0)
+
+
 def test_c3_full_size_properties():
     """BASELINE config 3 at n=4096: every step keeps F = I - G A (row-sampled) and the
     Richardson mismatch contracts; counters follow the reference DAG (6 mmm + 2 mvm)."""
