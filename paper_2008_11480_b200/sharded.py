@@ -59,8 +59,13 @@ class RowComm:
         self.bytes_gathered = 0
 
     def all_gather_rows(self, local: torch.Tensor) -> torch.Tensor:
+        return self.finish(self.start_gather(local))
+
+    def start_gather(self, local: torch.Tensor):
+        """Launch the all-gather of a row block (asynchronous on NCCL's stream);
+        ``finish`` makes the caller's stream wait and returns the full matrix."""
         if self.world == 1:
-            return local
+            return (None, local)
         cols = local.shape[1]
         rows = local.shape[0]
         if rows < self.pad:
@@ -69,8 +74,15 @@ class RowComm:
         else:
             padded = local.contiguous()
         out = torch.empty((self.world * self.pad, cols), dtype=local.dtype, device=local.device)
-        self.dist.all_gather_into_tensor(out, padded, group=self.group)
+        work = self.dist.all_gather_into_tensor(out, padded, group=self.group, async_op=True)
         self.bytes_gathered += out.numel() * out.element_size()
+        return (work, out)
+
+    def finish(self, pending) -> torch.Tensor:
+        work, out = pending
+        if work is None:
+            return out
+        work.wait()
         if all(r1 - r0 == self.pad for r0, r1 in self.splits):
             return out
         return torch.cat([out[p * self.pad:p * self.pad + (r1 - r0)]
@@ -118,15 +130,24 @@ class Sharded:
     t: torch.Tensor
     full: bool
     _gathered: torch.Tensor | None = None
+    _pending: tuple | None = None
 
 
 class ShardedEngine:
-    """Evaluators and steps on block-row sharded values."""
+    """Evaluators and steps on block-row sharded values.
 
-    def __init__(self, comm: RowComm, ops=None, ctr: MulCounter | None = None):
+    With ``prefetch`` (default) every product result that may serve as a right
+    operand starts its all-gather as soon as it is produced, on NCCL's stream,
+    so the transfer overlaps the products that follow; the first consumer waits
+    on it.  Residuals ``I - X A`` are only ever left operands and are not
+    gathered."""
+
+    def __init__(self, comm: RowComm, ops=None, ctr: MulCounter | None = None,
+                 prefetch: bool = True):
         self.comm = comm
         self.ops = ops if ops is not None else CudaOps()
         self.ctr = ctr if ctr is not None else MulCounter()
+        self.prefetch = prefetch
 
     # -- value helpers ------------------------------------------------------
     def rows_of(self, v: Sharded) -> torch.Tensor:
@@ -136,8 +157,16 @@ class ShardedEngine:
         if v.full:
             return v.t
         if v._gathered is None:
-            v._gathered = self.comm.all_gather_rows(v.t)
+            pending = v._pending if v._pending is not None else self.comm.start_gather(v.t)
+            v._gathered = self.comm.finish(pending)
+            v._pending = None
         return v._gathered
+
+    def _produced(self, t: torch.Tensor, gather: bool) -> Sharded:
+        v = Sharded(t, False)
+        if gather and self.prefetch and self.comm.world > 1:
+            v._pending = self.comm.start_gather(t)
+        return v
 
     def replicated(self, t: torch.Tensor) -> Sharded:
         return Sharded(t, True)
@@ -146,14 +175,14 @@ class ShardedEngine:
         return Sharded(t, False)
 
     def mm(self, lhs: Sharded, rhs: Sharded, alpha=1.0, c: Sharded | None = None, beta=0.0,
-           diag=0.0, mv=False) -> Sharded:
+           diag=0.0, mv=False, gather: bool = True) -> Sharded:
         out = self.ops.gemm(self.rows_of(lhs), self.full_of(rhs), alpha,
                             self.rows_of(c) if c is not None else None, beta, diag, self.comm.r0,
                             mv, self.ctr)
-        return Sharded(out, False)
+        return self._produced(out, gather and not mv)
 
-    def residual(self, x: Sharded, a: Sharded) -> Sharded:
-        return self.mm(x, a, alpha=-1.0, diag=1.0)
+    def residual(self, x: Sharded, a: Sharded, gather: bool = True) -> Sharded:
+        return self.mm(x, a, alpha=-1.0, diag=1.0, gather=gather)
 
     def lin(self, cdiag: float, terms, like: Sharded) -> Sharded:
         rows = self.comm.r1 - self.comm.r0
@@ -260,13 +289,13 @@ class ShardedEngine:
             r_c = self.mm(r_c, gs[i])
         nsp = self.horner(f, g, order_n)
         g_new = self.mm(r_c, nsp, c=t_c, beta=1.0)
-        f_new = self.residual(g_new, a)
+        f_new = self.residual(g_new, a, gather=False)  # F is only ever a left operand
         return g_new, f_new
 
     def ns_step(self, g: Sharded, f: Sharded, a: Sharded, order: int, plan=None):
         """newton_schulz.py:150-174 on row blocks."""
         new = self.horner(f, g, order) if plan is None else self.eval_node(plan, f, g, a)
-        return new, self.residual(new, a)
+        return new, self.residual(new, a, gather=False)
 
     def plain_richardson(self, theta: Sharded, p: Sharded, a: Sharded, b: Sharded) -> Sharded:
         """theta - P (A theta - b) with replicated theta/b; returns the
