@@ -153,6 +153,18 @@ SI_API int si_composite_step(si_handle h, int64_t n, const double* a, const doub
                       const int64_t* plan_offsets, const double* consts, int64_t nconsts,
                       int order_n, int concurrent, double* g_out, double* f_out,
                       int64_t* counters, void* stream);
+/* Opt-in hoisting (NOT the reference DAG, which recomputes the parts every
+ * step): the state-independent half of composite_step (newton_schulz.py:
+ * 204-216) -> T_comp, R_comp; and the state-dependent half (:218-220) that
+ * consumes them: G' = T_comp + R_comp S_n(F) G, F' = I - G' A. */
+SI_API int si_composite_parts(si_handle h, int64_t n, const double* a, const double* precond,
+                              const double* residual, const double* split_matrix, int nrates,
+                              const int32_t* rates, const int32_t* plans,
+                              const int64_t* plan_offsets, const double* consts, int64_t nconsts,
+                              double* t_out, double* r_out, int64_t* counters, void* stream);
+SI_API int si_composite_apply(si_handle h, int64_t n, const double* a, const double* g,
+                              const double* f, const double* t, const double* r, int order_n,
+                              double* g_out, double* f_out, int64_t* counters, void* stream);
 /* initial_double (newton_schulz.py:231-251) */
 SI_API int si_initial_double(si_handle h, int64_t n, const double* precond, const double* residual,
                       const double* a, int p, int w, int order, double* g_out, double* f_out,

@@ -377,6 +377,43 @@ int si_composite_step(si_handle h, int64_t n, const double* a, const double* g, 
   });
 }
 
+int si_composite_parts(si_handle h, int64_t n, const double* a, const double* precond,
+                       const double* residual, const double* split_matrix, int nrates,
+                       const int32_t* rates, const int32_t* plans, const int64_t* plan_offsets,
+                       const double* consts, int64_t nconsts, double* t_out, double* r_out,
+                       int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && precond && residual && split_matrix && t_out && r_out, "null pointer");
+    need(nrates >= 1 && rates, "composite spec needs at least one rate");
+    std::vector<int> rv(rates, rates + nrates);
+    std::vector<PlanPtr> owned(nrates);
+    std::vector<const PlanNode*> pv(nrates, nullptr);
+    for (int i = 0; i < nrates; ++i) {
+      need(rv[i] >= 1, "rates must be positive integers");
+      if (plans && plan_offsets && plan_offsets[i + 1] > plan_offsets[i]) {
+        owned[i] = decode_plan(plans + plan_offsets[i], plan_offsets[i + 1] - plan_offsets[i],
+                               consts, nconsts);
+        pv[i] = owned[i].get();
+      }
+    }
+    Call call(h, stream, counters);
+    composite_parts(call.c, sq(a, n), sq(precond, n), sq(residual, n), sq(split_matrix, n), rv, pv,
+                    sq(t_out, n), sq(r_out, n));
+  });
+}
+
+int si_composite_apply(si_handle h, int64_t n, const double* a, const double* g, const double* f,
+                       const double* t, const double* r, int order_n, double* g_out,
+                       double* f_out, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && g && f && t && r && g_out && f_out, "null pointer");
+    need(order_n >= 1, "order_n must be >= 1");
+    Call call(h, stream, counters);
+    composite_apply(call.c, sq(a, n), sq(g, n), sq(f, n), sq(t, n), sq(r, n), order_n,
+                    sq(g_out, n), sq(f_out, n));
+  });
+}
+
 int si_initial_double(si_handle h, int64_t n, const double* precond, const double* residual,
                       const double* a, int p, int w, int order, double* g_out, double* f_out,
                       double* l_out, double* r_out, int64_t* counters, void* stream) {

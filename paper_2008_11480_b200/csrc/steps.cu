@@ -79,6 +79,44 @@ void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, 
   residual_into(c, Fout, Gout, A);
 }
 
+// Opt-in hoisting (not in the reference, which recomputes them every step):
+// the state-independent half of composite_step (ns:204-216), T_comp and R_comp.
+void composite_parts(Ctx& c, const MV& A, const MV& P, const MV& B, const MV& Sm,
+                     const std::vector<int>& rates, const std::vector<const PlanNode*>& plans,
+                     const MV& Tout, const MV& Rout) {
+  if (rates.empty()) throw Error(kEInval, "composite spec needs at least one rate");
+  MV t, r;
+  for (size_t i = 0; i < rates.size(); ++i) {
+    if (rates[i] < 1) throw Error(kEInval, "rates must be positive integers");
+    MV ti;
+    if (rates[i] == 1) {
+      ti = alloc(c, P.v.rows, P.v.cols);
+      copy_into(c, ti, P);
+    } else {
+      ti = geometric(c, B, P, rates[i], Sm, plans[i]);
+    }
+    MV gi = residual(c, ti, A);
+    if (i == 0) {
+      t = ti;
+      r = gi;
+    } else {
+      t = gemm_new(c, r, ti, 1.0, &t, 1.0);
+      r = gemm_new(c, r, gi);
+    }
+  }
+  copy_into(c, Tout, t);
+  copy_into(c, Rout, r);
+}
+
+// The state-dependent half (ns:218-220) with hoisted T_comp / R_comp.
+void composite_apply(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& T, const MV& R,
+                     int order_n, const MV& Gout, const MV& Fout) {
+  if (order_n < 1) throw Error(kEInval, "order_n must be >= 1");
+  MV nsp = horner(c, F, G, order_n);
+  gemm(c, Gout, R, nsp, 1.0, &T, 1.0);
+  residual_into(c, Fout, Gout, A);
+}
+
 // ns:231-251
 void initial_double(Ctx& c, const MV& P, const MV& B, const MV& A, int p, int w, int order,
                     const MV& Gout, const MV& Fout, const MV& Lout, const MV& Rout) {

@@ -13,6 +13,11 @@ void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, 
                     const MV& Sm, const std::vector<int>& rates,
                     const std::vector<const PlanNode*>& plans, int order_n, bool concurrent,
                     const MV& Gout, const MV& Fout);
+void composite_parts(Ctx& c, const MV& A, const MV& P, const MV& B, const MV& Sm,
+                     const std::vector<int>& rates, const std::vector<const PlanNode*>& plans,
+                     const MV& Tout, const MV& Rout);
+void composite_apply(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& T, const MV& R,
+                     int order_n, const MV& Gout, const MV& Fout);
 void initial_double(Ctx& c, const MV& P, const MV& B, const MV& A, int p, int w, int order,
                     const MV& Gout, const MV& Fout, const MV& Lout, const MV& Rout);
 void double_ns_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& L, const MV& R,

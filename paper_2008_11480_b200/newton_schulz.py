@@ -21,7 +21,9 @@ from .series_toolkit import FactorPlan, encode_many, encode_plan, geometric_base
 from .splitting import Splitting
 
 __all__ = [
+    "CompositeParts",
     "CompositeSpec",
+    "composite_parts",
     "DoubleNsState",
     "NsState",
     "additive_correction_step",
@@ -149,17 +151,59 @@ def ns_step(st: NsState, a, plan: FactorPlan | None = None) -> NsState:
                    series_order=st.series_order, ctr=st.ctr)
 
 
+@dataclass
+class CompositeParts:
+    """Hoisted state-independent half of the composite step (opt-in; the
+    reference recomputes it every step): T_comp and R_comp (newton_schulz.py:204-216)."""
+
+    t_comp: torch.Tensor
+    r_comp: torch.Tensor
+    rates: tuple[int, ...]
+
+
+def composite_parts(a, split: Splitting, spec: CompositeSpec, ctr: MulCounter) -> CompositeParts:
+    """Evaluate the parts T_i, Gamma_i and their left fold once (opt-in hoisting)."""
+    a = as_device(a)
+    plans = [geometric_base_plan(x) if x > 1 else None for x in spec.rates]
+    code, offsets, consts = encode_many(plans)
+    t = torch.empty_like(a)
+    r = torch.empty_like(a)
+    h, s = _ctx(a)
+    buf = _lib.counter_buf()
+    _lib.call("si_composite_parts", h, a.shape[0], a.data_ptr(), split.precond.data_ptr(),
+              split.residual.data_ptr(), split.matrix.data_ptr(), len(spec.rates),
+              _lib.i32_array(list(spec.rates)), _lib.i32_array(code), _lib.i64_array(offsets),
+              _lib.f64_array(consts), len(consts), t.data_ptr(), r.data_ptr(), buf, s)
+    ctr.absorb(buf)
+    return CompositeParts(t_comp=t, r_comp=r, rates=tuple(spec.rates))
+
+
 def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_n: int,
-                   executor=None) -> NsState:
+                   executor=None, parts: CompositeParts | None = None) -> NsState:
     """G_k = T_comp + R_comp S_n(F) G, F_k = I - G_k A (newton_schulz.py:177-228).
 
     ``executor`` (not in the reference signature, whose parts run serially)
-    evaluates the independent parts on concurrent streams."""
+    evaluates the independent parts on concurrent streams.  ``parts`` (opt-in,
+    changes the GEMM count) reuses hoisted T_comp / R_comp from
+    :func:`composite_parts` instead of recomputing them."""
     if order_n < 1:
         raise ValueError("order_n must be >= 1")
     a = as_device(a)
     if a.shape != st.estimate.shape:
         raise ValueError("dimension mismatch between state and matrix")
+    if parts is not None:
+        if tuple(parts.rates) != tuple(spec.rates):
+            raise ValueError("hoisted parts were built for different rates")
+        g = torch.empty_like(st.estimate)
+        f = torch.empty_like(st.estimate)
+        h, s = _ctx(g)
+        buf = _lib.counter_buf()
+        _lib.call("si_composite_apply", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
+                  st.residual.data_ptr(), parts.t_comp.data_ptr(), parts.r_comp.data_ptr(),
+                  order_n, g.data_ptr(), f.data_ptr(), buf, s)
+        st.ctr.absorb(buf)
+        return NsState(estimate=g, residual=f, step=st.step + 1, order=order_n,
+                       series_order=st.series_order, ctr=st.ctr)
     plans = [geometric_base_plan(x) if x > 1 else None for x in spec.rates]
     code, offsets, consts = encode_many(plans)
     g = torch.empty_like(st.estimate)

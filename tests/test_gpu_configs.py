@@ -80,3 +80,27 @@ def test_c5_recipe_n768_20_iterations(variant):
     else:
         # first call builds the carried weight with Horner (16), then 18 per step
         assert steps_mmm[0] == 16 + 18 and all(s == 18 for s in steps_mmm[1:])
+
+
+def test_hoisted_composite_parts_bitwise():
+    """Opt-in hoisting evaluates the same T_comp / R_comp DAG once: the steps are
+    bitwise identical to the reference-faithful recompute, at 3 products per step
+    (order_n = 2) instead of 22."""
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import configs
+
+    a, _ = configs.c4_householder(n=640, rhs=1)
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False)
+    spec = P.CompositeSpec((2, 3, 4, 5))
+    s1 = P.initial_series(sp, 0, 1, order=2)
+    s2 = P.initial_series(sp, 0, 1, order=2)
+    parts = P.composite_parts(sp.matrix, sp, spec, s2.ctr)
+    assert s2.ctr.mmm == 19
+    for _ in range(3):
+        s1 = P.composite_step(s1, sp.matrix, sp, spec, 2)
+        c0 = s2.ctr.mmm
+        s2 = P.composite_step(s2, sp.matrix, sp, spec, 2, parts=parts)
+        assert s2.ctr.mmm - c0 == 3
+        assert torch.equal(s1.estimate, s2.estimate) and torch.equal(s1.residual, s2.residual)
+    with pytest.raises(ValueError):
+        P.composite_step(s2, sp.matrix, sp, P.CompositeSpec((2, 3)), 2, parts=parts)
