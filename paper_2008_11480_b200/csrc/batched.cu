@@ -318,11 +318,17 @@ template <int NP>
 __device__ void load_mat(double* dst, const double* __restrict__ src, int n) {
   using G = Geo<NP>;
   if (n == NP) {
+    // all of this thread's 16-byte loads in flight before the first store
+    constexpr int PER = NP * NP / 2 / G::THREADS;
     const double2* s2 = reinterpret_cast<const double2*>(src);
-    for (int i = threadIdx.x; i < NP * NP / 2; i += G::THREADS) {
-      const double2 v = __ldg(s2 + i);
+    double2 v[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) v[j] = __ldg(s2 + threadIdx.x + j * G::THREADS);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int i = threadIdx.x + j * G::THREADS;
       const int r = (2 * i) / NP, c = (2 * i) % NP;  // c even: one swizzled chunk
-      *reinterpret_cast<double2*>(dst + G::idx(r, c)) = v;
+      *reinterpret_cast<double2*>(dst + G::idx(r, c)) = v[j];
     }
   } else {
     for (int i = threadIdx.x; i < NP * NP; i += G::THREADS) {
@@ -344,6 +350,64 @@ __device__ void store_mat(double* __restrict__ dst, const double* src, int n) {
   } else {
     for (int i = threadIdx.x; i < n * n; i += G::THREADS) dst[i] = src[G::idx(i / n, i % n)];
   }
+}
+
+// One NP x NP x NP product of a recorded op by the whole CTA.  MODE: 0 = A@B,
+// 1 = I - A@B, 2 = A@B + C, 3 = generic alpha/beta/diag epilogue.
+template <int NP, int MODE>
+__device__ __forceinline__ void gemm_op(const double* A, const double* B, const double* C,
+                                        double* D, const BOp& o, int n, int warp, int g, int t) {
+  using G = Geo<NP>;
+  const int r0 = (warp >> 1) * G::WROWS, c0 = (warp & 1) * G::WCOLS;
+  // two accumulator sets (even / odd k-steps): dependent DMMA chains of NP/8
+  // instead of NP/4, combined once in a fixed order
+  double acc[2][G::MT][G::NT][2] = {};
+  double af[2][G::MT], bf[2][G::NT];
+#pragma unroll
+  for (int mi = 0; mi < G::MT; ++mi) af[0][mi] = A[G::idx(r0 + mi * 8 + g, t)];
+#pragma unroll
+  for (int ni = 0; ni < G::NT; ++ni) bf[0][ni] = B[G::idx(t, c0 + ni * 8 + g)];
+#pragma unroll
+  for (int kk = 0; kk < NP; kk += 4) {
+    const int cur = (kk >> 2) & 1, nxt = cur ^ 1;
+    if (kk + 4 < NP) {  // fragments of the next k-step in flight during this one
+#pragma unroll
+      for (int mi = 0; mi < G::MT; ++mi) af[nxt][mi] = A[G::idx(r0 + mi * 8 + g, kk + 4 + t)];
+#pragma unroll
+      for (int ni = 0; ni < G::NT; ++ni) bf[nxt][ni] = B[G::idx(kk + 4 + t, c0 + ni * 8 + g)];
+    }
+#pragma unroll
+    for (int mi = 0; mi < G::MT; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < G::NT; ++ni)
+        dmma(acc[cur][mi][ni][0], acc[cur][mi][ni][1], af[cur][mi], bf[cur][ni]);
+  }
+#pragma unroll
+  for (int mi = 0; mi < G::MT; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < G::NT; ++ni) {
+      const int row = r0 + mi * 8 + g, col = c0 + ni * 8 + 2 * t;
+      double v0 = __dadd_rn(acc[0][mi][ni][0], acc[1][mi][ni][0]);
+      double v1 = __dadd_rn(acc[0][mi][ni][1], acc[1][mi][ni][1]);
+      if (MODE == 1) {
+        v0 = (row == col && row < n) ? __dsub_rn(1.0, v0) : -v0;
+        v1 = (row == col + 1 && row < n) ? __dsub_rn(1.0, v1) : -v1;
+      } else if (MODE == 2) {
+        const double2 cv = *reinterpret_cast<const double2*>(C + G::idx(row, col));
+        v0 = __dadd_rn(v0, cv.x);
+        v1 = __dadd_rn(v1, cv.y);
+      } else if (MODE == 3) {
+        double2 cv = make_double2(0.0, 0.0);
+        if (C) cv = *reinterpret_cast<const double2*>(C + G::idx(row, col));
+        v0 = epi(v0, o.alpha, o.beta, cv.x);
+        v1 = epi(v1, o.alpha, o.beta, cv.y);
+        if (o.diag != 0.0 && row < n) {
+          if (row == col) v0 = __dadd_rn(v0, o.diag);
+          if (row == col + 1) v1 = __dadd_rn(v1, o.diag);
+        }
+      }
+      *reinterpret_cast<double2*>(D + G::idx(row, col)) = make_double2(v0, v1);
+    }
 }
 
 template <int NP>
@@ -379,39 +443,16 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS) resident_kernel(BatchArgs p)
           const double* B = mslot(o.b);
           const double* C = o.c >= 0 ? mslot(o.c) : nullptr;
           double* D = mslot(o.dst);
-          const int r0 = (warp >> 1) * G::WROWS, c0 = (warp & 1) * G::WCOLS;
-          // two accumulator sets (even / odd k-steps): dependent DMMA chains of
-          // NP/8 instead of NP/4, combined once in a fixed order
-          double acc[2][G::MT][G::NT][2] = {};
-#pragma unroll
-          for (int kk = 0; kk < NP; kk += 4) {
-            double af[G::MT], bf[G::NT];
-#pragma unroll
-            for (int mi = 0; mi < G::MT; ++mi) af[mi] = A[G::idx(r0 + mi * 8 + g, kk + t)];
-#pragma unroll
-            for (int ni = 0; ni < G::NT; ++ni) bf[ni] = B[G::idx(kk + t, c0 + ni * 8 + g)];
-            const int h = (kk >> 2) & 1;
-#pragma unroll
-            for (int mi = 0; mi < G::MT; ++mi)
-#pragma unroll
-              for (int ni = 0; ni < G::NT; ++ni)
-                dmma(acc[h][mi][ni][0], acc[h][mi][ni][1], af[mi], bf[ni]);
-          }
-#pragma unroll
-          for (int mi = 0; mi < G::MT; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < G::NT; ++ni) {
-              const int row = r0 + mi * 8 + g, col = c0 + ni * 8 + 2 * t;
-              double2 cv = make_double2(0.0, 0.0);
-              if (C) cv = *reinterpret_cast<const double2*>(C + G::idx(row, col));
-              double v0 = epi(__dadd_rn(acc[0][mi][ni][0], acc[1][mi][ni][0]), o.alpha, o.beta, cv.x);
-              double v1 = epi(__dadd_rn(acc[0][mi][ni][1], acc[1][mi][ni][1]), o.alpha, o.beta, cv.y);
-              if (o.diag != 0.0 && row < n) {
-                if (row == col) v0 = __dadd_rn(v0, o.diag);
-                if (row == col + 1) v1 = __dadd_rn(v1, o.diag);
-              }
-              *reinterpret_cast<double2*>(D + G::idx(row, col)) = make_double2(v0, v1);
-            }
+          // the DAG's epilogues are "X@Y", "I - X@Y" and "X@Y + Z": specialised,
+          // anything else goes through the generic path
+          if (!C && o.alpha == 1.0 && o.diag == 0.0)
+            gemm_op<NP, 0>(A, B, C, D, o, n, warp, g, t);
+          else if (!C && o.alpha == -1.0 && o.diag == 1.0)
+            gemm_op<NP, 1>(A, B, C, D, o, n, warp, g, t);
+          else if (C && o.alpha == 1.0 && o.beta == 1.0 && o.diag == 0.0)
+            gemm_op<NP, 2>(A, B, C, D, o, n, warp, g, t);
+          else
+            gemm_op<NP, 3>(A, B, C, D, o, n, warp, g, t);
         } else if (o.kind == OP_GEMV) {
           // every warp takes NP / WARPS rows; lanes split k, fixed-order shuffle sum
           const double* A = mslot(o.a);
