@@ -15,7 +15,8 @@ from ctypes import POINTER, c_double, c_int, c_int32, c_int64, c_void_p
 import torch
 
 LIB_NAME = "libseriesinv_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("SI_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 SI_OK, SI_EINVAL, SI_ECUDA, SI_ENOMEM = 0, -1, -2, -3
 

@@ -17,6 +17,8 @@
 // then the minimum 2 wavefronts, and slots are 8 KB (NP=32) / 32 KB (NP=64),
 // so three 32 x 32 systems fit per SM.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "batched.hpp"
 
@@ -292,6 +294,8 @@ struct BatchArgs {
   int n;
   int iters;
   int64_t batch;
+  int has_load;            // the program streams S^-1 / B in (OP_LOAD)
+  long long* prof;         // per-op cycle totals of CTA 0 (diagnostics; usually null)
   int sA, sG, sF, sT, sb;  // slots of A, the carried inputs, b
   int rG, rF, rT;          // slots of the carried outputs (copied back when different)
 };
@@ -299,7 +303,15 @@ struct BatchArgs {
 template <int NP>
 struct Geo {
   static constexpr int SLOT = NP * NP;
-  static constexpr int WARPS = NP == 32 ? 4 : 8;
+#ifndef SI_RESIDENT_WARPS32
+#define SI_RESIDENT_WARPS32 8
+#endif
+#ifndef SI_RESIDENT_WARPS64
+#define SI_RESIDENT_WARPS64 16
+#endif
+  // more warps than DMMA tiles per op would need: the ops are short dependent
+  // chains, so latency (not issue) bounds them and extra warps hide it
+  static constexpr int WARPS = NP == 32 ? SI_RESIDENT_WARPS32 : SI_RESIDENT_WARPS64;
   static constexpr int THREADS = WARPS * 32;
   static constexpr int WROWS = NP / (WARPS / 2);  // warp tile rows (16)
   static constexpr int WCOLS = NP / 2;             // warp tile cols (16 or 32)
@@ -411,7 +423,9 @@ __device__ __forceinline__ void gemm_op(const double* A, const double* B, const 
 }
 
 template <int NP>
-__global__ void __launch_bounds__(Geo<NP>::THREADS) resident_kernel(BatchArgs p) {
+// 32 x 32 systems: three CTAs per SM fit in shared memory, so registers must
+// not be the tighter limit
+__global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? 3 : 1) resident_kernel(BatchArgs p) {
   using G = Geo<NP>;
   extern __shared__ double sm[];
   // dynamic shared memory: [matrix slots][vector slots][program]
@@ -421,6 +435,10 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS) resident_kernel(BatchArgs p)
   const int n = p.n;
   const int64_t nn = (int64_t)n * n;
   auto mslot = [&](int s) { return sm + (size_t)s * G::SLOT; };
+  __shared__ long long prof_acc[kMaxOps];  // SI_RESIDENT_PROF diagnostics (CTA 0, thread 0)
+  long long prof_last = clock64();
+  if (p.prof && threadIdx.x == 0)
+    for (int k = 0; k < kMaxOps; ++k) prof_acc[k] = 0;
   auto vslot = [&](int s) { return sm + (size_t)p.nmat * G::SLOT + (size_t)s * NP; };
   for (int i = threadIdx.x; i < p.nops * (int)sizeof(BOp) / 4; i += G::THREADS)
     reinterpret_cast<int*>(prog)[i] = reinterpret_cast<const int*>(p.ops)[i];
@@ -435,10 +453,33 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS) resident_kernel(BatchArgs p)
       vslot(p.sb)[threadIdx.x] = threadIdx.x < n ? p.b[sys * n + threadIdx.x] : 0.0;
     }
     __syncthreads();
+    // S^-1 and B are streamed in every iteration; their global loads are issued
+    // into registers at the top of the iteration so the latency hides behind
+    // the ops that precede the LOAD ops (full-size systems only)
+    constexpr int PF = NP * NP / 2 / G::THREADS;
+    const bool prefetch = p.has_load && n == NP && PF >= 1;
+    double2 pf_p[PF > 0 ? PF : 1], pf_b[PF > 0 ? PF : 1];
     for (int it = 0; it < p.iters; ++it) {
+      if (prefetch) {
+        const double2* sp2 = reinterpret_cast<const double2*>(p.precond + sys * nn);
+        const double2* sb2 = reinterpret_cast<const double2*>(p.residual + sys * nn);
+#pragma unroll
+        for (int j = 0; j < PF; ++j) {
+          pf_p[j] = __ldg(sp2 + threadIdx.x + j * G::THREADS);
+          pf_b[j] = __ldg(sb2 + threadIdx.x + j * G::THREADS);
+        }
+      }
       for (int k = 0; k < p.nops; ++k) {
         const BOp& o = prog[k];
-        if (o.kind == OP_GEMM) {
+        if (o.kind == OP_LOAD && prefetch) {
+          double* dst = mslot(o.dst);
+#pragma unroll
+          for (int j = 0; j < PF; ++j) {
+            const int i = threadIdx.x + j * G::THREADS;
+            const int r = (2 * i) / NP, c = (2 * i) % NP;
+            *reinterpret_cast<double2*>(dst + G::idx(r, c)) = o.vec ? pf_b[j] : pf_p[j];
+          }
+        } else if (o.kind == OP_GEMM) {
           const double* A = mslot(o.a);
           const double* B = mslot(o.b);
           const double* C = o.c >= 0 ? mslot(o.c) : nullptr;
@@ -454,19 +495,24 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS) resident_kernel(BatchArgs p)
           else
             gemm_op<NP, 3>(A, B, C, D, o, n, warp, g, t);
         } else if (o.kind == OP_GEMV) {
-          // every warp takes NP / WARPS rows; lanes split k, fixed-order shuffle sum
-          const double* A = mslot(o.a);
-          const double* x = vslot(o.b);
-          constexpr int RPW = NP / G::WARPS;
+          // On the DMMA pipe, not the FP64 ALU: x becomes column 0 of an 8-wide B
+          // fragment (zeros elsewhere).  A DFMA + shuffle-tree GEMV contends with
+          // the other resident CTAs' DMMAs and was 2.5x slower than a full GEMM op.
+          if (warp < NP / 8) {
+            const double* A = mslot(o.a);
+            const double* x = vslot(o.b);
+            const int r0 = warp * 8;
+            double acc[2][2] = {};
 #pragma unroll
-          for (int rr = 0; rr < RPW; ++rr) {
-            const int row = warp * RPW + rr;
-            double s = 0.0;
-#pragma unroll
-            for (int kk = lane; kk < NP; kk += 32) s = fma(A[G::idx(row, kk)], x[kk], s);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-            if (lane == 0) {
+            for (int kk = 0; kk < NP; kk += 4) {
+              const double af = A[G::idx(r0 + g, kk + t)];
+              const double bf = g == 0 ? x[kk + t] : 0.0;
+              const int h = (kk >> 2) & 1;
+              dmma(acc[h][0], acc[h][1], af, bf);
+            }
+            if (t == 0) {  // lane (g, 0) holds row r0 + g, column 0
+              const int row = r0 + g;
+              const double s = __dadd_rn(acc[0][0], acc[1][0]);
               const double cv = o.c >= 0 ? vslot(o.c)[row] : 0.0;
               vslot(o.dst)[row] = epi(s, o.alpha, o.beta, cv);
             }
@@ -496,6 +542,11 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS) resident_kernel(BatchArgs p)
           }
         }
         __syncthreads();
+        if (p.prof && blockIdx.x == 0 && threadIdx.x == 0) {  // SI_RESIDENT_PROF diagnostics
+          const long long now = clock64();
+          prof_acc[k] += now - prof_last;
+          prof_last = now;
+        }
       }
       // carry the state where the allocator could not place it in place
       if (p.rG != p.sG || p.rF != p.sF) {
@@ -512,6 +563,8 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS) resident_kernel(BatchArgs p)
     if (threadIdx.x < n) p.theta_io[sys * n + threadIdx.x] = vslot(p.sT)[threadIdx.x];
     __syncthreads();
   }
+  if (p.prof && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int k = 0; k < p.nops; ++k) p.prof[k] = prof_acc[k];
 }
 
 int num_sms_b() {
@@ -596,6 +649,8 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
   args.n = (int)n;
   args.iters = iters;
   args.batch = batch;
+  args.has_load = 0;
+  for (const BOp& o : ops) args.has_load |= (o.kind == OP_LOAD);
   args.sA = al.phys[q.A];
   args.sG = al.phys[q.G];
   args.sF = al.phys[q.F];
@@ -613,7 +668,29 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
         "occupancy");
   if (per_sm < 1) throw Error(kEInval, "resident kernel does not fit on an SM");
   const int64_t grid = std::min<int64_t>(batch, (int64_t)num_sms_b() * per_sm);
+  long long* prof = nullptr;
+  const bool want_prof = std::getenv("SI_RESIDENT_PROF") != nullptr;
+  if (want_prof) {
+    check(cudaMalloc(&prof, sizeof(long long) * (kMaxOps + 1)), "cudaMalloc");
+    check(cudaMemset(prof, 0, sizeof(long long) * (kMaxOps + 1)), "cudaMemset");
+  }
+  args.prof = prof;
   resident_kernel<NP><<<(unsigned)grid, Gm::THREADS, smem, c.s>>>(args);
+  if (want_prof) {
+    std::vector<long long> h(kMaxOps + 1);
+    check(cudaMemcpy(h.data(), prof, sizeof(long long) * (kMaxOps + 1), cudaMemcpyDeviceToHost),
+          "memcpy");
+    cudaFree(prof);
+    const char* names[] = {"gemm", "gemv", "lin", "load"};
+    long long tot = 0;
+    for (size_t k = 0; k < ops.size(); ++k) tot += (k == 0 ? 0 : h[k]);
+    std::fprintf(stderr, "[resident] CTA0 cycles per op (grid %lld, %d CTAs/SM, smem %zu B):\n",
+                 (long long)grid, per_sm, smem);
+    for (size_t k = 0; k < ops.size(); ++k)
+      std::fprintf(stderr, "  op %2zu %-4s dst %d a %d b %d c %d: %lld\n", k, names[ops[k].kind],
+                   ops[k].dst, ops[k].a, ops[k].b, ops[k].c, h[k]);
+    std::fprintf(stderr, "  total (ops 1..) %lld\n", tot);
+  }
   check(cudaGetLastError(), "resident kernel launch");
   c.h->launches += 1;
   return per;
