@@ -163,6 +163,7 @@ class Workload:
         self.world = world
         self.hoist = hoist
         self.sharded = None
+        self.split_batch = False
         self.iters_per_step = 1
 
     # FLOPs of the executed reference DAG per step (2 M N K summed)
@@ -226,6 +227,14 @@ class Workload:
         elif cfg == "c2":
             self.batch = self.n or 16384
             a_np, b_np = configs.c2_batched(batch=self.batch)
+            if self.world > 1:
+                # independent systems: each rank takes a contiguous share, no communication
+                from paper_2008_11480_b200.sharded import row_splits
+
+                rank = int(os.environ.get("RANK", "0"))
+                lo, hi = row_splits(self.batch, self.world)[rank]
+                a_np, b_np = a_np[lo:hi], b_np[lo:hi]
+                self.split_batch = True
             self.a2, self.b2 = P.as_device(a_np), P.as_device(b_np)
             self.pre2, self.res2 = P.batched_scalar_split(self.a2)
             self.p2, self.f2 = self.pre2.clone(), self.res2.clone()
@@ -271,9 +280,29 @@ class Workload:
             self.a = None
             torch.cuda.empty_cache()
             self.plan16 = P.plan_order(16)
+            self.mmm_per_step = 18
+            if self.world > 1:
+                # block-row sharded recursive step (sharded.py) from the same initial state
+                from paper_2008_11480_b200.sharded import RowComm, ShardedEngine
+
+                comm = RowComm(self.n)
+                eng = ShardedEngine(comm)
+                rows = slice(comm.r0, comm.r1)
+                inner = self.st.inner
+                self.sharded = {
+                    "eng": eng, "comm": comm, "A": eng.replicated(self.sp.matrix),
+                    "b": eng.replicated(b), "theta": eng.replicated(self.st.theta),
+                    "state": [eng.local(m[rows].clone()) for m in
+                              (inner.estimate, inner.residual, inner.accel_estimate,
+                               inner.accel_residual)] + [None, None],
+                }
+                self.st = None
+                torch.cuda.empty_cache()
+                self.workload += f" [block-row x{self.world}]"
+                self.step()  # first recursive call builds the carried weight (untimed)
+                return
             self.st = P.richardson_recursive_step(self.st, self.sp.matrix, b,
                                                   factor_plan=self.plan16, doubling_sum=True)
-            self.mmm_per_step = 18
         else:
             order = {"c4": 2, "c3": 8, "c1": 3}[cfg]
             self.st = P.initial_series(self.sp, 0, 1, order=order)
@@ -300,6 +329,14 @@ class Workload:
                 s["a"], s["b"], s["p"], s["f"], s["t"], 3, self.iters_per_step)
             return
         if cfg == "c5":
+            if self.sharded is not None:
+                s = self.sharded
+                g, f, l, r, om, ns = s["state"]
+                g, f, l, r, om, ns, s["theta"] = s["eng"].richardson_recursive_step(
+                    g, f, l, r, om, ns, s["A"], s["theta"], s["b"], 16, factor_plan=self.plan16,
+                    doubling_sum=True)
+                s["state"] = [g, f, l, r, om, ns]
+                return
             self.st = P.richardson_recursive_step(self.st, self.sp.matrix, self.b,
                                                   factor_plan=self.plan16, doubling_sum=True)
             return
@@ -471,11 +508,11 @@ def run_ours(args):
     step_s = ms_max / 1e3 / args.steps
     # sharded (c3/c4 at N > 1): every rank works on the same job -> strong scaling;
     # otherwise N independent replicas each complete `steps` iterations -> weak
-    strong = w.sharded is not None
+    # sharded (c3/c4/c5) or batch-split (c2) at N > 1: all ranks work on ONE job of
+    # fixed size -> strong scaling; otherwise N replicas each run the job -> weak
+    strong = w.sharded is not None or w.split_batch
     value = (1 if strong else world) * args.steps * w.iters_per_step / (ms_max / 1e3)
     tflops = (1 if strong else world) * flops / step_s / 1e12
-    if strong:
-        flops = flops / world  # per-rank share, for the per-GPU fraction below
 
     peak = ctypes.c_double()
     _lib.call("si_dmma_peak", h, 20000, ctypes.byref(peak))
@@ -516,7 +553,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded PCG64 draws, SURVEY Appendix A recipe)",
             "config": {"workload": w.workload, "n": w.n,
-                       "parallelism": (f"block-row x{world} (NCCL all-gather)" if strong
+                       "parallelism": (f"block-row x{world} (NCCL all-gather)" if w.sharded is not None
+                                       else f"batch split x{world} (no communication)" if w.split_batch
                                        else (f"replicas x{world}" if world > 1 else "single-gpu")),
                        "l2": "inputs larger than L2 (2.1 GB per matrix), no flush"},
             "tflops": tflops,

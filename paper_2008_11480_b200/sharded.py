@@ -297,6 +297,58 @@ class ShardedEngine:
         new = self.horner(f, g, order) if plan is None else self.eval_node(plan, f, g, a)
         return new, self.residual(new, a, gather=False)
 
+    def identity_rows(self, like: Sharded) -> Sharded:
+        rows = self.comm.r1 - self.comm.r0
+        ref = self.rows_of(like)
+        return Sharded(self.ops.lin(1.0, self.comm.r0, [], rows, ref.shape[1], ref), False)
+
+    def power_sum(self, gamma: Sharded, n: int) -> Sharded:
+        """richardson.py:101-108 on row blocks: I + gamma + ... + gamma^(n-1)."""
+        acc = self.identity_rows(gamma)
+        cur = None
+        for _ in range(n - 1):
+            cur = gamma if cur is None else self.mm(cur, gamma, gather=False)
+            acc = self.lin(0.0, [(1.0, acc), (1.0, cur)], gamma)
+        return acc
+
+    def power_sum_doubling(self, gamma: Sharded, n: int) -> Sharded:
+        """Opt-in S_2t = S_t + gamma^t S_t (n = 2^m), as si_richardson_recursive_step."""
+        if n < 2 or n & (n - 1):
+            raise ValueError("doubling power sum needs n = 2^m >= 2")
+        s = self.lin(0.0, [(1.0, self.identity_rows(gamma)), (1.0, gamma)], gamma)
+        pw = gamma
+        t = 2
+        while t < n:
+            pw = self.mm(pw, pw)
+            s = self.mm(pw, s, c=s, beta=1.0)
+            t *= 2
+        return s
+
+    def richardson_recursive_step(self, g: Sharded, f: Sharded, l: Sharded, r: Sharded,
+                                  omega: Sharded | None, ns_part: Sharded | None, a: Sharded,
+                                  theta: Sharded, b: Sharded, order: int, factor_plan=None,
+                                  doubling_sum: bool = False):
+        """richardson.py:111-189 on row blocks (q == n).  Returns
+        (G', F', L', R', omega', ns', theta') with theta' replicated."""
+        n = order
+        if omega is None or ns_part is None:
+            ns_prev = self.horner(f, g, n)
+            om_prev = self.mm(r, ns_prev, c=l, beta=1.0)
+        else:
+            ns_prev, om_prev = ns_part, omega
+        s = self.power_sum_doubling(r, n) if doubling_sum else self.power_sum(r, n)
+        diff = self.lin(0.0, [(1.0, om_prev), (-1.0, ns_prev)], g)
+        g_new = self.mm(s, diff, c=ns_prev, beta=1.0)
+        f_new = self.residual(g_new, a, gather=False)
+        ns_new = (self.eval_node(factor_plan, f_new, g_new, a) if factor_plan is not None
+                  else self.horner(f_new, g_new, n))
+        l_new = self.mm(s, l)
+        r_new = self.residual(l_new, a)
+        om_new = self.mm(r_new, ns_new, c=l_new, beta=1.0)
+        resid = self.mm(a, theta, c=b, beta=-1.0, mv=True)
+        th = self.mm(om_new, resid, alpha=-1.0, c=theta, beta=1.0, mv=True)
+        return g_new, f_new, l_new, r_new, om_new, ns_new, Sharded(self.full_of(th), True)
+
     def plain_richardson(self, theta: Sharded, p: Sharded, a: Sharded, b: Sharded) -> Sharded:
         """theta - P (A theta - b) with replicated theta/b; returns the
         gathered (replicated) new theta."""

@@ -123,6 +123,78 @@ def test_sharded_composite_matches_oracle(world, n):
     assert gathered > 0
 
 
+def _worker_recursive(rank, world, port, outdir, n, steps, factorised):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from oracle import seriesinv_oracle as O
+    from paper_2008_11480_b200.sharded import RowComm, ShardedEngine
+    from paper_2008_11480_b200.series_toolkit import plan_order
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    a_np, b_np = _c5_like(n)
+    # initial state from the oracle (initial_richardson is setup, not the sharded step)
+    sp = O.split_scalar(a_np, O.inf_norm(a_np) / 2.0)
+    st = O.initial_richardson(sp, b_np, 0, 1, 4, 4)
+    comm = RowComm(n)
+    eng = ShardedEngine(comm, ops=CpuOps())
+    rows = slice(comm.r0, comm.r1)
+    loc = lambda m: eng.local(torch.as_tensor(m[rows]).clone())  # noqa: E731
+    g, f, l, r = (loc(m) for m in (st.inner.estimate, st.inner.residual,
+                                    st.inner.accel_estimate, st.inner.accel_residual))
+    A = eng.replicated(torch.as_tensor(sp.matrix))
+    b = eng.replicated(torch.as_tensor(b_np))
+    theta = eng.replicated(torch.as_tensor(st.theta))
+    om = ns = None
+    kw = {"factor_plan": plan_order(4), "doubling_sum": True} if factorised else {}
+    for _ in range(steps):
+        g, f, l, r, om, ns, theta = eng.richardson_recursive_step(g, f, l, r, om, ns, A, theta, b,
+                                                                   4, **kw)
+    g_full = comm.all_gather_rows(g.t)
+    om_full = comm.all_gather_rows(om.t)
+    if rank == 0:
+        np.save(os.path.join(outdir, "g.npy"), g_full.numpy())
+        np.save(os.path.join(outdir, "om.npy"), om_full.numpy())
+        np.save(os.path.join(outdir, "theta.npy"), theta.t.numpy())
+        np.save(os.path.join(outdir, "ctr.npy"), np.array([eng.ctr.mmm, eng.ctr.mvm]))
+    dist.destroy_process_group()
+
+
+def _c5_like(n):
+    rng = np.random.default_rng(5)
+    g = rng.standard_normal((n + n // 4, n))
+    a = g.T @ g / (n + n // 4) + 1e-3 * np.eye(n)
+    return (a + a.T) / 2.0, rng.standard_normal((n, 3))
+
+
+@pytest.mark.parametrize("world,n,factorised", [(2, 29, False), (3, 24, True)])
+def test_sharded_recursive_richardson_matches_oracle(world, n, factorised):
+    from oracle import seriesinv_oracle as O
+
+    steps = 3
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker_recursive, args=(world, _free_port(), d, n, steps, factorised),
+                 nprocs=world, join=True)
+        g = np.load(os.path.join(d, "g.npy"))
+        om = np.load(os.path.join(d, "om.npy"))
+        theta = np.load(os.path.join(d, "theta.npy"))
+        ctr = np.load(os.path.join(d, "ctr.npy"))
+    a, b = _c5_like(n)
+    sp = O.split_scalar(a, O.inf_norm(a) / 2.0)
+    st = O.initial_richardson(sp, b, 0, 1, 4, 4)
+    m0 = st.ctr.mmm
+    for _ in range(steps):
+        st = O.richardson_recursive_step(st, sp.matrix, b)
+    rel = lambda x, y: np.linalg.norm(x - y) / np.linalg.norm(y)  # noqa: E731
+    tol = 1e-9 if factorised else 1e-11  # factorised sums reassociate the series
+    assert rel(g, st.inner.estimate) <= tol
+    assert rel(om, st.omega) <= tol
+    assert rel(theta, st.theta) <= tol
+    if not factorised:
+        assert int(ctr[0]) == st.ctr.mmm - m0  # same DAG as the reference: 3n+2, then 2n+2
+
+
 def test_row_splits_cover():
     from paper_2008_11480_b200.sharded import row_splits
 
