@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? 3 : 1) resident_k
             D[i] = acc;
           }
         }
-        __syncthreads();
+        if (o.pad_) __syncthreads();  // elided when the next op is independent
         if (p.prof && blockIdx.x == 0 && threadIdx.x == 0) {  // SI_RESIDENT_PROF diagnostics
           const long long now = clock64();
           prof_acc[k] += now - prof_last;
@@ -625,6 +625,43 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
     o.c = ph(o.c);
     if (o.kind == OP_LIN)
       for (int j = 0; j < o.nterms; ++j) o.t[j] = ph(o.t[j]);
+  }
+  // Barrier elision: op k+1 may start before op k has finished in every warp
+  // when it neither reads a slot written since the last barrier (RAW) nor
+  // writes a slot read or written since then (WAR / WAW).  Independent ops of
+  // the DAG (e.g. Gamma_1 and the next part's first product) then overlap.
+  {
+    auto key = [&](const BOp& o, int s, bool vec) { return vec ? 1000 + s : s; };
+    std::vector<int> rd, wr;
+    auto hit = [](const std::vector<int>& v, int s) {
+      return std::find(v.begin(), v.end(), s) != v.end();
+    };
+    for (size_t k = 0; k < ops.size(); ++k) {
+      BOp& o = ops[k];
+      std::vector<int> reads, writes;
+      const bool vdst = (o.kind == OP_GEMV) || (o.kind == OP_LIN && o.vec);
+      writes.push_back(key(o, o.dst, vdst));
+      if (o.kind == OP_GEMM) {
+        reads = {key(o, o.a, false), key(o, o.b, false)};
+        if (o.c >= 0) reads.push_back(key(o, o.c, false));
+      } else if (o.kind == OP_GEMV) {
+        reads = {key(o, o.a, false), key(o, o.b, true)};
+        if (o.c >= 0) reads.push_back(key(o, o.c, true));
+      } else if (o.kind == OP_LIN) {
+        for (int j = 0; j < o.nterms; ++j) reads.push_back(key(o, o.t[j], o.vec));
+      }
+      bool need = false;
+      for (int s : reads) need |= hit(wr, s);
+      for (int s : writes) need |= hit(wr, s) || hit(rd, s);
+      if (k > 0) ops[k - 1].pad_ = need ? 1 : 0;  // barrier after the previous op
+      if (need) {
+        rd.clear();
+        wr.clear();
+      }
+      rd.insert(rd.end(), reads.begin(), reads.end());
+      wr.insert(wr.end(), writes.begin(), writes.end());
+    }
+    if (!ops.empty()) ops.back().pad_ = 1;  // end of iteration: carry copies follow
   }
   const size_t smem = (size_t)al.nmat * Gm::SLOT * sizeof(double) +
                       (size_t)al.nvec * NP * sizeof(double) + ops.size() * sizeof(BOp);
