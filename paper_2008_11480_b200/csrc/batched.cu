@@ -568,12 +568,9 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? 3 : 1) resident_k
 }
 
 int num_sms_b() {
-  static int n = 0;
-  if (!n) {
-    int d = 0;
-    cudaGetDevice(&d);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
-  }
+  int d = 0, n = 0;
+  cudaGetDevice(&d);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
   return n;
 }
 

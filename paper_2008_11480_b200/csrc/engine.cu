@@ -92,7 +92,7 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
   } else if (d.cols <= 4) {
     err = launch_gemv(A.v, B.v, d, e, c.s);
     h->launches += 1;
-  } else if (std::max(d.rows, d.cols) >= 128 && tma_eligible(A.v, B.v, d, e)) {
+  } else if (std::max(d.rows, d.cols) >= 128 && A.v.cols > 0 && tma_eligible(A.v, B.v, d, e)) {
     Handle::ProfRec rec{};
     if (h->profiling) {
       for (cudaEvent_t* ev : {&rec.start, &rec.stop}) {

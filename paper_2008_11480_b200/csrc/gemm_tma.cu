@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <mutex>
 
 namespace si {
@@ -327,12 +328,9 @@ bool make_map(CUtensorMap* map, const double* ptr, int64_t rows, int64_t cols, i
 }
 
 int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);  // cached by the runtime
   return n;
 }
 
@@ -355,12 +353,18 @@ cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& 
     set_error("cuTensorMapEncodeTiled failed");
     return cudaErrorInvalidValue;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::atomic<uint64_t> attr_set{0};  // one bit per device
+  if (dev < 64 && !(attr_set.load() & (1ull << dev))) {
     cudaError_t err = cudaFuncSetAttribute(gemm_f64_tma_kernel,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (err != cudaSuccess) return err;
-    attr_set = true;
+    attr_set.fetch_or(1ull << dev);
+  } else if (dev >= 64) {
+    cudaError_t err = cudaFuncSetAttribute(gemm_f64_tma_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (err != cudaSuccess) return err;
   }
   const int M = (int)D.rows, N = (int)D.cols, K = (int)A.cols;
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
