@@ -166,10 +166,11 @@ int si_gemm_ex(si_handle h, int64_t m, int64_t n, int64_t k, double alpha, const
                int64_t ldc, double diag, int64_t diag_offset, double* D, int64_t ldd, int is_mv,
                int64_t* counters, void* stream) {
   return guard([&] {
-    need(h && A && B && D, "null pointer");
+    // empty operands may be NULL (numpy / torch give empty arrays no storage)
+    need(h && (A || m * k == 0) && (B || k * n == 0) && (D || m * n == 0), "null pointer");
     need(m >= 0 && n >= 0 && k >= 0, "negative dimension");
     need(lda >= k && ldb >= n && ldd >= n, "leading dimension too small");
-    need(beta == 0.0 || (C && ldc >= n), "beta != 0 needs C");
+    need(beta == 0.0 || m * n == 0 || (C && ldc >= n), "beta != 0 needs C");
     Call call(h, stream, counters);
     MV a = view(const_cast<double*>(A), m, k, lda), b = view(const_cast<double*>(B), k, n, ldb);
     MV d = view(D, m, n, ldd);
