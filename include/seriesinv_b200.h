@@ -153,6 +153,21 @@ SI_API int si_composite_step(si_handle h, int64_t n, const double* a, const doub
                       const int64_t* plan_offsets, const double* consts, int64_t nconsts,
                       int order_n, int concurrent, double* g_out, double* f_out,
                       int64_t* counters, void* stream);
+/* si_composite_step with host-copy overlap: input_ready_events (may be NULL;
+ * entries may be NULL) are cudaEvent_t for {a, g, f, precond, residual,
+ * split_matrix} that the step waits on just before each input's first use
+ * (S^-1, B and the split matrix first, A at the first part residual, G and F
+ * for the NS part), so copies still in flight overlap the first products;
+ * g_done_event (may be NULL) is recorded once g_out is final, before the
+ * last product F' = I - G' A, so g_out can be read back while it runs. */
+SI_API int si_composite_step_ex(si_handle h, int64_t n, const double* a, const double* g,
+                                const double* f, const double* precond, const double* residual,
+                                const double* split_matrix, int nrates, const int32_t* rates,
+                                const int32_t* plans, const int64_t* plan_offsets,
+                                const double* consts, int64_t nconsts, int order_n,
+                                int concurrent, void* const* input_ready_events,
+                                void* g_done_event, double* g_out, double* f_out,
+                                int64_t* counters, void* stream);
 /* Opt-in hoisting (NOT the reference DAG, which recomputes the parts every
  * step): the state-independent half of composite_step (newton_schulz.py:
  * 204-216) -> T_comp, R_comp; and the state-dependent half (:218-220) that

@@ -355,6 +355,18 @@ int si_composite_step(si_handle h, int64_t n, const double* a, const double* g, 
                       const int64_t* plan_offsets, const double* consts, int64_t nconsts,
                       int order_n, int concurrent, double* g_out, double* f_out,
                       int64_t* counters, void* stream) {
+  return si_composite_step_ex(h, n, a, g, f, precond, residual, split_matrix, nrates, rates, plans,
+                              plan_offsets, consts, nconsts, order_n, concurrent, nullptr,
+                              nullptr, g_out, f_out, counters, stream);
+}
+
+int si_composite_step_ex(si_handle h, int64_t n, const double* a, const double* g,
+                         const double* f, const double* precond, const double* residual,
+                         const double* split_matrix, int nrates, const int32_t* rates,
+                         const int32_t* plans, const int64_t* plan_offsets, const double* consts,
+                         int64_t nconsts, int order_n, int concurrent,
+                         void* const* input_ready_events, void* g_done_event, double* g_out,
+                         double* f_out, int64_t* counters, void* stream) {
   return guard([&] {
     need(h && a && g && f && precond && residual && split_matrix && g_out && f_out,
          "null pointer");
@@ -371,10 +383,15 @@ int si_composite_step(si_handle h, int64_t n, const double* a, const double* g, 
         pv[i] = owned[i].get();
       }
     }
+    StepEvents ev;
+    if (input_ready_events)
+      for (int i = 0; i < StepEvents::kInputs; ++i)
+        ev.ready[i] = reinterpret_cast<cudaEvent_t>(input_ready_events[i]);
+    ev.g_done = reinterpret_cast<cudaEvent_t>(g_done_event);
     Call call(h, stream, counters);
     composite_step(call.c, sq(a, n), sq(g, n), sq(f, n), sq(precond, n), sq(residual, n),
                    sq(split_matrix, n), rv, pv, order_n, concurrent != 0, sq(g_out, n),
-                   sq(f_out, n));
+                   sq(f_out, n), &ev);
   });
 }
 

@@ -37,15 +37,32 @@ void ns_step(Ctx& c, const MV& A, const MV& G, const MV& F, int order, const Pla
 
 // ns:177-228 -- parts (T_i, Gamma_i) are independent of each other and of the
 // state; with `concurrent` each part (and the NS part) runs on its own stream.
+void StepEvents::wait(Ctx& c, int i) {
+  if (i >= 0 && i < kInputs && ready[i] && !waited[i]) {
+    check(cudaStreamWaitEvent(c.s, ready[i], 0), "cudaStreamWaitEvent");
+    waited[i] = true;
+  }
+}
+
 void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, const MV& B,
                     const MV& Sm, const std::vector<int>& rates,
                     const std::vector<const PlanNode*>& plans, int order_n, bool concurrent,
-                    const MV& Gout, const MV& Fout) {
+                    const MV& Gout, const MV& Fout, StepEvents* ev) {
   if (order_n < 1) throw Error(kEInval, "order_n must be >= 1");
   if (rates.empty()) throw Error(kEInval, "composite spec needs at least one rate");
   const size_t k = rates.size();
   std::vector<MV> ts(k), gs(k);
   MV nsp;
+  StepEvents none;
+  StepEvents& e = ev ? *ev : none;
+  if (concurrent)  // branches read every input: wait for all of them up front
+    for (int i = 0; i < StepEvents::kInputs; ++i) e.wait(c, i);
+  // serial order of first use: S^-1, B, split matrix (parts), A (their
+  // residuals), then G, F (the NS part) -- copies still in flight for the later
+  // inputs overlap the first products
+  e.wait(c, StepEvents::kPrecond);
+  e.wait(c, StepEvents::kResidual);
+  e.wait(c, StepEvents::kSplitMatrix);
   auto part = [&](Ctx& cc, size_t i) {
     if (rates[i] < 1) throw Error(kEInval, "rates must be positive integers");
     if (rates[i] == 1) {
@@ -54,6 +71,7 @@ void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, 
     } else {
       ts[i] = geometric(cc, B, P, rates[i], Sm, plans[i]);
     }
+    e.wait(cc, StepEvents::kA);
     gs[i] = residual(cc, ts[i], A);
   };
   if (concurrent) {
@@ -74,8 +92,13 @@ void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, 
     t = gemm_new(c, r, ts[i], 1.0, &t, 1.0);  // t + r T_i
     r = gemm_new(c, r, gs[i]);                // r Gamma_i
   }
-  if (!concurrent) nsp = horner(c, F, G, order_n);
+  if (!concurrent) {
+    e.wait(c, StepEvents::kF);
+    e.wait(c, StepEvents::kG);
+    nsp = horner(c, F, G, order_n);
+  }
   gemm(c, Gout, r, nsp, 1.0, &t, 1.0);  // G = t + r ns
+  if (e.g_done) check(cudaEventRecord(e.g_done, c.s), "cudaEventRecord");  // G' may go D2H now
   residual_into(c, Fout, Gout, A);
 }
 

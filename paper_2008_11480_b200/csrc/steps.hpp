@@ -9,10 +9,20 @@ void initial_series(Ctx& c, const MV& P, const MV& B, const MV& A, int p, int w,
                     const MV& Fout);
 void ns_step(Ctx& c, const MV& A, const MV& G, const MV& F, int order, const PlanNode* plan,
              const MV& Gout, const MV& Fout);
+// Optional per-input readiness (e.g. host->device copies still in flight on a
+// copy stream): the step waits on each event just before the input's first
+// use, and records g_done once G' is final (before F' = I - G' A).
+struct StepEvents {
+  enum { kA = 0, kG, kF, kPrecond, kResidual, kSplitMatrix, kInputs };
+  cudaEvent_t ready[kInputs] = {};
+  bool waited[kInputs] = {};
+  cudaEvent_t g_done = nullptr;
+  void wait(Ctx& c, int i);
+};
 void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, const MV& B,
                     const MV& Sm, const std::vector<int>& rates,
                     const std::vector<const PlanNode*>& plans, int order_n, bool concurrent,
-                    const MV& Gout, const MV& Fout);
+                    const MV& Gout, const MV& Fout, StepEvents* ev = nullptr);
 void composite_parts(Ctx& c, const MV& A, const MV& P, const MV& B, const MV& Sm,
                      const std::vector<int>& rates, const std::vector<const PlanNode*>& plans,
                      const MV& Tout, const MV& Rout);

@@ -10,6 +10,7 @@ here unchanged in meaning.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from math import sqrt
 
@@ -178,14 +179,24 @@ def composite_parts(a, split: Splitting, spec: CompositeSpec, ctr: MulCounter) -
     return CompositeParts(t_comp=t, r_comp=r, rates=tuple(spec.rates))
 
 
+_READY_ORDER = ("a", "estimate", "residual", "precond", "split_residual", "matrix")
+
+
 def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_n: int,
-                   executor=None, parts: CompositeParts | None = None) -> NsState:
+                   executor=None, parts: CompositeParts | None = None, *,
+                   inputs_ready: dict | None = None, estimate_done=None) -> NsState:
     """G_k = T_comp + R_comp S_n(F) G, F_k = I - G_k A (newton_schulz.py:177-228).
 
     ``executor`` (not in the reference signature, whose parts run serially)
     evaluates the independent parts on concurrent streams.  ``parts`` (opt-in,
     changes the GEMM count) reuses hoisted T_comp / R_comp from
-    :func:`composite_parts` instead of recomputing them."""
+    :func:`composite_parts` instead of recomputing them.
+
+    ``inputs_ready`` maps input names (``a``, ``estimate``, ``residual``,
+    ``precond``, ``split_residual``, ``matrix``) to recorded ``torch.cuda.Event``s
+    (e.g. host->device copies on another stream); the step waits on each right
+    before that input's first use.  ``estimate_done`` is recorded when the new
+    estimate is final, before the last product."""
     if order_n < 1:
         raise ValueError("order_n must be >= 1")
     a = as_device(a)
@@ -210,11 +221,20 @@ def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_
     f = torch.empty_like(st.estimate)
     h, s = _ctx(g)
     buf = _lib.counter_buf()
-    _lib.call("si_composite_step", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
+    ready = None
+    if inputs_ready:
+        unknown = set(inputs_ready) - set(_READY_ORDER)
+        if unknown:
+            raise ValueError(f"unknown inputs in inputs_ready: {sorted(unknown)}")
+        ready = (ctypes.c_void_p * len(_READY_ORDER))(
+            *[inputs_ready[k].cuda_event if k in inputs_ready else None for k in _READY_ORDER])
+    _lib.call("si_composite_step_ex", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
               st.residual.data_ptr(), split.precond.data_ptr(), split.residual.data_ptr(),
               split.matrix.data_ptr(), len(spec.rates), _lib.i32_array(list(spec.rates)),
               _lib.i32_array(code), _lib.i64_array(offsets), _lib.f64_array(consts), len(consts),
-              order_n, int(executor is not None), g.data_ptr(), f.data_ptr(), buf, s)
+              order_n, int(executor is not None), ready,
+              estimate_done.cuda_event if estimate_done is not None else None, g.data_ptr(),
+              f.data_ptr(), buf, s)
     st.ctr.absorb(buf)
     return NsState(estimate=g, residual=f, step=st.step + 1, order=order_n,
                    series_order=st.series_order, ctr=st.ctr)
