@@ -43,6 +43,62 @@ def test_c4_recipe_n1024_40_iterations():
     print(f"c4 n=1024 40 it: worst rel err {worst:.3e} (tol {tol:.1e})")
 
 
+def test_c3_full_size_25_iterations_vs_oracle():
+    """BASELINE config 3 exactly (n=4096, Gram 8192x4096, h8 plan + plain Richardson,
+    25 iterations): P_k and theta_k against the live oracle at every iteration."""
+    import paper_2008_11480_b200 as P
+    from oracle import seriesinv_oracle as O
+    from paper_2008_11480_b200 import configs
+
+    a, b = configs.c3_gram(n=4096)
+    tol = _kappa_tol(a)
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False)
+    st = P.initial_series(sp, 0, 1, order=8)
+    bd = P.as_device(b)
+    theta = torch.zeros_like(bd)
+    osp = O.split_scalar(a, O.inf_norm(a) / 2.0)
+    ost = O.initial_series(osp, 0, 1, 8)
+    oth = np.zeros_like(b)
+    plan, oplan = P.table_plans()[8][0], O.TABLE_ROOTS[8][0][1]
+    worst = 0.0
+    for k in range(25):
+        theta = P.plain_richardson(theta, st.estimate, sp.matrix, bd, st.ctr)
+        st = P.ns_step(st, sp.matrix, plan=plan)
+        oth = O.plain_richardson(oth, ost.estimate, osp.matrix, b, ost.ctr)
+        ost = O.ns_step(ost, osp.matrix, oplan)
+        ep = np.linalg.norm(st.estimate.cpu().numpy() - ost.estimate) / np.linalg.norm(ost.estimate)
+        et = np.linalg.norm(theta.cpu().numpy() - oth) / np.linalg.norm(oth)
+        worst = max(worst, ep, et)
+        assert ep <= tol and et <= tol, (k, ep, et)
+    assert (st.ctr.mmm, st.ctr.mvm) == (ost.ctr.mmm, ost.ctr.mvm) == (150, 50)
+    print(f"c3 full size: worst rel err {worst:.3e}")
+
+
+def test_c2_full_batch_sampled_vs_oracle():
+    """BASELINE config 2 exactly (16384 systems, 50 iterations, one launch); 48 sampled
+    systems against the oracle."""
+    import paper_2008_11480_b200 as P
+    from oracle import seriesinv_oracle as O
+    from paper_2008_11480_b200 import configs
+
+    a_np, b_np = configs.c2_batched(batch=16384)
+    a, b = P.as_device(a_np), P.as_device(b_np)
+    pre, res = P.batched_scalar_split(a)
+    ctr = P.MulCounter()
+    p, f, th = P.batched_composite_richardson(a, b, pre, res, pre, res, torch.zeros_like(b),
+                                              (2, 3), 2, 50, ctr)
+    assert (ctr.mmm, ctr.mvm) == (500, 100)  # per system: 10 + 2 per iteration
+    for i in np.random.default_rng(7).choice(16384, 48, replace=False):
+        sp = O.split_scalar(a_np[i], O.inf_norm(a_np[i]) / 2.0)
+        st = O.initial_series(sp, 0, 1, 2)
+        theta = np.zeros(32)
+        for _ in range(50):
+            theta = O.plain_richardson(theta, st.estimate, sp.matrix, b_np[i], st.ctr)
+            st = O.composite_step(st, sp.matrix, sp, (2, 3), 2)
+        assert np.linalg.norm(p[i].cpu().numpy() - st.estimate) <= 1e-10 * np.linalg.norm(st.estimate)
+        assert np.linalg.norm(th[i].cpu().numpy() - theta) <= 1e-10 * np.linalg.norm(theta)
+
+
 def _c5_inputs(n, rhs):
     m = int(round(n * 40000 / 32768))
     rng = np.random.default_rng(0)
