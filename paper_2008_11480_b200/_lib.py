@@ -141,7 +141,12 @@ def handle(device: int | None = None) -> int:
     lib = load_library()
     dev = torch.cuda.current_device() if device is None else int(device)
     h = _handles.get(dev)
-    if h is None:
+    if h is not None:
+        return h
+    with _lib_lock:
+        h = _handles.get(dev)
+        if h is not None:
+            return h
         out = c_void_p()
         st = lib.si_create(dev, ctypes.byref(out))
         if st != SI_OK:
