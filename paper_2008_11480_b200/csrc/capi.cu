@@ -49,10 +49,15 @@ void add_counters(int64_t* counters, const Ctx& c) {
   }
 }
 
+// One C-ABI call: serialises host-side use of the handle (its side streams,
+// events and profiling records) across threads -- the reference's executors
+// may call in from several threads -- and sets the device.
 struct Call {
+  std::lock_guard<std::recursive_mutex> lock;
   Ctx c;
   int64_t* counters;
-  Call(si_handle h, void* stream, int64_t* ctrs) : c(&h->h, as_stream(stream)), counters(ctrs) {
+  Call(si_handle h, void* stream, int64_t* ctrs)
+      : lock(h->h.mu), c(&h->h, as_stream(stream)), counters(ctrs) {
     check(cudaSetDevice(h->h.device), "cudaSetDevice");
   }
   ~Call() { add_counters(counters, c); }
@@ -526,6 +531,7 @@ int si_plain_richardson(si_handle h, int64_t n, int64_t nrhs, const double* a, c
 int si_profile_begin(si_handle h) {
   return guard([&] {
     need(h != nullptr, "null handle");
+    std::lock_guard<std::recursive_mutex> lock(h->h.mu);
     Handle& hh = h->h;
     for (auto& r : hh.prof) {
       hh.prof_pool.push_back(r.start);
@@ -541,6 +547,7 @@ int si_profile_end(si_handle h, double* gemm_ms, double* gemm_flops, int64_t* ge
                    int64_t* total_launches) {
   return guard([&] {
     need(h != nullptr, "null handle");
+    std::lock_guard<std::recursive_mutex> lock(h->h.mu);
     Handle& hh = h->h;
     hh.profiling = false;
     double ms = 0.0, fl = 0.0;

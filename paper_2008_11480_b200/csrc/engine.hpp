@@ -3,6 +3,7 @@
 // fused FP64 GEMMs on device-resident matrices.
 #pragma once
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -19,6 +20,7 @@ struct Error : std::runtime_error {
 };
 
 struct Handle {
+  std::recursive_mutex mu;  // held for the duration of every C-ABI call
   int device = 0;
   cudaMemPool_t pool = nullptr;
   static constexpr int kSide = 5;
