@@ -138,6 +138,46 @@ def test_c5_recipe_n768_20_iterations(variant):
         assert steps_mmm[0] == 16 + 18 and all(s == 18 for s in steps_mmm[1:])
 
 
+def test_host_threads_share_the_handle():
+    """The reference runs methods from executor threads (harness.py:371-380): steps
+    issued concurrently from several host threads give bitwise the serial results."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import configs
+
+    a, b = configs.c4_householder(n=384, rhs=4)
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False)
+    bd = P.as_device(b)
+
+    def run(kind):
+        torch.cuda.set_device(0)
+        if kind == "composite":
+            st = P.initial_series(sp, 0, 1, order=2)
+            for _ in range(3):
+                st = P.composite_step(st, sp.matrix, sp, P.CompositeSpec((2, 3, 4, 5)), 2)
+            out = st.estimate
+        elif kind == "double":
+            st = P.initial_double(sp, 1, 2, order=3)
+            for _ in range(3):
+                st = P.double_ns_step(st, sp.matrix, executor=True)
+            out = st.estimate
+        else:
+            st = P.initial_richardson(sp, bd, 0, 1, order=4, q=4)
+            for _ in range(3):
+                st = P.richardson_recursive_step(st, sp.matrix, bd, executor=True)
+            out = st.theta
+        torch.cuda.current_stream().synchronize()
+        return out.clone()
+
+    kinds = ["composite", "double", "recursive"] * 2
+    serial = [run(k) for k in kinds]
+    with ThreadPoolExecutor(max_workers=3) as pool:
+        threaded = list(pool.map(run, kinds))
+    for s, t in zip(serial, threaded):
+        assert torch.equal(s, t)
+
+
 def test_composite_step_with_inputs_in_flight():
     """Inputs copied host->device on another stream, the step waiting on per-input
     events: bitwise the same result as with resident inputs."""
