@@ -487,6 +487,64 @@ def cpu_sample(n: int, flops_step: float, reps: int = 1):
     return step_s, t
 
 
+def reference_step_seconds(cfg: str, n: int, flops: float, batch: int = 16384):
+    """Seconds the CPU oracle needs for ONE bench step of `cfg` (the same unit as
+    our arm's step), measured on a bounded sample; returns (seconds, description).
+
+    c1: the whole 30-iteration run, executed (milliseconds; best of 20 runs).
+    c2: 50 iterations of 64 of the systems, executed, scaled to the full batch.
+    c3: one full-size iteration (n=4096: plain Richardson + h8 ns_step), executed.
+    c4/c5: a full iteration is minutes of CPU: one full-size n^3 product of the
+        step DAG, extrapolated by the DAG's FLOP ratio (c5 sampled at n=16384
+        and scaled by n^3)."""
+    import numpy as np
+
+    from oracle import seriesinv_oracle as O
+    from paper_2008_11480_b200 import configs
+
+    if cfg == "c1":
+        a, b = configs.c1_dense_small(n=n)
+        sp = O.split_scalar(a, O.inf_norm(a) / 2.0)
+        best = float("inf")
+        for _ in range(20):
+            st = O.initial_series(sp, 0, 1, 3)
+            th = np.zeros_like(b)
+            t0 = time.perf_counter()
+            for _ in range(30):
+                th = O.plain_richardson(th, st.estimate, sp.matrix, b, st.ctr)
+                st = O.ns_step(st, sp.matrix)
+            best = min(best, time.perf_counter() - t0)
+        return best, "whole 30-iteration run through the oracle (best of 20)"
+    if cfg == "c2":
+        k = 64
+        a, b = configs.c2_batched(batch=k)
+        t0 = time.perf_counter()
+        for i in range(k):
+            sp = O.split_scalar(a[i], O.inf_norm(a[i]) / 2.0)
+            st = O.initial_series(sp, 0, 1, 2)
+            th = np.zeros(a.shape[1])
+            for _ in range(50):
+                th = O.plain_richardson(th, st.estimate, sp.matrix, b[i], st.ctr)
+                st = O.composite_step(st, sp.matrix, sp, (2, 3), 2)
+        t = time.perf_counter() - t0
+        return t * batch / k, f"50 iterations of {k} systems through the oracle, x{batch // k} systems"
+    if cfg == "c3":
+        a, b = configs.c3_gram(n=n)
+        sp = O.split_scalar(a, O.inf_norm(a) / 2.0)
+        st = O.initial_series(sp, 0, 1, 8)
+        th = np.zeros_like(b)
+        plan = O.TABLE_ROOTS[8][0][1]
+        t0 = time.perf_counter()
+        th = O.plain_richardson(th, st.estimate, sp.matrix, b, st.ctr)
+        st = O.ns_step(st, sp.matrix, plan)
+        return time.perf_counter() - t0, f"one full-size iteration (n={n}) through the oracle"
+    sample_n = min(n, 16384)
+    s, t = cpu_sample(sample_n, flops * (sample_n / n) ** 3, reps=2)
+    s *= (n / sample_n) ** 3
+    return s, (f"one {sample_n}^3 FP64 product through oracle.mm in {t:.2f} s, extrapolated "
+               f"by the step DAG's FLOP ratio ({flops:.4e} FLOP/step)")
+
+
 # --------------------------------------------------------------------------- arms
 
 
@@ -499,29 +557,31 @@ def run_reference(args):
     n = args.n or {"c4": 16384, "c3": 4096, "c1": 64, "c5": 32768, "c2": 32}[cfg]
     w = Workload(cfg, n)
     w.r = {"c4": 64, "c5": 256}.get(cfg, 1)
-    w.mmm_per_step = 34
-    w.batch = args.n or 16384
+    w.mmm_per_step = 34  # the reference's recursive step is Horner (ri:111-189)
+    w.batch = (args.n or 16384) if cfg == "c2" else 16384
+    if cfg == "c2":
+        w.n = 32
+    w.iters_per_step = {"c1": 30, "c2": 50}.get(cfg, 1)
     flops = w.flops()
     cores = host_cores()
-    sample_n = n if cfg not in ("c5",) else 16384
-    # each step: a bounded full-size sample, extrapolated to one step of the workload
-    step_times = []
+    # each step: a bounded sample of one bench step of the workload (see
+    # reference_step_seconds for what is executed and what is extrapolated)
+    step_times, sample = [], ""
     for i in range(args.warmup + args.steps):
-        s, t = cpu_sample(sample_n, flops * (sample_n / n) ** 3 if cfg == "c5" else flops, reps=2)
-        if cfg == "c5":
-            s *= (n / sample_n) ** 3
+        s, sample = reference_step_seconds(cfg, w.n, flops, batch=w.batch)
         if i >= args.warmup:
             step_times.append(s)
     step_s = statistics.mean(step_times)
-    value = 1.0 / step_s
-    sample = (f"one {sample_n}^3 FP64 GEMM through oracle.mm (numpy/OpenBLAS, {cores} threads) "
-              f"per step, extrapolated by the step DAG's FLOP ratio ({flops:.4e} FLOP/step)")
+    value = w.iters_per_step / step_s
+    sample = f"{sample}; numpy/OpenBLAS with {cores} host threads"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": step_s * 1e3, "iters_per_step": w.iters_per_step,
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg, "n": n, "sample": "extrapolated"},
+        "config": {"workload": cfg, "n": w.n,
+                   "sample": "executed" if cfg in ("c1", "c2", "c3") else "extrapolated"},
         "tflops": flops / step_s / 1e12,
         "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "port",
                          "sample": sample},
@@ -601,11 +661,15 @@ def run_ours(args):
         del host
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu and args.config in ("c4", "c3"):
-        s, t = cpu_sample(w.n, flops)
-        cpu = {"value": 1.0 / s, "unit": "iters/s", "cores": host_cores(), "kind": "port",
-               "sample": f"one {w.n}^3 FP64 GEMM through oracle.mm (numpy/OpenBLAS, all host "
-                         f"threads) in {t:.2f} s, extrapolated by the step's FLOP ratio"}
+    if rank == 0 and world == 1 and not args.no_cpu and not args.hoist:
+        # the oracle on the reference DAG (c5: Horner, 34 products per step)
+        ref_flops = flops
+        if args.config == "c5":
+            ref_flops = 34 * 2.0 * w.n**3 + 2 * 2.0 * w.n * w.n * w.r
+        s, desc = reference_step_seconds(args.config, w.n, ref_flops,
+                                         batch=getattr(w, "batch", 16384))
+        cpu = {"value": w.iters_per_step / s, "unit": "iters/s", "cores": host_cores(),
+               "kind": "port", "sample": f"{desc}; numpy/OpenBLAS, all host threads"}
 
     if rank == 0:
         line = {
