@@ -39,6 +39,21 @@ struct BOp {
 };
 constexpr int kMaxOps = 96;
 
+// Device form of an op: 32 bytes, read with two 16-byte shared loads.  The
+// epilogue variant is decided on the host (`mode`) and the few non-unit
+// constants live in a side table (`cidx`), so an op costs no FP64 compares.
+//   GEMM mode: 0 A@B, 1 I - A@B, 2 A@B + C, 3 generic (cst: alpha, beta, diag)
+//   GEMV mode: 1 A@x - c, 2 c - A@x, 3 generic (cst: alpha, beta)
+//   LIN:       cst: cdiag, coef[0..nterms)        LOAD mode: 0 S^-1, 1 B
+struct __align__(16) DOp {
+  uint8_t kind, mode, sync, nterms;
+  int16_t dst, a, b, c;
+  int16_t t[kMaxLinTerms];
+  int16_t cidx;
+  int16_t pad[3];
+};
+static_assert(sizeof(DOp) == 32, "DOp layout");
+
 // ------------------------------------------------------------------ recorder
 struct Rec {
   std::vector<BOp> ops;
@@ -287,7 +302,9 @@ struct BatchArgs {
   double* p_io;
   double* f_io;
   double* theta_io;
-  const BOp* ops;
+  const DOp* ops;
+  const double* cst;
+  int ncst;
   int nops;
   int nmat;
   int nvec;
@@ -368,7 +385,8 @@ __device__ void store_mat(double* __restrict__ dst, const double* src, int n) {
 // 1 = I - A@B, 2 = A@B + C, 3 = generic alpha/beta/diag epilogue.
 template <int NP, int MODE>
 __device__ __forceinline__ void gemm_op(const double* A, const double* B, const double* C,
-                                        double* D, const BOp& o, int n, int warp, int g, int t) {
+                                        double* D, const double* cst, int n, int warp, int g,
+                                        int t) {
   using G = Geo<NP>;
   const int r0 = (warp >> 1) * G::WROWS, c0 = (warp & 1) * G::WCOLS;
   // two accumulator sets (even / odd k-steps): dependent DMMA chains of NP/8
@@ -411,11 +429,11 @@ __device__ __forceinline__ void gemm_op(const double* A, const double* B, const 
       } else if (MODE == 3) {
         double2 cv = make_double2(0.0, 0.0);
         if (C) cv = *reinterpret_cast<const double2*>(C + G::idx(row, col));
-        v0 = epi(v0, o.alpha, o.beta, cv.x);
-        v1 = epi(v1, o.alpha, o.beta, cv.y);
-        if (o.diag != 0.0 && row < n) {
-          if (row == col) v0 = __dadd_rn(v0, o.diag);
-          if (row == col + 1) v1 = __dadd_rn(v1, o.diag);
+        v0 = epi(v0, cst[0], cst[1], cv.x);
+        v1 = epi(v1, cst[0], cst[1], cv.y);
+        if (cst[2] != 0.0 && row < n) {
+          if (row == col) v0 = __dadd_rn(v0, cst[2]);
+          if (row == col + 1) v1 = __dadd_rn(v1, cst[2]);
         }
       }
       *reinterpret_cast<double2*>(D + G::idx(row, col)) = make_double2(v0, v1);
@@ -428,8 +446,9 @@ template <int NP>
 __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? 3 : 1) resident_kernel(BatchArgs p) {
   using G = Geo<NP>;
   extern __shared__ double sm[];
-  // dynamic shared memory: [matrix slots][vector slots][program]
-  BOp* prog = reinterpret_cast<BOp*>(sm + (size_t)p.nmat * G::SLOT + (size_t)p.nvec * NP);
+  // dynamic shared memory: [matrix slots][vector slots][program][constants]
+  DOp* prog = reinterpret_cast<DOp*>(sm + (size_t)p.nmat * G::SLOT + (size_t)p.nvec * NP);
+  double* cst = reinterpret_cast<double*>(prog + p.nops);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int n = p.n;
@@ -440,8 +459,9 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? 3 : 1) resident_k
   if (p.prof && threadIdx.x == 0)
     for (int k = 0; k < kMaxOps; ++k) prof_acc[k] = 0;
   auto vslot = [&](int s) { return sm + (size_t)p.nmat * G::SLOT + (size_t)s * NP; };
-  for (int i = threadIdx.x; i < p.nops * (int)sizeof(BOp) / 4; i += G::THREADS)
-    reinterpret_cast<int*>(prog)[i] = reinterpret_cast<const int*>(p.ops)[i];
+  for (int i = threadIdx.x; i < p.nops * (int)sizeof(DOp) / 16; i += G::THREADS)
+    reinterpret_cast<int4*>(prog)[i] = reinterpret_cast<const int4*>(p.ops)[i];
+  for (int i = threadIdx.x; i < p.ncst; i += G::THREADS) cst[i] = p.cst[i];
   __syncthreads();
 
   for (int64_t sys = blockIdx.x; sys < p.batch; sys += gridDim.x) {
@@ -470,14 +490,15 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? 3 : 1) resident_k
         }
       }
       for (int k = 0; k < p.nops; ++k) {
-        const BOp& o = prog[k];
+        const DOp o = prog[k];
+        const double* oc = cst + o.cidx;
         if (o.kind == OP_LOAD && prefetch) {
           double* dst = mslot(o.dst);
 #pragma unroll
           for (int j = 0; j < PF; ++j) {
             const int i = threadIdx.x + j * G::THREADS;
             const int r = (2 * i) / NP, c = (2 * i) % NP;
-            *reinterpret_cast<double2*>(dst + G::idx(r, c)) = o.vec ? pf_b[j] : pf_p[j];
+            *reinterpret_cast<double2*>(dst + G::idx(r, c)) = o.mode ? pf_b[j] : pf_p[j];
           }
         } else if (o.kind == OP_GEMM) {
           const double* A = mslot(o.a);
@@ -486,14 +507,12 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? 3 : 1) resident_k
           double* D = mslot(o.dst);
           // the DAG's epilogues are "X@Y", "I - X@Y" and "X@Y + Z": specialised,
           // anything else goes through the generic path
-          if (!C && o.alpha == 1.0 && o.diag == 0.0)
-            gemm_op<NP, 0>(A, B, C, D, o, n, warp, g, t);
-          else if (!C && o.alpha == -1.0 && o.diag == 1.0)
-            gemm_op<NP, 1>(A, B, C, D, o, n, warp, g, t);
-          else if (C && o.alpha == 1.0 && o.beta == 1.0 && o.diag == 0.0)
-            gemm_op<NP, 2>(A, B, C, D, o, n, warp, g, t);
-          else
-            gemm_op<NP, 3>(A, B, C, D, o, n, warp, g, t);
+          switch (o.mode) {
+            case 0: gemm_op<NP, 0>(A, B, C, D, oc, n, warp, g, t); break;
+            case 1: gemm_op<NP, 1>(A, B, C, D, oc, n, warp, g, t); break;
+            case 2: gemm_op<NP, 2>(A, B, C, D, oc, n, warp, g, t); break;
+            default: gemm_op<NP, 3>(A, B, C, D, oc, n, warp, g, t); break;
+          }
         } else if (o.kind == OP_GEMV) {
           // On the DMMA pipe, not the FP64 ALU: x becomes column 0 of an 8-wide B
           // fragment (zeros elsewhere).  A DFMA + shuffle-tree GEMV contends with
@@ -514,34 +533,41 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? 3 : 1) resident_k
               const int row = r0 + g;
               const double s = __dadd_rn(acc[0][0], acc[1][0]);
               const double cv = o.c >= 0 ? vslot(o.c)[row] : 0.0;
-              vslot(o.dst)[row] = epi(s, o.alpha, o.beta, cv);
+              double v;
+              if (o.mode == 1)
+                v = __dsub_rn(s, cv);  // A x - c
+              else if (o.mode == 2)
+                v = __dsub_rn(cv, s);  // c - A x
+              else
+                v = epi(s, oc[0], oc[1], cv);
+              vslot(o.dst)[row] = v;
             }
           }
         } else if (o.kind == OP_LOAD) {
-          load_mat<NP>(mslot(o.dst), (o.vec ? p.residual : p.precond) + sys * nn, n);
-        } else if (o.vec) {
+          load_mat<NP>(mslot(o.dst), (o.mode ? p.residual : p.precond) + sys * nn, n);
+        } else if (o.mode) {  // LIN over vectors
           if (threadIdx.x < NP) {
             double acc = 0.0;
             for (int j = 0; j < o.nterms; ++j) {
               const double xv = vslot(o.t[j])[threadIdx.x];
-              acc = __dadd_rn(acc, o.coef[j] == 1.0 ? xv : __dmul_rn(o.coef[j], xv));
+              acc = __dadd_rn(acc, oc[1 + j] == 1.0 ? xv : __dmul_rn(oc[1 + j], xv));
             }
             vslot(o.dst)[threadIdx.x] = acc;
           }
-        } else {
+        } else {  // LIN over matrices
           double* D = mslot(o.dst);
           for (int i = threadIdx.x; i < NP * NP; i += G::THREADS) {
             const int r = i / NP;
             const int c = G::col_at(r, i % NP);
-            double acc = (r == c && r < n) ? o.diag : 0.0;
+            double acc = (r == c && r < n) ? oc[0] : 0.0;
             for (int j = 0; j < o.nterms; ++j) {
               const double xv = mslot(o.t[j])[i];
-              acc = __dadd_rn(acc, o.coef[j] == 1.0 ? xv : __dmul_rn(o.coef[j], xv));
+              acc = __dadd_rn(acc, oc[1 + j] == 1.0 ? xv : __dmul_rn(oc[1 + j], xv));
             }
             D[i] = acc;
           }
         }
-        if (o.pad_) __syncthreads();  // elided when the next op is independent
+        if (o.sync) __syncthreads();  // elided when the next op is independent
         if (p.prof && blockIdx.x == 0 && threadIdx.x == 0) {  // SI_RESIDENT_PROF diagnostics
           const long long now = clock64();
           prof_acc[k] += now - prof_last;
@@ -660,14 +686,55 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
     }
     if (!ops.empty()) ops.back().pad_ = 1;  // end of iteration: carry copies follow
   }
+  // device encoding: modes decided here, constants in a side table
+  std::vector<DOp> dev_ops(ops.size());
+  std::vector<double> csts = {0.0};  // slot 0: unused default
+  for (size_t k = 0; k < ops.size(); ++k) {
+    const BOp& o = ops[k];
+    DOp& d = dev_ops[k];
+    d = DOp{};
+    d.kind = (uint8_t)o.kind;
+    d.sync = (uint8_t)o.pad_;
+    d.nterms = (uint8_t)o.nterms;
+    d.dst = o.dst;
+    d.a = o.a;
+    d.b = o.b;
+    d.c = o.c;
+    for (int j = 0; j < kMaxLinTerms; ++j) d.t[j] = o.t[j];
+    d.cidx = (int16_t)csts.size();
+    if (o.kind == OP_GEMM) {
+      const bool hc = o.c >= 0;
+      d.mode = (!hc && o.alpha == 1.0 && o.diag == 0.0)                     ? 0
+               : (!hc && o.alpha == -1.0 && o.diag == 1.0)                  ? 1
+               : (hc && o.alpha == 1.0 && o.beta == 1.0 && o.diag == 0.0)   ? 2
+                                                                             : 3;
+      csts.insert(csts.end(), {o.alpha, o.beta, o.diag});
+    } else if (o.kind == OP_GEMV) {
+      const bool hc = o.c >= 0;
+      d.mode = (hc && o.alpha == 1.0 && o.beta == -1.0)    ? 1
+               : (hc && o.alpha == -1.0 && o.beta == 1.0)  ? 2
+                                                            : 3;
+      csts.insert(csts.end(), {o.alpha, o.beta});
+    } else if (o.kind == OP_LIN) {
+      d.mode = (uint8_t)o.vec;
+      csts.push_back(o.diag);
+      for (int j = 0; j < o.nterms; ++j) csts.push_back(o.coef[j]);
+    } else {
+      d.mode = (uint8_t)o.vec;  // OP_LOAD: which matrix
+    }
+  }
   const size_t smem = (size_t)al.nmat * Gm::SLOT * sizeof(double) +
-                      (size_t)al.nvec * NP * sizeof(double) + ops.size() * sizeof(BOp);
+                      (size_t)al.nvec * NP * sizeof(double) + dev_ops.size() * sizeof(DOp) +
+                      csts.size() * sizeof(double);
   if (smem > 227 * 1024) throw Error(kEInval, "resident program needs too much shared memory");
 
-  MV dops = alloc(c, (int64_t)((ops.size() * sizeof(BOp) + 7) / 8), 1);
-  check(cudaMemcpyAsync(dops.v.p, ops.data(), ops.size() * sizeof(BOp), cudaMemcpyHostToDevice,
-                        c.s),
+  const size_t op_bytes = dev_ops.size() * sizeof(DOp);
+  MV dops = alloc(c, (int64_t)((op_bytes + csts.size() * sizeof(double) + 7) / 8), 1);
+  check(cudaMemcpyAsync(dops.v.p, dev_ops.data(), op_bytes, cudaMemcpyHostToDevice, c.s),
         "memcpy program");
+  check(cudaMemcpyAsync(reinterpret_cast<char*>(dops.v.p) + op_bytes, csts.data(),
+                        csts.size() * sizeof(double), cudaMemcpyHostToDevice, c.s),
+        "memcpy constants");
   BatchArgs args{};
   args.a = a;
   args.b = b;
@@ -676,8 +743,10 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
   args.p_io = p_io;
   args.f_io = f_io;
   args.theta_io = theta_io;
-  args.ops = reinterpret_cast<const BOp*>(dops.v.p);
+  args.ops = reinterpret_cast<const DOp*>(dops.v.p);
   args.nops = (int)ops.size();
+  args.cst = reinterpret_cast<const double*>(reinterpret_cast<char*>(dops.v.p) + op_bytes);
+  args.ncst = (int)csts.size();
   args.nmat = al.nmat;
   args.nvec = al.nvec;
   args.n = (int)n;
