@@ -13,12 +13,17 @@
 // products, so MulCounter deltas match tick for tick.
 //
 // Shared-memory layout: a slot is an unpadded NP x NP row-major matrix whose
-// 16-byte chunks are XOR-swizzled by 2*(row & 3); every DMMA fragment load is
-// then the minimum 2 wavefronts, and slots are 8 KB (NP=32) / 32 KB (NP=64),
-// so three 32 x 32 systems fit per SM.
+// 16-byte chunks are XOR-swizzled by {0,4,2,6}[row & 3]; every DMMA fragment
+// load is then the minimum 2 wavefronts and every accumulator store / C load
+// (16 bytes per lane, rows g and g+1 in one quarter-warp) the minimum 4.
+// Slots are 8 KB (NP=32) / 32 KB (NP=64); the ops are reordered to minimise
+// live slots, so four 32 x 32 systems fit per SM.
 #include <algorithm>
+#include <bitset>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
+#include <unordered_map>
 
 #include "batched.hpp"
 
@@ -202,6 +207,87 @@ struct Rec {
   }
 };
 
+// Reorders the recorded ops (a topological order of the SSA DAG) so that the
+// peak number of live matrices -- the shared-memory footprint, hence CTAs per
+// SM -- is minimal.  Branch and bound over schedules, ready ops tried in
+// recorded order (so the recorded order is the first candidate and is kept on
+// ties), memoised on the set of scheduled ops, with a node budget.  Products
+// are unchanged, only their order, so every value is bitwise the same.
+void schedule_min_live(Rec& r, const std::vector<int>& pinned,
+                       const std::vector<std::pair<int, int>>& carried) {
+  const int nops = (int)r.ops.size(), nv = (int)r.is_vec.size();
+  if (nops > 128) return;
+  using Mask = std::bitset<128>;
+  std::vector<int> producer(nv, -1);
+  std::vector<std::vector<int>> reads(nops);  // unique matrix operands
+  std::vector<std::vector<int>> deps(nops);
+  for (int i = 0; i < nops; ++i) {
+    const BOp& o = r.ops[i];
+    producer[o.dst] = i;
+    std::vector<int> all = {o.a, o.b, o.c};
+    if (o.kind == OP_LIN)
+      for (int j = 0; j < o.nterms; ++j) all.push_back(o.t[j]);
+    for (int v : all) {
+      if (v < 0) continue;
+      if (!r.is_vec[v] && std::find(reads[i].begin(), reads[i].end(), v) == reads[i].end())
+        reads[i].push_back(v);
+    }
+    for (int v : all)
+      if (v >= 0 && producer[v] >= 0 && producer[v] != i) deps[i].push_back(producer[v]);
+  }
+  std::vector<char> keep(nv, 0);  // never released: pinned values and carried outputs
+  for (int v : pinned) keep[v] = 1;
+  for (auto& pr : carried) keep[pr.second] = 1;
+  std::vector<int> uses(nv, 0);
+  for (int i = 0; i < nops; ++i)
+    for (int v : reads[i]) uses[v] += 1;
+  int live0 = 0;
+  for (int v : pinned) live0 += !r.is_vec[v];
+  for (auto& pr : carried) live0 += (!r.is_vec[pr.first] && uses[pr.first] > 0);
+
+  std::vector<int> order, best_order;
+  int best = INT32_MAX;
+  long budget = 200000;
+  std::unordered_map<Mask, int> seen;
+  Mask done;
+  std::function<void(int, int)> dfs = [&](int live, int peak) {
+    if (peak >= best || --budget < 0) return;
+    if ((int)order.size() == nops) {
+      best = peak;
+      best_order = order;
+      return;
+    }
+    auto it = seen.find(done);
+    if (it != seen.end() && it->second <= peak) return;
+    seen[done] = peak;
+    for (int i = 0; i < nops; ++i) {
+      if (done[i]) continue;
+      bool ready = true;
+      for (int d : deps[i]) ready &= (bool)done[d];
+      if (!ready) continue;
+      const BOp& o = r.ops[i];
+      const bool mat = !r.is_vec[o.dst];
+      const int during = live + (mat ? 1 : 0);
+      int after = live;
+      if (mat && (uses[o.dst] > 0 || keep[o.dst])) after += 1;
+      for (int v : reads[i])
+        if (--uses[v] == 0 && !keep[v]) after -= 1;
+      done[i] = true;
+      order.push_back(i);
+      dfs(after, std::max(peak, during));
+      order.pop_back();
+      done[i] = false;
+      for (int v : reads[i]) ++uses[v];
+      if (budget < 0) return;
+    }
+  };
+  dfs(live0, live0);
+  if ((int)best_order.size() != nops) return;
+  std::vector<BOp> ops(nops);
+  for (int i = 0; i < nops; ++i) ops[i] = r.ops[best_order[i]];
+  r.ops.swap(ops);
+}
+
 // Linear-scan assignment of virtual registers to shared-memory slots.
 //  * pinned: live for the whole run (A, b);
 //  * carried (in, out): `in` holds the state at the start of an iteration and
@@ -312,6 +398,7 @@ struct BatchArgs {
   int iters;
   int64_t batch;
   int has_load;            // the program streams S^-1 / B in (OP_LOAD)
+  int last_load;           // index of the last OP_LOAD: the next prefetch is issued after it
   long long* prof;         // per-op cycle totals of CTA 0 (diagnostics; usually null)
   int sA, sG, sF, sT, sb;  // slots of A, the carried inputs, b
   int rG, rF, rT;          // slots of the carried outputs (copied back when different)
@@ -321,25 +408,32 @@ template <int NP>
 struct Geo {
   static constexpr int SLOT = NP * NP;
 #ifndef SI_RESIDENT_WARPS32
-#define SI_RESIDENT_WARPS32 8
+#define SI_RESIDENT_WARPS32 4
 #endif
 #ifndef SI_RESIDENT_WARPS64
 #define SI_RESIDENT_WARPS64 16
 #endif
-  // more warps than DMMA tiles per op would need: the ops are short dependent
-  // chains, so latency (not issue) bounds them and extra warps hide it
+  // NP=32: four warps with 16x16 warp tiles (2x2 DMMA tiles, one fragment
+  // load per DMMA); with several CTAs per SM the shared-memory pipe, not
+  // latency, is the tighter limit, and 8x16 warp tiles (1.5 loads per DMMA)
+  // measured 16% slower.  NP=64 runs one CTA per SM: 16 warps hide latency.
   static constexpr int WARPS = NP == 32 ? SI_RESIDENT_WARPS32 : SI_RESIDENT_WARPS64;
   static constexpr int THREADS = WARPS * 32;
   static constexpr int WROWS = NP / (WARPS / 2);  // warp tile rows (16)
   static constexpr int WCOLS = NP / 2;             // warp tile cols (16 or 32)
   static constexpr int MT = WROWS / 8, NT = WCOLS / 8;
-  // element (r, c) of a slot: 16-byte chunks XOR-swizzled by 2*(r & 3)
+  // 16-byte chunk swizzle of row r: a distinct even value for the four rows
+  // of a fragment (conflict-free 8-byte fragment loads), with rows 2q and 2q+1
+  // in opposite halves of the 128-byte bank window (conflict-free 16-byte
+  // accumulator stores)
+  __device__ static __forceinline__ int swz(int r) { return ((r & 1) << 2) | (r & 2); }
+  // element (r, c) of a slot
   __device__ static __forceinline__ int idx(int r, int c) {
-    return r * NP + ((((c >> 1) ^ ((r & 3) << 1))) << 1) + (c & 1);
+    return r * NP + ((((c >> 1) ^ swz(r))) << 1) + (c & 1);
   }
   // logical column of the element stored at position (r, p)
   __device__ static __forceinline__ int col_at(int r, int p) {
-    return ((((p >> 1) ^ ((r & 3) << 1))) << 1) + (p & 1);
+    return ((((p >> 1) ^ swz(r))) << 1) + (p & 1);
   }
 };
 
@@ -381,17 +475,40 @@ __device__ void store_mat(double* __restrict__ dst, const double* src, int n) {
   }
 }
 
+// Sign flip on the integer pipe: the FP64 pipe is shared with DMMA.
+__device__ __forceinline__ double flip(double x) {
+  return __hiloint2double(__double2hiint(x) ^ (int)0x80000000, __double2loint(x));
+}
+
 // One NP x NP x NP product of a recorded op by the whole CTA.  MODE: 0 = A@B,
 // 1 = I - A@B, 2 = A@B + C, 3 = generic alpha/beta/diag epilogue.
+// The epilogue terms of modes 1 and 2 enter through the accumulator (C, or
+// -I with the result negated), so those products issue no FP64-pipe
+// instruction besides the DMMAs: on sm_100 the FP64 ALU shares its dispatch
+// with the DMMA pipe, and epilogue adds stalled behind the other CTAs' DMMAs.
 template <int NP, int MODE>
 __device__ __forceinline__ void gemm_op(const double* A, const double* B, const double* C,
                                         double* D, const double* cst, int n, int warp, int g,
                                         int t) {
   using G = Geo<NP>;
   const int r0 = (warp >> 1) * G::WROWS, c0 = (warp & 1) * G::WCOLS;
-  // two accumulator sets (even / odd k-steps): dependent DMMA chains of NP/8
-  // instead of NP/4, combined once in a fixed order
-  double acc[2][G::MT][G::NT][2] = {};
+  double acc[G::MT][G::NT][2];
+#pragma unroll
+  for (int mi = 0; mi < G::MT; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < G::NT; ++ni) {
+      const int row = r0 + mi * 8 + g, col = c0 + ni * 8 + 2 * t;
+      if (MODE == 2) {
+        const double2 cv = *reinterpret_cast<const double2*>(C + G::idx(row, col));
+        acc[mi][ni][0] = cv.x;
+        acc[mi][ni][1] = cv.y;
+      } else if (MODE == 1) {
+        acc[mi][ni][0] = (row == col && row < n) ? -1.0 : 0.0;
+        acc[mi][ni][1] = (row == col + 1 && row < n) ? -1.0 : 0.0;
+      } else {
+        acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      }
+    }
   double af[2][G::MT], bf[2][G::NT];
 #pragma unroll
   for (int mi = 0; mi < G::MT; ++mi) af[0][mi] = A[G::idx(r0 + mi * 8 + g, t)];
@@ -410,22 +527,17 @@ __device__ __forceinline__ void gemm_op(const double* A, const double* B, const 
     for (int mi = 0; mi < G::MT; ++mi)
 #pragma unroll
       for (int ni = 0; ni < G::NT; ++ni)
-        dmma(acc[cur][mi][ni][0], acc[cur][mi][ni][1], af[cur][mi], bf[cur][ni]);
+        dmma(acc[mi][ni][0], acc[mi][ni][1], af[cur][mi], bf[cur][ni]);
   }
 #pragma unroll
   for (int mi = 0; mi < G::MT; ++mi)
 #pragma unroll
     for (int ni = 0; ni < G::NT; ++ni) {
       const int row = r0 + mi * 8 + g, col = c0 + ni * 8 + 2 * t;
-      double v0 = __dadd_rn(acc[0][mi][ni][0], acc[1][mi][ni][0]);
-      double v1 = __dadd_rn(acc[0][mi][ni][1], acc[1][mi][ni][1]);
+      double v0 = acc[mi][ni][0], v1 = acc[mi][ni][1];
       if (MODE == 1) {
-        v0 = (row == col && row < n) ? __dsub_rn(1.0, v0) : -v0;
-        v1 = (row == col + 1 && row < n) ? __dsub_rn(1.0, v1) : -v1;
-      } else if (MODE == 2) {
-        const double2 cv = *reinterpret_cast<const double2*>(C + G::idx(row, col));
-        v0 = __dadd_rn(v0, cv.x);
-        v1 = __dadd_rn(v1, cv.y);
+        v0 = flip(v0);
+        v1 = flip(v1);
       } else if (MODE == 3) {
         double2 cv = make_double2(0.0, 0.0);
         if (C) cv = *reinterpret_cast<const double2*>(C + G::idx(row, col));
@@ -441,9 +553,13 @@ __device__ __forceinline__ void gemm_op(const double* A, const double* B, const 
 }
 
 template <int NP>
-// 32 x 32 systems: three CTAs per SM fit in shared memory, so registers must
-// not be the tighter limit
-__global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? 3 : 1) resident_kernel(BatchArgs p) {
+// 32 x 32 systems: four CTAs per SM fit in shared memory, so registers must
+// not be the tighter limit (<= 128 per thread)
+#ifndef SI_RESIDENT_MINB32
+#define SI_RESIDENT_MINB32 4
+#endif
+__global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB32 : 1)
+    resident_kernel(BatchArgs p) {
   using G = Geo<NP>;
   extern __shared__ double sm[];
   // dynamic shared memory: [matrix slots][vector slots][program][constants]
@@ -464,6 +580,8 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? 3 : 1) resident_k
   for (int i = threadIdx.x; i < p.ncst; i += G::THREADS) cst[i] = p.cst[i];
   __syncthreads();
 
+  constexpr int PFD = NP * NP / 2 / G::THREADS > 0 ? NP * NP / 2 / G::THREADS : 1;
+  double2 pf_p[PFD], pf_b[PFD];
   for (int64_t sys = blockIdx.x; sys < p.batch; sys += gridDim.x) {
     load_mat<NP>(mslot(p.sA), p.a + sys * nn, n);
     load_mat<NP>(mslot(p.sG), p.p_io + sys * nn, n);
@@ -473,22 +591,23 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? 3 : 1) resident_k
       vslot(p.sb)[threadIdx.x] = threadIdx.x < n ? p.b[sys * n + threadIdx.x] : 0.0;
     }
     __syncthreads();
-    // S^-1 and B are streamed in every iteration; their global loads are issued
-    // into registers at the top of the iteration so the latency hides behind
-    // the ops that precede the LOAD ops (full-size systems only)
+    // S^-1 and B are streamed in every iteration through registers: the global
+    // loads for the next iteration (or the next system) are issued right after
+    // the last LOAD op consumed the previous ones, so their latency hides behind
+    // the rest of the iteration (full-size systems only)
     constexpr int PF = NP * NP / 2 / G::THREADS;
     const bool prefetch = p.has_load && n == NP && PF >= 1;
-    double2 pf_p[PF > 0 ? PF : 1], pf_b[PF > 0 ? PF : 1];
-    for (int it = 0; it < p.iters; ++it) {
-      if (prefetch) {
-        const double2* sp2 = reinterpret_cast<const double2*>(p.precond + sys * nn);
-        const double2* sb2 = reinterpret_cast<const double2*>(p.residual + sys * nn);
+    auto issue = [&](int64_t s) {
+      const double2* sp2 = reinterpret_cast<const double2*>(p.precond + s * nn);
+      const double2* sb2 = reinterpret_cast<const double2*>(p.residual + s * nn);
 #pragma unroll
-        for (int j = 0; j < PF; ++j) {
-          pf_p[j] = __ldg(sp2 + threadIdx.x + j * G::THREADS);
-          pf_b[j] = __ldg(sb2 + threadIdx.x + j * G::THREADS);
-        }
+      for (int j = 0; j < PF; ++j) {
+        pf_p[j] = __ldg(sp2 + threadIdx.x + j * G::THREADS);
+        pf_b[j] = __ldg(sb2 + threadIdx.x + j * G::THREADS);
       }
+    };
+    if (prefetch && sys == blockIdx.x) issue(sys);
+    for (int it = 0; it < p.iters; ++it) {
       for (int k = 0; k < p.nops; ++k) {
         const DOp o = prog[k];
         const double* oc = cst + o.cidx;
@@ -499,6 +618,12 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? 3 : 1) resident_k
             const int i = threadIdx.x + j * G::THREADS;
             const int r = (2 * i) / NP, c = (2 * i) % NP;
             *reinterpret_cast<double2*>(dst + G::idx(r, c)) = o.mode ? pf_b[j] : pf_p[j];
+          }
+          if (k == p.last_load) {
+            if (it + 1 < p.iters)
+              issue(sys);
+            else if (sys + gridDim.x < p.batch)
+              issue(sys + gridDim.x);
           }
         } else if (o.kind == OP_GEMM) {
           const double* A = mslot(o.a);
@@ -638,6 +763,7 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
   if (batch == 0 || iters == 0) return per;
   if ((int)q.r.ops.size() > kMaxOps) throw Error(kEInval, "resident program too long");
 
+  schedule_min_live(q.r, {q.A, q.bv}, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}});
   Alloc al = assign(q.r, {q.A, q.bv}, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}});
   std::vector<BOp> ops = q.r.ops;
   auto ph = [&](int v) -> int16_t { return v >= 0 ? al.phys[v] : (int16_t)-1; };
@@ -753,7 +879,12 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
   args.iters = iters;
   args.batch = batch;
   args.has_load = 0;
-  for (const BOp& o : ops) args.has_load |= (o.kind == OP_LOAD);
+  args.last_load = -1;
+  for (size_t k = 0; k < ops.size(); ++k)
+    if (ops[k].kind == OP_LOAD) {
+      args.has_load = 1;
+      args.last_load = (int)k;
+    }
   args.sA = al.phys[q.A];
   args.sG = al.phys[q.G];
   args.sF = al.phys[q.F];
