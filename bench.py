@@ -19,6 +19,10 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+# the sharded path's exchange streams wait on flags: give every stream its own
+# hardware work queue (paper_2008_11480_b200/peer.py); before CUDA initialises
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import statistics
 import subprocess
 import sys
@@ -172,10 +176,31 @@ def host_cores() -> int:
 # --------------------------------------------------------------------------- workloads
 
 
+def make_comm(n: int, kind: str):
+    """Row-panel exchange of the sharded path: "peer" (copy engines over CUDA
+    IPC, products gated per panel inside the DMMA kernel), "peer-stream"
+    (same transfers, stream waits before each product) or "nccl" (NCCL
+    all-gather, the library baseline)."""
+    from paper_2008_11480_b200.sharded import RowComm
+
+    if kind == "nccl":
+        return RowComm(n)
+    from paper_2008_11480_b200.peer import IpcFabric, PeerComm
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    return PeerComm(n, IpcFabric(dev), mode="fused" if kind == "peer" else "stream")
+
+
+_COMM_LABEL = {"peer": "copy-engine panel exchange, panel-gated products",
+               "peer-stream": "copy-engine panel exchange, stream-gated products",
+               "nccl": "NCCL all-gather"}
+
+
 class Workload:
     """One config: device state + one step function + algorithmic FLOPs per step."""
 
-    def __init__(self, cfg: str, n: int | None, world: int = 1, hoist: bool = False):
+    def __init__(self, cfg: str, n: int | None, world: int = 1, hoist: bool = False,
+                 comm: str = "peer"):
         self.cfg = cfg
         self.n = n
         self.world = world
@@ -270,10 +295,11 @@ class Workload:
         self.sharded = None
         if self.world > 1 and cfg in ("c4", "c3"):
             # block-row sharding over the ranks (sharded.py): A, S^-1, B replicated,
-            # G / F row blocks, one NCCL all-gather per product with a sharded right operand
-            from paper_2008_11480_b200.sharded import RowComm, ShardedEngine
+            # G / F row blocks, one row-panel exchange per product with a sharded
+            # right operand (peer.py: copy engines + panel-gated DMMA products)
+            from paper_2008_11480_b200.sharded import ShardedEngine
 
-            comm = RowComm(self.n)
+            comm = make_comm(self.n, comm)
             eng = ShardedEngine(comm)
             st = P.initial_series(self.sp, 0, 1, order={"c4": 2, "c3": 8}[cfg])
             self.sharded = {
@@ -301,9 +327,9 @@ class Workload:
             self.mmm_per_step = 18
             if self.world > 1:
                 # block-row sharded recursive step (sharded.py) from the same initial state
-                from paper_2008_11480_b200.sharded import RowComm, ShardedEngine
+                from paper_2008_11480_b200.sharded import ShardedEngine
 
-                comm = RowComm(self.n)
+                comm = make_comm(self.n, comm)
                 eng = ShardedEngine(comm)
                 rows = slice(comm.r0, comm.r1)
                 inner = self.st.inner
@@ -597,7 +623,7 @@ def run_ours(args):
     world, rank, local = dist_setup(args)
     from paper_2008_11480_b200 import _lib
 
-    w = Workload(args.config, args.n, world, hoist=args.hoist)
+    w = Workload(args.config, args.n, world, hoist=args.hoist, comm=args.comm)
     w.setup()
     flops = w.flops()
     h = _lib.handle()
@@ -680,7 +706,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded PCG64 draws, SURVEY Appendix A recipe)",
             "config": {"workload": w.workload, "n": w.n,
-                       "parallelism": (f"block-row x{world} (NCCL all-gather)" if w.sharded is not None
+                       "parallelism": (f"block-row x{world} ({_COMM_LABEL[args.comm]})"
+                                       if w.sharded is not None
                                        else f"batch split x{world} (no communication)" if w.split_batch
                                        else (f"replicas x{world}" if world > 1 else "single-gpu")),
                        "l2": "inputs larger than L2 (2.1 GB per matrix), no flush"},
@@ -718,6 +745,8 @@ def main():
     ap.add_argument("--hoist", action="store_true",
                     help="c4 only, opt-in labelled variant: hoist the state-independent "
                          "composite parts (NOT the reference DAG; FLOPs counted as executed)")
+    ap.add_argument("--comm", choices=["peer", "peer-stream", "nccl"], default="peer",
+                    help="row-panel exchange of the sharded path (N > 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

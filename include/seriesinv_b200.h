@@ -84,6 +84,42 @@ SI_API int si_gemm_ex(si_handle h, int64_t m, int64_t n, int64_t k, double alpha
                       const double* C, int64_t ldc, double diag, int64_t diag_offset, double* D,
                       int64_t ldd, int is_mv, int64_t* counters, void* stream);
 
+/* ---------------- sharded exchange over peer memory -----------
+ * The reference has no multi-GPU layer; these replace the all-gather of a
+ * row-sharded right operand (the exchange step of every `mat_mul(y, x)`
+ * with x sharded, matrix_core.py:101-106) by copy-engine transfers between
+ * IPC-mapped buffers plus flags, so the consuming product starts on the panels
+ * that have arrived. */
+
+/* si_gemm_ex whose k rows of B are split into npanels (<= 16) row
+ * panels [panel_bounds[p], panel_bounds[p+1]) (panel_bounds[0] = 0,
+ * panel_bounds[npanels] = k): rows of panel p are read only once
+ * ready_flags[p] >= epoch (wrap-safe).  The DMMA kernel gates its TMA loads
+ * per panel; other kernels wait on the stream.  npanels = 0: ungated. */
+SI_API int si_gemm_panels(si_handle h, int64_t m, int64_t n, int64_t k, double alpha,
+                          const double* A, int64_t lda, const double* B, int64_t ldb,
+                          double beta, const double* C, int64_t ldc, double diag,
+                          int64_t diag_offset, double* D, int64_t ldd,
+                          const uint32_t* ready_flags, uint32_t epoch,
+                          const int64_t* panel_bounds, int npanels, int is_mv,
+                          int64_t* counters, void* stream);
+
+/* Exchange buffer: cudaMalloc'd (zeroed) device memory and its 64-byte CUDA IPC
+ * handle, to be opened by the peer processes with si_sym_open. */
+SI_API int si_sym_alloc(si_handle h, size_t bytes, void** ptr, unsigned char handle_out[64]);
+SI_API int si_sym_free(si_handle h, void* ptr);
+SI_API int si_sym_open(si_handle h, const unsigned char handle[64], void** ptr);
+SI_API int si_sym_close(si_handle h, void* ptr);
+
+/* Stream memory operations (no SM involved): *addr = value once the stream's
+ * prior work is complete and visible; block the stream until
+ * (int32_t)(*addr - value) >= 0.  addr may be a peer (IPC) mapping. */
+SI_API int si_stream_write_u32(si_handle h, uint32_t* addr, uint32_t value, void* stream);
+SI_API int si_stream_wait_u32(si_handle h, const uint32_t* addr, uint32_t value, void* stream);
+
+/* Stream-ordered copy (copy engine; either side may be a peer mapping). */
+SI_API int si_copy_async(si_handle h, void* dst, const void* src, size_t bytes, void* stream);
+
 /* D = cdiag*I + sum_i coefs[i]*X[i] (nterms <= 6), one rounding per term in
  * order: the `Lin` instruction (series_toolkit.py:375-378). */
 SI_API int si_lincomb(si_handle h, int64_t m, int64_t n, double cdiag, int nterms, const double* coefs,

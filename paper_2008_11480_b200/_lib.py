@@ -34,6 +34,15 @@ SIGNATURES: dict[str, list] = {
     "si_set_allocator": [_P, _P, _P, _P],
     "si_gemm": [_P, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _D, _P, _I64, _I, _PI64, _P],
     "si_gemm_ex": [_P, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _D, _I64, _P, _I64, _I, _PI64, _P],
+    "si_gemm_panels": [_P, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _D, _I64, _P,
+                       _I64, _P, ctypes.c_uint32, _P, _I, _I, _PI64, _P],
+    "si_sym_alloc": [_P, ctypes.c_size_t, POINTER(c_void_p), _P],
+    "si_sym_free": [_P, _P],
+    "si_sym_open": [_P, _P, POINTER(c_void_p)],
+    "si_sym_close": [_P, _P],
+    "si_stream_write_u32": [_P, _P, ctypes.c_uint32, _P],
+    "si_stream_wait_u32": [_P, _P, ctypes.c_uint32, _P],
+    "si_copy_async": [_P, _P, _P, ctypes.c_size_t, _P],
     "si_lincomb": [_P, _I64, _I64, _D, _I, _P, _P, _P, _P, _I64, _P],
     "si_lincomb_ex": [_P, _I64, _I64, _D, _I64, _I, _P, _P, _P, _P, _I64, _P],
     "si_fro_norm": [_P, _I64, _I64, _P, _I64, POINTER(c_double), _P],

@@ -184,6 +184,116 @@ int si_gemm_ex(si_handle h, int64_t m, int64_t n, int64_t k, double alpha, const
   });
 }
 
+int si_gemm_panels(si_handle h, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+                   int64_t lda, const double* B, int64_t ldb, double beta, const double* C,
+                   int64_t ldc, double diag, int64_t diag_offset, double* D, int64_t ldd,
+                   const uint32_t* ready_flags, uint32_t epoch, const int64_t* panel_bounds,
+                   int npanels, int is_mv, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && (A || m * k == 0) && (B || k * n == 0) && (D || m * n == 0), "null pointer");
+    need(m >= 0 && n >= 0 && k >= 0, "negative dimension");
+    need(lda >= k && ldb >= n && ldd >= n, "leading dimension too small");
+    need(beta == 0.0 || m * n == 0 || (C && ldc >= n), "beta != 0 needs C");
+    need(npanels >= 0 && npanels <= kMaxPanels, "npanels out of range");
+    need(npanels == 0 || (ready_flags && panel_bounds), "null panel arrays");
+    PanelWait pw;
+    pw.ready = ready_flags;
+    pw.epoch = epoch;
+    pw.npanels = npanels;
+    for (int p = 0; p <= npanels; ++p) {
+      need(panel_bounds[p] >= 0 && panel_bounds[p] <= k, "panel bound out of range");
+      need(p == 0 || panel_bounds[p] >= panel_bounds[p - 1], "panel bounds not ascending");
+      pw.bounds[p] = (int)panel_bounds[p];
+    }
+    need(npanels == 0 || (panel_bounds[0] == 0 && panel_bounds[npanels] == k),
+         "panels must cover the k rows of B");
+    Call call(h, stream, counters);
+    MV a = view(const_cast<double*>(A), m, k, lda), b = view(const_cast<double*>(B), k, n, ldb);
+    MV d = view(D, m, n, ldd);
+    MV cm = view(const_cast<double*>(C), m, n, ldc);
+    gemm(call.c, d, a, b, alpha, C ? &cm : nullptr, beta, diag, is_mv != 0, diag_offset, &pw);
+  });
+}
+
+int si_sym_alloc(si_handle h, size_t bytes, void** ptr, unsigned char handle_out[64]) {
+  return guard([&] {
+    need(h && ptr && handle_out, "null pointer");
+    need(bytes > 0, "empty allocation");
+    check(cudaSetDevice(h->h.device), "cudaSetDevice");
+    void* p = nullptr;
+    const cudaError_t err = cudaMalloc(&p, bytes);
+    if (err == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      throw Error(kENoMem, "cudaMalloc of an exchange buffer failed");
+    }
+    check(err, "cudaMalloc");
+    check(cudaMemset(p, 0, bytes), "cudaMemset");
+    check(cudaDeviceSynchronize(), "sync");  // zeroed before any peer or stream sees it
+    cudaIpcMemHandle_t ipc;
+    const cudaError_t e2 = cudaIpcGetMemHandle(&ipc, p);
+    if (e2 != cudaSuccess) {
+      cudaFree(p);
+      check(e2, "cudaIpcGetMemHandle");
+    }
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    std::memcpy(handle_out, &ipc, 64);
+    *ptr = p;
+  });
+}
+
+int si_sym_free(si_handle h, void* ptr) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    if (!ptr) return;
+    check(cudaSetDevice(h->h.device), "cudaSetDevice");
+    check(cudaDeviceSynchronize(), "sync");
+    check(cudaFree(ptr), "cudaFree");
+  });
+}
+
+int si_sym_open(si_handle h, const unsigned char handle[64], void** ptr) {
+  return guard([&] {
+    need(h && handle && ptr, "null pointer");
+    check(cudaSetDevice(h->h.device), "cudaSetDevice");
+    cudaIpcMemHandle_t ipc;
+    std::memcpy(&ipc, handle, 64);
+    check(cudaIpcOpenMemHandle(ptr, ipc, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  });
+}
+
+int si_sym_close(si_handle h, void* ptr) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    if (!ptr) return;
+    check(cudaSetDevice(h->h.device), "cudaSetDevice");
+    check(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle");
+  });
+}
+
+int si_stream_write_u32(si_handle h, uint32_t* addr, uint32_t value, void* stream) {
+  return guard([&] {
+    need(h && addr, "null pointer");
+    Call call(h, stream, nullptr);
+    check(stream_write_u32(addr, value, call.c.s), "stream write");
+  });
+}
+
+int si_stream_wait_u32(si_handle h, const uint32_t* addr, uint32_t value, void* stream) {
+  return guard([&] {
+    need(h && addr, "null pointer");
+    Call call(h, stream, nullptr);
+    check(stream_wait_u32(addr, value, call.c.s), "stream wait");
+  });
+}
+
+int si_copy_async(si_handle h, void* dst, const void* src, size_t bytes, void* stream) {
+  return guard([&] {
+    need(h && (bytes == 0 || (dst && src)), "null pointer");
+    Call call(h, stream, nullptr);
+    if (bytes) check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, call.c.s), "copy");
+  });
+}
+
 int si_lincomb(si_handle h, int64_t m, int64_t n, double cdiag, int nterms, const double* coefs,
                const double* const* X, const int64_t* ldx, double* D, int64_t ldd, void* stream) {
   return si_lincomb_ex(h, m, n, cdiag, 0, nterms, coefs, X, ldx, D, ldd, stream);

@@ -26,11 +26,24 @@ struct Epilogue {
   int64_t ldc = 0;
 };
 
+// Panel gate of a product whose right operand B is being gathered row panel
+// by row panel (sharded path): rows [bounds[p], bounds[p+1]) of
+// B may be read once ready[p] has reached `epoch` (wrap-safe compare).  The
+// flags are written by stream memory operations behind the copy of each panel.
+constexpr int kMaxPanels = 16;
+struct PanelWait {
+  const unsigned* ready = nullptr;
+  unsigned epoch = 0;
+  int npanels = 0;
+  int bounds[kMaxPanels + 1] = {};
+};
+
 void set_error(const std::string& msg);
 const char* get_error();
 
 // Kernel launchers (stream-ordered, no host sync).
-cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, cudaStream_t s);
+cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, cudaStream_t s,
+                            const PanelWait* pw = nullptr);
 cudaError_t launch_gemm_generic(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, cudaStream_t s);
 cudaError_t launch_gemv(const Mat& A, const Mat& X, Mat& D, const Epilogue& e, cudaStream_t s);
 bool tma_eligible(const Mat& A, const Mat& B, const Mat& D, const Epilogue& e);
@@ -52,6 +65,11 @@ cudaError_t launch_diag_split(Mat& P, Mat& B, const Mat& A, cudaStream_t s);
 cudaError_t launch_sumsq(const Mat& X, double* out_dev, double* work, cudaStream_t s);
 cudaError_t launch_inf_norm(const Mat& X, double* out_dev, double* work, cudaStream_t s);
 size_t reduce_work_elems(const Mat& X);
+// Stream memory operations (driver entry points; executed by the stream's
+// front end, no SM involved): *addr = value after prior work, and wait until
+// (int32)(*addr - value) >= 0.  Either address may be a peer (IPC) mapping.
+cudaError_t stream_write_u32(unsigned* addr, unsigned value, cudaStream_t s);
+cudaError_t stream_wait_u32(const unsigned* addr, unsigned value, cudaStream_t s);
 // Register-only DMMA throughput of the current device (synchronous).
 cudaError_t dmma_peak_tflops(int iters, double* tflops);
 // (X + X^T) / 2 into D (splitting.py:73)

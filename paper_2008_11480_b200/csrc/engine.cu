@@ -72,7 +72,7 @@ MV alloc(Ctx& c, int64_t rows, int64_t cols) {
 // ---------------------------------------------------------------------------
 
 void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV* C, double beta,
-          double diag, bool mv, int64_t doff) {
+          double diag, bool mv, int64_t doff, const PanelWait* pw) {
   if (A.v.cols != B.v.rows || D.v.rows != A.v.rows || D.v.cols != B.v.cols)
     throw Error(kEInval, "dimension mismatch in product");
   if (C && (C->v.rows != D.v.rows || C->v.cols != D.v.cols))
@@ -87,12 +87,20 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
   Mat d = D.v;
   cudaError_t err;
   Handle* h = c.h;
+  const bool gated = pw && pw->ready && pw->npanels > 0;
+  const bool use_tma = d.rows > 0 && d.cols > 4 && std::max(d.rows, d.cols) >= 128 &&
+                       A.v.cols > 0 && tma_eligible(A.v, B.v, d, e);
+  if (gated && !use_tma) {
+    // kernels without the in-kernel gate: the stream waits for every panel
+    for (int p = 0; p < pw->npanels; ++p)
+      check(stream_wait_u32(pw->ready + p, pw->epoch, c.s), "panel wait");
+  }
   if (d.rows == 0 || d.cols == 0) {
     err = cudaSuccess;
   } else if (d.cols <= 4) {
     err = launch_gemv(A.v, B.v, d, e, c.s);
     h->launches += 1;
-  } else if (std::max(d.rows, d.cols) >= 128 && A.v.cols > 0 && tma_eligible(A.v, B.v, d, e)) {
+  } else if (use_tma) {
     Handle::ProfRec rec{};
     if (h->profiling) {
       for (cudaEvent_t* ev : {&rec.start, &rec.stop}) {
@@ -106,7 +114,7 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
       rec.flops = 2.0 * (double)d.rows * (double)d.cols * (double)A.v.cols;
       check(cudaEventRecord(rec.start, c.s), "cudaEventRecord");
     }
-    err = launch_gemm_tma(A.v, B.v, d, e, c.s);
+    err = launch_gemm_tma(A.v, B.v, d, e, c.s, gated ? pw : nullptr);
     h->launches += 1;
     if (h->profiling && err == cudaSuccess) {
       check(cudaEventRecord(rec.stop, c.s), "cudaEventRecord");

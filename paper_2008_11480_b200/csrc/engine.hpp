@@ -86,9 +86,10 @@ MV view(double* p, int64_t rows, int64_t cols, int64_t ld);
 MV alloc(Ctx& c, int64_t rows, int64_t cols);
 
 // D = alpha * A @ B + beta * C + diag * I  (one counted product; mv=true ticks mvm)
+// `pw` (optional) gates the reads of B's row panels on arrival flags.
 void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha = 1.0,
           const MV* C = nullptr, double beta = 0.0, double diag = 0.0, bool mv = false,
-          int64_t doff = 0);
+          int64_t doff = 0, const PanelWait* pw = nullptr);
 MV gemm_new(Ctx& c, const MV& A, const MV& B, double alpha = 1.0, const MV* C = nullptr,
             double beta = 0.0, double diag = 0.0, bool mv = false);
 // I - X @ A

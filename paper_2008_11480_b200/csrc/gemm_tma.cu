@@ -22,6 +22,11 @@
 //  * Persistent grid (<= #SMs CTAs), grouped tile rasterisation for L2 reuse;
 //    the producer runs ahead into the next tile while consumers drain the
 //    epilogue.
+//  * Optional panel gate (sharded path): when B is a matrix whose row panels
+//    are still arriving from peer GPUs (copy engines, flags written by stream
+//    memory operations), the producer lane acquires panel p's flag before its
+//    first TMA load from that panel -- the gather overlaps the product k-slab
+//    by k-slab instead of completing before the launch.
 #include "common.cuh"
 
 #include <cuda.h>
@@ -77,6 +82,34 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Blocks until every row panel overlapping rows [k0, k1) of B has arrived.
+// `known` caches the panels already seen.  A flag that has not arrived after
+// 60 s means a broken exchange: trap (the launch fails) rather than hang.
+__device__ __forceinline__ void panel_gate(const PanelWait& pw, int k0, int k1, uint32_t& known) {
+  for (int p = 0; p < pw.npanels; ++p) {
+    if (pw.bounds[p + 1] <= k0 || pw.bounds[p] >= k1 || (known >> p) & 1u) continue;
+    const uint64_t t0 = globaltimer_ns();
+    while ((int)(ld_acquire_u32(pw.ready + p) - pw.epoch) < 0) {
+      __nanosleep(256);
+      if (globaltimer_ns() - t0 > 60ull * 1000000000ull) __trap();
+    }
+    known |= 1u << p;
+    // the panel was written by a copy engine (generic proxy); TMA reads it
+    // through the async proxy
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+}
+
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                             int c0, int c1) {
   asm volatile(
@@ -129,7 +162,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, double* __restrict__ D,
                         int64_t ldd, const double* __restrict__ C, int64_t ldc, int M, int N,
-                        int K, double alpha, double beta, double diag, int64_t doff) {
+                        int K, double alpha, double beta, double diag, int64_t doff,
+                        const __grid_constant__ PanelWait pw) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -161,6 +195,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
       int stage = 0;
       uint32_t phase = 0;
+      uint32_t known = pw.ready ? 0u : ~0u;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         int tm, tn;
         tile_coords(tile, num_m, num_n, tm, tn);
@@ -168,6 +203,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int nboxes = min(8, (N - n0 + 15) / 16);
         const uint32_t bytes = A_STAGE_BYTES + nboxes * B_BOX_BYTES;
         for (int kb = 0; kb < kblocks; ++kb) {
+          if (~known) panel_gate(pw, kb * BK, min(K, kb * BK + BK), known);
           mbar_wait(empty_bar(stage), phase ^ 1u);
           const uint32_t sa = base + stage * STAGE_BYTES;
           const uint32_t sb = sa + A_STAGE_BYTES;
@@ -346,7 +382,7 @@ bool tma_eligible(const Mat& A, const Mat& B, const Mat& D, const Epilogue& e) {
 }
 
 cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& e,
-                            cudaStream_t s) {
+                            cudaStream_t s, const PanelWait* pw) {
   CUtensorMap ta, tb;
   if (!make_map(&ta, A.p, A.rows, A.cols, A.ld, BK, BM) ||
       !make_map(&tb, B.p, B.rows, B.cols, B.ld, 16, BK)) {
@@ -369,8 +405,10 @@ cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& 
   const int M = (int)D.rows, N = (int)D.cols, K = (int)A.cols;
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
+  PanelWait gate;
+  if (pw && pw->ready && pw->npanels > 0) gate = *pw;
   gemm_f64_tma_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, D.p, D.ld, e.c, e.ldc, M, N, K,
-                                                        e.alpha, e.beta, e.diag, e.doff);
+                                                        e.alpha, e.beta, e.diag, e.doff, gate);
   return cudaGetLastError();
 }
 

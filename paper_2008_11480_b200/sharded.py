@@ -100,11 +100,19 @@ class CudaOps:
         m, k = a.shape
         n = b.shape[1]
         a = a.contiguous()
-        b = b.contiguous()
         if c is not None:
             c = c.contiguous()
         out = torch.empty((m, n), dtype=torch.float64, device=a.device)
         buf = _lib.counter_buf()
+        if not isinstance(b, torch.Tensor):  # peer.GatedOperand: panel-gated product
+            _lib.call("si_gemm_panels", _lib.handle(a.device.index), m, n, k, alpha, a.data_ptr(),
+                      k, b.t.data_ptr(), n, beta if c is not None else 0.0,
+                      c.data_ptr() if c is not None else None, n, diag, doff, out.data_ptr(), n,
+                      b.ready, b.epoch, _lib.i64_array(b.bounds), len(b.bounds) - 1, int(is_mv),
+                      buf, _lib.stream_ptr(a.device))
+            ctr.absorb(buf)
+            return out
+        b = b.contiguous()
         _lib.call("si_gemm_ex", _lib.handle(a.device.index), m, n, k, alpha, a.data_ptr(), k,
                   b.data_ptr(), n, beta if c is not None else 0.0,
                   c.data_ptr() if c is not None else None, n, diag, doff, out.data_ptr(), n,
@@ -130,7 +138,8 @@ class Sharded:
     t: torch.Tensor
     full: bool
     _gathered: torch.Tensor | None = None
-    _pending: tuple | None = None
+    _pending: object | None = None
+    _gated: object | None = None
 
 
 class ShardedEngine:
@@ -159,8 +168,29 @@ class ShardedEngine:
         if v._gathered is None:
             pending = v._pending if v._pending is not None else self.comm.start_gather(v.t)
             v._gathered = self.comm.finish(pending)
-            v._pending = None
         return v._gathered
+
+    def operand_of(self, v: Sharded):
+        """Right operand of a product: the full matrix, or -- with a peer-memory
+        comm in fused mode -- a gated operand whose panels may still be in
+        flight (the product waits for each panel inside the kernel)."""
+        if v.full:
+            return v.t
+        if v._gathered is not None:
+            return v._gathered
+        if v._gated is not None:
+            return v._gated
+        gate = getattr(self.comm, "gate", None)
+        if gate is not None and self.comm.world > 1:
+            if v._pending is None:
+                v._pending = self.comm.start_gather(v.t)
+            g = gate(v._pending)
+            if not isinstance(g, torch.Tensor):
+                v._gated = g
+                return g
+            v._gathered = g
+            return g
+        return self.full_of(v)
 
     def _produced(self, t: torch.Tensor, gather: bool) -> Sharded:
         v = Sharded(t, False)
@@ -176,7 +206,7 @@ class ShardedEngine:
 
     def mm(self, lhs: Sharded, rhs: Sharded, alpha=1.0, c: Sharded | None = None, beta=0.0,
            diag=0.0, mv=False, gather: bool = True) -> Sharded:
-        out = self.ops.gemm(self.rows_of(lhs), self.full_of(rhs), alpha,
+        out = self.ops.gemm(self.rows_of(lhs), self.operand_of(rhs), alpha,
                             self.rows_of(c) if c is not None else None, beta, diag, self.comm.r0,
                             mv, self.ctr)
         return self._produced(out, gather and not mv)

@@ -1,6 +1,11 @@
 import os
 import sys
 
+# streams blocked on peer-exchange flags must not share a hardware work queue
+# with streams that have to progress (paper_2008_11480_b200/peer.py); set
+# before CUDA initialises
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import numpy as np
 import pytest
 
