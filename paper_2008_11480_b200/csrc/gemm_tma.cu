@@ -33,6 +33,7 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 
 namespace si {
@@ -404,7 +405,13 @@ cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& 
   }
   const int M = (int)D.rows, N = (int)D.cols, K = (int)A.cols;
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
+  int grid = tiles < num_sms() ? tiles : num_sms();
+  // SI_GEMM_MAX_CTAS (tests only): cap the persistent grid so that two
+  // panel-gated products of different virtual ranks can be resident together
+  if (const char* cap = std::getenv("SI_GEMM_MAX_CTAS")) {
+    const int c = std::atoi(cap);
+    if (c > 0 && c < grid) grid = c;
+  }
   PanelWait gate;
   if (pw && pw->ready && pw->npanels > 0) gate = *pw;
   gemm_f64_tma_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, D.p, D.ld, e.c, e.ldc, M, N, K,

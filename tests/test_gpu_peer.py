@@ -267,3 +267,38 @@ def test_ipc_processes_composite_step(tmp_path):
         assert mmm == 3 * 22
     assert np.array_equal(np.concatenate(gs), st.estimate.cpu().numpy())
     assert np.array_equal(np.concatenate(fs), st.residual.cpu().numpy())
+
+
+def test_virtual_ranks_fused_gate_engine(monkeypatch):
+    """Mode "fused" end to end: the products take GatedOperands and wait for
+    the panels inside the DMMA kernel.  Safe with two virtual ranks on one GPU
+    only because the persistent grid is capped below half the SMs
+    (SI_GEMM_MAX_CTAS), so each rank's spinning product leaves room for the
+    other rank's producers."""
+    import paper_2008_11480_b200 as P
+
+    monkeypatch.setenv("SI_GEMM_MAX_CTAS", "64")
+    n, world = 512, 2
+    rng = np.random.default_rng(7)
+    g = rng.standard_normal((2 * n, n))
+    a = torch.as_tensor(g.T @ g / (2 * n) + 0.5 * np.eye(n), device="cuda")
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False, verify=False)
+    st = P.initial_series(sp, 0, 1, order=2)
+    ref = st
+    for _ in range(2):
+        ref = P.composite_step(ref, a, sp, P.CompositeSpec((2, 3, 4, 5)), 2)
+    engs, streams = _virtual_ranks(n, world, mode="fused")
+    outs = []
+    for eng, s in zip(engs, streams):
+        c = eng.comm
+        with torch.cuda.stream(s):
+            s.wait_stream(torch.cuda.default_stream())
+            A, Pm, B = eng.replicated(a), eng.replicated(sp.precond), eng.replicated(sp.residual)
+            gr = eng.local(st.estimate[c.r0:c.r1].clone())
+            fr = eng.local(st.residual[c.r0:c.r1].clone())
+            for _ in range(2):
+                gr, fr = eng.composite_step(gr, fr, A, Pm, B, (2, 3, 4, 5), 2)
+            outs.append((gr, fr))
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([e.rows_of(o[0]) for e, o in zip(engs, outs)]), ref.estimate)
+    assert torch.equal(torch.cat([e.rows_of(o[1]) for e, o in zip(engs, outs)]), ref.residual)
