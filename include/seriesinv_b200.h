@@ -285,6 +285,15 @@ SI_API int si_batched_composite_richardson(si_handle h, int64_t batch, int64_t n
                                     const double* consts, int64_t nconsts, int order_n,
                                     int iters, double* p_io, double* f_io, double* theta_io,
                                     int64_t* counters, void* stream);
+/* The same with separate inputs and outputs (the caller keeps its inputs:
+ * the reference's steps are pure, newton_schulz.py:58-72); in == out is
+ * allowed and equals si_batched_composite_richardson. */
+SI_API int si_batched_composite_richardson_ex(
+    si_handle h, int64_t batch, int64_t n, const double* a, const double* b, const double* precond,
+    const double* residual, int nrates, const int32_t* rates, const int32_t* plans,
+    const int64_t* plan_offsets, const double* consts, int64_t nconsts, int order_n, int iters,
+    const double* p_in, const double* f_in, const double* theta_in, double* p_out, double* f_out,
+    double* theta_out, int64_t* counters, void* stream);
 
 /* BASELINE config 1 shape (batch = 1, n <= 64) and batches of it: `iters` x
  * { plain Richardson with P_k; ns_step(order, plan) } with the state resident
@@ -295,6 +304,13 @@ SI_API int si_batched_ns_richardson(si_handle h, int64_t batch, int64_t n, const
                                     int64_t plan_len, const double* consts, int64_t nconsts,
                                     int iters, double* p_io, double* f_io, double* theta_io,
                                     int64_t* counters, void* stream);
+/* Separate inputs and outputs (in == out allowed). */
+SI_API int si_batched_ns_richardson_ex(si_handle h, int64_t batch, int64_t n, const double* a,
+                                       const double* b, int order, const int32_t* plan,
+                                       int64_t plan_len, const double* consts, int64_t nconsts,
+                                       int iters, const double* p_in, const double* f_in,
+                                       const double* theta_in, double* p_out, double* f_out,
+                                       double* theta_out, int64_t* counters, void* stream);
 
 #ifdef __cplusplus
 }

@@ -77,6 +77,12 @@ SIGNATURES: dict[str, list] = {
     "si_batched_composite_richardson": [
         _P, _I64, _I64, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _PI64, _P,
     ],
+    "si_batched_ns_richardson_ex": [_P, _I64, _I64, _P, _P, _I, _P, _I64, _P, _I64, _I, _P, _P, _P,
+                                    _P, _P, _P, _PI64, _P],
+    "si_batched_composite_richardson_ex": [
+        _P, _I64, _I64, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _P, _P, _P,
+        _PI64, _P,
+    ],
 }
 
 _lib = None

@@ -48,16 +48,20 @@ def batched_composite_richardson(a, b, precond, residual, p, f, theta, rates, or
         raise ValueError("rates must be positive integers")
     if order_n < 1:
         raise ValueError("order_n must be >= 1")
-    p_io = as_device(p).clone()
-    f_io = as_device(f).clone()
-    th_io = as_device(theta).clone()
+    p_in = as_device(p).contiguous()
+    f_in = as_device(f).contiguous()
+    th_in = as_device(theta).contiguous()
+    if p_in.shape != a.shape or f_in.shape != a.shape or th_in.shape != b.shape:
+        raise ValueError("dimension mismatch")
+    p_io, f_io, th_io = torch.empty_like(p_in), torch.empty_like(f_in), torch.empty_like(th_in)
     plans = [geometric_base_plan(x) if x > 1 else None for x in rates]
     code, offsets, consts = encode_many(plans)
     buf = _lib.counter_buf()
-    _lib.call("si_batched_composite_richardson", _lib.handle(a.device.index), batch, n,
+    _lib.call("si_batched_composite_richardson_ex", _lib.handle(a.device.index), batch, n,
               a.data_ptr(), b.data_ptr(), precond.data_ptr(), residual.data_ptr(), len(rates),
               _lib.i32_array(list(rates)), _lib.i32_array(code), _lib.i64_array(offsets),
-              _lib.f64_array(consts), len(consts), order_n, iters, p_io.data_ptr(), f_io.data_ptr(),
+              _lib.f64_array(consts), len(consts), order_n, iters, p_in.data_ptr(),
+              f_in.data_ptr(), th_in.data_ptr(), p_io.data_ptr(), f_io.data_ptr(),
               th_io.data_ptr(), buf, _lib.stream_ptr(a.device))
     if ctr is not None:
         ctr.absorb(buf)
@@ -84,15 +88,17 @@ def batched_ns_richardson(a, b, p, f, theta, order: int, iters: int, plan=None,
         raise ValueError("order must be >= 1")
     if plan is not None and plan.order_h != order:
         raise ValueError(f"plan order {plan.order_h} != iteration order {order}")
-    p_io = as_device(p).reshape(batch, n, n).clone()
-    f_io = as_device(f).reshape(batch, n, n).clone()
-    th_io = as_device(theta).reshape(batch, n).clone()
+    p_in = as_device(p).reshape(batch, n, n).contiguous()
+    f_in = as_device(f).reshape(batch, n, n).contiguous()
+    th_in = as_device(theta).reshape(batch, n).contiguous()
+    p_io, f_io, th_io = torch.empty_like(p_in), torch.empty_like(f_in), torch.empty_like(th_in)
     code, consts = encode_plan(plan) if plan is not None else ([], [])
     buf = _lib.counter_buf()
-    _lib.call("si_batched_ns_richardson", _lib.handle(a.device.index), batch, n, a.data_ptr(),
+    _lib.call("si_batched_ns_richardson_ex", _lib.handle(a.device.index), batch, n, a.data_ptr(),
               b.contiguous().data_ptr(), order, _lib.i32_array(code) if code else None, len(code),
-              _lib.f64_array(consts) if consts else None, len(consts), iters, p_io.data_ptr(),
-              f_io.data_ptr(), th_io.data_ptr(), buf, _lib.stream_ptr(a.device))
+              _lib.f64_array(consts) if consts else None, len(consts), iters, p_in.data_ptr(),
+              f_in.data_ptr(), th_in.data_ptr(), p_io.data_ptr(), f_io.data_ptr(),
+              th_io.data_ptr(), buf, _lib.stream_ptr(a.device))
     if ctr is not None:
         ctr.absorb(buf)
     if squeeze:

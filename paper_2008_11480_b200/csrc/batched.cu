@@ -22,7 +22,9 @@
 #include <bitset>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <functional>
+#include <string>
 #include <unordered_map>
 
 #include "batched.hpp"
@@ -385,7 +387,10 @@ struct BatchArgs {
   const double* b;
   const double* precond;
   const double* residual;
-  double* p_io;
+  const double* p_in;  // carried state in (may equal the outputs)
+  const double* f_in;
+  const double* theta_in;
+  double* p_io;  // carried state out
   double* f_io;
   double* theta_io;
   const DOp* ops;
@@ -584,10 +589,10 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
   double2 pf_p[PFD], pf_b[PFD];
   for (int64_t sys = blockIdx.x; sys < p.batch; sys += gridDim.x) {
     load_mat<NP>(mslot(p.sA), p.a + sys * nn, n);
-    load_mat<NP>(mslot(p.sG), p.p_io + sys * nn, n);
-    load_mat<NP>(mslot(p.sF), p.f_io + sys * nn, n);
+    load_mat<NP>(mslot(p.sG), p.p_in + sys * nn, n);
+    load_mat<NP>(mslot(p.sF), p.f_in + sys * nn, n);
     if (threadIdx.x < NP) {
-      vslot(p.sT)[threadIdx.x] = threadIdx.x < n ? p.theta_io[sys * n + threadIdx.x] : 0.0;
+      vslot(p.sT)[threadIdx.x] = threadIdx.x < n ? p.theta_in[sys * n + threadIdx.x] : 0.0;
       vslot(p.sb)[threadIdx.x] = threadIdx.x < n ? p.b[sys * n + threadIdx.x] : 0.0;
     }
     __syncthreads();
@@ -750,8 +755,9 @@ void record_plain(Recipe& q) {
 
 template <int NP>
 Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, const double* b,
-                const double* precond, const double* residual, int iters, double* p_io,
-                double* f_io, double* theta_io) {
+                const double* precond, const double* residual, int iters, const double* p_in,
+                const double* f_in, const double* theta_in, double* p_io, double* f_io,
+                double* theta_io) {
   using Gm = Geo<NP>;
   Counters per;
   for (const BOp& o : q.r.ops) {
@@ -760,7 +766,15 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
   }
   per.mmm *= iters;
   per.mvm *= iters;
-  if (batch == 0 || iters == 0) return per;
+  if (batch == 0) return per;
+  if (iters == 0) {  // outputs = inputs
+    const size_t mat = (size_t)batch * n * n * sizeof(double), vec = (size_t)batch * n * 8;
+    if (p_io != p_in) check(cudaMemcpyAsync(p_io, p_in, mat, cudaMemcpyDeviceToDevice, c.s), "copy");
+    if (f_io != f_in) check(cudaMemcpyAsync(f_io, f_in, mat, cudaMemcpyDeviceToDevice, c.s), "copy");
+    if (theta_io != theta_in)
+      check(cudaMemcpyAsync(theta_io, theta_in, vec, cudaMemcpyDeviceToDevice, c.s), "copy");
+    return per;
+  }
   if ((int)q.r.ops.size() > kMaxOps) throw Error(kEInval, "resident program too long");
 
   schedule_min_live(q.r, {q.A, q.bv}, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}});
@@ -854,24 +868,40 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
                       csts.size() * sizeof(double);
   if (smem > 227 * 1024) throw Error(kEInval, "resident program needs too much shared memory");
 
+  // program + constants, uploaded once per distinct program (handle cache)
   const size_t op_bytes = dev_ops.size() * sizeof(DOp);
-  MV dops = alloc(c, (int64_t)((op_bytes + csts.size() * sizeof(double) + 7) / 8), 1);
-  check(cudaMemcpyAsync(dops.v.p, dev_ops.data(), op_bytes, cudaMemcpyHostToDevice, c.s),
-        "memcpy program");
-  check(cudaMemcpyAsync(reinterpret_cast<char*>(dops.v.p) + op_bytes, csts.data(),
-                        csts.size() * sizeof(double), cudaMemcpyHostToDevice, c.s),
-        "memcpy constants");
+  std::string blob(op_bytes + csts.size() * sizeof(double), '\0');
+  std::memcpy(&blob[0], dev_ops.data(), op_bytes);
+  std::memcpy(&blob[op_bytes], csts.data(), csts.size() * sizeof(double));
+  void* prog_dev = nullptr;
+  {
+    auto it = c.h->programs.find(blob);
+    if (it != c.h->programs.end()) {
+      prog_dev = it->second;
+    } else {
+      check(cudaMalloc(&prog_dev, blob.size()), "cudaMalloc");
+      const cudaError_t err =
+          cudaMemcpyAsync(prog_dev, blob.data(), blob.size(), cudaMemcpyHostToDevice, c.s);
+      if (err == cudaSuccess) check(cudaStreamSynchronize(c.s), "sync");  // blob is freed below
+      if (err != cudaSuccess) cudaFree(prog_dev);
+      check(err, "memcpy program");
+      c.h->programs.emplace(blob, prog_dev);
+    }
+  }
   BatchArgs args{};
   args.a = a;
   args.b = b;
   args.precond = precond;
   args.residual = residual;
+  args.p_in = p_in;
+  args.f_in = f_in;
+  args.theta_in = theta_in;
   args.p_io = p_io;
   args.f_io = f_io;
   args.theta_io = theta_io;
-  args.ops = reinterpret_cast<const DOp*>(dops.v.p);
+  args.ops = reinterpret_cast<const DOp*>(prog_dev);
   args.nops = (int)ops.size();
-  args.cst = reinterpret_cast<const double*>(reinterpret_cast<char*>(dops.v.p) + op_bytes);
+  args.cst = reinterpret_cast<const double*>(reinterpret_cast<char*>(prog_dev) + op_bytes);
   args.ncst = (int)csts.size();
   args.nmat = al.nmat;
   args.nvec = al.nvec;
@@ -936,7 +966,9 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
                                       const double* b, const double* precond,
                                       const double* residual, const std::vector<int>& rates,
                                       const std::vector<const PlanNode*>& plans, int order_n,
-                                      int iters, double* p_io, double* f_io, double* theta_io) {
+                                      int iters, const double* p_in, const double* f_in,
+                                      const double* theta_in, double* p_io, double* f_io,
+                                      double* theta_io) {
   Recipe q = new_recipe();
   record_plain(q);
   // composite_step (newton_schulz.py:177-228).  The NS part S_n(F) G is
@@ -958,12 +990,15 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
   q.gn = q.r.gemm(rc, nsp, 1.0, tc, 1.0);
   q.fn = q.r.residual(q.gn, q.A);
   if (n <= 32)
-    return launch<32>(c, q, batch, n, a, b, precond, residual, iters, p_io, f_io, theta_io);
-  return launch<64>(c, q, batch, n, a, b, precond, residual, iters, p_io, f_io, theta_io);
+    return launch<32>(c, q, batch, n, a, b, precond, residual, iters, p_in, f_in, theta_in, p_io,
+                      f_io, theta_io);
+  return launch<64>(c, q, batch, n, a, b, precond, residual, iters, p_in, f_in, theta_in, p_io,
+                    f_io, theta_io);
 }
 
 Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a, const double* b,
-                               int order, const PlanNode* plan, int iters, double* p_io,
+                               int order, const PlanNode* plan, int iters, const double* p_in,
+                               const double* f_in, const double* theta_in, double* p_io,
                                double* f_io, double* theta_io) {
   Recipe q = new_recipe();
   record_plain(q);
@@ -972,8 +1007,10 @@ Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a
   q.gn = gnew == q.G ? q.r.copy(q.G) : gnew;
   q.fn = q.r.residual(q.gn, q.A);
   if (n <= 32)
-    return launch<32>(c, q, batch, n, a, b, nullptr, nullptr, iters, p_io, f_io, theta_io);
-  return launch<64>(c, q, batch, n, a, b, nullptr, nullptr, iters, p_io, f_io, theta_io);
+    return launch<32>(c, q, batch, n, a, b, nullptr, nullptr, iters, p_in, f_in, theta_in, p_io,
+                      f_io, theta_io);
+  return launch<64>(c, q, batch, n, a, b, nullptr, nullptr, iters, p_in, f_in, theta_in, p_io,
+                    f_io, theta_io);
 }
 
 }  // namespace si

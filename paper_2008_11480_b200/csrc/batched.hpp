@@ -16,12 +16,16 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
                                       const double* b, const double* precond,
                                       const double* residual, const std::vector<int>& rates,
                                       const std::vector<const PlanNode*>& plans, int order_n,
-                                      int iters, double* p_io, double* f_io, double* theta_io);
+                                      int iters, const double* p_in, const double* f_in,
+                                      const double* theta_in, double* p_out, double* f_out,
+                                      double* theta_out);
 
 // BASELINE config 1 (batch = 1) and batches of it: `iters` x { plain
 // Richardson with P_k; ns_step(order, plan) (newton_schulz.py:150-174) }.
 Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a, const double* b,
-                               int order, const PlanNode* plan, int iters, double* p_io,
-                               double* f_io, double* theta_io);
+                               int order, const PlanNode* plan, int iters, const double* p_in,
+                               const double* f_in, const double* theta_in, double* p_out,
+                               double* f_out, double* theta_out);
+// Inputs may equal outputs (in place).
 
 }  // namespace si

@@ -135,6 +135,7 @@ int si_destroy(si_handle h) {
       if (h->h.side[i]) cudaStreamDestroy(h->h.side[i]);
     if (h->h.red_work) cudaFree(h->h.red_work);
     if (h->h.scalar) cudaFree(h->h.scalar);
+    for (auto& kv : h->h.programs) cudaFree(kv.second);
     if (h->h.pool) cudaMemPoolDestroy(h->h.pool);
     delete h;
   });
@@ -690,8 +691,23 @@ int si_batched_composite_richardson(si_handle h, int64_t batch, int64_t n, const
                                     const double* consts, int64_t nconsts, int order_n,
                                     int iters, double* p_io, double* f_io, double* theta_io,
                                     int64_t* counters, void* stream) {
+  return si_batched_composite_richardson_ex(h, batch, n, a, b, precond, residual, nrates, rates,
+                                            plans, plan_offsets, consts, nconsts, order_n, iters,
+                                            p_io, f_io, theta_io, p_io, f_io, theta_io, counters,
+                                            stream);
+}
+
+int si_batched_composite_richardson_ex(si_handle h, int64_t batch, int64_t n, const double* a,
+                                       const double* b, const double* precond,
+                                       const double* residual, int nrates, const int32_t* rates,
+                                       const int32_t* plans, const int64_t* plan_offsets,
+                                       const double* consts, int64_t nconsts, int order_n,
+                                       int iters, const double* p_in, const double* f_in,
+                                       const double* theta_in, double* p_out, double* f_out,
+                                       double* theta_out, int64_t* counters, void* stream) {
   return guard([&] {
-    need(h && a && b && precond && residual && rates && p_io && f_io && theta_io,
+    need(h && a && b && precond && residual && rates && p_in && f_in && theta_in && p_out &&
+             f_out && theta_out,
          "null pointer");
     need(batch >= 0 && n >= 1 && n <= kBatchMaxN, "batched path supports 1 <= n <= 64");
     need(nrates >= 1 && nrates <= kBatchMaxRates, "batched path supports 1..4 rates");
@@ -709,7 +725,8 @@ int si_batched_composite_richardson(si_handle h, int64_t batch, int64_t n, const
     }
     Call call(h, stream, nullptr);
     Counters per = batched_composite_richardson(call.c, batch, n, a, b, precond, residual, rv, pv,
-                                                order_n, iters, p_io, f_io, theta_io);
+                                                order_n, iters, p_in, f_in, theta_in, p_out,
+                                                f_out, theta_out);
     if (counters) {
       counters[0] += per.mmm;
       counters[1] += per.mvm;
@@ -721,15 +738,26 @@ int si_batched_ns_richardson(si_handle h, int64_t batch, int64_t n, const double
                              const double* b, int order, const int32_t* plan, int64_t plan_len,
                              const double* consts, int64_t nconsts, int iters, double* p_io,
                              double* f_io, double* theta_io, int64_t* counters, void* stream) {
+  return si_batched_ns_richardson_ex(h, batch, n, a, b, order, plan, plan_len, consts, nconsts,
+                                     iters, p_io, f_io, theta_io, p_io, f_io, theta_io, counters,
+                                     stream);
+}
+
+int si_batched_ns_richardson_ex(si_handle h, int64_t batch, int64_t n, const double* a,
+                                const double* b, int order, const int32_t* plan,
+                                int64_t plan_len, const double* consts, int64_t nconsts,
+                                int iters, const double* p_in, const double* f_in,
+                                const double* theta_in, double* p_out, double* f_out,
+                                double* theta_out, int64_t* counters, void* stream) {
   return guard([&] {
-    need(h && a && b && p_io && f_io && theta_io, "null pointer");
+    need(h && a && b && p_in && f_in && theta_in && p_out && f_out && theta_out, "null pointer");
     need(batch >= 0 && n >= 1 && n <= kBatchMaxN, "batched path supports 1 <= n <= 64");
     need(order >= 1 && iters >= 0, "bad order / iters");
     PlanPtr pl = opt_plan(plan, plan_len, consts, nconsts);
     if (pl) need(plan_order_of(*pl) == order, "plan order != iteration order");
     Call call(h, stream, nullptr);
-    Counters per = batched_ns_richardson(call.c, batch, n, a, b, order, pl.get(), iters, p_io,
-                                         f_io, theta_io);
+    Counters per = batched_ns_richardson(call.c, batch, n, a, b, order, pl.get(), iters, p_in,
+                                         f_in, theta_in, p_out, f_out, theta_out);
     if (counters) {
       counters[0] += per.mmm;
       counters[1] += per.mvm;

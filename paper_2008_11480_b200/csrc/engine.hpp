@@ -6,6 +6,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -45,6 +46,9 @@ struct Handle {
   void* (*alloc_fn)(void* ctx, size_t bytes, void* stream) = nullptr;
   void (*free_fn)(void* ctx, void* ptr, void* stream) = nullptr;
   void* alloc_ctx = nullptr;
+  // Resident-kernel programs (batched.cu) already on the device, keyed by
+  // their encoded bytes: repeated launches of the same run skip the upload.
+  std::unordered_map<std::string, void*> programs;
 };
 
 // Owning device buffer, released stream-ordered on its root stream (the
