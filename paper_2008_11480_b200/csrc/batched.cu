@@ -723,6 +723,320 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
     for (int k = 0; k < p.nops; ++k) p.prof[k] = prof_acc[k];
 }
 
+// ---------------------------------------------------------------- clusters
+// Latency-bound small batches (config 1: ONE 64 x 64 system): a thread-block
+// cluster of CL CTAs (CL SMs) works on one system.  Every CTA keeps a full
+// copy of every slot but computes only its block of NP/CL rows of each op;
+// results that a later op reads in full (right operands of products, the x of
+// a GEMV, loop-carried ones included) are also stored into the peers' copies
+// through distributed shared memory, and cluster barriers order those
+// exchanges (flags decided on the host, cluster_flags()).
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t peer_addr(const double* local, unsigned cta) {
+  const uint32_t la = static_cast<uint32_t>(__cvta_generic_to_shared(local));
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(cta));
+  return ra;
+}
+__device__ __forceinline__ void st_peer2(const double* local, unsigned cta, double x, double y) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(peer_addr(local, cta)), "d"(x),
+               "d"(y)
+               : "memory");
+}
+__device__ __forceinline__ void st_peer1(const double* local, unsigned cta, double x) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(peer_addr(local, cta)), "d"(x) : "memory");
+}
+
+constexpr int kClusterThreads = 256;  // 8 warps per CTA
+constexpr uint8_t kSyncCta = 1, kSyncCluster = 2, kBcast = 4;
+
+// Rows [rbase, rbase + 64/CL) of one 64 x 64 x 64 product, 8 warps.
+template <int CL, int MODE>
+__device__ __forceinline__ void gemm_rows(const double* A, const double* B, const double* C,
+                                          double* D, const double* cst, int n, int warp, int g,
+                                          int t, int rbase, bool bcast, unsigned rank) {
+  using G = Geo<64>;
+  constexpr int RT = 64 / CL / 8;             // 8-row tiles per CTA
+  constexpr int NTW = RT >= 2 ? 2 : 1;        // column tiles per warp
+  constexpr int CG = 8 / NTW, RG = 8 / CG;    // warp grid
+  constexpr int MTW = RT / RG;                // row tiles per warp
+  const int r0 = rbase + (warp / CG) * MTW * 8, c0 = (warp % CG) * NTW * 8;
+  double acc[MTW][NTW][2];
+#pragma unroll
+  for (int mi = 0; mi < MTW; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NTW; ++ni) {
+      const int row = r0 + mi * 8 + g, col = c0 + ni * 8 + 2 * t;
+      if (MODE == 2) {
+        const double2 cv = *reinterpret_cast<const double2*>(C + G::idx(row, col));
+        acc[mi][ni][0] = cv.x;
+        acc[mi][ni][1] = cv.y;
+      } else if (MODE == 1) {
+        acc[mi][ni][0] = (row == col && row < n) ? -1.0 : 0.0;
+        acc[mi][ni][1] = (row == col + 1 && row < n) ? -1.0 : 0.0;
+      } else {
+        acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      }
+    }
+  double af[2][MTW], bf[2][NTW];
+#pragma unroll
+  for (int mi = 0; mi < MTW; ++mi) af[0][mi] = A[G::idx(r0 + mi * 8 + g, t)];
+#pragma unroll
+  for (int ni = 0; ni < NTW; ++ni) bf[0][ni] = B[G::idx(t, c0 + ni * 8 + g)];
+#pragma unroll
+  for (int kk = 0; kk < 64; kk += 4) {
+    const int cur = (kk >> 2) & 1, nxt = cur ^ 1;
+    if (kk + 4 < 64) {
+#pragma unroll
+      for (int mi = 0; mi < MTW; ++mi) af[nxt][mi] = A[G::idx(r0 + mi * 8 + g, kk + 4 + t)];
+#pragma unroll
+      for (int ni = 0; ni < NTW; ++ni) bf[nxt][ni] = B[G::idx(kk + 4 + t, c0 + ni * 8 + g)];
+    }
+#pragma unroll
+    for (int mi = 0; mi < MTW; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NTW; ++ni)
+        dmma(acc[mi][ni][0], acc[mi][ni][1], af[cur][mi], bf[cur][ni]);
+  }
+#pragma unroll
+  for (int mi = 0; mi < MTW; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NTW; ++ni) {
+      const int row = r0 + mi * 8 + g, col = c0 + ni * 8 + 2 * t;
+      double v0 = acc[mi][ni][0], v1 = acc[mi][ni][1];
+      if (MODE == 1) {
+        v0 = flip(v0);
+        v1 = flip(v1);
+      } else if (MODE == 3) {
+        double2 cv = make_double2(0.0, 0.0);
+        if (C) cv = *reinterpret_cast<const double2*>(C + G::idx(row, col));
+        v0 = epi(v0, cst[0], cst[1], cv.x);
+        v1 = epi(v1, cst[0], cst[1], cv.y);
+        if (cst[2] != 0.0 && row < n) {
+          if (row == col) v0 = __dadd_rn(v0, cst[2]);
+          if (row == col + 1) v1 = __dadd_rn(v1, cst[2]);
+        }
+      }
+      double* dp = D + G::idx(row, col);
+      *reinterpret_cast<double2*>(dp) = make_double2(v0, v1);
+      if (bcast)
+#pragma unroll
+        for (unsigned q = 0; q < CL; ++q)
+          if (q != rank) st_peer2(dp, q, v0, v1);
+    }
+}
+
+template <int CL>
+__global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(BatchArgs p) {
+  constexpr int NP = 64, RB = NP / CL, TH = kClusterThreads;
+  using G = Geo<64>;
+  extern __shared__ double sm[];
+  DOp* prog = reinterpret_cast<DOp*>(sm + (size_t)p.nmat * G::SLOT + (size_t)p.nvec * NP);
+  double* cst = reinterpret_cast<double*>(prog + p.nops);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int n = p.n;
+  const int64_t nn = (int64_t)n * n;
+  const unsigned rank = cluster_rank();
+  const int rbase = (int)rank * RB;
+  auto mslot = [&](int s) { return sm + (size_t)s * G::SLOT; };
+  auto vslot = [&](int s) { return sm + (size_t)p.nmat * G::SLOT + (size_t)s * NP; };
+  auto load_full = [&](double* dst, const double* src) {
+    for (int i = threadIdx.x; i < NP * NP; i += TH) {
+      const int r = i / NP, c = i % NP;
+      dst[G::idx(r, c)] = (r < n && c < n) ? src[r * n + c] : 0.0;
+    }
+  };
+  for (int i = threadIdx.x; i < p.nops * (int)sizeof(DOp) / 16; i += TH)
+    reinterpret_cast<int4*>(prog)[i] = reinterpret_cast<const int4*>(p.ops)[i];
+  for (int i = threadIdx.x; i < p.ncst; i += TH) cst[i] = p.cst[i];
+
+  const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  for (int64_t sys = cid; sys < p.batch; sys += ncl) {
+    load_full(mslot(p.sA), p.a + sys * nn);
+    load_full(mslot(p.sG), p.p_in + sys * nn);
+    load_full(mslot(p.sF), p.f_in + sys * nn);
+    if (threadIdx.x < NP) {
+      vslot(p.sT)[threadIdx.x] = threadIdx.x < n ? p.theta_in[sys * n + threadIdx.x] : 0.0;
+      vslot(p.sb)[threadIdx.x] = threadIdx.x < n ? p.b[sys * n + threadIdx.x] : 0.0;
+    }
+    cluster_sync_all();  // every CTA of the cluster is running and loaded
+    for (int it = 0; it < p.iters; ++it) {
+      for (int k = 0; k < p.nops; ++k) {
+        const DOp o = prog[k];
+        const double* oc = cst + o.cidx;
+        const bool bc = (o.sync & kBcast) != 0;
+        if (o.kind == OP_GEMM) {
+          const double* A = mslot(o.a);
+          const double* B = mslot(o.b);
+          const double* C = o.c >= 0 ? mslot(o.c) : nullptr;
+          double* D = mslot(o.dst);
+          switch (o.mode) {
+            case 0: gemm_rows<CL, 0>(A, B, C, D, oc, n, warp, g, t, rbase, bc, rank); break;
+            case 1: gemm_rows<CL, 1>(A, B, C, D, oc, n, warp, g, t, rbase, bc, rank); break;
+            case 2: gemm_rows<CL, 2>(A, B, C, D, oc, n, warp, g, t, rbase, bc, rank); break;
+            default: gemm_rows<CL, 3>(A, B, C, D, oc, n, warp, g, t, rbase, bc, rank); break;
+          }
+        } else if (o.kind == OP_GEMV) {
+          if (warp < RB / 8) {
+            const double* A = mslot(o.a);
+            const double* x = vslot(o.b);
+            const int r0 = rbase + warp * 8;
+            double acc[2][2] = {};
+#pragma unroll
+            for (int kk = 0; kk < NP; kk += 4) {
+              const double af = A[G::idx(r0 + g, kk + t)];
+              const double bf = g == 0 ? x[kk + t] : 0.0;
+              dmma(acc[(kk >> 2) & 1][0], acc[(kk >> 2) & 1][1], af, bf);
+            }
+            if (t == 0) {
+              const int row = r0 + g;
+              const double s = __dadd_rn(acc[0][0], acc[1][0]);
+              const double cv = o.c >= 0 ? vslot(o.c)[row] : 0.0;
+              const double v = o.mode == 1   ? __dsub_rn(s, cv)
+                               : o.mode == 2 ? __dsub_rn(cv, s)
+                                             : epi(s, oc[0], oc[1], cv);
+              double* dp = vslot(o.dst) + row;
+              *dp = v;
+              if (bc)
+                for (unsigned q = 0; q < CL; ++q)
+                  if (q != rank) st_peer1(dp, q, v);
+            }
+          }
+        } else if (o.kind == OP_LOAD) {
+          load_full(mslot(o.dst), (o.mode ? p.residual : p.precond) + sys * nn);
+        } else if (o.mode) {  // LIN over vectors, own rows
+          if (threadIdx.x < RB) {
+            const int row = rbase + threadIdx.x;
+            double acc = 0.0;
+            for (int j = 0; j < o.nterms; ++j) {
+              const double xv = vslot(o.t[j])[row];
+              acc = __dadd_rn(acc, oc[1 + j] == 1.0 ? xv : __dmul_rn(oc[1 + j], xv));
+            }
+            double* dp = vslot(o.dst) + row;
+            *dp = acc;
+            if (bc)
+              for (unsigned q = 0; q < CL; ++q)
+                if (q != rank) st_peer1(dp, q, acc);
+          }
+        } else {  // LIN over matrices, own rows
+          double* D = mslot(o.dst);
+          for (int i = rbase * NP + threadIdx.x; i < (rbase + RB) * NP; i += TH) {
+            const int r = i / NP;
+            const int c = G::col_at(r, i % NP);
+            double acc = (r == c && r < n) ? oc[0] : 0.0;
+            for (int j = 0; j < o.nterms; ++j) {
+              const double xv = mslot(o.t[j])[i];
+              acc = __dadd_rn(acc, oc[1 + j] == 1.0 ? xv : __dmul_rn(oc[1 + j], xv));
+            }
+            D[i] = acc;
+            if (bc)
+              for (unsigned q = 0; q < CL; ++q)
+                if (q != rank) st_peer1(D + i, q, acc);
+          }
+        }
+        if (o.sync & kSyncCluster)
+          cluster_sync_all();
+        else if (o.sync & kSyncCta)
+          __syncthreads();
+      }
+      if (p.rG != p.sG || p.rF != p.sF || p.rT != p.sT) {  // carries (full local copies)
+        for (int i = threadIdx.x; i < NP * NP; i += TH) {
+          if (p.rG != p.sG) mslot(p.sG)[i] = mslot(p.rG)[i];
+          if (p.rF != p.sF) mslot(p.sF)[i] = mslot(p.rF)[i];
+        }
+        if (p.rT != p.sT && threadIdx.x < NP) vslot(p.sT)[threadIdx.x] = vslot(p.rT)[threadIdx.x];
+        cluster_sync_all();
+      }
+    }
+    // own rows of the outputs
+    for (int i = rbase * n + threadIdx.x; i < min(rbase + RB, n) * n; i += TH) {
+      const int r = i / n, c = i % n;
+      p.p_io[sys * nn + i] = mslot(p.sG)[G::idx(r, c)];
+      p.f_io[sys * nn + i] = mslot(p.sF)[G::idx(r, c)];
+    }
+    if (threadIdx.x < RB && rbase + (int)threadIdx.x < n)
+      p.theta_io[sys * n + rbase + threadIdx.x] = vslot(p.sT)[rbase + threadIdx.x];
+    cluster_sync_all();  // peers are done with this system before slots are reloaded
+  }
+}
+
+// Barrier / exchange flags of a cluster program (ops already on physical
+// slots; `vec_dst[k]`: op k writes a vector slot; `bcast[k]`: its result is
+// read in full somewhere, so it goes to every peer's copy too).  Before op
+// j+1: a cluster barrier when it reads in full a slot broadcast since the last
+// cluster barrier, or broadcasts into a slot read in full / broadcast since
+// then; otherwise a CTA barrier on the usual RAW / WAR / WAW rule.  The last
+// op of an iteration ends with a cluster barrier.
+std::vector<uint8_t> cluster_flags(const std::vector<BOp>& ops, const std::vector<bool>& bcast) {
+  const size_t m = ops.size();
+  std::vector<uint8_t> fl(m, 0);
+  auto key = [](int s, bool vec) { return vec ? 1000 + s : s; };
+  struct Acc {
+    std::vector<int> rloc, rfull;
+    int w;
+    bool full_write = false;  // OP_LOAD: every CTA writes all rows of its copy
+  };
+  std::vector<Acc> acc(m);
+  for (size_t k = 0; k < m; ++k) {
+    const BOp& o = ops[k];
+    Acc& a = acc[k];
+    const bool vdst = (o.kind == OP_GEMV) || (o.kind == OP_LIN && o.vec);
+    a.w = key(o.dst, vdst);
+    if (o.kind == OP_GEMM) {
+      a.rloc = {key(o.a, false)};
+      if (o.c >= 0) a.rloc.push_back(key(o.c, false));
+      a.rfull = {key(o.b, false)};
+    } else if (o.kind == OP_GEMV) {
+      a.rloc = {key(o.a, false)};
+      if (o.c >= 0) a.rloc.push_back(key(o.c, true));
+      a.rfull = {key(o.b, true)};
+    } else if (o.kind == OP_LIN) {
+      for (int j = 0; j < o.nterms; ++j) a.rloc.push_back(key(o.t[j], o.vec));
+    } else {
+      a.full_write = true;
+    }
+  }
+  auto in = [](const std::vector<int>& v, int s) { return std::find(v.begin(), v.end(), s) != v.end(); };
+  std::vector<int> rdC, wrC, rdF, wrB, wrF;
+  for (size_t k = 0; k < m; ++k) {
+    const Acc& a = acc[k];
+    if (k > 0) {
+      bool clu = false, cta = false;
+      for (int s : a.rfull) clu |= in(wrB, s);
+      if (bcast[k]) clu |= in(rdF, a.w) || in(wrB, a.w) || in(wrF, a.w);
+      for (int s : a.rloc) cta |= in(wrC, s);
+      for (int s : a.rfull) cta |= in(wrC, s);
+      cta |= in(rdC, a.w) || in(wrC, a.w);
+      if (clu) {
+        fl[k - 1] |= kSyncCluster;
+        rdC.clear(); wrC.clear(); rdF.clear(); wrB.clear(); wrF.clear();
+      } else if (cta) {
+        fl[k - 1] |= kSyncCta;
+        rdC.clear(); wrC.clear();
+      }
+    }
+    rdC.insert(rdC.end(), a.rloc.begin(), a.rloc.end());
+    rdC.insert(rdC.end(), a.rfull.begin(), a.rfull.end());
+    rdF.insert(rdF.end(), a.rfull.begin(), a.rfull.end());
+    wrC.push_back(a.w);
+    if (bcast[k]) wrB.push_back(a.w);
+    if (a.full_write) wrF.push_back(a.w);
+  }
+  if (m) fl[m - 1] |= kSyncCluster;
+  for (size_t k = 0; k < m; ++k)
+    if (bcast[k]) fl[k] |= kBcast;
+  return fl;
+}
+
 int num_sms_b() {
   int d = 0, n = 0;
   cudaGetDevice(&d);
@@ -826,6 +1140,32 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
     }
     if (!ops.empty()) ops.back().pad_ = 1;  // end of iteration: carry copies follow
   }
+  // Cluster mode (NP = 64, few systems: latency-bound on one SM each): one
+  // cluster of `cl` CTAs per system.  SI_RESIDENT_CLUSTER = 0/2/4/8 overrides.
+  int cl = 0;
+  if (NP == 64) {
+    const char* env = std::getenv("SI_RESIDENT_CLUSTER");
+    if (env) {
+      cl = std::atoi(env);
+      if (cl != 0 && cl != 2 && cl != 4 && cl != 8) cl = 0;
+    } else if (batch * 4 <= num_sms_b()) {
+      cl = 4;
+    }
+  }
+  std::vector<uint8_t> cflags;
+  if (cl) {
+    // values read in full (right operands, GEMV x), loop-carried ones included
+    const auto& vo = q.r.ops;
+    std::vector<char> full(q.r.is_vec.size(), 0);
+    for (const BOp& o : vo)
+      if (o.kind == OP_GEMM || o.kind == OP_GEMV) full[o.b] = 1;
+    for (auto pr : {std::make_pair(q.G, q.gn), std::make_pair(q.F, q.fn),
+                    std::make_pair(q.T, q.tn)})
+      if (full[pr.first]) full[pr.second] = 1;
+    std::vector<bool> bcast(vo.size());
+    for (size_t k = 0; k < vo.size(); ++k) bcast[k] = vo[k].kind != OP_LOAD && full[vo[k].dst];
+    cflags = cluster_flags(ops, bcast);
+  }
   // device encoding: modes decided here, constants in a side table
   std::vector<DOp> dev_ops(ops.size());
   std::vector<double> csts = {0.0};  // slot 0: unused default
@@ -834,7 +1174,7 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
     DOp& d = dev_ops[k];
     d = DOp{};
     d.kind = (uint8_t)o.kind;
-    d.sync = (uint8_t)o.pad_;
+    d.sync = cl ? cflags[k] : (uint8_t)o.pad_;
     d.nterms = (uint8_t)o.nterms;
     d.dst = o.dst;
     d.a = o.a;
@@ -923,6 +1263,29 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
   args.rG = al.phys[q.gn];
   args.rF = al.phys[q.fn];
   args.rT = al.phys[q.tn];
+  if (cl) {
+    auto kern = cl == 2 ? resident_cluster_kernel<2>
+                : cl == 4 ? resident_cluster_kernel<4> : resident_cluster_kernel<8>;
+    check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+          "cudaFuncSetAttribute");
+    args.prof = nullptr;
+    const int64_t clusters = std::min<int64_t>(batch, std::max(1, num_sms_b() / cl));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(clusters * cl));
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    check(cudaLaunchKernelEx(&cfg, kern, args), "resident cluster kernel launch");
+    c.h->launches += 1;
+    return per;
+  }
   check(cudaFuncSetAttribute(resident_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem),
         "cudaFuncSetAttribute");
