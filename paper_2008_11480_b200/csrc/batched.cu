@@ -209,6 +209,20 @@ struct Rec {
   }
 };
 
+// Operands an op may overwrite in place (dst in the same slot): each element
+// is read and then written by the same thread -- the C operand of a product
+// (read into the accumulator or in the epilogue), the c vector of a GEMV, the
+// terms of a LIN -- and only when it is not also read as A / B / x.
+std::vector<int> inplace_operands(const BOp& o) {
+  std::vector<int> v;
+  if (o.kind == OP_GEMM || o.kind == OP_GEMV) {
+    if (o.c >= 0 && o.c != o.a && o.c != o.b) v.push_back(o.c);
+  } else if (o.kind == OP_LIN) {
+    for (int j = 0; j < o.nterms; ++j) v.push_back(o.t[j]);
+  }
+  return v;
+}
+
 // Reorders the recorded ops (a topological order of the SSA DAG) so that the
 // peak number of live matrices -- the shared-memory footprint, hence CTAs per
 // SM -- is minimal.  Branch and bound over schedules, ready ops tried in
@@ -269,7 +283,11 @@ void schedule_min_live(Rec& r, const std::vector<int>& pinned,
       if (!ready) continue;
       const BOp& o = r.ops[i];
       const bool mat = !r.is_vec[o.dst];
-      const int during = live + (mat ? 1 : 0);
+      bool inplace = false;
+      for (int v : inplace_operands(o))
+        inplace |= !r.is_vec[v] && uses[v] == 1 && !keep[v] &&
+                   std::count(reads[i].begin(), reads[i].end(), v) == 1;
+      const int during = live + (mat && !inplace ? 1 : 0);
       int after = live;
       if (mat && (uses[o.dst] > 0 || keep[o.dst])) after += 1;
       for (int v : reads[i])
@@ -346,6 +364,18 @@ Alloc assign(const Rec& r, const std::vector<int>& pinned,
   for (int i = 0; i < (int)r.ops.size(); ++i) {
     const BOp& o = r.ops[i];
     const bool vec = r.is_vec[o.dst];
+    if (al.phys[o.dst] < 0) {
+      // in place over an operand that dies here (the carried input first)
+      int reuse = -1;
+      for (int v : inplace_operands(o)) {
+        if (v < 0 || r.is_vec[v] != vec || al.phys[v] < 0 || last[v] != i) continue;
+        if (reuse < 0 || v == out_of[o.dst]) reuse = v;
+      }
+      if (reuse >= 0) {
+        al.phys[o.dst] = al.phys[reuse];
+        last[reuse] = -2;  // its slot now belongs to dst
+      }
+    }
     if (al.phys[o.dst] < 0) {
       const int in = out_of[o.dst];
       auto& fl = vec ? free_v : free_m;
@@ -858,6 +888,10 @@ __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(Ba
   for (int i = threadIdx.x; i < p.nops * (int)sizeof(DOp) / 16; i += TH)
     reinterpret_cast<int4*>(prog)[i] = reinterpret_cast<const int4*>(p.ops)[i];
   for (int i = threadIdx.x; i < p.ncst; i += TH) cst[i] = p.cst[i];
+  __shared__ long long prof_acc[kMaxOps];  // SI_RESIDENT_PROF diagnostics (CTA 0, thread 0)
+  if (p.prof && threadIdx.x == 0)
+    for (int k = 0; k < kMaxOps; ++k) prof_acc[k] = 0;
+  long long prof_last = clock64();
 
   const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   for (int64_t sys = cid; sys < p.batch; sys += ncl) {
@@ -947,8 +981,14 @@ __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(Ba
           cluster_sync_all();
         else if (o.sync & kSyncCta)
           __syncthreads();
+        if (p.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+          const long long now = clock64();
+          prof_acc[k] += now - prof_last;
+          prof_last = now;
+        }
       }
       if (p.rG != p.sG || p.rF != p.sF || p.rT != p.sT) {  // carries (full local copies)
+        cluster_sync_all();  // every broadcast into the carried outputs has landed
         for (int i = threadIdx.x; i < NP * NP; i += TH) {
           if (p.rG != p.sG) mslot(p.sG)[i] = mslot(p.rG)[i];
           if (p.rF != p.sF) mslot(p.sF)[i] = mslot(p.rF)[i];
@@ -967,6 +1007,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(Ba
       p.theta_io[sys * n + rbase + threadIdx.x] = vslot(p.sT)[rbase + threadIdx.x];
     cluster_sync_all();  // peers are done with this system before slots are reloaded
   }
+  if (p.prof && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int k = 0; k < p.nops; ++k) p.prof[k] = prof_acc[k];
 }
 
 // Barrier / exchange flags of a cluster program (ops already on physical
@@ -974,9 +1016,19 @@ __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(Ba
 // read in full somewhere, so it goes to every peer's copy too).  Before op
 // j+1: a cluster barrier when it reads in full a slot broadcast since the last
 // cluster barrier, or broadcasts into a slot read in full / broadcast since
-// then; otherwise a CTA barrier on the usual RAW / WAR / WAW rule.  The last
-// op of an iteration ends with a cluster barrier.
-std::vector<uint8_t> cluster_flags(const std::vector<BOp>& ops, const std::vector<bool>& bcast) {
+// then; otherwise a CTA barrier on the usual RAW / WAR / WAW rule.  The
+// program is analysed as a loop (iteration i's tail against i+1's head).
+std::vector<uint8_t> cluster_flags(const std::vector<BOp>& prog, const std::vector<bool>& pbc) {
+  // The program repeats: analyse three copies and keep the middle one's flags,
+  // whose windows already carry the previous iteration's tail (the first
+  // iteration starts after a cluster barrier, a subset of that state).
+  const size_t m0 = prog.size();
+  std::vector<BOp> ops;
+  std::vector<bool> bcast;
+  for (int rep = 0; rep < 3; ++rep) {
+    ops.insert(ops.end(), prog.begin(), prog.end());
+    bcast.insert(bcast.end(), pbc.begin(), pbc.end());
+  }
   const size_t m = ops.size();
   std::vector<uint8_t> fl(m, 0);
   auto key = [](int s, bool vec) { return vec ? 1000 + s : s; };
@@ -1031,10 +1083,13 @@ std::vector<uint8_t> cluster_flags(const std::vector<BOp>& ops, const std::vecto
     if (bcast[k]) wrB.push_back(a.w);
     if (a.full_write) wrF.push_back(a.w);
   }
-  if (m) fl[m - 1] |= kSyncCluster;
-  for (size_t k = 0; k < m; ++k)
-    if (bcast[k]) fl[k] |= kBcast;
-  return fl;
+  std::vector<uint8_t> out(fl.begin() + m0, fl.begin() + 2 * m0);
+  bool any = false;
+  for (uint8_t f : out) any |= (f & kSyncCluster) != 0;
+  if (!any && m0) out[m0 - 1] |= kSyncCluster;  // windows must not grow without bound
+  for (size_t k = 0; k < m0; ++k)
+    if (pbc[k]) out[k] |= kBcast;
+  return out;
 }
 
 int num_sms_b() {
@@ -1268,7 +1323,13 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
                 : cl == 4 ? resident_cluster_kernel<4> : resident_cluster_kernel<8>;
     check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
           "cudaFuncSetAttribute");
-    args.prof = nullptr;
+    long long* cprof = nullptr;
+    const bool cwant = std::getenv("SI_RESIDENT_PROF") != nullptr;
+    if (cwant) {
+      check(cudaMalloc(&cprof, sizeof(long long) * (kMaxOps + 1)), "cudaMalloc");
+      check(cudaMemset(cprof, 0, sizeof(long long) * (kMaxOps + 1)), "cudaMemset");
+    }
+    args.prof = cprof;
     const int64_t clusters = std::min<int64_t>(batch, std::max(1, num_sms_b() / cl));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(clusters * cl));
@@ -1283,6 +1344,18 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     check(cudaLaunchKernelEx(&cfg, kern, args), "resident cluster kernel launch");
+    if (cwant) {
+      std::vector<long long> hp(kMaxOps + 1);
+      check(cudaMemcpy(hp.data(), cprof, sizeof(long long) * (kMaxOps + 1), cudaMemcpyDeviceToHost),
+            "memcpy");
+      cudaFree(cprof);
+      const char* names[] = {"gemm", "gemv", "lin", "load"};
+      std::fprintf(stderr, "[resident cluster %d] CTA0 cycles per op:\n", cl);
+      for (size_t k = 0; k < ops.size(); ++k)
+        std::fprintf(stderr, "  op %2zu %-4s dst %d a %d b %d c %d flags %d: %lld\n", k,
+                     names[ops[k].kind], ops[k].dst, ops[k].a, ops[k].b, ops[k].c,
+                     (int)cflags[k], hp[k]);
+    }
     c.h->launches += 1;
     return per;
   }
