@@ -23,6 +23,7 @@ import os
 # the sharded path's exchange streams wait on flags: give every stream its own
 # hardware work queue (paper_2008_11480_b200/peer.py); before CUDA initialises
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+SHARE_GPU = os.environ.get("SI_BENCH_SHARE_GPU") == "1"
 import statistics
 import subprocess
 import sys
@@ -107,6 +108,15 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and SHARE_GPU:
+        # test mode (SI_BENCH_SHARE_GPU=1): every rank on cuda:0, gloo for the
+        # host-side collectives; exercises the N > 1 code paths on a 1-GPU box
+        # (timings are meaningless: the ranks share one GPU)
+        import torch.distributed as dist
+
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+        return world, rank, 0
     if world > 1:
         import torch.distributed as dist
 
@@ -130,7 +140,7 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARE_GPU else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -181,6 +191,8 @@ def make_comm(n: int, kind: str):
     IPC, products gated per panel inside the DMMA kernel), "peer-stream"
     (same transfers, stream waits before each product) or "nccl" (NCCL
     all-gather, the library baseline)."""
+    import torch
+
     from paper_2008_11480_b200.sharded import RowComm
 
     if kind == "nccl":
@@ -188,6 +200,9 @@ def make_comm(n: int, kind: str):
     from paper_2008_11480_b200.peer import IpcFabric, PeerComm
 
     dev = torch.device("cuda", torch.cuda.current_device())
+    if SHARE_GPU:
+        # ranks sharing one GPU must not spin in kernels on each other's panels
+        kind = "peer-stream"
     return PeerComm(n, IpcFabric(dev), mode="fused" if kind == "peer" else "stream")
 
 
@@ -205,6 +220,7 @@ class Workload:
         self.n = n
         self.world = world
         self.hoist = hoist
+        self.comm_kind = comm
         self.sharded = None
         self.split_batch = False
         self.iters_per_step = 1
@@ -299,7 +315,7 @@ class Workload:
             # right operand (peer.py: copy engines + panel-gated DMMA products)
             from paper_2008_11480_b200.sharded import ShardedEngine
 
-            comm = make_comm(self.n, comm)
+            comm = make_comm(self.n, self.comm_kind)
             eng = ShardedEngine(comm)
             st = P.initial_series(self.sp, 0, 1, order={"c4": 2, "c3": 8}[cfg])
             self.sharded = {
@@ -329,7 +345,7 @@ class Workload:
                 # block-row sharded recursive step (sharded.py) from the same initial state
                 from paper_2008_11480_b200.sharded import ShardedEngine
 
-                comm = make_comm(self.n, comm)
+                comm = make_comm(self.n, self.comm_kind)
                 eng = ShardedEngine(comm)
                 rows = slice(comm.r0, comm.r1)
                 inner = self.st.inner
@@ -471,6 +487,48 @@ class Workload:
         host["out"]["f"].copy_(new.residual, non_blocking=True)
         host["out"]["theta"].copy_(theta, non_blocking=True)
         main.wait_stream(down)
+        h2d = sum(v.numel() * 8 for v in host["in"].values())
+        d2h = sum(v.numel() * 8 for v in host["out"].values())
+        return h2d, d2h
+
+    def pinned_inputs_sharded(self):
+        """This rank's host inputs of a sharded step: the replicated operands and
+        its G / F row blocks, in pinned memory; outputs likewise."""
+        import torch
+
+        s = self.sharded
+        eng = s["eng"]
+
+        def pin(t):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            return h
+
+        host = {"in": {"a": pin(s["A"].t), "precond": pin(s["P"].t), "residual": pin(s["B"].t),
+                       "b": pin(s["b"].t), "theta": pin(s["theta"].t),
+                       "g": pin(eng.rows_of(s["g"])), "f": pin(eng.rows_of(s["f"]))}}
+        host["out"] = {k: torch.empty_like(host["in"][k], pin_memory=True)
+                       for k in ("g", "f", "theta")}
+        return host
+
+    def e2e_step_sharded(self, host):
+        """One sharded step through the block-row API from host buffers: H2D of this
+        rank's inputs, the step, D2H of its G' / F' row blocks and theta'."""
+        s = self.sharded
+        eng = s["eng"]
+        dev = s["A"].t.device
+        d = {k: v.to(dev, non_blocking=True) for k, v in host["in"].items()}
+        A, Pm, B = eng.replicated(d["a"]), eng.replicated(d["precond"]), eng.replicated(d["residual"])
+        theta = eng.plain_richardson(eng.replicated(d["theta"]), eng.local(d["g"]), A,
+                                     eng.replicated(d["b"]))
+        if self.cfg == "c4":
+            g, f = eng.composite_step(eng.local(d["g"]), eng.local(d["f"]), A, Pm, B,
+                                      (2, 3, 4, 5), 2)
+        else:
+            g, f = eng.ns_step(eng.local(d["g"]), eng.local(d["f"]), A, 8, plan=self.plan8)
+        host["out"]["g"].copy_(eng.rows_of(g), non_blocking=True)
+        host["out"]["f"].copy_(eng.rows_of(f), non_blocking=True)
+        host["out"]["theta"].copy_(theta.t, non_blocking=True)
         h2d = sum(v.numel() * 8 for v in host["in"].values())
         d2h = sum(v.numel() * 8 for v in host["out"].values())
         return h2d, d2h
@@ -668,6 +726,25 @@ def run_ours(args):
     achieved = (g_fl.value / (g_ms.value / 1e3) / 1e12) if g_ms.value > 0 else None
 
     e2e = None
+    if not args.no_e2e and args.config in ("c4", "c3") and w.sharded is not None:
+        host = w.pinned_inputs_sharded()
+        ksteps = max(1, min(args.steps, 3))
+        w.e2e_step_sharded(host)  # warm
+        torch.cuda.synchronize()
+        barrier(world)
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(ksteps):
+            h2d, d2h = w.e2e_step_sharded(host)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks(f0.elapsed_time(f1), world)
+        # one job of fixed size over all ranks; bytes are this rank's copies
+        e2e = {"value": ksteps / (e_ms / 1e3), "unit": "iters/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": ksteps,
+               "bytes": "per rank (A, S^-1, B, b, theta replicated; G, F row blocks)"}
+        del host
     if not args.no_e2e and args.config in ("c4", "c3") and w.sharded is None and not args.hoist:
         host = w.pinned_inputs()
         h2d = d2h = 0
@@ -739,7 +816,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c4")
-    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--n", "--size", dest="n", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--hoist", action="store_true",

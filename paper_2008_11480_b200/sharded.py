@@ -360,6 +360,10 @@ class ShardedEngine:
                                   doubling_sum: bool = False):
         """richardson.py:111-189 on row blocks (q == n).  Returns
         (G', F', L', R', omega', ns', theta') with theta' replicated."""
+        vec = theta.t.ndim == 1
+        if vec:
+            theta = Sharded(theta.t.reshape(-1, 1), theta.full)
+            b = Sharded(b.t.reshape(-1, 1), b.full)
         n = order
         if omega is None or ns_part is None:
             ns_prev = self.horner(f, g, n)
@@ -377,14 +381,21 @@ class ShardedEngine:
         om_new = self.mm(r_new, ns_new, c=l_new, beta=1.0)
         resid = self.mm(a, theta, c=b, beta=-1.0, mv=True)
         th = self.mm(om_new, resid, alpha=-1.0, c=theta, beta=1.0, mv=True)
-        return g_new, f_new, l_new, r_new, om_new, ns_new, Sharded(self.full_of(th), True)
+        th_full = self.full_of(th)
+        return (g_new, f_new, l_new, r_new, om_new, ns_new,
+                Sharded(th_full.reshape(-1) if vec else th_full, True))
 
     def plain_richardson(self, theta: Sharded, p: Sharded, a: Sharded, b: Sharded) -> Sharded:
         """theta - P (A theta - b) with replicated theta/b; returns the
-        gathered (replicated) new theta."""
+        gathered (replicated) new theta.  A vector theta/b (n,) is handled as n x 1."""
+        vec = theta.t.ndim == 1
+        if vec:
+            theta = Sharded(theta.t.reshape(-1, 1), theta.full)
+            b = Sharded(b.t.reshape(-1, 1), b.full)
         resid = self.mm(a, theta, c=b, beta=-1.0, mv=True)
         new = self.mm(p, resid, alpha=-1.0, c=theta, beta=1.0, mv=True)
-        return Sharded(self.full_of(new), True)
+        out = self.full_of(new)
+        return Sharded(out.reshape(-1) if vec else out, True)
 
 
 def _reads(ins, reg: str) -> bool:
