@@ -183,6 +183,19 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
+def use_all_host_threads() -> int:
+    """The CPU baseline runs on every host core it may use: torchrun exports
+    OMP_NUM_THREADS=1, which would otherwise pin OpenBLAS to one thread."""
+    n = host_cores()
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(limits=n)
+    except ImportError:
+        pass
+    return n
+
+
 # --------------------------------------------------------------------------- workloads
 
 
@@ -647,7 +660,7 @@ def run_reference(args):
         w.n = 32
     w.iters_per_step = {"c1": 30, "c2": 50}.get(cfg, 1)
     flops = w.flops()
-    cores = host_cores()
+    cores = use_all_host_threads()
     # each step: a bounded sample of one bench step of the workload (see
     # reference_step_seconds for what is executed and what is extrapolated)
     step_times, sample = [], ""
@@ -765,6 +778,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.hoist:
+        use_all_host_threads()
         # the oracle on the reference DAG (c5: Horner, 34 products per step)
         ref_flops = flops
         if args.config == "c5":
