@@ -330,5 +330,15 @@ class PeerComm:
         if self.world > 1 and isinstance(self.fabric, IpcFabric):
             self.fabric.dist.barrier(group=self.fabric.group)
 
+    def all_reduce_sum(self, x: float) -> float:
+        """Scalar sum over the ranks (stop rule); host collective of the group."""
+        if self.world == 1:
+            return x
+        if not isinstance(self.fabric, IpcFabric):
+            raise NotImplementedError("scalar reductions need a process group (IpcFabric)")
+        t = torch.tensor([x], dtype=torch.float64)
+        self.fabric.dist.all_reduce(t, group=self.fabric.group)
+        return float(t.item())
+
     def close(self):
         self.fabric.close()

@@ -92,6 +92,16 @@ class RowComm:
         if self.world > 1:
             self.dist.barrier(group=self.group)
 
+    def all_reduce_sum(self, x: float) -> float:
+        """Scalar sum over the ranks (the one reduction of the stop rule)."""
+        if self.world == 1:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64)
+        self.dist.all_reduce(t, group=self.group)
+        return float(t.item())
+
 
 class CudaOps:
     """Local products and sums on the DMMA library (no host fallback)."""
@@ -119,6 +129,14 @@ class CudaOps:
                   int(is_mv), buf, _lib.stream_ptr(a.device))
         ctr.absorb(buf)
         return out
+
+    def sumsq(self, x) -> float:
+        """Sum of squares of a local block (si_fro_norm, squared)."""
+        x2 = x.contiguous()
+        out = ctypes.c_double()
+        _lib.call("si_fro_norm", _lib.handle(x2.device.index), x2.shape[0], x2.shape[1],
+                  x2.data_ptr(), x2.shape[1], ctypes.byref(out), _lib.stream_ptr(x2.device))
+        return float(out.value) ** 2
 
     def lin(self, cdiag, doff, terms, rows, cols, like):
         out = torch.empty((rows, cols), dtype=torch.float64, device=like.device)
@@ -219,6 +237,17 @@ class ShardedEngine:
         loc = [(coef, self.rows_of(v)) for coef, v in terms]
         cols = self.rows_of(like).shape[1]
         return Sharded(self.ops.lin(cdiag, self.comm.r0, loc, rows, cols, self.rows_of(like)), False)
+
+    # -- stop rule (newton_schulz.py:328-331, matrix_core.py:167-168) ----------
+    def fro_norm(self, v: Sharded) -> float:
+        """||V||_F of a row-sharded (or replicated) matrix: local sums of squares
+        and one scalar all-reduce."""
+        if v.full:
+            return self.ops.sumsq(v.t) ** 0.5
+        return self.comm.all_reduce_sum(self.ops.sumsq(v.t)) ** 0.5
+
+    def converged(self, f: Sharded, n: int) -> bool:
+        return self.fro_norm(f) <= 1e-13 * n ** 0.5
 
     # -- evaluators (series_toolkit.py:263-457) -----------------------------
     def horner(self, y: Sharded, x: Sharded, h: int) -> Sharded:

@@ -38,6 +38,9 @@ class CpuOps:
             ctr.mmm += 1
         return out
 
+    def sumsq(self, x):
+        return float((x * x).sum())
+
     def lin(self, cdiag, doff, terms, rows, cols, like):
         out = torch.zeros((rows, cols), dtype=torch.float64)
         if cdiag:
@@ -79,6 +82,8 @@ def _worker(rank, world, port, outdir, n, steps):
         theta = eng.plain_richardson(theta, g, A, b)
         g, f = eng.composite_step(g, f, A, P, B, (2, 3, 4, 5), 2)
     g_full = comm.all_gather_rows(g.t)
+    f_norm = eng.fro_norm(f)           # one scalar all-reduce (stop rule)
+    f_conv = eng.converged(f, n)
     h_full = eng.ns_step(g, f, A, 8, plan=None)[0]
     h_full = comm.all_gather_rows(h_full.t)
     if rank == 0:
@@ -87,6 +92,7 @@ def _worker(rank, world, port, outdir, n, steps):
         np.save(os.path.join(outdir, "h.npy"), h_full.numpy())
         np.save(os.path.join(outdir, "ctr.npy"), np.array([eng.ctr.mmm, eng.ctr.mvm]))
         np.save(os.path.join(outdir, "gathered.npy"), np.array([comm.bytes_gathered]))
+        np.save(os.path.join(outdir, "fnorm.npy"), np.array([f_norm, float(f_conv)]))
     dist.destroy_process_group()
 
 
@@ -103,6 +109,7 @@ def test_sharded_composite_matches_oracle(world, n):
         h = np.load(os.path.join(d, "h.npy"))
         ctr = np.load(os.path.join(d, "ctr.npy"))
         gathered = int(np.load(os.path.join(d, "gathered.npy"))[0])
+        f_norm, f_conv = np.load(os.path.join(d, "fnorm.npy"))
     a, b = configs.c4_householder(n=n, rhs=3)
     sp = O.split_scalar(a, O.inf_norm(a) / 2.0)
     st = O.initial_series(sp, 0, 1, 2)
@@ -118,6 +125,10 @@ def test_sharded_composite_matches_oracle(world, n):
     assert rel(g, st.estimate) <= 1e-11
     assert rel(theta, th) <= 1e-11
     assert rel(h, h_ref) <= 1e-11
+    # sharded ||F||_F (ns:328-331 stop rule) = the oracle's full-matrix norm
+    f_ref = np.linalg.norm(st.residual)  # matrix_core.fro_norm (mc:167-168)
+    assert abs(f_norm - f_ref) <= 1e-11 * f_ref
+    assert bool(f_conv) == (f_ref <= 1e-13 * np.sqrt(n))
     # same DAG as the reference: 22 products + 2 per composite step, then 8 for ns_step(8)
     assert int(ctr[0]) == mmm_ref + 8 and int(ctr[1]) == mvm_ref
     assert gathered > 0
