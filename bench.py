@@ -435,37 +435,16 @@ class Workload:
     def e2e_step(self, host):
         """The public API called with HOST inputs: H2D of the step's inputs from pinned
         memory, the step, D2H of its result; returns (h2d_bytes, d2h_bytes)."""
-        import torch
-
-        P = self.P
-        dev = self.a.device
-        if self.cfg == "c4":
-            return self._e2e_step_overlapped(host)
-        d = {k: v.to(dev, non_blocking=True) for k, v in host["in"].items()}
-        sp = P.Splitting(precond=d["precond"], residual=d["residual"], matrix=d["a"], kind="scalar",
-                         verify=False)
-        st = P.NsState(estimate=d["g"], residual=d["f"], step=0, order=self.st.order,
-                       series_order=1, ctr=P.MulCounter())
-        theta = P.plain_richardson(d["theta"], st.estimate, sp.matrix, d["b"], st.ctr)
-        if self.cfg == "c4":
-            st = P.composite_step(st, sp.matrix, sp, self.spec, 2)
-        elif self.cfg == "c3":
-            st = P.ns_step(st, sp.matrix, plan=self.plan8)
-        else:
-            st = P.ns_step(st, sp.matrix)
-        host["out"]["g"].copy_(st.estimate, non_blocking=True)
-        host["out"]["f"].copy_(st.residual, non_blocking=True)
-        host["out"]["theta"].copy_(theta, non_blocking=True)
-        h2d = sum(v.numel() * 8 for v in host["in"].values())
-        d2h = sum(v.numel() * 8 for v in host["out"].values())
-        del d, st, theta, sp
-        return h2d, d2h
+        if self.cfg not in ("c4", "c3"):
+            raise ValueError("e2e is measured for the dense configs c3 / c4")
+        return self._e2e_step_overlapped(host)
 
     def _e2e_step_overlapped(self, host):
-        """c4 through the public API with HOST inputs, copies overlapped with the step:
-        every input is copied H2D on a copy stream in order of first use and the step
-        waits on each input's event right before it needs it (composite_step's
-        ``inputs_ready``); G' is read back while F' = I - G' A is computed."""
+        """c4 / c3 through the public API with HOST inputs, copies overlapped with the
+        step: every input is copied H2D on a copy stream in order of first use and
+        the step waits on each input's event right before it needs it
+        (``inputs_ready``); G' is read back while F' = I - G' A is computed, F'
+        while the plain-Richardson products run."""
         import torch
 
         P = self.P
@@ -476,31 +455,43 @@ class Workload:
         up, down = self._copy_streams
         up.wait_stream(main)
         d, ev = {}, {}
+        order = (("precond", "residual", "a", "g", "f", "b", "theta") if self.cfg == "c4"
+                 else ("f", "g", "a", "b", "theta"))
         with torch.cuda.stream(up):
-            for k in ("precond", "residual", "a", "g", "f", "b", "theta"):
+            for k in order:
                 d[k] = host["in"][k].to(dev, non_blocking=True)
                 d[k].record_stream(main)
                 ev[k] = torch.cuda.Event()
                 ev[k].record(up)
-        sp = P.Splitting(precond=d["precond"], residual=d["residual"], matrix=d["a"], kind="scalar",
-                         verify=False)
         st = P.NsState(estimate=d["g"], residual=d["f"], step=0, order=self.st.order,
                        series_order=1, ctr=P.MulCounter())
         g_done = torch.cuda.Event()
-        new = P.composite_step(st, sp.matrix, sp, self.spec, 2, inputs_ready={
-            "precond": ev["precond"], "split_residual": ev["residual"], "matrix": ev["a"],
-            "a": ev["a"], "estimate": ev["g"], "residual": ev["f"]}, estimate_done=g_done)
+        if self.cfg == "c4":
+            sp = P.Splitting(precond=d["precond"], residual=d["residual"], matrix=d["a"],
+                             kind="scalar", verify=False)
+            new = P.composite_step(st, sp.matrix, sp, self.spec, 2, inputs_ready={
+                "precond": ev["precond"], "split_residual": ev["residual"], "matrix": ev["a"],
+                "a": ev["a"], "estimate": ev["g"], "residual": ev["f"]}, estimate_done=g_done)
+        else:
+            new = P.ns_step(st, d["a"], plan=self.plan8, inputs_ready={
+                "a": ev["a"], "estimate": ev["g"], "residual": ev["f"]}, estimate_done=g_done)
         down.wait_event(g_done)
         with torch.cuda.stream(down):
             host["out"]["g"].copy_(new.estimate, non_blocking=True)
             new.estimate.record_stream(down)
-        main.wait_event(ev["b"])
-        main.wait_event(ev["theta"])
-        theta = P.plain_richardson(d["theta"], st.estimate, sp.matrix, d["b"], st.ctr)
-        host["out"]["f"].copy_(new.residual, non_blocking=True)
+        # F' goes back while the plain-Richardson products run
+        f_done = torch.cuda.Event()
+        f_done.record(main)
+        down.wait_event(f_done)
+        with torch.cuda.stream(down):
+            host["out"]["f"].copy_(new.residual, non_blocking=True)
+            new.residual.record_stream(down)
+        for k in ("a", "b", "theta"):
+            main.wait_event(ev[k])
+        theta = P.plain_richardson(d["theta"], st.estimate, d["a"], d["b"], st.ctr)
         host["out"]["theta"].copy_(theta, non_blocking=True)
         main.wait_stream(down)
-        h2d = sum(v.numel() * 8 for v in host["in"].values())
+        h2d = sum(host["in"][k].numel() * 8 for k in order)
         d2h = sum(v.numel() * 8 for v in host["out"].values())
         return h2d, d2h
 
@@ -554,10 +545,12 @@ class Workload:
             h.copy_(t)
             return h
 
-        host = {"in": {"a": pin(self.sp.matrix), "precond": pin(self.sp.precond),
-                       "residual": pin(self.sp.residual), "g": pin(self.st.estimate),
+        host = {"in": {"a": pin(self.sp.matrix), "g": pin(self.st.estimate),
                        "f": pin(self.st.residual), "b": pin(self.b), "theta": pin(self.theta)},
                 "out": {}}
+        if self.cfg == "c4":  # the composite step's parts read the splitting too
+            host["in"]["precond"] = pin(self.sp.precond)
+            host["in"]["residual"] = pin(self.sp.residual)
         host["out"] = {"g": torch.empty_like(host["in"]["g"], pin_memory=True),
                        "f": torch.empty_like(host["in"]["f"], pin_memory=True),
                        "theta": torch.empty_like(host["in"]["theta"], pin_memory=True)}

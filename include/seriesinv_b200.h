@@ -181,6 +181,15 @@ SI_API int si_initial_series(si_handle h, int64_t n, const double* precond, cons
 SI_API int si_ns_step(si_handle h, int64_t n, const double* a, const double* g, const double* f,
                int order, const int32_t* plan, int64_t plan_len, const double* consts,
                int64_t nconsts, double* g_out, double* f_out, int64_t* counters, void* stream);
+/* si_ns_step with inputs still in flight: input_ready_events (may be NULL, or
+ * 3 cudaEvent_t, each may be NULL) = {a, g, f}; the step makes its stream wait
+ * on an input's event right before the first kernel that reads it, and
+ * records g_done_event (may be NULL) once G' is final, before F' = I - G'A. */
+SI_API int si_ns_step_ex(si_handle h, int64_t n, const double* a, const double* g,
+                         const double* f, int order, const int32_t* plan, int64_t plan_len,
+                         const double* consts, int64_t nconsts, void* const* input_ready_events,
+                         void* g_done_event, double* g_out, double* f_out, int64_t* counters,
+                         void* stream);
 /* composite_step (newton_schulz.py:177-228).  plans/plan_offsets[nrates+1]
  * hold, per rate, the geometric_apply base plan (empty for rate 1). */
 SI_API int si_composite_step(si_handle h, int64_t n, const double* a, const double* g, const double* f,

@@ -57,6 +57,7 @@ SIGNATURES: dict[str, list] = {
     "si_mat_pow_counted": [_P, _I64, _P, _I, _P, _PI64, _P],
     "si_initial_series": [_P, _I64, _P, _P, _P, _I, _I, _P, _P, _PI64, _P],
     "si_ns_step": [_P, _I64, _P, _P, _P, _I, _P, _I64, _P, _I64, _P, _P, _PI64, _P],
+    "si_ns_step_ex": [_P, _I64, _P, _P, _P, _I, _P, _I64, _P, _I64, _P, _P, _P, _P, _PI64, _P],
     "si_composite_step": [_P, _I64, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _P, _P, _PI64, _P],
     "si_composite_step_ex": [_P, _I64, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _P, _PI64, _P],
     "si_composite_parts": [_P, _I64, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I64, _P, _P, _PI64, _P],

@@ -465,6 +465,26 @@ int si_ns_step(si_handle h, int64_t n, const double* a, const double* g, const d
   });
 }
 
+int si_ns_step_ex(si_handle h, int64_t n, const double* a, const double* g, const double* f,
+                  int order, const int32_t* plan, int64_t plan_len, const double* consts,
+                  int64_t nconsts, void* const* input_ready_events, void* g_done_event,
+                  double* g_out, double* f_out, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && g && f && g_out && f_out, "null pointer");
+    PlanPtr pl = opt_plan(plan, plan_len, consts, nconsts);
+    Call call(h, stream, counters);
+    if (input_ready_events) {
+      const double* bases[3] = {a, g, f};
+      for (int i = 0; i < 3; ++i)
+        if (input_ready_events[i])
+          call.c.awaits.push_back({bases[i], reinterpret_cast<cudaEvent_t>(input_ready_events[i]),
+                                   false});
+    }
+    ns_step(call.c, sq(a, n), sq(g, n), sq(f, n), order, pl.get(), sq(g_out, n), sq(f_out, n),
+            reinterpret_cast<cudaEvent_t>(g_done_event));
+  });
+}
+
 int si_composite_step(si_handle h, int64_t n, const double* a, const double* g, const double* f,
                       const double* precond, const double* residual, const double* split_matrix,
                       int nrates, const int32_t* rates, const int32_t* plans,

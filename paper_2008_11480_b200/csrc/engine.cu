@@ -71,6 +71,14 @@ MV alloc(Ctx& c, int64_t rows, int64_t cols) {
 // products
 // ---------------------------------------------------------------------------
 
+void Ctx::await_ptr(const void* p) {
+  for (Await& a : awaits)
+    if (!a.done && a.base == p) {
+      check(cudaStreamWaitEvent(s, a.ev, 0), "cudaStreamWaitEvent");
+      a.done = true;
+    }
+}
+
 void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV* C, double beta,
           double diag, bool mv, int64_t doff, const PanelWait* pw) {
   if (A.v.cols != B.v.rows || D.v.rows != A.v.rows || D.v.cols != B.v.cols)
@@ -87,6 +95,11 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
   Mat d = D.v;
   cudaError_t err;
   Handle* h = c.h;
+  if (!c.awaits.empty()) {
+    c.await_ptr(A.v.p);
+    c.await_ptr(B.v.p);
+    if (C) c.await_ptr(C->v.p);
+  }
   const bool gated = pw && pw->ready && pw->npanels > 0;
   const bool use_tma = d.rows > 0 && d.cols > 4 && std::max(d.rows, d.cols) >= 128 &&
                        A.v.cols > 0 && tma_eligible(A.v, B.v, d, e);
@@ -146,6 +159,7 @@ void residual_into(Ctx& c, const MV& D, const MV& X, const MV& A) {
 
 void copy_into(Ctx& c, const MV& D, const MV& X) {
   if (D.v.p == X.v.p) return;
+  if (!c.awaits.empty()) c.await_ptr(X.v.p);
   Mat d = D.v;
   check(launch_copy(d, X.v, c.s), "copy");
   c.h->launches += 1;
@@ -160,6 +174,7 @@ MV lincomb(Ctx& c, double cdiag, const std::vector<std::pair<double, const MV*>>
   for (size_t i = 0; i < terms.size(); ++i) {
     coef[i] = terms[i].first;
     xs[i] = terms[i].second->v;
+    if (!c.awaits.empty()) c.await_ptr(xs[i].p);
   }
   check(launch_lincomb(D.v, cdiag, 0, (int)terms.size(), coef, xs, c.s), "lincomb");
   c.h->launches += 1;
@@ -434,6 +449,8 @@ Ctx Fork::branch(int i) {
   Ctx ch(parent.h, parent.root);
   ch.s = parent.h->side[i];
   ch.keep = std::make_shared<std::vector<std::shared_ptr<Buf>>>();
+  ch.awaits = parent.awaits;  // the side stream has not waited for any input yet
+  for (auto& a : ch.awaits) a.done = false;
   check(cudaStreamWaitEvent(ch.s, evs[0], 0), "cudaStreamWaitEvent");
   return ch;
 }

@@ -82,6 +82,15 @@ struct Ctx {
   Counters ctr;
   // set on branch contexts: buffers allocated in the branch, released at join
   std::shared_ptr<std::vector<std::shared_ptr<Buf>>> keep;
+  // Inputs still in flight (host->device copies): the first kernel that reads
+  // one of these base pointers on this stream waits for its event first.
+  struct Await {
+    const void* base;
+    cudaEvent_t ev;
+    bool done;
+  };
+  std::vector<Await> awaits;
+  void await_ptr(const void* p);
   Ctx(Handle* hh, cudaStream_t st) : h(hh), root(st), s(st) {}
 };
 

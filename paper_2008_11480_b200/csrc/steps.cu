@@ -22,7 +22,7 @@ void initial_series(Ctx& c, const MV& P, const MV& B, const MV& A, int p, int w,
 
 // ns:150-174
 void ns_step(Ctx& c, const MV& A, const MV& G, const MV& F, int order, const PlanNode* plan,
-             const MV& Gout, const MV& Fout) {
+             const MV& Gout, const MV& Fout, cudaEvent_t g_done) {
   if (order < 1) throw Error(kEInval, "order must be >= 1");
   MV g;
   if (plan) {
@@ -32,6 +32,7 @@ void ns_step(Ctx& c, const MV& A, const MV& G, const MV& F, int order, const Pla
     g = horner(c, F, G, order);
   }
   copy_into(c, Gout, g);
+  if (g_done) check(cudaEventRecord(g_done, c.s), "cudaEventRecord");  // G' may go D2H now
   residual_into(c, Fout, Gout, A);
 }
 

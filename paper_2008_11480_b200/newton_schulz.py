@@ -127,8 +127,13 @@ def initial_series(split: Splitting, p: int, w: int, order: int = 2) -> NsState:
     return NsState(estimate=g, residual=f, step=0, order=order, series_order=w * (p + 1), ctr=ctr)
 
 
-def ns_step(st: NsState, a, plan: FactorPlan | None = None) -> NsState:
-    """G_k = S_n(F) G (Horner or ``plan``), F_k = I - G_k A (newton_schulz.py:150-174)."""
+def ns_step(st: NsState, a, plan: FactorPlan | None = None, *, inputs_ready: dict | None = None,
+            estimate_done=None) -> NsState:
+    """G_k = S_n(F) G (Horner or ``plan``), F_k = I - G_k A (newton_schulz.py:150-174).
+
+    ``inputs_ready`` (keys ``a``, ``estimate``, ``residual``) and ``estimate_done``
+    as in :func:`composite_step`: inputs still being copied are waited for right
+    before their first use; ``estimate_done`` is recorded before the last product."""
     n = st.order
     a = as_device(a)
     if a.shape != st.estimate.shape:
@@ -143,10 +148,19 @@ def ns_step(st: NsState, a, plan: FactorPlan | None = None) -> NsState:
     f = torch.empty_like(st.estimate)
     h, s = _ctx(g)
     buf = _lib.counter_buf()
-    _lib.call("si_ns_step", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
+    ready = None
+    if inputs_ready:
+        order3 = ("a", "estimate", "residual")
+        unknown = set(inputs_ready) - set(order3)
+        if unknown:
+            raise ValueError(f"unknown inputs in inputs_ready: {sorted(unknown)}")
+        ready = (ctypes.c_void_p * 3)(
+            *[inputs_ready[k].cuda_event if k in inputs_ready else None for k in order3])
+    _lib.call("si_ns_step_ex", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
               st.residual.data_ptr(), n, _lib.i32_array(code) if code else None, len(code),
-              _lib.f64_array(consts) if consts else None, len(consts), g.data_ptr(), f.data_ptr(),
-              buf, s)
+              _lib.f64_array(consts) if consts else None, len(consts), ready,
+              estimate_done.cuda_event if estimate_done is not None else None, g.data_ptr(),
+              f.data_ptr(), buf, s)
     st.ctr.absorb(buf)
     return NsState(estimate=g, residual=f, step=st.step + 1, order=n,
                    series_order=st.series_order, ctr=st.ctr)

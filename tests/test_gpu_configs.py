@@ -217,6 +217,43 @@ def test_composite_step_with_inputs_in_flight():
         P.composite_step(st, sp.matrix, sp, spec, 2, inputs_ready={"bogus": done})
 
 
+def test_ns_step_with_inputs_in_flight():
+    """ns_step (h8 plan and Horner) with A, G, F still being copied on another
+    stream: waits on each input right before its first reader; bitwise equal."""
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import configs
+
+    a, _ = configs.c3_gram(n=640)
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False)
+    plan8 = P.table_plans()[8][0]
+    for order, plan in ((8, plan8), (3, None)):
+        st = P.initial_series(sp, 0, 1, order=order)
+        ref = P.ns_step(st, sp.matrix, plan=plan)
+        host = {k: v.cpu().pin_memory() for k, v in (("a", sp.matrix), ("g", st.estimate),
+                                                       ("f", st.residual))}
+        up = torch.cuda.Stream()
+        main = torch.cuda.current_stream()
+        up.wait_stream(main)
+        d, ev = {}, {}
+        with torch.cuda.stream(up):
+            for k in ("f", "g", "a"):
+                d[k] = host[k].to("cuda", non_blocking=True)
+                d[k].record_stream(main)
+                ev[k] = torch.cuda.Event()
+                ev[k].record(up)
+        st2 = P.NsState(estimate=d["g"], residual=d["f"], step=0, order=order, series_order=1,
+                        ctr=P.MulCounter())
+        done = torch.cuda.Event()
+        out = P.ns_step(st2, d["a"], plan=plan, inputs_ready={
+            "a": ev["a"], "estimate": ev["g"], "residual": ev["f"]}, estimate_done=done)
+        done.synchronize()
+        assert torch.equal(out.estimate, ref.estimate)
+        torch.cuda.synchronize()
+        assert torch.equal(out.residual, ref.residual)
+    with pytest.raises(ValueError):
+        P.ns_step(st, sp.matrix, inputs_ready={"bogus": done})
+
+
 def test_hoisted_composite_parts_bitwise():
     """Opt-in hoisting evaluates the same T_comp / R_comp DAG once: the steps are
     bitwise identical to the reference-faithful recompute, at 3 products per step
