@@ -368,6 +368,13 @@ def test_c4_full_size_step():
     assert torch.equal(th.t, theta1)
     rows = np.random.default_rng(4).choice(n, 8, replace=False)
     _row_sample_check(st1.residual, st1.estimate, sp.matrix, rows, alpha=-1.0, diag=1.0)
+    # exponent law at full size: F_1 = B^(2+3+4+5) F_0^2 = B^16 since
+    # F_0 = B; rows of B^16 by 15 row-vector products (checker: torch/cuBLAS)
+    x = sp.residual[rows].clone()
+    for _ in range(15):
+        x = x @ sp.residual
+    err = float(torch.linalg.norm(st1.residual[rows] - x) / torch.linalg.norm(x))
+    assert err <= 1e-12, err
 
 
 def test_c3_full_size_properties():
@@ -387,7 +394,14 @@ def test_c3_full_size_properties():
     for k in range(6):
         c0 = st.ctr.copy()
         theta = P.plain_richardson(theta, st.estimate, sp.matrix, b, st.ctr)
+        f_prev = st.residual
         st = P.ns_step(st, sp.matrix, plan=plan)
+        if k < 2:  # exponent law F_k = F_{k-1}^8 (ns:150-174), sampled rows
+            x = f_prev[rows].clone()
+            for _ in range(7):
+                x = x @ f_prev
+            err = float(torch.linalg.norm(st.residual[rows] - x) / torch.linalg.norm(x))
+            assert err <= 1e-11, (k, err)
         assert (st.ctr.mmm - c0.mmm, st.ctr.mvm - c0.mvm) == (6, 2)
         _row_sample_check(st.residual, st.estimate, sp.matrix, rows, alpha=-1.0, diag=1.0)
         norms.append(float(torch.linalg.norm(sp.matrix @ theta - b)))
