@@ -377,6 +377,35 @@ def test_c4_full_size_step():
     assert err <= 1e-12, err
 
 
+def test_c5_full_size_recursive_step():
+    """BASELINE config 5 at its full size (n=32768, 256 RHS) through the opt-in
+    factorised recursive step (the bench path): F' = I - G' A on sampled rows,
+    the Richardson mismatch drops, and the first call's products follow the DAG."""
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import configs
+
+    n = 32768
+    a, b = configs.c5_gram_device(n=n, m=40000, rhs=256)
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False, verify=False)
+    del a
+    st = P.initial_richardson(sp, b, 0, 1, order=16, q=16)
+    sp = P.Splitting(precond=sp.matrix[:1, :1], residual=sp.matrix[:1, :1], matrix=sp.matrix,
+                     kind="scalar", verify=False)
+    torch.cuda.empty_cache()
+    r0 = float(torch.linalg.norm(sp.matrix @ st.theta - b))
+    st1 = P.richardson_recursive_step(st, sp.matrix, b, factor_plan=P.plan_order(16),
+                                      doubling_sum=True)
+    r1 = float(torch.linalg.norm(sp.matrix @ st1.theta - b))
+    assert r1 < r0
+    rows = np.random.default_rng(5).choice(n, 4, replace=False)
+    g = st1.inner.estimate
+    f = st1.inner.residual
+    x = (-(g[rows] @ sp.matrix)).cpu().numpy()
+    x[np.arange(len(rows)), rows] += 1.0
+    got = f[rows].cpu().numpy()
+    assert np.max(np.abs(got - x)) <= 1e-9 * max(1.0, np.max(np.abs(x)))
+
+
 def test_c3_full_size_properties():
     """BASELINE config 3 at n=4096: every step keeps F = I - G A (row-sampled) and the
     Richardson mismatch contracts; counters follow the reference DAG (6 mmm + 2 mvm)."""
