@@ -441,37 +441,84 @@ class Workload:
 
     def _e2e_step_overlapped(self, host):
         """c4 / c3 through the public API with HOST inputs, copies overlapped with the
-        step: every input is copied H2D on a copy stream in order of first use and
-        the step waits on each input's event right before it needs it
-        (``inputs_ready``); G' is read back while F' = I - G' A is computed, F'
-        while the plain-Richardson products run."""
+        step.  c4: the inputs are copied H2D in row panels on a copy stream, each
+        panel raising a flag, and ``composite_step(input_panels=...)`` gates its
+        DMMA loads per panel, so the first product starts once the first panels
+        are in (not after whole matrices); G' is read back while F' = I - G' A
+        is computed and F' row block by row block (``residual_chunks``).  c3:
+        per-input events (``ns_step(inputs_ready=...)``).  The plain-Richardson
+        products run while F' goes back."""
         import torch
+
+        from paper_2008_11480_b200 import _lib
 
         P = self.P
         dev = self.a.device
         main = torch.cuda.current_stream(dev)
         if not hasattr(self, "_copy_streams"):
             self._copy_streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+            self._e2e_flags = torch.zeros(96, dtype=torch.int32, device=dev)
+            self._e2e_epoch = 0
         up, down = self._copy_streams
         up.wait_stream(main)
         d, ev = {}, {}
-        order = (("precond", "residual", "a", "g", "f", "b", "theta") if self.cfg == "c4"
-                 else ("f", "g", "a", "b", "theta"))
-        with torch.cuda.stream(up):
-            for k in order:
-                d[k] = host["in"][k].to(dev, non_blocking=True)
-                d[k].record_stream(main)
-                ev[k] = torch.cuda.Event()
-                ev[k].record(up)
+        n = self.n
+        npanels = 8
+        bounds = [n * p // npanels for p in range(npanels + 1)]
+        h = _lib.handle(dev.index)
+        self._e2e_epoch += 1
+        epoch = self._e2e_epoch
+        flags = self._e2e_flags
+        slot = {"a": (0, 5), "g": (1,), "f": (2,), "precond": (3,), "residual": (4,)}
+
+        def panel(k, p):
+            r0, r1 = bounds[p], bounds[p + 1]
+            d[k][r0:r1].copy_(host["in"][k][r0:r1], non_blocking=True)
+            for i in slot[k]:
+                _lib.call("si_stream_write_u32", h, flags.data_ptr() + 4 * (16 * i + p), epoch,
+                          up.cuda_stream)
+
+        if self.cfg == "c4":
+            order = ("precond", "residual", "a", "g", "f", "b", "theta")
+            with torch.cuda.stream(up):
+                for k in order:
+                    d[k] = torch.empty(host["in"][k].shape, dtype=torch.float64, device=dev)
+                    d[k].record_stream(main)
+                # the first product B S^-1 + S^-1 needs B's first row tiles and all of
+                # S^-1's k-panels: B panel 0, S^-1, the rest of B, then A, G, F
+                panel("residual", 0)
+                for p in range(npanels):
+                    panel("precond", p)
+                for p in range(1, npanels):
+                    panel("residual", p)
+                for k in ("a", "g", "f"):
+                    for p in range(npanels):
+                        panel(k, p)
+                    ev[k] = torch.cuda.Event()
+                    ev[k].record(up)
+                for k in ("b", "theta"):
+                    d[k].copy_(host["in"][k], non_blocking=True)
+                    ev[k] = torch.cuda.Event()
+                    ev[k].record(up)
+        else:
+            order = ("f", "g", "a", "b", "theta")
+            with torch.cuda.stream(up):
+                for k in order:
+                    d[k] = host["in"][k].to(dev, non_blocking=True)
+                    d[k].record_stream(main)
+                    ev[k] = torch.cuda.Event()
+                    ev[k].record(up)
         st = P.NsState(estimate=d["g"], residual=d["f"], step=0, order=self.st.order,
                        series_order=1, ctr=P.MulCounter())
         g_done = torch.cuda.Event()
+        chunks = []
         if self.cfg == "c4":
             sp = P.Splitting(precond=d["precond"], residual=d["residual"], matrix=d["a"],
                              kind="scalar", verify=False)
-            new = P.composite_step(st, sp.matrix, sp, self.spec, 2, inputs_ready={
-                "precond": ev["precond"], "split_residual": ev["residual"], "matrix": ev["a"],
-                "a": ev["a"], "estimate": ev["g"], "residual": ev["f"]}, estimate_done=g_done)
+            chunks = [torch.cuda.Event() for _ in range(npanels)]
+            new = P.composite_step(st, sp.matrix, sp, self.spec, 2,
+                                   input_panels=(flags, epoch, npanels), residual_chunks=chunks,
+                                   estimate_done=g_done)
         else:
             new = P.ns_step(st, d["a"], plan=self.plan8, inputs_ready={
                 "a": ev["a"], "estimate": ev["g"], "residual": ev["f"]}, estimate_done=g_done)
@@ -479,14 +526,20 @@ class Workload:
         with torch.cuda.stream(down):
             host["out"]["g"].copy_(new.estimate, non_blocking=True)
             new.estimate.record_stream(down)
-        # F' goes back while the plain-Richardson products run
-        f_done = torch.cuda.Event()
-        f_done.record(main)
-        down.wait_event(f_done)
-        with torch.cuda.stream(down):
-            host["out"]["f"].copy_(new.residual, non_blocking=True)
             new.residual.record_stream(down)
-        for k in ("a", "b", "theta"):
+        if chunks:  # F' row block by row block, while the next blocks are computed
+            for p, e in enumerate(chunks):
+                down.wait_event(e)
+                with torch.cuda.stream(down):
+                    r0, r1 = bounds[p], bounds[p + 1]
+                    host["out"]["f"][r0:r1].copy_(new.residual[r0:r1], non_blocking=True)
+        else:
+            f_done = torch.cuda.Event()
+            f_done.record(main)
+            down.wait_event(f_done)
+            with torch.cuda.stream(down):
+                host["out"]["f"].copy_(new.residual, non_blocking=True)
+        for k in ("a", "g", "b", "theta"):
             main.wait_event(ev[k])
         theta = P.plain_richardson(d["theta"], st.estimate, d["a"], d["b"], st.ctr)
         host["out"]["theta"].copy_(theta, non_blocking=True)

@@ -213,6 +213,25 @@ SI_API int si_composite_step_ex(si_handle h, int64_t n, const double* a, const d
                                 int concurrent, void* const* input_ready_events,
                                 void* g_done_event, double* g_out, double* f_out,
                                 int64_t* counters, void* stream);
+
+/* si_composite_step_ex for inputs that arrive in row panels (host->device
+ * copies still in flight): input_flags (may be NULL) = 6 x 16 uint32 flags for
+ * {a, g, f, precond, residual, split_matrix}; rows [n p / npanels,
+ * n (p+1) / npanels) of input i are valid once input_flags[16 i + p] >= epoch.
+ * The DMMA products gate their A-tile / B-slab loads on those flags, so the
+ * first product starts while later panels are still copying.  f_chunks > 0:
+ * F' = I - G'A is produced in f_chunks row blocks, f_chunk_events[k] recorded
+ * after block k (one product in the counters). */
+SI_API int si_composite_step_gated(si_handle h, int64_t n, const double* a, const double* g,
+                                   const double* f, const double* precond,
+                                   const double* residual, const double* split_matrix,
+                                   int nrates, const int32_t* rates, const int32_t* plans,
+                                   const int64_t* plan_offsets, const double* consts,
+                                   int64_t nconsts, int order_n, int concurrent,
+                                   const uint32_t* input_flags, uint32_t epoch, int npanels,
+                                   void* g_done_event, void* const* f_chunk_events, int f_chunks,
+                                   double* g_out, double* f_out, int64_t* counters,
+                                   void* stream);
 /* Opt-in hoisting (NOT the reference DAG, which recomputes the parts every
  * step): the state-independent half of composite_step (newton_schulz.py:
  * 204-216) -> T_comp, R_comp; and the state-dependent half (:218-220) that

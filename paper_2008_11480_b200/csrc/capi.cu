@@ -531,6 +531,58 @@ int si_composite_step_ex(si_handle h, int64_t n, const double* a, const double* 
   });
 }
 
+int si_composite_step_gated(si_handle h, int64_t n, const double* a, const double* g,
+                            const double* f, const double* precond, const double* residual,
+                            const double* split_matrix, int nrates, const int32_t* rates,
+                            const int32_t* plans, const int64_t* plan_offsets,
+                            const double* consts, int64_t nconsts, int order_n, int concurrent,
+                            const uint32_t* input_flags, uint32_t epoch, int npanels,
+                            void* g_done_event, void* const* f_chunk_events, int f_chunks,
+                            double* g_out, double* f_out, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && g && f && precond && residual && split_matrix && g_out && f_out,
+         "null pointer");
+    need(nrates >= 1 && rates, "composite spec needs at least one rate");
+    need(order_n >= 1, "order_n must be >= 1");
+    need(!input_flags || (npanels >= 1 && npanels <= kMaxPanels), "npanels out of range");
+    need(f_chunks >= 0 && (f_chunks == 0 || f_chunk_events), "bad f_chunks");
+    std::vector<int> rv(rates, rates + nrates);
+    std::vector<PlanPtr> owned(nrates);
+    std::vector<const PlanNode*> pv(nrates, nullptr);
+    for (int i = 0; i < nrates; ++i) {
+      need(rv[i] >= 1, "rates must be positive integers");
+      if (plans && plan_offsets && plan_offsets[i + 1] > plan_offsets[i]) {
+        owned[i] = decode_plan(plans + plan_offsets[i], plan_offsets[i + 1] - plan_offsets[i],
+                               consts, nconsts);
+        pv[i] = owned[i].get();
+      }
+    }
+    StepEvents ev;
+    ev.g_done = reinterpret_cast<cudaEvent_t>(g_done_event);
+    std::vector<cudaEvent_t> chunks(f_chunks);
+    for (int k = 0; k < f_chunks; ++k) chunks[k] = reinterpret_cast<cudaEvent_t>(f_chunk_events[k]);
+    ev.f_chunk = f_chunks ? chunks.data() : nullptr;
+    ev.f_chunks = f_chunks;
+    Call call(h, stream, counters);
+    if (input_flags) {
+      const double* bases[6] = {a, g, f, precond, residual, split_matrix};
+      for (int i = 0; i < 6; ++i) {
+        Ctx::Gate gt{};
+        gt.base = bases[i];
+        gt.pw.ready = input_flags + kMaxPanels * i;
+        gt.pw.epoch = epoch;
+        gt.pw.npanels = npanels;
+        for (int p = 0; p <= npanels; ++p) gt.pw.bounds[p] = (int)(n * p / npanels);
+        gt.stream_done = false;
+        call.c.gates.push_back(gt);
+      }
+    }
+    composite_step(call.c, sq(a, n), sq(g, n), sq(f, n), sq(precond, n), sq(residual, n),
+                   sq(split_matrix, n), rv, pv, order_n, concurrent != 0, sq(g_out, n),
+                   sq(f_out, n), &ev);
+  });
+}
+
 int si_composite_parts(si_handle h, int64_t n, const double* a, const double* precond,
                        const double* residual, const double* split_matrix, int nrates,
                        const int32_t* rates, const int32_t* plans, const int64_t* plan_offsets,

@@ -43,7 +43,7 @@ const char* get_error();
 
 // Kernel launchers (stream-ordered, no host sync).
 cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, cudaStream_t s,
-                            const PanelWait* pw = nullptr);
+                            const PanelWait* pw = nullptr, const PanelWait* pwa = nullptr);
 cudaError_t launch_gemm_generic(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, cudaStream_t s);
 cudaError_t launch_gemv(const Mat& A, const Mat& X, Mat& D, const Epilogue& e, cudaStream_t s);
 bool tma_eligible(const Mat& A, const Mat& B, const Mat& D, const Epilogue& e);

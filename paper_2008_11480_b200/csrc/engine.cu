@@ -79,6 +79,21 @@ void Ctx::await_ptr(const void* p) {
     }
 }
 
+const PanelWait* Ctx::gate_of(const void* p) const {
+  for (const Gate& g : gates)
+    if (g.base == p && !g.stream_done) return &g.pw;
+  return nullptr;
+}
+
+void Ctx::gate_stream(const void* p) {
+  for (Gate& g : gates)
+    if (g.base == p && !g.stream_done) {
+      for (int i = 0; i < g.pw.npanels; ++i)
+        check(stream_wait_u32(g.pw.ready + i, g.pw.epoch, s), "panel wait");
+      g.stream_done = true;
+    }
+}
+
 void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV* C, double beta,
           double diag, bool mv, int64_t doff, const PanelWait* pw) {
   if (A.v.cols != B.v.rows || D.v.rows != A.v.rows || D.v.cols != B.v.cols)
@@ -100,9 +115,23 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
     c.await_ptr(B.v.p);
     if (C) c.await_ptr(C->v.p);
   }
-  const bool gated = pw && pw->ready && pw->npanels > 0;
   const bool use_tma = d.rows > 0 && d.cols > 4 && std::max(d.rows, d.cols) >= 128 &&
                        A.v.cols > 0 && tma_eligible(A.v, B.v, d, e);
+  // inputs still arriving in row panels: in-kernel gates for A rows / B k-slabs
+  // of the DMMA GEMM, stream waits for everything else
+  const PanelWait* pwa = nullptr;
+  if (!c.gates.empty()) {
+    if (use_tma) {
+      pwa = c.gate_of(A.v.p);
+      if (!pw) pw = c.gate_of(B.v.p);
+      if (C && C->v.p != B.v.p) c.gate_stream(C->v.p);  // C == B: its panels gate the k-loop
+    } else {
+      c.gate_stream(A.v.p);
+      c.gate_stream(B.v.p);
+      if (C) c.gate_stream(C->v.p);
+    }
+  }
+  const bool gated = pw && pw->ready && pw->npanels > 0;
   if (gated && !use_tma) {
     // kernels without the in-kernel gate: the stream waits for every panel
     for (int p = 0; p < pw->npanels; ++p)
@@ -127,7 +156,7 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
       rec.flops = 2.0 * (double)d.rows * (double)d.cols * (double)A.v.cols;
       check(cudaEventRecord(rec.start, c.s), "cudaEventRecord");
     }
-    err = launch_gemm_tma(A.v, B.v, d, e, c.s, gated ? pw : nullptr);
+    err = launch_gemm_tma(A.v, B.v, d, e, c.s, gated ? pw : nullptr, pwa);
     h->launches += 1;
     if (h->profiling && err == cudaSuccess) {
       check(cudaEventRecord(rec.stop, c.s), "cudaEventRecord");
@@ -160,6 +189,7 @@ void residual_into(Ctx& c, const MV& D, const MV& X, const MV& A) {
 void copy_into(Ctx& c, const MV& D, const MV& X) {
   if (D.v.p == X.v.p) return;
   if (!c.awaits.empty()) c.await_ptr(X.v.p);
+  if (!c.gates.empty()) c.gate_stream(X.v.p);
   Mat d = D.v;
   check(launch_copy(d, X.v, c.s), "copy");
   c.h->launches += 1;
@@ -175,6 +205,7 @@ MV lincomb(Ctx& c, double cdiag, const std::vector<std::pair<double, const MV*>>
     coef[i] = terms[i].first;
     xs[i] = terms[i].second->v;
     if (!c.awaits.empty()) c.await_ptr(xs[i].p);
+    if (!c.gates.empty()) c.gate_stream(xs[i].p);
   }
   check(launch_lincomb(D.v, cdiag, 0, (int)terms.size(), coef, xs, c.s), "lincomb");
   c.h->launches += 1;
@@ -451,6 +482,8 @@ Ctx Fork::branch(int i) {
   ch.keep = std::make_shared<std::vector<std::shared_ptr<Buf>>>();
   ch.awaits = parent.awaits;  // the side stream has not waited for any input yet
   for (auto& a : ch.awaits) a.done = false;
+  ch.gates = parent.gates;
+  for (auto& g : ch.gates) g.stream_done = false;
   check(cudaStreamWaitEvent(ch.s, evs[0], 0), "cudaStreamWaitEvent");
   return ch;
 }

@@ -91,6 +91,17 @@ struct Ctx {
   };
   std::vector<Await> awaits;
   void await_ptr(const void* p);
+  // Inputs arriving in row panels (flags raised behind each panel's copy): the
+  // DMMA GEMM gates its A-tile / B-slab loads per panel; every other reader
+  // makes its stream wait for all panels first.
+  struct Gate {
+    const void* base;
+    PanelWait pw;
+    bool stream_done;
+  };
+  std::vector<Gate> gates;
+  const PanelWait* gate_of(const void* p) const;
+  void gate_stream(const void* p);  // stream-wait for every panel of p (once)
   Ctx(Handle* hh, cudaStream_t st) : h(hh), root(st), s(st) {}
 };
 

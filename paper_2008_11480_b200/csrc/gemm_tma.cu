@@ -22,6 +22,8 @@
 //  * Persistent grid (<= #SMs CTAs), grouped tile rasterisation for L2 reuse;
 //    the producer runs ahead into the next tile while consumers drain the
 //    epilogue.
+//  * Optional row-panel gates on A (per tile rows) and B (per k-slab); used for
+//    inputs whose host->device copy is still in flight.
 //  * Optional panel gate (sharded path): when B is a matrix whose row panels
 //    are still arriving from peer GPUs (copy engines, flags written by stream
 //    memory operations), the producer lane acquires panel p's flag before its
@@ -164,7 +166,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                         const __grid_constant__ CUtensorMap tmB, double* __restrict__ D,
                         int64_t ldd, const double* __restrict__ C, int64_t ldc, int M, int N,
                         int K, double alpha, double beta, double diag, int64_t doff,
-                        const __grid_constant__ PanelWait pw) {
+                        const __grid_constant__ PanelWait pw,
+                        const __grid_constant__ PanelWait pwa) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -197,10 +200,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t known = pw.ready ? 0u : ~0u;
+      uint32_t known_a = pwa.ready ? 0u : ~0u;  // row panels of A (inputs in flight)
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         int tm, tn;
         tile_coords(tile, num_m, num_n, tm, tn);
         const int n0 = tn * BN;
+        if (~known_a) panel_gate(pwa, tm * BM, min(M, tm * BM + BM), known_a);
         const int nboxes = min(8, (N - n0 + 15) / 16);
         const uint32_t bytes = A_STAGE_BYTES + nboxes * B_BOX_BYTES;
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -383,7 +388,7 @@ bool tma_eligible(const Mat& A, const Mat& B, const Mat& D, const Epilogue& e) {
 }
 
 cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& e,
-                            cudaStream_t s, const PanelWait* pw) {
+                            cudaStream_t s, const PanelWait* pw, const PanelWait* pwa) {
   CUtensorMap ta, tb;
   if (!make_map(&ta, A.p, A.rows, A.cols, A.ld, BK, BM) ||
       !make_map(&tb, B.p, B.rows, B.cols, B.ld, 16, BK)) {
@@ -412,10 +417,12 @@ cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& 
     const int c = std::atoi(cap);
     if (c > 0 && c < grid) grid = c;
   }
-  PanelWait gate;
+  PanelWait gate, gate_a;
   if (pw && pw->ready && pw->npanels > 0) gate = *pw;
+  if (pwa && pwa->ready && pwa->npanels > 0) gate_a = *pwa;
   gemm_f64_tma_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, D.p, D.ld, e.c, e.ldc, M, N, K,
-                                                        e.alpha, e.beta, e.diag, e.doff, gate);
+                                                        e.alpha, e.beta, e.diag, e.doff, gate,
+                                                        gate_a);
   return cudaGetLastError();
 }
 

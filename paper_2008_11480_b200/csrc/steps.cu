@@ -100,6 +100,18 @@ void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, 
   }
   gemm(c, Gout, r, nsp, 1.0, &t, 1.0);  // G = t + r ns
   if (e.g_done) check(cudaEventRecord(e.g_done, c.s), "cudaEventRecord");  // G' may go D2H now
+  if (e.f_chunks > 0 && e.f_chunk) {
+    const int64_t n = Fout.v.rows;
+    for (int k = 0; k < e.f_chunks; ++k) {
+      const int64_t r0 = n * k / e.f_chunks, r1 = n * (k + 1) / e.f_chunks;
+      MV fr = view(Fout.v.p + r0 * Fout.v.ld, r1 - r0, Fout.v.cols, Fout.v.ld);
+      MV gr = view(Gout.v.p + r0 * Gout.v.ld, r1 - r0, Gout.v.cols, Gout.v.ld);
+      gemm(c, fr, gr, A, -1.0, nullptr, 0.0, 1.0, false, r0);  // rows of I - G'A
+      if (e.f_chunk[k]) check(cudaEventRecord(e.f_chunk[k], c.s), "cudaEventRecord");
+    }
+    c.ctr.mmm -= e.f_chunks - 1;  // one product of the reference DAG
+    return;
+  }
   residual_into(c, Fout, Gout, A);
 }
 

@@ -19,6 +19,10 @@ struct StepEvents {
   cudaEvent_t ready[kInputs] = {};
   bool waited[kInputs] = {};
   cudaEvent_t g_done = nullptr;
+  // F' = I - G' A in f_chunks row blocks, f_chunk[k] recorded after block k
+  // (its rows may go device->host while the next block is computed)
+  const cudaEvent_t* f_chunk = nullptr;
+  int f_chunks = 0;
   void wait(Ctx& c, int i);
 };
 void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, const MV& B,

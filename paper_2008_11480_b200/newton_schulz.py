@@ -198,7 +198,9 @@ _READY_ORDER = ("a", "estimate", "residual", "precond", "split_residual", "matri
 
 def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_n: int,
                    executor=None, parts: CompositeParts | None = None, *,
-                   inputs_ready: dict | None = None, estimate_done=None) -> NsState:
+                   inputs_ready: dict | None = None, estimate_done=None,
+                   input_panels: tuple | None = None,
+                   residual_chunks: list | None = None) -> NsState:
     """G_k = T_comp + R_comp S_n(F) G, F_k = I - G_k A (newton_schulz.py:177-228).
 
     ``executor`` (not in the reference signature, whose parts run serially)
@@ -210,7 +212,15 @@ def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_
     ``precond``, ``split_residual``, ``matrix``) to recorded ``torch.cuda.Event``s
     (e.g. host->device copies on another stream); the step waits on each right
     before that input's first use.  ``estimate_done`` is recorded when the new
-    estimate is final, before the last product."""
+    estimate is final, before the last product.
+
+    ``input_panels = (flags, epoch, npanels)`` instead: the inputs arrive in row
+    panels; ``flags`` is a CUDA int32 tensor of 6 x 16 flags (inputs a,
+    estimate, residual, precond, split_residual, matrix; panel p of n rows is
+    rows [n p / npanels, n (p+1) / npanels)), raised (>= epoch) behind each
+    panel's copy -- the products gate their loads per panel.
+    ``residual_chunks`` (list of ``torch.cuda.Event``): F' is produced in that
+    many row blocks, each event recorded after its block."""
     if order_n < 1:
         raise ValueError("order_n must be >= 1")
     a = as_device(a)
@@ -235,6 +245,29 @@ def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_
     f = torch.empty_like(st.estimate)
     h, s = _ctx(g)
     buf = _lib.counter_buf()
+    if input_panels is not None or residual_chunks:
+        if inputs_ready:
+            raise ValueError("inputs_ready and input_panels are exclusive")
+        flags_ptr, epoch, npanels = None, 0, 0
+        if input_panels is not None:
+            flags, epoch, npanels = input_panels
+            if flags.dtype != torch.int32 or flags.numel() < 96 or not flags.is_cuda:
+                raise ValueError("input_panels flags must be a CUDA int32 tensor of 6 x 16")
+            if not 1 <= npanels <= 16:
+                raise ValueError("npanels must be in 1..16")
+            flags_ptr = flags.data_ptr()
+        chunks = list(residual_chunks or [])
+        evs = (ctypes.c_void_p * max(len(chunks), 1))(*[e.cuda_event for e in chunks])
+        _lib.call("si_composite_step_gated", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
+                  st.residual.data_ptr(), split.precond.data_ptr(), split.residual.data_ptr(),
+                  split.matrix.data_ptr(), len(spec.rates), _lib.i32_array(list(spec.rates)),
+                  _lib.i32_array(code), _lib.i64_array(offsets), _lib.f64_array(consts),
+                  len(consts), order_n, int(executor is not None), flags_ptr, epoch, npanels,
+                  estimate_done.cuda_event if estimate_done is not None else None,
+                  evs if chunks else None, len(chunks), g.data_ptr(), f.data_ptr(), buf, s)
+        st.ctr.absorb(buf)
+        return NsState(estimate=g, residual=f, step=st.step + 1, order=order_n,
+                       series_order=st.series_order, ctr=st.ctr)
     ready = None
     if inputs_ready:
         unknown = set(inputs_ready) - set(_READY_ORDER)

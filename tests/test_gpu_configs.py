@@ -217,6 +217,56 @@ def test_composite_step_with_inputs_in_flight():
         P.composite_step(st, sp.matrix, sp, spec, 2, inputs_ready={"bogus": done})
 
 
+def test_composite_step_with_inputs_in_row_panels():
+    """Inputs copied host->device panel by panel (out of order, a delaying copy
+    first) with flags; the DMMA products gate their loads per panel and F' comes
+    out in row blocks: bitwise the resident-input result, same product count."""
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import _lib, configs
+
+    n, npanels = 768, 6
+    a, _ = configs.c4_householder(n=n, rhs=1)
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False)
+    spec = P.CompositeSpec((2, 3, 4, 5))
+    st = P.initial_series(sp, 0, 1, order=2)
+    c0 = st.ctr.mmm
+    ref = P.composite_step(st, sp.matrix, sp, spec, 2)
+    n_ref = ref.ctr.mmm - c0
+    host = {k: v.cpu().pin_memory() for k, v in (("a", sp.matrix), ("p", sp.precond),
+                                                   ("b", sp.residual), ("g", st.estimate),
+                                                   ("f", st.residual))}
+    flags = torch.zeros(96, dtype=torch.int32, device="cuda")
+    slot = {"a": (0, 5), "g": (1,), "f": (2,), "p": (3,), "b": (4,)}
+    d = {k: torch.empty_like(v, device="cuda") for k, v in host.items()}
+    big = torch.empty(32 << 20, dtype=torch.float64, device="cuda")
+    big2 = torch.empty_like(big)
+    torch.cuda.synchronize()
+    up = torch.cuda.Stream()
+    h = _lib.handle(0)
+    bounds = [n * p // npanels for p in range(npanels + 1)]
+    st2 = P.NsState(estimate=d["g"], residual=d["f"], step=0, order=2, series_order=1,
+                    ctr=P.MulCounter())
+    sp2 = P.Splitting(precond=d["p"], residual=d["b"], matrix=d["a"], kind="scalar", verify=False)
+    chunks = [torch.cuda.Event() for _ in range(4)]
+    done = torch.cuda.Event()
+    out = P.composite_step(st2, sp2.matrix, sp2, spec, 2, input_panels=(flags, 3, npanels),
+                           residual_chunks=chunks, estimate_done=done)
+    with torch.cuda.stream(up):
+        big2.copy_(big)  # the step is already waiting on the flags
+        for k in ("b", "p", "a", "g", "f"):
+            for p in reversed(range(npanels)):
+                r0, r1 = bounds[p], bounds[p + 1]
+                d[k][r0:r1].copy_(host[k][r0:r1], non_blocking=True)
+                for i in slot[k]:
+                    _lib.call("si_stream_write_u32", h, flags.data_ptr() + 4 * (16 * i + p), 3,
+                              up.cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(out.estimate, ref.estimate)
+    assert torch.equal(out.residual, ref.residual)
+    assert out.ctr.mmm == n_ref
+    assert all(e.query() for e in chunks)
+
+
 def test_ns_step_with_inputs_in_flight():
     """ns_step (h8 plan and Horner) with A, G, F still being copied on another
     stream: waits on each input right before its first reader; bitwise equal."""
