@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <string>
 #include <unordered_map>
 
@@ -306,6 +307,31 @@ void schedule_min_live(Rec& r, const std::vector<int>& pinned,
   std::vector<BOp> ops(nops);
   for (int i = 0; i < nops; ++i) ops[i] = r.ops[best_order[i]];
   r.ops.swap(ops);
+}
+
+// The search is deterministic in the recorded program, so its result is
+// memoised (repeated launches of the same run re-record the same program).
+void schedule_min_live_cached(Rec& r, const std::vector<int>& pinned,
+                              const std::vector<std::pair<int, int>>& carried) {
+  static std::mutex mu;
+  static std::unordered_map<std::string, std::vector<BOp>> cache;
+  std::string key(reinterpret_cast<const char*>(r.ops.data()), r.ops.size() * sizeof(BOp));
+  for (int v : pinned) key.append(reinterpret_cast<const char*>(&v), sizeof v);
+  for (auto& pr : carried) {
+    key.append(reinterpret_cast<const char*>(&pr.first), sizeof pr.first);
+    key.append(reinterpret_cast<const char*>(&pr.second), sizeof pr.second);
+  }
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      r.ops = it->second;
+      return;
+    }
+  }
+  schedule_min_live(r, pinned, carried);
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() < 256) cache.emplace(std::move(key), r.ops);
 }
 
 // Linear-scan assignment of virtual registers to shared-memory slots.
@@ -1146,7 +1172,7 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
   }
   if ((int)q.r.ops.size() > kMaxOps) throw Error(kEInval, "resident program too long");
 
-  schedule_min_live(q.r, {q.A, q.bv}, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}});
+  schedule_min_live_cached(q.r, {q.A, q.bv}, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}});
   Alloc al = assign(q.r, {q.A, q.bv}, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}});
   std::vector<BOp> ops = q.r.ops;
   auto ph = [&](int v) -> int16_t { return v >= 0 ? al.phys[v] : (int16_t)-1; };

@@ -34,3 +34,23 @@ def rel_fro(x, ref):
     ref = np.asarray(ref)
     den = np.linalg.norm(ref)
     return float(np.linalg.norm(x - ref) / (den if den > 0 else 1.0))
+
+
+def release_gpu_memory():
+    """Hand cached device memory back before a test starts other GPU processes
+    (the caching allocator of this process may still hold tens of GB from the
+    full-size tests)."""
+    import gc
+
+    gc.collect()
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+            from paper_2008_11480_b200 import _lib
+
+            _lib.call("si_trim", _lib.handle(0))
+    except Exception:  # noqa: BLE001 -- best effort
+        pass

@@ -404,6 +404,10 @@ def test_c5_full_size_recursive_step():
     x[np.arange(len(rows)), rows] += 1.0
     got = f[rows].cpu().numpy()
     assert np.max(np.abs(got - x)) <= 1e-9 * max(1.0, np.max(np.abs(x)))
+    del st, st1, sp, g, f, b
+    from conftest import release_gpu_memory
+
+    release_gpu_memory()
 
 
 def test_c3_full_size_properties():

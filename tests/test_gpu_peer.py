@@ -233,6 +233,9 @@ def test_ipc_processes_composite_step(tmp_path):
 
     import paper_2008_11480_b200 as P
 
+    from conftest import release_gpu_memory
+
+    release_gpu_memory()
     n, world = 384, 2
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
