@@ -469,15 +469,17 @@ template <int NP>
 struct Geo {
   static constexpr int SLOT = NP * NP;
 #ifndef SI_RESIDENT_WARPS32
-#define SI_RESIDENT_WARPS32 4
+#define SI_RESIDENT_WARPS32 2
 #endif
 #ifndef SI_RESIDENT_WARPS64
 #define SI_RESIDENT_WARPS64 16
 #endif
-  // NP=32: four warps with 16x16 warp tiles (2x2 DMMA tiles, one fragment
-  // load per DMMA); with several CTAs per SM the shared-memory pipe, not
-  // latency, is the tighter limit, and 8x16 warp tiles (1.5 loads per DMMA)
-  // measured 16% slower.  NP=64 runs one CTA per SM: 16 warps hide latency.
+  // NP=32: two warps with 32x16 warp tiles (4x2 DMMA tiles: 0.75 fragment
+  // loads per DMMA and 8 independent accumulator chains per warp); with four
+  // CTAs per SM the shared-memory pipe and DMMA dependency latency, not warp
+  // count, are the limits (measured: 8 warps of 8x16 tiles 1739 iters/s,
+  // 4 warps of 16x16 2430, 2 warps of 32x16 2511).  NP=64 runs one CTA per
+  // SM: 16 warps hide latency.
   static constexpr int WARPS = NP == 32 ? SI_RESIDENT_WARPS32 : SI_RESIDENT_WARPS64;
   static constexpr int THREADS = WARPS * 32;
   static constexpr int WROWS = NP / (WARPS / 2);  // warp tile rows (16)
@@ -703,10 +705,10 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
           // On the DMMA pipe, not the FP64 ALU: x becomes column 0 of an 8-wide B
           // fragment (zeros elsewhere).  A DFMA + shuffle-tree GEMV contends with
           // the other resident CTAs' DMMAs and was 2.5x slower than a full GEMM op.
-          if (warp < NP / 8) {
+          for (int rt = warp; rt < NP / 8; rt += G::WARPS) {  // 8-row tiles
             const double* A = mslot(o.a);
             const double* x = vslot(o.b);
-            const int r0 = warp * 8;
+            const int r0 = rt * 8;
             double acc[2][2] = {};
 #pragma unroll
             for (int kk = 0; kk < NP; kk += 4) {
