@@ -91,3 +91,17 @@ def test_exact_inverse_is_reproduced():
                           P.CompositeSpec((3,)), 2)
     assert np.allclose(st.estimate.cpu().numpy(), np.diag([0.5, 0.25]), atol=1e-15)
     assert P.fro_norm(st.residual) <= 1e-15
+
+
+def test_c_host_demo():
+    """A non-Python host of the C ABI (examples/c_host_demo.c: split, initial
+    series, plain Richardson + NS steps, norms, error status) built by build()."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples",
+                       "c_host_demo")
+    assert os.path.exists(exe), "examples/c_host_demo not built (run build())"
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "bad-call status=-1" in out.stdout
