@@ -11,10 +11,13 @@ results are independent of the number of ranks.
 
 The GEMM DAG is the reference's (series_toolkit.py:263-457,
 newton_schulz.py:177-228, richardson.py:81-189), so ``MulCounter`` deltas
-match the single-GPU path and the reference tick for tick.  The collective
-layer is ``torch.distributed`` (NCCL over NVLink on B200 boxes, gloo in the
-CPU tests); the local-ops layer is injectable so the orchestration can be
-exercised on CPU, but the product default (:class:`CudaOps`) has no host path.
+match the single-GPU path and the reference tick for tick.  The row-panel
+exchange is pluggable: :class:`~paper_2008_11480_b200.peer.PeerComm` (copy
+engines over CUDA IPC, products gated per panel inside the DMMA kernel -- the
+product path) or :class:`RowComm` (``torch.distributed`` all-gather: NCCL as
+the baseline, gloo in the CPU tests).  The local-ops layer is injectable so
+the orchestration can be exercised on CPU, but the product default
+(:class:`CudaOps`) has no host path.
 """
 
 from __future__ import annotations
