@@ -277,7 +277,37 @@ def config_runs():
     np.savez_compressed(os.path.join(HERE, "c5.npz"), **d)
 
 
+def harness_runs():
+    """run_comparison (harness.py:343-387) + records_to_csv (hx:395-404) on a small
+    SPD system, every method kind, with a deterministic injected timer."""
+    rng = np.random.default_rng(1234)
+    n = 24
+    a = spd(n, rng, shift=0.8)
+    theta_star = rng.standard_normal(n)
+    b = a @ theta_star
+    methods = [si.MethodSpec("ns", order=2, h=1), si.MethodSpec("ns", order=3, h=4),
+               si.MethodSpec("double", order=2, h=2),
+               si.MethodSpec("composite", order=2, h=1, rates=(2, 3)),
+               si.MethodSpec("sri", order=2, h=3), si.MethodSpec("ns-estimator", order=2, h=1),
+               si.MethodSpec("richardson", order=2, h=1),
+               si.MethodSpec("richardson-recursive", order=3, h=2)]
+    clock = [0]
+
+    def timer():
+        clock[0] += 1000
+        return clock[0]
+
+    recs = si.run_comparison(a, b, theta_star, methods, 4, timer=timer)
+    out = {"a": a.tolist(), "b": b.tolist(), "theta_star": theta_star.tolist(), "steps": 4,
+           "methods": [[m.kind, m.order, m.h, m.q, list(m.rates), m.label] for m in methods],
+           "csv": si.records_to_csv(recs),
+           "diverged": [bool(r.diverged) for r in recs]}
+    with open(os.path.join(HERE, "harness.json"), "w") as fh:
+        json.dump(out, fh)
+
+
 if __name__ == "__main__":
+    harness_runs()
     plans_json()
     toolkit()
     ns_family()

@@ -1,0 +1,82 @@
+"""The comparison-run / CSV layer (paper_2008_11480_b200/harness.py) against the
+reference's own run_comparison output (tests/golden/harness.json, written by
+tests/golden/make_golden.py with a deterministic timer).
+
+CPU: method names, (p, w) choice, CSV round trip of the reference's text.
+GPU: the device run gives the same records -- integers (k, exponent,
+mmm_cum, wall_ns) exactly, norms and bounds within the FP64 tolerance."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+
+def _fixture():
+    with open(os.path.join(GOLDEN, "harness.json")) as fh:
+        return json.load(fh)
+
+
+def _methods(d):
+    from paper_2008_11480_b200.harness import MethodSpec
+
+    return [MethodSpec(kind, order, h, q, tuple(rates), label)
+            for kind, order, h, q, rates, label in d["methods"]]
+
+
+def test_csv_round_trip_of_reference_text():
+    from paper_2008_11480_b200.harness import parse_run_records, records_to_csv
+
+    d = _fixture()
+    recs = parse_run_records(d["csv"])
+    assert records_to_csv(recs) == d["csv"]
+    with pytest.raises(ValueError):
+        parse_run_records("nope\n")
+    with pytest.raises(ValueError):
+        parse_run_records(d["csv"].splitlines()[0] + "\nx,1,2\n")
+
+
+def test_method_names_and_series_params():
+    from paper_2008_11480_b200.harness import parse_run_records, series_params
+
+    d = _fixture()
+    names = sorted({r.method for r in parse_run_records(d["csv"])})
+    assert names == sorted(m.name() for m in _methods(d))
+    assert series_params(1) == (0, 1)
+    with pytest.raises(ValueError):
+        series_params(0)
+    for h in range(2, 20):
+        p, w = series_params(h)
+        assert w * (p + 1) == h
+
+
+@pytest.mark.gpu
+def test_device_run_matches_reference_records():
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200.harness import parse_run_records
+
+    d = _fixture()
+    clock = [0]
+
+    def timer():
+        clock[0] += 1000
+        return clock[0]
+
+    recs = P.run_comparison(np.array(d["a"]), np.array(d["b"]), np.array(d["theta_star"]),
+                            _methods(d), d["steps"], timer=timer)
+    ref = parse_run_records(d["csv"])
+    assert [(r.method, r.k, r.exponent, r.mmm_cum, r.wall_ns) for r in recs] == \
+        [(r.method, r.k, r.exponent, r.mmm_cum, r.wall_ns) for r in ref]
+    assert [r.diverged for r in recs] == d["diverged"]
+    err0 = {q.method: q.error_norm for q in ref if q.k == 0}
+    for r, q in zip(recs, ref):
+        # norms of quantities that converge to 0: relative, plus an absolute floor
+        # of 1e-12 x the method's initial error (the FP64 noise of a residual)
+        tol = 1e-10 * q.error_norm + 1e-12 * err0[q.method]
+        assert abs(r.error_norm - q.error_norm) <= tol, (r, q)
+        assert abs(r.predicted_bound - q.predicted_bound) <= 1e-8 * max(q.predicted_bound,
+                                                                          1e-300), (r, q)
+    assert P.records_to_csv(recs).splitlines()[0] == P.CSV_HEADER
