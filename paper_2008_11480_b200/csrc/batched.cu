@@ -705,21 +705,32 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
           // On the DMMA pipe, not the FP64 ALU: x becomes column 0 of an 8-wide B
           // fragment (zeros elsewhere).  A DFMA + shuffle-tree GEMV contends with
           // the other resident CTAs' DMMAs and was 2.5x slower than a full GEMM op.
-          for (int rt = warp; rt < NP / 8; rt += G::WARPS) {  // 8-row tiles
-            const double* A = mslot(o.a);
-            const double* x = vslot(o.b);
-            const int r0 = rt * 8;
-            double acc[2][2] = {};
+          // Each warp takes its 8-row tiles side by side with K split over 4
+          // accumulator sets: the dependent DMMA chains are NP/16 deep and
+          // interleaved (GEMVs are latency, not throughput).
+          constexpr int RTW = (NP / 8 + G::WARPS - 1) / G::WARPS;
+          const double* A = mslot(o.a);
+          const double* x = vslot(o.b);
+          double acc[RTW][4][2] = {};
 #pragma unroll
-            for (int kk = 0; kk < NP; kk += 4) {
-              const double af = A[G::idx(r0 + g, kk + t)];
-              const double bf = g == 0 ? x[kk + t] : 0.0;
-              const int h = (kk >> 2) & 1;
-              dmma(acc[h][0], acc[h][1], af, bf);
+          for (int kk = 0; kk < NP; kk += 4) {
+            const double bf = g == 0 ? x[kk + t] : 0.0;
+#pragma unroll
+            for (int j = 0; j < RTW; ++j) {
+              const int rt = warp + j * G::WARPS;
+              if (rt < NP / 8) {
+                const double af = A[G::idx(rt * 8 + g, kk + t)];
+                dmma(acc[j][(kk >> 2) & 3][0], acc[j][(kk >> 2) & 3][1], af, bf);
+              }
             }
-            if (t == 0) {  // lane (g, 0) holds row r0 + g, column 0
-              const int row = r0 + g;
-              const double s = __dadd_rn(acc[0][0], acc[1][0]);
+          }
+#pragma unroll
+          for (int j = 0; j < RTW; ++j) {
+            const int rt = warp + j * G::WARPS;
+            if (rt < NP / 8 && t == 0) {  // lane (g, 0) holds row rt*8 + g, column 0
+              const int row = rt * 8 + g;
+              const double s = __dadd_rn(__dadd_rn(acc[j][0][0], acc[j][1][0]),
+                                         __dadd_rn(acc[j][2][0], acc[j][3][0]));
               const double cv = o.c >= 0 ? vslot(o.c)[row] : 0.0;
               double v;
               if (o.mode == 1)
