@@ -95,7 +95,9 @@ SI_API int si_gemm_ex(si_handle h, int64_t m, int64_t n, int64_t k, double alpha
  * panels [panel_bounds[p], panel_bounds[p+1]) (panel_bounds[0] = 0,
  * panel_bounds[npanels] = k): rows of panel p are read only once
  * ready_flags[p] >= epoch (wrap-safe).  The DMMA kernel gates its TMA loads
- * per panel; other kernels wait on the stream.  npanels = 0: ungated. */
+ * per panel; other kernels wait on the stream.  npanels = 0: ungated.  The
+ * flags must be raised by work that needs no SM (copy engines, stream memory
+ * operations): the gated kernel may occupy every SM while it waits. */
 SI_API int si_gemm_panels(si_handle h, int64_t m, int64_t n, int64_t k, double alpha,
                           const double* A, int64_t lda, const double* B, int64_t ldb,
                           double beta, const double* C, int64_t ldc, double diag,
@@ -219,7 +221,9 @@ SI_API int si_composite_step_ex(si_handle h, int64_t n, const double* a, const d
  * {a, g, f, precond, residual, split_matrix}; rows [n p / npanels,
  * n (p+1) / npanels) of input i are valid once input_flags[16 i + p] >= epoch.
  * The DMMA products gate their A-tile / B-slab loads on those flags, so the
- * first product starts while later panels are still copying.  f_chunks > 0:
+ * first product starts while later panels are still copying.  The flags must
+ * be raised by work that needs no SM (copy engines, stream memory operations):
+ * gated products may occupy every SM while they wait.  f_chunks > 0:
  * F' = I - G'A is produced in f_chunks row blocks, f_chunk_events[k] recorded
  * after block k (one product in the counters). */
 SI_API int si_composite_step_gated(si_handle h, int64_t n, const double* a, const double* g,

@@ -218,7 +218,9 @@ def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_
     panels; ``flags`` is a CUDA int32 tensor of 6 x 16 flags (inputs a,
     estimate, residual, precond, split_residual, matrix; panel p of n rows is
     rows [n p / npanels, n (p+1) / npanels)), raised (>= epoch) behind each
-    panel's copy -- the products gate their loads per panel.
+    panel's copy -- the products gate their loads per panel.  The flags must be
+    raised by work that needs no SM (copy-engine copies, stream memory
+    operations): the gated products may hold every SM while they wait.
     ``residual_chunks`` (list of ``torch.cuda.Event``): F' is produced in that
     many row blocks, each event recorded after its block."""
     if order_n < 1:

@@ -217,7 +217,8 @@ def test_composite_step_with_inputs_in_flight():
         P.composite_step(st, sp.matrix, sp, spec, 2, inputs_ready={"bogus": done})
 
 
-def test_composite_step_with_inputs_in_row_panels():
+@pytest.mark.parametrize("concurrent", [False, True])
+def test_composite_step_with_inputs_in_row_panels(concurrent):
     """Inputs copied host->device panel by panel (out of order, a delaying copy
     first) with flags; the DMMA products gate their loads per panel and F' comes
     out in row blocks: bitwise the resident-input result, same product count."""
@@ -238,8 +239,10 @@ def test_composite_step_with_inputs_in_row_panels():
     flags = torch.zeros(96, dtype=torch.int32, device="cuda")
     slot = {"a": (0, 5), "g": (1,), "f": (2,), "p": (3,), "b": (4,)}
     d = {k: torch.empty_like(v, device="cuda") for k, v in host.items()}
-    big = torch.empty(32 << 20, dtype=torch.float64, device="cuda")
-    big2 = torch.empty_like(big)
+    # the delay on the copy stream must not need SMs (the gated products may hold
+    # them all while they wait): a host->device copy runs on a copy engine
+    big = torch.empty(16 << 20, dtype=torch.float64).pin_memory()
+    big2 = torch.empty(big.shape, dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
     up = torch.cuda.Stream()
     h = _lib.handle(0)
@@ -249,10 +252,11 @@ def test_composite_step_with_inputs_in_row_panels():
     sp2 = P.Splitting(precond=d["p"], residual=d["b"], matrix=d["a"], kind="scalar", verify=False)
     chunks = [torch.cuda.Event() for _ in range(4)]
     done = torch.cuda.Event()
-    out = P.composite_step(st2, sp2.matrix, sp2, spec, 2, input_panels=(flags, 3, npanels),
-                           residual_chunks=chunks, estimate_done=done)
+    out = P.composite_step(st2, sp2.matrix, sp2, spec, 2, object() if concurrent else None,
+                           input_panels=(flags, 3, npanels), residual_chunks=chunks,
+                           estimate_done=done)
     with torch.cuda.stream(up):
-        big2.copy_(big)  # the step is already waiting on the flags
+        big2.copy_(big, non_blocking=True)  # the step is already waiting on the flags
         for k in ("b", "p", "a", "g", "f"):
             for p in reversed(range(npanels)):
                 r0, r1 = bounds[p], bounds[p + 1]
