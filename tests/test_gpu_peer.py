@@ -305,3 +305,32 @@ def test_virtual_ranks_fused_gate_engine(monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(torch.cat([e.rows_of(o[0]) for e, o in zip(engs, outs)]), ref.estimate)
     assert torch.equal(torch.cat([e.rows_of(o[1]) for e, o in zip(engs, outs)]), ref.residual)
+
+
+def test_virtual_ranks_fused_four_ranks_at_size(monkeypatch):
+    """Four virtual ranks, fused (in-kernel panel gates), n=2048: the persistent
+    grid is capped at 36 CTAs so the four ranks' products are co-resident; the
+    composite step over the peer exchange equals the native step bitwise."""
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import configs
+
+    monkeypatch.setenv("SI_GEMM_MAX_CTAS", "36")
+    n, world = 2048, 4
+    a = P.as_device(configs.c4_householder(n=n, rhs=1)[0])
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False, verify=False)
+    st = P.initial_series(sp, 0, 1, order=2)
+    ref = P.composite_step(st, a, sp, P.CompositeSpec((2, 3, 4, 5)), 2)
+    engs, streams = _virtual_ranks(n, world, mode="fused")
+    outs = []
+    for eng, s in zip(engs, streams):
+        c = eng.comm
+        with torch.cuda.stream(s):
+            s.wait_stream(torch.cuda.default_stream())
+            A, Pm, B = eng.replicated(a), eng.replicated(sp.precond), eng.replicated(sp.residual)
+            g, f = eng.composite_step(eng.local(st.estimate[c.r0:c.r1].clone()),
+                                      eng.local(st.residual[c.r0:c.r1].clone()), A, Pm, B,
+                                      (2, 3, 4, 5), 2)
+            outs.append((g, f))
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([e.rows_of(o[0]) for e, o in zip(engs, outs)]), ref.estimate)
+    assert torch.equal(torch.cat([e.rows_of(o[1]) for e, o in zip(engs, outs)]), ref.residual)
