@@ -107,13 +107,14 @@ def _virtual_ranks(n, world, mode="stream"):
     return engs, streams
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_virtual_ranks_composite_step_bitwise(world):
+@pytest.mark.parametrize("world,n", [(2, 384), (3, 384), (3, 386), (4, 200)])
+def test_virtual_ranks_composite_step_bitwise(world, n):
     """composite_step (newton_schulz.py:177-228) on P block-row virtual ranks
-    exchanging panels over the peer path equals the native single-GPU step."""
+    exchanging panels over the peer path equals the native single-GPU step
+    (uneven splits: 386 = 129 + 129 + 128, panel bounds off the 16-row k-slabs;
+    n = 200: row blocks of 50 below the DMMA kernel's 128-row tiles)."""
     import paper_2008_11480_b200 as P
 
-    n = 384
     rng = np.random.default_rng(5)
     g = rng.standard_normal((2 * n, n))
     a_np = g.T @ g / (2 * n) + 0.5 * np.eye(n)
