@@ -441,13 +441,12 @@ class Workload:
 
     def _e2e_step_overlapped(self, host):
         """c4 / c3 through the public API with HOST inputs, copies overlapped with the
-        step.  c4: the inputs are copied H2D in row panels on a copy stream, each
-        panel raising a flag, and ``composite_step(input_panels=...)`` gates its
-        DMMA loads per panel, so the first product starts once the first panels
-        are in (not after whole matrices); G' is read back while F' = I - G' A
-        is computed and F' row block by row block (``residual_chunks``).  c3:
-        per-input events (``ns_step(inputs_ready=...)``).  The plain-Richardson
-        products run while F' goes back."""
+        step: the inputs are copied H2D in row panels on a copy stream, each
+        panel raising a flag, and the step (``input_panels=...``) gates its DMMA
+        loads per panel, so the first product starts once the first panels are
+        in (not after whole matrices); G' is read back while F' = I - G' A is
+        computed and F' row block by row block (``residual_chunks``).  The
+        plain-Richardson products run while F' goes back."""
         import torch
 
         from paper_2008_11480_b200 import _lib
@@ -479,49 +478,50 @@ class Workload:
                           up.cuda_stream)
 
         if self.cfg == "c4":
+            # the first product B S^-1 + S^-1 needs B's first row tiles and all of
+            # S^-1's k-panels: B panel 0, S^-1, the rest of B, then A, G, F
             order = ("precond", "residual", "a", "g", "f", "b", "theta")
-            with torch.cuda.stream(up):
-                for k in order:
-                    d[k] = torch.empty(host["in"][k].shape, dtype=torch.float64, device=dev)
-                    d[k].record_stream(main)
-                # the first product B S^-1 + S^-1 needs B's first row tiles and all of
-                # S^-1's k-panels: B panel 0, S^-1, the rest of B, then A, G, F
-                panel("residual", 0)
-                for p in range(npanels):
-                    panel("precond", p)
-                for p in range(1, npanels):
-                    panel("residual", p)
-                for k in ("a", "g", "f"):
-                    for p in range(npanels):
-                        panel(k, p)
-                    ev[k] = torch.cuda.Event()
-                    ev[k].record(up)
-                for k in ("b", "theta"):
-                    d[k].copy_(host["in"][k], non_blocking=True)
-                    ev[k] = torch.cuda.Event()
-                    ev[k].record(up)
+            first_a, first_b, rest = "residual", "precond", ("a", "g", "f")
         else:
-            order = ("f", "g", "a", "b", "theta")
-            with torch.cuda.stream(up):
-                for k in order:
-                    d[k] = host["in"][k].to(dev, non_blocking=True)
-                    d[k].record_stream(main)
-                    ev[k] = torch.cuda.Event()
-                    ev[k].record(up)
+            # the first product F G + G (h8 plan): F's first rows, all of G, then
+            # the rest of F and A
+            order = ("g", "f", "a", "b", "theta")
+            first_a, first_b, rest = "f", "g", ("a",)
+        with torch.cuda.stream(up):
+            for k in order:
+                d[k] = torch.empty(host["in"][k].shape, dtype=torch.float64, device=dev)
+                d[k].record_stream(main)
+            panel(first_a, 0)
+            for p in range(npanels):
+                panel(first_b, p)
+            ev[first_b] = torch.cuda.Event()
+            ev[first_b].record(up)
+            for p in range(1, npanels):
+                panel(first_a, p)
+            ev[first_a] = torch.cuda.Event()
+            ev[first_a].record(up)
+            for k in rest:
+                for p in range(npanels):
+                    panel(k, p)
+                ev[k] = torch.cuda.Event()
+                ev[k].record(up)
+            for k in ("b", "theta"):
+                d[k].copy_(host["in"][k], non_blocking=True)
+                ev[k] = torch.cuda.Event()
+                ev[k].record(up)
         st = P.NsState(estimate=d["g"], residual=d["f"], step=0, order=self.st.order,
                        series_order=1, ctr=P.MulCounter())
         g_done = torch.cuda.Event()
-        chunks = []
+        chunks = [torch.cuda.Event() for _ in range(npanels)]
         if self.cfg == "c4":
             sp = P.Splitting(precond=d["precond"], residual=d["residual"], matrix=d["a"],
                              kind="scalar", verify=False)
-            chunks = [torch.cuda.Event() for _ in range(npanels)]
             new = P.composite_step(st, sp.matrix, sp, self.spec, 2,
                                    input_panels=(flags, epoch, npanels), residual_chunks=chunks,
                                    estimate_done=g_done)
         else:
-            new = P.ns_step(st, d["a"], plan=self.plan8, inputs_ready={
-                "a": ev["a"], "estimate": ev["g"], "residual": ev["f"]}, estimate_done=g_done)
+            new = P.ns_step(st, d["a"], plan=self.plan8, input_panels=(flags, epoch, npanels),
+                            residual_chunks=chunks, estimate_done=g_done)
         down.wait_event(g_done)
         with torch.cuda.stream(down):
             host["out"]["g"].copy_(new.estimate, non_blocking=True)

@@ -192,6 +192,15 @@ SI_API int si_ns_step_ex(si_handle h, int64_t n, const double* a, const double* 
                          const double* consts, int64_t nconsts, void* const* input_ready_events,
                          void* g_done_event, double* g_out, double* f_out, int64_t* counters,
                          void* stream);
+/* si_ns_step for inputs arriving in row panels (see si_composite_step_gated):
+ * input_flags = 3 x 16 uint32 flags for {a, g, f}; f_chunks > 0: F' produced in
+ * f_chunks row blocks, f_chunk_events[k] recorded after block k. */
+SI_API int si_ns_step_gated(si_handle h, int64_t n, const double* a, const double* g,
+                            const double* f, int order, const int32_t* plan, int64_t plan_len,
+                            const double* consts, int64_t nconsts, const uint32_t* input_flags,
+                            uint32_t epoch, int npanels, void* g_done_event,
+                            void* const* f_chunk_events, int f_chunks, double* g_out,
+                            double* f_out, int64_t* counters, void* stream);
 /* composite_step (newton_schulz.py:177-228).  plans/plan_offsets[nrates+1]
  * hold, per rate, the geometric_apply base plan (empty for rate 1). */
 SI_API int si_composite_step(si_handle h, int64_t n, const double* a, const double* g, const double* f,

@@ -485,6 +485,38 @@ int si_ns_step_ex(si_handle h, int64_t n, const double* a, const double* g, cons
   });
 }
 
+int si_ns_step_gated(si_handle h, int64_t n, const double* a, const double* g, const double* f,
+                     int order, const int32_t* plan, int64_t plan_len, const double* consts,
+                     int64_t nconsts, const uint32_t* input_flags, uint32_t epoch, int npanels,
+                     void* g_done_event, void* const* f_chunk_events, int f_chunks,
+                     double* g_out, double* f_out, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && g && f && g_out && f_out, "null pointer");
+    need(!input_flags || (npanels >= 1 && npanels <= kMaxPanels), "npanels out of range");
+    need(f_chunks >= 0 && (f_chunks == 0 || f_chunk_events), "bad f_chunks");
+    PlanPtr pl = opt_plan(plan, plan_len, consts, nconsts);
+    std::vector<cudaEvent_t> chunks(f_chunks);
+    for (int k = 0; k < f_chunks; ++k) chunks[k] = reinterpret_cast<cudaEvent_t>(f_chunk_events[k]);
+    Call call(h, stream, counters);
+    if (input_flags) {
+      const double* bases[3] = {a, g, f};
+      for (int i = 0; i < 3; ++i) {
+        Ctx::Gate gt{};
+        gt.base = bases[i];
+        gt.pw.ready = input_flags + kMaxPanels * i;
+        gt.pw.epoch = epoch;
+        gt.pw.npanels = npanels;
+        for (int p = 0; p <= npanels; ++p) gt.pw.bounds[p] = (int)(n * p / npanels);
+        gt.stream_done = false;
+        call.c.gates.push_back(gt);
+      }
+    }
+    ns_step(call.c, sq(a, n), sq(g, n), sq(f, n), order, pl.get(), sq(g_out, n), sq(f_out, n),
+            reinterpret_cast<cudaEvent_t>(g_done_event), f_chunks,
+            f_chunks ? chunks.data() : nullptr);
+  });
+}
+
 int si_composite_step(si_handle h, int64_t n, const double* a, const double* g, const double* f,
                       const double* precond, const double* residual, const double* split_matrix,
                       int nrates, const int32_t* rates, const int32_t* plans,

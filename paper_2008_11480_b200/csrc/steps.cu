@@ -20,9 +20,26 @@ void initial_series(Ctx& c, const MV& P, const MV& B, const MV& A, int p, int w,
   residual_into(c, Fout, Gout, A);
 }
 
+// F' = I - G' A in `chunks` row blocks, events[k] recorded after block k (its
+// rows may go device->host while the next block is computed); one counted
+// product, as in the reference DAG.
+static void residual_chunked(Ctx& c, const MV& Fout, const MV& Gout, const MV& A, int chunks,
+                             const cudaEvent_t* events) {
+  const int64_t n = Fout.v.rows;
+  for (int k = 0; k < chunks; ++k) {
+    const int64_t r0 = n * k / chunks, r1 = n * (k + 1) / chunks;
+    MV fr = view(Fout.v.p + r0 * Fout.v.ld, r1 - r0, Fout.v.cols, Fout.v.ld);
+    MV gr = view(Gout.v.p + r0 * Gout.v.ld, r1 - r0, Gout.v.cols, Gout.v.ld);
+    gemm(c, fr, gr, A, -1.0, nullptr, 0.0, 1.0, false, r0);  // rows of I - G'A
+    if (events && events[k]) check(cudaEventRecord(events[k], c.s), "cudaEventRecord");
+  }
+  c.ctr.mmm -= chunks - 1;
+}
+
 // ns:150-174
 void ns_step(Ctx& c, const MV& A, const MV& G, const MV& F, int order, const PlanNode* plan,
-             const MV& Gout, const MV& Fout, cudaEvent_t g_done) {
+             const MV& Gout, const MV& Fout, cudaEvent_t g_done, int f_chunks,
+             const cudaEvent_t* f_chunk) {
   if (order < 1) throw Error(kEInval, "order must be >= 1");
   MV g;
   if (plan) {
@@ -33,7 +50,10 @@ void ns_step(Ctx& c, const MV& A, const MV& G, const MV& F, int order, const Pla
   }
   copy_into(c, Gout, g);
   if (g_done) check(cudaEventRecord(g_done, c.s), "cudaEventRecord");  // G' may go D2H now
-  residual_into(c, Fout, Gout, A);
+  if (f_chunks > 0)
+    residual_chunked(c, Fout, Gout, A, f_chunks, f_chunk);
+  else
+    residual_into(c, Fout, Gout, A);
 }
 
 // ns:177-228 -- parts (T_i, Gamma_i) are independent of each other and of the
@@ -101,15 +121,7 @@ void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, 
   gemm(c, Gout, r, nsp, 1.0, &t, 1.0);  // G = t + r ns
   if (e.g_done) check(cudaEventRecord(e.g_done, c.s), "cudaEventRecord");  // G' may go D2H now
   if (e.f_chunks > 0 && e.f_chunk) {
-    const int64_t n = Fout.v.rows;
-    for (int k = 0; k < e.f_chunks; ++k) {
-      const int64_t r0 = n * k / e.f_chunks, r1 = n * (k + 1) / e.f_chunks;
-      MV fr = view(Fout.v.p + r0 * Fout.v.ld, r1 - r0, Fout.v.cols, Fout.v.ld);
-      MV gr = view(Gout.v.p + r0 * Gout.v.ld, r1 - r0, Gout.v.cols, Gout.v.ld);
-      gemm(c, fr, gr, A, -1.0, nullptr, 0.0, 1.0, false, r0);  // rows of I - G'A
-      if (e.f_chunk[k]) check(cudaEventRecord(e.f_chunk[k], c.s), "cudaEventRecord");
-    }
-    c.ctr.mmm -= e.f_chunks - 1;  // one product of the reference DAG
+    residual_chunked(c, Fout, Gout, A, e.f_chunks, e.f_chunk);
     return;
   }
   residual_into(c, Fout, Gout, A);

@@ -9,8 +9,10 @@ void initial_series(Ctx& c, const MV& P, const MV& B, const MV& A, int p, int w,
                     const MV& Fout);
 // g_done (optional) is recorded once G' is final, before F' = I - G' A.
 // Inputs in flight are registered on the Ctx (Ctx::awaits).
+// f_chunks > 0: F' in that many row blocks, f_chunk[k] recorded after block k.
 void ns_step(Ctx& c, const MV& A, const MV& G, const MV& F, int order, const PlanNode* plan,
-             const MV& Gout, const MV& Fout, cudaEvent_t g_done = nullptr);
+             const MV& Gout, const MV& Fout, cudaEvent_t g_done = nullptr, int f_chunks = 0,
+             const cudaEvent_t* f_chunk = nullptr);
 // Optional per-input readiness (e.g. host->device copies still in flight on a
 // copy stream): the step waits on each event just before the input's first
 // use, and records g_done once G' is final (before F' = I - G' A).

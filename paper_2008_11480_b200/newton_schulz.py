@@ -128,12 +128,13 @@ def initial_series(split: Splitting, p: int, w: int, order: int = 2) -> NsState:
 
 
 def ns_step(st: NsState, a, plan: FactorPlan | None = None, *, inputs_ready: dict | None = None,
-            estimate_done=None) -> NsState:
+            estimate_done=None, input_panels: tuple | None = None,
+            residual_chunks: list | None = None) -> NsState:
     """G_k = S_n(F) G (Horner or ``plan``), F_k = I - G_k A (newton_schulz.py:150-174).
 
-    ``inputs_ready`` (keys ``a``, ``estimate``, ``residual``) and ``estimate_done``
-    as in :func:`composite_step`: inputs still being copied are waited for right
-    before their first use; ``estimate_done`` is recorded before the last product."""
+    ``inputs_ready`` (keys ``a``, ``estimate``, ``residual``), ``estimate_done``,
+    ``input_panels`` (flags 3 x 16 for a, estimate, residual) and
+    ``residual_chunks`` as in :func:`composite_step`."""
     n = st.order
     a = as_device(a)
     if a.shape != st.estimate.shape:
@@ -148,6 +149,20 @@ def ns_step(st: NsState, a, plan: FactorPlan | None = None, *, inputs_ready: dic
     f = torch.empty_like(st.estimate)
     h, s = _ctx(g)
     buf = _lib.counter_buf()
+    if input_panels is not None or residual_chunks:
+        if inputs_ready:
+            raise ValueError("inputs_ready and input_panels are exclusive")
+        flags_ptr, epoch, npanels = _panel_args(input_panels, 48)
+        chunks = list(residual_chunks or [])
+        evs = (ctypes.c_void_p * max(len(chunks), 1))(*[e.cuda_event for e in chunks])
+        _lib.call("si_ns_step_gated", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
+                  st.residual.data_ptr(), n, _lib.i32_array(code) if code else None, len(code),
+                  _lib.f64_array(consts) if consts else None, len(consts), flags_ptr, epoch,
+                  npanels, estimate_done.cuda_event if estimate_done is not None else None,
+                  evs if chunks else None, len(chunks), g.data_ptr(), f.data_ptr(), buf, s)
+        st.ctr.absorb(buf)
+        return NsState(estimate=g, residual=f, step=st.step + 1, order=n,
+                       series_order=st.series_order, ctr=st.ctr)
     ready = None
     if inputs_ready:
         order3 = ("a", "estimate", "residual")
@@ -164,6 +179,18 @@ def ns_step(st: NsState, a, plan: FactorPlan | None = None, *, inputs_ready: dic
     st.ctr.absorb(buf)
     return NsState(estimate=g, residual=f, step=st.step + 1, order=n,
                    series_order=st.series_order, ctr=st.ctr)
+
+
+def _panel_args(input_panels, words: int):
+    """(flags pointer, epoch, npanels) of an ``input_panels`` tuple (or Nones)."""
+    if input_panels is None:
+        return None, 0, 0
+    flags, epoch, npanels = input_panels
+    if flags.dtype != torch.int32 or flags.numel() < words or not flags.is_cuda:
+        raise ValueError(f"input_panels flags must be a CUDA int32 tensor of {words} flags")
+    if not 1 <= npanels <= 16:
+        raise ValueError("npanels must be in 1..16")
+    return flags.data_ptr(), epoch, npanels
 
 
 @dataclass
@@ -250,14 +277,7 @@ def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_
     if input_panels is not None or residual_chunks:
         if inputs_ready:
             raise ValueError("inputs_ready and input_panels are exclusive")
-        flags_ptr, epoch, npanels = None, 0, 0
-        if input_panels is not None:
-            flags, epoch, npanels = input_panels
-            if flags.dtype != torch.int32 or flags.numel() < 96 or not flags.is_cuda:
-                raise ValueError("input_panels flags must be a CUDA int32 tensor of 6 x 16")
-            if not 1 <= npanels <= 16:
-                raise ValueError("npanels must be in 1..16")
-            flags_ptr = flags.data_ptr()
+        flags_ptr, epoch, npanels = _panel_args(input_panels, 96)
         chunks = list(residual_chunks or [])
         evs = (ctypes.c_void_p * max(len(chunks), 1))(*[e.cuda_event for e in chunks])
         _lib.call("si_composite_step_gated", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),

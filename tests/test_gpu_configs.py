@@ -308,6 +308,50 @@ def test_ns_step_with_inputs_in_flight():
         P.ns_step(st, sp.matrix, inputs_ready={"bogus": done})
 
 
+def test_ns_step_with_inputs_in_row_panels():
+    """ns_step (h8 plan) with F, G, A arriving in row panels behind flags and F'
+    in row blocks: bitwise equal to resident inputs, same product count."""
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import _lib, configs
+
+    n, npanels = 640, 5
+    a, _ = configs.c3_gram(n=n)
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False)
+    plan8 = P.table_plans()[8][0]
+    st = P.initial_series(sp, 0, 1, order=8)
+    c0 = st.ctr.mmm
+    ref = P.ns_step(st, sp.matrix, plan=plan8)
+    n_ref = ref.ctr.mmm - c0
+    host = {k: v.cpu().pin_memory() for k, v in (("a", sp.matrix), ("g", st.estimate),
+                                                   ("f", st.residual))}
+    d = {k: torch.empty_like(v, device="cuda") for k, v in host.items()}
+    flags = torch.zeros(48, dtype=torch.int32, device="cuda")
+    slot = {"a": 0, "g": 1, "f": 2}
+    big = torch.empty(16 << 20, dtype=torch.float64).pin_memory()
+    big2 = torch.empty(big.shape, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    up = torch.cuda.Stream()
+    h = _lib.handle(0)
+    bounds = [n * p // npanels for p in range(npanels + 1)]
+    st2 = P.NsState(estimate=d["g"], residual=d["f"], step=0, order=8, series_order=1,
+                    ctr=P.MulCounter())
+    chunks = [torch.cuda.Event() for _ in range(3)]
+    out = P.ns_step(st2, d["a"], plan=plan8, input_panels=(flags, 9, npanels),
+                    residual_chunks=chunks)
+    with torch.cuda.stream(up):
+        big2.copy_(big, non_blocking=True)  # copy engine: the step waits on flags meanwhile
+        for k in ("g", "f", "a"):
+            for p in range(npanels):
+                r0, r1 = bounds[p], bounds[p + 1]
+                d[k][r0:r1].copy_(host[k][r0:r1], non_blocking=True)
+                _lib.call("si_stream_write_u32", h, flags.data_ptr() + 4 * (16 * slot[k] + p), 9,
+                          up.cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(out.estimate, ref.estimate)
+    assert torch.equal(out.residual, ref.residual)
+    assert out.ctr.mmm == n_ref
+
+
 def test_hoisted_composite_parts_bitwise():
     """Opt-in hoisting evaluates the same T_comp / R_comp DAG once: the steps are
     bitwise identical to the reference-faithful recompute, at 3 products per step
