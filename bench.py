@@ -548,6 +548,73 @@ class Workload:
         d2h = sum(v.numel() * 8 for v in host["out"].values())
         return h2d, d2h
 
+    def pinned_inputs_resident(self):
+        """Host (pinned) inputs and outputs of one resident-kernel launch (c1 / c2)."""
+        import torch
+
+        def pin(t):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            return h
+
+        if self.cfg == "c1":
+            s = self.c1
+            host = {"in": {k: pin(s[k]) for k in ("a", "b", "p", "f", "t")}}
+        else:
+            host = {"in": {"a": pin(self.a2), "b": pin(self.b2), "pre": pin(self.pre2),
+                           "res": pin(self.res2), "p": pin(self.p2), "f": pin(self.f2),
+                           "t": pin(self.t2)}}
+        host["out"] = {k: torch.empty_like(host["in"][k], pin_memory=True) for k in ("p", "f", "t")}
+        return host
+
+    def e2e_step_resident(self, host, chunks: int = 4):
+        """One resident run through the public API from host buffers.  c2: the
+        batch goes in `chunks` slices -- slice i+1 is copied host->device (copy
+        stream) while slice i computes, and slice i's P, F, theta go back while
+        slice i+1 computes.  c1: one system, copies in series."""
+        import torch
+
+        P = self.P
+        main = torch.cuda.current_stream()
+        if not hasattr(self, "_copy_streams"):
+            self._copy_streams = (torch.cuda.Stream(), torch.cuda.Stream())
+        up, down = self._copy_streams
+        up.wait_stream(main)
+        hin, hout = host["in"], host["out"]
+        if self.cfg == "c1":
+            d = {k: v.to("cuda", non_blocking=True) for k, v in hin.items()}
+            p, f, t = P.batched_ns_richardson(d["a"], d["b"], d["p"], d["f"], d["t"], 3,
+                                              self.iters_per_step)
+            hout["p"].copy_(p, non_blocking=True)
+            hout["f"].copy_(f, non_blocking=True)
+            hout["t"].copy_(t, non_blocking=True)
+        else:
+            batch = hin["a"].shape[0]
+            cuts = [batch * i // chunks for i in range(chunks + 1)]
+            for i in range(chunks):
+                lo, hi = cuts[i], cuts[i + 1]
+                with torch.cuda.stream(up):
+                    d = {k: v[lo:hi].to("cuda", non_blocking=True) for k, v in hin.items()}
+                    for v in d.values():
+                        v.record_stream(main)
+                    ready = torch.cuda.Event()
+                    ready.record(up)
+                main.wait_event(ready)
+                p, f, t = P.batched_composite_richardson(d["a"], d["b"], d["pre"], d["res"],
+                                                         d["p"], d["f"], d["t"], (2, 3), 2,
+                                                         self.iters_per_step)
+                done = torch.cuda.Event()
+                done.record(main)
+                down.wait_event(done)
+                with torch.cuda.stream(down):
+                    for k, v in (("p", p), ("f", f), ("t", t)):
+                        hout[k][lo:hi].copy_(v, non_blocking=True)
+                        v.record_stream(down)
+            main.wait_stream(down)
+        h2d = sum(v.numel() * 8 for v in hin.values())
+        d2h = sum(v.numel() * 8 for v in hout.values())
+        return h2d, d2h
+
     def pinned_inputs_sharded(self):
         """This rank's host inputs of a sharded step: the replicated operands and
         its G / F row blocks, in pinned memory; outputs likewise."""
@@ -803,6 +870,22 @@ def run_ours(args):
         e2e = {"value": ksteps / (e_ms / 1e3), "unit": "iters/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": ksteps,
                "bytes": "per rank (A, S^-1, B, b, theta replicated; G, F row blocks)"}
+        del host
+    if not args.no_e2e and args.config in ("c1", "c2") and not w.split_batch:
+        host = w.pinned_inputs_resident()
+        ksteps = max(1, min(args.steps, 3))
+        w.e2e_step_resident(host)  # warm
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(ksteps):
+            h2d, d2h = w.e2e_step_resident(host)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks(f0.elapsed_time(f1), world)
+        e2e = {"value": world * ksteps * w.iters_per_step / (e_ms / 1e3), "unit": "iters/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": ksteps}
         del host
     if not args.no_e2e and args.config in ("c4", "c3") and w.sharded is None and not args.hoist:
         host = w.pinned_inputs()
