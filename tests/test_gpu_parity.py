@@ -488,3 +488,34 @@ def test_resident_ns_plan_and_batch_vs_oracle():
             st = o.ns_step(st, sp.matrix, o.TABLE_ROOTS[8][0][1])
         assert np.linalg.norm(p[i].cpu().numpy() - st.estimate) <= TOL * np.linalg.norm(st.estimate)
         assert np.linalg.norm(th[i].cpu().numpy() - theta) <= TOL * np.linalg.norm(theta)
+
+
+@pytest.mark.parametrize("batch,n,cluster", [(64, 48, None), (40, 64, None), (5, 64, "2"),
+                                             (5, 48, "8"), (3, 64, "0")])
+def test_resident_ns_single_cta_and_cluster_sizes(batch, n, cluster, monkeypatch):
+    """Config-1-shaped runs through both resident kernels: many systems (one CTA
+    per system, 16 warps) and the cluster kernel with 2 / 8 CTAs per system (and
+    cluster mode switched off), each vs the oracle per system."""
+    import paper_2008_11480_b200 as P
+    from oracle import seriesinv_oracle as o
+
+    if cluster is not None:
+        monkeypatch.setenv("SI_RESIDENT_CLUSTER", cluster)
+    rng = np.random.default_rng(batch * 1000 + n)
+    g = rng.standard_normal((batch, 2 * n, n))
+    a_np = np.einsum("bki,bkj->bij", g, g) / (2 * n) + 0.3 * np.eye(n)
+    b_np = rng.standard_normal((batch, n))
+    a = torch.as_tensor(a_np, device="cuda")
+    b = torch.as_tensor(b_np, device="cuda")
+    pre, res = P.batched_scalar_split(a)
+    iters = 4
+    p, f, th = P.batched_ns_richardson(a, b, pre, res, torch.zeros_like(b), 3, iters)
+    for i in sorted({0, batch // 2, batch - 1}):
+        sp = o.split_scalar(a_np[i], o.inf_norm(a_np[i]) / 2.0)
+        st = o.initial_series(sp, 0, 1, 3)
+        theta = np.zeros(n)
+        for _ in range(iters):
+            theta = o.plain_richardson(theta, st.estimate, sp.matrix, b_np[i], st.ctr)
+            st = o.ns_step(st, sp.matrix)
+        assert np.linalg.norm(p[i].cpu().numpy() - st.estimate) <= TOL * np.linalg.norm(st.estimate)
+        assert np.linalg.norm(th[i].cpu().numpy() - theta) <= TOL * np.linalg.norm(theta)
