@@ -462,6 +462,7 @@ struct BatchArgs {
   int last_load;           // index of the last OP_LOAD: the next prefetch is issued after it
   long long* prof;         // per-op cycle totals of CTA 0 (diagnostics; usually null)
   int sA, sG, sF, sT, sb;  // slots of A, the carried inputs, b
+  int sP, sB;              // resident splitting S^-1, B (-1: streamed by OP_LOAD)
   int rG, rF, rT;          // slots of the carried outputs (copied back when different)
 };
 
@@ -647,6 +648,8 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
   double2 pf_p[PFD], pf_b[PFD];
   for (int64_t sys = blockIdx.x; sys < p.batch; sys += gridDim.x) {
     load_mat<NP>(mslot(p.sA), p.a + sys * nn, n);
+    if (p.sP >= 0) load_mat<NP>(mslot(p.sP), p.precond + sys * nn, n);
+    if (p.sB >= 0) load_mat<NP>(mslot(p.sB), p.residual + sys * nn, n);
     load_mat<NP>(mslot(p.sG), p.p_in + sys * nn, n);
     load_mat<NP>(mslot(p.sF), p.f_in + sys * nn, n);
     if (threadIdx.x < NP) {
@@ -935,6 +938,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(Ba
   const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   for (int64_t sys = cid; sys < p.batch; sys += ncl) {
     load_full(mslot(p.sA), p.a + sys * nn);
+    if (p.sP >= 0) load_full(mslot(p.sP), p.precond + sys * nn);
+    if (p.sB >= 0) load_full(mslot(p.sB), p.residual + sys * nn);
     load_full(mslot(p.sG), p.p_in + sys * nn);
     load_full(mslot(p.sF), p.f_in + sys * nn);
     if (threadIdx.x < NP) {
@@ -1142,6 +1147,7 @@ int num_sms_b() {
 struct Recipe {
   Rec r;
   int A, G, F, T, bv;
+  int P = -1, B = -1;  // resident splitting (pinned) instead of per-iteration loads
   int gn = -1, fn = -1, tn = -1;
 };
 
@@ -1185,8 +1191,11 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
   }
   if ((int)q.r.ops.size() > kMaxOps) throw Error(kEInval, "resident program too long");
 
-  schedule_min_live_cached(q.r, {q.A, q.bv}, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}});
-  Alloc al = assign(q.r, {q.A, q.bv}, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}});
+  std::vector<int> pinned = {q.A, q.bv};
+  if (q.P >= 0) pinned.push_back(q.P);
+  if (q.B >= 0) pinned.push_back(q.B);
+  schedule_min_live_cached(q.r, pinned, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}});
+  Alloc al = assign(q.r, pinned, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}});
   std::vector<BOp> ops = q.r.ops;
   auto ph = [&](int v) -> int16_t { return v >= 0 ? al.phys[v] : (int16_t)-1; };
   for (BOp& o : ops) {
@@ -1350,6 +1359,8 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
       args.last_load = (int)k;
     }
   args.sA = al.phys[q.A];
+  args.sP = q.P >= 0 ? al.phys[q.P] : -1;
+  args.sB = q.B >= 0 ? al.phys[q.B] : -1;
   args.sG = al.phys[q.G];
   args.sF = al.phys[q.F];
   args.sT = al.phys[q.T];
@@ -1450,7 +1461,19 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
   // evaluated first (the parts are independent of it) so G and F die early;
   // S^-1 and B are streamed in for the parts and die after the last one.
   const int nsp = q.r.horner(q.F, q.G, order_n);
-  const int P = q.r.load(0), B = q.r.load(1);
+  // S^-1 and B: resident for the whole run (pinned slots), or streamed in every
+  // iteration through registers (OP_LOAD) when their two slots would cost a
+  // CTA per SM (SI_RESIDENT_PIN_SPLIT=0/1 overrides)
+  bool pin = false;
+  if (const char* env = std::getenv("SI_RESIDENT_PIN_SPLIT")) pin = std::atoi(env) != 0;
+  int P, B;
+  if (pin) {
+    q.P = P = q.r.fresh(false);
+    q.B = B = q.r.fresh(false);
+  } else {
+    P = q.r.load(0);
+    B = q.r.load(1);
+  }
   std::vector<int> ts, gs;
   for (size_t i = 0; i < rates.size(); ++i) {
     const int ti = q.r.geometric(B, P, rates[i], q.A, plans[i]);
