@@ -157,12 +157,13 @@ class _LocalView:
 
 
 class _Slot:
-    __slots__ = ("index", "shape", "ptr", "peers", "epoch", "busy")
+    __slots__ = ("index", "shape", "ptr", "peers", "epoch", "busy", "reserved")
 
     def __init__(self, index, shape, ptr, peers):
         self.index, self.shape, self.ptr, self.peers = index, shape, ptr, peers
         self.epoch = 0
         self.busy = False
+        self.reserved = 0  # epoch handed to an in-place producer (output_rows)
 
 
 class _Lease:
@@ -188,10 +189,13 @@ class GatedOperand:
 
 
 class _Pending:
-    __slots__ = ("lease", "epoch", "events", "rows", "cols")
+    __slots__ = ("slot", "keep", "epoch", "events", "rows", "cols")
 
-    def __init__(self, lease, epoch, events, rows, cols):
-        self.lease, self.epoch, self.events, self.rows, self.cols = lease, epoch, events, rows, cols
+    def __init__(self, slot, keep, epoch, events, rows, cols):
+        # `keep` holds the slot's lease (directly, or through the producer's
+        # in-place output view) while the exchange may still read it
+        self.slot, self.keep, self.epoch, self.events = slot, keep, epoch, events
+        self.rows, self.cols = rows, cols
 
 
 class PeerComm:
@@ -212,6 +216,7 @@ class PeerComm:
         self.r0, self.r1 = self.splits[self.rank]
         self.bounds = [s[0] for s in self.splits] + [n]
         self.bytes_gathered = 0
+        self.local_copies = 0  # row blocks copied into a slot (not produced in place)
         self._slots: list[_Slot] = []
         self._cs = None
         self._h = _lib.handle(self.device.index)
@@ -237,6 +242,7 @@ class PeerComm:
     def _acquire(self, shape) -> _Slot:
         for s in self._slots:
             if not s.busy and s.shape == shape:
+                s.reserved = 0  # an in-place reservation whose value died unpublished
                 return s
         if len(self._slots) >= _MAX_SLOTS:
             raise MemoryError("too many live exchange slots")
@@ -250,6 +256,29 @@ class PeerComm:
     def all_gather_rows(self, local: torch.Tensor) -> torch.Tensor:
         return self.finish(self.start_gather(local))
 
+    def _war_wait(self, slot: _Slot, e: int, stream_ptr: int) -> None:
+        """Peers have finished pulling our previous block out of this slot."""
+        if e > 1:
+            for q in range(self.world):
+                if q != self.rank:
+                    _lib.call("si_stream_wait_u32", self._h,
+                              self._flag(self._flags, self._CONSUMED, slot.index, q), e - 1,
+                              stream_ptr)
+
+    def output_rows(self, cols: int):
+        """This rank's row block inside a fresh exchange slot: a product written
+        there is published by :meth:`start_gather` without a copy (the slot's
+        reuse guard is queued now, before the producer writes)."""
+        if self.world == 1:
+            return None
+        slot = self._acquire((self.n, cols))
+        lease = _Lease(slot)
+        e = slot.epoch + 1
+        self._war_wait(slot, e, torch.cuda.current_stream(self.device).cuda_stream)
+        slot.reserved = e
+        return _tensor(slot.ptr + self.r0 * cols * 8, (self.r1 - self.r0, cols), self.device,
+                       lease)
+
     def start_gather(self, local: torch.Tensor):
         """Publish this rank's row block and queue the pulls of the others'."""
         if self.world == 1:
@@ -257,23 +286,27 @@ class PeerComm:
         if local.shape[0] != self.r1 - self.r0:
             raise ValueError("row block does not match this rank's split")
         cols = local.shape[1]
-        slot = self._acquire((self.n, cols))
-        lease = _Lease(slot)
-        slot.epoch += 1
-        e, b = slot.epoch, slot.index
+        row_bytes = cols * 8
         h, me = self._h, self.rank
         cur = torch.cuda.current_stream(self.device)
         sp = cur.cuda_stream
-        row_bytes = cols * 8
-        # WAR: peers have finished pulling our previous block out of this slot
-        if e > 1:
-            for q in range(self.world):
-                if q != me:
-                    _lib.call("si_stream_wait_u32", h,
-                              self._flag(self._flags, self._CONSUMED, b, q), e - 1, sp)
-        src = local.contiguous()
-        _lib.call("si_copy_async", h, slot.ptr + self.r0 * row_bytes, src.data_ptr(),
-                  (self.r1 - self.r0) * row_bytes, sp)
+        slot = next((sl for sl in self._slots if sl.reserved and sl.shape == (self.n, cols)
+                     and sl.ptr + self.r0 * row_bytes == local.data_ptr()), None)
+        if slot is not None:  # produced in place by output_rows: no copy
+            keep = local
+            slot.epoch, slot.reserved = slot.reserved, 0
+            e, b = slot.epoch, slot.index
+        else:
+            slot = self._acquire((self.n, cols))
+            keep = _Lease(slot)
+            slot.epoch += 1
+            e, b = slot.epoch, slot.index
+            self._war_wait(slot, e, sp)
+        if keep is not local:
+            self.local_copies += 1
+            src = local.contiguous()
+            _lib.call("si_copy_async", h, slot.ptr + self.r0 * row_bytes, src.data_ptr(),
+                      (self.r1 - self.r0) * row_bytes, sp)
         for q in range(self.world):
             if q != me:
                 _lib.call("si_stream_write_u32", h,
@@ -302,11 +335,10 @@ class PeerComm:
         done.record(cs)
         events = [done]
         self.bytes_gathered += (self.n - (self.r1 - self.r0)) * row_bytes
-        return _Pending(lease, e, events, self.n, cols)
+        return _Pending(slot, keep, e, events, self.n, cols)
 
     def _view(self, pend: _Pending) -> torch.Tensor:
-        slot = pend.lease.slot
-        return _tensor(slot.ptr, (pend.rows, pend.cols), self.device, pend.lease)
+        return _tensor(pend.slot.ptr, (pend.rows, pend.cols), self.device, pend.keep)
 
     def finish(self, pending) -> torch.Tensor:
         """The full matrix, with the current stream ordered after every pull."""
@@ -321,10 +353,9 @@ class PeerComm:
         """A :class:`GatedOperand` (mode "fused") or the finished matrix."""
         if isinstance(pending, tuple) or self.mode != "fused":
             return self.finish(pending)
-        slot = pending.lease.slot
-        ready = self._flag(self._flags, self._READY, slot.index, 0)
+        ready = self._flag(self._flags, self._READY, pending.slot.index, 0)
         return GatedOperand(self._view(pending), ready, pending.epoch, list(self.bounds),
-                            pending.lease)
+                            pending.keep)
 
     def barrier(self):
         if self.world > 1 and isinstance(self.fabric, IpcFabric):

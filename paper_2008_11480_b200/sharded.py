@@ -109,13 +109,14 @@ class RowComm:
 class CudaOps:
     """Local products and sums on the DMMA library (no host fallback)."""
 
-    def gemm(self, a, b, alpha, c, beta, diag, doff, is_mv, ctr: MulCounter):
+    def gemm(self, a, b, alpha, c, beta, diag, doff, is_mv, ctr: MulCounter, out=None):
         m, k = a.shape
         n = b.shape[1]
         a = a.contiguous()
         if c is not None:
             c = c.contiguous()
-        out = torch.empty((m, n), dtype=torch.float64, device=a.device)
+        if out is None:
+            out = torch.empty((m, n), dtype=torch.float64, device=a.device)
         buf = _lib.counter_buf()
         if not isinstance(b, torch.Tensor):  # peer.GatedOperand: panel-gated product
             _lib.call("si_gemm_panels", _lib.handle(a.device.index), m, n, k, alpha, a.data_ptr(),
@@ -227,10 +228,16 @@ class ShardedEngine:
 
     def mm(self, lhs: Sharded, rhs: Sharded, alpha=1.0, c: Sharded | None = None, beta=0.0,
            diag=0.0, mv=False, gather: bool = True) -> Sharded:
-        out = self.ops.gemm(self.rows_of(lhs), self.operand_of(rhs), alpha,
+        gather = gather and not mv
+        r = self.operand_of(rhs)
+        kw = {}
+        out_rows = getattr(self.comm, "output_rows", None)
+        if gather and self.prefetch and self.comm.world > 1 and out_rows is not None:
+            kw["out"] = out_rows(r.shape[1])  # written in place into its exchange slot
+        out = self.ops.gemm(self.rows_of(lhs), r, alpha,
                             self.rows_of(c) if c is not None else None, beta, diag, self.comm.r0,
-                            mv, self.ctr)
-        return self._produced(out, gather and not mv)
+                            mv, self.ctr, **kw)
+        return self._produced(out, gather)
 
     def residual(self, x: Sharded, a: Sharded, gather: bool = True) -> Sharded:
         return self.mm(x, a, alpha=-1.0, diag=1.0, gather=gather)

@@ -145,6 +145,10 @@ def test_virtual_ranks_composite_step_bitwise(world, n):
     for eng in engs:
         assert eng.ctr.mmm == 2 * 22
         assert eng.comm.bytes_gathered > 0
+        # products are written straight into their exchange slots; copied in are
+        # only the first step's input G and, per step, the one part whose plan
+        # ends in a Lin (not a product)
+        assert eng.comm.local_copies <= 1 + 2
 
 
 def test_virtual_ranks_recursive_step_bitwise():
