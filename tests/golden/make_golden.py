@@ -302,6 +302,19 @@ def harness_runs():
            "methods": [[m.kind, m.order, m.h, m.q, list(m.rates), m.label] for m in methods],
            "csv": si.records_to_csv(recs),
            "diverged": [bool(r.diverged) for r in recs]}
+    # the acceptance criterion-8 run (tests/test_acceptance.py:244-271) on the
+    # reference's default harmonic fixture: inputs and the reference's records
+    ha, hb, hts = si.gen_harmonic_matrix(si.HarmonicRegressorSpec.default())
+    hm = [si.MethodSpec(kind="richardson", order=3, q=3, h=16),
+          si.MethodSpec(kind="ns-estimator", order=8, h=16)]
+    clock[0] = 0
+    hrecs = si.run_comparison(ha, hb, hts, hm, steps=5, eps=0.01 * si.inf_norm(ha), timer=timer)
+    out["harmonic"] = {"a": np.asarray(ha).tolist(), "b": np.asarray(hb).tolist(),
+                       "theta_star": np.asarray(hts).tolist(),
+                       "eps": 0.01 * si.inf_norm(ha), "steps": 5,
+                       "methods": [[m.kind, m.order, m.h, m.q, list(m.rates), m.label]
+                                   for m in hm],
+                       "csv": si.records_to_csv(hrecs)}
     with open(os.path.join(HERE, "harness.json"), "w") as fh:
         json.dump(out, fh)
 
