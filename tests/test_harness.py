@@ -112,3 +112,93 @@ def test_acceptance_criterion_8_on_device():
     for r, q in zip(recs, ref):  # before convergence, the device errors track the reference's
         if q.error_norm > 1e-6:
             assert abs(r.error_norm - q.error_norm) <= 1e-6 * q.error_norm, (r, q)
+
+
+def test_method_name_labels():
+    from paper_2008_11480_b200.harness import CSV_HEADER, MethodSpec, series_params
+
+    assert MethodSpec(kind="ns", order=8, h=2).name() == "ns:n8:h2"
+    assert MethodSpec(kind="sri", order=3).name() == "sri:p3:h1"
+    assert MethodSpec(kind="richardson", order=3).name() == "richardson:n3:q3:h1"
+    assert MethodSpec(kind="composite", order=2, rates=(2, 3)).name() == "composite:n2:h1:r2-3"
+    assert MethodSpec(kind="ns", order=2, label="mine").name() == "mine"
+    assert CSV_HEADER == "method,k,error_norm,predicted_bound,exponent,mmm_cum,wall_ns"
+    assert series_params(2) == (1, 1)
+    p, w = series_params(45)
+    assert w * (p + 1) == 45
+
+
+def _harmonic():
+    hd = _fixture()["harmonic"]
+    return np.array(hd["a"]), np.array(hd["b"]), np.array(hd["theta_star"])
+
+
+class _Clock:
+    def __init__(self):
+        self.t = 0
+
+    def __call__(self):
+        self.t += 1
+        return self.t
+
+
+@pytest.mark.gpu
+def test_run_comparison_behaviour():
+    """The reference's run-comparison tests (its tests/test_harness.py:121-196)
+    on the device: initialisation rows, per-method step sequences for every
+    kind, two-loop beats classical, errors inside the predicted bound, and the
+    divergence flag with the run continuing."""
+    import paper_2008_11480_b200 as P
+
+    a, b, th = _harmonic()
+    M = P.MethodSpec
+    recs = P.run_comparison(a, b, th, [M(kind="ns", order=2), M(kind="double", order=2)], 0)
+    assert [r.k for r in recs] == [0, 0]
+    kinds = [M(kind="ns", order=3), M(kind="double", order=2),
+             M(kind="composite", order=2, rates=(2,)), M(kind="sri", order=2),
+             M(kind="ns-estimator", order=2), M(kind="richardson", order=2),
+             M(kind="richardson-recursive", order=2)]
+    by = {}
+    for r in P.run_comparison(a, b, th, kinds, 3):
+        by.setdefault(r.method, []).append(r.k)
+    assert len(by) == len(kinds) and all(ks == list(range(4)) for ks in by.values())
+    recs = P.run_comparison(a, b, th, [M(kind="double", order=2), M(kind="ns", order=2)], 3)
+    dbl = {r.k: r.error_norm for r in recs if r.method.startswith("double")}
+    cls = {r.k: r.error_norm for r in recs if r.method.startswith("ns:")}
+    assert all(dbl[k] <= cls[k] for k in range(1, 4))
+    recs = P.run_comparison(a, b, th, [M(kind="ns", order=2), M(kind="double", order=2),
+                                       M(kind="richardson", order=2)], 4)
+    err0 = {r.method: r.error_norm for r in recs if r.k == 0}
+    for r in recs:
+        if r.predicted_bound >= 1e-11 * err0[r.method]:
+            assert r.error_norm <= r.predicted_bound * (1.0 + 1e-6) + 1e-250
+    start = P.initial_richardson(P.split_scalar(a), P.as_device(b), order=2, q=2)
+    decoy = start.theta.cpu().numpy() + 1e-9
+    recs = P.run_comparison(a, b, decoy, [M(kind="richardson", order=2)], 3)
+    assert len(recs) == 4 and not recs[0].diverged and recs[-1].diverged
+
+
+@pytest.mark.gpu
+def test_csv_behaviour():
+    """CSV round trip, byte-identical repeated runs, and concurrent = serial
+    (the reference's tests/test_harness.py:198-241) on the device."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import paper_2008_11480_b200 as P
+
+    a, b, th = _harmonic()
+    M = P.MethodSpec
+    recs = P.run_comparison(a, b, th, [M(kind="ns", order=2), M(kind="richardson", order=2)], 3,
+                            timer=_Clock())
+    text = P.records_to_csv(recs)
+    assert text.splitlines()[0] == P.CSV_HEADER and P.parse_run_records(text) == recs
+    ms = [M(kind="double", order=2), M(kind="richardson", order=3)]
+    one = P.records_to_csv(P.run_comparison(a, b, th, ms, 3, timer=_Clock()))
+    two = P.records_to_csv(P.run_comparison(a, b, th, ms, 3, timer=_Clock()))
+    assert one.encode() == two.encode()
+    ms = [M(kind="ns", order=3), M(kind="double", order=2), M(kind="richardson", order=2)]
+    serial = P.records_to_csv(P.run_comparison(a, b, th, ms, 3, timer=lambda: 0))
+    with ThreadPoolExecutor(max_workers=3) as pool:
+        threaded = P.records_to_csv(P.run_comparison(a, b, th, ms, 3, timer=lambda: 0,
+                                                     executor=pool))
+    assert serial == threaded
