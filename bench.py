@@ -572,11 +572,11 @@ class Workload:
         host["out"] = {k: torch.empty_like(host["in"][k], pin_memory=True) for k in ("p", "f", "t")}
         return host
 
-    def e2e_step_resident(self, host, chunks: int = 4):
-        """One resident run through the public API from host buffers.  c2: the
-        batch goes in `chunks` slices -- slice i+1 is copied host->device (copy
-        stream) while slice i computes, and slice i's P, F, theta go back while
-        slice i+1 computes.  c1: one system, copies in series."""
+    def e2e_step_resident(self, host):
+        """One resident run through the public API from host buffers.  c2: one
+        launch fed by chunks of systems (``input_chunks`` flags behind each
+        chunk's copy) whose outputs go back chunk by chunk (``chunk_done``
+        counters); c1: one system, one packed copy each way."""
         import torch
 
         P = self.P
@@ -600,27 +600,54 @@ class Workload:
             main.wait_stream(down)
             return host["pack_in"].numel() * 8, host["pack_out"].numel() * 8
         else:
+            # the batch arrives by chunks of one launch round (grid = 4 CTAs x
+            # 148 SMs): the kernel waits per chunk for its flag, counts finished
+            # systems per chunk, and each chunk's outputs go back as soon as
+            # its counter is full
+            from paper_2008_11480_b200 import _lib
+
             batch = hin["a"].shape[0]
-            cuts = [batch * i // chunks for i in range(chunks + 1)]
-            for i in range(chunks):
-                lo, hi = cuts[i], cuts[i + 1]
-                with torch.cuda.stream(up):
-                    d = {k: v[lo:hi].to("cuda", non_blocking=True) for k, v in hin.items()}
-                    for v in d.values():
-                        v.record_stream(main)
-                    ready = torch.cuda.Event()
-                    ready.record(up)
-                main.wait_event(ready)
-                p, f, t = P.batched_composite_richardson(d["a"], d["b"], d["pre"], d["res"],
-                                                         d["p"], d["f"], d["t"], (2, 3), 2,
-                                                         self.iters_per_step)
-                done = torch.cuda.Event()
-                done.record(main)
-                down.wait_event(done)
-                with torch.cuda.stream(down):
+            chunk = 4 * torch.cuda.get_device_properties(0).multi_processor_count
+            nchunks = (batch + chunk - 1) // chunk
+            if not hasattr(self, "_c2_flags") or self._c2_flags.numel() < nchunks:
+                self._c2_flags = torch.zeros(nchunks, dtype=torch.int32, device="cuda")
+                self._c2_done = torch.zeros(nchunks, dtype=torch.int32, device="cuda")
+                self._c2_target = [0] * nchunks
+                self._c2_epoch = 0
+            self._c2_epoch += 1
+            epoch = self._c2_epoch
+            h = _lib.handle(0)
+            d = {}
+            with torch.cuda.stream(up):
+                for k, v in hin.items():
+                    d[k] = torch.empty(v.shape, dtype=v.dtype, device="cuda")
+                    d[k].record_stream(main)
+                for c in range(nchunks):
+                    lo, hi = c * chunk, min(batch, (c + 1) * chunk)
+                    for k, v in hin.items():
+                        d[k][lo:hi].copy_(v[lo:hi], non_blocking=True)
+                    _lib.call("si_stream_write_u32", h, self._c2_flags.data_ptr() + 4 * c, epoch,
+                              up.cuda_stream)
+            # the read-back must not wait for the whole launch: only for main's work
+            # before it (the output blocks are handed out from memory freed by
+            # that work); each chunk then waits on its own counter
+            before = torch.cuda.Event()
+            before.record(main)
+            p, f, t = P.batched_composite_richardson(
+                d["a"], d["b"], d["pre"], d["res"], d["p"], d["f"], d["t"], (2, 3), 2,
+                self.iters_per_step, input_chunks=(self._c2_flags, epoch, chunk),
+                chunk_done=self._c2_done)
+            down.wait_event(before)
+            with torch.cuda.stream(down):
+                for c in range(nchunks):
+                    lo, hi = c * chunk, min(batch, (c + 1) * chunk)
+                    self._c2_target[c] += hi - lo
+                    _lib.call("si_stream_wait_u32", h, self._c2_done.data_ptr() + 4 * c,
+                              self._c2_target[c], down.cuda_stream)
                     for k, v in (("p", p), ("f", f), ("t", t)):
-                        hout[k][lo:hi].copy_(v, non_blocking=True)
-                        v.record_stream(down)
+                        hout[k][lo:hi].copy_(v[lo:hi], non_blocking=True)
+                for v in (p, f, t):
+                    v.record_stream(down)
             main.wait_stream(down)
         h2d = sum(v.numel() * 8 for v in hin.values())
         d2h = sum(v.numel() * 8 for v in hout.values())

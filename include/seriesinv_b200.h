@@ -335,6 +335,20 @@ SI_API int si_batched_composite_richardson_ex(
     const int64_t* plan_offsets, const double* consts, int64_t nconsts, int order_n, int iters,
     const double* p_in, const double* f_in, const double* theta_in, double* p_out, double* f_out,
     double* theta_out, int64_t* counters, void* stream);
+/* si_batched_composite_richardson_ex for inputs that arrive by chunks of
+ * `chunk` systems (host->device copies in flight): system i's inputs are read
+ * once chunk_ready[i / chunk] >= epoch (wrap-safe); chunk_done (may be NULL)
+ * gets +1 per finished system of each chunk, after its outputs are written, so
+ * a copy stream can wait (si_stream_wait_u32) and read a chunk back early.
+ * Flags must be raised by work that needs no SM (copy engines, stream memory
+ * operations). */
+SI_API int si_batched_composite_richardson_gated(
+    si_handle h, int64_t batch, int64_t n, const double* a, const double* b, const double* precond,
+    const double* residual, int nrates, const int32_t* rates, const int32_t* plans,
+    const int64_t* plan_offsets, const double* consts, int64_t nconsts, int order_n, int iters,
+    const double* p_in, const double* f_in, const double* theta_in, double* p_out, double* f_out,
+    double* theta_out, const uint32_t* chunk_ready, uint32_t epoch, int64_t chunk,
+    uint32_t* chunk_done, int64_t* counters, void* stream);
 
 /* BASELINE config 1 shape (batch = 1, n <= 64) and batches of it: `iters` x
  * { plain Richardson with P_k; ns_step(order, plan) } with the state resident

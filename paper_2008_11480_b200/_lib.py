@@ -88,6 +88,10 @@ SIGNATURES: dict[str, list] = {
         _P, _I64, _I64, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _P, _P, _P,
         _PI64, _P,
     ],
+    "si_batched_composite_richardson_gated": [
+        _P, _I64, _I64, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _P, _P, _P,
+        _P, ctypes.c_uint32, _I64, _P, _PI64, _P,
+    ],
 }
 
 _lib = None

@@ -34,8 +34,16 @@ def batched_scalar_split(a: torch.Tensor, eps_factor: float = 0.5):
 
 
 def batched_composite_richardson(a, b, precond, residual, p, f, theta, rates, order_n: int,
-                                 iters: int, ctr: MulCounter | None = None):
-    """Returns new (P, F, theta) after ``iters`` fused iterations; inputs untouched."""
+                                 iters: int, ctr: MulCounter | None = None, *,
+                                 input_chunks: tuple | None = None, chunk_done=None):
+    """Returns new (P, F, theta) after ``iters`` fused iterations; inputs untouched.
+
+    ``input_chunks = (flags, epoch, chunk)``: the inputs are still arriving by
+    chunks of ``chunk`` systems; system i is read once ``flags[i // chunk] >=
+    epoch`` (a CUDA int32 tensor raised behind each chunk's copy by SM-free
+    work: copy engines / stream memory operations).  ``chunk_done`` (CUDA int32
+    tensor) gets +1 per finished system of each chunk after its outputs are
+    written (a copy stream can wait on it and read the chunk back early)."""
     a, b = as_device(a), as_device(b)
     precond, residual = as_device(precond), as_device(residual)
     batch, n, n2 = a.shape
@@ -57,12 +65,23 @@ def batched_composite_richardson(a, b, precond, residual, p, f, theta, rates, or
     plans = [geometric_base_plan(x) if x > 1 else None for x in rates]
     code, offsets, consts = encode_many(plans)
     buf = _lib.counter_buf()
-    _lib.call("si_batched_composite_richardson_ex", _lib.handle(a.device.index), batch, n,
+    flags_ptr, epoch, chunk = None, 0, 1
+    if input_chunks is not None:
+        flags, epoch, chunk = input_chunks
+        if flags.dtype != torch.int32 or not flags.is_cuda or chunk < 1 or \
+                flags.numel() < (batch + chunk - 1) // chunk:
+            raise ValueError("input_chunks: a CUDA int32 flag per chunk and chunk >= 1")
+        flags_ptr = flags.data_ptr()
+    if chunk_done is not None and (chunk_done.dtype != torch.int32 or not chunk_done.is_cuda):
+        raise ValueError("chunk_done must be a CUDA int32 tensor")
+    _lib.call("si_batched_composite_richardson_gated", _lib.handle(a.device.index), batch, n,
               a.data_ptr(), b.data_ptr(), precond.data_ptr(), residual.data_ptr(), len(rates),
               _lib.i32_array(list(rates)), _lib.i32_array(code), _lib.i64_array(offsets),
               _lib.f64_array(consts), len(consts), order_n, iters, p_in.data_ptr(),
               f_in.data_ptr(), th_in.data_ptr(), p_io.data_ptr(), f_io.data_ptr(),
-              th_io.data_ptr(), buf, _lib.stream_ptr(a.device))
+              th_io.data_ptr(), flags_ptr, epoch, chunk,
+              chunk_done.data_ptr() if chunk_done is not None else None, buf,
+              _lib.stream_ptr(a.device))
     if ctr is not None:
         ctr.absorb(buf)
     return p_io, f_io, th_io

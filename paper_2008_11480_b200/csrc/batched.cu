@@ -463,6 +463,13 @@ struct BatchArgs {
   long long* prof;         // per-op cycle totals of CTA 0 (diagnostics; usually null)
   int sA, sG, sF, sT, sb;  // slots of A, the carried inputs, b
   int sP, sB;              // resident splitting S^-1, B (-1: streamed by OP_LOAD)
+  // inputs arriving by chunks of systems (host->device copies in flight): the
+  // CTA waits for chunk_ready[sys / chunk] >= epoch before loading system sys
+  // and counts finished systems in chunk_done[sys / chunk] (may be null)
+  const unsigned* chunk_ready;
+  unsigned* chunk_done;
+  unsigned epoch;
+  int64_t chunk;
   int rG, rF, rT;          // slots of the carried outputs (copied back when different)
 };
 
@@ -537,6 +544,17 @@ __device__ void store_mat(double* __restrict__ dst, const double* src, int n) {
   } else {
     for (int i = threadIdx.x; i < n * n; i += G::THREADS) dst[i] = src[G::idx(i / n, i % n)];
   }
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32_b(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t resident_timer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 // Sign flip on the integer pipe: the FP64 pipe is shared with DMMA.
@@ -647,6 +665,17 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
   constexpr int PFD = NP * NP / 2 / G::THREADS > 0 ? NP * NP / 2 / G::THREADS : 1;
   double2 pf_p[PFD], pf_b[PFD];
   for (int64_t sys = blockIdx.x; sys < p.batch; sys += gridDim.x) {
+    if (p.chunk_ready) {  // this system's inputs may still be copying
+      if (threadIdx.x == 0) {
+        const unsigned* f = p.chunk_ready + sys / p.chunk;
+        const uint64_t t0 = resident_timer_ns();
+        while ((int)(ld_acquire_u32_b(f) - p.epoch) < 0) {
+          __nanosleep(128);
+          if (resident_timer_ns() - t0 > 60ull * 1000000000ull) __trap();
+        }
+      }
+      __syncthreads();
+    }
     load_mat<NP>(mslot(p.sA), p.a + sys * nn, n);
     if (p.sP >= 0) load_mat<NP>(mslot(p.sP), p.precond + sys * nn, n);
     if (p.sB >= 0) load_mat<NP>(mslot(p.sB), p.residual + sys * nn, n);
@@ -672,7 +701,7 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
         pf_b[j] = __ldg(sb2 + threadIdx.x + j * G::THREADS);
       }
     };
-    if (prefetch && sys == blockIdx.x) issue(sys);
+    if (prefetch && (sys == blockIdx.x || p.chunk_ready)) issue(sys);
     for (int it = 0; it < p.iters; ++it) {
       for (int k = 0; k < p.nops; ++k) {
         const DOp o = prog[k];
@@ -688,7 +717,7 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
           if (k == p.last_load) {
             if (it + 1 < p.iters)
               issue(sys);
-            else if (sys + gridDim.x < p.batch)
+            else if (sys + gridDim.x < p.batch && !p.chunk_ready)  // gated: at system start
               issue(sys + gridDim.x);
           }
         } else if (o.kind == OP_GEMM) {
@@ -790,6 +819,10 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
     store_mat<NP>(p.f_io + sys * nn, mslot(p.sF), n);
     if (threadIdx.x < n) p.theta_io[sys * n + threadIdx.x] = vslot(p.sT)[threadIdx.x];
     __syncthreads();
+    if (p.chunk_done && threadIdx.x == 0) {  // outputs of sys visible, then counted
+      __threadfence_system();
+      atomicAdd(p.chunk_done + sys / p.chunk, 1u);
+    }
   }
   if (p.prof && blockIdx.x == 0 && threadIdx.x == 0)
     for (int k = 0; k < p.nops; ++k) p.prof[k] = prof_acc[k];
@@ -1171,7 +1204,7 @@ template <int NP>
 Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, const double* b,
                 const double* precond, const double* residual, int iters, const double* p_in,
                 const double* f_in, const double* theta_in, double* p_io, double* f_io,
-                double* theta_io) {
+                double* theta_io, const ChunkGate* gate = nullptr) {
   using Gm = Geo<NP>;
   Counters per;
   for (const BOp& o : q.r.ops) {
@@ -1254,6 +1287,7 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
     } else if (batch * 4 <= num_sms_b()) {
       cl = 4;
     }
+    if (gate && gate->ready) cl = 0;  // the chunk gate lives in the one-CTA kernel
   }
   std::vector<uint8_t> cflags;
   if (cl) {
@@ -1358,6 +1392,12 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
       args.has_load = 1;
       args.last_load = (int)k;
     }
+  if (gate && gate->ready) {
+    args.chunk_ready = gate->ready;
+    args.chunk_done = gate->done;
+    args.epoch = gate->epoch;
+    args.chunk = gate->chunk;
+  }
   args.sA = al.phys[q.A];
   args.sP = q.P >= 0 ? al.phys[q.P] : -1;
   args.sB = q.B >= 0 ? al.phys[q.B] : -1;
@@ -1454,7 +1494,7 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
                                       const std::vector<const PlanNode*>& plans, int order_n,
                                       int iters, const double* p_in, const double* f_in,
                                       const double* theta_in, double* p_io, double* f_io,
-                                      double* theta_io) {
+                                      double* theta_io, const ChunkGate* gate) {
   Recipe q = new_recipe();
   record_plain(q);
   // composite_step (newton_schulz.py:177-228).  The NS part S_n(F) G is
@@ -1489,9 +1529,9 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
   q.fn = q.r.residual(q.gn, q.A);
   if (n <= 32)
     return launch<32>(c, q, batch, n, a, b, precond, residual, iters, p_in, f_in, theta_in, p_io,
-                      f_io, theta_io);
+                      f_io, theta_io, gate);
   return launch<64>(c, q, batch, n, a, b, precond, residual, iters, p_in, f_in, theta_in, p_io,
-                    f_io, theta_io);
+                    f_io, theta_io, gate);
 }
 
 Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a, const double* b,

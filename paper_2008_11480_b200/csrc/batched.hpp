@@ -6,6 +6,16 @@
 namespace si {
 
 constexpr int kBatchMaxN = 64;
+
+// Inputs arriving by chunks of `chunk` systems: chunk k's inputs are valid once
+// ready[k] >= epoch (wrap-safe); done[k] (may be null) is incremented once per
+// finished system of chunk k, after its outputs are written.
+struct ChunkGate {
+  const unsigned* ready = nullptr;
+  unsigned* done = nullptr;
+  unsigned epoch = 0;
+  int64_t chunk = 1;
+};
 constexpr int kBatchMaxRates = 4;
 
 // BASELINE config 2: `iters` x { plain Richardson with P_k;
@@ -18,7 +28,7 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
                                       const std::vector<const PlanNode*>& plans, int order_n,
                                       int iters, const double* p_in, const double* f_in,
                                       const double* theta_in, double* p_out, double* f_out,
-                                      double* theta_out);
+                                      double* theta_out, const ChunkGate* gate = nullptr);
 
 // BASELINE config 1 (batch = 1) and batches of it: `iters` x { plain
 // Richardson with P_k; ns_step(order, plan) (newton_schulz.py:150-174) }.

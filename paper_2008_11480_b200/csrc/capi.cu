@@ -809,7 +809,21 @@ int si_batched_composite_richardson_ex(si_handle h, int64_t batch, int64_t n, co
                                        int iters, const double* p_in, const double* f_in,
                                        const double* theta_in, double* p_out, double* f_out,
                                        double* theta_out, int64_t* counters, void* stream) {
+  return si_batched_composite_richardson_gated(
+      h, batch, n, a, b, precond, residual, nrates, rates, plans, plan_offsets, consts, nconsts,
+      order_n, iters, p_in, f_in, theta_in, p_out, f_out, theta_out, nullptr, 0, 1, nullptr,
+      counters, stream);
+}
+
+int si_batched_composite_richardson_gated(
+    si_handle h, int64_t batch, int64_t n, const double* a, const double* b, const double* precond,
+    const double* residual, int nrates, const int32_t* rates, const int32_t* plans,
+    const int64_t* plan_offsets, const double* consts, int64_t nconsts, int order_n, int iters,
+    const double* p_in, const double* f_in, const double* theta_in, double* p_out, double* f_out,
+    double* theta_out, const uint32_t* chunk_ready, uint32_t epoch, int64_t chunk,
+    uint32_t* chunk_done, int64_t* counters, void* stream) {
   return guard([&] {
+    need(!chunk_ready || chunk >= 1, "chunk must be >= 1");
     need(h && a && b && precond && residual && rates && p_in && f_in && theta_in && p_out &&
              f_out && theta_out,
          "null pointer");
@@ -828,9 +842,14 @@ int si_batched_composite_richardson_ex(si_handle h, int64_t batch, int64_t n, co
       }
     }
     Call call(h, stream, nullptr);
+    ChunkGate gate;
+    gate.ready = chunk_ready;
+    gate.done = chunk_done;
+    gate.epoch = epoch;
+    gate.chunk = chunk;
     Counters per = batched_composite_richardson(call.c, batch, n, a, b, precond, residual, rv, pv,
                                                 order_n, iters, p_in, f_in, theta_in, p_out,
-                                                f_out, theta_out);
+                                                f_out, theta_out, chunk_ready ? &gate : nullptr);
     if (counters) {
       counters[0] += per.mmm;
       counters[1] += per.mvm;

@@ -374,3 +374,43 @@ def test_hoisted_composite_parts_bitwise():
         assert torch.equal(s1.estimate, s2.estimate) and torch.equal(s1.residual, s2.residual)
     with pytest.raises(ValueError):
         P.composite_step(s2, sp.matrix, sp, P.CompositeSpec((2, 3)), 2, parts=parts)
+
+
+def test_batched_composite_with_inputs_by_chunks():
+    """Config-2 launch fed by chunks of systems (flags behind each chunk's
+    copy, raised late and out of order) and read back per chunk on the done
+    counters: bitwise the resident-input result."""
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import _lib, configs
+
+    batch, chunk = 1500, 400
+    a_np, b_np = configs.c2_batched(batch=batch)
+    a, b = P.as_device(a_np), P.as_device(b_np)
+    pre, res = P.batched_scalar_split(a)
+    t0 = torch.zeros_like(b)
+    ref = P.batched_composite_richardson(a, b, pre, res, pre, res, t0, (2, 3), 2, 5)
+    host = {k: v.cpu().pin_memory() for k, v in
+            (("a", a), ("b", b), ("pre", pre), ("res", res), ("t", t0))}
+    d = {k: torch.empty_like(v, device="cuda") for k, v in host.items()}
+    nch = (batch + chunk - 1) // chunk
+    flags = torch.zeros(nch, dtype=torch.int32, device="cuda")
+    done = torch.zeros(nch, dtype=torch.int32, device="cuda")
+    big = torch.empty(16 << 20, dtype=torch.float64).pin_memory()
+    big2 = torch.empty(big.shape, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    up = torch.cuda.Stream()
+    h = _lib.handle(0)
+    out = P.batched_composite_richardson(d["a"], d["b"], d["pre"], d["res"], d["pre"], d["res"],
+                                         d["t"], (2, 3), 2, 5, input_chunks=(flags, 4, chunk),
+                                         chunk_done=done)
+    with torch.cuda.stream(up):
+        big2.copy_(big, non_blocking=True)  # copy engine delay: the kernel waits meanwhile
+        for c in reversed(range(nch)):
+            lo, hi = c * chunk, min(batch, (c + 1) * chunk)
+            for k in d:
+                d[k][lo:hi].copy_(host[k][lo:hi], non_blocking=True)
+            _lib.call("si_stream_write_u32", h, flags.data_ptr() + 4 * c, 4, up.cuda_stream)
+    torch.cuda.synchronize()
+    for x, y in zip(out, ref):
+        assert torch.equal(x, y)
+    assert done.tolist() == [min(batch, (c + 1) * chunk) - c * chunk for c in range(nch)]
