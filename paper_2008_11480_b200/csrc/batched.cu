@@ -1200,6 +1200,25 @@ void record_plain(Recipe& q) {
   q.tn = q.r.gemv(q.G, res, -1.0, q.T, 1.0);            // theta - P resid
 }
 
+// theta' is only read by the next iteration: move its GEMV behind the first
+// product, so that product overlaps both GEMVs (the residual GEMV runs while
+// the product's other warps start; theta' runs while the next product does)
+// instead of the GEMV pair forming a serial prologue.
+void defer_theta_update(Recipe& q) {
+  auto& ops = q.r.ops;
+  int i1 = -1;
+  for (int i = 0; i < (int)ops.size(); ++i)
+    if (ops[i].dst == q.tn) i1 = i;
+  if (i1 < 0) return;
+  for (int j = i1 + 1; j < (int)ops.size(); ++j)
+    if (ops[j].kind == OP_GEMM) {
+      const BOp mv = ops[i1];
+      ops.erase(ops.begin() + i1);
+      ops.insert(ops.begin() + j, mv);  // now just after that product
+      return;
+    }
+}
+
 template <int NP>
 Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, const double* b,
                 const double* precond, const double* residual, int iters, const double* p_in,
@@ -1527,6 +1546,7 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
   }
   q.gn = q.r.gemm(rc, nsp, 1.0, tc, 1.0);
   q.fn = q.r.residual(q.gn, q.A);
+  defer_theta_update(q);
   if (n <= 32)
     return launch<32>(c, q, batch, n, a, b, precond, residual, iters, p_in, f_in, theta_in, p_io,
                       f_io, theta_io, gate);
@@ -1544,6 +1564,9 @@ Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a
   const int gnew = plan ? q.r.eval(*plan, q.F, q.G, q.A) : q.r.horner(q.F, q.G, order);
   q.gn = gnew == q.G ? q.r.copy(q.G) : gnew;
   q.fn = q.r.residual(q.gn, q.A);
+  // (no defer_theta_update here: in the cluster kernel the deferred GEMV
+  // reads G, whose slot the next product overwrites in place -- a barrier
+  // either way -- and the config-1 iteration measured slower)
   if (n <= 32)
     return launch<32>(c, q, batch, n, a, b, nullptr, nullptr, iters, p_in, f_in, theta_in, p_io,
                       f_io, theta_io);
