@@ -158,6 +158,18 @@ def ncu_traffic(w) -> float | None:
         return None
 
 
+def l2_note(w) -> str:
+    """How the timed region relates to the 126 MB L2 (timing rule: inputs larger
+    than L2, or a flush)."""
+    if w.cfg == "c1":
+        return ("no flush: one launch runs 30 iterations out of shared memory/DSMEM; "
+                "its inputs (a few 64x64 matrices) are read once per launch (latency-bound config)")
+    if w.cfg == "c2":
+        return (f"inputs larger than L2 ({8 * w.batch * w.n * w.n / 1e6:.0f} MB per "
+                f"{w.batch}x{w.n}^2 stack, read once per launch), no flush")
+    return f"inputs larger than L2 ({8 * w.n * w.n / 1e9:.2f} GB per n x n matrix), no flush"
+
+
 def resident_roofline(w, tflops_per_gpu: float, step_s: float, peak: float) -> dict:
     """Configs 1/2: one resident_kernel launch per step (the whole timed region), so
     the kernel's achieved rate is the step's; HBM bytes are algorithmic: per system
@@ -979,7 +991,7 @@ def run_ours(args):
                                        if w.sharded is not None
                                        else f"batch split x{world} (no communication)" if w.split_batch
                                        else (f"replicas x{world}" if world > 1 else "single-gpu")),
-                       "l2": "inputs larger than L2 (2.1 GB per matrix), no flush"},
+                       "l2": l2_note(w)},
             "tflops": tflops,
             "tflops_frac_of_dmma_peak": tflops / (world * peak.value),
             "roofline": resident_roofline(w, tflops / world, step_s, peak.value) if w.cfg in ("c1", "c2") else
