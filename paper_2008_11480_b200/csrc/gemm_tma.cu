@@ -161,6 +161,7 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int&
   tn = r / gsize;
 }
 
+template <int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, double* __restrict__ D,
@@ -221,6 +222,18 @@ __global__ void __launch_bounds__(THREADS, 1)
             stage = 0;
             phase ^= 1u;
           }
+        }
+        if (EPI == 1 && C != nullptr && beta != 0.0) {
+          // the consumers reach this tile's epilogue ~STAGES k-blocks from now:
+          // pull its C rows into L2 so the epilogue loads do not wait on HBM
+          const int m0 = tm * BM, rows = min(BM, M - m0);
+          const uint32_t bytes_row = (uint32_t)(min(BN, N - n0) * 8) & ~15u;
+          if (bytes_row)
+            for (int r = 0; r < rows; ++r)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                               C + (int64_t)(m0 + r) * ldc + n0),
+                           "r"(bytes_row)
+                           : "memory");
         }
       }
     }
@@ -306,6 +319,56 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------- fused epilogue ----------------
     const int row0 = tm * BM + wm * 64 + g;
     const int col0 = tn * BN + wn * 32 + 2 * t;
+    if (EPI == 1 && beta != 0.0) {
+      // C loads issued a pair of fragment rows ahead of the stores that use them
+      // (each thread reads its own elements before writing them, so D == C is fine)
+      auto load_c = [&](double2 (&cv)[2][4], int mi0) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = row0 + (mi0 + h) * 8;
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) {
+            const int col = col0 + ni * 8;
+            cv[h][ni] = make_double2(0.0, 0.0);
+            if (row < M && col < N) {
+              const double* pc = C + (int64_t)row * ldc + col;
+              if (col + 1 < N) cv[h][ni] = *reinterpret_cast<const double2*>(pc);
+              else cv[h][ni].x = *pc;
+            }
+          }
+        }
+      };
+      double2 cbuf[2][2][4];
+      load_c(cbuf[0], 0);
+#pragma unroll
+      for (int mp = 0; mp < 4; ++mp) {
+        if (mp + 1 < 4) load_c(cbuf[(mp + 1) & 1], 2 * (mp + 1));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int mi = 2 * mp + h;
+          const int row = row0 + mi * 8;
+          if (row >= M) continue;
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) {
+            const int col = col0 + ni * 8;
+            if (col >= N) continue;
+            const double2 cv = cbuf[mp & 1][h][ni];
+            double v0 = apply_epi(acc[mi][ni][0], alpha, beta, cv.x);
+            double v1 = apply_epi(acc[mi][ni][1], alpha, beta, cv.y);
+            if (diag != 0.0) {
+              if (row + doff == col) v0 = __dadd_rn(v0, diag);
+              if (row + doff == col + 1) v1 = __dadd_rn(v1, diag);
+            }
+            if (col + 1 < N) {
+              *reinterpret_cast<double2*>(D + (int64_t)row * ldd + col) = make_double2(v0, v1);
+            } else {
+              D[(int64_t)row * ldd + col] = v0;
+            }
+          }
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int mi = 0; mi < 8; ++mi) {
       const int row = row0 + mi * 8;
@@ -399,14 +462,18 @@ cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& 
   cudaGetDevice(&dev);
   static std::atomic<uint64_t> attr_set{0};  // one bit per device
   if (dev < 64 && !(attr_set.load() & (1ull << dev))) {
-    cudaError_t err = cudaFuncSetAttribute(gemm_f64_tma_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (err != cudaSuccess) return err;
+    for (auto fn : {gemm_f64_tma_kernel<0>, gemm_f64_tma_kernel<1>}) {
+      cudaError_t err =
+          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+      if (err != cudaSuccess) return err;
+    }
     attr_set.fetch_or(1ull << dev);
   } else if (dev >= 64) {
-    cudaError_t err = cudaFuncSetAttribute(gemm_f64_tma_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (err != cudaSuccess) return err;
+    for (auto fn : {gemm_f64_tma_kernel<0>, gemm_f64_tma_kernel<1>}) {
+      cudaError_t err =
+          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+      if (err != cudaSuccess) return err;
+    }
   }
   const int M = (int)D.rows, N = (int)D.cols, K = (int)A.cols;
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
@@ -420,7 +487,12 @@ cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& 
   PanelWait gate, gate_a;
   if (pw && pw->ready && pw->npanels > 0) gate = *pw;
   if (pwa && pwa->ready && pwa->npanels > 0) gate_a = *pwa;
-  gemm_f64_tma_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, D.p, D.ld, e.c, e.ldc, M, N, K,
+  static const int epi = [] {
+    const char* v = std::getenv("SI_GEMM_EPI");
+    return v ? std::atoi(v) : 1;
+  }();
+  auto kern = epi == 1 ? gemm_f64_tma_kernel<1> : gemm_f64_tma_kernel<0>;
+  kern<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, D.p, D.ld, e.c, e.ldc, M, N, K,
                                                         e.alpha, e.beta, e.diag, e.doff, gate,
                                                         gate_a);
   return cudaGetLastError();
