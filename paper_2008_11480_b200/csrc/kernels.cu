@@ -93,8 +93,21 @@ __global__ void __launch_bounds__(128) gemm_generic_kernel(
   }
 }
 
+// 16-byte read-only load that does not allocate in L1 (the matrix row is
+// streamed once; X stays cached)
+__device__ __forceinline__ double2 ldg_stream2(const double2* p) {
+  double2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+
 // D[i, j] = alpha * sum_k A[i,k] X[k,j] + beta*C[i,j] + diag*[i==j], j < NR <= 4.
-template <int NR>
+// One warp per row.  VEC: the row is read as 16-byte pairs, eight per lane in
+// flight (A 16-byte aligned, lda and K even) -- the row stream is the whole
+// cost, so memory-level parallelism is what sets the bandwidth.
+template <int NR, bool VEC>
 __global__ void __launch_bounds__(256) gemv_kernel(const double* __restrict__ A, int64_t lda,
                                                    const double* __restrict__ X, int64_t ldx,
                                                    double* __restrict__ D, int64_t ldd,
@@ -108,10 +121,32 @@ __global__ void __launch_bounds__(256) gemv_kernel(const double* __restrict__ A,
 #pragma unroll
   for (int j = 0; j < NR; ++j) s[j] = 0.0;
   const double* a = A + row * lda;
-  for (int64_t k = lane; k < K; k += 32) {
-    const double av = __ldg(a + k);
+  if (VEC) {
+    const double2* a2 = reinterpret_cast<const double2*>(a);
+    const int64_t K2 = K >> 1;
+    auto step = [&](double2 av, int64_t k2) {
+      const int64_t k = 2 * k2;
 #pragma unroll
-    for (int j = 0; j < NR; ++j) s[j] = fma(av, __ldg(X + k * ldx + j), s[j]);
+      for (int j = 0; j < NR; ++j) {
+        s[j] = fma(av.x, __ldg(X + k * ldx + j), s[j]);
+        s[j] = fma(av.y, __ldg(X + (k + 1) * ldx + j), s[j]);
+      }
+    };
+    int64_t k2 = lane;
+    for (; k2 + 32 * 7 < K2; k2 += 256) {
+      double2 av[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) av[u] = ldg_stream2(a2 + k2 + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) step(av[u], k2 + 32 * u);
+    }
+    for (; k2 < K2; k2 += 32) step(ldg_stream2(a2 + k2), k2);
+  } else {
+    for (int64_t k = lane; k < K; k += 32) {
+      const double av = __ldg(a + k);
+#pragma unroll
+      for (int j = 0; j < NR; ++j) s[j] = fma(av, __ldg(X + k * ldx + j), s[j]);
+    }
   }
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
@@ -315,23 +350,18 @@ cudaError_t launch_gemm_generic(const Mat& A, const Mat& B, Mat& D, const Epilog
 
 cudaError_t launch_gemv(const Mat& A, const Mat& X, Mat& D, const Epilogue& e, cudaStream_t s) {
   const unsigned grid = (unsigned)((D.rows + 7) / 8);
+  // pairs only pay for long rows; short rows keep the one-element-per-lane order
+  const bool vec = A.cols >= 256 && ((reinterpret_cast<uintptr_t>(A.p) & 15u) == 0) &&
+                   !(A.ld & 1) && !(A.cols & 1);
+  auto go = [&](auto kern) {
+    kern<<<grid, 256, 0, s>>>(A.p, A.ld, X.p, X.ld, D.p, D.ld, e.c, e.ldc, D.rows, A.cols, e.alpha,
+                              e.beta, e.diag, e.doff);
+  };
   switch (D.cols) {
-    case 1:
-      gemv_kernel<1><<<grid, 256, 0, s>>>(A.p, A.ld, X.p, X.ld, D.p, D.ld, e.c, e.ldc, D.rows,
-                                          A.cols, e.alpha, e.beta, e.diag, e.doff);
-      break;
-    case 2:
-      gemv_kernel<2><<<grid, 256, 0, s>>>(A.p, A.ld, X.p, X.ld, D.p, D.ld, e.c, e.ldc, D.rows,
-                                          A.cols, e.alpha, e.beta, e.diag, e.doff);
-      break;
-    case 3:
-      gemv_kernel<3><<<grid, 256, 0, s>>>(A.p, A.ld, X.p, X.ld, D.p, D.ld, e.c, e.ldc, D.rows,
-                                          A.cols, e.alpha, e.beta, e.diag, e.doff);
-      break;
-    default:
-      gemv_kernel<4><<<grid, 256, 0, s>>>(A.p, A.ld, X.p, X.ld, D.p, D.ld, e.c, e.ldc, D.rows,
-                                          A.cols, e.alpha, e.beta, e.diag, e.doff);
-      break;
+    case 1: vec ? go(gemv_kernel<1, true>) : go(gemv_kernel<1, false>); break;
+    case 2: vec ? go(gemv_kernel<2, true>) : go(gemv_kernel<2, false>); break;
+    case 3: vec ? go(gemv_kernel<3, true>) : go(gemv_kernel<3, false>); break;
+    default: vec ? go(gemv_kernel<4, true>) : go(gemv_kernel<4, false>); break;
   }
   return cudaGetLastError();
 }
