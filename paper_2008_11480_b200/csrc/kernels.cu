@@ -270,11 +270,36 @@ __global__ void __launch_bounds__(RED_THREADS) sumsq_partial(const double* __res
                                                             int64_t ldx, int64_t M, int64_t N,
                                                             double* __restrict__ part) {
   double s = 0.0;
-  const int64_t total = M * N;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = X[(i / N) * ldx + (i % N)];
-    s = fma(v, v, s);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ldx == N && !(reinterpret_cast<uintptr_t>(X) & 15u)) {
+    // contiguous: 16-byte streaming loads, four per thread in flight
+    const double2* x2 = reinterpret_cast<const double2*>(X);
+    const int64_t n2 = (M * N) >> 1;
+    int64_t i = tid;
+    for (; i + 3 * stride < n2; i += 4 * stride) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = ldg_stream2(x2 + i + u * stride);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s = fma(v[u].x, v[u].x, s);
+        s = fma(v[u].y, v[u].y, s);
+      }
+    }
+    for (; i < n2; i += stride) {
+      const double2 v = ldg_stream2(x2 + i);
+      s = fma(v.x, v.x, s);
+      s = fma(v.y, v.y, s);
+    }
+    if (tid == 0 && ((M * N) & 1)) s = fma(X[M * N - 1], X[M * N - 1], s);
+  } else {
+    // strided rows: one block per row at a time
+    for (int64_t r = blockIdx.x; r < M; r += gridDim.x)
+      for (int64_t c = threadIdx.x; c < N; c += blockDim.x) {
+        const double v = X[r * ldx + c];
+        s = fma(v, v, s);
+      }
   }
   s = block_sum(s);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
