@@ -240,8 +240,9 @@ class Workload:
     """One config: device state + one step function + algorithmic FLOPs per step."""
 
     def __init__(self, cfg: str, n: int | None, world: int = 1, hoist: bool = False,
-                 comm: str = "peer"):
+                 comm: str = "peer", shard: str = "rows"):
         self.cfg = cfg
+        self.shard = shard
         self.n = n
         self.world = world
         self.hoist = hoist
@@ -334,6 +335,28 @@ class Workload:
         self.b = b
         self.sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False, verify=False)
         self.sharded = None
+        if self.world > 1 and cfg == "c4" and self.shard == "parts":
+            # composite parts on GPU groups + one ordered (t, r) tree reduction
+            # (grouped.py); the state lives on the root group, row-sharded inside it
+            from paper_2008_11480_b200.grouped import GroupedComposite
+
+            gc = GroupedComposite(self.n, (2, 3, 4, 5), 2)
+            eng, comm = gc.eng, gc.comm
+            st = P.initial_series(self.sp, 0, 1, order=2)
+            self.sharded = {
+                "gc": gc, "eng": eng, "comm": comm,
+                "A": eng.replicated(self.sp.matrix), "P": eng.replicated(self.sp.precond),
+                "B": eng.replicated(self.sp.residual), "b": eng.replicated(b),
+                "g": eng.local(st.estimate[comm.r0:comm.r1].clone()) if gc.is_root else None,
+                "f": eng.local(st.residual[comm.r0:comm.r1].clone()) if gc.is_root else None,
+                "theta": eng.replicated(torch.zeros_like(b)),
+            }
+            del st
+            torch.cuda.empty_cache()
+            self.spec = P.CompositeSpec((2, 3, 4, 5))
+            self.workload += (f" [parts on {len(gc.groups)} GPU groups "
+                              f"{[len(g) for g in gc.groups]}, segments {gc.segments}]")
+            return
         if self.world > 1 and cfg in ("c4", "c3"):
             # block-row sharding over the ranks (sharded.py): A, S^-1, B replicated,
             # G / F row blocks, one row-panel exchange per product with a sharded
@@ -424,6 +447,12 @@ class Workload:
                 return
             self.st = P.richardson_recursive_step(self.st, self.sp.matrix, self.b,
                                                   factor_plan=self.plan16, doubling_sum=True)
+            return
+        if self.sharded is not None and "gc" in self.sharded:
+            s = self.sharded
+            gc = s["gc"]
+            s["theta"] = gc.plain_richardson(s["theta"], s["g"], s["A"], s["b"])
+            s["g"], s["f"] = gc.step(s["g"], s["f"], s["A"], s["P"], s["B"])
             return
         if self.sharded is not None:
             s = self.sharded
@@ -678,11 +707,14 @@ class Workload:
             h.copy_(t)
             return h
 
-        host = {"in": {"a": pin(s["A"].t), "precond": pin(s["P"].t), "residual": pin(s["B"].t),
-                       "b": pin(s["b"].t), "theta": pin(s["theta"].t),
-                       "g": pin(eng.rows_of(s["g"])), "f": pin(eng.rows_of(s["f"]))}}
-        host["out"] = {k: torch.empty_like(host["in"][k], pin_memory=True)
-                       for k in ("g", "f", "theta")}
+        host = {"in": {"a": pin(s["A"].t), "precond": pin(s["P"].t), "residual": pin(s["B"].t)}}
+        if s["g"] is not None:  # grouped mode: the state lives on the root group only
+            host["in"].update({"b": pin(s["b"].t), "theta": pin(s["theta"].t),
+                               "g": pin(eng.rows_of(s["g"])), "f": pin(eng.rows_of(s["f"]))})
+            host["out"] = {k: torch.empty_like(host["in"][k], pin_memory=True)
+                           for k in ("g", "f", "theta")}
+        else:
+            host["out"] = {}
         return host
 
     def e2e_step_sharded(self, host):
@@ -693,6 +725,21 @@ class Workload:
         dev = s["A"].t.device
         d = {k: v.to(dev, non_blocking=True) for k, v in host["in"].items()}
         A, Pm, B = eng.replicated(d["a"]), eng.replicated(d["precond"]), eng.replicated(d["residual"])
+        if "gc" in s:
+            gc = s["gc"]
+            g = f = theta = None
+            if gc.is_root:
+                theta = gc.plain_richardson(eng.replicated(d["theta"]), eng.local(d["g"]), A,
+                                            eng.replicated(d["b"]))
+                g, f = eng.local(d["g"]), eng.local(d["f"])
+            g, f = gc.step(g, f, A, Pm, B)
+            if gc.is_root:
+                host["out"]["g"].copy_(eng.rows_of(g), non_blocking=True)
+                host["out"]["f"].copy_(eng.rows_of(f), non_blocking=True)
+                host["out"]["theta"].copy_(theta.t, non_blocking=True)
+            h2d = sum(v.numel() * 8 for v in host["in"].values())
+            d2h = sum(v.numel() * 8 for v in host["out"].values())
+            return h2d, d2h
         theta = eng.plain_richardson(eng.replicated(d["theta"]), eng.local(d["g"]), A,
                                      eng.replicated(d["b"]))
         if self.cfg == "c4":
@@ -882,7 +929,7 @@ def run_ours(args):
     world, rank, local = dist_setup(args)
     from paper_2008_11480_b200 import _lib
 
-    w = Workload(args.config, args.n, world, hoist=args.hoist, comm=args.comm)
+    w = Workload(args.config, args.n, world, hoist=args.hoist, comm=args.comm, shard=args.shard)
     w.setup()
     flops = w.flops()
     h = _lib.handle()
@@ -987,7 +1034,9 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded PCG64 draws, SURVEY Appendix A recipe)",
             "config": {"workload": w.workload, "n": w.n,
-                       "parallelism": (f"block-row x{world} ({_COMM_LABEL[args.comm]})"
+                       "parallelism": (f"composite parts on GPU groups x{world} (NCCL p2p tree)"
+                                       if w.sharded is not None and "gc" in w.sharded
+                                       else f"block-row x{world} ({_COMM_LABEL[args.comm]})"
                                        if w.sharded is not None
                                        else f"batch split x{world} (no communication)" if w.split_batch
                                        else (f"replicas x{world}" if world > 1 else "single-gpu")),
@@ -1028,6 +1077,9 @@ def main():
                          "composite parts (NOT the reference DAG; FLOPs counted as executed)")
     ap.add_argument("--comm", choices=["peer", "peer-stream", "nccl"], default="peer",
                     help="row-panel exchange of the sharded path (N > 1)")
+    ap.add_argument("--shard", choices=["rows", "parts"], default="rows",
+                    help="c4 at N > 1: block-row sharding of every product (rows) or the "
+                         "composite parts on GPU groups + one tree reduction (parts)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

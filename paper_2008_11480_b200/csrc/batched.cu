@@ -490,8 +490,10 @@ struct Geo {
   // SM: 16 warps hide latency.
   static constexpr int WARPS = NP == 32 ? SI_RESIDENT_WARPS32 : SI_RESIDENT_WARPS64;
   static constexpr int THREADS = WARPS * 32;
-  static constexpr int WROWS = NP / (WARPS / 2);  // warp tile rows (16)
-  static constexpr int WCOLS = NP / 2;             // warp tile cols (16 or 32)
+  // warp tile: a single warp owns the whole NP x NP product; otherwise the
+  // warps form a (WARPS/2) x 2 grid
+  static constexpr int WROWS = WARPS == 1 ? NP : NP / (WARPS / 2);
+  static constexpr int WCOLS = WARPS == 1 ? NP : NP / 2;
   static constexpr int MT = WROWS / 8, NT = WCOLS / 8;
   // 16-byte chunk swizzle of row r: a distinct even value for the four rows
   // of a fragment (conflict-free 8-byte fragment loads), with rows 2q and 2q+1
