@@ -337,7 +337,7 @@ class Workload:
         self.sharded = None
         if self.world > 1 and cfg == "c4" and self.shard == "parts":
             # composite parts on GPU groups + one ordered (t, r) tree reduction
-            # (grouped.py); the state lives on the root group, row-sharded inside it
+            # (grouped.py); the state is block-row sharded over all ranks
             from paper_2008_11480_b200.grouped import GroupedComposite
 
             gc = GroupedComposite(self.n, (2, 3, 4, 5), 2)
@@ -347,8 +347,8 @@ class Workload:
                 "gc": gc, "eng": eng, "comm": comm,
                 "A": eng.replicated(self.sp.matrix), "P": eng.replicated(self.sp.precond),
                 "B": eng.replicated(self.sp.residual), "b": eng.replicated(b),
-                "g": eng.local(st.estimate[comm.r0:comm.r1].clone()) if gc.is_root else None,
-                "f": eng.local(st.residual[comm.r0:comm.r1].clone()) if gc.is_root else None,
+                "g": eng.local(st.estimate[comm.r0:comm.r1].clone()),
+                "f": eng.local(st.residual[comm.r0:comm.r1].clone()),
                 "theta": eng.replicated(torch.zeros_like(b)),
             }
             del st
@@ -707,14 +707,11 @@ class Workload:
             h.copy_(t)
             return h
 
-        host = {"in": {"a": pin(s["A"].t), "precond": pin(s["P"].t), "residual": pin(s["B"].t)}}
-        if s["g"] is not None:  # grouped mode: the state lives on the root group only
-            host["in"].update({"b": pin(s["b"].t), "theta": pin(s["theta"].t),
-                               "g": pin(eng.rows_of(s["g"])), "f": pin(eng.rows_of(s["f"]))})
-            host["out"] = {k: torch.empty_like(host["in"][k], pin_memory=True)
-                           for k in ("g", "f", "theta")}
-        else:
-            host["out"] = {}
+        host = {"in": {"a": pin(s["A"].t), "precond": pin(s["P"].t), "residual": pin(s["B"].t),
+                       "b": pin(s["b"].t), "theta": pin(s["theta"].t),
+                       "g": pin(eng.rows_of(s["g"])), "f": pin(eng.rows_of(s["f"]))}}
+        host["out"] = {k: torch.empty_like(host["in"][k], pin_memory=True)
+                       for k in ("g", "f", "theta")}
         return host
 
     def e2e_step_sharded(self, host):
@@ -725,24 +722,11 @@ class Workload:
         dev = s["A"].t.device
         d = {k: v.to(dev, non_blocking=True) for k, v in host["in"].items()}
         A, Pm, B = eng.replicated(d["a"]), eng.replicated(d["precond"]), eng.replicated(d["residual"])
-        if "gc" in s:
-            gc = s["gc"]
-            g = f = theta = None
-            if gc.is_root:
-                theta = gc.plain_richardson(eng.replicated(d["theta"]), eng.local(d["g"]), A,
-                                            eng.replicated(d["b"]))
-                g, f = eng.local(d["g"]), eng.local(d["f"])
-            g, f = gc.step(g, f, A, Pm, B)
-            if gc.is_root:
-                host["out"]["g"].copy_(eng.rows_of(g), non_blocking=True)
-                host["out"]["f"].copy_(eng.rows_of(f), non_blocking=True)
-                host["out"]["theta"].copy_(theta.t, non_blocking=True)
-            h2d = sum(v.numel() * 8 for v in host["in"].values())
-            d2h = sum(v.numel() * 8 for v in host["out"].values())
-            return h2d, d2h
         theta = eng.plain_richardson(eng.replicated(d["theta"]), eng.local(d["g"]), A,
                                      eng.replicated(d["b"]))
-        if self.cfg == "c4":
+        if "gc" in s:  # composite parts on GPU groups (grouped.py)
+            g, f = s["gc"].step(eng.local(d["g"]), eng.local(d["f"]), A, Pm, B)
+        elif self.cfg == "c4":
             g, f = eng.composite_step(eng.local(d["g"]), eng.local(d["f"]), A, Pm, B,
                                       (2, 3, 4, 5), 2)
         else:

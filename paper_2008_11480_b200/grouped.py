@@ -14,11 +14,12 @@ GPUs at the same time.  The fold is associative as an operation on pairs,
 
 so each GPU group folds a contiguous segment of the parts locally (left to
 right, exactly the reference's fold inside the segment) and the segment results
-are combined by an ordered binary tree -- one reduction -- into the root group,
-which holds the state, computes S_n(F) G while the other groups work on their
-parts, and assembles G', F'.  Inside a group the products are block-row
-sharded (:class:`~paper_2008_11480_b200.sharded.ShardedEngine` on a
-sub-communicator), so e.g. 8 GPUs and 4 parts run 4 groups of 2.
+are combined by an ordered binary tree -- one reduction -- whose every combine
+runs block-row sharded over the union of the two groups' ranks; the root of the
+tree covers all ranks, which hold the state block-row sharded, compute
+S_n(F) G together and assemble G', F' together.  Inside a group the products
+are block-row sharded too (:class:`~paper_2008_11480_b200.sharded.ShardedEngine`
+on a sub-communicator), so e.g. 8 GPUs and 4 parts run 4 groups of 2.
 
 Same GEMM DAG size as the reference: every part product, 2 per fold/combine
 (the tree performs k - 1 combines like the left fold), S_n and the two
@@ -29,12 +30,13 @@ the single-GPU ``composite_step``; with several, the tree's association
 differs from the left fold, so agreement is within the FP64 tolerance
 (rounding at the kappa(A) u level), not bitwise.
 
-The pair exchange of the tree is point-to-point (``torch.distributed``
-isend/irecv: NCCL over NVLink on GPUs, gloo in the CPU tests): every rank of
-the sending group ships its row blocks of (t, r) to every rank of the
-receiving group.  Work is partitioned by a cost model (products per part,
-divided by the group size) that picks the contiguous segmentation with the
-shortest critical path.
+The exchange of a combine is point-to-point (``torch.distributed``
+``batch_isend_irecv``: NCCL over NVLink on GPUs; gloo isend/irecv in the CPU
+tests): the union's ranks receive their rows of the left range's (t, r) and the
+right range's (t, r) in full.  Work is partitioned by a cost model (products
+per part divided by the group size, combines divided by the union size) that
+picks group sizes and the contiguous segmentation with the shortest critical
+path.
 """
 
 from __future__ import annotations
@@ -91,50 +93,73 @@ def part_cost(x: int) -> int:
     return eng.ctr.mmm
 
 
-def _critical_path(segments, sizes, costs, order_n) -> float:
-    """Time (in products of one GPU) until the root group has G', F'."""
-    ready = []
-    for gi, seg in enumerate(segments):
-        work = sum(costs[i] for i in seg) + 2 * (len(seg) - 1)
-        if gi == 0:
-            work += order_n - 1  # S_n(F) G on the root group
-        ready.append(work / sizes[gi])
-    g = len(segments)
+def _tree_levels(ngroups: int):
+    """Ordered binary tree over the groups: per level d = 1, 2, 4, ... the
+    combines (lo, mid, hi) of group ranges L = [lo, mid), R = [mid, hi)."""
+    out = []
     d = 1
-    while d < g:
-        for i in range(0, g, 2 * d):
-            if i + d < g:
-                ready[i] = max(ready[i], ready[i + d]) + 2 / sizes[i]
+    while d < ngroups:
+        out.append([(i, i + d, min(i + 2 * d, ngroups)) for i in range(0, ngroups, 2 * d)
+                    if i + d < ngroups])
         d *= 2
-    return ready[0] + 2 / sizes[0]
+    return out
+
+
+def _critical_path(segments, sizes, costs, order_n) -> float:
+    """Time (in products of one GPU) until every rank has its rows of G', F':
+    S_n(F) G block-row over all ranks, each group's parts and fold block-row
+    over the group, every tree combine block-row over the union of its two
+    ranges, G' and F' block-row over all ranks."""
+    world = sum(sizes)
+    pre = (order_n - 1) / world
+    ready = [pre + (sum(costs[i] for i in seg) + 2 * (len(seg) - 1)) / sizes[gi]
+             for gi, seg in enumerate(segments)]
+    for level in _tree_levels(len(segments)):
+        for lo, mid, hi in level:
+            ready[lo] = max(ready[lo], ready[mid]) + 2 / sum(sizes[lo:hi])
+    return ready[0] + 2 / world
+
+
+def _compositions(total: int, parts: int):
+    """Ordered ways to write ``total`` as ``parts`` positive integers."""
+    for cuts in itertools.combinations(range(1, total), parts - 1):
+        b = (0,) + cuts + (total,)
+        yield [b[i + 1] - b[i] for i in range(parts)]
 
 
 def plan_groups(world: int, costs, order_n: int):
-    """Split ``world`` ranks into G = min(world, parts) contiguous groups of
-    near-equal size and the parts into G contiguous segments, choosing the
-    segmentation with the shortest critical path.  Returns (groups, segments):
-    lists of rank lists and of part-index lists."""
+    """Split ``world`` ranks into G = min(world, parts) contiguous groups and the
+    parts into G contiguous segments, choosing group sizes and segmentation with
+    the shortest critical path (ties: the first found, near-equal sizes first).
+    Returns (groups, segments): lists of rank lists and of part-index lists."""
     k = len(costs)
     if k < 1:
         raise ValueError("composite spec needs at least one rate")
     g = max(1, min(world, k))
-    groups = [list(range(r0, r1)) for r0, r1 in row_splits(world, g)]
-    sizes = [len(x) for x in groups]
+    even = [r1 - r0 for r0, r1 in row_splits(world, g)]
+    size_opts = [even] + [s for s in _compositions(world, g) if s != even]
     best, best_t = None, None
-    for cuts in itertools.combinations(range(1, k), g - 1):
-        bounds = (0,) + cuts + (k,)
-        segs = [list(range(bounds[i], bounds[i + 1])) for i in range(g)]
-        t = _critical_path(segs, sizes, costs, order_n)
-        if best_t is None or t < best_t - 1e-12:
-            best, best_t = segs, t
-    return groups, best
+    for sizes in size_opts:
+        for cuts in itertools.combinations(range(1, k), g - 1):
+            bounds = (0,) + cuts + (k,)
+            segs = [list(range(bounds[i], bounds[i + 1])) for i in range(g)]
+            t = _critical_path(segs, sizes, costs, order_n)
+            if best_t is None or t < best_t - 1e-9:
+                best, best_t = (sizes, segs), t
+    sizes, segs = best
+    groups, r = [], 0
+    for sz in sizes:
+        groups.append(list(range(r, r + sz)))
+        r += sz
+    return groups, segs
 
 
 class GroupedComposite:
     """The composite step with its parts on GPU groups and one tree reduction.
 
-    Every rank holds A, S^-1, B (replicated); the state (G, F) and theta live
-    on the root group (group 0) as row blocks of its sub-communicator.
+    Every rank holds A, S^-1, B (replicated).  The state (G, F) and theta are
+    block-row sharded over all ranks (``world_eng``), like the block-row path:
+    S_n(F) G and the assembly G' = t + r S_n(F) G, F' = I - G' A use every GPU.
     ``ops`` injects the local-ops layer (CPU in the gloo tests); the default is
     the DMMA library."""
 
@@ -153,31 +178,66 @@ class GroupedComposite:
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.costs = [part_cost(x) for x in self.rates]
         self.groups, self.segments = plan_groups(self.world, self.costs, order_n)
+        self.levels = _tree_levels(len(self.groups))
         self.gid = next(i for i, g in enumerate(self.groups) if self.rank in g)
-        pg = None
-        if self.world > 1:
-            # every rank creates every subgroup, in the same order
-            for i, ranks in enumerate(self.groups):
-                h = dist.new_group(ranks)
-                if i == self.gid:
-                    pg = h
-        self.comm = RowComm(n, group=pg)
-        self.eng = ShardedEngine(self.comm, ops=ops, prefetch=prefetch)
-        self.is_root = self.gid == 0
-        self.bytes_sent = 0
-        # gloo point-to-point moves host memory only: stage device blocks through
-        # the host (the 1-GPU test mode that runs every rank on cuda:0)
         self._stage = self.world > 1 and dist.get_backend() == "gloo"
+        self.bytes_moved = 0
+
+        def ranks_of(lo, hi):
+            return [r for g in self.groups[lo:hi] for r in g]
+
+        # communicators: every rank creates every subgroup, in the same order; a
+        # range covering all ranks uses the default group
+        ranges = [tuple(g) for g in self.groups]
+        for level in self.levels:
+            ranges += [tuple(ranks_of(lo, hi)) for lo, _, hi in level]
+        pgs = {}
+        for rr in ranges:
+            if rr in pgs:
+                continue
+            if len(rr) == self.world:
+                pgs[rr] = None
+            else:
+                pg = dist.new_group(list(rr)) if self.world > 1 else None
+                pgs[rr] = pg
+        engines = {}
+
+        def engine(rr):
+            rr = tuple(rr)
+            if rr not in engines:
+                comm = RowComm(n, group=pgs.get(rr)) if self.rank in rr else None
+                engines[rr] = ShardedEngine(comm, ops=ops, prefetch=prefetch) if comm else None
+            return engines[rr]
+
+        self.world_eng = engine(tuple(range(self.world)))
+        self.group_eng = engine(self.groups[self.gid])
+        # this rank's combines: (L ranks, R ranks, union engine) per level
+        self.plan = []
+        for level in self.levels:
+            for lo, mid, hi in level:
+                u = ranks_of(lo, hi)
+                if self.rank in u:
+                    self.plan.append((ranks_of(lo, mid), ranks_of(mid, hi), engine(u)))
+        self._engines = [e for e in engines.values() if e is not None]
+        # the exchange of the tree uses point-to-point ops: wire them up front
+        # (NCCL's batched p2p needs the pair communicators' first use collective)
+        self.eng = self.world_eng
+        self.comm = self.world_eng.comm
 
     # -- helpers ---------------------------------------------------------------
     @property
     def ctr(self) -> MulCounter:
-        """This rank's counter (each rank of a group ticks once per group product)."""
-        return self.eng.ctr
+        """This rank's products (each rank of a communicator ticks once per
+        product of that communicator)."""
+        c = MulCounter()
+        for e in self._engines:
+            c.mmm += e.ctr.mmm
+            c.mvm += e.ctr.mvm
+        return c
 
     def products_executed(self) -> int:
-        """Products over all groups so far (group leaders' counters summed)."""
-        own = self.eng.ctr.mmm if self.comm.rank == 0 else 0
+        """Products over all groups so far (each communicator's leader counts)."""
+        own = sum(e.ctr.mmm for e in self._engines if e.comm.rank == 0)
         if self.world == 1:
             return own
         dev = "cuda" if self.dist.get_backend() == "nccl" else "cpu"
@@ -185,39 +245,70 @@ class GroupedComposite:
         self.dist.all_reduce(t)
         return int(t.item())
 
-    def _send_pair(self, t: Sharded, r: Sharded, dst_group: int):
-        """Ship this rank's row blocks of (t, r) to every rank of ``dst_group``."""
-        works = []
-        for v in (t, r):
-            blk = self.eng.rows_of(v).contiguous()
-            if self._stage and blk.is_cuda:
-                blk = blk.cpu()
-            for dst in self.groups[dst_group]:
-                works.append(self.dist.isend(blk, dst))
-                self.bytes_sent += blk.numel() * blk.element_size()
-        for w in works:
-            w.wait()
+    def _move(self, blocks, count: int, src, dst, full: bool, like: torch.Tensor):
+        """Row blocks of ``count`` matrices held by the ranks ``src`` (near-equal
+        row split over them; ``blocks`` on src ranks) -> on the ranks ``dst``
+        either the full matrices (``full``) or their rows of dst's split.
+        Point-to-point; returns a list on dst ranks, else None."""
+        n = self.n
+        me = self.rank
+        ssplit = row_splits(n, len(src))
+        dsplit = row_splits(n, len(dst))
 
-    def _recv_pair(self, src_group: int, like: torch.Tensor):
-        """Full (t, r) of ``src_group``, assembled from its ranks' row blocks."""
-        src = self.groups[src_group]
-        splits = row_splits(self.n, len(src))
-        dev = "cpu" if self._stage else like.device
-        fulls, works = [], []
-        for _ in range(2):
-            full = torch.empty((self.n, self.n), dtype=torch.float64, device=dev)
-            for s, (r0, r1) in zip(src, splits):
-                works.append(self.dist.irecv(full[r0:r1], s))
-            fulls.append(full)
-        for w in works:
-            w.wait()
-        if self._stage and like.is_cuda:
-            fulls = [x.to(like.device) for x in fulls]
-        return fulls
+        def want(t):
+            return (0, n) if full else dsplit[dst.index(t)]
+
+        ops, out, copies = [], None, []
+        if me in dst:
+            c, d = want(me)
+            out = [torch.empty((d - c, n), dtype=torch.float64, device=like.device)
+                   for _ in range(count)]
+            for j in range(count):
+                for si, s in enumerate(src):
+                    a, b = ssplit[si]
+                    lo, hi = max(a, c), min(b, d)
+                    if lo >= hi:
+                        continue
+                    if s == me:
+                        out[j][lo - c:hi - c].copy_(blocks[j][lo - a:hi - a])
+                    elif self._stage:
+                        buf = torch.empty((hi - lo, n), dtype=torch.float64)
+                        ops.append(("recv", buf, s))
+                        copies.append((out[j][lo - c:hi - c], buf))
+                    else:
+                        ops.append(("recv", out[j][lo - c:hi - c], s))
+        if me in src:
+            a, b = ssplit[src.index(me)]
+            for j in range(len(blocks)):
+                for t in dst:
+                    if t == me:
+                        continue
+                    c, d = want(t)
+                    lo, hi = max(a, c), min(b, d)
+                    if lo >= hi:
+                        continue
+                    x = blocks[j][lo - a:hi - a].contiguous()
+                    if self._stage:
+                        x = x.cpu()
+                    ops.append(("send", x, t))
+                    self.bytes_moved += x.numel() * 8
+        if ops:
+            if self._stage:  # gloo: tagged, non-blocking point-to-point
+                works = [self.dist.isend(x, p) if k == "send" else self.dist.irecv(x, p)
+                         for k, x, p in ops]
+            else:  # NCCL: one group, no ordering constraints between peers
+                works = self.dist.batch_isend_irecv(
+                    [self.dist.P2POp(self.dist.isend if k == "send" else self.dist.irecv, x, p)
+                     for k, x, p in ops])
+            for w in works:
+                w.wait()
+        for dstv, buf in copies:
+            dstv.copy_(buf)
+        return out
 
     def _segment(self, a: Sharded, precond: Sharded, residual: Sharded):
         """Left fold over this group's parts (newton_schulz.py:204-216)."""
-        eng = self.eng
+        eng = self.group_eng
         t_c = r_c = None
         for i in self.segments[self.gid]:
             x = self.rates[i]
@@ -229,39 +320,31 @@ class GroupedComposite:
             else:
                 t_c = eng.mm(r_c, t, c=t_c, beta=1.0)
                 r_c = eng.mm(r_c, gam)
-        return t_c, r_c
+        return eng.rows_of(t_c), eng.rows_of(r_c)
 
     # -- the step ----------------------------------------------------------------
-    def step(self, g: Sharded | None, f: Sharded | None, a: Sharded, precond: Sharded,
-             residual: Sharded):
-        """One composite step.  On root-group ranks ``g``/``f`` are this rank's row
-        blocks and (G', F') row blocks are returned; elsewhere they are ignored
-        and (None, None) is returned."""
-        eng = self.eng
-        nsp = None
-        if self.is_root:
-            if g is None or f is None:
-                raise ValueError("the root group needs the state (g, f)")
-            nsp = eng.horner(f, g, self.order_n)  # state part, overlaps the others' parts
-        t_c, r_c = self._segment(a, precond, residual)
-        ng = len(self.groups)
-        d = 1
-        while d < ng:
-            if self.gid % (2 * d) == d:
-                self._send_pair(t_c, r_c, self.gid - d)
-                return None, None
-            if self.gid % (2 * d) == 0 and self.gid + d < ng:
-                t_r, r_r = self._recv_pair(self.gid + d, eng.rows_of(a))
-                t_c = eng.mm(r_c, eng.replicated(t_r), c=t_c, beta=1.0)
-                r_c = eng.mm(r_c, eng.replicated(r_r))
-                del t_r, r_r
-            d *= 2
-        g_new = eng.mm(r_c, nsp, c=t_c, beta=1.0)
-        f_new = eng.residual(g_new, a, gather=False)  # F is only ever a left operand
+    def step(self, g: Sharded, f: Sharded, a: Sharded, precond: Sharded, residual: Sharded):
+        """One composite step on world-split row blocks ``g``, ``f`` (Sharded of
+        ``world_eng``); returns the (G', F') row blocks."""
+        W = self.world_eng
+        nsp = W.horner(f, g, self.order_n)  # state part, block-row over all ranks
+        t, r = self._segment(a, precond, residual)
+        like = W.rows_of(a)
+        for left, right, ue in self.plan:
+            # my current blocks belong to `left` or `right` (their owners' split)
+            union = left + right
+            t_l, r_l = self._move([t, r] if self.rank in left else [], 2, left, union, False, like)
+            t_r, r_r = self._move([t, r] if self.rank in right else [], 2, right, union, True, like)
+            t = ue.ops.gemm(r_l, t_r, 1.0, t_l, 1.0, 0.0, ue.comm.r0, False, ue.ctr)
+            r = ue.ops.gemm(r_l, r_r, 1.0, None, 0.0, 0.0, ue.comm.r0, False, ue.ctr)
+            del t_l, r_l, t_r, r_r
+        if self.plan:
+            assert self.plan[-1][2].comm.world == self.world
+        g_new = W.mm(W.local(r), nsp, c=W.local(t), beta=1.0)
+        f_new = W.residual(g_new, a, gather=False)  # F is only ever a left operand
         return g_new, f_new
 
     def plain_richardson(self, theta: Sharded, p: Sharded, a: Sharded, b: Sharded):
-        """theta - P (A theta - b) on the root group."""
-        if not self.is_root:
-            return theta
-        return self.eng.plain_richardson(theta, p, a, b)
+        """theta - P (A theta - b) with world-split P."""
+        return self.world_eng.plain_richardson(theta, p, a, b)
+

@@ -62,25 +62,21 @@ def _worker(rank, world, port, outdir, n, steps):
     eng, comm = gc.eng, gc.comm
     A, Pm, B = (eng.replicated(x) for x in (sp.matrix, sp.precond, sp.residual))
     b = eng.replicated(P.as_device(b_np))
-    g = f = theta = None
-    if gc.is_root:
-        g = eng.local(st.estimate[comm.r0:comm.r1].clone())
-        f = eng.local(st.residual[comm.r0:comm.r1].clone())
-        theta = eng.replicated(torch.zeros_like(b.t))
+    g = eng.local(st.estimate[comm.r0:comm.r1].clone())
+    f = eng.local(st.residual[comm.r0:comm.r1].clone())
+    theta = eng.replicated(torch.zeros_like(b.t))
     for _ in range(steps):
-        if gc.is_root:
-            theta = gc.plain_richardson(theta, g, A, b)
+        theta = gc.plain_richardson(theta, g, A, b)
         g, f = gc.step(g, f, A, Pm, B)
     torch.cuda.synchronize()
     total = gc.products_executed()
-    if gc.is_root:
-        g_full = comm.all_gather_rows(g.t)
-        f_full = comm.all_gather_rows(f.t)
-        if comm.rank == 0:
-            np.save(os.path.join(outdir, "g.npy"), g_full.cpu().numpy())
-            np.save(os.path.join(outdir, "f.npy"), f_full.cpu().numpy())
-            np.save(os.path.join(outdir, "theta.npy"), theta.t.cpu().numpy())
-            np.save(os.path.join(outdir, "meta.npy"), np.array([total, len(gc.groups)]))
+    g_full = comm.all_gather_rows(g.t)
+    f_full = comm.all_gather_rows(f.t)
+    if rank == 0:
+        np.save(os.path.join(outdir, "g.npy"), g_full.cpu().numpy())
+        np.save(os.path.join(outdir, "f.npy"), f_full.cpu().numpy())
+        np.save(os.path.join(outdir, "theta.npy"), theta.t.cpu().numpy())
+        np.save(os.path.join(outdir, "meta.npy"), np.array([total, len(gc.groups)]))
     dist.destroy_process_group()
 
 
