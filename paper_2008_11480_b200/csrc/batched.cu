@@ -706,6 +706,8 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
     if (prefetch && (sys == blockIdx.x || p.chunk_ready)) issue(sys);
     for (int it = 0; it < p.iters; ++it) {
       for (int k = 0; k < p.nops; ++k) {
+        // (the LIN term list is read from shared memory, prog[k].t[j]: indexing
+        // the register copy with a runtime j would put `o` in local memory)
         const DOp o = prog[k];
         const double* oc = cst + o.cidx;
         if (o.kind == OP_LOAD && prefetch) {
@@ -782,7 +784,7 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
           if (threadIdx.x < NP) {
             double acc = 0.0;
             for (int j = 0; j < o.nterms; ++j) {
-              const double xv = vslot(o.t[j])[threadIdx.x];
+              const double xv = vslot(prog[k].t[j])[threadIdx.x];
               acc = __dadd_rn(acc, oc[1 + j] == 1.0 ? xv : __dmul_rn(oc[1 + j], xv));
             }
             vslot(o.dst)[threadIdx.x] = acc;
@@ -794,7 +796,7 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
             const int c = G::col_at(r, i % NP);
             double acc = (r == c && r < n) ? oc[0] : 0.0;
             for (int j = 0; j < o.nterms; ++j) {
-              const double xv = mslot(o.t[j])[i];
+              const double xv = mslot(prog[k].t[j])[i];
               acc = __dadd_rn(acc, oc[1 + j] == 1.0 ? xv : __dmul_rn(oc[1 + j], xv));
             }
             D[i] = acc;
@@ -1031,7 +1033,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(Ba
             const int row = rbase + threadIdx.x;
             double acc = 0.0;
             for (int j = 0; j < o.nterms; ++j) {
-              const double xv = vslot(o.t[j])[row];
+              const double xv = vslot(prog[k].t[j])[row];
               acc = __dadd_rn(acc, oc[1 + j] == 1.0 ? xv : __dmul_rn(oc[1 + j], xv));
             }
             double* dp = vslot(o.dst) + row;
@@ -1047,7 +1049,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(Ba
             const int c = G::col_at(r, i % NP);
             double acc = (r == c && r < n) ? oc[0] : 0.0;
             for (int j = 0; j < o.nterms; ++j) {
-              const double xv = mslot(o.t[j])[i];
+              const double xv = mslot(prog[k].t[j])[i];
               acc = __dadd_rn(acc, oc[1 + j] == 1.0 ? xv : __dmul_rn(oc[1 + j], xv));
             }
             D[i] = acc;
