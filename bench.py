@@ -236,6 +236,24 @@ _COMM_LABEL = {"peer": "copy-engine panel exchange, panel-gated products",
                "nccl": "NCCL all-gather"}
 
 
+def workload_desc(cfg: str, n: int, batch: int = 16384) -> str:
+    """The `config.workload` string of a config (both arms print the same one)."""
+    if cfg == "c4":
+        return (f"c4: dense SPD n={n}, Householder(64) eigenbasis, kappa 1e6, 64 RHS; "
+                "composite NS rates (2,3,4,5) order_n=2 + plain Richardson")
+    if cfg == "c3":
+        return f"c3: Gram n={n}; order-8 factorised NS (h8) + plain Richardson"
+    if cfg == "c1":
+        return (f"c1: dense SPD n={n}; 30 x (plain Richardson + NS order 3), "
+                "resident kernel (one launch per 30-iteration run)")
+    if cfg == "c5":
+        return f"c5: Gram n={n}, 256 RHS; recursive Richardson/NS order 16"
+    if cfg == "c2":
+        return (f"c2: {batch} systems 32x32; 50 x (plain Richardson + composite "
+                "(2,3) order_n=2), resident kernel (one launch per 50-iteration run)")
+    raise ValueError(cfg)
+
+
 class Workload:
     """One config: device state + one step function + algorithmic FLOPs per step."""
 
@@ -282,13 +300,13 @@ class Workload:
                 a, b = configs.c4_householder_device(n=self.n, rhs=self.r)
             else:
                 a, b = (P.as_device(x) for x in configs.c4_householder(n=self.n, rhs=self.r))
-            self.workload = f"c4: dense SPD n={self.n}, Householder(64) eigenbasis, kappa 1e6, {self.r} RHS; composite NS rates (2,3,4,5) order_n=2 + plain Richardson"
+            self.workload = workload_desc(cfg, self.n)
         elif cfg == "c3":
             self.n = self.n or 4096
             self.r = 1
             a_np, b_np = configs.c3_gram(n=self.n)
             a, b = P.as_device(a_np), P.as_device(b_np)
-            self.workload = f"c3: Gram n={self.n}; order-8 factorised NS (h8) + plain Richardson"
+            self.workload = workload_desc(cfg, self.n)
         elif cfg == "c1":
             self.n = self.n or 64
             self.r = 1
@@ -296,8 +314,7 @@ class Workload:
             a, b = P.as_device(a_np), P.as_device(b_np)
             # one bench step = the whole 30-iteration run in one resident launch
             self.iters_per_step = 30
-            self.workload = (f"c1: dense SPD n={self.n}; 30 x (plain Richardson + NS order 3), "
-                             "resident kernel (one launch per 30-iteration run)")
+            self.workload = workload_desc(cfg, self.n)
             alpha = float(torch.max(torch.sum(torch.abs(a), dim=1)))
             eye = torch.eye(self.n, dtype=torch.float64, device=a.device)
             self.c1 = {"a": a, "b": b, "p": eye / alpha, "f": eye - a / alpha,
@@ -308,7 +325,7 @@ class Workload:
             self.n = self.n or 32768
             self.r = 256
             a, b = configs.c5_gram_device(n=self.n, m=int(self.n * 40000 / 32768), rhs=self.r)
-            self.workload = f"c5: Gram n={self.n}, {self.r} RHS; recursive Richardson/NS order 16"
+            self.workload = workload_desc(cfg, self.n)
         elif cfg == "c2":
             self.batch = self.n or 16384
             a_np, b_np = configs.c2_batched(batch=self.batch)
@@ -325,8 +342,7 @@ class Workload:
             self.p2, self.f2 = self.pre2.clone(), self.res2.clone()
             self.t2 = torch.zeros_like(self.b2)
             self.iters_per_step = 50
-            self.workload = (f"c2: {self.batch} systems 32x32; 50 x (plain Richardson + composite "
-                             "(2,3) order_n=2), resident kernel (one launch per 50-iteration run)")
+            self.workload = workload_desc(cfg, 32, self.batch)
             self.n = 32
             return
         else:
@@ -871,7 +887,8 @@ def run_reference(args):
         "ms_per_step": step_s * 1e3, "iters_per_step": w.iters_per_step,
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg, "n": w.n,
+        "config": {"workload": workload_desc(cfg, w.n, w.batch), "n": w.n,
+                   "parallelism": f"host CPU, {cores} threads (rank 0 only)",
                    "sample": "executed" if cfg in ("c1", "c2", "c3") else "extrapolated"},
         "tflops": flops / step_s / 1e12,
         "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "port",
