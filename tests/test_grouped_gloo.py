@@ -45,7 +45,7 @@ def test_plan_groups_shapes():
         plan_groups(2, [], 2)
 
 
-def _worker(rank, world, port, outdir, n, steps, rates):
+def _worker(rank, world, port, outdir, n, steps, rates, order_n=2):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -56,7 +56,7 @@ def _worker(rank, world, port, outdir, n, steps, rates):
                             world_size=world)
     a_np, b_np = configs.c4_householder(n=n, rhs=3)
     alpha = np.max(np.sum(np.abs(a_np), axis=1))
-    gc = GroupedComposite(n, rates, 2, ops=CpuOps())
+    gc = GroupedComposite(n, rates, order_n, ops=CpuOps())
     eng, comm = gc.eng, gc.comm
     A = eng.replicated(torch.as_tensor(a_np))
     P = eng.replicated(torch.eye(n, dtype=torch.float64) / alpha)
@@ -80,16 +80,18 @@ def _worker(rank, world, port, outdir, n, steps, rates):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,rates", [(2, 40, (2, 3, 4, 5)), (4, 33, (2, 3, 4, 5)),
-                                           (3, 24, (2, 3, 1, 4, 5)), (5, 26, (2, 3, 4, 5)),
-                                           (8, 40, (2, 3, 4, 5)), (6, 30, (2, 3, 4))])
-def test_grouped_composite_matches_oracle(world, n, rates):
+@pytest.mark.parametrize("world,n,rates,order_n", [
+    (2, 40, (2, 3, 4, 5), 2), (4, 33, (2, 3, 4, 5), 2), (3, 24, (2, 3, 1, 4, 5), 2),
+    (5, 26, (2, 3, 4, 5), 2), (8, 40, (2, 3, 4, 5), 2), (6, 30, (2, 3, 4), 2),
+    (2, 21, (3, 2), 1), (3, 27, (2, 5, 3), 3)])
+def test_grouped_composite_matches_oracle(world, n, rates, order_n):
     from oracle import seriesinv_oracle as O
     from paper_2008_11480_b200 import configs
 
     steps = 3
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, _free_port(), d, n, steps, rates), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), d, n, steps, rates, order_n), nprocs=world,
+                 join=True)
         g = np.load(os.path.join(d, "g.npy"))
         f = np.load(os.path.join(d, "f.npy"))
         theta = np.load(os.path.join(d, "theta.npy"))
@@ -101,7 +103,7 @@ def test_grouped_composite_matches_oracle(world, n, rates):
     m0 = st.ctr.mmm
     for _ in range(steps):
         th = O.plain_richardson(th, st.estimate, sp.matrix, b, st.ctr)
-        st = O.composite_step(st, sp.matrix, sp, rates, 2)
+        st = O.composite_step(st, sp.matrix, sp, rates, order_n)
     rel = lambda x, y: np.linalg.norm(x - y) / np.linalg.norm(y)  # noqa: E731
     # the tree associates the fold differently: rounding-level, kappa-scaled
     assert rel(g, st.estimate) <= 1e-10
