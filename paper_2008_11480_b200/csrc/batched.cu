@@ -17,7 +17,9 @@
 // load is then the minimum 2 wavefronts and every accumulator store / C load
 // (16 bytes per lane, rows g and g+1 in one quarter-warp) the minimum 4.
 // Slots are 8 KB (NP=32) / 32 KB (NP=64); the ops are reordered to minimise
-// live slots, so four 32 x 32 systems fit per SM.
+// live slots (32 x 32 products may overwrite their own operands), so five
+// 32 x 32 systems fit per SM (config 2: 5 slots, 42 KB per CTA); systems are
+// claimed dynamically by the CTAs.
 #include <algorithm>
 #include <bitset>
 #include <cstdio>
@@ -58,7 +60,8 @@ struct __align__(16) DOp {
   int16_t dst, a, b, c;
   int16_t t[kMaxLinTerms];
   int16_t cidx;
-  int16_t pad[3];
+  int16_t prebar;  // GEMM writing over its A or B operand: barrier before the stores
+  int16_t pad[2];
 };
 static_assert(sizeof(DOp) == 32, "DOp layout");
 
@@ -213,11 +216,19 @@ struct Rec {
 // Operands an op may overwrite in place (dst in the same slot): each element
 // is read and then written by the same thread -- the C operand of a product
 // (read into the accumulator or in the epilogue), the c vector of a GEMV, the
-// terms of a LIN -- and only when it is not also read as A / B / x.
-std::vector<int> inplace_operands(const BOp& o) {
+// terms of a LIN -- and only when it is not also read as A / B / x.  With
+// `ab` (the one-CTA-per-system kernel, whose slots no other CTA reads) a
+// product may also overwrite its A or B operand: every warp has finished its
+// main loop -- the last read of A and B -- at a CTA barrier before the first
+// store (DOp::prebar); the C operand is preferred (no barrier).
+std::vector<int> inplace_operands(const BOp& o, bool ab = false) {
   std::vector<int> v;
   if (o.kind == OP_GEMM || o.kind == OP_GEMV) {
     if (o.c >= 0 && o.c != o.a && o.c != o.b) v.push_back(o.c);
+    if (ab && o.kind == OP_GEMM) {
+      if (o.a >= 0 && o.a != o.c) v.push_back(o.a);
+      if (o.b >= 0 && o.b != o.c && o.b != o.a) v.push_back(o.b);
+    }
   } else if (o.kind == OP_LIN) {
     for (int j = 0; j < o.nterms; ++j) v.push_back(o.t[j]);
   }
@@ -231,7 +242,7 @@ std::vector<int> inplace_operands(const BOp& o) {
 // ties), memoised on the set of scheduled ops, with a node budget.  Products
 // are unchanged, only their order, so every value is bitwise the same.
 void schedule_min_live(Rec& r, const std::vector<int>& pinned,
-                       const std::vector<std::pair<int, int>>& carried) {
+                       const std::vector<std::pair<int, int>>& carried, bool ab) {
   const int nops = (int)r.ops.size(), nv = (int)r.is_vec.size();
   if (nops > 128) return;
   using Mask = std::bitset<128>;
@@ -285,7 +296,7 @@ void schedule_min_live(Rec& r, const std::vector<int>& pinned,
       const BOp& o = r.ops[i];
       const bool mat = !r.is_vec[o.dst];
       bool inplace = false;
-      for (int v : inplace_operands(o))
+      for (int v : inplace_operands(o, ab))
         inplace |= !r.is_vec[v] && uses[v] == 1 && !keep[v] &&
                    std::count(reads[i].begin(), reads[i].end(), v) == 1;
       const int during = live + (mat && !inplace ? 1 : 0);
@@ -312,10 +323,11 @@ void schedule_min_live(Rec& r, const std::vector<int>& pinned,
 // The search is deterministic in the recorded program, so its result is
 // memoised (repeated launches of the same run re-record the same program).
 void schedule_min_live_cached(Rec& r, const std::vector<int>& pinned,
-                              const std::vector<std::pair<int, int>>& carried) {
+                              const std::vector<std::pair<int, int>>& carried, bool ab) {
   static std::mutex mu;
   static std::unordered_map<std::string, std::vector<BOp>> cache;
   std::string key(reinterpret_cast<const char*>(r.ops.data()), r.ops.size() * sizeof(BOp));
+  key.push_back(ab ? 'b' : 'c');
   for (int v : pinned) key.append(reinterpret_cast<const char*>(&v), sizeof v);
   for (auto& pr : carried) {
     key.append(reinterpret_cast<const char*>(&pr.first), sizeof pr.first);
@@ -329,7 +341,7 @@ void schedule_min_live_cached(Rec& r, const std::vector<int>& pinned,
       return;
     }
   }
-  schedule_min_live(r, pinned, carried);
+  schedule_min_live(r, pinned, carried, ab);
   std::lock_guard<std::mutex> lk(mu);
   if (cache.size() < 256) cache.emplace(std::move(key), r.ops);
 }
@@ -345,7 +357,7 @@ struct Alloc {
 };
 
 Alloc assign(const Rec& r, const std::vector<int>& pinned,
-             const std::vector<std::pair<int, int>>& carried) {
+             const std::vector<std::pair<int, int>>& carried, bool ab) {
   const int nv = (int)r.is_vec.size();
   std::vector<int> last(nv, -1);
   auto use = [&](int v, int i) {
@@ -393,7 +405,7 @@ Alloc assign(const Rec& r, const std::vector<int>& pinned,
     if (al.phys[o.dst] < 0) {
       // in place over an operand that dies here (the carried input first)
       int reuse = -1;
-      for (int v : inplace_operands(o)) {
+      for (int v : inplace_operands(o, ab)) {
         if (v < 0 || r.is_vec[v] != vec || al.phys[v] < 0 || last[v] != i) continue;
         if (reuse < 0 || v == out_of[o.dst]) reuse = v;
       }
@@ -471,6 +483,10 @@ struct BatchArgs {
   unsigned epoch;
   int64_t chunk;
   int rG, rF, rT;          // slots of the carried outputs (copied back when different)
+  // dynamic system scheduling (one-CTA-per-system kernel): CTA b starts with
+  // system b and claims gridDim.x + atomicAdd(sys_counter, 1) next (zeroed per
+  // launch); null = static stride gridDim.x
+  unsigned long long* sys_counter;
 };
 
 template <int NP>
@@ -573,7 +589,7 @@ __device__ __forceinline__ double flip(double x) {
 template <int NP, int MODE>
 __device__ __forceinline__ void gemm_op(const double* A, const double* B, const double* C,
                                         double* D, const double* cst, int n, int warp, int g,
-                                        int t) {
+                                        int t, bool prebar) {
   using G = Geo<NP>;
   const int r0 = (warp >> 1) * G::WROWS, c0 = (warp & 1) * G::WCOLS;
   double acc[G::MT][G::NT][2];
@@ -613,6 +629,7 @@ __device__ __forceinline__ void gemm_op(const double* A, const double* B, const 
       for (int ni = 0; ni < G::NT; ++ni)
         dmma(acc[mi][ni][0], acc[mi][ni][1], af[cur][mi], bf[cur][ni]);
   }
+  if (prebar) __syncthreads();  // D is A's or B's slot: every warp is done reading it
 #pragma unroll
   for (int mi = 0; mi < G::MT; ++mi)
 #pragma unroll
@@ -637,10 +654,10 @@ __device__ __forceinline__ void gemm_op(const double* A, const double* B, const 
 }
 
 template <int NP>
-// 32 x 32 systems: four CTAs per SM fit in shared memory, so registers must
-// not be the tighter limit (<= 128 per thread)
+// 32 x 32 systems: five CTAs per SM fit in shared memory, so registers must
+// not be the tighter limit (<= 204 per thread; ptxas settles at 160)
 #ifndef SI_RESIDENT_MINB32
-#define SI_RESIDENT_MINB32 4
+#define SI_RESIDENT_MINB32 5
 #endif
 __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB32 : 1)
     resident_kernel(BatchArgs p) {
@@ -666,7 +683,16 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
 
   constexpr int PFD = NP * NP / 2 / G::THREADS > 0 ? NP * NP / 2 / G::THREADS : 1;
   double2 pf_p[PFD], pf_b[PFD];
-  for (int64_t sys = blockIdx.x; sys < p.batch; sys += gridDim.x) {
+  // Systems are claimed dynamically: the CTAs of an SM sub-partition holding
+  // more warps than another run slower, and a static stride would leave the
+  // whole launch waiting on them.  Which CTA runs a system does not change its
+  // result (same program, same order).
+  __shared__ int64_t s_next;
+  int64_t sys = blockIdx.x;
+  for (bool first = true; sys < p.batch; first = false) {
+    if (threadIdx.x == 0)
+      s_next = p.sys_counter ? (int64_t)gridDim.x + (int64_t)atomicAdd(p.sys_counter, 1ull)
+                             : sys + gridDim.x;
     if (p.chunk_ready) {  // this system's inputs may still be copying
       if (threadIdx.x == 0) {
         const unsigned* f = p.chunk_ready + sys / p.chunk;
@@ -688,6 +714,7 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
       vslot(p.sb)[threadIdx.x] = threadIdx.x < n ? p.b[sys * n + threadIdx.x] : 0.0;
     }
     __syncthreads();
+    const int64_t nxt = s_next;  // written by thread 0 before the barrier above
     // S^-1 and B are streamed in every iteration through registers: the global
     // loads for the next iteration (or the next system) are issued right after
     // the last LOAD op consumed the previous ones, so their latency hides behind
@@ -703,7 +730,7 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
         pf_b[j] = __ldg(sb2 + threadIdx.x + j * G::THREADS);
       }
     };
-    if (prefetch && (sys == blockIdx.x || p.chunk_ready)) issue(sys);
+    if (prefetch && (first || p.chunk_ready)) issue(sys);
     for (int it = 0; it < p.iters; ++it) {
       for (int k = 0; k < p.nops; ++k) {
         // (the LIN term list is read from shared memory, prog[k].t[j]: indexing
@@ -721,21 +748,22 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
           if (k == p.last_load) {
             if (it + 1 < p.iters)
               issue(sys);
-            else if (sys + gridDim.x < p.batch && !p.chunk_ready)  // gated: at system start
-              issue(sys + gridDim.x);
+            else if (nxt < p.batch && !p.chunk_ready)  // gated: at system start
+              issue(nxt);
           }
         } else if (o.kind == OP_GEMM) {
           const double* A = mslot(o.a);
           const double* B = mslot(o.b);
           const double* C = o.c >= 0 ? mslot(o.c) : nullptr;
           double* D = mslot(o.dst);
+          const bool pb = o.prebar != 0;
           // the DAG's epilogues are "X@Y", "I - X@Y" and "X@Y + Z": specialised,
           // anything else goes through the generic path
           switch (o.mode) {
-            case 0: gemm_op<NP, 0>(A, B, C, D, oc, n, warp, g, t); break;
-            case 1: gemm_op<NP, 1>(A, B, C, D, oc, n, warp, g, t); break;
-            case 2: gemm_op<NP, 2>(A, B, C, D, oc, n, warp, g, t); break;
-            default: gemm_op<NP, 3>(A, B, C, D, oc, n, warp, g, t); break;
+            case 0: gemm_op<NP, 0>(A, B, C, D, oc, n, warp, g, t, pb); break;
+            case 1: gemm_op<NP, 1>(A, B, C, D, oc, n, warp, g, t, pb); break;
+            case 2: gemm_op<NP, 2>(A, B, C, D, oc, n, warp, g, t, pb); break;
+            default: gemm_op<NP, 3>(A, B, C, D, oc, n, warp, g, t, pb); break;
           }
         } else if (o.kind == OP_GEMV) {
           // On the DMMA pipe, not the FP64 ALU: x becomes column 0 of an 8-wide B
@@ -827,6 +855,7 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
       __threadfence_system();
       atomicAdd(p.chunk_done + sys / p.chunk, 1u);
     }
+    sys = nxt;
   }
   if (p.prof && blockIdx.x == 0 && threadIdx.x == 0)
     for (int k = 0; k < p.nops; ++k) p.prof[k] = prof_acc[k];
@@ -1250,8 +1279,11 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
   std::vector<int> pinned = {q.A, q.bv};
   if (q.P >= 0) pinned.push_back(q.P);
   if (q.B >= 0) pinned.push_back(q.B);
-  schedule_min_live_cached(q.r, pinned, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}});
-  Alloc al = assign(q.r, pinned, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}});
+  // products over their own A / B operand: one-CTA-per-system kernel only
+  // (NP = 64 may run as a cluster, whose peers read broadcast copies)
+  const bool ab = NP == 32;
+  schedule_min_live_cached(q.r, pinned, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}}, ab);
+  Alloc al = assign(q.r, pinned, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}}, ab);
   std::vector<BOp> ops = q.r.ops;
   auto ph = [&](int v) -> int16_t { return v >= 0 ? al.phys[v] : (int16_t)-1; };
   for (BOp& o : ops) {
@@ -1342,6 +1374,7 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
     d.c = o.c;
     for (int j = 0; j < kMaxLinTerms; ++j) d.t[j] = o.t[j];
     d.cidx = (int16_t)csts.size();
+    d.prebar = (int16_t)(o.kind == OP_GEMM && (o.dst == o.a || o.dst == o.b));
     if (o.kind == OP_GEMM) {
       const bool hc = o.c >= 0;
       d.mode = (!hc && o.alpha == 1.0 && o.diag == 0.0)                     ? 0
@@ -1488,6 +1521,12 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
     check(cudaMemset(prof, 0, sizeof(long long) * (kMaxOps + 1)), "cudaMemset");
   }
   args.prof = prof;
+  MV counter;  // dynamic system claims (released stream-ordered after the launch)
+  if (batch > grid) {
+    counter = alloc(c, 1, 1);
+    check(cudaMemsetAsync(counter.v.p, 0, sizeof(unsigned long long), c.s), "memset");
+    args.sys_counter = reinterpret_cast<unsigned long long*>(counter.v.p);
+  }
   resident_kernel<NP><<<(unsigned)grid, Gm::THREADS, smem, c.s>>>(args);
   if (want_prof) {
     std::vector<long long> h(kMaxOps + 1);
