@@ -657,14 +657,14 @@ class Workload:
             main.wait_stream(down)
             return host["pack_in"].numel() * 8, host["pack_out"].numel() * 8
         else:
-            # the batch arrives by chunks of one launch round (grid = 5 CTAs x
+            # the batch arrives by chunks of one launch round (grid = 4 CTAs x
             # 148 SMs): the kernel waits per chunk for its flag, counts finished
             # systems per chunk, and each chunk's outputs go back as soon as
             # its counter is full
             from paper_2008_11480_b200 import _lib
 
             batch = hin["a"].shape[0]
-            chunk = 5 * torch.cuda.get_device_properties(0).multi_processor_count
+            chunk = 4 * torch.cuda.get_device_properties(0).multi_processor_count
             nchunks = (batch + chunk - 1) // chunk
             if not hasattr(self, "_c2_flags") or self._c2_flags.numel() < nchunks:
                 self._c2_flags = torch.zeros(nchunks, dtype=torch.int32, device="cuda")

@@ -17,9 +17,8 @@
 // load is then the minimum 2 wavefronts and every accumulator store / C load
 // (16 bytes per lane, rows g and g+1 in one quarter-warp) the minimum 4.
 // Slots are 8 KB (NP=32) / 32 KB (NP=64); the ops are reordered to minimise
-// live slots (32 x 32 products may overwrite their own operands), so five
-// 32 x 32 systems fit per SM (config 2: 5 slots, 42 KB per CTA); systems are
-// claimed dynamically by the CTAs.
+// live slots (32 x 32 products may overwrite their own operands: config 2
+// needs 5 slots, 42 KB per CTA); systems are claimed dynamically by the CTAs.
 #include <algorithm>
 #include <bitset>
 #include <cstdio>
@@ -493,17 +492,17 @@ template <int NP>
 struct Geo {
   static constexpr int SLOT = NP * NP;
 #ifndef SI_RESIDENT_WARPS32
-#define SI_RESIDENT_WARPS32 2
+#define SI_RESIDENT_WARPS32 4
 #endif
 #ifndef SI_RESIDENT_WARPS64
 #define SI_RESIDENT_WARPS64 16
 #endif
-  // NP=32: two warps with 32x16 warp tiles (4x2 DMMA tiles: 0.75 fragment
-  // loads per DMMA and 8 independent accumulator chains per warp); with four
-  // CTAs per SM the shared-memory pipe and DMMA dependency latency, not warp
-  // count, are the limits (measured: 8 warps of 8x16 tiles 1739 iters/s,
-  // 4 warps of 16x16 2430, 2 warps of 32x16 2511).  NP=64 runs one CTA per
-  // SM: 16 warps hide latency.
+  // NP=32: four warps with 16x16 warp tiles (2x2 DMMA tiles), four CTAs per
+  // SM (registers: 122 per thread) -- 16 warps, 4 per SM sub-partition, all
+  // CTAs alike.  Measured at C2 with dynamic system claims (tools/c2time.py):
+  // 4 warps x 4 CTAs 2746 iters/s, x 5 CTAs (95 registers) 2722, x 3 CTAs
+  // 2603; 2 warps of 32x16 x 5 CTAs 2680, x 4 CTAs 2625; 1 warp of 32x32
+  // 1866.  NP=64 runs one CTA per SM: 16 warps hide latency.
   static constexpr int WARPS = NP == 32 ? SI_RESIDENT_WARPS32 : SI_RESIDENT_WARPS64;
   static constexpr int THREADS = WARPS * 32;
   // warp tile: a single warp owns the whole NP x NP product; otherwise the
@@ -654,10 +653,10 @@ __device__ __forceinline__ void gemm_op(const double* A, const double* B, const 
 }
 
 template <int NP>
-// 32 x 32 systems: five CTAs per SM fit in shared memory, so registers must
-// not be the tighter limit (<= 204 per thread; ptxas settles at 160)
+// 32 x 32 systems: four CTAs of four warps per SM (<= 128 registers per
+// thread; five fit in shared memory but measured slower, see Geo)
 #ifndef SI_RESIDENT_MINB32
-#define SI_RESIDENT_MINB32 5
+#define SI_RESIDENT_MINB32 4
 #endif
 __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB32 : 1)
     resident_kernel(BatchArgs p) {
