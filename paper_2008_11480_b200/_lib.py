@@ -106,6 +106,8 @@ class NativeUnavailable(RuntimeError):
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     """Load the shared library and declare every prototype (no GPU needed)."""
     global _lib
+    if _lib is not None and path == LIB_PATH:  # loaded: no lock on the hot path
+        return _lib
     with _lib_lock:
         if _lib is not None:
             return _lib
@@ -160,6 +162,10 @@ def handle(device: int | None = None) -> int:
     """Per-device library handle (side streams, events); the library's
     temporaries are allocated from PyTorch's caching allocator so one allocator
     owns all device memory."""
+    if _handles:  # fast path: a handle exists, so CUDA and the library are up
+        h = _handles.get(torch.cuda.current_device() if device is None else int(device))
+        if h is not None:
+            return h
     if not torch.cuda.is_available():
         raise NativeUnavailable("no CUDA device visible: the seriesinv B200 path has no CPU fallback")
     lib = load_library()
@@ -191,7 +197,15 @@ def call(name: str, *args) -> None:
         _raise(st, name)
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_ptr(device: torch.device | None = None) -> int:
+    """The current CUDA stream of ``device`` (default: the current device) as a
+    raw pointer; the raw accessor avoids building a Stream object per call."""
+    if _raw_stream is not None:
+        idx = device.index if isinstance(device, torch.device) else device
+        return _raw_stream(torch.cuda.current_device() if idx is None else int(idx))
     return torch.cuda.current_stream(device).cuda_stream
 
 

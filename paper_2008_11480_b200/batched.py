@@ -88,10 +88,12 @@ def batched_composite_richardson(a, b, precond, residual, p, f, theta, rates, or
 
 
 def batched_ns_richardson(a, b, p, f, theta, order: int, iters: int, plan=None,
-                          ctr: MulCounter | None = None):
+                          ctr: MulCounter | None = None, out=None):
     """``iters`` x { plain Richardson with P_k; ns_step(order, plan) } for a batch of
     n x n systems (n <= 64) in one launch; BASELINE config 1 is batch = 1, n = 64,
-    order 3.  Returns new (P, F, theta); inputs untouched."""
+    order 3.  Returns new (P, F, theta); inputs untouched.  ``out`` (optional):
+    caller-owned contiguous device tensors (P', F', theta') of the input shapes
+    to write into, e.g. views of one packed buffer for a single read-back."""
     from .series_toolkit import encode_plan
 
     a, b = as_device(a), as_device(b)
@@ -110,7 +112,17 @@ def batched_ns_richardson(a, b, p, f, theta, order: int, iters: int, plan=None,
     p_in = as_device(p).reshape(batch, n, n).contiguous()
     f_in = as_device(f).reshape(batch, n, n).contiguous()
     th_in = as_device(theta).reshape(batch, n).contiguous()
-    p_io, f_io, th_io = torch.empty_like(p_in), torch.empty_like(f_in), torch.empty_like(th_in)
+    if out is None:
+        p_io, f_io, th_io = torch.empty_like(p_in), torch.empty_like(f_in), torch.empty_like(th_in)
+    else:
+        p_io, f_io, th_io = out
+        for o, ref in ((p_io, p_in), (f_io, f_in), (th_io, th_in)):
+            if (not isinstance(o, torch.Tensor) or o.numel() != ref.numel() or
+                    o.dtype != torch.float64 or o.device != ref.device or not o.is_contiguous()):
+                raise ValueError("out tensors must be contiguous float64 device tensors "
+                                 "of the input shapes")
+        p_io, f_io, th_io = (p_io.view(p_in.shape), f_io.view(f_in.shape),
+                             th_io.view(th_in.shape))
     code, consts = encode_plan(plan) if plan is not None else ([], [])
     buf = _lib.counter_buf()
     _lib.call("si_batched_ns_richardson_ex", _lib.handle(a.device.index), batch, n, a.data_ptr(),

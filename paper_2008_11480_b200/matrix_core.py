@@ -80,6 +80,13 @@ def _device() -> torch.device:
 
 def as_device(x, device: torch.device | None = None) -> torch.Tensor:
     """float64, contiguous, on the current CUDA device (copies only if needed)."""
+    # fast path (small-system calls are host-bound): already a contiguous
+    # float64 tensor on the current device -- returned as is, no dispatch
+    if (isinstance(x, torch.Tensor) and x.dtype == torch.float64 and x.is_cuda
+            and x.is_contiguous()
+            and x.device.index == (torch.cuda.current_device() if device is None
+                                   else device.index)):
+        return x
     dev = device or _device()
     if isinstance(x, torch.Tensor):
         return x.to(device=dev, dtype=torch.float64).contiguous()

@@ -105,3 +105,27 @@ def test_c_host_demo():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "bad-call status=-1" in out.stdout
+
+
+def test_batched_ns_richardson_into_packed_outputs():
+    """``out=`` views of one packed buffer (the single read-back of bench.py's C1
+    e2e path) hold exactly what the default outputs hold; bad ``out`` raises."""
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import configs
+
+    a_np, b_np = configs.c1_dense_small()
+    a, b = P.as_device(a_np), P.as_device(b_np)
+    alpha = float(torch.max(torch.sum(torch.abs(a), dim=1)))
+    eye = torch.eye(64, dtype=torch.float64, device="cuda")
+    p0, f0, t0 = eye / alpha, eye - a / alpha, torch.zeros_like(b)
+    ref = P.batched_ns_richardson(a, b, p0, f0, t0, 3, 7)
+    packed = torch.full((2 * 64 * 64 + 64,), float("nan"), dtype=torch.float64, device="cuda")
+    got = P.batched_ns_richardson(a, b, p0, f0, t0, 3, 7,
+                                  out=(packed[:4096], packed[4096:8192], packed[8192:]))
+    torch.cuda.synchronize()
+    for x, y in zip(got, ref):
+        assert torch.equal(x, y)
+    assert torch.equal(packed[:4096].view(64, 64), ref[0])
+    assert torch.equal(packed[8192:], ref[2])
+    with pytest.raises(ValueError):
+        P.batched_ns_richardson(a, b, p0, f0, t0, 3, 7, out=(packed[:100], packed, packed))
