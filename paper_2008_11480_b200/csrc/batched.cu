@@ -1338,6 +1338,8 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
     if (env) {
       cl = std::atoi(env);
       if (cl != 0 && cl != 2 && cl != 4 && cl != 8) cl = 0;
+    } else if (batch * 8 <= num_sms_b()) {
+      cl = 8;  // C1: 8-row blocks per SM, 192k vs 187k iters/s with 4 SMs
     } else if (batch * 4 <= num_sms_b()) {
       cl = 4;
     }
