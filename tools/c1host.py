@@ -1,3 +1,5 @@
+"""Host cost of one config-1 batched call (diagnostics): the Python wrapper
+vs the C-ABI call alone.  python tools/c1host.py"""
 import sys, time, torch
 sys.path.insert(0, ".")
 import paper_2008_11480_b200 as P
@@ -30,4 +32,3 @@ for _ in range(200): _lib.call("si_batched_ns_richardson_ex", *args)
 hc = time.perf_counter() - t
 torch.cuda.synchronize()
 print(f"C-ABI call alone {hc/200*1e6:.1f} us")
-fn = _lib.lib().si_batched_ns_richardson_ex if hasattr(_lib, "lib") else None

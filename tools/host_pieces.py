@@ -1,3 +1,4 @@
+"""Per-piece host cost of the Python call path (diagnostics)."""
 import sys, time, torch, ctypes
 sys.path.insert(0, ".")
 import paper_2008_11480_b200 as P
