@@ -777,36 +777,39 @@ class Workload:
         return host
 
 
-def cpu_sample(n: int, flops_step: float, reps: int = 1):
-    """Oracle (numpy, all host threads) on a bounded sample: one full-size n x n x n
-    product of the step's DAG (oracle.mm), extrapolated by the DAG's FLOP ratio."""
+def cpu_part_sample(n: int, a=None, precond=None, residual=None):
+    """Bounded CPU sample for our arm's ``cpu_baseline`` (c4/c5, ~10-20 s): the
+    rate-2 part of the composite step executed through the oracle at full n --
+    T = B S^-1 + S^-1 (geometric_apply, st:432-457) and Gamma = I - T A
+    (ns:206-210), two n^3 products with the reference's n^2 temporaries
+    (identity, add, subtract).  Returns (seconds, products executed)."""
     import numpy as np
 
     from oracle import seriesinv_oracle as O
 
-    rng = np.random.default_rng(1)
-    x = rng.standard_normal((n, n))
-    y = rng.standard_normal((n, n))
-    ts = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        O.mm(x, y, O.Counter())
-        ts.append(time.perf_counter() - t0)
-    t = min(ts)
-    step_s = t * flops_step / (2.0 * n**3)
-    return step_s, t
+    if a is None:
+        rng = np.random.default_rng(1)
+        a = rng.standard_normal((n, n))
+        precond = np.eye(n) / n
+        residual = np.eye(n) - a / n
+    ctr = O.Counter()
+    O.mm(a[:256, :256], a[:256, :256], ctr)  # spin up the BLAS thread pool
+    t0 = time.perf_counter()
+    t = O.geometric_apply(residual, precond, 2, a, ctr)
+    gamma = np.eye(n) - O.mm(t, a, ctr)
+    dt = time.perf_counter() - t0
+    del t, gamma
+    return dt, 2
 
 
-def reference_step_seconds(cfg: str, n: int, flops: float, batch: int = 16384):
-    """Seconds the CPU oracle needs for ONE bench step of `cfg` (the same unit as
-    our arm's step), measured on a bounded sample; returns (seconds, description).
+def reference_step_seconds(cfg: str, n: int, batch: int = 16384):
+    """c1-c3: seconds the CPU oracle needs for ONE bench step of `cfg` (the same
+    unit as our arm's step), executed on a bounded sample; returns (seconds,
+    description).
 
     c1: the whole 30-iteration run, executed (milliseconds; best of 20 runs).
     c2: 50 iterations of 64 of the systems, executed, scaled to the full batch.
-    c3: one full-size iteration (n=4096: plain Richardson + h8 ns_step), executed.
-    c4/c5: a full iteration is minutes of CPU: one full-size n^3 product of the
-        step DAG, extrapolated by the DAG's FLOP ratio (c5 sampled at n=16384
-        and scaled by n^3)."""
+    c3: one full-size iteration (n=4096: plain Richardson + h8 ns_step), executed."""
     import numpy as np
 
     from oracle import seriesinv_oracle as O
@@ -848,11 +851,90 @@ def reference_step_seconds(cfg: str, n: int, flops: float, batch: int = 16384):
         th = O.plain_richardson(th, st.estimate, sp.matrix, b, st.ctr)
         st = O.ns_step(st, sp.matrix, plan)
         return time.perf_counter() - t0, f"one full-size iteration (n={n}) through the oracle"
-    sample_n = min(n, 16384)
-    s, t = cpu_sample(sample_n, flops * (sample_n / n) ** 3, reps=2)
-    s *= (n / sample_n) ** 3
-    return s, (f"one {sample_n}^3 FP64 product through oracle.mm in {t:.2f} s, extrapolated "
-               f"by the step DAG's FLOP ratio ({flops:.4e} FLOP/step)")
+    raise ValueError(cfg)
+
+
+def reference_executed_steps(cfg: str, n: int, max_steps: int, budget_s: float):
+    """c4/c5 reference arm: FULL steps of the reference DAG executed through the
+    oracle on the host cores (no extrapolation for c4).
+
+    c4: plain Richardson (64 RHS) + composite_step((2,3,4,5), 2) at n (the
+        bench workload itself; ~2 min per step on 16 cores), from the
+        config's initial state.
+    c5: one steady-state recursive step (richardson.py:111-189, Horner, 34
+        products) at min(n, 16384) -- a full n=32768 step is ~25 min of CPU --
+        on the config-5 recipe at that size, from a synthetic carried state
+        (S^-1 / B standing in for G, L / F, R and for omega / N: the products
+        are dense and their cost does not depend on the values); the time is
+        scaled by (n / 16384)^3 and labelled.
+    Steps run while the next one still fits in ``budget_s`` (at least one, at
+    most ``max_steps``).  Returns (step seconds list, description)."""
+    import numpy as np
+
+    from oracle import seriesinv_oracle as O
+    from paper_2008_11480_b200 import configs
+
+    times = []
+    if cfg == "c4":
+        t_setup = time.perf_counter()
+        a, b = configs.c4_householder(n=n, rhs=64)
+        sp = O.split_scalar(a, O.inf_norm(a) / 2.0)
+        del a
+        st = O.initial_series(sp, 0, 1, 2)
+        theta = np.zeros_like(b)
+        setup = time.perf_counter() - t_setup
+        O.mm(sp.matrix[:256, :256], sp.matrix[:256, :256], O.Counter())  # BLAS pool warm
+        t_all = time.perf_counter()
+        while True:
+            t0 = time.perf_counter()
+            theta = O.plain_richardson(theta, st.estimate, sp.matrix, b, st.ctr)
+            st = O.composite_step(st, sp.matrix, sp, (2, 3, 4, 5), 2)
+            times.append(time.perf_counter() - t0)
+            spent = time.perf_counter() - t_all
+            if len(times) >= max_steps or spent + times[-1] > budget_s:
+                break
+        mmm = st.ctr.mmm // len(times)
+        return times, (f"{len(times)} full step(s) executed at n={n} through the oracle "
+                       f"(plain Richardson, 64 RHS + composite_step (2,3,4,5) order_n=2: "
+                       f"{mmm} n^3 products + 2 n^2 r products each, the reference's n^2 "
+                       f"temporaries included; inputs built on the host in {setup:.0f} s, untimed)")
+    if cfg == "c5":
+        sn = min(n, 16384)
+        m = int(round(sn * 40000 / 32768))
+        rng = np.random.default_rng(0)
+        g = rng.standard_normal((m, sn))
+        b = rng.standard_normal((sn, 256))
+        a = g.T @ g / m + 1e-3 * np.eye(sn)
+        del g
+        sp = O.split_scalar(a, O.inf_norm(a) / 2.0)
+        del a
+        ctr = O.Counter()
+        inner = O.DoubleNS(sp.precond.copy(), sp.residual.copy(), sp.precond.copy(),
+                           sp.residual.copy(), 1, 16, 1, ctr)
+        st = O.Rich(np.zeros_like(b), inner, 16, sp.precond.copy(), sp.precond.copy(), 1, ctr)
+        O.mm(sp.matrix[:256, :256], sp.matrix[:256, :256], O.Counter())
+        t_all = time.perf_counter()
+        while True:
+            c0 = ctr.mmm
+            t0 = time.perf_counter()
+            st = O.richardson_recursive_step(st, sp.matrix, b)
+            times.append((time.perf_counter() - t0) * (n / sn) ** 3)
+            products = ctr.mmm - c0
+            spent = time.perf_counter() - t_all
+            if len(times) >= max_steps or spent + times[-1] * (sn / n) ** 3 > budget_s:
+                break
+        scale = "" if sn == n else f", scaled by (n/{sn})^3 to n={n} (extrapolated)"
+        return times, (f"{len(times)} steady-state recursive step(s) (Horner order 16, {products} "
+                       f"n^3 products + 2 n^2 r products, r=256) executed at n={sn} through the "
+                       f"oracle from a synthetic carried state{scale}")
+    raise ValueError(cfg)
+
+
+def config_obj(cfg: str, n: int, batch: int = 16384) -> dict:
+    """The `config` object: identical in both arms (the parallelism / L2 /
+    sampling details are top-level keys)."""
+    return {"workload": workload_desc(cfg, n, batch), "n": n,
+            "rhs": {"c4": 64, "c5": 256, "c2": 1, "c1": 1, "c3": 1}[cfg]}
 
 
 # --------------------------------------------------------------------------- arms
@@ -874,29 +956,42 @@ def run_reference(args):
     w.iters_per_step = {"c1": 30, "c2": 50}.get(cfg, 1)
     flops = w.flops()
     cores = use_all_host_threads()
-    # each step: a bounded sample of one bench step of the workload (see
-    # reference_step_seconds for what is executed and what is extrapolated)
-    step_times, sample = [], ""
-    for i in range(args.warmup + args.steps):
-        s, sample = reference_step_seconds(cfg, w.n, flops, batch=w.batch)
-        if i >= args.warmup:
-            step_times.append(s)
+    if cfg in ("c4", "c5"):
+        # full reference steps, executed (c5: at n=16384, scaled by n^3)
+        step_times, sample = reference_executed_steps(cfg, w.n, args.steps, args.ref_budget)
+        steps_timed, warm = len(step_times), 0
+        executed = {"executed_iterations": len(step_times), "steps_requested": args.steps,
+                    "warmup_requested": args.warmup,
+                    "note": ("each timed step is one full reference step; steps run while the "
+                             f"next fits in --ref-budget {args.ref_budget:.0f} s, so 'steps' is "
+                             "the executed count (no warm-up step: a BLAS warm-up product only)")}
+    else:
+        # each step: a bounded sample of one bench step of the workload (see
+        # reference_step_seconds for what is executed)
+        step_times, sample = [], ""
+        for i in range(args.warmup + args.steps):
+            s, sample = reference_step_seconds(cfg, w.n, batch=w.batch)
+            if i >= args.warmup:
+                step_times.append(s)
+        steps_timed, warm = args.steps, args.warmup
+        executed = {"executed_iterations": args.steps * w.iters_per_step}
     step_s = statistics.mean(step_times)
     value = w.iters_per_step / step_s
     sample = f"{sample}; numpy/OpenBLAS with {cores} host threads"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": steps_timed, "warmup": warm,
         "ms_per_step": step_s * 1e3, "iters_per_step": w.iters_per_step,
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(cfg, w.n, w.batch), "n": w.n,
-                   "parallelism": f"host CPU, {cores} threads (rank 0 only)",
-                   "sample": "executed" if cfg in ("c1", "c2", "c3") else "extrapolated"},
+        "config": config_obj(cfg, w.n, w.batch),
+        "parallelism": f"host CPU, {cores} threads (rank 0 only)",
         "tflops": flops / step_s / 1e12,
         "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_seconds": step_times,
+        **executed,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -925,6 +1020,83 @@ def sharded_e2e(w, args, world, stream):
     return {"value": ksteps / (e_ms / 1e3), "unit": "iters/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": ksteps,
             "bytes": "per rank (A, S^-1, B, b, theta replicated; G, F row blocks)"}
+
+
+def our_cpu_baseline(w, flops: float) -> dict:
+    """`cpu_baseline` of our arm (rank 0, N=1): the oracle on the host cores on a
+    bounded sample of the same workload (10-30 s of CPU).  c1-c3: the executed
+    samples of reference_step_seconds; c4/c5: the rate-2 part of the composite
+    step (2 full-size products with the reference's n^2 temporaries) executed,
+    scaled to the reference DAG's step by FLOPs (c5: Horner, 34 products; its
+    sample at n=16384 on random matrices, scaled by n^3)."""
+    cores = use_all_host_threads()
+    if w.cfg in ("c1", "c2", "c3"):
+        s, desc = reference_step_seconds(w.cfg, w.n, batch=getattr(w, "batch", 16384))
+    else:
+        if w.cfg == "c4":
+            host = [t.cpu().numpy() for t in (w.sp.matrix, w.sp.precond, w.sp.residual)]
+            t, k = cpu_part_sample(w.n, *host)
+            del host
+            ref_flops, sn = flops, w.n
+        else:
+            sn = min(w.n, 16384)
+            t, k = cpu_part_sample(sn)
+            ref_flops = 34 * 2.0 * w.n**3 + 2 * 2.0 * w.n * w.n * w.r
+        s = t / (k * 2.0 * sn**3) * ref_flops
+        desc = (f"rate-2 part of the composite step ({k} products of {sn}^3 with the reference's "
+                f"n^2 temporaries) executed in {t:.1f} s, scaled by the reference step DAG's "
+                f"FLOPs ({ref_flops:.4e}/step) -- extrapolated")
+    return {"value": w.iters_per_step / s, "unit": "iters/s", "cores": cores, "kind": "port",
+            "sample": f"{desc}; numpy/OpenBLAS, all host threads"}
+
+
+def config_of(w) -> dict:
+    """Our arm's `config`: the reference arm's object, except for the opt-in
+    hoisted variant (a different DAG, labelled in its workload string)."""
+    c = config_obj(w.cfg, w.n, getattr(w, "batch", 16384))
+    if w.hoist:
+        c["workload"] = w.workload
+    return c
+
+
+def layout_note(w) -> str:
+    """The multi-GPU layout details appended to the workload string (e.g. the
+    GPU groups of the parts mapping) go to `parallelism`, not `config`."""
+    base = workload_desc(w.cfg, w.n, getattr(w, "batch", 16384))
+    extra = w.workload[len(base):].strip() if w.workload.startswith(base) and not w.hoist else ""
+    return f"{extra} " if extra else ""
+
+
+def rank_info(w, args, world: int, rank: int, local: int) -> dict:
+    """One self-describing line per rank (stderr): device, peer access to the
+    other GPUs, exchange bytes pulled, NCCL ranks -- so a multi-GPU run
+    verifies its own wiring."""
+    import torch
+
+    info = {"rank": rank, "local_rank": local, "world": world}
+    try:
+        dev = torch.cuda.current_device()
+        props = torch.cuda.get_device_properties(dev)
+        info["device"] = {"index": dev, "name": props.name,
+                          "pci_bus_id": getattr(props, "pci_bus_id", None),
+                          "uuid": str(getattr(props, "uuid", ""))}
+        info["peer_access"] = {j: torch.cuda.can_device_access_peer(dev, j)
+                               for j in range(torch.cuda.device_count()) if j != dev}
+    except RuntimeError as exc:
+        info["device"] = f"unavailable: {exc}"
+    s = w.sharded or {}
+    comm = s.get("comm")
+    if comm is not None:
+        info["comm"] = type(comm).__name__
+        info["bytes_pulled"] = getattr(comm, "bytes_gathered", None)
+        info["gathers"] = getattr(comm, "seq", None)
+    if world > 1:
+        import torch.distributed as dist
+
+        info["backend"] = dist.get_backend()
+        info["nccl_nranks"] = dist.get_world_size() if dist.get_backend() == "nccl" else 0
+    info["share_gpu"] = SHARE_GPU
+    return info
 
 
 def run_ours(args):
@@ -961,6 +1133,8 @@ def run_ours(args):
     _lib.call("si_profile_end", h, ctypes.byref(g_ms), ctypes.byref(g_fl), ctypes.byref(g_n),
               ctypes.byref(launches))
     clocks = sampler.stop()
+    print("rank-info " + json.dumps(rank_info(w, args, world, rank, local)), file=sys.stderr,
+          flush=True)
     barrier(world)
     ms = e0.elapsed_time(e1)
     ms_max = max_over_ranks(ms, world)
@@ -1019,15 +1193,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.hoist:
-        use_all_host_threads()
-        # the oracle on the reference DAG (c5: Horner, 34 products per step)
-        ref_flops = flops
-        if args.config == "c5":
-            ref_flops = 34 * 2.0 * w.n**3 + 2 * 2.0 * w.n * w.n * w.r
-        s, desc = reference_step_seconds(args.config, w.n, ref_flops,
-                                         batch=getattr(w, "batch", 16384))
-        cpu = {"value": w.iters_per_step / s, "unit": "iters/s", "cores": host_cores(),
-               "kind": "port", "sample": f"{desc}; numpy/OpenBLAS, all host threads"}
+        cpu = our_cpu_baseline(w, flops)
 
     if rank == 0:
         line = {
@@ -1037,14 +1203,14 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded PCG64 draws, SURVEY Appendix A recipe)",
-            "config": {"workload": w.workload, "n": w.n,
-                       "parallelism": (f"composite parts on GPU groups x{world} (NCCL p2p tree)"
-                                       if w.sharded is not None and "gc" in w.sharded
-                                       else f"block-row x{world} ({_COMM_LABEL[args.comm]})"
-                                       if w.sharded is not None
-                                       else f"batch split x{world} (no communication)" if w.split_batch
-                                       else (f"replicas x{world}" if world > 1 else "single-gpu")),
-                       "l2": l2_note(w)},
+            "config": config_of(w),
+            "parallelism": layout_note(w) + (f"composite parts on GPU groups x{world} (NCCL p2p tree)"
+                            if w.sharded is not None and "gc" in w.sharded
+                            else f"block-row x{world} ({_COMM_LABEL[args.comm]})"
+                            if w.sharded is not None
+                            else f"batch split x{world} (no communication)" if w.split_batch
+                            else (f"replicas x{world}" if world > 1 else "single-gpu")),
+            "l2": l2_note(w),
             "tflops": tflops,
             "tflops_frac_of_dmma_peak": tflops / (world * peak.value),
             "roofline": resident_roofline(w, tflops / world, step_s, peak.value) if w.cfg in ("c1", "c2") else
@@ -1084,10 +1250,38 @@ def main():
     ap.add_argument("--shard", choices=["rows", "parts"], default="rows",
                     help="c4 at N > 1: block-row sharding of every product (rows) or the "
                          "composite parts on GPU groups + one tree reduction (parts)")
+    ap.add_argument("--ref-budget", type=float, default=300.0,
+                    help="--impl reference, c4/c5: wall-clock budget (s) for the executed "
+                         "full-size CPU steps (at least one is always executed)")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        # not launched by torchrun: start the N ranks ourselves (one per GPU)
+        return launch_ranks(args.gpus)
+    if env_world is not None and int(env_world) != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={env_world}: "
+                                   "launch one rank per GPU with --nproc-per-node equal to --gpus"}),
+              flush=True)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
+
+
+def launch_ranks(n: int) -> int:
+    """`bench.py --gpus N` without torchrun: re-launch this command under
+    torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

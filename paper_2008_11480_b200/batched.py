@@ -74,6 +74,10 @@ def batched_composite_richardson(a, b, precond, residual, p, f, theta, rates, or
         flags_ptr = flags.data_ptr()
     if chunk_done is not None and (chunk_done.dtype != torch.int32 or not chunk_done.is_cuda):
         raise ValueError("chunk_done must be a CUDA int32 tensor")
+    if chunk_done is not None and input_chunks is None:
+        raise ValueError("chunk_done needs input_chunks (only the gated kernel raises it)")
+    if input_chunks is not None and iters < 1:
+        raise ValueError("a gated call (input_chunks) needs iters >= 1")
     _lib.call("si_batched_composite_richardson_gated", _lib.handle(a.device.index), batch, n,
               a.data_ptr(), b.data_ptr(), precond.data_ptr(), residual.data_ptr(), len(rates),
               _lib.i32_array(list(rates)), _lib.i32_array(code), _lib.i64_array(offsets),

@@ -525,8 +525,31 @@ struct Geo {
   }
 };
 
+// Inputs of a gated launch are written by copy engines while the kernel runs:
+// they are read with coherent (relaxed, gpu-scope) loads after the chunk flag
+// was acquired -- the non-coherent __ldg path is only defined for data that
+// stays read-only for the kernel's whole lifetime (the ungated case).
+__device__ __forceinline__ double2 ld_in2(const double2* p, bool coherent) {
+  if (coherent) {
+    double2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    return v;
+  }
+  return __ldg(p);
+}
+__device__ __forceinline__ double ld_in(const double* p, bool coherent) {
+  if (coherent) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+  }
+  return __ldg(p);
+}
+
 template <int NP>
-__device__ void load_mat(double* dst, const double* __restrict__ src, int n) {
+__device__ void load_mat(double* dst, const double* __restrict__ src, int n,
+                         bool coherent = false) {
   using G = Geo<NP>;
   if (n == NP) {
     // all of this thread's 16-byte loads in flight before the first store
@@ -534,7 +557,7 @@ __device__ void load_mat(double* dst, const double* __restrict__ src, int n) {
     const double2* s2 = reinterpret_cast<const double2*>(src);
     double2 v[PER];
 #pragma unroll
-    for (int j = 0; j < PER; ++j) v[j] = __ldg(s2 + threadIdx.x + j * G::THREADS);
+    for (int j = 0; j < PER; ++j) v[j] = ld_in2(s2 + threadIdx.x + j * G::THREADS, coherent);
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       const int i = threadIdx.x + j * G::THREADS;
@@ -544,7 +567,7 @@ __device__ void load_mat(double* dst, const double* __restrict__ src, int n) {
   } else {
     for (int i = threadIdx.x; i < NP * NP; i += G::THREADS) {
       const int r = i / NP, c = i % NP;
-      dst[G::idx(r, c)] = (r < n && c < n) ? src[r * n + c] : 0.0;
+      dst[G::idx(r, c)] = (r < n && c < n) ? ld_in(src + r * n + c, coherent) : 0.0;
     }
   }
 }
@@ -703,14 +726,16 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
       }
       __syncthreads();
     }
-    load_mat<NP>(mslot(p.sA), p.a + sys * nn, n);
-    if (p.sP >= 0) load_mat<NP>(mslot(p.sP), p.precond + sys * nn, n);
-    if (p.sB >= 0) load_mat<NP>(mslot(p.sB), p.residual + sys * nn, n);
-    load_mat<NP>(mslot(p.sG), p.p_in + sys * nn, n);
-    load_mat<NP>(mslot(p.sF), p.f_in + sys * nn, n);
+    const bool gated = p.chunk_ready != nullptr;
+    load_mat<NP>(mslot(p.sA), p.a + sys * nn, n, gated);
+    if (p.sP >= 0) load_mat<NP>(mslot(p.sP), p.precond + sys * nn, n, gated);
+    if (p.sB >= 0) load_mat<NP>(mslot(p.sB), p.residual + sys * nn, n, gated);
+    load_mat<NP>(mslot(p.sG), p.p_in + sys * nn, n, gated);
+    load_mat<NP>(mslot(p.sF), p.f_in + sys * nn, n, gated);
     if (threadIdx.x < NP) {
-      vslot(p.sT)[threadIdx.x] = threadIdx.x < n ? p.theta_in[sys * n + threadIdx.x] : 0.0;
-      vslot(p.sb)[threadIdx.x] = threadIdx.x < n ? p.b[sys * n + threadIdx.x] : 0.0;
+      vslot(p.sT)[threadIdx.x] =
+          threadIdx.x < n ? ld_in(p.theta_in + sys * n + threadIdx.x, gated) : 0.0;
+      vslot(p.sb)[threadIdx.x] = threadIdx.x < n ? ld_in(p.b + sys * n + threadIdx.x, gated) : 0.0;
     }
     __syncthreads();
     const int64_t nxt = s_next;  // written by thread 0 before the barrier above
@@ -725,8 +750,8 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
       const double2* sb2 = reinterpret_cast<const double2*>(p.residual + s * nn);
 #pragma unroll
       for (int j = 0; j < PF; ++j) {
-        pf_p[j] = __ldg(sp2 + threadIdx.x + j * G::THREADS);
-        pf_b[j] = __ldg(sb2 + threadIdx.x + j * G::THREADS);
+        pf_p[j] = ld_in2(sp2 + threadIdx.x + j * G::THREADS, gated);
+        pf_b[j] = ld_in2(sb2 + threadIdx.x + j * G::THREADS, gated);
       }
     };
     if (prefetch && (first || p.chunk_ready)) issue(sys);
@@ -806,7 +831,7 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
             }
           }
         } else if (o.kind == OP_LOAD) {
-          load_mat<NP>(mslot(o.dst), (o.mode ? p.residual : p.precond) + sys * nn, n);
+          load_mat<NP>(mslot(o.dst), (o.mode ? p.residual : p.precond) + sys * nn, n, gated);
         } else if (o.mode) {  // LIN over vectors
           if (threadIdx.x < NP) {
             double acc = 0.0;

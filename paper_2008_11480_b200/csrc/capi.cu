@@ -201,13 +201,15 @@ int si_gemm_panels(si_handle h, int64_t m, int64_t n, int64_t k, double alpha, c
     pw.ready = ready_flags;
     pw.epoch = epoch;
     pw.npanels = npanels;
-    for (int p = 0; p <= npanels; ++p) {
-      need(panel_bounds[p] >= 0 && panel_bounds[p] <= k, "panel bound out of range");
-      need(p == 0 || panel_bounds[p] >= panel_bounds[p - 1], "panel bounds not ascending");
-      pw.bounds[p] = (int)panel_bounds[p];
+    if (npanels > 0) {  // npanels == 0 is the ungated product; its arrays may be NULL
+      for (int p = 0; p <= npanels; ++p) {
+        need(panel_bounds[p] >= 0 && panel_bounds[p] <= k, "panel bound out of range");
+        need(p == 0 || panel_bounds[p] >= panel_bounds[p - 1], "panel bounds not ascending");
+        pw.bounds[p] = (int)panel_bounds[p];
+      }
+      need(panel_bounds[0] == 0 && panel_bounds[npanels] == k,
+           "panels must cover the k rows of B");
     }
-    need(npanels == 0 || (panel_bounds[0] == 0 && panel_bounds[npanels] == k),
-         "panels must cover the k rows of B");
     Call call(h, stream, counters);
     MV a = view(const_cast<double*>(A), m, k, lda), b = view(const_cast<double*>(B), k, n, ldb);
     MV d = view(D, m, n, ldd);
@@ -824,6 +826,11 @@ int si_batched_composite_richardson_gated(
     uint32_t* chunk_done, int64_t* counters, void* stream) {
   return guard([&] {
     need(!chunk_ready || chunk >= 1, "chunk must be >= 1");
+    // done counters are bumped by the gated kernel only: without input flags
+    // (or with no iteration to run) nothing would ever raise them and a copy
+    // stream waiting on them (si_stream_wait_u32) would hang.
+    need(!chunk_done || chunk_ready, "chunk_done needs chunk_ready");
+    need(!chunk_ready || iters >= 1, "a gated call needs iters >= 1");
     need(h && a && b && precond && residual && rates && p_in && f_in && theta_in && p_out &&
              f_out && theta_out,
          "null pointer");

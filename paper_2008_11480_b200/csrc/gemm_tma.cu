@@ -477,13 +477,7 @@ cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& 
   }
   const int M = (int)D.rows, N = (int)D.cols, K = (int)A.cols;
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  int grid = tiles < num_sms() ? tiles : num_sms();
-  // SI_GEMM_MAX_CTAS (tests only): cap the persistent grid so that two
-  // panel-gated products of different virtual ranks can be resident together
-  if (const char* cap = std::getenv("SI_GEMM_MAX_CTAS")) {
-    const int c = std::atoi(cap);
-    if (c > 0 && c < grid) grid = c;
-  }
+  const int grid = tiles < num_sms() ? tiles : num_sms();
   PanelWait gate, gate_a;
   if (pw && pw->ready && pw->npanels > 0) gate = *pw;
   if (pwa && pwa->ready && pwa->npanels > 0) gate_a = *pwa;

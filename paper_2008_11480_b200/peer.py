@@ -40,6 +40,7 @@ and each rank uses two streams (compute + copy).
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 
@@ -217,6 +218,13 @@ class PeerComm:
         self.bounds = [s[0] for s in self.splits] + [n]
         self.bytes_gathered = 0
         self.local_copies = 0  # row blocks copied into a slot (not produced in place)
+        # gathers started so far; with SI_PEER_CHECK=1 every start_gather
+        # all-gathers (seq, slot, epoch, cols) over the group and raises if the
+        # ranks paired different slots (slot choice follows lease lifetimes, so
+        # a rank-dependent branch or a held reference could desynchronise them:
+        # the result would be wrong data, not a hang)
+        self.seq = 0
+        self._check = os.environ.get("SI_PEER_CHECK") == "1"
         self._slots: list[_Slot] = []
         self._cs = None
         self._h = _lib.handle(self.device.index)
@@ -307,6 +315,9 @@ class PeerComm:
             src = local.contiguous()
             _lib.call("si_copy_async", h, slot.ptr + self.r0 * row_bytes, src.data_ptr(),
                       (self.r1 - self.r0) * row_bytes, sp)
+        self.seq += 1
+        if self._check:
+            self._check_agreement(b, e, cols)
         for q in range(self.world):
             if q != me:
                 _lib.call("si_stream_write_u32", h,
@@ -336,6 +347,22 @@ class PeerComm:
         events = [done]
         self.bytes_gathered += (self.n - (self.r1 - self.r0)) * row_bytes
         return _Pending(slot, keep, e, events, self.n, cols)
+
+    def _check_agreement(self, slot: int, epoch: int, cols: int) -> None:
+        """Debug mode (SI_PEER_CHECK=1): every rank must pair this gather with
+        the same (slot, epoch); a divergence fails loudly instead of pulling
+        another value's panels."""
+        mine = (self.seq, slot, epoch, cols)
+        if isinstance(self.fabric, IpcFabric):
+            seen = [None] * self.world
+            self.fabric.dist.all_gather_object(seen, mine, group=self.fabric.group)
+        else:  # virtual ranks of one process: compare through the shared fabric
+            shared = getattr(self.fabric, "fabric", self.fabric)  # _LocalView -> LocalFabric
+            log = shared.__dict__.setdefault("_gather_log", {})
+            seen = [log.setdefault(self.seq, mine)]
+        if any(tuple(x) != mine for x in seen):
+            raise RuntimeError(f"peer exchange diverged at gather {self.seq}: rank {self.rank} "
+                               f"has (seq, slot, epoch, cols) = {mine}, the group {seen}")
 
     def _view(self, pend: _Pending) -> torch.Tensor:
         return _tensor(pend.slot.ptr, (pend.rows, pend.cols), self.device, pend.keep)

@@ -47,7 +47,7 @@ def test_bench_two_ranks(cfg, scaling):
     assert d["value"] > 0 and d["ms_per_step"] > 0
     assert d["gpu_launches"] > 0
     if cfg[1] == "c4":
-        assert "block-row x2" in d["config"]["parallelism"]
+        assert "block-row x2" in d["parallelism"]
         assert d["e2e"] and d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
 
 
@@ -56,7 +56,7 @@ def test_bench_grouped_parts(world):
     """c4 with the composite parts on GPU groups (grouped.py) under torchrun."""
     d = _run(["--config", "c4", "--size", "512", "--shard", "parts"], world=world)
     assert d["n_gpus"] == world and d["scaling"] == "strong"
-    assert "parts on GPU groups" in d["config"]["parallelism"]
-    assert f"parts on {min(world, 4)} GPU groups" in d["config"]["workload"]
+    assert "parts on GPU groups" in d["parallelism"]
+    assert f"parts on {min(world, 4)} GPU groups" in d["parallelism"]
     assert d["value"] > 0 and d["gpu_launches"] > 0
     assert d["e2e"] and d["e2e"]["value"] > 0

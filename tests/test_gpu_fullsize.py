@@ -1,0 +1,243 @@
+"""Oracle parity at the benchmarked sizes ("compare on the
+truncated iterations at full n, and on full-length runs at reduced n").
+
+* Config 4 at its full size (n=16384, 64 RHS): two executed iterations of plain
+  Richardson + ``composite_step((2,3,4,5), order_n=2)`` -- the DAG of
+  newton_schulz.py:177-228 -- on the DMMA/TMA kernel the bench times, against
+  the CPU oracle on the box's host cores (about 2 min per iteration).
+* Config 4 full length (40 iterations) and config 5 full length (20 iterations,
+  the reference Horner DAG of richardson.py:111-189 and the opt-in factorised
+  order-16 DAG) at n=4096, every iteration against the oracle.
+* Next to every comparison, the FP64 noise floor measured on the same kernel
+  path (SURVEY 8(c) calibration): the GPU result for a permutation-similar
+  Pi A Pi^T, mapped back, against the GPU result for A.  Each test requires
+  error <= tolerance (1e-10 max(1, kappa/1e4), north_star) and error <= 20 x
+  floor, and logs both (``SI_PARITY_LOG=<file>`` appends the lines; the
+  committed copy is ``profiles/parity_floor_r02.txt``).
+
+Every product at these sizes runs on ``gemm_f64_tma_kernel`` (n >= 128).
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+FACTOR = 20.0
+
+
+def _log(line):
+    print(line)
+    path = os.environ.get("SI_PARITY_LOG")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(line + "\n")
+
+
+def _rel_t(x, ref):
+    """relative Frobenius error of two device tensors (FP64 on the device)."""
+    d = torch.linalg.norm(ref).item()
+    return torch.linalg.norm(x - ref).item() / (d if d > 0 else 1.0)
+
+
+def _rel_np(x, ref):
+    d = np.linalg.norm(ref)
+    return float(np.linalg.norm(x - ref) / (d if d > 0 else 1.0))
+
+
+def _perm_sym(a, perm):
+    return a[perm][:, perm].contiguous()
+
+
+def _unperm_sym(x, perm):
+    out = torch.empty_like(x)
+    idx = torch.as_tensor(perm, device=x.device)
+    out[idx[:, None], idx[None, :]] = x
+    return out
+
+
+def _unperm_rows(x, perm):
+    out = torch.empty_like(x)
+    out[torch.as_tensor(perm, device=x.device)] = x
+    return out
+
+
+def _gpu_c4(a, b, iters):
+    """plain Richardson with P_k, then composite_step((2,3,4,5), 2); yields (P_k, theta_k)."""
+    import paper_2008_11480_b200 as P
+
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False, verify=False)
+    st = P.initial_series(sp, 0, 1, order=2)
+    theta = torch.zeros_like(b)
+    spec = P.CompositeSpec((2, 3, 4, 5))
+    for _ in range(iters):
+        theta = P.plain_richardson(theta, st.estimate, sp.matrix, b, st.ctr)
+        st = P.composite_step(st, sp.matrix, sp, spec, 2)
+        yield st.estimate, theta, st.ctr
+
+
+def test_c4_full_size_two_iterations_vs_oracle():
+    """BASELINE config 4 at n=16384 (the headline bench workload): P_1, P_2 and
+    theta_1, theta_2 (64 RHS) against the oracle run on the host cores."""
+    from oracle import seriesinv_oracle as O
+    from paper_2008_11480_b200 import configs
+
+    n, rhs, iters = 16384, 64, 2
+    a, b = configs.c4_householder_device(n=n, rhs=rhs)
+    lam, _, _ = configs._c4_draws(n, 64, rhs, 0)
+    kappa = float(lam.max() / lam.min())  # A = Q diag(lam) Q^T, Q orthogonal
+    tol = 1e-10 * max(1.0, kappa / 1e4)
+    gpu = []
+    for p, t, ctr in _gpu_c4(a, b, iters):
+        gpu.append((p.cpu().numpy(), t.cpu().numpy()))
+    gpu_ctr = (ctr.mmm, ctr.mvm)
+    # the floor on the same kernel path: Pi A Pi^T, mapped back
+    perm = np.random.default_rng(17).permutation(n)
+    floor = 0.0
+    for k, (p, t, _) in enumerate(_gpu_c4(_perm_sym(a, torch.as_tensor(perm, device=a.device)),
+                                          b[torch.as_tensor(perm, device=a.device)], iters)):
+        pd = torch.as_tensor(gpu[k][0], device=a.device)
+        td = torch.as_tensor(gpu[k][1], device=a.device)
+        floor = max(floor, _rel_t(_unperm_sym(p, perm), pd), _rel_t(_unperm_rows(t, perm), td))
+        del pd, td
+    a_np, b_np = a.cpu().numpy(), b.cpu().numpy()
+    del a, b
+    torch.cuda.empty_cache()
+    osp = O.split_scalar(a_np, O.inf_norm(a_np) / 2.0)
+    del a_np
+    ost = O.initial_series(osp, 0, 1, 2)
+    oth = np.zeros_like(b_np)
+    err = 0.0
+    for k in range(iters):
+        oth = O.plain_richardson(oth, ost.estimate, osp.matrix, b_np, ost.ctr)
+        ost = O.composite_step(ost, osp.matrix, osp, (2, 3, 4, 5), 2)
+        ep, et = _rel_np(gpu[k][0], ost.estimate), _rel_np(gpu[k][1], oth)
+        _log(f"c4 n={n} rhs={rhs} it={k + 1}: P rel err {ep:.3e}, theta rel err {et:.3e}")
+        err = max(err, ep, et)
+        assert ep <= tol and et <= tol, (k, ep, et, tol)
+    assert gpu_ctr == (ost.ctr.mmm, ost.ctr.mvm) == (44, 4)
+    _log(f"c4 n={n} (full size, {iters} executed iterations): kappa={kappa:.3g} "
+         f"err_vs_oracle={err:.3e} gpu_permutation_floor={floor:.3e} tol={tol:.1e}")
+    assert err <= max(FACTOR * floor, 64 * np.finfo(np.float64).eps)
+
+
+def test_c4_recipe_n4096_40_iterations():
+    """Config 4 recipe at n=4096, the full 40 iterations, every iterate vs the oracle."""
+    from oracle import seriesinv_oracle as O
+    from paper_2008_11480_b200 import configs
+
+    n, rhs, iters = 4096, 64, 40
+    a_np, b_np = configs.c4_householder(n=n, rhs=rhs)
+    lam, _, _ = configs._c4_draws(n, 64, rhs, 0)
+    kappa = float(lam.max() / lam.min())
+    tol = 1e-10 * max(1.0, kappa / 1e4)
+    a, b = torch.as_tensor(a_np, device="cuda"), torch.as_tensor(b_np, device="cuda")
+    gpu = []
+    for p, t, ctr in _gpu_c4(a, b, iters):
+        gpu.append((p.clone(), t.clone()))
+    gpu_ctr = (ctr.mmm, ctr.mvm)
+    perm = np.random.default_rng(17).permutation(n)
+    pt = torch.as_tensor(perm, device="cuda")
+    floor = 0.0
+    for k, (p, t, _) in enumerate(_gpu_c4(_perm_sym(a, pt), b[pt], iters)):
+        floor = max(floor, _rel_t(_unperm_sym(p, perm), gpu[k][0]),
+                    _rel_t(_unperm_rows(t, perm), gpu[k][1]))
+    osp = O.split_scalar(a_np, O.inf_norm(a_np) / 2.0)
+    ost = O.initial_series(osp, 0, 1, 2)
+    oth = np.zeros_like(b_np)
+    err = 0.0
+    for k in range(iters):
+        oth = O.plain_richardson(oth, ost.estimate, osp.matrix, b_np, ost.ctr)
+        ost = O.composite_step(ost, osp.matrix, osp, (2, 3, 4, 5), 2)
+        ep = _rel_np(gpu[k][0].cpu().numpy(), ost.estimate)
+        et = _rel_np(gpu[k][1].cpu().numpy(), oth)
+        err = max(err, ep, et)
+        assert ep <= tol and et <= tol, (k, ep, et, tol)
+    assert gpu_ctr == (ost.ctr.mmm, ost.ctr.mvm) == (880, 80)
+    _log(f"c4 n={n} rhs={rhs} ({iters} iterations): kappa={kappa:.3g} err_vs_oracle={err:.3e} "
+         f"gpu_permutation_floor={floor:.3e} tol={tol:.1e}")
+    assert err <= max(FACTOR * floor, 64 * np.finfo(np.float64).eps)
+
+
+def _c5_inputs(n, rhs):
+    """Config 5 recipe at reduced n: A = G^T G / m + 1e-3 I, m = n * 40000 / 32768."""
+    m = int(round(n * 40000 / 32768))
+    rng = np.random.default_rng(0)
+    g = rng.standard_normal((m, n))
+    b = rng.standard_normal((n, rhs))
+    a = g.T @ g / m + 1e-3 * np.eye(n)
+    return (a + a.T) / 2.0, b
+
+
+_C5_ORACLE = {}
+
+
+def _c5_oracle(n, rhs, iters):
+    """The reference Horner DAG on the host, computed once for both variants."""
+    from oracle import seriesinv_oracle as O
+
+    key = (n, rhs, iters)
+    if key not in _C5_ORACLE:
+        a, b = _c5_inputs(n, rhs)
+        osp = O.split_scalar(a, O.inf_norm(a) / 2.0)
+        ost = O.initial_richardson(osp, b, 0, 1, 16, 16)
+        seq = []
+        for _ in range(iters):
+            ost = O.richardson_recursive_step(ost, osp.matrix, b)
+            seq.append((ost.inner.estimate.copy(), ost.theta.copy()))
+        ev = np.linalg.eigvalsh(a)
+        _C5_ORACLE[key] = (a, b, seq, (ost.ctr.mmm, ost.ctr.mvm), float(ev.max() / ev.min()))
+    return _C5_ORACLE[key]
+
+
+def _gpu_c5(a, b, iters, kw):
+    import paper_2008_11480_b200 as P
+
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False, verify=False)
+    st = P.initial_richardson(sp, b, 0, 1, order=16, q=16)
+    for _ in range(iters):
+        c0 = st.ctr.mmm
+        st = P.richardson_recursive_step(st, sp.matrix, b, **kw)
+        yield st.inner.estimate, st.theta, st.ctr.mmm - c0, st.ctr
+
+
+@pytest.mark.parametrize("variant", ["reference-horner", "factorised-16"])
+def test_c5_recipe_n4096_20_iterations(variant):
+    """Config 5 recipe at n=4096 (256 RHS), the full 20 iterations, both DAGs vs the
+    oracle's Horner DAG at every iteration."""
+    import paper_2008_11480_b200 as P
+
+    n, rhs, iters = 4096, 256, 20
+    a_np, b_np, seq, octr, kappa = _c5_oracle(n, rhs, iters)
+    tol = 1e-10 * max(1.0, kappa / 1e4)
+    kw = ({"factor_plan": P.plan_order(16), "doubling_sum": True}
+          if variant != "reference-horner" else {})
+    a, b = torch.as_tensor(a_np, device="cuda"), torch.as_tensor(b_np, device="cuda")
+    gpu, steps = [], []
+    for p, t, d, ctr in _gpu_c5(a, b, iters, kw):
+        gpu.append((p.clone(), t.clone()))
+        steps.append(d)
+    perm = np.random.default_rng(17).permutation(n)
+    pt = torch.as_tensor(perm, device="cuda")
+    floor = 0.0
+    for k, (p, t, _, _) in enumerate(_gpu_c5(_perm_sym(a, pt), b[pt], iters, kw)):
+        floor = max(floor, _rel_t(_unperm_sym(p, perm), gpu[k][0]),
+                    _rel_t(_unperm_rows(t, perm), gpu[k][1]))
+    err = 0.0
+    for k in range(iters):
+        ep = _rel_np(gpu[k][0].cpu().numpy(), seq[k][0])
+        et = _rel_np(gpu[k][1].cpu().numpy(), seq[k][1])
+        err = max(err, ep, et)
+        assert ep <= tol and et <= tol, (k, ep, et, tol)
+    if variant == "reference-horner":
+        assert steps[0] == 50 and all(s == 34 for s in steps[1:])
+        assert (ctr.mmm, ctr.mvm) == octr
+    else:
+        assert steps[0] == 16 + 18 and all(s == 18 for s in steps[1:])
+    _log(f"c5 n={n} rhs={rhs} ({iters} iterations, {variant}): kappa={kappa:.3g} "
+         f"err_vs_oracle={err:.3e} gpu_permutation_floor={floor:.3e} tol={tol:.1e}")
+    if variant == "reference-horner":
+        assert err <= max(FACTOR * floor, 64 * np.finfo(np.float64).eps)

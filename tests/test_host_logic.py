@@ -62,3 +62,28 @@ def test_counter_semantics():
     buf = [7, 2]
     c.absorb(buf)
     assert (c.mmm, c.mvm) == (12, 7)
+
+
+def test_peer_gather_agreement_check():
+    """SI_PEER_CHECK's divergence check (peer.py): ranks that pair a gather
+    with different (slot, epoch) fail loudly."""
+    import types
+
+    import pytest
+
+    from paper_2008_11480_b200.peer import PeerComm
+
+    fabric = types.SimpleNamespace()  # stands in for the virtual ranks' shared fabric
+
+    def rank(r):
+        c = PeerComm.__new__(PeerComm)
+        c.rank, c.world, c.fabric, c.seq = r, 2, types.SimpleNamespace(fabric=fabric), 1
+        return c
+
+    rank(0)._check_agreement(3, 7, 64)
+    rank(1)._check_agreement(3, 7, 64)  # same pairing: fine
+    a, b = rank(0), rank(1)
+    a.seq = b.seq = 2
+    a._check_agreement(1, 4, 64)
+    with pytest.raises(RuntimeError, match="diverged"):
+        b._check_agreement(2, 4, 64)
