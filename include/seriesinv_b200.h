@@ -52,6 +52,13 @@ extern "C" {
 #endif
 
 typedef struct si_handle_s* si_handle;
+typedef struct si_comm_s* si_comm;
+/* exchange callbacks of si_comm_create_callback: all-gather `count` doubles
+ * per rank (rank-major into recv), in-place sum of `count` doubles; both
+ * ordered on `stream` (a cudaStream_t); return 0 on success */
+typedef int (*si_allgather_fn)(void* ctx, const double* send, double* recv, int64_t count,
+                               void* stream);
+typedef int (*si_allreduce_fn)(void* ctx, double* buf, int64_t count, void* stream);
 
 SI_API int si_version(void);
 SI_API const char* si_last_error(void);
@@ -148,6 +155,94 @@ SI_API int si_split_diagonal(si_handle h, int64_t n, const double* A, double* pr
                       void* stream);
 /* out = (A + A^T)/2  (splitting.py:73) */
 SI_API int si_symmetrize(si_handle h, int64_t n, const double* A, double* out, void* stream);
+
+/* Fused symmetry check + symmetrize (splitting.py:67-73, _check_symmetric):
+ * out = (A + A^T)/2 (out may equal A) in one pass over tile pairs, and the
+ * host scalars asym_fro = ||A - A^T||_F, fro = ||A||_F, nonfinite = number of
+ * non-finite entries (fixed-order reductions; synchronises `stream`).  The
+ * caller applies the reference's test asym_fro > 1e-10 max(fro, 1e-300). */
+SI_API int si_symmetrize_checked(si_handle h, int64_t n, const double* A, double* out,
+                                 double* asym_fro, double* fro, double* nonfinite, void* stream);
+/* is_positive_definite (splitting.py:76-98): Cholesky of (A + A^T)/2 with the
+ * pivot floor d <= tol -> not PD; tol = 1e-12 ||A||_inf when default_tol != 0,
+ * else pivot_tol.  Blocked (128-wide panels) with the trailing updates on the
+ * DMMA GEMM; A is not modified (a workspace copy is factored).  *is_pd = 1/0;
+ * on failure fail_index / fail_pivot (may be NULL) give the first failing
+ * pivot.  Synchronises `stream`. */
+SI_API int si_is_positive_definite(si_handle h, int64_t n, const double* A, int64_t lda,
+                                   double pivot_tol, int default_tol, int* is_pd,
+                                   int64_t* fail_index, double* fail_pivot, void* stream);
+/* Norm-ratio power iteration (matrix_core.py:183-239, spectral_radius) from
+ * the unit start vector x (device, n; overwritten with the current iterate):
+ * y = A x, est = ||y||, the reference's stop rule (|est - prev| <= tol est on
+ * 3 consecutive iterations), x = y / est -- all on the device; the host looks
+ * at the state every `check_every` iterations (one synchronisation each).
+ * *status: 1 converged (*est), 2 est == 0 (x in the null space: the caller
+ * restarts with a fresh vector, as the reference does), 3 max_iter reached
+ * (*best = last estimate).  *iters = iterations executed (<= max_iter). */
+SI_API int si_power_iterate(si_handle h, int64_t n, const double* A, int64_t lda, double* x,
+                            double tol, int64_t max_iter, int check_every, double* est,
+                            double* best, int64_t* iters, int* status, void* stream);
+
+/* ---------------- block-row sharded steps (several GPUs) ----------------
+ * One rank per GPU.  Every state matrix (G, F, L, R, omega, N) is split into
+ * contiguous row blocks -- rank r owns rows [r0, r1) of the near-equal split
+ * returned by si_comm_rows (the first n % nranks blocks one row longer) --
+ * and is passed as that block (r1 - r0 rows, contiguous).  A, S^-1, B, b and
+ * theta are replicated (full n rows on every rank).  Products compute the
+ * local rows; a sharded right operand is all-gathered first (one exchange per
+ * state x state product: the C4 composite step has 11, as sharded.py).  The
+ * GEMM DAG, the counters and every result bit equal the single-GPU entry
+ * points (the per-tile K order does not depend on the split).  Every rank must
+ * make the same sequence of calls (the exchanges are collective).
+ * Replaces the Python block-row engine's orchestration (sharded.py), with the
+ * reference's steps (newton_schulz.py:150-228, richardson.py:111-189). */
+/* NCCL communicator (libnccl.so.2 is loaded on first use): rank 0 makes the id
+ * with si_comm_unique_id and shares it with the other ranks (out of band). */
+SI_API int si_comm_unique_id(unsigned char id[128]);
+SI_API int si_comm_create_nccl(si_handle h, int nranks, int rank, const unsigned char id[128],
+                               int64_t n, si_comm* out);
+/* caller-provided exchange (an MPI layer, a host transport, tests) */
+SI_API int si_comm_create_callback(int nranks, int rank, int64_t n, si_allgather_fn allgather,
+                                   si_allreduce_fn allreduce, void* ctx, si_comm* out);
+SI_API int si_comm_destroy(si_comm c);
+/* this rank's rows and the exchange totals so far (any pointer may be NULL) */
+SI_API int si_comm_rows(si_comm c, int64_t* r0, int64_t* r1, int64_t* gathers,
+                        int64_t* bytes_received);
+/* ns_step (newton_schulz.py:150-174) on row blocks */
+SI_API int si_sharded_ns_step(si_handle h, si_comm comm, int64_t n, const double* a,
+                              const double* g_rows, const double* f_rows, int order,
+                              const int32_t* plan, int64_t plan_len, const double* consts,
+                              int64_t nconsts, double* g_out_rows, double* f_out_rows,
+                              int64_t* counters, void* stream);
+/* composite_step (newton_schulz.py:177-228) on row blocks (serial part order) */
+SI_API int si_sharded_composite_step(si_handle h, si_comm comm, int64_t n, const double* a,
+                                     const double* g_rows, const double* f_rows,
+                                     const double* precond, const double* residual,
+                                     const double* split_matrix, int nrates, const int32_t* rates,
+                                     const int32_t* plans, const int64_t* plan_offsets,
+                                     const double* consts, int64_t nconsts, int order_n,
+                                     double* g_out_rows, double* f_out_rows, int64_t* counters,
+                                     void* stream);
+/* richardson_recursive_step (richardson.py:111-189) on row blocks; theta_out
+ * (n x nrhs) is replicated on return */
+SI_API int si_sharded_richardson_recursive_step(
+    si_handle h, si_comm comm, int64_t n, int64_t nrhs, const double* a, const double* b,
+    const double* theta, const double* g_rows, const double* f_rows, const double* l_rows,
+    const double* r_rows, const double* omega_rows, const double* ns_rows, int order,
+    const int32_t* factor_plan, int64_t plan_len, const double* consts, int64_t nconsts,
+    int doubling_sum, double* g_out_rows, double* f_out_rows, double* l_out_rows,
+    double* r_out_rows, double* omega_out_rows, double* ns_out_rows, double* theta_out,
+    int64_t* counters, void* stream);
+/* theta - P (A theta - b) with P row-sharded; theta_out replicated on return */
+SI_API int si_sharded_plain_richardson(si_handle h, si_comm comm, int64_t n, int64_t nrhs,
+                                       const double* a, const double* b, const double* theta,
+                                       const double* p_rows, double* theta_out, int64_t* counters,
+                                       void* stream);
+/* ||X||_F of a row-sharded n x cols matrix (the stop rule newton_schulz.py:328-331):
+ * local sums of squares + one all-reduce; synchronises `stream` */
+SI_API int si_sharded_fro_norm(si_handle h, si_comm comm, int64_t n, int64_t cols,
+                               const double* x_rows, double* out, void* stream);
 
 /* ---------------- evaluators (series_toolkit.py:279-457) ---------------- */
 

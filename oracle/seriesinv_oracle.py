@@ -125,6 +125,98 @@ def _symmetrize(a):
     return (a + a.T) / 2.0
 
 
+def check_symmetric(a):
+    """sp:67-73 -- (||A - A^T||_F, ||A||_F, (A + A^T)/2); the caller rejects
+    asym > 1e-10 max(fro, 1e-300) (sp:70-71)."""
+    a = np.array(a, dtype=np.float64)
+    return fro(a - a.T), fro(a), (a + a.T) / 2.0
+
+
+def is_positive_definite(a, pivot_tol=None) -> bool:
+    """sp:76-98 -- left-looking Cholesky of (a + a^T)/2; a pivot d <= pivot_tol
+    (default 1e-12 ||a||_inf) means not PD.  Python loop over columns: for
+    n in the hundreds (use is_positive_definite_blocked above that)."""
+    a = np.array(a, dtype=np.float64)
+    a = (a + a.T) / 2.0
+    n = a.shape[0]
+    if pivot_tol is None:
+        pivot_tol = 1e-12 * inf_norm(a)
+    lower = np.zeros_like(a)
+    for j in range(n):
+        d = a[j, j] - np.dot(lower[j, :j], lower[j, :j])
+        if d <= pivot_tol:
+            return False
+        lower[j, j] = np.sqrt(d)
+        if j + 1 < n:
+            lower[j + 1:, j] = (a[j + 1:, j] - lower[j + 1:, :j] @ lower[j, :j]) / lower[j, j]
+    return True
+
+
+def is_positive_definite_blocked(a, pivot_tol=None, nb: int = 256) -> bool:
+    """The same test as :func:`is_positive_definite` (sp:76-98) for large n:
+    right-looking blocked Cholesky in numpy/LAPACK (the diagonal blocks by the
+    column loop, panels by triangular solves, trailing updates by BLAS), the
+    same pivot floor on every pivot.  Pivots equal the loop's up to rounding, so
+    the verdict agrees on every input whose smallest pivot is not within
+    rounding of the floor."""
+    a = np.array(a, dtype=np.float64)
+    a = (a + a.T) / 2.0
+    n = a.shape[0]
+    if pivot_tol is None:
+        pivot_tol = 1e-12 * inf_norm(a)
+    for k in range(0, n, nb):
+        e = min(n, k + nb)
+        blk = a[k:e, k:e]
+        lk = np.zeros_like(blk)
+        for j in range(e - k):
+            d = blk[j, j] - np.dot(lk[j, :j], lk[j, :j])
+            if d <= pivot_tol:
+                return False
+            lk[j, j] = np.sqrt(d)
+            if j + 1 < e - k:
+                lk[j + 1:, j] = (blk[j + 1:, j] - lk[j + 1:, :j] @ lk[j, :j]) / lk[j, j]
+        if e < n:
+            import scipy.linalg as sla
+
+            w = sla.solve_triangular(lk, a[e:, k:e].T, lower=True).T  # A21 L11^-T
+            a[e:, e:] -= w @ w.T
+    return True
+
+
+def spectral_radius(a, tol=1e-12, max_iter=10000, seed=0) -> float:
+    """mc:183-239 -- norm-ratio power iteration, restarts on est == 0; raises
+    RuntimeError with the best estimate when it does not settle."""
+    dim = a.shape[0]
+    rng = np.random.default_rng(seed)
+    best, restarts = 0.0, 0
+    x = rng.standard_normal(dim)
+    x /= np.linalg.norm(x)
+    prev, streak = None, 0
+    for _ in range(max_iter):
+        y = a @ x
+        est = float(np.linalg.norm(y))
+        if est == 0.0:
+            if not np.any(a):
+                return 0.0
+            restarts += 1
+            if restarts > 3:
+                return 0.0
+            x = rng.standard_normal(dim)
+            x /= np.linalg.norm(x)
+            prev, streak = None, 0
+            continue
+        best = est
+        if prev is not None and abs(est - prev) <= tol * est:
+            streak += 1
+            if streak >= 3:
+                return est
+        else:
+            streak = 0
+        prev = est
+        x = y / est
+    raise RuntimeError(f"power iteration did not converge (best estimate {best:.6e})")
+
+
 def split_scalar(a, eps=None) -> Split:
     """sp:124-146 -- S^-1 = I/alpha, alpha = ||A||_inf/2 + eps (PD check skipped:
     the oracle is only fed SPD fixtures)."""

@@ -50,6 +50,26 @@ SIGNATURES: dict[str, list] = {
     "si_split_scalar": [_P, _I64, _P, _D, _P, _P, _P],
     "si_split_diagonal": [_P, _I64, _P, _P, _P, _P],
     "si_symmetrize": [_P, _I64, _P, _P, _P],
+    "si_symmetrize_checked": [_P, _I64, _P, _P, POINTER(c_double), POINTER(c_double),
+                              POINTER(c_double), _P],
+    "si_is_positive_definite": [_P, _I64, _P, _I64, _D, _I, POINTER(c_int), _PI64,
+                                POINTER(c_double), _P],
+    "si_comm_unique_id": [_P],
+    "si_comm_create_nccl": [_P, _I, _I, _P, _I64, POINTER(c_void_p)],
+    "si_comm_create_callback": [_I, _I, _I64, _P, _P, _P, POINTER(c_void_p)],
+    "si_comm_destroy": [_P],
+    "si_comm_rows": [_P, _PI64, _PI64, _PI64, _PI64],
+    "si_sharded_ns_step": [_P, _P, _I64, _P, _P, _P, _I, _P, _I64, _P, _I64, _P, _P, _PI64, _P],
+    "si_sharded_composite_step": [_P, _P, _I64, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _I64,
+                                  _I, _P, _P, _PI64, _P],
+    "si_sharded_richardson_recursive_step": [
+        _P, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I64, _P, _I64, _I,
+        _P, _P, _P, _P, _P, _P, _P, _PI64, _P,
+    ],
+    "si_sharded_plain_richardson": [_P, _P, _I64, _I64, _P, _P, _P, _P, _P, _PI64, _P],
+    "si_sharded_fro_norm": [_P, _P, _I64, _I64, _P, POINTER(c_double), _P],
+    "si_power_iterate": [_P, _I64, _P, _I64, _P, _D, _I64, _I, POINTER(c_double),
+                         POINTER(c_double), _PI64, POINTER(c_int), _P],
     "si_horner_eval": [_P, _I64, _P, _P, _I, _P, _I, _P, _PI64, _P],
     "si_factored_eval": [_P, _I64, _P, _P, _P, _I, _I, _I, _P, _PI64, _P],
     "si_nested_eval": [_P, _I64, _P, _P, _P, _P, _I64, _P, _I64, _I, _P, _PI64, _P],

@@ -1,17 +1,29 @@
 // extern "C" boundary (include/seriesinv_b200.h).  Validates arguments, maps
 // exceptions to status codes, never throws across the ABI.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
 
 #include "../../include/seriesinv_b200.h"
 #include "batched.hpp"
+#include "setup.hpp"
+#include "shard.hpp"
 #include "steps.hpp"
 
 using namespace si;
 
 struct si_handle_s {
   Handle h;
+};
+
+// A block-row communicator (SURVEY 8(b) "sharded variants that take the
+// communicators created inside the handle"): the exchange plus the row split.
+struct si_comm_s {
+  std::unique_ptr<Exchange> ex;
+  int rank = 0, world = 1;
+  int64_t n = 0;
+  int64_t gathers = 0, bytes_in = 0;
 };
 
 namespace {
@@ -61,6 +73,31 @@ struct Call {
     check(cudaSetDevice(h->h.device), "cudaSetDevice");
   }
   ~Call() { add_counters(counters, c); }
+};
+
+// One sharded C-ABI call: Call + this call's Shard (row split, gather cache).
+struct ShardCall {
+  Call call;
+  Shard sh;
+  si_comm comm;
+  ShardCall(si_handle h, si_comm cm, int64_t n, void* stream, int64_t* ctrs)
+      : call(h, stream, ctrs), comm(cm) {
+    if (!cm) throw Error(kEInval, "null communicator");
+    if (n != cm->n) throw Error(kEInval, "n differs from the communicator's n");
+    sh.ex = cm->ex.get();
+    sh.init(n, cm->rank, cm->world);
+    call.c.shard = &sh;
+  }
+  ~ShardCall() {
+    comm->gathers += sh.gathers;
+    comm->bytes_in += sh.bytes_in;
+  }
+  int64_t rows() const { return sh.r1 - sh.r0; }
+  MV loc(const double* p, int64_t cols) {
+    MV m = view(const_cast<double*>(p), rows(), cols, cols);
+    m.local = true;
+    return m;
+  }
 };
 
 PlanPtr opt_plan(const int32_t* code, int64_t len, const double* consts, int64_t nconsts) {
@@ -378,6 +415,81 @@ int si_symmetrize(si_handle h, int64_t n, const double* A, double* out, void* st
     Call call(h, stream, nullptr);
     Mat d = view(out, n, n, n).v;
     check(launch_symmetrize(d, sq(A, n).v, call.c.s), "symmetrize");
+  });
+}
+
+int si_symmetrize_checked(si_handle h, int64_t n, const double* A, double* out, double* asym_fro,
+                          double* fro, double* nonfinite, void* stream) {
+  return guard([&] {
+    need(h && A && out && asym_fro && fro && nonfinite, "null pointer");
+    need(n >= 0, "negative dimension");
+    Call call(h, stream, nullptr);
+    if (n == 0) {
+      *asym_fro = *fro = *nonfinite = 0.0;
+      return;
+    }
+    MV work = alloc(call.c, 1, (int64_t)symcheck_work_elems() + 3);
+    double* res = work.v.p + symcheck_work_elems();
+    Mat d = view(out, n, n, n).v;
+    check(launch_symcheck(d, sq(A, n).v, work.v.p, res, call.c.s), "symcheck");
+    h->h.launches += 2;
+    double host[3];
+    check(cudaMemcpyAsync(host, res, sizeof(host), cudaMemcpyDeviceToHost, call.c.s), "memcpy");
+    check(cudaStreamSynchronize(call.c.s), "sync");
+    *asym_fro = host[0];
+    *fro = host[1];
+    *nonfinite = host[2];
+  });
+}
+
+int si_is_positive_definite(si_handle h, int64_t n, const double* A, int64_t lda,
+                            double pivot_tol, int default_tol, int* is_pd, int64_t* fail_index,
+                            double* fail_pivot, void* stream) {
+  return guard([&] {
+    need(h && (A || n == 0) && is_pd, "null pointer");
+    need(n >= 0 && lda >= n, "bad dimensions");
+    Call call(h, stream, nullptr);
+    int64_t idx = -1;
+    double piv = 0.0;
+    *is_pd = cholesky_pd(call.c, view(const_cast<double*>(A), n, n, lda), pivot_tol,
+                         default_tol != 0, &idx, &piv)
+                 ? 1
+                 : 0;
+    if (fail_index) *fail_index = idx;
+    if (fail_pivot) *fail_pivot = piv;
+  });
+}
+
+int si_power_iterate(si_handle h, int64_t n, const double* A, int64_t lda, double* x,
+                     double tol, int64_t max_iter, int check_every, double* est, double* best,
+                     int64_t* iters, int* status, void* stream) {
+  return guard([&] {
+    need(h && A && x && est && best && iters && status, "null pointer");
+    need(n >= 1 && lda >= n && max_iter >= 1 && check_every >= 1, "bad arguments");
+    Call call(h, stream, nullptr);
+    const int np = sumsq_partials();
+    // y, partial sums, and the PowerState (as doubles)
+    MV work = alloc(call.c, 1, n + np + 8);
+    double* y = work.v.p;
+    double* part = y + n;
+    PowerState* st = reinterpret_cast<PowerState*>(part + np);
+    check(cudaMemsetAsync(st, 0, sizeof(PowerState), call.c.s), "memset");
+    PowerState hs{};
+    Mat a = view(const_cast<double*>(A), n, n, lda).v;
+    int64_t queued = 0;
+    while (queued < max_iter) {
+      const int k = (int)std::min<int64_t>(check_every, max_iter - queued);
+      check(launch_power_iters(a, x, y, part, st, tol, max_iter, k, call.c.s), "power iteration");
+      h->h.launches += 3 * k;
+      queued += k;
+      check(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, call.c.s), "memcpy");
+      check(cudaStreamSynchronize(call.c.s), "sync");
+      if (hs.status != kPowerRunning) break;
+    }
+    *est = hs.est;
+    *best = hs.best;
+    *iters = hs.iters;
+    *status = hs.status;
   });
 }
 
@@ -742,6 +854,156 @@ int si_plain_richardson(si_handle h, int64_t n, int64_t nrhs, const double* a, c
     Call call(h, stream, counters);
     plain_richardson(call.c, sq(a, n), rect(b, n, nrhs), rect(theta, n, nrhs), sq(p, n),
                      rect(theta_out, n, nrhs));
+  });
+}
+
+// ---------------- block-row sharded steps ----------------
+
+int si_comm_unique_id(unsigned char id[128]) {
+  return guard([&] {
+    need(id != nullptr, "null pointer");
+    if (!nccl_unique_id(id)) throw Error(kECuda, "ncclGetUniqueId failed (is libnccl.so.2 present?)");
+  });
+}
+
+int si_comm_create_nccl(si_handle h, int nranks, int rank, const unsigned char id[128], int64_t n,
+                        si_comm* out) {
+  return guard([&] {
+    need(h && id && out, "null pointer");
+    need(nranks >= 1 && rank >= 0 && rank < nranks && n >= nranks, "bad communicator shape");
+    check(cudaSetDevice(h->h.device), "cudaSetDevice");
+    auto c = std::make_unique<si_comm_s>();
+    c->ex = make_nccl_exchange(nranks, rank, id);
+    c->rank = rank;
+    c->world = nranks;
+    c->n = n;
+    *out = c.release();
+  });
+}
+
+int si_comm_create_callback(int nranks, int rank, int64_t n, si_allgather_fn allgather,
+                            si_allreduce_fn allreduce, void* ctx, si_comm* out) {
+  return guard([&] {
+    need(allgather && allreduce && out, "null pointer");
+    need(nranks >= 1 && rank >= 0 && rank < nranks && n >= nranks, "bad communicator shape");
+    auto c = std::make_unique<si_comm_s>();
+    c->ex = make_callback_exchange(allgather, allreduce, ctx);
+    c->rank = rank;
+    c->world = nranks;
+    c->n = n;
+    *out = c.release();
+  });
+}
+
+int si_comm_destroy(si_comm c) {
+  return guard([&] { delete c; });
+}
+
+int si_comm_rows(si_comm c, int64_t* r0, int64_t* r1, int64_t* gathers, int64_t* bytes_in) {
+  return guard([&] {
+    need(c != nullptr, "null communicator");
+    Shard sh;
+    sh.init(c->n, c->rank, c->world);
+    if (r0) *r0 = sh.r0;
+    if (r1) *r1 = sh.r1;
+    if (gathers) *gathers = c->gathers;
+    if (bytes_in) *bytes_in = c->bytes_in;
+  });
+}
+
+int si_sharded_ns_step(si_handle h, si_comm comm, int64_t n, const double* a, const double* g_rows,
+                       const double* f_rows, int order, const int32_t* plan, int64_t plan_len,
+                       const double* consts, int64_t nconsts, double* g_out_rows,
+                       double* f_out_rows, int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && g_rows && f_rows && g_out_rows && f_out_rows, "null pointer");
+    PlanPtr pl = opt_plan(plan, plan_len, consts, nconsts);
+    ShardCall sc(h, comm, n, stream, counters);
+    ns_step(sc.call.c, sq(a, n), sc.loc(g_rows, n), sc.loc(f_rows, n), order, pl.get(),
+            sc.loc(g_out_rows, n), sc.loc(f_out_rows, n));
+  });
+}
+
+int si_sharded_composite_step(si_handle h, si_comm comm, int64_t n, const double* a,
+                              const double* g_rows, const double* f_rows, const double* precond,
+                              const double* residual, const double* split_matrix, int nrates,
+                              const int32_t* rates, const int32_t* plans,
+                              const int64_t* plan_offsets, const double* consts, int64_t nconsts,
+                              int order_n, double* g_out_rows, double* f_out_rows,
+                              int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && g_rows && f_rows && precond && residual && split_matrix && g_out_rows &&
+             f_out_rows,
+         "null pointer");
+    need(nrates >= 1 && rates, "composite spec needs at least one rate");
+    need(order_n >= 1, "order_n must be >= 1");
+    std::vector<int> rv(rates, rates + nrates);
+    std::vector<PlanPtr> owned(nrates);
+    std::vector<const PlanNode*> pv(nrates, nullptr);
+    for (int i = 0; i < nrates; ++i) {
+      need(rv[i] >= 1, "rates must be positive integers");
+      if (plans && plan_offsets && plan_offsets[i + 1] > plan_offsets[i]) {
+        owned[i] = decode_plan(plans + plan_offsets[i], plan_offsets[i + 1] - plan_offsets[i],
+                               consts, nconsts);
+        pv[i] = owned[i].get();
+      }
+    }
+    ShardCall sc(h, comm, n, stream, counters);
+    // serial order only: every rank must issue its exchanges in the same order
+    composite_step(sc.call.c, sq(a, n), sc.loc(g_rows, n), sc.loc(f_rows, n), sq(precond, n),
+                   sq(residual, n), sq(split_matrix, n), rv, pv, order_n, false,
+                   sc.loc(g_out_rows, n), sc.loc(f_out_rows, n));
+  });
+}
+
+int si_sharded_richardson_recursive_step(
+    si_handle h, si_comm comm, int64_t n, int64_t nrhs, const double* a, const double* b,
+    const double* theta, const double* g_rows, const double* f_rows, const double* l_rows,
+    const double* r_rows, const double* omega_rows, const double* ns_rows, int order,
+    const int32_t* factor_plan, int64_t plan_len, const double* consts, int64_t nconsts,
+    int doubling_sum, double* g_out_rows, double* f_out_rows, double* l_out_rows,
+    double* r_out_rows, double* omega_out_rows, double* ns_out_rows, double* theta_out,
+    int64_t* counters, void* stream) {
+  return guard([&] {
+    need(h && a && b && theta && g_rows && f_rows && l_rows && r_rows && g_out_rows &&
+             f_out_rows && l_out_rows && r_out_rows && omega_out_rows && ns_out_rows && theta_out,
+         "null pointer");
+    need(nrhs >= 1, "nrhs must be >= 1");
+    need((omega_rows == nullptr) == (ns_rows == nullptr), "omega and ns_part go together");
+    PlanPtr pl = opt_plan(factor_plan, plan_len, consts, nconsts);
+    if (pl) need(plan_order_of(*pl) == order, "factor plan order != iteration order");
+    ShardCall sc(h, comm, n, stream, counters);
+    MV om = omega_rows ? sc.loc(omega_rows, n) : MV{};
+    MV nsp = ns_rows ? sc.loc(ns_rows, n) : MV{};
+    richardson_recursive_step(sc.call.c, sq(a, n), rect(b, n, nrhs), rect(theta, n, nrhs),
+                              sc.loc(g_rows, n), sc.loc(f_rows, n), sc.loc(l_rows, n),
+                              sc.loc(r_rows, n), omega_rows ? &om : nullptr,
+                              ns_rows ? &nsp : nullptr, order, false, pl.get(), doubling_sum != 0,
+                              sc.loc(g_out_rows, n), sc.loc(f_out_rows, n), sc.loc(l_out_rows, n),
+                              sc.loc(r_out_rows, n), sc.loc(omega_out_rows, n),
+                              sc.loc(ns_out_rows, n), rect(theta_out, n, nrhs));
+  });
+}
+
+int si_sharded_plain_richardson(si_handle h, si_comm comm, int64_t n, int64_t nrhs,
+                                const double* a, const double* b, const double* theta,
+                                const double* p_rows, double* theta_out, int64_t* counters,
+                                void* stream) {
+  return guard([&] {
+    need(h && a && b && theta && p_rows && theta_out, "null pointer");
+    need(nrhs >= 1, "nrhs must be >= 1");
+    ShardCall sc(h, comm, n, stream, counters);
+    plain_richardson(sc.call.c, sq(a, n), rect(b, n, nrhs), rect(theta, n, nrhs),
+                     sc.loc(p_rows, n), rect(theta_out, n, nrhs));
+  });
+}
+
+int si_sharded_fro_norm(si_handle h, si_comm comm, int64_t n, int64_t cols, const double* x_rows,
+                        double* out, void* stream) {
+  return guard([&] {
+    need(h && x_rows && out, "null pointer");
+    ShardCall sc(h, comm, n, stream, nullptr);
+    *out = shard_fro(sc.call.c, sc.loc(x_rows, cols));
   });
 }
 

@@ -65,6 +65,9 @@ cudaError_t launch_diag_split(Mat& P, Mat& B, const Mat& A, cudaStream_t s);
 cudaError_t launch_sumsq(const Mat& X, double* out_dev, double* work, cudaStream_t s);
 cudaError_t launch_inf_norm(const Mat& X, double* out_dev, double* work, cudaStream_t s);
 size_t reduce_work_elems(const Mat& X);
+// per-block partial sums of squares only (sumsq_partials() of them, fixed order)
+cudaError_t launch_sumsq_partials(const Mat& X, double* part, cudaStream_t s);
+int sumsq_partials();
 // Stream memory operations (driver entry points; executed by the stream's
 // front end, no SM involved): *addr = value after prior work, and wait until
 // (int32)(*addr - value) >= 0.  Either address may be a peer (IPC) mapping.

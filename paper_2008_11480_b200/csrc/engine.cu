@@ -3,6 +3,7 @@
 // each) is the reference's, so the mmm/mvm counters match matrix_core.py:71-98
 // tick for tick, while the element-wise ops are fused into the GEMM epilogues.
 #include "engine.hpp"
+#include "shard.hpp"
 
 #include <algorithm>
 #include <cstring>
@@ -96,6 +97,26 @@ void Ctx::gate_stream(const void* p) {
 
 void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV* C, double beta,
           double diag, bool mv, int64_t doff, const PanelWait* pw) {
+  if (c.shard) {
+    // block-row sharded: this rank's rows of A @ B (+ C rows, diag at the
+    // block's global diagonal), B gathered if it is sharded; a replicated
+    // output is completed by an all-gather of its row blocks
+    Shard* sh = c.shard;
+    const MV a = shard_rows(c, A), b = shard_full(c, B);
+    MV cr;
+    if (C) cr = shard_rows(c, *C);
+    const MV d = shard_rows(c, D);
+    c.shard = nullptr;
+    try {
+      gemm(c, d, a, b, alpha, C ? &cr : nullptr, beta, diag, mv, doff + sh->r0, pw);
+    } catch (...) {
+      c.shard = sh;
+      throw;
+    }
+    c.shard = sh;
+    if (!D.local) shard_gather_into(c, D);
+    return;
+  }
   if (A.v.cols != B.v.rows || D.v.rows != A.v.rows || D.v.cols != B.v.cols)
     throw Error(kEInval, "dimension mismatch in product");
   if (C && (C->v.rows != D.v.rows || C->v.cols != D.v.cols))
@@ -173,9 +194,33 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
     c.ctr.mmm += 1;
 }
 
+MV alloc_like(Ctx& c, const MV& x) {
+  if (!c.shard) return alloc(c, x.v.rows, x.v.cols);
+  MV d = alloc(c, c.shard->r1 - c.shard->r0, x.v.cols);
+  d.local = true;
+  return d;
+}
+
+MV identity_like(Ctx& c, const MV& x, double scale) {
+  MV d = alloc_like(c, x);
+  if (c.shard) {  // this rank's rows of scale * I
+    check(launch_lincomb(d.v, scale, c.shard->r0, 0, nullptr, nullptr, c.s), "identity rows");
+  } else {
+    check(launch_fill_identity(d.v, scale, c.s), "identity");
+  }
+  c.h->launches += 1;
+  return d;
+}
+
 MV gemm_new(Ctx& c, const MV& A, const MV& B, double alpha, const MV* C, double beta, double diag,
             bool mv) {
-  MV D = alloc(c, A.v.rows, B.v.cols);
+  MV D;
+  if (c.shard) {  // this rank's rows of the product
+    D = alloc(c, c.shard->r1 - c.shard->r0, B.v.cols);
+    D.local = true;
+  } else {
+    D = alloc(c, A.v.rows, B.v.cols);
+  }
   gemm(c, D, A, B, alpha, C, beta, diag, mv);
   return D;
 }
@@ -187,6 +232,15 @@ void residual_into(Ctx& c, const MV& D, const MV& X, const MV& A) {
 }
 
 void copy_into(Ctx& c, const MV& D, const MV& X) {
+  if (c.shard) {
+    const MV d = shard_rows(c, D), x = shard_rows(c, X);
+    Shard* sh = c.shard;
+    c.shard = nullptr;
+    copy_into(c, d, x);
+    c.shard = sh;
+    if (!D.local) shard_gather_into(c, D);
+    return;
+  }
   if (D.v.p == X.v.p) return;
   if (!c.awaits.empty()) c.await_ptr(X.v.p);
   if (!c.gates.empty()) c.gate_stream(X.v.p);
@@ -197,17 +251,25 @@ void copy_into(Ctx& c, const MV& D, const MV& X) {
 
 MV lincomb(Ctx& c, double cdiag, const std::vector<std::pair<double, const MV*>>& terms,
            int64_t rows, int64_t cols) {
+  int64_t doff = 0;
+  std::vector<MV> loc;
+  if (c.shard) {  // this rank's rows of every term; cdiag * I on the block's diagonal
+    rows = c.shard->r1 - c.shard->r0;
+    doff = c.shard->r0;
+    for (auto& t : terms) loc.push_back(shard_rows(c, *t.second));
+  }
   MV D = alloc(c, rows, cols);
+  D.local = c.shard != nullptr;
   if ((int)terms.size() > kMaxLinTerms) throw Error(kEInval, "too many lin terms");
   double coef[kMaxLinTerms];
   Mat xs[kMaxLinTerms];
   for (size_t i = 0; i < terms.size(); ++i) {
     coef[i] = terms[i].first;
-    xs[i] = terms[i].second->v;
+    xs[i] = c.shard ? loc[i].v : terms[i].second->v;
     if (!c.awaits.empty()) c.await_ptr(xs[i].p);
     if (!c.gates.empty()) c.gate_stream(xs[i].p);
   }
-  check(launch_lincomb(D.v, cdiag, 0, (int)terms.size(), coef, xs, c.s), "lincomb");
+  check(launch_lincomb(D.v, cdiag, doff, (int)terms.size(), coef, xs, c.s), "lincomb");
   c.h->launches += 1;
   return D;
 }
@@ -417,12 +479,7 @@ MV eval_node(Ctx& c, const PlanNode& node, const MV& y, const MV& x, const MV& a
 
 // mc:137-151
 MV mat_pow_counted(Ctx& c, const MV& y, int e) {
-  if (e == 0) {
-    MV d = alloc(c, y.v.rows, y.v.cols);
-    check(launch_fill_identity(d.v, 1.0, c.s), "identity");
-    c.h->launches += 1;
-    return d;
-  }
+  if (e == 0) return identity_like(c, y);
   MV base = y, result;
   bool have = false;
   while (e > 0) {
@@ -440,7 +497,7 @@ MV mat_pow_counted(Ctx& c, const MV& y, int e) {
 MV geometric(Ctx& c, const MV& y, const MV& x, int order, const MV& a, const PlanNode* base) {
   if (order < 1) throw Error(kEInval, "order must be >= 1");
   if (order == 1) {
-    MV d = alloc(c, x.v.rows, x.v.cols);
+    MV d = alloc_like(c, x);
     copy_into(c, d, x);
     return d;
   }
@@ -483,6 +540,7 @@ Ctx Fork::branch(int i) {
   ch.awaits = parent.awaits;  // the side stream has not waited for any input yet
   for (auto& a : ch.awaits) a.done = false;
   ch.gates = parent.gates;
+  ch.shard = parent.shard;
   for (auto& g : ch.gates) g.stream_done = false;
   check(cudaStreamWaitEvent(ch.s, evs[0], 0), "cudaStreamWaitEvent");
   return ch;

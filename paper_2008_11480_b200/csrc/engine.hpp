@@ -64,11 +64,17 @@ struct Buf {
 };
 
 // A matrix value: a view plus (optional) shared ownership of its storage.
+// `local` (block-row sharded calls only, Ctx::shard set): the value is this
+// rank's row block [r0, r1) of an n-row matrix; otherwise it is the whole
+// matrix (replicated on every rank).
 struct MV {
   Mat v;
   std::shared_ptr<Buf> own;
+  bool local = false;
   int64_t n() const { return v.rows; }
 };
+
+struct Shard;  // shard.hpp: row split + the exchange of one sharded C-ABI call
 
 struct Counters {
   int64_t mmm = 0, mvm = 0;
@@ -102,6 +108,10 @@ struct Ctx {
   std::vector<Gate> gates;
   const PanelWait* gate_of(const void* p) const;
   void gate_stream(const void* p);  // stream-wait for every panel of p (once)
+  // Block-row sharded execution (shard.cu): every product yields
+  // this rank's rows; a replicated left / epilogue operand is read through its
+  // row view, a sharded right operand is all-gathered first.
+  Shard* shard = nullptr;
   Ctx(Handle* hh, cudaStream_t st) : h(hh), root(st), s(st) {}
 };
 
@@ -122,6 +132,10 @@ void residual_into(Ctx& c, const MV& D, const MV& X, const MV& A);
 void copy_into(Ctx& c, const MV& D, const MV& X);
 MV lincomb(Ctx& c, double cdiag, const std::vector<std::pair<double, const MV*>>& terms,
            int64_t rows, int64_t cols);
+// a fresh buffer shaped like x (this rank's rows of it in a sharded call)
+MV alloc_like(Ctx& c, const MV& x);
+// scale * I shaped like x (the identity's rows of this rank in a sharded call)
+MV identity_like(Ctx& c, const MV& x, double scale = 1.0);
 
 // ---- plans (series_toolkit.py:71-157), decoded from the int32 preorder form ----
 struct PlanNode;

@@ -24,6 +24,18 @@
 //    epilogue.
 //  * Optional row-panel gates on A (per tile rows) and B (per k-slab); used for
 //    inputs whose host->device copy is still in flight.
+//  * Wave lockstep (multi-wave products): the producer lanes of all CTAs
+//    advance through k in epochs of kSyncEpoch k-blocks and a lane may start
+//    epoch E only when every CTA has issued epoch E-2 (per-epoch arrival
+//    counters in a 4-slot ring).  The CTAs of a wave then read each k-slab of
+//    their shared A / B panels within ~2 epochs of each other, so the slab is
+//    still in L2 for all of them: without it the CTAs drift apart over a long
+//    launch and every CTA streams its panels from HBM (n=32768: 3.2 TB of DRAM
+//    traffic per product against a 0.4 TB lockstep floor).  The order in which
+//    a tile accumulates k is unchanged, so results are bitwise unchanged; the
+//    slowest CTA never waits, and a wait that exceeds 1 ms (CTAs of this grid
+//    not yet resident, e.g. beside a concurrent product) turns the throttle off
+//    for that CTA rather than stall it.
 //  * Optional panel gate (sharded path): when B is a matrix whose row panels
 //    are still arriving from peer GPUs (copy engines, flags written by stream
 //    memory operations), the producer lane acquires panel p's flag before its
@@ -56,6 +68,21 @@ constexpr int B_STAGE_BYTES = BK * BN * 8;  // 16 KB
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
 constexpr int GROUP_M = 8;
+constexpr int kSyncEpoch = 8;     // k-blocks per lockstep epoch
+constexpr int kSyncRing = 4;      // arrival counters per launch (epochs e, e+4, ... share one)
+constexpr int kSyncSets = 64;     // counter sets per device, handed out round robin
+constexpr int kSyncMinKBlocks = 64;
+
+// One launch's lockstep counters (self-cleaning: the last CTA to finish zeroes them).
+struct alignas(64) SyncSet {
+  unsigned ring[kSyncRing];
+  unsigned done;
+  unsigned pad[11];
+};
+
+struct WaveSync {
+  SyncSet* set = nullptr;  // null: no lockstep (single wave / short K)
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -113,6 +140,24 @@ __device__ __forceinline__ void panel_gate(const PanelWait& pw, int k0, int k1, 
   }
 }
 
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Arrivals expected in ring slot (e % kSyncRing) once every CTA has issued
+// epochs 0..e: CTAs own `hi` = T-tile or `lo` = (T-1)-tile schedules with EH /
+// EL epochs each; slot j collects epochs j, j + R, j + 2R, ...
+__device__ __forceinline__ unsigned sync_expected(int e, int n_hi, int eh, int n_lo, int el) {
+  const int j = e % kSyncRing;
+  auto cnt = [&](int epochs) {
+    const int m = min(e, epochs - 1);
+    return m >= j ? (m - j) / kSyncRing + 1 : 0;
+  };
+  return (unsigned)(n_hi * cnt(eh) + n_lo * cnt(el));
+}
+
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                             int c0, int c1) {
   asm volatile(
@@ -168,7 +213,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         int64_t ldd, const double* __restrict__ C, int64_t ldc, int M, int N,
                         int K, double alpha, double beta, double diag, int64_t doff,
                         const __grid_constant__ PanelWait pw,
-                        const __grid_constant__ PanelWait pwa) {
+                        const __grid_constant__ PanelWait pwa, SyncSet* __restrict__ sync) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -202,6 +247,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       uint32_t known = pw.ready ? 0u : ~0u;
       uint32_t known_a = pwa.ready ? 0u : ~0u;  // row panels of A (inputs in flight)
+      // wave lockstep: this CTA's k-blocks are numbered g = 0, 1, ... across its
+      // tiles; epoch g / kSyncEpoch.  Tile counts per CTA are T or T-1.
+      bool lockstep = sync != nullptr;
+      const int T = (num_tiles + (int)gridDim.x - 1) / (int)gridDim.x;
+      const int n_hi = num_tiles - (T - 1) * (int)gridDim.x;
+      const int n_lo = (int)gridDim.x - n_hi;
+      const int eh = (T * kblocks + kSyncEpoch - 1) / kSyncEpoch;
+      const int el = ((T - 1) * kblocks + kSyncEpoch - 1) / kSyncEpoch;
+      int g = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         int tm, tn;
         tile_coords(tile, num_m, num_n, tm, tn);
@@ -209,7 +263,25 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (~known_a) panel_gate(pwa, tm * BM, min(M, tm * BM + BM), known_a);
         const int nboxes = min(8, (N - n0 + 15) / 16);
         const uint32_t bytes = A_STAGE_BYTES + nboxes * B_BOX_BYTES;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = 0; kb < kblocks; ++kb, ++g) {
+          if (sync != nullptr && g > 0 && g % kSyncEpoch == 0) {
+            const int e = g / kSyncEpoch;  // about to start epoch e: epoch e-1 is issued
+            atomicAdd(&sync->ring[(e - 1) % kSyncRing], 1u);
+            if (lockstep && e >= 2) {
+              const unsigned want = sync_expected(e - 2, n_hi, eh, n_lo, el);
+              const unsigned* slot = &sync->ring[(e - 2) % kSyncRing];
+              if ((int)(ld_relaxed_u32(slot) - want) < 0) {
+                const uint64_t t0 = globaltimer_ns();
+                while ((int)(ld_relaxed_u32(slot) - want) < 0) {
+                  __nanosleep(64);
+                  if (globaltimer_ns() - t0 > 1000000ull) {  // 1 ms: stop throttling
+                    lockstep = false;
+                    break;
+                  }
+                }
+              }
+            }
+          }
           if (~known) panel_gate(pw, kb * BK, min(K, kb * BK + BK), known);
           mbar_wait(empty_bar(stage), phase ^ 1u);
           const uint32_t sa = base + stage * STAGE_BYTES;
@@ -234,6 +306,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                                C + (int64_t)(m0 + r) * ldc + n0),
                            "r"(bytes_row)
                            : "memory");
+        }
+      }
+      if (sync != nullptr) {
+        if (g > 0) atomicAdd(&sync->ring[((g - 1) / kSyncEpoch) % kSyncRing], 1u);
+        // every arrival and every wait of this CTA is behind this point: the
+        // last CTA out leaves the set zeroed for the next launch that draws it
+        __threadfence();
+        if (atomicAdd(&sync->done, 1u) == gridDim.x - 1) {
+          for (int j = 0; j < kSyncRing; ++j) atomicExch(&sync->ring[j], 0u);
+          atomicExch(&sync->done, 0u);
         }
       }
     }
@@ -432,6 +514,43 @@ bool make_map(CUtensorMap* map, const double* ptr, int64_t rows, int64_t cols, i
   return r == CUDA_SUCCESS;
 }
 
+// kSyncSets lockstep counter sets per device (zeroed once; every launch
+// leaves its set zeroed).  A set is in use for one launch; handing them out
+// round robin keeps concurrently running products on different sets.
+SyncSet* draw_sync_set(int dev) {
+  static std::mutex mu;
+  static SyncSet* sets[64] = {};
+  static std::atomic<unsigned> next{0};
+  if (dev < 0 || dev >= 64) return nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!sets[dev]) {
+      void* p = nullptr;
+      if (cudaMalloc(&p, kSyncSets * sizeof(SyncSet)) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+      if (cudaMemset(p, 0, kSyncSets * sizeof(SyncSet)) != cudaSuccess ||
+          cudaDeviceSynchronize() != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(p);
+        return nullptr;
+      }
+      sets[dev] = static_cast<SyncSet*>(p);
+    }
+  }
+  return sets[dev] + next.fetch_add(1) % kSyncSets;
+}
+
+// SI_GEMM_LOCKSTEP=0 turns the wave lockstep off (A/B measurements; read once)
+bool lockstep_disabled() {
+  static const bool off = [] {
+    const char* v = std::getenv("SI_GEMM_LOCKSTEP");
+    return v != nullptr && v[0] == '0';
+  }();
+  return off;
+}
+
 int num_sms() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -478,6 +597,10 @@ cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& 
   const int M = (int)D.rows, N = (int)D.cols, K = (int)A.cols;
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
+  // lockstep only pays for products of several waves with a long K loop
+  const int kblocks = (K + BK - 1) / BK;
+  SyncSet* sync = (tiles > grid && kblocks >= kSyncMinKBlocks && !lockstep_disabled())
+                      ? draw_sync_set(dev) : nullptr;
   PanelWait gate, gate_a;
   if (pw && pw->ready && pw->npanels > 0) gate = *pw;
   if (pwa && pwa->ready && pwa->npanels > 0) gate_a = *pwa;
@@ -488,7 +611,7 @@ cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& 
   auto kern = epi == 1 ? gemm_f64_tma_kernel<1> : gemm_f64_tma_kernel<0>;
   kern<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, D.p, D.ld, e.c, e.ldc, M, N, K,
                                                         e.alpha, e.beta, e.diag, e.doff, gate,
-                                                        gate_a);
+                                                        gate_a, sync);
   return cudaGetLastError();
 }
 

@@ -471,6 +471,13 @@ cudaError_t launch_sumsq(const Mat& X, double* out_dev, double* work, cudaStream
   return cudaGetLastError();
 }
 
+int sumsq_partials() { return RED_BLOCKS; }
+
+cudaError_t launch_sumsq_partials(const Mat& X, double* part, cudaStream_t s) {
+  sumsq_partial<<<RED_BLOCKS, RED_THREADS, 0, s>>>(X.p, X.ld, X.rows, X.cols, part);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_inf_norm(const Mat& X, double* out_dev, double* work, cudaStream_t s) {
   const unsigned grid = (unsigned)((X.rows + RED_THREADS / 32 - 1) / (RED_THREADS / 32));
   rowabs_kernel<<<grid, RED_THREADS, 0, s>>>(X.p, X.ld, X.rows, X.cols, work);

@@ -87,7 +87,7 @@ void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, 
   auto part = [&](Ctx& cc, size_t i) {
     if (rates[i] < 1) throw Error(kEInval, "rates must be positive integers");
     if (rates[i] == 1) {
-      ts[i] = alloc(cc, P.v.rows, P.v.cols);
+      ts[i] = alloc_like(cc, P);
       copy_into(cc, ts[i], P);
     } else {
       ts[i] = geometric(cc, B, P, rates[i], Sm, plans[i]);
@@ -138,7 +138,7 @@ void composite_parts(Ctx& c, const MV& A, const MV& P, const MV& B, const MV& Sm
     if (rates[i] < 1) throw Error(kEInval, "rates must be positive integers");
     MV ti;
     if (rates[i] == 1) {
-      ti = alloc(c, P.v.rows, P.v.cols);
+      ti = alloc_like(c, P);
       copy_into(c, ti, P);
     } else {
       ti = geometric(c, B, P, rates[i], Sm, plans[i]);
@@ -226,9 +226,7 @@ void richardson_step(Ctx& c, const MV& A, const MV& b, const MV& theta, const MV
 
 // ri:101-108  I + gamma + ... + gamma^(n-1)
 MV power_sum(Ctx& c, const MV& gamma, int n) {
-  MV acc = alloc(c, gamma.v.rows, gamma.v.cols);
-  check(launch_fill_identity(acc.v, 1.0, c.s), "identity");
-  c.h->launches += 1;
+  MV acc = identity_like(c, gamma);
   MV cur;
   bool have = false;
   for (int i = 0; i < n - 1; ++i) {
@@ -244,9 +242,7 @@ MV power_sum(Ctx& c, const MV& gamma, int n) {
 // instead of the n-2 of power_sum.
 MV power_sum_doubling(Ctx& c, const MV& gamma, int n) {
   if (n < 2 || (n & (n - 1))) throw Error(kEInval, "doubling power sum needs n = 2^m >= 2");
-  MV eye = alloc(c, gamma.v.rows, gamma.v.cols);
-  check(launch_fill_identity(eye.v, 1.0, c.s), "identity");
-  c.h->launches += 1;
+  MV eye = identity_like(c, gamma);
   MV s = lincomb(c, 0.0, {{1.0, &eye}, {1.0, &gamma}}, gamma.v.rows, gamma.v.cols);  // I + gamma
   MV pw = gamma;
   for (int t = 2; t < n; t *= 2) {

@@ -282,40 +282,51 @@ class SpectralRadiusError(RuntimeError):
         self.best_estimate = best_estimate
 
 
-def spectral_radius(a, tol: float = 1e-12, max_iter: int = 10000, seed: int = 0) -> float:
-    """Norm-ratio power iteration (matrix_core.py:183-239) on the device GEMV."""
+def spectral_radius(a, tol: float = 1e-12, max_iter: int = 10000, seed: int = 0,
+                    check_every: int = 32) -> float:
+    """Norm-ratio power iteration (matrix_core.py:183-239).
+
+    The iteration runs on the device (``si_power_iterate``: GEMV, norm, the
+    reference's streak rule and x = y / est in kernels, no host round trip per
+    iteration); the host looks at the state every ``check_every`` iterations.
+    Start and restart vectors are the reference's draws (``default_rng(seed)``
+    normals, normalised on the host), so the sequence of estimates is the
+    reference's up to GEMV rounding."""
     a = as_device(a)
     dim = a.shape[0]
-    if a.shape != (dim, dim):
+    if a.ndim != 2 or a.shape != (dim, dim):
         raise ValueError("spectral_radius expects a square matrix")
+    a = a.contiguous()
     rng = np.random.default_rng(seed)
 
     def fresh():
         x = rng.standard_normal(dim)
         return as_device(x / np.linalg.norm(x))
 
-    best, restarts, prev, streak = 0.0, 0, None, 0
+    best, restarts, used = 0.0, 0, 0
     x = fresh()
-    for _ in range(max_iter):
-        y = _gemm(a, x, True, None)
-        est = fro_norm(y)
-        if est == 0.0:
+    h, s = _lib.handle(a.device.index), _lib.stream_ptr(a.device)
+    while used < max_iter:
+        est, bst = ctypes.c_double(), ctypes.c_double()
+        its, status = ctypes.c_int64(), ctypes.c_int()
+        _lib.call("si_power_iterate", h, dim, a.data_ptr(), dim, x.data_ptr(), float(tol),
+                  max_iter - used, int(check_every), ctypes.byref(est), ctypes.byref(bst),
+                  ctypes.byref(its), ctypes.byref(status), s)
+        used += its.value
+        if bst.value != 0.0:
+            best = bst.value
+        if status.value == 1:
+            return est.value
+        if status.value == 2:
+            # est == 0: x is (numerically) in the null space (matrix_core.py:203-215)
             if fro_norm(a) == 0.0:
                 return 0.0
             restarts += 1
             if restarts > 3:
                 return 0.0
-            x, prev, streak = fresh(), None, 0
+            x = fresh()
             continue
-        best = est
-        if prev is not None and abs(est - prev) <= tol * est:
-            streak += 1
-            if streak >= 3:
-                return est
-        else:
-            streak = 0
-        prev = est
-        x = y / est
+        break
     raise SpectralRadiusError(
         f"power iteration did not converge within {max_iter} iterations (best estimate {best:.6e})",
         best_estimate=best,

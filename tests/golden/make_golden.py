@@ -319,7 +319,62 @@ def harness_runs():
         json.dump(out, fh)
 
 
+def setup_family():
+    """Setup path: symmetry check + symmetrize (sp:67-73), PD
+    verdicts with the pivot floor (sp:76-98), spectral radius (mc:183-239)."""
+    from seriesinv.splitting import _check_symmetric
+
+    rng = np.random.default_rng(808)
+    d = {}
+    # symmetry: relative asymmetry 1e-13 (accepted) / 1e-8 (rejected)
+    for i, (dim, rel) in enumerate([(5, 1e-13), (40, 1e-13), (40, 1e-8), (130, 0.0), (130, 1e-7)]):
+        a = spd(dim, rng)
+        a = a + rel * np.linalg.norm(a) / dim * rng.standard_normal((dim, dim))
+        d[f"sym{i}_a"] = a
+        try:
+            d[f"sym{i}_out"] = _check_symmetric(a)
+            d[f"sym{i}_ok"] = np.array(1)
+        except ValueError:
+            d[f"sym{i}_ok"] = np.array(0)
+    # positive definiteness
+    cases = [np.eye(3), np.array([[1.0, 2.0], [2.0, 1.0]]), np.zeros((2, 2)),
+             np.array([[1.0, 1.0], [1.0, 1.0 + 1e-16]])]
+    for dim in (7, 64, 200, 300):
+        a = spd(dim, rng)
+        cases.append(a)                                    # SPD
+        ev_min = float(np.linalg.eigvalsh(a).min())
+        cases.append(a - (ev_min + 1e-3) * np.eye(dim))    # indefinite by a clear margin
+        cases.append(a - (ev_min - 1e-6) * np.eye(dim))    # SPD, lambda_min = 1e-6
+    big = spd(150, rng)
+    blk = np.zeros((152, 152))
+    blk[:75, :75] = big[:75, :75]
+    blk[75:77, 75:77] = [[1.0, 1.0], [1.0, 1.0 + 1e-16]]   # exactly singular pivot mid-matrix
+    blk[77:, 77:] = big[75:, 75:]
+    cases.append(blk)
+    for i, a in enumerate(cases):
+        d[f"pd{i}_a"] = a
+        d[f"pd{i}_default"] = np.array(int(si.is_positive_definite(a)))
+        d[f"pd{i}_zero_tol"] = np.array(int(si.is_positive_definite(a, pivot_tol=0.0)))
+    d["pd_count"] = np.array(len(cases))
+    # spectral radius
+    rads = [np.diag([0.9, 0.1]), np.eye(4), np.zeros((3, 3))]
+    for dim in (6, 50, 200):
+        q, _ = np.linalg.qr(rng.standard_normal((dim, dim)))
+        ev = rng.uniform(-0.5, 0.5, dim)
+        ev[0] = 0.95
+        rads.append((q * ev) @ q.T)
+    for i, m in enumerate(rads):
+        d[f"rho{i}_a"] = m
+        d[f"rho{i}"] = np.array(si.spectral_radius(m))
+    d["rho_count"] = np.array(len(rads))
+    np.savez_compressed(os.path.join(HERE, "setup.npz"), **d)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["setup"]:  # regenerate only setup.npz
+        setup_family()
+        sys.exit(0)
+    setup_family()
     harness_runs()
     plans_json()
     toolkit()

@@ -46,3 +46,27 @@ def test_oracle_reproduces_reference(B, name, fixture):
 
 def test_oracle_batched_fixture(B):
     cases.compare(cases.case_c2_oracle(B), "c2.npz", B, rtol=1e-12, ftol=1e-13)
+
+
+def test_oracle_setup_path_matches_reference():
+    """Symmetry check, PD verdicts (loop and blocked forms) and spectral radius
+    of the oracle against the reference's outputs (setup.npz)."""
+    import numpy as np
+
+    from conftest import golden
+    from oracle import seriesinv_oracle as O
+
+    g = golden("setup.npz")
+    for i in range(5):
+        asym, fro, out = O.check_symmetric(g[f"sym{i}_a"])
+        ok = int(asym <= 1e-10 * max(fro, 1e-300))
+        assert ok == int(g[f"sym{i}_ok"])
+        if ok:
+            assert np.array_equal(out, g[f"sym{i}_out"])
+    for i in range(int(g["pd_count"])):
+        a = g[f"pd{i}_a"]
+        assert int(O.is_positive_definite(a)) == int(g[f"pd{i}_default"]), i
+        assert int(O.is_positive_definite(a, pivot_tol=0.0)) == int(g[f"pd{i}_zero_tol"]), i
+        assert int(O.is_positive_definite_blocked(a, nb=32)) == int(g[f"pd{i}_default"]), i
+    for i in range(int(g["rho_count"])):
+        assert O.spectral_radius(g[f"rho{i}_a"]) == float(g[f"rho{i}"])
