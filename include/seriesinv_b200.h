@@ -184,6 +184,15 @@ SI_API int si_power_iterate(si_handle h, int64_t n, const double* A, int64_t lda
                             double tol, int64_t max_iter, int check_every, double* est,
                             double* best, int64_t* iters, int* status, void* stream);
 
+/* Build tooling (host only, no device needed): the C++ source of the
+ * compile-time program of the config-2 resident kernel for this recipe
+ * (tools/gen_resident_fixed.py writes it to csrc/resident_fixed_c2.inc).
+ * *len = length; written to out when cap > *len. */
+SI_API int si_resident_program_source(int64_t n, int nrates, const int32_t* rates,
+                                      const int32_t* plans, const int64_t* plan_offsets,
+                                      const double* consts, int64_t nconsts, int order_n,
+                                      char* out, int64_t cap, int64_t* len);
+
 /* ---------------- block-row sharded steps (several GPUs) ----------------
  * One rank per GPU.  Every state matrix (G, F, L, R, omega, N) is split into
  * contiguous row blocks -- rank r owns rows [r0, r1) of the near-equal split

@@ -27,7 +27,9 @@
 #include <functional>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <unordered_map>
+#include <utility>
 
 #include "batched.hpp"
 
@@ -675,7 +677,31 @@ __device__ __forceinline__ void gemm_op(const double* A, const double* B, const 
     }
 }
 
-template <int NP>
+// The op program either comes from shared memory (interpreted: any recipe)
+// or is baked in at compile time (FX::kFixed: the config-2 recipe, generated
+// into resident_fixed_c2.inc by tools/gen_resident_fixed.py): then every op's
+// kind, mode, slots and barrier flag are constants, the op loop is straight-
+// line code, and no op is decoded or branched on at run time.
+struct NoFixed {
+  static constexpr bool kFixed = false;
+  static constexpr int nops = 1;
+  static constexpr DOp ops[1] = {};
+};
+
+#if __has_include("resident_fixed_c2.inc")
+// BASELINE config 2's program (n = 32, rates (2, 3), order_n = 2)
+struct FixedC2 {
+#include "resident_fixed_c2.inc"
+};
+#define SI_HAVE_FIXED_C2 1
+#endif
+
+template <class F, int... K>
+__device__ __forceinline__ void static_for(F&& f, std::integer_sequence<int, K...>) {
+  (f(std::integral_constant<int, K>{}), ...);
+}
+
+template <int NP, class FX = NoFixed>
 // 32 x 32 systems: four CTAs of four warps per SM (<= 128 registers per
 // thread; five fit in shared memory but measured slower, see Geo)
 #ifndef SI_RESIDENT_MINB32
@@ -755,11 +781,8 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
       }
     };
     if (prefetch && (first || p.chunk_ready)) issue(sys);
-    for (int it = 0; it < p.iters; ++it) {
-      for (int k = 0; k < p.nops; ++k) {
-        // (the LIN term list is read from shared memory, prog[k].t[j]: indexing
-        // the register copy with a runtime j would put `o` in local memory)
-        const DOp o = prog[k];
+    // one op of the program; `o` is a compile-time constant on the fixed path
+    auto exec = [&](const DOp& o, int k, int it) {
         const double* oc = cst + o.cidx;
         if (o.kind == OP_LOAD && prefetch) {
           double* dst = mslot(o.dst);
@@ -836,7 +859,11 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
           if (threadIdx.x < NP) {
             double acc = 0.0;
             for (int j = 0; j < o.nterms; ++j) {
-              const double xv = vslot(prog[k].t[j])[threadIdx.x];
+              // (the term list is read from shared memory on the interpreted
+              // path: indexing a register copy of `o` with a runtime j would
+              // put it in local memory)
+              const int tj = FX::kFixed ? o.t[j] : prog[k].t[j];
+              const double xv = vslot(tj)[threadIdx.x];
               acc = __dadd_rn(acc, oc[1 + j] == 1.0 ? xv : __dmul_rn(oc[1 + j], xv));
             }
             vslot(o.dst)[threadIdx.x] = acc;
@@ -848,7 +875,8 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
             const int c = G::col_at(r, i % NP);
             double acc = (r == c && r < n) ? oc[0] : 0.0;
             for (int j = 0; j < o.nterms; ++j) {
-              const double xv = mslot(prog[k].t[j])[i];
+              const int tj = FX::kFixed ? o.t[j] : prog[k].t[j];
+              const double xv = mslot(tj)[i];
               acc = __dadd_rn(acc, oc[1 + j] == 1.0 ? xv : __dmul_rn(oc[1 + j], xv));
             }
             D[i] = acc;
@@ -859,6 +887,21 @@ __global__ void __launch_bounds__(Geo<NP>::THREADS, NP == 32 ? SI_RESIDENT_MINB3
           const long long now = clock64();
           prof_acc[k] += now - prof_last;
           prof_last = now;
+        }
+    };
+    for (int it = 0; it < p.iters; ++it) {
+      if constexpr (FX::kFixed) {
+        static_for(
+            [&](auto kc) {
+              constexpr int k = decltype(kc)::value;
+              constexpr DOp o = FX::ops[k];
+              exec(o, k, it);
+            },
+            std::make_integer_sequence<int, FX::nops>{});
+      } else {
+        for (int k = 0; k < p.nops; ++k) {
+          const DOp o = prog[k];
+          exec(o, k, it);
         }
       }
       // carry the state where the allocator could not place it in place
@@ -1226,6 +1269,15 @@ std::vector<uint8_t> cluster_flags(const std::vector<BOp>& prog, const std::vect
   return out;
 }
 
+// SI_RESIDENT_FIXED=0: always interpret (A/B measurements; read once)
+bool fixed_disabled() {
+  static const bool off = [] {
+    const char* v = std::getenv("SI_RESIDENT_FIXED");
+    return v != nullptr && v[0] == '0';
+  }();
+  return off;
+}
+
 int num_sms_b() {
   int d = 0, n = 0;
   cudaGetDevice(&d);
@@ -1276,28 +1328,22 @@ void defer_theta_update(Recipe& q) {
     }
 }
 
+// The device program of a recipe: scheduled, slot-allocated, barrier flags,
+// device encoding (host only; no CUDA call except the SM count for NP = 64).
+struct Built {
+  std::vector<BOp> ops;
+  std::vector<DOp> dev_ops;
+  std::vector<double> csts;
+  Alloc al;
+  int cl = 0;
+  std::vector<uint8_t> cflags;
+  size_t smem = 0;
+  std::string blob;  // dev_ops + csts: what the kernel reads
+};
+
 template <int NP>
-Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, const double* b,
-                const double* precond, const double* residual, int iters, const double* p_in,
-                const double* f_in, const double* theta_in, double* p_io, double* f_io,
-                double* theta_io, const ChunkGate* gate = nullptr) {
+Built build_program(Recipe& q, int64_t batch, const ChunkGate* gate) {
   using Gm = Geo<NP>;
-  Counters per;
-  for (const BOp& o : q.r.ops) {
-    if (o.kind == OP_GEMM) per.mmm += 1;
-    if (o.kind == OP_GEMV) per.mvm += 1;
-  }
-  per.mmm *= iters;
-  per.mvm *= iters;
-  if (batch == 0) return per;
-  if (iters == 0) {  // outputs = inputs
-    const size_t mat = (size_t)batch * n * n * sizeof(double), vec = (size_t)batch * n * 8;
-    if (p_io != p_in) check(cudaMemcpyAsync(p_io, p_in, mat, cudaMemcpyDeviceToDevice, c.s), "copy");
-    if (f_io != f_in) check(cudaMemcpyAsync(f_io, f_in, mat, cudaMemcpyDeviceToDevice, c.s), "copy");
-    if (theta_io != theta_in)
-      check(cudaMemcpyAsync(theta_io, theta_in, vec, cudaMemcpyDeviceToDevice, c.s), "copy");
-    return per;
-  }
   if ((int)q.r.ops.size() > kMaxOps) throw Error(kEInval, "resident program too long");
 
   std::vector<int> pinned = {q.A, q.bv};
@@ -1307,8 +1353,11 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
   // (NP = 64 may run as a cluster, whose peers read broadcast copies)
   const bool ab = NP == 32;
   schedule_min_live_cached(q.r, pinned, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}}, ab);
-  Alloc al = assign(q.r, pinned, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}}, ab);
-  std::vector<BOp> ops = q.r.ops;
+  Built bt;
+  Alloc& al = bt.al;
+  al = assign(q.r, pinned, {{q.G, q.gn}, {q.F, q.fn}, {q.T, q.tn}}, ab);
+  std::vector<BOp>& ops = bt.ops;
+  ops = q.r.ops;
   auto ph = [&](int v) -> int16_t { return v >= 0 ? al.phys[v] : (int16_t)-1; };
   for (BOp& o : ops) {
     o.dst = ph(o.dst);
@@ -1357,7 +1406,7 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
   }
   // Cluster mode (NP = 64, few systems: latency-bound on one SM each): one
   // cluster of `cl` CTAs per system.  SI_RESIDENT_CLUSTER = 0/2/4/8 overrides.
-  int cl = 0;
+  int& cl = bt.cl;
   if (NP == 64) {
     const char* env = std::getenv("SI_RESIDENT_CLUSTER");
     if (env) {
@@ -1370,7 +1419,7 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
     }
     if (gate && gate->ready) cl = 0;  // the chunk gate lives in the one-CTA kernel
   }
-  std::vector<uint8_t> cflags;
+  std::vector<uint8_t>& cflags = bt.cflags;
   if (cl) {
     // values read in full (right operands, GEMV x), loop-carried ones included
     const auto& vo = q.r.ops;
@@ -1385,8 +1434,10 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
     cflags = cluster_flags(ops, bcast);
   }
   // device encoding: modes decided here, constants in a side table
-  std::vector<DOp> dev_ops(ops.size());
-  std::vector<double> csts = {0.0};  // slot 0: unused default
+  std::vector<DOp>& dev_ops = bt.dev_ops;
+  dev_ops.resize(ops.size());
+  std::vector<double>& csts = bt.csts;
+  csts = {0.0};  // slot 0: unused default
   for (size_t k = 0; k < ops.size(); ++k) {
     const BOp& o = ops[k];
     DOp& d = dev_ops[k];
@@ -1426,12 +1477,47 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
                       (size_t)al.nvec * NP * sizeof(double) + dev_ops.size() * sizeof(DOp) +
                       csts.size() * sizeof(double);
   if (smem > 227 * 1024) throw Error(kEInval, "resident program needs too much shared memory");
+  bt.smem = smem;
+  const size_t op_bytes = dev_ops.size() * sizeof(DOp);
+  bt.blob.assign(op_bytes + csts.size() * sizeof(double), '\0');
+  std::memcpy(&bt.blob[0], dev_ops.data(), op_bytes);
+  std::memcpy(&bt.blob[op_bytes], csts.data(), csts.size() * sizeof(double));
+  return bt;
+}
 
+template <int NP>
+Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, const double* b,
+                const double* precond, const double* residual, int iters, const double* p_in,
+                const double* f_in, const double* theta_in, double* p_io, double* f_io,
+                double* theta_io, const ChunkGate* gate = nullptr) {
+  using Gm = Geo<NP>;
+  Counters per;
+  for (const BOp& o : q.r.ops) {
+    if (o.kind == OP_GEMM) per.mmm += 1;
+    if (o.kind == OP_GEMV) per.mvm += 1;
+  }
+  per.mmm *= iters;
+  per.mvm *= iters;
+  if (batch == 0) return per;
+  if (iters == 0) {  // outputs = inputs
+    const size_t mat = (size_t)batch * n * n * sizeof(double), vec = (size_t)batch * n * 8;
+    if (p_io != p_in) check(cudaMemcpyAsync(p_io, p_in, mat, cudaMemcpyDeviceToDevice, c.s), "copy");
+    if (f_io != f_in) check(cudaMemcpyAsync(f_io, f_in, mat, cudaMemcpyDeviceToDevice, c.s), "copy");
+    if (theta_io != theta_in)
+      check(cudaMemcpyAsync(theta_io, theta_in, vec, cudaMemcpyDeviceToDevice, c.s), "copy");
+    return per;
+  }
+  Built bt = build_program<NP>(q, batch, gate);
+  const std::vector<BOp>& ops = bt.ops;
+  const std::vector<DOp>& dev_ops = bt.dev_ops;
+  const std::vector<double>& csts = bt.csts;
+  const Alloc& al = bt.al;
+  const int cl = bt.cl;
+  const std::vector<uint8_t>& cflags = bt.cflags;
+  const size_t smem = bt.smem;
   // program + constants, uploaded once per distinct program (handle cache)
   const size_t op_bytes = dev_ops.size() * sizeof(DOp);
-  std::string blob(op_bytes + csts.size() * sizeof(double), '\0');
-  std::memcpy(&blob[0], dev_ops.data(), op_bytes);
-  std::memcpy(&blob[op_bytes], csts.data(), csts.size() * sizeof(double));
+  const std::string& blob = bt.blob;
   void* prog_dev = nullptr;
   {
     auto it = c.h->programs.find(blob);
@@ -1553,7 +1639,22 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
     check(cudaMemsetAsync(counter.v.p, 0, sizeof(unsigned long long), c.s), "memset");
     args.sys_counter = reinterpret_cast<unsigned long long*>(counter.v.p);
   }
-  resident_kernel<NP><<<(unsigned)grid, Gm::THREADS, smem, c.s>>>(args);
+  bool fixed = false;
+#ifdef SI_HAVE_FIXED_C2
+  // the launcher's program is byte for byte the baked one: straight-line kernel
+  if constexpr (NP == 32) {
+    if (!want_prof && !(gate && gate->ready) && !fixed_disabled() &&
+        blob.size() == sizeof(FixedC2::blob) &&
+        std::memcmp(blob.data(), FixedC2::blob, blob.size()) == 0) {
+      check(cudaFuncSetAttribute(resident_kernel<NP, FixedC2>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+            "cudaFuncSetAttribute");
+      resident_kernel<NP, FixedC2><<<(unsigned)grid, Gm::THREADS, smem, c.s>>>(args);
+      fixed = true;
+    }
+  }
+#endif
+  if (!fixed) resident_kernel<NP><<<(unsigned)grid, Gm::THREADS, smem, c.s>>>(args);
   if (want_prof) {
     std::vector<long long> h(kMaxOps + 1);
     check(cudaMemcpy(h.data(), prof, sizeof(long long) * (kMaxOps + 1), cudaMemcpyDeviceToHost),
@@ -1576,13 +1677,10 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
 
 }  // namespace
 
-Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const double* a,
-                                      const double* b, const double* precond,
-                                      const double* residual, const std::vector<int>& rates,
-                                      const std::vector<const PlanNode*>& plans, int order_n,
-                                      int iters, const double* p_in, const double* f_in,
-                                      const double* theta_in, double* p_io, double* f_io,
-                                      double* theta_io, const ChunkGate* gate) {
+namespace {
+
+Recipe composite_recipe(const std::vector<int>& rates, const std::vector<const PlanNode*>& plans,
+                        int order_n) {
   Recipe q = new_recipe();
   record_plain(q);
   // composite_step (newton_schulz.py:177-228).  The NS part S_n(F) G is
@@ -1616,6 +1714,50 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
   q.gn = q.r.gemm(rc, nsp, 1.0, tc, 1.0);
   q.fn = q.r.residual(q.gn, q.A);
   defer_theta_update(q);
+  return q;
+}
+
+}  // namespace
+
+std::string resident_program_source(int64_t n, const std::vector<int>& rates,
+                                    const std::vector<const PlanNode*>& plans, int order_n) {
+  if (n > 32) throw Error(kEInval, "the baked program is for n <= 32");
+  Recipe q = composite_recipe(rates, plans, order_n);
+  Built bt = build_program<32>(q, int64_t(1) << 30, nullptr);
+  std::string out;
+  char buf[256];
+  std::snprintf(buf, sizeof(buf),
+                "  static constexpr bool kFixed = true;\n  static constexpr int nops = %zu;\n"
+                "  static constexpr DOp ops[%zu] = {\n",
+                bt.dev_ops.size(), bt.dev_ops.size());
+  out += buf;
+  for (const DOp& d : bt.dev_ops) {
+    std::snprintf(buf, sizeof(buf),
+                  "      {%d, %d, %d, %d, %d, %d, %d, %d, {%d, %d, %d, %d, %d, %d}, %d, %d, {0, 0}},\n",
+                  d.kind, d.mode, d.sync, d.nterms, d.dst, d.a, d.b, d.c, d.t[0], d.t[1], d.t[2],
+                  d.t[3], d.t[4], d.t[5], d.cidx, d.prebar);
+    out += buf;
+  }
+  out += "  };\n";
+  std::snprintf(buf, sizeof(buf), "  static constexpr unsigned char blob[%zu] = {", bt.blob.size());
+  out += buf;
+  for (size_t i = 0; i < bt.blob.size(); ++i) {
+    std::snprintf(buf, sizeof(buf), "%s%s%u", i ? "," : "", i % 24 == 0 ? "\n      " : "",
+                  (unsigned)(unsigned char)bt.blob[i]);
+    out += buf;
+  }
+  out += "};\n";
+  return out;
+}
+
+Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const double* a,
+                                      const double* b, const double* precond,
+                                      const double* residual, const std::vector<int>& rates,
+                                      const std::vector<const PlanNode*>& plans, int order_n,
+                                      int iters, const double* p_in, const double* f_in,
+                                      const double* theta_in, double* p_io, double* f_io,
+                                      double* theta_io, const ChunkGate* gate) {
+  Recipe q = composite_recipe(rates, plans, order_n);
   if (n <= 32)
     return launch<32>(c, q, batch, n, a, b, precond, residual, iters, p_in, f_in, theta_in, p_io,
                       f_io, theta_io, gate);

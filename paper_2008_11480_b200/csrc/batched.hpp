@@ -1,4 +1,5 @@
 #pragma once
+#include <string>
 #include <vector>
 
 #include "engine.hpp"
@@ -37,5 +38,11 @@ Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a
                                const double* f_in, const double* theta_in, double* p_out,
                                double* f_out, double* theta_out);
 // Inputs may equal outputs (in place).
+
+// The body of a compile-time program struct (FX of resident_kernel) for the
+// composite recipe at n <= 32: the scheduled, slot-allocated op list and the
+// bytes the launcher matches it against (tools/gen_resident_fixed.py).
+std::string resident_program_source(int64_t n, const std::vector<int>& rates,
+                                    const std::vector<const PlanNode*>& plans, int order_n);
 
 }  // namespace si

@@ -1126,6 +1126,27 @@ int si_batched_composite_richardson_gated(
   });
 }
 
+int si_resident_program_source(int64_t n, int nrates, const int32_t* rates, const int32_t* plans,
+                               const int64_t* plan_offsets, const double* consts,
+                               int64_t nconsts, int order_n, char* out, int64_t cap,
+                               int64_t* len) {
+  return guard([&] {
+    need(rates && len && nrates >= 1 && nrates <= kBatchMaxRates && order_n >= 1, "bad arguments");
+    std::vector<int> rv(rates, rates + nrates);
+    std::vector<PlanPtr> owned(nrates);
+    std::vector<const PlanNode*> pv(nrates, nullptr);
+    for (int i = 0; i < nrates; ++i)
+      if (plans && plan_offsets && plan_offsets[i + 1] > plan_offsets[i]) {
+        owned[i] = decode_plan(plans + plan_offsets[i], plan_offsets[i + 1] - plan_offsets[i],
+                               consts, nconsts);
+        pv[i] = owned[i].get();
+      }
+    const std::string src = resident_program_source(n, rv, pv, order_n);
+    *len = (int64_t)src.size();
+    if (out && cap > (int64_t)src.size()) std::memcpy(out, src.c_str(), src.size() + 1);
+  });
+}
+
 int si_batched_ns_richardson(si_handle h, int64_t batch, int64_t n, const double* a,
                              const double* b, int order, const int32_t* plan, int64_t plan_len,
                              const double* consts, int64_t nconsts, int iters, double* p_io,
