@@ -757,6 +757,59 @@ class Workload:
         d2h = sum(v.numel() * 8 for v in host["out"].values())
         return h2d, d2h
 
+    def pinned_inputs_c5(self):
+        """c5: the numpy-facing call's inputs (A, b, theta and the six carried
+        state matrices) and outputs in pinned host memory; the device copy of
+        the state is released (the GPU holds one state at a time: 8.6 GB per
+        matrix)."""
+        import torch
+
+        def pin(t):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            return h
+
+        st = self.st
+        inner = st.inner
+        host = {"in": {"a": pin(self.sp.matrix), "b": pin(self.b), "theta": pin(st.theta),
+                       "g": pin(inner.estimate), "f": pin(inner.residual),
+                       "l": pin(inner.accel_estimate), "r": pin(inner.accel_residual),
+                       "omega": pin(st.omega), "ns": pin(st.ns_part)}}
+        host["out"] = {k: torch.empty_like(host["in"][k], pin_memory=True)
+                       for k in ("theta", "g", "f", "l", "r", "omega", "ns")}
+        self.st = None
+        self.sp = None
+        self.b = None
+        torch.cuda.empty_cache()
+        return host
+
+    def e2e_step_c5(self, host):
+        """One steady-state recursive step (factorised order 16, the bench DAG)
+        through the public API from host buffers: H2D of the inputs, the step,
+        D2H of the new state and theta."""
+        import torch
+
+        P = self.P
+        dev = torch.device("cuda", torch.cuda.current_device())
+        d = {k: v.to(dev, non_blocking=True) for k, v in host["in"].items()}
+        inner = P.DoubleNsState(estimate=d["g"], residual=d["f"], accel_estimate=d["l"],
+                                accel_residual=d["r"], step=1, order=16, series_order=1,
+                                ctr=P.MulCounter())
+        st = P.RichardsonState(theta=d["theta"], inner=inner, q=16, omega=d["omega"],
+                               ns_part=d["ns"], step=1, ctr=inner.ctr)
+        a, b = d.pop("a"), d.pop("b")
+        del d
+        new = P.richardson_recursive_step(st, a, b, factor_plan=self.plan16, doubling_sum=True)
+        del st, inner
+        out = host["out"]
+        for k, v in (("theta", new.theta), ("g", new.inner.estimate), ("f", new.inner.residual),
+                     ("l", new.inner.accel_estimate), ("r", new.inner.accel_residual),
+                     ("omega", new.omega), ("ns", new.ns_part)):
+            out[k].copy_(v, non_blocking=True)
+        h2d = sum(v.numel() * 8 for v in host["in"].values())
+        d2h = sum(v.numel() * 8 for v in out.values())
+        return h2d, d2h
+
     def pinned_inputs(self):
         import torch
 
@@ -1190,6 +1243,25 @@ def run_ours(args):
         e2e = {"value": world * ksteps / (e_ms / 1e3), "unit": "iters/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": ksteps}
         del host
+
+    if not args.no_e2e and args.config == "c5" and w.sharded is None:
+        try:
+            host = w.pinned_inputs_c5()
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            h2d, d2h = w.e2e_step_c5(host)  # one step: ~37 s
+            f1.record(stream)
+            torch.cuda.synchronize()
+            e_ms = max_over_ranks(f0.elapsed_time(f1), world)
+            e2e = {"value": world / (e_ms / 1e3), "unit": "iters/s",
+                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": 1,
+                   "note": "copies not overlapped with the step (A, b, theta and the six "
+                           "carried n x n matrices in, the new state and theta out)"}
+            del host
+        except (RuntimeError, MemoryError) as exc:  # pinned host memory exhausted, ...
+            e2e = {"unavailable": f"c5 e2e failed: {exc}"[:200]}
+        # (the device state was released for the e2e copies: c5 ends here)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.hoist:

@@ -196,11 +196,12 @@ __device__ __forceinline__ double apply_epi(double acc, double alpha, double bet
   return v;
 }
 
-__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& tm, int& tn) {
-  const int per_group = GROUP_M * num_n;
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int group_m, int& tm,
+                                            int& tn) {
+  const int per_group = group_m * num_n;
   const int group = tile / per_group;
-  const int first_m = group * GROUP_M;
-  const int gsize = min(num_m - first_m, GROUP_M);
+  const int first_m = group * group_m;
+  const int gsize = min(num_m - first_m, group_m);
   const int r = tile % per_group;
   tm = first_m + r % gsize;
   tn = r / gsize;
@@ -213,7 +214,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                         int64_t ldd, const double* __restrict__ C, int64_t ldc, int M, int N,
                         int K, double alpha, double beta, double diag, int64_t doff,
                         const __grid_constant__ PanelWait pw,
-                        const __grid_constant__ PanelWait pwa, SyncSet* __restrict__ sync) {
+                        const __grid_constant__ PanelWait pwa, SyncSet* __restrict__ sync,
+                        int group_m) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       int g = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         int tm, tn;
-        tile_coords(tile, num_m, num_n, tm, tn);
+        tile_coords(tile, num_m, num_n, group_m, tm, tn);
         const int n0 = tn * BN;
         if (~known_a) panel_gate(pwa, tm * BM, min(M, tm * BM + BM), known_a);
         const int nboxes = min(8, (N - n0 + 15) / 16);
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t phase = 0;
   for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
     int tm, tn;
-    tile_coords(tile, num_m, num_n, tm, tn);
+    tile_coords(tile, num_m, num_n, group_m, tm, tn);
     double acc[8][4][2];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -551,6 +553,18 @@ bool lockstep_disabled() {
   return off;
 }
 
+// Row tiles per rasterisation group (a wave of 148 tiles spans GROUP_M row
+// panels x 148 / GROUP_M column panels); SI_GEMM_GROUP_M overrides (A/B
+// measurements of DRAM traffic; the tile -> CTA map changes, no result does)
+int group_m() {
+  static const int g = [] {
+    const char* v = std::getenv("SI_GEMM_GROUP_M");
+    const int x = v ? std::atoi(v) : GROUP_M;
+    return x >= 1 ? x : GROUP_M;
+  }();
+  return g;
+}
+
 int num_sms() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -611,7 +625,7 @@ cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& 
   auto kern = epi == 1 ? gemm_f64_tma_kernel<1> : gemm_f64_tma_kernel<0>;
   kern<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, D.p, D.ld, e.c, e.ldc, M, N, K,
                                                         e.alpha, e.beta, e.diag, e.doff, gate,
-                                                        gate_a, sync);
+                                                        gate_a, sync, group_m());
   return cudaGetLastError();
 }
 

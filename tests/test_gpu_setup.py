@@ -114,11 +114,11 @@ def test_pd_full_size_verdicts_vs_oracle():
           f"TFLOP/s of n^3/3)")
     a_np = a.cpu().numpy()
     assert ok and idx == -1
-    assert O.is_positive_definite_blocked(a_np)
+    assert O.is_positive_definite_blocked(a_np, nb=1024)
     a -= 2.0 * torch.eye(n, dtype=torch.float64, device="cuda")
     ok2, idx2, piv2 = _pd_info(a)
     assert not ok2 and piv2 <= 1e-12 * float(torch.max(torch.sum(torch.abs(a), dim=1)))
-    assert not O.is_positive_definite_blocked(a_np - 2.0 * np.eye(n))
+    assert not O.is_positive_definite_blocked(a_np - 2.0 * np.eye(n), nb=1024)
     del a_np
     # exactly singular pivot in the middle: [[1, 1], [1, 1 + 1e-16]] at 8000
     a += 2.0 * torch.eye(n, dtype=torch.float64, device="cuda")
@@ -129,7 +129,7 @@ def test_pd_full_size_verdicts_vs_oracle():
     ok3, idx3, piv3 = _pd_info(a)
     dt3 = time.perf_counter() - t0
     assert not ok3 and idx3 == 8001 and piv3 == 0.0
-    assert not O.is_positive_definite_blocked(a.cpu().numpy())
+    assert not O.is_positive_definite_blocked(a.cpu().numpy(), nb=1024)
     print(f"singular pivot at 8001 found in {dt3 * 1e3:.1f} ms (early exit)")
 
 
