@@ -349,7 +349,12 @@ class Workload:
             raise ValueError(cfg)
         self.a = a
         self.b = b
-        self.sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False, verify=False)
+        # the reference's full setup (splitting.py:124-146, :58-64): fused symmetry
+        # check, blocked-Cholesky PD check, the verification product -- untimed
+        t_setup = time.perf_counter()
+        self.sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=True, verify=True)
+        torch.cuda.synchronize()
+        self.setup_s = time.perf_counter() - t_setup
         self.sharded = None
         if self.world > 1 and cfg == "c4" and self.shard == "parts":
             # composite parts on GPU groups + one ordered (t, r) tree reduction
@@ -1294,6 +1299,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches.value,
+            "setup_s": getattr(w, "setup_s", None),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

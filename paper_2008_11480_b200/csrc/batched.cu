@@ -405,10 +405,15 @@ Alloc assign(const Rec& r, const std::vector<int>& pinned,
     const bool vec = r.is_vec[o.dst];
     if (al.phys[o.dst] < 0) {
       // in place over an operand that dies here (the carried input first)
+      // (preference: the carried input itself, then an operand that sits in the
+      // carried input's slot -- the next value lands where the next iteration
+      // reads it, so no carry copy is needed -- then the first candidate)
       int reuse = -1;
+      const int home = out_of[o.dst] >= 0 ? al.phys[out_of[o.dst]] : -1;
+      auto rank = [&](int v) { return v == out_of[o.dst] ? 2 : (home >= 0 && al.phys[v] == home); };
       for (int v : inplace_operands(o, ab)) {
         if (v < 0 || r.is_vec[v] != vec || al.phys[v] < 0 || last[v] != i) continue;
-        if (reuse < 0 || v == out_of[o.dst]) reuse = v;
+        if (reuse < 0 || rank(v) > rank(reuse)) reuse = v;
       }
       if (reuse >= 0) {
         al.phys[o.dst] = al.phys[reuse];
