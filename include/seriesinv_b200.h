@@ -193,6 +193,11 @@ SI_API int si_resident_program_source(int64_t n, int nrates, const int32_t* rate
                                       const double* consts, int64_t nconsts, int order_n,
                                       char* out, int64_t cap, int64_t* len);
 
+/* ... and of the config-1 cluster kernel (NS order `order`, 32 < n <= 64,
+ * `cluster` CTAs per system; csrc/resident_fixed_c1.inc). */
+SI_API int si_resident_program_source_ns(int64_t n, int order, int cluster, char* out,
+                                         int64_t cap, int64_t* len);
+
 /* ---------------- block-row sharded steps (several GPUs) ----------------
  * One rank per GPU.  Every state matrix (G, F, L, R, omega, N) is split into
  * contiguous row blocks -- rank r owns rows [r0, r1) of the near-equal split

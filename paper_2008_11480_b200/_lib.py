@@ -55,6 +55,7 @@ SIGNATURES: dict[str, list] = {
     "si_is_positive_definite": [_P, _I64, _P, _I64, _D, _I, POINTER(c_int), _PI64,
                                 POINTER(c_double), _P],
     "si_resident_program_source": [_I64, _I, _P, _P, _P, _P, _I64, _I, _P, _I64, _PI64],
+    "si_resident_program_source_ns": [_I64, _I, _I, _P, _I64, _PI64],
     "si_comm_unique_id": [_P],
     "si_comm_create_nccl": [_P, _I, _I, _P, _I64, POINTER(c_void_p)],
     "si_comm_create_callback": [_I, _I, _I64, _P, _P, _P, POINTER(c_void_p)],

@@ -700,6 +700,13 @@ struct FixedC2 {
 };
 #define SI_HAVE_FIXED_C2 1
 #endif
+#if __has_include("resident_fixed_c1.inc")
+// BASELINE config 1's program (one 64 x 64 system, NS order 3, 8-CTA cluster)
+struct FixedC1 {
+#include "resident_fixed_c1.inc"
+};
+#define SI_HAVE_FIXED_C1 1
+#endif
 
 template <class F, int... K>
 __device__ __forceinline__ void static_for(F&& f, std::integer_sequence<int, K...>) {
@@ -1044,7 +1051,7 @@ __device__ __forceinline__ void gemm_rows(const double* A, const double* B, cons
     }
 }
 
-template <int CL>
+template <int CL, class FX = NoFixed>
 __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(BatchArgs p) {
   constexpr int NP = 64, RB = NP / CL, TH = kClusterThreads;
   using G = Geo<64>;
@@ -1085,9 +1092,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(Ba
       vslot(p.sb)[threadIdx.x] = threadIdx.x < n ? p.b[sys * n + threadIdx.x] : 0.0;
     }
     cluster_sync_all();  // every CTA of the cluster is running and loaded
-    for (int it = 0; it < p.iters; ++it) {
-      for (int k = 0; k < p.nops; ++k) {
-        const DOp o = prog[k];
+    // one op; `o` is a compile-time constant on the fixed path (FX::kFixed)
+    auto exec = [&](const DOp& o, int k) {
         const double* oc = cst + o.cidx;
         const bool bc = (o.sync & kBcast) != 0;
         if (o.kind == OP_GEMM) {
@@ -1134,7 +1140,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(Ba
             const int row = rbase + threadIdx.x;
             double acc = 0.0;
             for (int j = 0; j < o.nterms; ++j) {
-              const double xv = vslot(prog[k].t[j])[row];
+              const double xv = vslot((FX::kFixed ? o.t[j] : prog[k].t[j]))[row];
               acc = __dadd_rn(acc, oc[1 + j] == 1.0 ? xv : __dmul_rn(oc[1 + j], xv));
             }
             double* dp = vslot(o.dst) + row;
@@ -1150,7 +1156,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(Ba
             const int c = G::col_at(r, i % NP);
             double acc = (r == c && r < n) ? oc[0] : 0.0;
             for (int j = 0; j < o.nterms; ++j) {
-              const double xv = mslot(prog[k].t[j])[i];
+              const double xv = mslot((FX::kFixed ? o.t[j] : prog[k].t[j]))[i];
               acc = __dadd_rn(acc, oc[1 + j] == 1.0 ? xv : __dmul_rn(oc[1 + j], xv));
             }
             D[i] = acc;
@@ -1167,6 +1173,21 @@ __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(Ba
           const long long now = clock64();
           prof_acc[k] += now - prof_last;
           prof_last = now;
+        }
+    };
+    for (int it = 0; it < p.iters; ++it) {
+      if constexpr (FX::kFixed) {
+        static_for(
+            [&](auto kc) {
+              constexpr int k = decltype(kc)::value;
+              constexpr DOp o = FX::ops[k];
+              exec(o, k);
+            },
+            std::make_integer_sequence<int, FX::nops>{});
+      } else {
+        for (int k = 0; k < p.nops; ++k) {
+          const DOp o = prog[k];
+          exec(o, k);
         }
       }
       if (p.rG != p.sG || p.rF != p.sF || p.rT != p.sT) {  // carries (full local copies)
@@ -1347,7 +1368,7 @@ struct Built {
 };
 
 template <int NP>
-Built build_program(Recipe& q, int64_t batch, const ChunkGate* gate) {
+Built build_program(Recipe& q, int64_t batch, const ChunkGate* gate, int force_cl = -1) {
   using Gm = Geo<NP>;
   if ((int)q.r.ops.size() > kMaxOps) throw Error(kEInval, "resident program too long");
 
@@ -1414,7 +1435,9 @@ Built build_program(Recipe& q, int64_t batch, const ChunkGate* gate) {
   int& cl = bt.cl;
   if (NP == 64) {
     const char* env = std::getenv("SI_RESIDENT_CLUSTER");
-    if (env) {
+    if (force_cl >= 0) {
+      cl = force_cl;  // (build tooling: no device to ask for its SM count)
+    } else if (env) {
       cl = std::atoi(env);
       if (cl != 0 && cl != 2 && cl != 4 && cl != 8) cl = 0;
     } else if (batch * 8 <= num_sms_b()) {
@@ -1584,6 +1607,13 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
   if (cl) {
     auto kern = cl == 2 ? resident_cluster_kernel<2>
                 : cl == 4 ? resident_cluster_kernel<4> : resident_cluster_kernel<8>;
+#ifdef SI_HAVE_FIXED_C1
+    // the program is byte for byte the baked config-1 one: straight-line kernel
+    if (cl == 8 && !fixed_disabled() && std::getenv("SI_RESIDENT_PROF") == nullptr &&
+        blob.size() == sizeof(FixedC1::blob) &&
+        std::memcmp(blob.data(), FixedC1::blob, blob.size()) == 0)
+      kern = resident_cluster_kernel<8, FixedC1>;
+#endif
     check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
           "cudaFuncSetAttribute");
     long long* cprof = nullptr;
@@ -1724,11 +1754,8 @@ Recipe composite_recipe(const std::vector<int>& rates, const std::vector<const P
 
 }  // namespace
 
-std::string resident_program_source(int64_t n, const std::vector<int>& rates,
-                                    const std::vector<const PlanNode*>& plans, int order_n) {
-  if (n > 32) throw Error(kEInval, "the baked program is for n <= 32");
-  Recipe q = composite_recipe(rates, plans, order_n);
-  Built bt = build_program<32>(q, int64_t(1) << 30, nullptr);
+namespace {
+std::string program_source(const Built& bt) {
   std::string out;
   char buf[256];
   std::snprintf(buf, sizeof(buf),
@@ -1754,6 +1781,15 @@ std::string resident_program_source(int64_t n, const std::vector<int>& rates,
   out += "};\n";
   return out;
 }
+}  // namespace
+
+std::string resident_program_source(int64_t n, const std::vector<int>& rates,
+                                    const std::vector<const PlanNode*>& plans, int order_n) {
+  if (n > 32) throw Error(kEInval, "the baked program is for n <= 32");
+  Recipe q = composite_recipe(rates, plans, order_n);
+  Built bt = build_program<32>(q, int64_t(1) << 30, nullptr);
+  return program_source(bt);
+}
 
 Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const double* a,
                                       const double* b, const double* precond,
@@ -1770,10 +1806,8 @@ Counters batched_composite_richardson(Ctx& c, int64_t batch, int64_t n, const do
                     f_io, theta_io, gate);
 }
 
-Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a, const double* b,
-                               int order, const PlanNode* plan, int iters, const double* p_in,
-                               const double* f_in, const double* theta_in, double* p_io,
-                               double* f_io, double* theta_io) {
+namespace {
+Recipe ns_recipe(int order, const PlanNode* plan) {
   Recipe q = new_recipe();
   record_plain(q);
   // ns_step (newton_schulz.py:150-174)
@@ -1783,6 +1817,22 @@ Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a
   // (no defer_theta_update here: in the cluster kernel the deferred GEMV
   // reads G, whose slot the next product overwrites in place -- a barrier
   // either way -- and the config-1 iteration measured slower)
+  return q;
+}
+}  // namespace
+
+std::string resident_program_source_ns(int64_t n, int order, int cl) {
+  if (n <= 32 || n > 64) throw Error(kEInval, "the baked cluster program is for 32 < n <= 64");
+  Recipe q = ns_recipe(order, nullptr);
+  Built bt = build_program<64>(q, 1, nullptr, cl);
+  return program_source(bt);
+}
+
+Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a, const double* b,
+                               int order, const PlanNode* plan, int iters, const double* p_in,
+                               const double* f_in, const double* theta_in, double* p_io,
+                               double* f_io, double* theta_io) {
+  Recipe q = ns_recipe(order, plan);
   if (n <= 32)
     return launch<32>(c, q, batch, n, a, b, nullptr, nullptr, iters, p_in, f_in, theta_in, p_io,
                       f_io, theta_io);

@@ -44,5 +44,7 @@ Counters batched_ns_richardson(Ctx& c, int64_t batch, int64_t n, const double* a
 // bytes the launcher matches it against (tools/gen_resident_fixed.py).
 std::string resident_program_source(int64_t n, const std::vector<int>& rates,
                                     const std::vector<const PlanNode*>& plans, int order_n);
+// ... and for the NS recipe of config 1 (32 < n <= 64) in cluster mode with `cl` CTAs.
+std::string resident_program_source_ns(int64_t n, int order, int cl);
 
 }  // namespace si

@@ -1147,6 +1147,16 @@ int si_resident_program_source(int64_t n, int nrates, const int32_t* rates, cons
   });
 }
 
+int si_resident_program_source_ns(int64_t n, int order, int cluster, char* out, int64_t cap,
+                                  int64_t* len) {
+  return guard([&] {
+    need(len && order >= 1 && (cluster == 2 || cluster == 4 || cluster == 8), "bad arguments");
+    const std::string src = resident_program_source_ns(n, order, cluster);
+    *len = (int64_t)src.size();
+    if (out && cap > (int64_t)src.size()) std::memcpy(out, src.c_str(), src.size() + 1);
+  });
+}
+
 int si_batched_ns_richardson(si_handle h, int64_t batch, int64_t n, const double* a,
                              const double* b, int order, const int32_t* plan, int64_t plan_len,
                              const double* consts, int64_t nconsts, int iters, double* p_io,
