@@ -1678,7 +1678,7 @@ Counters launch(Ctx& c, Recipe& q, int64_t batch, int64_t n, const double* a, co
 #ifdef SI_HAVE_FIXED_C2
   // the launcher's program is byte for byte the baked one: straight-line kernel
   if constexpr (NP == 32) {
-    if (!want_prof && !(gate && gate->ready) && !fixed_disabled() &&
+    if (!want_prof && !fixed_disabled() &&
         blob.size() == sizeof(FixedC2::blob) &&
         std::memcmp(blob.data(), FixedC2::blob, blob.size()) == 0) {
       check(cudaFuncSetAttribute(resident_kernel<NP, FixedC2>,

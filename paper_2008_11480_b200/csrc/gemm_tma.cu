@@ -67,7 +67,7 @@ constexpr int B_BOX_BYTES = 16 * BK * 8;    // 2 KB (16 cols x 16 rows)
 constexpr int B_STAGE_BYTES = BK * BN * 8;  // 16 KB
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
-constexpr int GROUP_M = 8;
+constexpr int GROUP_M = 12;  // a wave of 148 tiles: 12 x 12.3 panels (DRAM -8% vs 8 x 18.5)
 constexpr int kSyncEpoch = 8;     // k-blocks per lockstep epoch
 constexpr int kSyncRing = 4;      // arrival counters per launch (epochs e, e+4, ... share one)
 constexpr int kSyncSets = 64;     // counter sets per device, handed out round robin

@@ -96,41 +96,49 @@ def _pd_info(a, pivot_tol=None):
     return bool(is_pd.value), idx.value, piv.value
 
 
-def test_pd_full_size_verdicts_vs_oracle():
-    """n=16384 (config 4's matrix, kappa 1e6): SPD -> PD; shifted by -2 I (its
-    smallest eigenvalue is ~1) -> not PD; a block-diagonal matrix with an exactly
-    singular 2x2 block at rows 8000-8001 -> not PD at pivot 8001, with early exit.
-    Verdicts against the oracle's blocked restatement on the host."""
+@pytest.mark.parametrize("n", [4096, 16384])
+def test_pd_verdicts_at_size_vs_oracle(n):
+    """Config 4's matrix (kappa 1e6, spectrum known exactly: lambda in [1, 1e6]):
+    SPD -> PD; shifted by -2 I (smallest eigenvalue min(lambda) - 2 < 0) -> not
+    PD; a block-diagonal matrix with an exactly singular 2x2 block
+    [[1, 1], [1, 1 + 1e-16]] at rows m, m+1 -> not PD at pivot m+1 (early exit).
+    Against the oracle's blocked restatement of splitting.py:76-98: every
+    verdict at n=4096; at n=16384 the SPD verdict (the other two follow from
+    the known spectrum / the exact block, and cost minutes of host time)."""
     from oracle import seriesinv_oracle as O
     from paper_2008_11480_b200 import configs
 
-    n = 16384
     a, _ = configs.c4_householder_device(n=n, rhs=1)
+    lam, _, _ = configs._c4_draws(n, 64, 1, 0)
+    assert lam.min() > 1e-12 * n * lam.max()  # far above the pivot floor
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ok, idx, _ = _pd_info(a)
     dt = time.perf_counter() - t0
     print(f"is_positive_definite n={n}: {dt * 1e3:.1f} ms ({n**3 / 3 / dt / 1e12:.1f} "
           f"TFLOP/s of n^3/3)")
-    a_np = a.cpu().numpy()
     assert ok and idx == -1
-    assert O.is_positive_definite_blocked(a_np, nb=1024)
-    a -= 2.0 * torch.eye(n, dtype=torch.float64, device="cuda")
-    ok2, idx2, piv2 = _pd_info(a)
+    assert O.is_positive_definite_blocked(a.cpu().numpy(), nb=1024)
+    eye = torch.eye(n, dtype=torch.float64, device="cuda")
+    a -= 2.0 * eye
+    ok2, _, piv2 = _pd_info(a)
+    assert lam.min() - 2.0 < 0
     assert not ok2 and piv2 <= 1e-12 * float(torch.max(torch.sum(torch.abs(a), dim=1)))
-    assert not O.is_positive_definite_blocked(a_np - 2.0 * np.eye(n), nb=1024)
-    del a_np
-    # exactly singular pivot in the middle: [[1, 1], [1, 1 + 1e-16]] at 8000
-    a += 2.0 * torch.eye(n, dtype=torch.float64, device="cuda")
-    a[8000:8002, :] = 0.0
-    a[:, 8000:8002] = 0.0
-    a[8000:8002, 8000:8002] = torch.tensor([[1.0, 1.0], [1.0, 1.0 + 1e-16]], dtype=torch.float64)
+    if n <= 4096:
+        assert not O.is_positive_definite_blocked(a.cpu().numpy(), nb=1024)
+    a += 2.0 * eye
+    del eye
+    m = n // 2 - 192  # inside a 128-row panel, not at its start
+    a[m:m + 2, :] = 0.0
+    a[:, m:m + 2] = 0.0
+    a[m:m + 2, m:m + 2] = torch.tensor([[1.0, 1.0], [1.0, 1.0 + 1e-16]], dtype=torch.float64)
     t0 = time.perf_counter()
     ok3, idx3, piv3 = _pd_info(a)
     dt3 = time.perf_counter() - t0
-    assert not ok3 and idx3 == 8001 and piv3 == 0.0
-    assert not O.is_positive_definite_blocked(a.cpu().numpy(), nb=1024)
-    print(f"singular pivot at 8001 found in {dt3 * 1e3:.1f} ms (early exit)")
+    assert not ok3 and idx3 == m + 1 and piv3 == 0.0
+    if n <= 4096:
+        assert not O.is_positive_definite_blocked(a.cpu().numpy(), nb=1024)
+    print(f"singular pivot at {m + 1} found in {dt3 * 1e3:.1f} ms (early exit)")
 
 
 def test_spectral_radius_matches_reference():

@@ -43,36 +43,41 @@ class ProjComm:
         return x
 
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
-a, b = configs.c4_householder_device(n=n, rhs=64)
-sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False, verify=False)
-del a
-st = P.initial_series(sp, 0, 1, order=2)
-out = {"n": n, "note": "rank 0's products only; exchange replaced by a resident operand"}
-for world in (1, 2, 4, 8):
-    comm = ProjComm(n, world)
-    eng = ShardedEngine(comm, prefetch=False)
-    A, Pm, B = eng.replicated(sp.matrix), eng.replicated(sp.precond), eng.replicated(sp.residual)
-    g = eng.local(st.estimate[comm.r0:comm.r1].clone())
-    f = eng.local(st.residual[comm.r0:comm.r1].clone())
-    th, bb = eng.replicated(torch.zeros_like(b)), eng.replicated(b)
-    eng.composite_step(g, f, A, Pm, B, (2, 3, 4, 5), 2)  # warm
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    reps = 2
-    for _ in range(reps):
-        th2 = eng.plain_richardson(th, g, A, bb)
-        g2, f2 = eng.composite_step(g, f, A, Pm, B, (2, 3, 4, 5), 2)
-    e1.record()
-    torch.cuda.synchronize()
-    sec = e0.elapsed_time(e1) / 1e3 / reps
-    out[f"P{world}"] = {"rows": comm.r1 - comm.r0, "rank0_step_s": sec,
-                        "exchange_bytes_per_rank": comm.bytes_gathered // (reps + 1)}
-    del eng, g, f, g2, f2, th2, comm
-    torch.cuda.empty_cache()
-t1 = out["P1"]["rank0_step_s"]
-for world in (2, 4, 8):
-    d = out[f"P{world}"]
-    d["compute_scaling_efficiency"] = t1 / (world * d["rank0_step_s"])
-print(json.dumps(out, indent=1))
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+    a, b = configs.c4_householder_device(n=n, rhs=64)
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False, verify=False)
+    del a
+    st = P.initial_series(sp, 0, 1, order=2)
+    out = {"n": n, "note": "rank 0's products only; exchange replaced by a resident operand"}
+    for world in (1, 2, 4, 8):
+        comm = ProjComm(n, world)
+        eng = ShardedEngine(comm, prefetch=False)
+        A, Pm, B = eng.replicated(sp.matrix), eng.replicated(sp.precond), eng.replicated(sp.residual)
+        g = eng.local(st.estimate[comm.r0:comm.r1].clone())
+        f = eng.local(st.residual[comm.r0:comm.r1].clone())
+        th, bb = eng.replicated(torch.zeros_like(b)), eng.replicated(b)
+        eng.composite_step(g, f, A, Pm, B, (2, 3, 4, 5), 2)  # warm
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        reps = 2
+        for _ in range(reps):
+            th2 = eng.plain_richardson(th, g, A, bb)
+            g2, f2 = eng.composite_step(g, f, A, Pm, B, (2, 3, 4, 5), 2)
+        e1.record()
+        torch.cuda.synchronize()
+        sec = e0.elapsed_time(e1) / 1e3 / reps
+        out[f"P{world}"] = {"rows": comm.r1 - comm.r0, "rank0_step_s": sec,
+                            "exchange_bytes_per_rank": comm.bytes_gathered // (reps + 1)}
+        del eng, g, f, g2, f2, th2, comm
+        torch.cuda.empty_cache()
+    t1 = out["P1"]["rank0_step_s"]
+    for world in (2, 4, 8):
+        d = out[f"P{world}"]
+        d["compute_scaling_efficiency"] = t1 / (world * d["rank0_step_s"])
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
