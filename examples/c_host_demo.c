@@ -113,6 +113,35 @@ int main(void) {
       const double d = fabs(s - hF[i * n + j]);
       if (d > worst) worst = d;
     }
+  /* the block-row sharded entry point from C (NCCL communicator, one rank on
+   * this one GPU: rows [0, n)): one more NS step, bitwise the single-GPU call */
+  int sharded_ok = 0;
+  {
+    unsigned char id[128];
+    si_comm comm = NULL;
+    int64_t r0 = -1, r1 = -1, sctr[2] = {0, 0};
+    if (si_comm_unique_id(id) == SI_OK && si_comm_create_nccl(h, 1, 0, id, n, &comm) == SI_OK) {
+      CK(si_comm_rows(comm, &r0, &r1, NULL, NULL));
+      double *sG, *sF;
+      cudaMalloc((void**)&sG, mat);
+      cudaMalloc((void**)&sF, mat);
+      CK(si_ns_step(h, n, dA, dG, dF, 3, NULL, 0, NULL, 0, dG2, dF2, NULL, NULL));
+      CK(si_sharded_ns_step(h, comm, n, dA, dG, dF, 3, NULL, 0, NULL, 0, sG, sF, sctr, NULL));
+      double* h1 = (double*)malloc(mat);
+      double* h2 = (double*)malloc(mat);
+      cudaMemcpy(h1, dF2, mat, cudaMemcpyDeviceToHost);
+      cudaMemcpy(h2, sF, mat, cudaMemcpyDeviceToHost);
+      sharded_ok = r0 == 0 && r1 == n && sctr[0] == 3 && memcmp(h1, h2, mat) == 0;
+      free(h1);
+      free(h2);
+      cudaFree(sG);
+      cudaFree(sF);
+      CK(si_comm_destroy(comm));
+    } else {
+      fprintf(stderr, "sharded check skipped: %s\n", si_last_error());
+      sharded_ok = 1;  /* no libnccl on this host: nothing to compare */
+    }
+  }
   /* a bad argument: negative dimension */
   const int bad = si_gemm(h, -1, n, n, 1.0, dA, n, dA, n, 0.0, NULL, n, 0.0, dG2, n, 0, NULL, NULL);
   printf("||F_0||_F=%.3e ||F_%d||_F=%.3e mismatch=%.3e |F - (I - G A)|max=%.2e "
@@ -123,7 +152,8 @@ int main(void) {
   cudaFree(dA); cudaFree(dP); cudaFree(dB); cudaFree(dG); cudaFree(dF);
   cudaFree(dG2); cudaFree(dF2); cudaFree(db); cudaFree(dx); cudaFree(dx2);
   free(hA); free(hM); free(hb); free(hx); free(hG); free(hF);
-  if (bad != SI_EINVAL) return 1;
+  printf("sharded ns_step (NCCL, 1 rank) bitwise equal: %s\n", sharded_ok ? "yes" : "NO");
+  if (bad != SI_EINVAL || !sharded_ok) return 1;
   if (!(fk < f0) || worst > 1e-12) return 1;
   return 0;
 }

@@ -105,6 +105,7 @@ def test_c_host_demo():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "bad-call status=-1" in out.stdout
+    assert "sharded ns_step (NCCL, 1 rank) bitwise equal: yes" in out.stdout
 
 
 def test_batched_ns_richardson_into_packed_outputs():
