@@ -78,3 +78,36 @@ def test_abi_rejects_bad_arguments_without_gpu():
     assert lib.si_gemm(None, 1, 1, 1, 1.0, None, 1, None, 1, 0.0, None, 1, 0.0, None, 1, 0, None,
                        None) == _lib.SI_EINVAL
     del buf
+
+
+def test_baked_resident_programs_are_current():
+    """The compile-time programs of the config-1/2 resident kernels
+    (csrc/resident_fixed_c*.inc, tools/gen_resident_fixed.py) equal what the
+    library's recorder / scheduler / allocator build today (host-only entry
+    points, no device): a stale file would silently fall back to the
+    interpreter."""
+    import ctypes
+    import os
+
+    from paper_2008_11480_b200 import _lib
+    from paper_2008_11480_b200.series_toolkit import encode_many, geometric_base_plan
+
+    lib = _lib.load_library()
+    csrc = os.path.join(os.path.dirname(_lib.__file__), "csrc")
+
+    def body(path):
+        with open(path) as fh:
+            return "".join(ln for ln in fh if not ln.startswith("//"))
+
+    code, offsets, consts = encode_many([geometric_base_plan(x) for x in (2, 3)])
+    n = ctypes.c_int64()
+    args = [32, 2, _lib.i32_array([2, 3]), _lib.i32_array(code), _lib.i64_array(offsets),
+            _lib.f64_array(consts), len(consts), 2]
+    assert lib.si_resident_program_source(*args, None, 0, ctypes.byref(n)) == 0
+    buf = ctypes.create_string_buffer(n.value + 1)
+    assert lib.si_resident_program_source(*args, buf, n.value + 1, ctypes.byref(n)) == 0
+    assert buf.value.decode() == body(os.path.join(csrc, "resident_fixed_c2.inc"))
+    assert lib.si_resident_program_source_ns(64, 3, 8, None, 0, ctypes.byref(n)) == 0
+    buf = ctypes.create_string_buffer(n.value + 1)
+    assert lib.si_resident_program_source_ns(64, 3, 8, buf, n.value + 1, ctypes.byref(n)) == 0
+    assert buf.value.decode() == body(os.path.join(csrc, "resident_fixed_c1.inc"))
