@@ -6,6 +6,7 @@
 #include "setup.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 
@@ -306,15 +307,18 @@ bool cholesky_pd(Ctx& c, const MV& a, double pivot_tol, bool default_tol, int64_
   check(cudaMemsetAsync(stat.v.p, 0, 2 * sizeof(double), c.s), "memset");
   MV wpanel = alloc(c, n, NB);
   MV wt = alloc(c, NB, ld);
-  static bool attr = false;
-  if (!attr) {
-    check(cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               NB * (NB + 1) * 8),
-          "cudaFuncSetAttribute");
-    check(cudaFuncSetAttribute(chol_trsm_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               NB * NB * 8),
-          "cudaFuncSetAttribute");
-    attr = true;
+  {  // opt-in shared memory of the two kernels, once per device
+    static std::atomic<uint64_t> attr_set{0};
+    const int dev = c.h->device;
+    if (dev >= 64 || !(attr_set.load() & (1ull << dev))) {
+      check(cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 NB * (NB + 1) * 8),
+            "cudaFuncSetAttribute");
+      check(cudaFuncSetAttribute(chol_trsm_kernel<NB>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, NB * NB * 8),
+            "cudaFuncSetAttribute");
+      if (dev < 64) attr_set.fetch_or(1ull << dev);
+    }
   }
   int hstat[4] = {0, 0, 0, 0};
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
