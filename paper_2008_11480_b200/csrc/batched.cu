@@ -986,7 +986,13 @@ __device__ __forceinline__ void gemm_rows(const double* A, const double* B, cons
   constexpr int CG = 8 / NTW, RG = 8 / CG;    // warp grid
   constexpr int MTW = RT / RG;                // row tiles per warp
   const int r0 = rbase + (warp / CG) * MTW * 8, c0 = (warp % CG) * NTW * 8;
+  // KS accumulator sets take the k-steps in turn (k-step s into set s % KS)
+  // and are summed in a fixed order at the end: with one 8 x 8 tile per warp
+  // (8-CTA clusters) the 16 dependent DMMAs of a single chain (26 cycles
+  // each) would set the op's latency
+  constexpr int KS = MTW * NTW == 1 ? 4 : 1;
   double acc[MTW][NTW][2];
+  double ex[KS > 1 ? KS - 1 : 1][2] = {};
 #pragma unroll
   for (int mi = 0; mi < MTW; ++mi)
 #pragma unroll
@@ -1017,11 +1023,21 @@ __device__ __forceinline__ void gemm_rows(const double* A, const double* B, cons
 #pragma unroll
       for (int ni = 0; ni < NTW; ++ni) bf[nxt][ni] = B[G::idx(kk + 4 + t, c0 + ni * 8 + g)];
     }
+    const int set = (kk >> 2) % KS;
+    if (KS > 1 && set > 0) {
+      dmma(ex[set - 1][0], ex[set - 1][1], af[cur][0], bf[cur][0]);
+      continue;
+    }
 #pragma unroll
     for (int mi = 0; mi < MTW; ++mi)
 #pragma unroll
       for (int ni = 0; ni < NTW; ++ni)
         dmma(acc[mi][ni][0], acc[mi][ni][1], af[cur][mi], bf[cur][ni]);
+  }
+  if constexpr (KS == 4) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      acc[0][0][h] = __dadd_rn(__dadd_rn(acc[0][0][h], ex[0][h]), __dadd_rn(ex[1][h], ex[2][h]));
   }
 #pragma unroll
   for (int mi = 0; mi < MTW; ++mi)
@@ -1112,16 +1128,17 @@ __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(Ba
             const double* A = mslot(o.a);
             const double* x = vslot(o.b);
             const int r0 = rbase + warp * 8;
-            double acc[2][2] = {};
+            double acc[4][2] = {};  // four interleaved chains of 4 dependent DMMAs
 #pragma unroll
             for (int kk = 0; kk < NP; kk += 4) {
               const double af = A[G::idx(r0 + g, kk + t)];
               const double bf = g == 0 ? x[kk + t] : 0.0;
-              dmma(acc[(kk >> 2) & 1][0], acc[(kk >> 2) & 1][1], af, bf);
+              dmma(acc[(kk >> 2) & 3][0], acc[(kk >> 2) & 3][1], af, bf);
             }
             if (t == 0) {
               const int row = r0 + g;
-              const double s = __dadd_rn(acc[0][0], acc[1][0]);
+              const double s = __dadd_rn(__dadd_rn(acc[0][0], acc[1][0]),
+                                         __dadd_rn(acc[2][0], acc[3][0]));
               const double cv = o.c >= 0 ? vslot(o.c)[row] : 0.0;
               const double v = o.mode == 1   ? __dsub_rn(s, cv)
                                : o.mode == 2 ? __dsub_rn(cv, s)
