@@ -46,3 +46,17 @@ def test_config_object_is_shared_by_both_arms():
         c = bench.config_obj(cfg, n)
         assert set(c) == {"workload", "n", "rhs"}
         assert c["workload"] == bench.workload_desc(cfg, n)
+
+
+def test_reference_arm_executes_full_steps_c4_c5():
+    """The reference arm's c4 / c5 legs execute full steps of the reference DAG
+    through the oracle (small n here) and report what was executed."""
+    for cfg, extra in (("c4", []), ("c5", [])):
+        out = _bench(["--impl", "reference", "--config", cfg, "--n", "256", "--steps", "2",
+                      "--warmup", "1", "--ref-budget", "60"] + extra)
+        assert out.returncode == 0, out.stderr[-2000:]
+        d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+        assert d["impl"] == "reference" and d["steps"] == d["executed_iterations"] == 2
+        assert len(d["step_seconds"]) == 2 and d["value"] > 0
+        assert d["config"]["n"] == 256 and set(d["config"]) == {"workload", "n", "rhs"}
+        assert "executed" in d["cpu_baseline"]["sample"]
