@@ -233,7 +233,8 @@ def make_comm(n: int, kind: str):
 
 _COMM_LABEL = {"peer": "copy-engine panel exchange, panel-gated products",
                "peer-stream": "copy-engine panel exchange, stream-gated products",
-               "nccl": "NCCL all-gather"}
+               "nccl": "NCCL all-gather",
+               "native": "library block-row engine (si_sharded_*), NCCL all-gather"}
 
 
 def workload_desc(cfg: str, n: int, batch: int = 16384) -> str:
@@ -266,6 +267,7 @@ class Workload:
         self.hoist = hoist
         self.comm_kind = comm
         self.sharded = None
+        self.native = None
         self.split_batch = False
         self.iters_per_step = 1
 
@@ -378,6 +380,42 @@ class Workload:
             self.workload += (f" [parts on {len(gc.groups)} GPU groups "
                               f"{[len(g) for g in gc.groups]}, segments {gc.segments}]")
             return
+        if self.world > 1 and cfg in ("c4", "c3", "c5") and self.comm_kind == "native":
+            # the same block-row DAG orchestrated inside the library (si_sharded_*,
+            # NCCL all-gathers; on a shared GPU the host exchange)
+            from paper_2008_11480_b200 import native_sharded as NS
+
+            comm = NS.NativeComm.host(self.n) if SHARE_GPU else NS.NativeComm.nccl(self.n)
+            self.native = {"comm": comm, "NS": NS, "A": self.sp.matrix, "b": b,
+                           "theta": torch.zeros_like(b) if cfg != "c5" else None}
+            self.spec = P.CompositeSpec((2, 3, 4, 5))
+            self.plan8 = P.table_plans()[8][0]
+            self.plan16 = P.plan_order(16)
+            self.mmm_per_step = 18
+            if cfg == "c5":
+                st = P.initial_richardson(self.sp, b, 0, 1, order=16, q=16)
+                inner = st.inner
+                self.native["state"] = [comm.rows_of(m) for m in (
+                    inner.estimate, inner.residual, inner.accel_estimate,
+                    inner.accel_residual)] + [None, None]
+                self.native["theta"] = st.theta
+                del st, inner
+                # the recursive steps only read A: drop S^-1 and B (2 x 8.6 GB at n=32768)
+                self.sp = P.Splitting(precond=self.sp.matrix[:1, :1],
+                                      residual=self.sp.matrix[:1, :1], matrix=self.sp.matrix,
+                                      kind="scalar", verify=False)
+                del a
+                self.a = None
+            else:
+                st = P.initial_series(self.sp, 0, 1, order={"c4": 2, "c3": 8}[cfg])
+                self.native["g"] = comm.rows_of(st.estimate)
+                self.native["f"] = comm.rows_of(st.residual)
+                del st
+            self.sharded = {"comm": comm, "native": True}
+            torch.cuda.empty_cache()
+            if cfg == "c5":
+                self.step()  # first recursive call builds the carried weight (untimed)
+            return
         if self.world > 1 and cfg in ("c4", "c3"):
             # block-row sharding over the ranks (sharded.py): A, S^-1, B replicated,
             # G / F row blocks, one row-panel exchange per product with a sharded
@@ -447,6 +485,22 @@ class Workload:
     def step(self):
         P = self.P
         cfg = self.cfg
+        if getattr(self, "native", None) is not None:
+            s = self.native
+            NS, comm = s["NS"], s["comm"]
+            if cfg == "c5":
+                s["state"], s["theta"] = NS.richardson_recursive_step(
+                    comm, s["state"], s["A"], s["theta"], s["b"], 16, factor_plan=self.plan16,
+                    doubling_sum=True)
+                return
+            s["theta"] = NS.plain_richardson(comm, s["theta"], s["g"], s["A"], s["b"])
+            if cfg == "c4":
+                s["g"], s["f"] = NS.composite_step(comm, s["g"], s["f"], s["A"], self.sp.precond,
+                                                   self.sp.residual, self.sp.matrix,
+                                                   (2, 3, 4, 5), 2)
+            else:
+                s["g"], s["f"] = NS.ns_step(comm, s["g"], s["f"], s["A"], 8, self.plan8)
+            return
         if cfg == "c2":
             self.p2, self.f2, self.t2 = P.batched_composite_richardson(
                 self.a2, self.b2, self.pre2, self.res2, self.pre2, self.res2, self.t2 * 0, (2, 3),
@@ -1146,8 +1200,11 @@ def rank_info(w, args, world: int, rank: int, local: int) -> dict:
     comm = s.get("comm")
     if comm is not None:
         info["comm"] = type(comm).__name__
-        info["bytes_pulled"] = getattr(comm, "bytes_gathered", None)
-        info["gathers"] = getattr(comm, "seq", None)
+        if s.get("native"):
+            info["gathers"], info["bytes_pulled"] = comm.stats()
+        else:
+            info["bytes_pulled"] = getattr(comm, "bytes_gathered", None)
+            info["gathers"] = getattr(comm, "seq", None)
     if world > 1:
         import torch.distributed as dist
 
@@ -1210,7 +1267,9 @@ def run_ours(args):
     achieved = (g_fl.value / (g_ms.value / 1e3) / 1e12) if g_ms.value > 0 else None
 
     e2e = None
-    if not args.no_e2e and args.config in ("c4", "c3") and w.sharded is not None:
+    if w.sharded is not None and w.sharded.get("native"):
+        e2e = {"unavailable": "--comm native: e2e is measured on the peer / nccl paths"}
+    elif not args.no_e2e and args.config in ("c4", "c3") and w.sharded is not None:
         try:
             e2e = sharded_e2e(w, args, world, stream)
         except (RuntimeError, MemoryError) as exc:  # e.g. pinned host memory exhausted
@@ -1323,8 +1382,9 @@ def main():
     ap.add_argument("--hoist", action="store_true",
                     help="c4 only, opt-in labelled variant: hoist the state-independent "
                          "composite parts (NOT the reference DAG; FLOPs counted as executed)")
-    ap.add_argument("--comm", choices=["peer", "peer-stream", "nccl"], default="peer",
-                    help="row-panel exchange of the sharded path (N > 1)")
+    ap.add_argument("--comm", choices=["peer", "peer-stream", "nccl", "native"], default="peer",
+                    help="row-panel exchange of the sharded path (N > 1); native = the "
+                         "library's own block-row engine behind si_sharded_* (NCCL)")
     ap.add_argument("--shard", choices=["rows", "parts"], default="rows",
                     help="c4 at N > 1: block-row sharding of every product (rows) or the "
                          "composite parts on GPU groups + one tree reduction (parts)")

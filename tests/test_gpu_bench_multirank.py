@@ -60,3 +60,14 @@ def test_bench_grouped_parts(world):
     assert f"parts on {min(world, 4)} GPU groups" in d["parallelism"]
     assert d["value"] > 0 and d["gpu_launches"] > 0
     assert d["e2e"] and d["e2e"]["value"] > 0
+
+
+@pytest.mark.parametrize("cfg", [["--config", "c4", "--size", "768"],
+                                 ["--config", "c5", "--size", "640"]])
+def test_bench_native_sharded(cfg):
+    """bench.py --comm native: the library's block-row engine (si_sharded_*) under
+    torchrun; on a shared GPU the exchange is the host (gloo) one."""
+    d = _run(cfg + ["--comm", "native"])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert "si_sharded" in d["parallelism"]
+    assert d["value"] > 0 and d["gpu_launches"] > 0
