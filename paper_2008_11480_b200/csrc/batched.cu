@@ -688,9 +688,7 @@ __device__ __forceinline__ void gemm_op(const double* A, const double* B, const 
 // kind, mode, slots and barrier flag are constants, the op loop is straight-
 // line code, and no op is decoded or branched on at run time.
 struct NoFixed {
-  static constexpr bool kFixed = false;
-  static constexpr int nops = 1;
-  static constexpr DOp ops[1] = {};
+  static constexpr bool kFixed = false;  // (ops / nops are only read under if constexpr)
 };
 
 #if __has_include("resident_fixed_c2.inc")
