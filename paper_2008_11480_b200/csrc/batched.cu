@@ -988,7 +988,11 @@ __device__ __forceinline__ void gemm_rows(const double* A, const double* B, cons
   // and are summed in a fixed order at the end: with one 8 x 8 tile per warp
   // (8-CTA clusters) the 16 dependent DMMAs of a single chain (26 cycles
   // each) would set the op's latency
-  constexpr int KS = MTW * NTW == 1 ? 4 : 1;
+#ifndef SI_CLUSTER_KS
+#define SI_CLUSTER_KS 4
+#endif
+  constexpr int KS = MTW * NTW == 1 ? SI_CLUSTER_KS : 1;
+  static_assert(KS == 1 || KS == 4, "k-step accumulator sets: 1 or 4");
   double acc[MTW][NTW][2];
   double ex[KS > 1 ? KS - 1 : 1][2] = {};
 #pragma unroll
@@ -1126,12 +1130,14 @@ __global__ void __launch_bounds__(kClusterThreads, 1) resident_cluster_kernel(Ba
             const double* A = mslot(o.a);
             const double* x = vslot(o.b);
             const int r0 = rbase + warp * 8;
-            double acc[4][2] = {};  // four interleaved chains of 4 dependent DMMAs
+            // interleaved chains of dependent DMMAs (4: chains of 4)
+            constexpr int GS = SI_CLUSTER_KS == 1 ? 2 : 4;
+            double acc[4][2] = {};
 #pragma unroll
             for (int kk = 0; kk < NP; kk += 4) {
               const double af = A[G::idx(r0 + g, kk + t)];
               const double bf = g == 0 ? x[kk + t] : 0.0;
-              dmma(acc[(kk >> 2) & 3][0], acc[(kk >> 2) & 3][1], af, bf);
+              dmma(acc[(kk >> 2) % GS][0], acc[(kk >> 2) % GS][1], af, bf);
             }
             if (t == 0) {
               const int row = r0 + g;
