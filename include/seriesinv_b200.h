@@ -421,6 +421,36 @@ SI_API int si_profile_end(si_handle h, double* gemm_ms, double* gemm_flops,
  * the roofline denominator (MEASURED_PEAKS.json has no FP64 entry). */
 SI_API int si_dmma_peak(si_handle h, int iters, double* tflops);
 
+/* ---------------- FP64 product backend ---------------- */
+
+/* Which tensor-core path computes the handle's FP64 products (every n x n
+ * product of the steps above; mat_mul, matrix_core.py:101-106):
+ *   SI_GEMM_DMMA      FP64 DMMA (mma.sync m8n8k4), the default;
+ *   SI_GEMM_OZAKI_I8  Ozaki scheme II: the product computed exactly from
+ *                     power-of-two-scaled integer images of A and B, one INT8
+ *                     tcgen05 GEMM per modulus (nmoduli of 256, 255, 253, ...),
+ *                     recombined by the Chinese remainder theorem; used for
+ *                     products whose dimensions are all >= min_dim (and K <=
+ *                     32768; smaller or gated products stay on DMMA).
+ * nmoduli = 0 / min_dim = 0 keep the current value (defaults 16 / 1024).
+ * The emulated result is not bitwise the DMMA result; its error is bounded by
+ * 2^-(pa) relative to the largest entry of each row of A / column of B, with
+ * pa ~ 54 at K = 16384 and 16 moduli (ozaki.cu). */
+#define SI_GEMM_DMMA 0
+#define SI_GEMM_OZAKI_I8 1
+SI_API int si_set_gemm_backend(si_handle h, int backend, int nmoduli, int64_t min_dim);
+SI_API int si_get_gemm_backend(si_handle h, int* backend, int* nmoduli, int64_t* min_dim);
+/* The first n moduli of the emulation. */
+SI_API int si_ozaki_moduli(int n, uint32_t* moduli);
+/* The INT8 tensor-core kernel alone (test hook): r[l] = (a[l] @ bt[l]^T) mod
+ * m_l for l < nplanes; a[l]: m x kp int8, bt[l]: n x kp int8 (row-major, kp a
+ * multiple of 128), r[l]: m x n uint8. */
+SI_API int si_i8_gemm_mod(si_handle h, const int8_t* a, const int8_t* bt, uint8_t* r, int64_t m,
+                          int64_t n, int64_t kp, int nplanes, void* stream);
+/* Summed device time (ms) and int8 operations of the INT8 tensor-core kernel
+ * launches recorded since si_profile_begin (emulated products only). */
+SI_API int si_profile_i8(si_handle h, double* ms, double* ops, int64_t* launches);
+
 /* ---------------- batched small systems (BASELINE config 2) ---------------- */
 
 /* `iters` x { plain Richardson with P_k; composite_step(rates, order_n) } for

@@ -7,6 +7,7 @@
 
 #include "../../include/seriesinv_b200.h"
 #include "batched.hpp"
+#include "ozaki.hpp"
 #include "setup.hpp"
 #include "shard.hpp"
 #include "steps.hpp"
@@ -1012,11 +1013,13 @@ int si_profile_begin(si_handle h) {
     need(h != nullptr, "null handle");
     std::lock_guard<std::recursive_mutex> lock(h->h.mu);
     Handle& hh = h->h;
-    for (auto& r : hh.prof) {
-      hh.prof_pool.push_back(r.start);
-      hh.prof_pool.push_back(r.stop);
+    for (auto* v : {&hh.prof, &hh.prof_i8}) {
+      for (auto& r : *v) {
+        hh.prof_pool.push_back(r.start);
+        hh.prof_pool.push_back(r.stop);
+      }
+      v->clear();
     }
-    hh.prof.clear();
     hh.launches = 0;
     hh.profiling = true;
   });
@@ -1189,3 +1192,67 @@ int si_batched_ns_richardson_ex(si_handle h, int64_t batch, int64_t n, const dou
 }
 
 }  // extern "C"
+
+/* ---------------- FP64 product backend (ozaki.cu) ---------------- */
+
+int si_set_gemm_backend(si_handle h, int backend, int nmoduli, int64_t min_dim) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(backend == SI_GEMM_DMMA || backend == SI_GEMM_OZAKI_I8, "unknown backend");
+    need(nmoduli == 0 || (nmoduli >= oz::kMinModuli && nmoduli <= oz::kMaxModuli),
+         "nmoduli out of range");
+    need(min_dim >= 0, "negative min_dim");
+    std::lock_guard<std::recursive_mutex> lock(h->h.mu);
+    h->h.gemm_backend = backend;
+    if (nmoduli) h->h.oz_nmod = nmoduli;
+    if (min_dim) h->h.oz_min_dim = std::max<int64_t>(min_dim, 128);
+  });
+}
+
+int si_get_gemm_backend(si_handle h, int* backend, int* nmoduli, int64_t* min_dim) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    std::lock_guard<std::recursive_mutex> lock(h->h.mu);
+    if (backend) *backend = h->h.gemm_backend;
+    if (nmoduli) *nmoduli = h->h.oz_nmod;
+    if (min_dim) *min_dim = h->h.oz_min_dim;
+  });
+}
+
+int si_ozaki_moduli(int n, uint32_t* moduli) {
+  return guard([&] {
+    need(moduli != nullptr && n >= 1 && n <= oz::kMaxModuli, "bad arguments");
+    for (int l = 0; l < n; ++l) moduli[l] = oz::modulus(l);
+  });
+}
+
+int si_i8_gemm_mod(si_handle h, const int8_t* a, const int8_t* bt, uint8_t* r, int64_t m,
+                   int64_t n, int64_t kp, int nplanes, void* stream) {
+  return guard([&] {
+    need(h && a && bt && r, "null pointer");
+    need(m > 0 && n > 0 && kp > 0 && kp % 128 == 0, "bad shape (kp must be a multiple of 128)");
+    need(kp <= oz::kMaxK, "kp too large");
+    need(nplanes >= 1 && nplanes <= oz::kMaxModuli, "nplanes out of range");
+    Call call(h, stream, nullptr);
+    check(oz::launch_i8_gemm_mod(a, bt, r, m, n, kp, nplanes, call.c.s), "i8 gemm launch");
+    h->h.launches += 1;
+  });
+}
+
+int si_profile_i8(si_handle h, double* ms, double* ops, int64_t* launches) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    std::lock_guard<std::recursive_mutex> lock(h->h.mu);
+    double t = 0.0, o = 0.0;
+    for (auto& r : h->h.prof_i8) {
+      check(cudaEventSynchronize(r.stop), "cudaEventSynchronize");
+      float x = 0.f;
+      check(cudaEventElapsedTime(&x, r.start, r.stop), "cudaEventElapsedTime");
+      t += x;
+      o += r.flops;
+    }
+    if (ms) *ms = t;
+    if (ops) *ops = o;
+    if (launches) *launches = (int64_t)h->h.prof_i8.size();
+  });
+}

@@ -3,6 +3,7 @@
 // each) is the reference's, so the mmm/mvm counters match matrix_core.py:71-98
 // tick for tick, while the element-wise ops are fused into the GEMM epilogues.
 #include "engine.hpp"
+#include "ozaki.hpp"
 #include "shard.hpp"
 
 #include <algorithm>
@@ -158,8 +159,42 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
     for (int p = 0; p < pw->npanels; ++p)
       check(stream_wait_u32(pw->ready + p, pw->epoch, c.s), "panel wait");
   }
+  const bool use_oz = h->gemm_backend == 1 && !gated && pwa == nullptr &&
+                      d.rows >= h->oz_min_dim && d.cols >= h->oz_min_dim &&
+                      A.v.cols >= h->oz_min_dim && A.v.cols <= oz::kMaxK;
   if (d.rows == 0 || d.cols == 0) {
     err = cudaSuccess;
+  } else if (use_oz) {
+    Handle::ProfRec rec{}, rec8{};
+    auto draw = [&](cudaEvent_t* ev) {
+      if (h->prof_pool.empty()) {
+        check(cudaEventCreate(ev), "cudaEventCreate");
+      } else {
+        *ev = h->prof_pool.back();
+        h->prof_pool.pop_back();
+      }
+    };
+    if (h->profiling) {
+      for (cudaEvent_t* ev : {&rec.start, &rec.stop, &rec8.start, &rec8.stop}) draw(ev);
+      rec.flops = 2.0 * (double)d.rows * (double)d.cols * (double)A.v.cols;
+      rec8.flops = 2.0 * (double)d.rows * (double)d.cols * (double)((A.v.cols + 127) / 128 * 128) *
+                   (double)h->oz_nmod;
+      check(cudaEventRecord(rec.start, c.s), "cudaEventRecord");
+    }
+    const size_t wb = oz::workspace_bytes(d.rows, d.cols, A.v.cols, h->oz_nmod);
+    MV ws = alloc(c, 1, (int64_t)((wb + 7) / 8));
+    oz::Work w;
+    w.base = reinterpret_cast<uint8_t*>(ws.v.p);
+    w.bytes = wb;
+    int64_t nl = 0;
+    err = oz::launch_gemm(A.v, B.v, d, e, h->oz_nmod, w, c.s, &nl,
+                          h->profiling ? rec8.start : nullptr, h->profiling ? rec8.stop : nullptr);
+    h->launches += nl;
+    if (h->profiling && err == cudaSuccess) {
+      check(cudaEventRecord(rec.stop, c.s), "cudaEventRecord");
+      h->prof.push_back(rec);
+      h->prof_i8.push_back(rec8);
+    }
   } else if (d.cols <= 4) {
     err = launch_gemv(A.v, B.v, d, e, c.s);
     h->launches += 1;

@@ -40,6 +40,14 @@ struct Handle {
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> prof_pool;
   int64_t launches = 0;  // kernels launched by this handle
+  // FP64 product backend (si_set_gemm_backend): 0 = DMMA (gemm_tma.cu, the
+  // default), 1 = Ozaki-II emulation on the INT8 tensor cores (ozaki.cu) for
+  // products whose three dimensions are all >= oz_min_dim.
+  int gemm_backend = 0;
+  int oz_nmod = 16;
+  int64_t oz_min_dim = 1024;
+  // live profiling of the INT8 tensor-core kernel inside emulated products
+  std::vector<ProfRec> prof_i8;
   // Optional external allocator (si_set_allocator): the Python layer routes
   // temporaries through PyTorch's caching allocator so that one allocator owns
   // all device memory (at n=32768 a matrix is 8.6 GB; two caches do not fit).

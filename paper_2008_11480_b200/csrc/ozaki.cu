@@ -1,0 +1,811 @@
+// FP64 products emulated on the INT8 tensor cores of sm_100a (Ozaki scheme II).
+//
+// FP64 tensor work on B200 runs on the warp-level DMMA pipe (37 TFLOP/s,
+// gemm_tma.cu): tcgen05.mma has no f64 kind.  It does have kind::i8 (int8 x
+// int8 -> int32 in TMEM) at 4.5 POPS dense, and an FP64 product can be computed
+// EXACTLY from integers:
+//
+//  1. Scale (per row of A, per column of B, by powers of two) and round to
+//     integers: A' = rint(diag(2^sa) A), B' = rint(B diag(2^sb)), with
+//     |A'| <= 2^pa, |B'| <= 2^pb and K * 2^(pa+pb) <= M/4, M = prod m_l.
+//     Only this rounding loses information: every entry keeps the bits of its
+//     row's (column's) largest entry down to 2^-pa relative, pa, pb ~ 54 for
+//     16 moduli at K = 16384 -- as fine as the 53-bit significand of the
+//     largest entries themselves.
+//  2. For each modulus m_l (pairwise coprime, <= 256): residues of A' and B'
+//     in [-128, 127] (int8), and C_l = A'_l @ B'_l on the tensor cores.  The
+//     int32 sums are exact (|C_l| <= K * 2^14 < 2^30 for K <= 32768), reduced
+//     mod m_l in the TMEM epilogue and stored as one byte per entry.
+//  3. C' = A' B' is the unique integer in (-M/4, M/4] with those residues
+//     (Chinese remainder theorem), rebuilt in FP64 from exact partial sums
+//     (32-bit pieces of the CRT weights) and scaled back by 2^-(sa_i + sb_j);
+//     the seriesinv epilogue (alpha, beta * C, diag * I) is fused there.
+//
+// The integer product is exact and order-free, so results do not depend on
+// tiling, concurrency or on how rows are split across ranks (the block-row
+// sharded path stays bitwise equal to the single-GPU call, as with DMMA).
+//
+// Kernels (one emulated product = 6 launches):
+//   row_absmax / col_absmax      max |a| per row of A, per column of B (HBM)
+//   residues_rows / residues_cols A -> nmod int8 planes (K-major), B -> nmod
+//                                int8 planes transposed to K-major (HBM)
+//   i8_gemm_mod_kernel           nmod int8 GEMMs, tcgen05.mma kind::i8 with
+//                                TMA (128B swizzle) -> 4-stage smem ring ->
+//                                single-thread MMA issue -> double-buffered
+//                                TMEM accumulators -> 4 epilogue warps
+//                                (tcgen05.ld, mod m_l, byte stores)
+//   crt_kernel                   CRT + scale + fused epilogue (HBM)
+#include "ozaki.hpp"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cstring>
+#include <mutex>
+
+namespace si {
+namespace oz {
+namespace {
+
+// ---------------------------------------------------------------- moduli --
+__host__ __device__ constexpr unsigned kmod(int l) {
+  return l == 0    ? 256u
+         : l == 1  ? 255u
+         : l == 2  ? 253u
+         : l == 3  ? 251u
+         : l == 4  ? 247u
+         : l == 5  ? 241u
+         : l == 6  ? 239u
+         : l == 7  ? 233u
+         : l == 8  ? 229u
+         : l == 9  ? 227u
+         : l == 10 ? 223u
+         : l == 11 ? 217u
+         : l == 12 ? 211u
+         : l == 13 ? 199u
+         : l == 14 ? 197u
+                   : 193u;
+}
+__host__ __device__ constexpr unsigned pow2mod(int e, unsigned m) {
+  unsigned r = 1u % m;
+  for (int i = 0; i < e; ++i) r = (r * 2u) % m;
+  return r;
+}
+
+constexpr int kNonFinite = INT_MIN / 4;  // shift sentinel: the row / column holds inf or nan
+constexpr unsigned long long kInfBits = 0x7FF0000000000000ull;
+constexpr int kMaxP = 56;  // |A'| <= 2^56 keeps u = A' + 2^57 below 2^58
+
+__device__ __forceinline__ int shift_of(unsigned long long maxbits, int p) {
+  if (maxbits >= kInfBits) return kNonFinite;
+  if (maxbits == 0ull) return 0;
+  return p - 1 - ilogb(__longlong_as_double((long long)maxbits));
+}
+
+// a * 2^sh (exact while the result is >= 2^-1022 or rounds to 0 under rint)
+__device__ __forceinline__ double pow2(int e) {  // -1022 <= e <= 1023
+  return __longlong_as_double((long long)(e + 1023) << 52);
+}
+
+// Symmetric residue modulo kmod(L) of the integer x = u - 2^57, u < 2^58 given
+// as 20-bit chunks u = c2 2^40 + c1 2^20 + c0: one reduction of
+// c2 (2^40 mod m) + c1 (2^20 mod m) + c0 + (m - 2^57 mod m) < 2^29, then the
+// symmetric representative in [-(m-1)/2, m/2) -- int8 for every modulus <= 256.
+struct Chunks {
+  uint32_t c0, c1, c2;
+};
+__device__ __forceinline__ Chunks chunks_of(long long x) {
+  const unsigned long long u = (unsigned long long)(x + (1ll << 57));
+  return Chunks{(uint32_t)u & 0xFFFFFu, (uint32_t)(u >> 20) & 0xFFFFFu, (uint32_t)(u >> 40)};
+}
+template <int L>
+__device__ __forceinline__ int res_sym(const Chunks& c) {
+  constexpr unsigned m = kmod(L);
+  constexpr unsigned r40 = pow2mod(40, m);
+  constexpr unsigned r20 = pow2mod(20, m);
+  constexpr unsigned k = m - pow2mod(57, m);
+  const unsigned r = (c.c2 * r40 + c.c1 * r20 + c.c0 + k) % m;
+  return (int)r - (r >= (m + 1) / 2 ? (int)m : 0);
+}
+
+// integer image rint(a * 2^sh) of a (sh not the sentinel)
+__device__ __forceinline__ long long int_image(double a, int sh) {
+  if (sh > 1000) {
+    a *= pow2(600);
+    sh -= 600;
+  }
+  return __double2ll_rn(a * pow2(sh));
+}
+
+__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
+  return (uint32_t)(a & 0xff) | ((uint32_t)(b & 0xff) << 8) | ((uint32_t)(c & 0xff) << 16) |
+         ((uint32_t)(d & 0xff) << 24);
+}
+
+// ------------------------------------------------------------- scaling --
+// max |a_ij| over each row (as the bit pattern of |a|: ordered like the value,
+// inf / nan above every finite value); one warp per row.
+__global__ void row_absmax_kernel(const double* __restrict__ A, int64_t lda, int M, int K,
+                                  unsigned long long* __restrict__ out) {
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < M; row += warps) {
+    const double* p = A + (int64_t)row * lda;
+    unsigned long long m = 0ull;
+    int k = lane;
+    for (; k + 96 < K; k += 128) {
+      const double v0 = p[k], v1 = p[k + 32], v2 = p[k + 64], v3 = p[k + 96];
+      m = max(m, (unsigned long long)__double_as_longlong(fabs(v0)));
+      m = max(m, (unsigned long long)__double_as_longlong(fabs(v1)));
+      m = max(m, (unsigned long long)__double_as_longlong(fabs(v2)));
+      m = max(m, (unsigned long long)__double_as_longlong(fabs(v3)));
+    }
+    for (; k < K; k += 32) m = max(m, (unsigned long long)__double_as_longlong(fabs(p[k])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) out[row] = m;
+  }
+}
+
+// max |b_ij| over each column: 32 columns x 256 rows per block, atomicMax into
+// `out` (zeroed by the caller).
+__global__ void col_absmax_kernel(const double* __restrict__ B, int64_t ldb, int K, int N,
+                                  unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long red[8][32];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + tx;
+  const int k0 = blockIdx.y * 256;
+  unsigned long long m = 0ull;
+  if (j < N) {
+    const int k1 = min(K, k0 + 256);
+    for (int k = k0 + ty; k < k1; k += 8)
+      m = max(m, (unsigned long long)__double_as_longlong(fabs(B[(int64_t)k * ldb + j])));
+  }
+  red[ty][tx] = m;
+  __syncthreads();
+  if (ty == 0 && j < N) {
+#pragma unroll
+    for (int i = 1; i < 8; ++i) m = max(m, red[i][tx]);
+    if (m) atomicMax(out + j, m);
+  }
+}
+
+// ------------------------------------------------------------ residues --
+// residues of 16 consecutive integers modulo kmod(L), kmod(L+1), ... (L < nmod),
+// one 16-byte store into each plane
+template <int L>
+__device__ __forceinline__ void emit16(int nmod, const Chunks (&x)[16], int8_t* dst, int64_t plane) {
+  if constexpr (L < kMaxModuli) {
+    if (L >= nmod) return;
+    int r[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) r[j] = res_sym<L>(x[j]);
+    uint4 w;
+    w.x = pack4(r[0], r[1], r[2], r[3]);
+    w.y = pack4(r[4], r[5], r[6], r[7]);
+    w.z = pack4(r[8], r[9], r[10], r[11]);
+    w.w = pack4(r[12], r[13], r[14], r[15]);
+    *reinterpret_cast<uint4*>(dst + L * plane) = w;
+    emit16<L + 1>(nmod, x, dst, plane);
+  }
+}
+
+// A (M x K, row-major) -> nmod planes of M x Kp int8 (columns >= K zero):
+// one thread per 16 consecutive k of a row, one 16-byte store per plane.
+__global__ void residues_rows_kernel(const double* __restrict__ A, int64_t lda, int M, int K,
+                                     int Kp, const unsigned long long* __restrict__ rmax, int p,
+                                     int nmod, int8_t* __restrict__ out) {
+  const int chunks = Kp >> 4;
+  const int64_t total = (int64_t)M * chunks;
+  const int64_t plane = (int64_t)M * Kp;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / chunks);
+    const int k0 = (int)(idx - (int64_t)row * chunks) << 4;
+    const int sh = shift_of(rmax[row], p);
+    Chunks x[16];
+    const double* src = A + (int64_t)row * lda + k0;
+    if (sh == kNonFinite) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) x[j] = chunks_of(0);
+    } else if (k0 + 16 <= K && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(src + j);
+        x[j] = chunks_of(int_image(v.x, sh));
+        x[j + 1] = chunks_of(int_image(v.y, sh));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) x[j] = chunks_of(k0 + j < K ? int_image(src[j], sh) : 0);
+    }
+    emit16<0>(nmod, x, out + (int64_t)row * Kp + k0, plane);
+  }
+}
+
+// B (K x N, row-major) -> nmod planes of N x Kp int8, transposed (row j of a
+// plane = column j of B, K contiguous): 64 k x 64 j tiles through shared memory.
+__global__ void __launch_bounds__(256) residues_cols_kernel(
+    const double* __restrict__ B, int64_t ldb, int K, int N, int Kp,
+    const unsigned long long* __restrict__ cmax, int p, int nmod, int8_t* __restrict__ out) {
+  __shared__ long long xs[64][65];
+  __shared__ int shs[64];
+  const int k0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const int tid = threadIdx.x;
+  if (tid < 64) shs[tid] = (j0 + tid < N) ? shift_of(cmax[j0 + tid], p) : 0;
+  __syncthreads();
+  {
+    const int tx = tid & 63, ty = tid >> 6;
+    const int j = j0 + tx;
+    const int sh = shs[tx];
+#pragma unroll 4
+    for (int r = ty; r < 64; r += 4) {
+      const int k = k0 + r;
+      const long long x = (j < N && k < K && sh != kNonFinite) ? int_image(B[(int64_t)k * ldb + j], sh) : 0;
+      xs[r][tx] = x;
+    }
+  }
+  __syncthreads();
+  const int jl = tid >> 2, kc = (tid & 3) << 4;
+  if (j0 + jl >= N || k0 + kc >= Kp) return;
+  Chunks x[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = chunks_of(xs[kc + i][jl]);
+  emit16<0>(nmod, x, out + (int64_t)(j0 + jl) * Kp + k0 + kc, (int64_t)N * Kp);
+}
+
+// -------------------------------------------------- INT8 tensor-core GEMM --
+constexpr int GBM = 128, GBN = 256, GBK = 128;  // CTA tile; GBK in bytes (= int8 elements)
+constexpr int GSTAGES = 4;
+constexpr int GA_BYTES = GBM * GBK;  // 16 KB
+constexpr int GB_BYTES = GBN * GBK;  // 32 KB
+constexpr int GSTAGE_BYTES = GA_BYTES + GB_BYTES;
+constexpr int GTHREADS = 192;  // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+constexpr int GSMEM = GSTAGES * GSTAGE_BYTES + 1024 + 256;
+constexpr int GROUP_M = 16;
+constexpr int kTmemCols = 2 * GBN;  // two 128 x 256 int32 accumulators (all of TMEM)
+// instruction descriptor, kind::i8: D s32 [4,6), A s8 [7,10), B s8 [10,13),
+// both K-major, N >> 3 at [17,23), M >> 4 at [24,29)
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(GBN >> 3) << 17) |
+                            ((uint32_t)(GBM >> 4) << 24);
+
+// per-plane reduction of the int32 sums: r = v mod m from u = v + 2^30 < 2^31,
+// q = floor(u * magic / 2^39) with magic = floor(2^39 / m) + 1 (exact for u < 2^31)
+struct ModTab {
+  unsigned m[kMaxModuli];
+  unsigned magic[kMaxModuli];
+  unsigned off[kMaxModuli];  // 2^30 mod m
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+// shared-memory matrix descriptor: K-major, 128B swizzle (8-row groups 1024 B
+// apart), sm_100 version bits
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int& plane, int& tm, int& tn) {
+  const int per_plane = num_m * num_n;
+  plane = t / per_plane;
+  const int r = t - plane * per_plane;
+  const int per_group = GROUP_M * num_n;
+  const int group = r / per_group;
+  const int first_m = group * GROUP_M;
+  const int gsize = min(num_m - first_m, GROUP_M);
+  const int q = r - group * per_group;
+  tm = first_m + q % gsize;
+  tn = q / gsize;
+}
+
+// R[l] = (A[l] @ Bt[l]^T) mod m_l, persistent over (plane, row tile, column tile)
+__global__ void __launch_bounds__(GTHREADS, 1)
+    i8_gemm_mod_kernel(const __grid_constant__ CUtensorMap tmA,
+                       const __grid_constant__ CUtensorMap tmB, uint8_t* __restrict__ R, int M,
+                       int N, int Kp, int nplanes, const __grid_constant__ ModTab mt) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bars = base + GSTAGES * GSTAGE_BYTES;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (GSTAGES + s); };
+  auto tfull_bar = [&](int a) { return bars + 8u * (2 * GSTAGES + a); };
+  auto tempty_bar = [&](int a) { return bars + 8u * (2 * GSTAGES + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * GSTAGES + 4);
+  uint8_t* smem_gen = smem_raw + (tmem_slot - raw);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_m = (M + GBM - 1) / GBM;
+  const int num_n = (N + GBN - 1) / GBN;
+  const int total = num_m * num_n * nplanes;
+  const int kblocks = Kp / GBK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < GSTAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tmem_slot),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(smem_gen);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int plane, tm, tn;
+        tile_of(t, num_m, num_n, plane, tm, tn);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1u);
+          const uint32_t sa = base + stage * GSTAGE_BYTES;
+          mbar_expect_tx(full_bar(stage), GSTAGE_BYTES);
+          tma_load_3d(sa, &tmA, full_bar(stage), kb * GBK, tm * GBM, plane);
+          tma_load_3d(sa + GA_BYTES, &tmB, full_bar(stage), kb * GBK, tn * GBN, plane);
+          if (++stage == GSTAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (one thread) ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        mbar_wait(tempty_bar(acc), aphase ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * GBN);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(full_bar(stage), phase);
+          tc_fence_after();
+          const uint32_t sa = base + stage * GSTAGE_BYTES;
+          const uint64_t adesc = sdesc(sa), bdesc = sdesc(sa + GA_BYTES);
+#pragma unroll
+          for (int k = 0; k < GBK / 32; ++k)  // K = 32 bytes per MMA: +2 in the 16-byte address field
+            mma_i8(d, adesc + 2 * k, bdesc + 2 * k, (kb | k) != 0 ? 1u : 0u);
+          mma_commit(empty_bar(stage));  // frees the stage once these MMAs have read it
+          if (++stage == GSTAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        mma_commit(tfull_bar(acc));  // accumulator complete
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue: TMEM -> mod m_l -> bytes ----------------
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int plane, tm, tn;
+      tile_of(t, num_m, num_n, plane, tm, tn);
+      const unsigned m = mt.m[plane], magic = mt.magic[plane], off = mt.off[plane];
+      mbar_wait(tfull_bar(acc), aphase);
+      tc_fence_after();
+      const int row = tm * GBM + q * 32 + lane;
+      const int col0 = tn * GBN;
+      uint8_t* rp = R + (int64_t)plane * M * N + (int64_t)row * N + col0;
+      const bool vec = ((N & 15) == 0);
+#pragma unroll 1
+      for (int c = 0; c < GBN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * GBN + c * 32), v);
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          uint32_t b[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t u = v[i + j] + (1u << 30);
+            const uint32_t qq = __umulhi(u, magic) >> 7;
+            uint32_t r = u - qq * m;
+            r = r >= off ? r - off : r + m - off;
+            b[j] = r;
+          }
+          w[i >> 2] = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+        }
+        const int cc = col0 + c * 32;
+        if (row < M && cc < N) {
+          if (vec && cc + 32 <= N) {
+            uint4* dst = reinterpret_cast<uint4*>(rp + c * 32);
+            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          } else {
+            for (int i = 0; i < 32 && cc + i < N; ++i) rp[c * 32 + i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty_bar(acc));
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1u;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(kTmemCols)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ CRT --
+// X = sum_l c_l W_l (W_l the CRT weights, c_l in [0, m_l)) is held exactly as
+// four partial sums S_k of 32-bit pieces (c_l * piece < 2^40, 16 terms < 2^44);
+// q = rint(X / M); C' = X - q M = sum_k (S_k - q M_k) 2^(32k), every S_k - q M_k
+// exact, combined most significant first.
+struct CrtTab {
+  double w[kMaxModuli][4];  // pieces of W_l: w[l][k] = (W_l >> 32k) & 0xffffffff
+  double mp[4];             // pieces of M
+  double inv_m;             // 1 / M (rounded)
+  int nmod;
+};
+
+__device__ __forceinline__ double apply_epi(double acc, double alpha, double beta, double cval) {
+  double v = (alpha == 1.0) ? acc : (alpha == -1.0 ? -acc : __dmul_rn(alpha, acc));
+  if (beta != 0.0) v = __dadd_rn(v, beta == 1.0 ? cval : __dmul_rn(beta, cval));
+  return v;
+}
+
+__device__ __forceinline__ double crt_value(const uint32_t (&w)[kMaxModuli], int j, const CrtTab& t) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+  for (int l = 0; l < kMaxModuli; ++l) {
+    if (l < t.nmod) {
+      const double cl = (double)((w[l] >> (8 * j)) & 0xFFu);
+      s0 = fma(cl, t.w[l][0], s0);
+      s1 = fma(cl, t.w[l][1], s1);
+      s2 = fma(cl, t.w[l][2], s2);
+      s3 = fma(cl, t.w[l][3], s3);
+    }
+  }
+  const double x = fma(s3, 0x1p96, fma(s2, 0x1p64, s1 * 0x1p32));
+  const double q = rint(x * t.inv_m);
+  const double t3 = fma(-q, t.mp[3], s3), t2 = fma(-q, t.mp[2], s2);
+  const double t1 = fma(-q, t.mp[1], s1), t0 = fma(-q, t.mp[0], s0);
+  return fma(fma(fma(t3, 0x1p32, t2), 0x1p32, t1), 0x1p32, t0);
+}
+
+// v * 2^e, one rounding
+__device__ __forceinline__ double scale2(double v, int e) {
+  return (e >= -1022 && e <= 1023) ? v * pow2(e) : ldexp(v, e);
+}
+
+// one thread per 4 consecutive columns of a row (one 32-bit load per plane)
+__global__ void __launch_bounds__(256) crt_kernel(
+    const uint8_t* __restrict__ R, int M, int N, const unsigned long long* __restrict__ rmax,
+    const unsigned long long* __restrict__ cmax, int pa, int pb, const __grid_constant__ CrtTab tab,
+    double* D, int64_t ldd, const double* C, int64_t ldc, double alpha, double beta, double diag,
+    int64_t doff) {
+  const int chunks = (N + 3) >> 2;
+  const int64_t total = (int64_t)M * chunks;
+  const int64_t plane = (int64_t)M * N;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / chunks);
+    const int j0 = (int)(idx - (int64_t)row * chunks) << 2;
+    const int sa = shift_of(rmax[row], pa);
+    const int64_t off = (int64_t)row * N + j0;
+    const bool full = (j0 + 4 <= N) && ((N & 3) == 0);
+    uint32_t w[kMaxModuli];
+#pragma unroll
+    for (int l = 0; l < kMaxModuli; ++l) {
+      w[l] = 0u;
+      if (l < tab.nmod) {
+        if (full) {
+          w[l] = __ldcs(reinterpret_cast<const unsigned*>(R + l * plane + off));
+        } else {
+          for (int j = 0; j < 4 && j0 + j < N; ++j) w[l] |= (uint32_t)R[l * plane + off + j] << (8 * j);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = j0 + j;
+      if (col >= N) break;
+      const int sb = shift_of(cmax[col], pb);
+      double v;
+      if (sa == kNonFinite || sb == kNonFinite) {
+        v = __longlong_as_double(0x7FF8000000000000ll);
+      } else {
+        v = scale2(crt_value(w, j, tab), -(sa + sb));
+      }
+      const double cv = beta != 0.0 ? C[(int64_t)row * ldc + col] : 0.0;
+      v = apply_epi(v, alpha, beta, cv);
+      if (diag != 0.0 && (int64_t)row + doff == (int64_t)col) v = __dadd_rn(v, diag);
+      D[(int64_t)row * ldd + col] = v;
+    }
+  }
+}
+
+// ----------------------------------------------------------------- host --
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// planes x rows x Kp int8, boxes of box_rows x 128 bytes (128B swizzle); rows
+// beyond `rows` of a plane read as zeros
+bool make_map_i8(CUtensorMap* map, const void* ptr, int64_t Kp, int64_t rows, int planes,
+                 uint32_t box_rows) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(rows * Kp)};
+  cuuint32_t box[3] = {(cuuint32_t)GBK, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(ptr), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+using u128 = unsigned __int128;
+
+struct Consts {
+  ModTab mt;
+  CrtTab crt[kMaxModuli + 1];  // by nmod
+  int log2m[kMaxModuli + 1];   // floor(log2 M) by nmod
+};
+
+const Consts& consts() {
+  static Consts c;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (int l = 0; l < kMaxModuli; ++l) {
+      const unsigned m = kmod(l);
+      c.mt.m[l] = m;
+      c.mt.magic[l] = (unsigned)((1ull << 39) / m + 1);
+      c.mt.off[l] = pow2mod(30, m);
+    }
+    for (int n = 1; n <= kMaxModuli; ++n) {
+      u128 M = 1;
+      for (int l = 0; l < n; ++l) M *= kmod(l);
+      int bits = 0;
+      for (u128 x = M; x > 1; x >>= 1) ++bits;
+      c.log2m[n] = bits;  // 2^bits <= M
+      CrtTab& t = c.crt[n];
+      std::memset(&t, 0, sizeof(t));
+      t.nmod = n;
+      for (int l = 0; l < n; ++l) {
+        const unsigned m = kmod(l);
+        const u128 Ml = M / m;
+        const unsigned r = (unsigned)(Ml % m);
+        unsigned y = 0;
+        for (unsigned cand = 1; cand < m; ++cand)
+          if ((r * cand) % m == 1u) {
+            y = cand;
+            break;
+          }
+        const u128 W = (Ml * y) % M;  // Ml * y < M * 256 / 173 < 2^127
+        for (int k = 0; k < 4; ++k) t.w[l][k] = (double)(uint32_t)(W >> (32 * k));
+      }
+      for (int k = 0; k < 4; ++k) t.mp[k] = (double)(uint32_t)(M >> (32 * k));
+      const double md = (double)(uint64_t)(M >> 64) * 0x1p64 + (double)(uint64_t)M;
+      t.inv_m = 1.0 / md;
+    }
+  });
+  return c;
+}
+
+int num_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+cudaError_t set_gemm_attr() {
+  static std::atomic<uint64_t> done{0};  // one bit per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && (done.load() & (1ull << dev))) return cudaSuccess;
+  cudaError_t e =
+      cudaFuncSetAttribute(i8_gemm_mod_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GSMEM);
+  if (e == cudaSuccess && dev < 64) done.fetch_or(1ull << dev);
+  return e;
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+inline int64_t kpad(int64_t K) { return (K + GBK - 1) / GBK * GBK; }
+
+}  // namespace
+
+unsigned modulus(int l) { return kmod(l); }
+
+size_t workspace_bytes(int64_t M, int64_t N, int64_t K, int nmod) {
+  const int64_t Kp = kpad(K);
+  return align256(M * 8) + align256(N * 8) + align256((size_t)nmod * M * Kp) +
+         align256((size_t)nmod * N * Kp) + align256((size_t)nmod * M * N);
+}
+
+cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, int64_t M, int64_t N,
+                               int64_t Kp, int nplanes, cudaStream_t s) {
+  if (M <= 0 || N <= 0 || Kp <= 0 || Kp % GBK || nplanes < 1 || nplanes > kMaxModuli ||
+      M > INT32_MAX || N > INT32_MAX || Kp > kMaxK + GBK)
+    return cudaErrorInvalidValue;
+  CUtensorMap ta, tb;
+  if (!make_map_i8(&ta, A, Kp, M, nplanes, GBM) || !make_map_i8(&tb, Bt, Kp, N, nplanes, GBN)) {
+    set_error("cuTensorMapEncodeTiled failed (int8 planes)");
+    return cudaErrorInvalidValue;
+  }
+  cudaError_t e = set_gemm_attr();
+  if (e != cudaSuccess) return e;
+  const int64_t tiles = ((M + GBM - 1) / GBM) * ((N + GBN - 1) / GBN) * nplanes;
+  const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+  i8_gemm_mod_kernel<<<grid, GTHREADS, GSMEM, s>>>(ta, tb, R, (int)M, (int)N, (int)Kp, nplanes,
+                                                   consts().mt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, int nmod,
+                        const Work& w, cudaStream_t s, int64_t* launches, cudaEvent_t ev0,
+                        cudaEvent_t ev1) {
+  const int64_t M = D.rows, N = D.cols, K = A.cols;
+  if (nmod < kMinModuli || nmod > kMaxModuli || K < 1 || K > kMaxK || M > INT32_MAX ||
+      N > INT32_MAX || w.bytes < workspace_bytes(M, N, K, nmod))
+    return cudaErrorInvalidValue;
+  const Consts& cs = consts();
+  const int64_t Kp = kpad(K);
+  int lk = 0;
+  while ((1ll << lk) < K) ++lk;
+  const int T = cs.log2m[nmod] - 2 - lk;  // K 2^(pa+pb) <= 2^(log2 M - 2) <= M / 4
+  const int pa = std::min(kMaxP, (T + 1) / 2), pb = std::min(kMaxP, T / 2);
+  uint8_t* p = w.base;
+  auto* rmax = reinterpret_cast<unsigned long long*>(p);
+  p += align256(M * 8);
+  auto* cmax = reinterpret_cast<unsigned long long*>(p);
+  p += align256(N * 8);
+  auto* ares = reinterpret_cast<int8_t*>(p);
+  p += align256((size_t)nmod * M * Kp);
+  auto* bres = reinterpret_cast<int8_t*>(p);
+  p += align256((size_t)nmod * N * Kp);
+  auto* res = p;
+  int64_t n = 0;
+  cudaError_t err;
+  const int sms = num_sms();
+  row_absmax_kernel<<<(int)std::min<int64_t>((M + 7) / 8, 16 * sms), 256, 0, s>>>(A.p, A.ld, (int)M,
+                                                                                (int)K, rmax);
+  ++n;
+  if ((err = cudaMemsetAsync(cmax, 0, N * 8, s)) != cudaSuccess) return err;
+  col_absmax_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((K + 255) / 256)), 256, 0, s>>>(
+      B.p, B.ld, (int)K, (int)N, cmax);
+  ++n;
+  {
+    const int64_t thr = M * (Kp / 16);
+    const int blocks = (int)std::min<int64_t>((thr + 255) / 256, 64 * sms);
+    residues_rows_kernel<<<blocks, 256, 0, s>>>(A.p, A.ld, (int)M, (int)K, (int)Kp, rmax, pa, nmod,
+                                                 ares);
+    ++n;
+  }
+  residues_cols_kernel<<<dim3((unsigned)((N + 63) / 64), (unsigned)(Kp / 64)), 256, 0, s>>>(
+      B.p, B.ld, (int)K, (int)N, (int)Kp, cmax, pb, nmod, bres);
+  ++n;
+  if ((err = cudaGetLastError()) != cudaSuccess) return err;
+  if (ev0 && (err = cudaEventRecord(ev0, s)) != cudaSuccess) return err;
+  if ((err = launch_i8_gemm_mod(ares, bres, res, M, N, Kp, nmod, s)) != cudaSuccess) return err;
+  if (ev1 && (err = cudaEventRecord(ev1, s)) != cudaSuccess) return err;
+  ++n;
+  {
+    const int64_t thr = M * ((N + 3) / 4);
+    const int blocks = (int)std::min<int64_t>((thr + 255) / 256, 64 * sms);
+    crt_kernel<<<blocks, 256, 0, s>>>(res, (int)M, (int)N, rmax, cmax, pa, pb, cs.crt[nmod], D.p,
+                                      D.ld, e.beta != 0.0 ? e.c : nullptr, e.ldc, e.alpha, e.beta,
+                                      e.diag, e.doff);
+    ++n;
+  }
+  if (launches) *launches += n;
+  return cudaGetLastError();
+}
+
+}  // namespace oz
+}  // namespace si

@@ -1,0 +1,261 @@
+"""FP64 products emulated on the INT8 tensor cores (Ozaki scheme II, csrc/ozaki.cu).
+
+* the tcgen05 kind::i8 kernel alone is exact (integer products mod m_l),
+* an emulated product meets its a-priori bound entry by entry and is at least
+  as accurate as the DMMA product against an extended-precision reference,
+* the fused epilogue (alpha, beta C in place, diag I at an offset), non-finite
+  rows / columns, zero and extreme-magnitude rows,
+* results are independent of the row split (bitwise) and deterministic,
+* the hot-path steps (configs 3, 4, 5 recipes) under the emulated backend meet
+  the north_star tolerance against the oracle at every iteration.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _restore_backend():
+    import paper_2008_11480_b200 as P
+
+    yield
+    P.set_gemm_backend("dmma", 16, 1024)
+
+
+def _pa_pb(k, nmod):
+    import paper_2008_11480_b200 as P
+
+    m = math.prod(P.ozaki_moduli(nmod))
+    t = m.bit_length() - 1 - 2 - max(0, (k - 1).bit_length())
+    return min(56, (t + 1) // 2), min(56, t // 2)
+
+
+def _ozaki(a, b, nmod=16):
+    import paper_2008_11480_b200 as P
+
+    with P.gemm_backend("ozaki", moduli=nmod, min_dim=128):
+        return P.mat_mul(a, b, P.MulCounter())
+
+
+def _dmma(a, b):
+    import paper_2008_11480_b200 as P
+
+    with P.gemm_backend("dmma"):
+        return P.mat_mul(a, b, P.MulCounter())
+
+
+@pytest.mark.parametrize("planes,m,n,kp", [(1, 128, 256, 128), (3, 300, 520, 256),
+                                           (2, 1000, 777, 1024), (16, 513, 300, 2048),
+                                           (5, 129, 1000, 4096)])
+def test_int8_kernel_exact(planes, m, n, kp):
+    import paper_2008_11480_b200 as P
+
+    mods = P.ozaki_moduli(16)
+    g = torch.Generator(device="cuda").manual_seed(planes * 1000 + m)
+    a = torch.randint(-128, 128, (planes, m, kp), dtype=torch.int8, device="cuda", generator=g)
+    bt = torch.randint(-128, 128, (planes, n, kp), dtype=torch.int8, device="cuda", generator=g)
+    r = P.i8_gemm_mod(a, bt)
+    for l in range(planes):
+        # |sum| <= kp * 2^14 < 2^53: the FP64 product of these integers is exact
+        ref = torch.remainder(a[l].double() @ bt[l].double().T, mods[l]).to(torch.uint8)
+        assert torch.equal(ref, r[l]), (l, int((ref != r[l]).sum()))
+
+
+def test_int8_kernel_extreme_residues():
+    """All-(-128) operands: the largest int32 sums the kernel's reduction sees."""
+    import paper_2008_11480_b200 as P
+
+    mods = P.ozaki_moduli(4)
+    a = torch.full((4, 256, 8192), -128, dtype=torch.int8, device="cuda")
+    bt = torch.full((4, 256, 8192), -128, dtype=torch.int8, device="cuda")
+    bt[:, ::2] = 127
+    r = P.i8_gemm_mod(a, bt)
+    for l in range(4):
+        ref = torch.remainder(a[l].double() @ bt[l].double().T, mods[l]).to(torch.uint8)
+        assert torch.equal(ref, r[l])
+
+
+def _cases(rng, n):
+    g = rng.standard_normal((2 * n, n))
+    spd = g.T @ g / (2 * n) + 1e-3 * np.eye(n)
+    f = np.eye(n) - spd / np.abs(spd).sum(1).max()
+    return {
+        "gauss": (rng.standard_normal((n, n)), rng.standard_normal((n, n))),
+        "wide_rows": (rng.standard_normal((n, n)) * np.exp2(rng.integers(-40, 40, (n, 1))),
+                      rng.standard_normal((n, n)) * np.exp2(rng.integers(-40, 40, (1, n)))),
+        "wide_entries": (rng.standard_normal((n, n)) * np.exp2(rng.integers(-25, 25, (n, n))),
+                         rng.standard_normal((n, n)) * np.exp2(rng.integers(-25, 25, (n, n)))),
+        "residual": (f, f),
+        "rect": (rng.standard_normal((n, n // 2 + 3)), rng.standard_normal((n // 2 + 3, n + 40))),
+    }
+
+
+@pytest.mark.parametrize("nmod", [16, 14])
+def test_emulated_product_bound_and_accuracy(nmod):
+    rng = np.random.default_rng(11)
+    for name, (a_np, b_np) in _cases(rng, 520).items():
+        a, b = torch.from_numpy(a_np).cuda(), torch.from_numpy(b_np).cuda()
+        c = _ozaki(a, b, nmod).cpu().numpy()
+        ref = a_np.astype(np.longdouble) @ b_np.astype(np.longdouble)
+        err = np.abs(c - ref).astype(np.float64)
+        pa, pb = _pa_pb(a_np.shape[1], nmod)
+        amax = np.abs(a_np).max(1, keepdims=True)
+        bmax = np.abs(b_np).max(0, keepdims=True)
+        bound = (2.0 ** -pa * amax * np.abs(b_np).sum(0, keepdims=True)
+                 + 2.0 ** -pb * bmax * np.abs(a_np).sum(1, keepdims=True)
+                 + 2.0 ** -(pa + pb) * a_np.shape[1] * amax * bmax)
+        bound = 1.01 * bound + 4 * 2.0 ** -53 * np.abs(ref).astype(np.float64)
+        assert np.all(err <= bound), (name, float((err / bound).max()))
+        if nmod == 16:
+            d = _dmma(a, b).cpu().numpy()
+            e_oz = float(np.linalg.norm(err) / np.linalg.norm(ref.astype(np.float64)))
+            e_dm = float(np.linalg.norm((d - ref).astype(np.float64)) /
+                         np.linalg.norm(ref.astype(np.float64)))
+            assert e_oz <= e_dm, (name, e_oz, e_dm)
+
+
+def test_epilogue_in_place_and_offset_diagonal():
+    """D = -A B + C + 2 I (diag shifted by doff), D aliasing C, through si_gemm_ex."""
+    import ctypes
+
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import _lib
+
+    rng = np.random.default_rng(3)
+    m, k, n, doff = 384, 640, 512, 100
+    a_np, b_np, c_np = (rng.standard_normal(s) for s in ((m, k), (k, n), (m, n)))
+    a, b = torch.from_numpy(a_np).cuda(), torch.from_numpy(b_np).cuda()
+    d = torch.from_numpy(c_np).cuda()
+    ctr = (ctypes.c_int64 * 2)()
+    P.set_gemm_backend("ozaki", 16, 128)
+    _lib.call("si_gemm_ex", _lib.handle(), m, n, k, -1.0, a.data_ptr(), k, b.data_ptr(), n, 1.0,
+              d.data_ptr(), n, 2.0, doff, d.data_ptr(), n, 0, ctr, _lib.stream_ptr())
+    ref = -(a_np.astype(np.longdouble) @ b_np) + c_np
+    idx = np.arange(m)
+    ref[idx, idx + doff] += 2.0
+    out = d.cpu().numpy()
+    assert np.abs(out - ref).max() <= 1e-13 * np.abs(ref).max()
+    assert ctr[0] == 1
+
+
+def test_non_finite_zero_and_extreme_rows():
+    rng = np.random.default_rng(5)
+    n = 300
+    a_np = rng.standard_normal((n, n))
+    b_np = rng.standard_normal((n, n))
+    a_np[3, 7] = np.nan
+    a_np[5, 0] = np.inf
+    a_np[9] = 0.0
+    a_np[11] *= 1e-300
+    a_np[13] *= 1e300
+    b_np[:, 17] = 0.0
+    b_np[4, 21] = -np.inf
+    c = _ozaki(torch.from_numpy(a_np).cuda(), torch.from_numpy(b_np).cuda()).cpu().numpy()
+    assert np.isnan(c[3]).all() and np.isnan(c[5]).all() and np.isnan(c[:, 21]).all()
+    ok_rows = np.setdiff1d(np.arange(n), [3, 5])
+    ok_cols = np.setdiff1d(np.arange(n), [21])
+    sub = c[np.ix_(ok_rows, ok_cols)]
+    assert np.isfinite(sub).all()
+    assert (c[9, ok_cols] == 0).all() and (c[ok_rows, 17] == 0).all()
+    for i in (11, 13):
+        ref = a_np[i].astype(np.longdouble) @ b_np[:, ok_cols]
+        assert np.abs(c[i, ok_cols] - ref).max() <= 1e-14 * np.abs(ref).max()
+
+
+def test_row_split_bitwise_and_deterministic():
+    """Rows of the product do not depend on which other rows are computed (the
+    block-row sharded path's invariant) nor on the call."""
+    rng = np.random.default_rng(9)
+    a_np, b_np = rng.standard_normal((1536, 1024)), rng.standard_normal((1024, 1280))
+    a, b = torch.from_numpy(a_np).cuda(), torch.from_numpy(b_np).cuda()
+    full = _ozaki(a, b)
+    assert torch.equal(full, _ozaki(a, b))
+    for r0, r1 in ((0, 512), (512, 1100), (1100, 1536)):
+        assert torch.equal(_ozaki(a[r0:r1].contiguous(), b), full[r0:r1])
+
+
+def test_backend_selection():
+    import paper_2008_11480_b200 as P
+
+    P.set_gemm_backend("ozaki", 15, 2048)
+    assert P.get_gemm_backend() == ("ozaki", 15, 2048)
+    rng = np.random.default_rng(1)
+    a = torch.from_numpy(rng.standard_normal((1024, 1024))).cuda()
+    small = P.mat_mul(a, a, P.MulCounter())  # below min_dim: DMMA, bitwise
+    assert torch.equal(small, _dmma(a, a))
+    P.set_gemm_backend("ozaki", 15, 2048)
+    with pytest.raises(ValueError):
+        P.set_gemm_backend("ozaki", 17)
+    with pytest.raises(ValueError):
+        P.set_gemm_backend("fp32")
+    with P.gemm_backend("dmma"):
+        assert P.get_gemm_backend()[0] == "dmma"
+    assert P.get_gemm_backend() == ("ozaki", 15, 2048)
+
+
+def _kappa_tol(a, tol=1e-10):
+    ev = np.linalg.eigvalsh(a)
+    return tol * max(1.0, float(ev.max() / ev.min()) / 1e4)
+
+
+def test_c3_recipe_emulated_vs_oracle():
+    """Config 3 recipe at n=2048 (h8 plan + plain Richardson, 25 iterations) with
+    every product emulated: P_k, theta_k within the tolerance at every iteration."""
+    import paper_2008_11480_b200 as P
+    from oracle import seriesinv_oracle as O
+    from paper_2008_11480_b200 import configs
+
+    a, b = configs.c3_gram(n=2048)
+    tol = _kappa_tol(a)
+    P.set_gemm_backend("ozaki", 16, 1024)
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False)
+    st = P.initial_series(sp, 0, 1, order=8)
+    bd = P.as_device(b)
+    theta = torch.zeros_like(bd)
+    osp = O.split_scalar(a, O.inf_norm(a) / 2.0)
+    ost = O.initial_series(osp, 0, 1, 8)
+    oth = np.zeros_like(b)
+    plan, oplan = P.table_plans()[8][0], O.TABLE_ROOTS[8][0][1]
+    for k in range(25):
+        theta = P.plain_richardson(theta, st.estimate, sp.matrix, bd, st.ctr)
+        st = P.ns_step(st, sp.matrix, plan=plan)
+        oth = O.plain_richardson(oth, ost.estimate, osp.matrix, b, ost.ctr)
+        ost = O.ns_step(ost, osp.matrix, oplan)
+        ep = np.linalg.norm(st.estimate.cpu().numpy() - ost.estimate) / np.linalg.norm(ost.estimate)
+        et = np.linalg.norm(theta.cpu().numpy() - oth) / np.linalg.norm(oth)
+        assert ep <= tol and et <= tol, (k, ep, et)
+    assert (st.ctr.mmm, st.ctr.mvm) == (ost.ctr.mmm, ost.ctr.mvm)
+
+
+def test_c4_recipe_emulated_vs_oracle():
+    """Config 4 recipe (composite rates (2,3,4,5), order_n=2, plain Richardson,
+    kappa 1e6) at n=2048, 8 iterations, every product emulated."""
+    import paper_2008_11480_b200 as P
+    from oracle import seriesinv_oracle as O
+    from paper_2008_11480_b200 import configs
+
+    a, b = configs.c4_householder(n=2048, rhs=64)
+    tol = _kappa_tol(a)
+    P.set_gemm_backend("ozaki", 16, 1024)
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False)
+    st = P.initial_series(sp, 0, 1, order=2)
+    bd = P.as_device(b)
+    theta = torch.zeros_like(bd)
+    osp = O.split_scalar(a, O.inf_norm(a) / 2.0)
+    ost = O.initial_series(osp, 0, 1, 2)
+    oth = np.zeros_like(b)
+    spec = P.CompositeSpec((2, 3, 4, 5))
+    for k in range(8):
+        theta = P.plain_richardson(theta, st.estimate, sp.matrix, bd, st.ctr)
+        st = P.composite_step(st, sp.matrix, sp, spec, 2)
+        oth = O.plain_richardson(oth, ost.estimate, osp.matrix, b, ost.ctr)
+        ost = O.composite_step(ost, osp.matrix, osp, (2, 3, 4, 5), 2)
+        ep = np.linalg.norm(st.estimate.cpu().numpy() - ost.estimate) / np.linalg.norm(ost.estimate)
+        et = np.linalg.norm(theta.cpu().numpy() - oth) / np.linalg.norm(oth)
+        assert ep <= tol and et <= tol, (k, ep, et)
+    assert (st.ctr.mmm, st.ctr.mvm) == (ost.ctr.mmm, ost.ctr.mvm)
