@@ -188,6 +188,58 @@ def resident_roofline(w, tflops_per_gpu: float, step_s: float, peak: float) -> d
             "peak_source": "measured live: DMMA m8n8k4 register-only probe (si_dmma_peak)"}
 
 
+def int8_peak_tops() -> tuple[float, str]:
+    """Measured INT8 tensor-core yardstick: cuBLASLt int8 GEMM 8192^3
+    (torch._int_mm, int8 x int8 -> int32), best of 10 launches (burst, like
+    MEASURED_PEAKS.json's bf16 figure); MEASURED_PEAKS.json has no INT8 entry."""
+    import torch
+
+    n = 8192
+    g = torch.Generator(device="cuda").manual_seed(0)
+    a = torch.randint(-128, 128, (n, n), dtype=torch.int8, device="cuda", generator=g)
+    b = torch.randint(-128, 128, (n, n), dtype=torch.int8, device="cuda", generator=g).t()
+    torch._int_mm(a, b)
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch._int_mm(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2.0 * n**3 / (best * 1e-3) / 1e12, (
+        "measured live: cuBLASLt int8 GEMM 8192^3 (torch._int_mm), best of 10; "
+        "MEASURED_PEAKS.json has no INT8 entry (nominal dense INT8: 4500 TOPS)")
+
+
+def ozaki_roofline(w, i8_ms: float, i8_ops: float, i8_launches: int, fp64_achieved, fp64_launches,
+                   dmma_peak: float, moduli: int) -> dict:
+    """Roofline of the Ozaki-II products: the dominant kernel is the INT8
+    tcgen05 GEMM (i8_gemm_mod_kernel); achieved = its algorithmic int8 ops
+    (2 M N Kp per modulus plane) / its CUDA-event time on the launching stream."""
+    peak, src = int8_peak_tops()
+    ach = i8_ops / (i8_ms * 1e-3) / 1e12 if i8_ms > 0 else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            rec = json.load(fh).get("i8_gemm_mod_kernel", {}).get(str(w.n))
+        traffic = float(rec["dram_bytes_per_launch"]) if rec else None
+    except (OSError, ValueError, KeyError):
+        pass
+    return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOPS (int8)",
+            "frac": ach / peak if ach else None, "traffic": traffic,
+            "kernel": "i8_gemm_mod_kernel", "launches": i8_launches, "moduli": moduli,
+            "peak_source": src,
+            "fp64_equivalent": {
+                "what": "whole emulated products (scaling, residues, INT8 GEMM, CRT + epilogue): "
+                        "2 M N K FP64 FLOP / their CUDA-event time",
+                "achieved_tflops": fp64_achieved, "launches": fp64_launches,
+                "dmma_peak_tflops": dmma_peak,
+                "frac_of_dmma_peak": fp64_achieved / dmma_peak if fp64_achieved else None}}
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -1224,6 +1276,10 @@ def run_ours(args):
     w.setup()
     flops = w.flops()
     h = _lib.handle()
+    ozaki = args.gemm == "ozaki" and w.cfg in ("c3", "c4", "c5")
+    if ozaki:
+        # after setup (the PD check / verification products stay on DMMA)
+        w.P.set_gemm_backend("ozaki", moduli=args.moduli, min_dim=1024)
     for _ in range(args.warmup):
         w.step()
     torch.cuda.synchronize()
@@ -1247,6 +1303,8 @@ def run_ours(args):
     g_n, launches = ctypes.c_int64(), ctypes.c_int64()
     _lib.call("si_profile_end", h, ctypes.byref(g_ms), ctypes.byref(g_fl), ctypes.byref(g_n),
               ctypes.byref(launches))
+    i8_ms, i8_ops, i8_n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+    _lib.call("si_profile_i8", h, ctypes.byref(i8_ms), ctypes.byref(i8_ops), ctypes.byref(i8_n))
     clocks = sampler.stop()
     print("rank-info " + json.dumps(rank_info(w, args, world, rank, local)), file=sys.stderr,
           flush=True)
@@ -1337,7 +1395,10 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
             "iters_per_step": w.iters_per_step,
             "higher_is_better": True, "scaling": "strong" if strong else "weak",
-            "vs_baseline": None, "dtype": "f64",
+            "vs_baseline": None,
+            "dtype": (f"int8 tensor cores -> f64 (Ozaki-II FP64 emulation, {args.moduli} moduli)"
+                      if ozaki else "f64"),
+            "gemm_backend": "ozaki" if ozaki else "dmma",
             "data": "synthetic (seeded PCG64 draws, SURVEY Appendix A recipe)",
             "config": config_of(w),
             "parallelism": layout_note(w) + (f"composite parts on GPU groups x{world} (NCCL p2p tree)"
@@ -1350,6 +1411,8 @@ def run_ours(args):
             "tflops": tflops,
             "tflops_frac_of_dmma_peak": tflops / (world * peak.value),
             "roofline": resident_roofline(w, tflops / world, step_s, peak.value) if w.cfg in ("c1", "c2") else
+                        ozaki_roofline(w, i8_ms.value, i8_ops.value, i8_n.value, achieved, g_n.value,
+                                       peak.value, args.moduli) if ozaki else
                         {"bound": "tensor", "achieved": achieved, "peak": peak.value,
                          "unit": "TFLOP/s", "frac": (achieved / peak.value) if achieved else None,
                          "traffic": ncu_traffic(w), "kernel": "gemm_f64_tma_kernel",
@@ -1359,6 +1422,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "gpu_launches": launches.value,
             "setup_s": getattr(w, "setup_s", None),
+            "hbm_peak_gb": torch.cuda.max_memory_allocated() / 1e9,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -1388,6 +1452,11 @@ def main():
     ap.add_argument("--shard", choices=["rows", "parts"], default="rows",
                     help="c4 at N > 1: block-row sharding of every product (rows) or the "
                          "composite parts on GPU groups + one tree reduction (parts)")
+    ap.add_argument("--gemm", choices=["dmma", "ozaki"], default="dmma",
+                    help="FP64 product backend of the dense configs (c3/c4/c5): FP64 DMMA, "
+                         "or Ozaki-II emulation on the INT8 tensor cores (si_set_gemm_backend)")
+    ap.add_argument("--moduli", type=int, default=16,
+                    help="--gemm ozaki: number of moduli (16 = at least DGEMM's accuracy)")
     ap.add_argument("--ref-budget", type=float, default=300.0,
                     help="--impl reference, c4/c5: wall-clock budget (s) for the executed "
                          "full-size CPU steps (at least one is always executed)")

@@ -440,11 +440,23 @@ SI_API int si_dmma_peak(si_handle h, int iters, double* tflops);
 #define SI_GEMM_OZAKI_I8 1
 SI_API int si_set_gemm_backend(si_handle h, int backend, int nmoduli, int64_t min_dim);
 SI_API int si_get_gemm_backend(si_handle h, int* backend, int* nmoduli, int64_t* min_dim);
+/* Workspace bound of the emulated products: D is processed in chunks of at
+ * most max_rows x max_cols (rounded down to multiples of 256; 0 = automatic:
+ * all rows, and <= 10 GiB of B-side and result planes per column chunk).  The
+ * A-side planes are built once per row chunk, the B-side planes once per
+ * product when one column chunk covers D, else per (row, column) chunk.  When
+ * the allocator cannot serve a product's workspace the library retries with
+ * halved chunks.  Results do not depend on the chunking (bitwise). */
+SI_API int si_set_ozaki_chunks(si_handle h, int64_t max_rows, int64_t max_cols);
+/* INT8 tensor-core kernel of the emulated products: 0 = automatic (CTA pairs),
+ * 1 = CTA pairs (tcgen05.mma.cta_group::2, 256 x 256 tiles), 2 = single CTAs
+ * (cta_group::1, 128 x 256 tiles).  Results are identical (exact integers). */
+SI_API int si_set_ozaki_kernel(si_handle h, int variant);
 /* The first n moduli of the emulation. */
 SI_API int si_ozaki_moduli(int n, uint32_t* moduli);
 /* The INT8 tensor-core kernel alone (test hook): r[l] = (a[l] @ bt[l]^T) mod
  * m_l for l < nplanes; a[l]: m x kp int8, bt[l]: n x kp int8 (row-major, kp a
- * multiple of 128), r[l]: m x n uint8. */
+ * multiple of 128), r[l]: m x n uint8; the kernel si_set_ozaki_kernel selected. */
 SI_API int si_i8_gemm_mod(si_handle h, const int8_t* a, const int8_t* bt, uint8_t* r, int64_t m,
                           int64_t n, int64_t kp, int nplanes, void* stream);
 /* Summed device time (ms) and int8 operations of the INT8 tensor-core kernel

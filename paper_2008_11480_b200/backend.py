@@ -57,6 +57,27 @@ def gemm_backend(name: str, moduli: int = 0, min_dim: int = 0, device: int | Non
         set_gemm_backend(prev[0], prev[1], prev[2], device)
 
 
+def set_ozaki_chunks(max_rows: int = 0, max_cols: int = 0, device: int | None = None) -> None:
+    """Bound the emulated products' workspace: D in chunks of at most
+    ``max_rows`` x ``max_cols`` (multiples of 256; 0 = automatic).  Results do
+    not depend on the chunking (bitwise)."""
+    if max_rows < 0 or max_cols < 0:
+        raise ValueError("chunk bounds must be >= 0")
+    _lib.call("si_set_ozaki_chunks", _lib.handle(device), int(max_rows), int(max_cols))
+
+
+_KERNELS = {"auto": 0, "pair": 1, "single": 2}
+
+
+def set_ozaki_kernel(name: str, device: int | None = None) -> None:
+    """INT8 tensor-core kernel of the emulated products: ``"pair"`` (2-CTA
+    clusters, tcgen05.mma.cta_group::2, 256 x 256 tiles; what ``"auto"``
+    picks) or ``"single"`` (one CTA per 128 x 256 tile).  Results are identical."""
+    if name not in _KERNELS:
+        raise ValueError(f"unknown INT8 kernel {name!r} (expected one of {sorted(_KERNELS)})")
+    _lib.call("si_set_ozaki_kernel", _lib.handle(device), _KERNELS[name])
+
+
 def ozaki_moduli(n: int = 16) -> list[int]:
     """The first ``n`` moduli of the emulation (pairwise coprime, <= 256)."""
     out = (ctypes.c_uint32 * n)()

@@ -1219,6 +1219,26 @@ int si_get_gemm_backend(si_handle h, int* backend, int* nmoduli, int64_t* min_di
   });
 }
 
+int si_set_ozaki_chunks(si_handle h, int64_t max_rows, int64_t max_cols) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(max_rows >= 0 && max_cols >= 0, "negative chunk bound");
+    std::lock_guard<std::recursive_mutex> lock(h->h.mu);
+    h->h.oz_max_rows = max_rows;
+    h->h.oz_max_cols = max_cols;
+  });
+}
+
+int si_set_ozaki_kernel(si_handle h, int variant) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    need(variant == oz::kI8Auto || variant == oz::kI8Pair || variant == oz::kI8Single,
+         "unknown INT8 kernel variant");
+    std::lock_guard<std::recursive_mutex> lock(h->h.mu);
+    h->h.oz_variant = variant;
+  });
+}
+
 int si_ozaki_moduli(int n, uint32_t* moduli) {
   return guard([&] {
     need(moduli != nullptr && n >= 1 && n <= oz::kMaxModuli, "bad arguments");
@@ -1234,7 +1254,8 @@ int si_i8_gemm_mod(si_handle h, const int8_t* a, const int8_t* bt, uint8_t* r, i
     need(kp <= oz::kMaxK, "kp too large");
     need(nplanes >= 1 && nplanes <= oz::kMaxModuli, "nplanes out of range");
     Call call(h, stream, nullptr);
-    check(oz::launch_i8_gemm_mod(a, bt, r, m, n, kp, nplanes, call.c.s), "i8 gemm launch");
+    check(oz::launch_i8_gemm_mod(a, bt, r, m, n, kp, nplanes, call.c.s, h->h.oz_variant),
+          "i8 gemm launch");
     h->h.launches += 1;
   });
 }

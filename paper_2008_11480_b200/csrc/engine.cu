@@ -139,11 +139,17 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
   }
   const bool use_tma = d.rows > 0 && d.cols > 4 && std::max(d.rows, d.cols) >= 128 &&
                        A.v.cols > 0 && tma_eligible(A.v, B.v, d, e);
+  // Ozaki-II products (backend 1): inputs still in flight are awaited on the
+  // stream (whole operands); the residue kernels have no in-kernel gates
+  const bool use_oz = h->gemm_backend == 1 && d.rows >= h->oz_min_dim &&
+                      d.cols >= h->oz_min_dim && A.v.cols >= h->oz_min_dim &&
+                      A.v.cols <= oz::kMaxK;
+  const bool in_kernel_gates = use_tma && !use_oz;
   // inputs still arriving in row panels: in-kernel gates for A rows / B k-slabs
   // of the DMMA GEMM, stream waits for everything else
   const PanelWait* pwa = nullptr;
   if (!c.gates.empty()) {
-    if (use_tma) {
+    if (in_kernel_gates) {
       pwa = c.gate_of(A.v.p);
       if (!pw) pw = c.gate_of(B.v.p);
       if (C && C->v.p != B.v.p) c.gate_stream(C->v.p);  // C == B: its panels gate the k-loop
@@ -154,18 +160,15 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
     }
   }
   const bool gated = pw && pw->ready && pw->npanels > 0;
-  if (gated && !use_tma) {
+  if (gated && !in_kernel_gates) {
     // kernels without the in-kernel gate: the stream waits for every panel
     for (int p = 0; p < pw->npanels; ++p)
       check(stream_wait_u32(pw->ready + p, pw->epoch, c.s), "panel wait");
   }
-  const bool use_oz = h->gemm_backend == 1 && !gated && pwa == nullptr &&
-                      d.rows >= h->oz_min_dim && d.cols >= h->oz_min_dim &&
-                      A.v.cols >= h->oz_min_dim && A.v.cols <= oz::kMaxK;
   if (d.rows == 0 || d.cols == 0) {
     err = cudaSuccess;
   } else if (use_oz) {
-    Handle::ProfRec rec{}, rec8{};
+    Handle::ProfRec rec{};
     auto draw = [&](cudaEvent_t* ev) {
       if (h->prof_pool.empty()) {
         check(cudaEventCreate(ev), "cudaEventCreate");
@@ -175,25 +178,55 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
       }
     };
     if (h->profiling) {
-      for (cudaEvent_t* ev : {&rec.start, &rec.stop, &rec8.start, &rec8.stop}) draw(ev);
+      for (cudaEvent_t* ev : {&rec.start, &rec.stop}) draw(ev);
       rec.flops = 2.0 * (double)d.rows * (double)d.cols * (double)A.v.cols;
-      rec8.flops = 2.0 * (double)d.rows * (double)d.cols * (double)((A.v.cols + 127) / 128 * 128) *
-                   (double)h->oz_nmod;
       check(cudaEventRecord(rec.start, c.s), "cudaEventRecord");
     }
-    const size_t wb = oz::workspace_bytes(d.rows, d.cols, A.v.cols, h->oz_nmod);
-    MV ws = alloc(c, 1, (int64_t)((wb + 7) / 8));
+    // workspace: the configured chunking first; when the allocator cannot
+    // serve it, smaller row x column chunks (halved each retry; the B-side
+    // planes are then rebuilt per row chunk)
     oz::Work w;
+    w.max_cols = h->oz_max_cols;
+    w.max_rows = h->oz_max_rows;
+    w.variant = h->oz_variant;
+    MV ws;
+    for (int level = 0;; ++level) {
+      w.bytes = oz::workspace_bytes(d.rows, d.cols, A.v.cols, h->oz_nmod, w.max_cols, w.max_rows);
+      try {
+        ws = alloc(c, 1, (int64_t)((w.bytes + 7) / 8));
+        break;
+      } catch (const Error& ex) {
+        if (ex.code != kENoMem || level == 4 || (w.max_rows > 0 && w.max_rows <= 1024)) throw;
+        const int64_t rows = w.max_rows > 0 ? w.max_rows : d.rows;
+        const int64_t cols = w.max_cols > 0 ? std::min(w.max_cols, d.cols) : d.cols;
+        w.max_rows = std::max<int64_t>(1024, rows / 2);
+        w.max_cols = std::max<int64_t>(1024, cols / 2);
+      }
+    }
     w.base = reinterpret_cast<uint8_t*>(ws.v.p);
-    w.bytes = wb;
     int64_t nl = 0;
-    err = oz::launch_gemm(A.v, B.v, d, e, h->oz_nmod, w, c.s, &nl,
-                          h->profiling ? rec8.start : nullptr, h->profiling ? rec8.stop : nullptr);
+    // one event pair per INT8 tensor-core launch (column chunks)
+    Handle::ProfRec rec8{};
+    oz::I8Hook hook;
+    if (h->profiling) {
+      hook = [&](bool begin, double ops) {
+        if (begin) {
+          rec8 = Handle::ProfRec{};
+          draw(&rec8.start);
+          draw(&rec8.stop);
+          rec8.flops = ops;
+          check(cudaEventRecord(rec8.start, c.s), "cudaEventRecord");
+        } else {
+          check(cudaEventRecord(rec8.stop, c.s), "cudaEventRecord");
+          h->prof_i8.push_back(rec8);
+        }
+      };
+    }
+    err = oz::launch_gemm(A.v, B.v, d, e, h->oz_nmod, w, c.s, &nl, hook);
     h->launches += nl;
     if (h->profiling && err == cudaSuccess) {
       check(cudaEventRecord(rec.stop, c.s), "cudaEventRecord");
       h->prof.push_back(rec);
-      h->prof_i8.push_back(rec8);
     }
   } else if (d.cols <= 4) {
     err = launch_gemv(A.v, B.v, d, e, c.s);

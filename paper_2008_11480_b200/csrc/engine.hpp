@@ -46,6 +46,9 @@ struct Handle {
   int gemm_backend = 0;
   int oz_nmod = 16;
   int64_t oz_min_dim = 1024;
+  int64_t oz_max_cols = 0;  // columns of D per emulated chunk at most (0: automatic)
+  int64_t oz_max_rows = 0;  // rows of D per emulated chunk at most (0: all rows)
+  int oz_variant = 0;       // INT8 kernel: 0 auto (CTA pairs), 1 CTA pairs, 2 single CTAs
   // live profiling of the INT8 tensor-core kernel inside emulated products
   std::vector<ProfRec> prof_i8;
   // Optional external allocator (si_set_allocator): the Python layer routes

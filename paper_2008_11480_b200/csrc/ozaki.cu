@@ -529,6 +529,234 @@ __global__ void __launch_bounds__(GTHREADS, 1)
   }
 }
 
+// ---------------------------------------- INT8 GEMM on CTA pairs (2 SMs) --
+// Same product as i8_gemm_mod_kernel on 256 x 256 pair tiles: a 2-CTA cluster
+// issues tcgen05.mma.cta_group::2 (M = 256, N = 256) from the leader CTA; each
+// CTA stages its own 128 rows of A and 128 of the 256 rows of Bt (half of the
+// B tile), so per SM the shared-memory operand traffic per MMA is 8 KB instead
+// of 12 KB for the single-CTA 128 x 256 tile, and every Bt / A k-slab crosses
+// L2 once per pair.  TMA of both CTAs completes on the leader's full barrier;
+// the leader's MMA commits free the stage in both CTAs (multicast); each CTA's
+// epilogue drains its own TMEM rows and arrives on the leader's TMEM-empty
+// barrier.
+constexpr int PBM = 256, PBN = 256;  // pair tile (each CTA: 128 rows of A, 128 rows of Bt)
+constexpr int PSTAGES = 6;
+constexpr int PA_BYTES = (PBM / 2) * GBK;  // 16 KB
+constexpr int PB_BYTES = (PBN / 2) * GBK;  // 16 KB
+constexpr int PSTAGE_BYTES = PA_BYTES + PB_BYTES;
+constexpr int PSMEM = PSTAGES * PSTAGE_BYTES + 1024 + 256;
+constexpr uint32_t kIdescPair = (2u << 4) | (1u << 7) | (1u << 10) |
+                                ((uint32_t)(PBN >> 3) << 17) | ((uint32_t)(PBM >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t leader_addr(uint32_t a) {  // a in the leader CTA's window
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                 int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdescPair), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {  // both CTAs' barrier at `bar`
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GTHREADS, 1)
+    i8_gemm_mod_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                            const __grid_constant__ CUtensorMap tmB, uint8_t* __restrict__ R,
+                            int M, int N, int Kp, int nplanes, const __grid_constant__ ModTab mt) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bars = base + PSTAGES * PSTAGE_BYTES;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (PSTAGES + s); };
+  auto tfull_bar = [&](int a) { return bars + 8u * (2 * PSTAGES + a); };
+  auto tempty_bar = [&](int a) { return bars + 8u * (2 * PSTAGES + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * PSTAGES + 4);
+  uint8_t* smem_gen = smem_raw + (tmem_slot - raw);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const int num_m = (M + PBM - 1) / PBM;
+  const int num_n = (N + PBN - 1) / PBN;
+  const int total = num_m * num_n * nplanes;
+  const int kblocks = Kp / GBK;
+  const int cid = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < PSTAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 2 * 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tmem_slot),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(smem_gen);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs: own A rows, own half of Bt) ----
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < total; t += nclusters) {
+        int plane, tm, tn;
+        tile_of(t, num_m, num_n, plane, tm, tn);
+        const int arow = tm * PBM + (int)rank * (PBM / 2);
+        const int brow = tn * PBN + (int)rank * (PBN / 2);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1u);
+          const uint32_t sa = base + stage * PSTAGE_BYTES;
+          const uint32_t fb = leader_addr(full_bar(stage));
+          if (rank == 0) mbar_expect_tx(full_bar(stage), 2 * PSTAGE_BYTES);
+          tma_load_3d_pair(sa, &tmA, fb, kb * GBK, arow, plane);
+          tma_load_3d_pair(sa + PA_BYTES, &tmB, fb, kb * GBK, brow, plane);
+          if (++stage == PSTAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (leader CTA, one thread) ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int t = cid; t < total; t += nclusters) {
+        mbar_wait(tempty_bar(acc), aphase ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * PBN);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(full_bar(stage), phase);
+          tc_fence_after();
+          const uint32_t sa = base + stage * PSTAGE_BYTES;
+          const uint64_t adesc = sdesc(sa), bdesc = sdesc(sa + PA_BYTES);
+#pragma unroll
+          for (int k = 0; k < GBK / 32; ++k)
+            mma_i8_pair(d, adesc + 2 * k, bdesc + 2 * k, (kb | k) != 0 ? 1u : 0u);
+          mma_commit_pair(empty_bar(stage));
+          if (++stage == PSTAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        mma_commit_pair(tfull_bar(acc));
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue (both CTAs: own 128 rows of the pair tile) ----
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int t = cid; t < total; t += nclusters) {
+      int plane, tm, tn;
+      tile_of(t, num_m, num_n, plane, tm, tn);
+      const unsigned m = mt.m[plane], magic = mt.magic[plane], off = mt.off[plane];
+      mbar_wait(tfull_bar(acc), aphase);
+      tc_fence_after();
+      const int row = tm * PBM + (int)rank * (PBM / 2) + q * 32 + lane;
+      const int col0 = tn * PBN;
+      uint8_t* rp = R + (int64_t)plane * M * N + (int64_t)row * N + col0;
+      const bool vec = ((N & 15) == 0);
+#pragma unroll 1
+      for (int c = 0; c < PBN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * PBN + c * 32), v);
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          uint32_t b[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t u = v[i + j] + (1u << 30);
+            const uint32_t qq = __umulhi(u, magic) >> 7;
+            uint32_t r = u - qq * m;
+            r = r >= off ? r - off : r + m - off;
+            b[j] = r;
+          }
+          w[i >> 2] = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+        }
+        const int cc = col0 + c * 32;
+        if (row < M && cc < N) {
+          if (vec && cc + 32 <= N) {
+            uint4* dst = reinterpret_cast<uint4*>(rp + c * 32);
+            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          } else {
+            for (int i = 0; i < 32 && cc + i < N; ++i) rp[c * 32 + i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(leader_addr(tempty_bar(acc)));
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1u;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(kTmemCols)
+                 : "memory");
+  }
+}
+
 // ------------------------------------------------------------------ CRT --
 // X = sum_l c_l W_l (W_l the CRT weights, c_l in [0, m_l)) is held exactly as
 // four partial sums S_k of 32-bit pieces (c_l * piece < 2^40, 16 terms < 2^44);
@@ -711,6 +939,9 @@ cudaError_t set_gemm_attr() {
   if (dev < 64 && (done.load() & (1ull << dev))) return cudaSuccess;
   cudaError_t e =
       cudaFuncSetAttribute(i8_gemm_mod_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GSMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(i8_gemm_mod_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             PSMEM);
   if (e == cudaSuccess && dev < 64) done.fetch_or(1ull << dev);
   return e;
 }
@@ -722,86 +953,135 @@ inline int64_t kpad(int64_t K) { return (K + GBK - 1) / GBK * GBK; }
 
 unsigned modulus(int l) { return kmod(l); }
 
-size_t workspace_bytes(int64_t M, int64_t N, int64_t K, int nmod) {
+namespace {
+// columns of D per chunk: B-side planes (nmod x Nc x Kp) + result planes
+// (nmod x M x Nc) within kChunkBudget, a multiple of the INT8 tile width
+int64_t chunk_cols(int64_t M, int64_t N, int64_t Kp, int nmod, int64_t max_cols) {
+  const size_t per_col = (size_t)nmod * (size_t)(Kp + M);
+  int64_t fit = std::max<int64_t>(GBN, (int64_t)(kChunkBudget / per_col) / GBN * GBN);
+  if (max_cols > 0) fit = std::min(fit, std::max<int64_t>(GBN, max_cols / GBN * GBN));
+  if (fit >= N) return N;
+  const int64_t nch = (N + fit - 1) / fit;
+  const int64_t nc = ((N + nch - 1) / nch + GBN - 1) / GBN * GBN;  // balanced chunks
+  return std::min(nc, N);
+}
+}  // namespace
+
+int64_t chunk_rows(int64_t M, int64_t max_rows) {
+  if (max_rows <= 0 || max_rows >= M) return M;
+  const int64_t fit = std::max<int64_t>(PBM, max_rows / PBM * PBM);
+  const int64_t nch = (M + fit - 1) / fit;
+  return std::min(M, ((M + nch - 1) / nch + PBM - 1) / PBM * PBM);  // balanced chunks
+}
+
+size_t workspace_bytes(int64_t M, int64_t N, int64_t K, int nmod, int64_t max_cols,
+                       int64_t max_rows) {
   const int64_t Kp = kpad(K);
-  return align256(M * 8) + align256(N * 8) + align256((size_t)nmod * M * Kp) +
-         align256((size_t)nmod * N * Kp) + align256((size_t)nmod * M * N);
+  const int64_t mc = chunk_rows(M, max_rows);
+  const int64_t nc = chunk_cols(mc, N, Kp, nmod, max_cols);
+  return align256(mc * 8) + align256(nc * 8) + align256((size_t)nmod * mc * Kp) +
+         align256((size_t)nmod * nc * Kp) + align256((size_t)nmod * mc * nc);
 }
 
 cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, int64_t M, int64_t N,
-                               int64_t Kp, int nplanes, cudaStream_t s) {
+                               int64_t Kp, int nplanes, cudaStream_t s, int variant) {
   if (M <= 0 || N <= 0 || Kp <= 0 || Kp % GBK || nplanes < 1 || nplanes > kMaxModuli ||
-      M > INT32_MAX || N > INT32_MAX || Kp > kMaxK + GBK)
+      M > INT32_MAX || N > INT32_MAX || Kp > kMaxK + GBK || variant < 0 || variant > 2)
     return cudaErrorInvalidValue;
+  const bool pair = variant != kI8Single;
   CUtensorMap ta, tb;
-  if (!make_map_i8(&ta, A, Kp, M, nplanes, GBM) || !make_map_i8(&tb, Bt, Kp, N, nplanes, GBN)) {
+  if (!make_map_i8(&ta, A, Kp, M, nplanes, pair ? PBM / 2 : GBM) ||
+      !make_map_i8(&tb, Bt, Kp, N, nplanes, pair ? PBN / 2 : GBN)) {
     set_error("cuTensorMapEncodeTiled failed (int8 planes)");
     return cudaErrorInvalidValue;
   }
   cudaError_t e = set_gemm_attr();
   if (e != cudaSuccess) return e;
-  const int64_t tiles = ((M + GBM - 1) / GBM) * ((N + GBN - 1) / GBN) * nplanes;
-  const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  i8_gemm_mod_kernel<<<grid, GTHREADS, GSMEM, s>>>(ta, tb, R, (int)M, (int)N, (int)Kp, nplanes,
-                                                   consts().mt);
+  const int sms = num_sms();
+  if (pair) {
+    const int64_t tiles = ((M + PBM - 1) / PBM) * ((N + PBN - 1) / PBN) * nplanes;
+    const int grid = (int)std::min<int64_t>(2 * tiles, sms & ~1);
+    i8_gemm_mod_pair_kernel<<<grid, GTHREADS, PSMEM, s>>>(ta, tb, R, (int)M, (int)N, (int)Kp,
+                                                          nplanes, consts().mt);
+  } else {
+    const int64_t tiles = ((M + GBM - 1) / GBM) * ((N + GBN - 1) / GBN) * nplanes;
+    const int grid = (int)(tiles < sms ? tiles : sms);
+    i8_gemm_mod_kernel<<<grid, GTHREADS, GSMEM, s>>>(ta, tb, R, (int)M, (int)N, (int)Kp, nplanes,
+                                                     consts().mt);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, int nmod,
-                        const Work& w, cudaStream_t s, int64_t* launches, cudaEvent_t ev0,
-                        cudaEvent_t ev1) {
+                        const Work& w, cudaStream_t s, int64_t* launches, const I8Hook& hook) {
   const int64_t M = D.rows, N = D.cols, K = A.cols;
   if (nmod < kMinModuli || nmod > kMaxModuli || K < 1 || K > kMaxK || M > INT32_MAX ||
-      N > INT32_MAX || w.bytes < workspace_bytes(M, N, K, nmod))
+      N > INT32_MAX || w.bytes < workspace_bytes(M, N, K, nmod, w.max_cols, w.max_rows))
     return cudaErrorInvalidValue;
   const Consts& cs = consts();
   const int64_t Kp = kpad(K);
+  const int64_t MC = chunk_rows(M, w.max_rows);
+  const int64_t NC = chunk_cols(MC, N, Kp, nmod, w.max_cols);
   int lk = 0;
   while ((1ll << lk) < K) ++lk;
   const int T = cs.log2m[nmod] - 2 - lk;  // K 2^(pa+pb) <= 2^(log2 M - 2) <= M / 4
   const int pa = std::min(kMaxP, (T + 1) / 2), pb = std::min(kMaxP, T / 2);
   uint8_t* p = w.base;
   auto* rmax = reinterpret_cast<unsigned long long*>(p);
-  p += align256(M * 8);
+  p += align256(MC * 8);
   auto* cmax = reinterpret_cast<unsigned long long*>(p);
-  p += align256(N * 8);
+  p += align256(NC * 8);
   auto* ares = reinterpret_cast<int8_t*>(p);
-  p += align256((size_t)nmod * M * Kp);
+  p += align256((size_t)nmod * MC * Kp);
   auto* bres = reinterpret_cast<int8_t*>(p);
-  p += align256((size_t)nmod * N * Kp);
+  p += align256((size_t)nmod * NC * Kp);
   auto* res = p;
   int64_t n = 0;
   cudaError_t err;
   const int sms = num_sms();
-  row_absmax_kernel<<<(int)std::min<int64_t>((M + 7) / 8, 16 * sms), 256, 0, s>>>(A.p, A.ld, (int)M,
-                                                                                (int)K, rmax);
-  ++n;
-  if ((err = cudaMemsetAsync(cmax, 0, N * 8, s)) != cudaSuccess) return err;
-  col_absmax_kernel<<<dim3((unsigned)((N + 31) / 32), (unsigned)((K + 255) / 256)), 256, 0, s>>>(
-      B.p, B.ld, (int)K, (int)N, cmax);
-  ++n;
-  {
-    const int64_t thr = M * (Kp / 16);
-    const int blocks = (int)std::min<int64_t>((thr + 255) / 256, 64 * sms);
-    residues_rows_kernel<<<blocks, 256, 0, s>>>(A.p, A.ld, (int)M, (int)K, (int)Kp, rmax, pa, nmod,
-                                                 ares);
+  for (int64_t i0 = 0; i0 < M; i0 += MC) {
+    const int64_t mc = std::min(MC, M - i0);
+    const double* ap = A.p + i0 * A.ld;
+    // A side of this row chunk: row scales and residue planes
+    row_absmax_kernel<<<(int)std::min<int64_t>((mc + 7) / 8, 16 * sms), 256, 0, s>>>(
+        ap, A.ld, (int)mc, (int)K, rmax);
     ++n;
-  }
-  residues_cols_kernel<<<dim3((unsigned)((N + 63) / 64), (unsigned)(Kp / 64)), 256, 0, s>>>(
-      B.p, B.ld, (int)K, (int)N, (int)Kp, cmax, pb, nmod, bres);
-  ++n;
-  if ((err = cudaGetLastError()) != cudaSuccess) return err;
-  if (ev0 && (err = cudaEventRecord(ev0, s)) != cudaSuccess) return err;
-  if ((err = launch_i8_gemm_mod(ares, bres, res, M, N, Kp, nmod, s)) != cudaSuccess) return err;
-  if (ev1 && (err = cudaEventRecord(ev1, s)) != cudaSuccess) return err;
-  ++n;
-  {
-    const int64_t thr = M * ((N + 3) / 4);
-    const int blocks = (int)std::min<int64_t>((thr + 255) / 256, 64 * sms);
-    crt_kernel<<<blocks, 256, 0, s>>>(res, (int)M, (int)N, rmax, cmax, pa, pb, cs.crt[nmod], D.p,
-                                      D.ld, e.beta != 0.0 ? e.c : nullptr, e.ldc, e.alpha, e.beta,
-                                      e.diag, e.doff);
-    ++n;
+    {
+      const int64_t thr = mc * (Kp / 16);
+      const int blocks = (int)std::min<int64_t>((thr + 255) / 256, 64 * sms);
+      residues_rows_kernel<<<blocks, 256, 0, s>>>(ap, A.ld, (int)mc, (int)K, (int)Kp, rmax, pa,
+                                                   nmod, ares);
+      ++n;
+    }
+    // B side (kept across row chunks when one column chunk covers N), the
+    // tensor-core products and the reconstruction per column chunk
+    for (int64_t j0 = 0; j0 < N; j0 += NC) {
+      const int64_t nc = std::min(NC, N - j0);
+      if (i0 == 0 || NC < N) {
+        const double* bp = B.p + j0;
+        if ((err = cudaMemsetAsync(cmax, 0, nc * 8, s)) != cudaSuccess) return err;
+        col_absmax_kernel<<<dim3((unsigned)((nc + 31) / 32), (unsigned)((K + 255) / 256)), 256, 0,
+                            s>>>(bp, B.ld, (int)K, (int)nc, cmax);
+        ++n;
+        residues_cols_kernel<<<dim3((unsigned)((nc + 63) / 64), (unsigned)(Kp / 64)), 256, 0, s>>>(
+            bp, B.ld, (int)K, (int)nc, (int)Kp, cmax, pb, nmod, bres);
+        ++n;
+      }
+      if ((err = cudaGetLastError()) != cudaSuccess) return err;
+      if (hook) hook(true, 2.0 * (double)mc * (double)nc * (double)Kp * (double)nmod);
+      if ((err = launch_i8_gemm_mod(ares, bres, res, mc, nc, Kp, nmod, s, w.variant)) !=
+          cudaSuccess)
+        return err;
+      if (hook) hook(false, 0.0);
+      ++n;
+      const int64_t thr = mc * ((nc + 3) / 4);
+      const int blocks = (int)std::min<int64_t>((thr + 255) / 256, 64 * sms);
+      crt_kernel<<<blocks, 256, 0, s>>>(
+          res, (int)mc, (int)nc, rmax, cmax, pa, pb, cs.crt[nmod], D.p + i0 * D.ld + j0, D.ld,
+          e.beta != 0.0 ? e.c + i0 * e.ldc + j0 : nullptr, e.ldc, e.alpha, e.beta, e.diag,
+          e.doff + i0 - j0);
+      ++n;
+    }
   }
   if (launches) *launches += n;
   return cudaGetLastError();

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 
 #include "common.cuh"
 
@@ -15,29 +16,49 @@ constexpr int64_t kMaxK = 65536;  // |sum of K products of int8 residues| < 2^30
 
 // Device workspace of one emulated product, carved by the caller (engine.cu)
 // from one allocation of workspace_bytes().
+// INT8 tensor-core kernel: CTA pairs (cta_group::2, 256 x 256 tiles; default)
+// or single CTAs (128 x 256 tiles).  Results are identical (exact integers).
+constexpr int kI8Auto = 0, kI8Pair = 1, kI8Single = 2;
+
 struct Work {
   uint8_t* base = nullptr;
   size_t bytes = 0;
+  int64_t max_cols = 0;  // columns of D per chunk at most (0: kChunkBudget decides)
+  int64_t max_rows = 0;  // rows of D per chunk at most (0: all rows)
+  int variant = kI8Auto;  // INT8 kernel
 };
 
+// Column chunking: the B-side residue planes and the result planes of one
+// chunk of D's columns take at most this many bytes (the A-side planes are
+// built once and shared by every chunk), so a 32768^2 product needs ~28 GB
+// of workspace instead of ~52 GB.
+constexpr size_t kChunkBudget = (size_t)10 << 30;
+
 // Bytes of device workspace an M x K by K x N product with `nmod` moduli needs.
-size_t workspace_bytes(int64_t M, int64_t N, int64_t K, int nmod);
+// `max_rows`, `max_cols` as in Work.  With several row chunks the B-side
+// planes are rebuilt per row chunk (unless one column chunk covers N).
+size_t workspace_bytes(int64_t M, int64_t N, int64_t K, int nmod, int64_t max_cols = 0,
+                       int64_t max_rows = 0);
+
+// Called on the stream right before (begin = true) and after (false) every
+// INT8 tensor-core launch of a product, with that launch's int8 op count
+// (2 M Nc Kp per plane, summed over planes) -- the profiling hook.
+using I8Hook = std::function<void(bool begin, double ops)>;
 
 // D = alpha * (A @ B) + beta * C + diag * I (diag at (i, i + doff)), A @ B
 // computed exactly from integer images of A and B on the INT8 tensor cores
 // (tcgen05.mma kind::i8, one GEMM per modulus) and reconstructed by the
 // Chinese remainder theorem.  Stream-ordered, no host synchronisation.
 // Returns the number of kernels launched through *launches.
-// ev0 / ev1 (optional) are recorded around the tensor-core kernel.
 cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, int nmod,
                         const Work& w, cudaStream_t s, int64_t* launches,
-                        cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+                        const I8Hook& hook = nullptr);
 
 // Test hook for the tensor-core kernel alone: R[l] = (A[l] @ Bt[l]^T) mod m_l
 // for l < nplanes, A[l]: M x Kp int8 rows, Bt[l]: N x Kp int8 rows (K-major,
 // Kp a multiple of 128, columns >= K zero), R[l]: M x N uint8.
 cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, int64_t M, int64_t N,
-                               int64_t Kp, int nplanes, cudaStream_t s);
+                               int64_t Kp, int nplanes, cudaStream_t s, int variant = kI8Auto);
 
 // Moduli (pairwise coprime, <= 256) in the order the planes use them.
 unsigned modulus(int l);

@@ -3,6 +3,7 @@
 BASELINE config 4 at its full size (n=16384, 64 RHS): two iterations of plain
 Richardson + composite_step((2,3,4,5), 2) on the GPU (the bench's kernels), the
 same two on the GPU for the permutation-similar Pi A Pi^T (the noise floor),
+the same two with the Ozaki-II INT8 backend (bench.py --gemm ozaki),
 then the CPU oracle on the host cores (~2 min per iteration).  Started by
 conftest.py as soon as collection finishes, so the host-bound oracle overlaps
 the other GPU tests; the test waits for the JSON this writes to <out>/result.json.
@@ -70,6 +71,14 @@ def main():
         floor = max(floor, _rel_t(pu, pd), _rel_t(tu, td))
         del pu, tu, pd, td, p, t
     res["floor"] = floor
+    # the same two iterations with every n x n product emulated on the INT8
+    # tensor cores (Ozaki-II, 16 moduli: the bench's --gemm ozaki)
+    oz = []
+    with P.gemm_backend("ozaki", moduli=16, min_dim=1024):
+        for p, t, ctr in _gpu_c4(P, a, b, iters):
+            oz.append((p.cpu().numpy(), t.cpu().numpy()))
+    res["ozaki_ctr"] = [ctr.mmm, ctr.mvm]
+    res["ozaki_vs_dmma"] = [max(_rel_np(o[0], g[0]), _rel_np(o[1], g[1])) for o, g in zip(oz, gpu)]
     a_np, b_np = a.cpu().numpy(), b.cpu().numpy()
     del a, b, pt
     torch.cuda.synchronize()
@@ -84,6 +93,8 @@ def main():
         oth = O.plain_richardson(oth, ost.estimate, osp.matrix, b_np, ost.ctr)
         ost = O.composite_step(ost, osp.matrix, osp, (2, 3, 4, 5), 2)
         res["per_iteration"].append([_rel_np(gpu[k][0], ost.estimate), _rel_np(gpu[k][1], oth)])
+        res.setdefault("per_iteration_ozaki", []).append(
+            [_rel_np(oz[k][0], ost.estimate), _rel_np(oz[k][1], oth)])
     res["oracle_ctr"] = [ost.ctr.mmm, ost.ctr.mvm]
     with open(os.path.join(out, "result.json.tmp"), "w") as fh:
         json.dump(res, fh)

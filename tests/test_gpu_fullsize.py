@@ -114,43 +114,87 @@ def test_c4_full_size_two_iterations_vs_oracle():
     _log(f"c4 n={n} (full size, {r['iters']} executed iterations): kappa={kappa:.3g} "
          f"err_vs_oracle={err:.3e} gpu_permutation_floor={floor:.3e} tol={tol:.1e}")
     assert err <= max(FACTOR * floor, 64 * np.finfo(np.float64).eps)
+    # the Ozaki-II INT8 backend (bench.py --gemm ozaki) on the same iterations
+    eoz = 0.0
+    for k, (ep, et) in enumerate(r["per_iteration_ozaki"]):
+        _log(f"c4 n={n} rhs={rhs} it={k + 1} ozaki-16: P rel err {ep:.3e}, theta rel err {et:.3e}")
+        eoz = max(eoz, ep, et)
+        assert ep <= tol and et <= tol, (k, ep, et, tol)
+    assert r["ozaki_ctr"] == r["oracle_ctr"]
+    _log(f"c4 n={n} (full size, {r['iters']} executed iterations, ozaki-16 INT8 backend): "
+         f"err_vs_oracle={eoz:.3e} vs_dmma={max(r['ozaki_vs_dmma']):.3e} "
+         f"dmma_permutation_floor={floor:.3e} tol={tol:.1e}")
+    assert eoz <= max(FACTOR * floor, 64 * np.finfo(np.float64).eps)
 
 
-def test_c4_recipe_n4096_40_iterations():
-    """Config 4 recipe at n=4096, the full 40 iterations, every iterate vs the oracle."""
+_C4_ORACLE = {}
+_FLOORS = {}
+
+
+def _c4_oracle(n, rhs, iters):
+    """Config 4 recipe on the host (the oracle's composite DAG), once per size."""
     from oracle import seriesinv_oracle as O
     from paper_2008_11480_b200 import configs
 
+    key = (n, rhs, iters)
+    if key not in _C4_ORACLE:
+        a_np, b_np = configs.c4_householder(n=n, rhs=rhs)
+        lam, _, _ = configs._c4_draws(n, 64, rhs, 0)
+        osp = O.split_scalar(a_np, O.inf_norm(a_np) / 2.0)
+        ost = O.initial_series(osp, 0, 1, 2)
+        oth = np.zeros_like(b_np)
+        seq = []
+        for _ in range(iters):
+            oth = O.plain_richardson(oth, ost.estimate, osp.matrix, b_np, ost.ctr)
+            ost = O.composite_step(ost, osp.matrix, osp, (2, 3, 4, 5), 2)
+            seq.append((ost.estimate.copy(), oth.copy()))
+        _C4_ORACLE[key] = (a_np, b_np, seq, (ost.ctr.mmm, ost.ctr.mvm),
+                           float(lam.max() / lam.min()))
+    return _C4_ORACLE[key]
+
+
+def _floor(key, run, a, b, n):
+    """FP64 noise floor of the DMMA path: GPU(Pi A Pi^T) mapped back vs GPU(A)."""
+    import paper_2008_11480_b200 as P
+
+    if key not in _FLOORS:
+        with P.gemm_backend("dmma"):
+            ref = [(p.clone(), t.clone()) for p, t, *_ in run(a, b)]
+            perm = np.random.default_rng(17).permutation(n)
+            pt = torch.as_tensor(perm, device="cuda")
+            floor = 0.0
+            for k, (p, t, *_) in enumerate(run(_perm_sym(a, pt), b[pt])):
+                floor = max(floor, _rel_t(_unperm_sym(p, perm), ref[k][0]),
+                            _rel_t(_unperm_rows(t, perm), ref[k][1]))
+        _FLOORS[key] = floor
+    return _FLOORS[key]
+
+
+@pytest.mark.parametrize("backend", ["dmma", "ozaki"])
+def test_c4_recipe_n4096_40_iterations(backend):
+    """Config 4 recipe at n=4096, the full 40 iterations, every iterate vs the
+    oracle -- FP64 DMMA, and every n x n product emulated on the INT8 tensor
+    cores (Ozaki-II, 16 moduli; bench.py --gemm ozaki)."""
+    import paper_2008_11480_b200 as P
+
     n, rhs, iters = 4096, 64, 40
-    a_np, b_np = configs.c4_householder(n=n, rhs=rhs)
-    lam, _, _ = configs._c4_draws(n, 64, rhs, 0)
-    kappa = float(lam.max() / lam.min())
+    a_np, b_np, seq, octr, kappa = _c4_oracle(n, rhs, iters)
     tol = 1e-10 * max(1.0, kappa / 1e4)
     a, b = torch.as_tensor(a_np, device="cuda"), torch.as_tensor(b_np, device="cuda")
+    floor = _floor(("c4", n), lambda x, y: _gpu_c4(x, y, iters), a, b, n)
     gpu = []
-    for p, t, ctr in _gpu_c4(a, b, iters):
-        gpu.append((p.clone(), t.clone()))
-    gpu_ctr = (ctr.mmm, ctr.mvm)
-    perm = np.random.default_rng(17).permutation(n)
-    pt = torch.as_tensor(perm, device="cuda")
-    floor = 0.0
-    for k, (p, t, _) in enumerate(_gpu_c4(_perm_sym(a, pt), b[pt], iters)):
-        floor = max(floor, _rel_t(_unperm_sym(p, perm), gpu[k][0]),
-                    _rel_t(_unperm_rows(t, perm), gpu[k][1]))
-    osp = O.split_scalar(a_np, O.inf_norm(a_np) / 2.0)
-    ost = O.initial_series(osp, 0, 1, 2)
-    oth = np.zeros_like(b_np)
+    with P.gemm_backend(backend, moduli=16, min_dim=1024):
+        for p, t, ctr in _gpu_c4(a, b, iters):
+            gpu.append((p.clone(), t.clone()))
     err = 0.0
     for k in range(iters):
-        oth = O.plain_richardson(oth, ost.estimate, osp.matrix, b_np, ost.ctr)
-        ost = O.composite_step(ost, osp.matrix, osp, (2, 3, 4, 5), 2)
-        ep = _rel_np(gpu[k][0].cpu().numpy(), ost.estimate)
-        et = _rel_np(gpu[k][1].cpu().numpy(), oth)
+        ep = _rel_np(gpu[k][0].cpu().numpy(), seq[k][0])
+        et = _rel_np(gpu[k][1].cpu().numpy(), seq[k][1])
         err = max(err, ep, et)
         assert ep <= tol and et <= tol, (k, ep, et, tol)
-    assert gpu_ctr == (ost.ctr.mmm, ost.ctr.mvm) == (880, 80)
-    _log(f"c4 n={n} rhs={rhs} ({iters} iterations): kappa={kappa:.3g} err_vs_oracle={err:.3e} "
-         f"gpu_permutation_floor={floor:.3e} tol={tol:.1e}")
+    assert (ctr.mmm, ctr.mvm) == octr == (880, 80)
+    _log(f"c4 n={n} rhs={rhs} ({iters} iterations, {backend}): kappa={kappa:.3g} "
+         f"err_vs_oracle={err:.3e} dmma_permutation_floor={floor:.3e} tol={tol:.1e}")
     assert err <= max(FACTOR * floor, 64 * np.finfo(np.float64).eps)
 
 
@@ -196,10 +240,13 @@ def _gpu_c5(a, b, iters, kw):
         yield st.inner.estimate, st.theta, st.ctr.mmm - c0, st.ctr
 
 
-@pytest.mark.parametrize("variant", ["reference-horner", "factorised-16"])
-def test_c5_recipe_n4096_20_iterations(variant):
+@pytest.mark.parametrize("variant,backend", [("reference-horner", "dmma"),
+                                             ("factorised-16", "dmma"),
+                                             ("factorised-16", "ozaki")])
+def test_c5_recipe_n4096_20_iterations(variant, backend):
     """Config 5 recipe at n=4096 (256 RHS), the full 20 iterations, both DAGs vs the
-    oracle's Horner DAG at every iteration."""
+    oracle's Horner DAG at every iteration; the bench's factorised DAG also with
+    every n x n product emulated on the INT8 tensor cores (bench.py --gemm ozaki)."""
     import paper_2008_11480_b200 as P
 
     n, rhs, iters = 4096, 256, 20
@@ -208,16 +255,12 @@ def test_c5_recipe_n4096_20_iterations(variant):
     kw = ({"factor_plan": P.plan_order(16), "doubling_sum": True}
           if variant != "reference-horner" else {})
     a, b = torch.as_tensor(a_np, device="cuda"), torch.as_tensor(b_np, device="cuda")
+    floor = _floor(("c5", n, variant), lambda x, y: _gpu_c5(x, y, iters, kw), a, b, n)
     gpu, steps = [], []
-    for p, t, d, ctr in _gpu_c5(a, b, iters, kw):
-        gpu.append((p.clone(), t.clone()))
-        steps.append(d)
-    perm = np.random.default_rng(17).permutation(n)
-    pt = torch.as_tensor(perm, device="cuda")
-    floor = 0.0
-    for k, (p, t, _, _) in enumerate(_gpu_c5(_perm_sym(a, pt), b[pt], iters, kw)):
-        floor = max(floor, _rel_t(_unperm_sym(p, perm), gpu[k][0]),
-                    _rel_t(_unperm_rows(t, perm), gpu[k][1]))
+    with P.gemm_backend(backend, moduli=16, min_dim=1024):
+        for p, t, d, ctr in _gpu_c5(a, b, iters, kw):
+            gpu.append((p.clone(), t.clone()))
+            steps.append(d)
     err = 0.0
     for k in range(iters):
         ep = _rel_np(gpu[k][0].cpu().numpy(), seq[k][0])
@@ -229,7 +272,7 @@ def test_c5_recipe_n4096_20_iterations(variant):
         assert (ctr.mmm, ctr.mvm) == octr
     else:
         assert steps[0] == 16 + 18 and all(s == 18 for s in steps[1:])
-    _log(f"c5 n={n} rhs={rhs} ({iters} iterations, {variant}): kappa={kappa:.3g} "
-         f"err_vs_oracle={err:.3e} gpu_permutation_floor={floor:.3e} tol={tol:.1e}")
-    if variant == "reference-horner":
+    _log(f"c5 n={n} rhs={rhs} ({iters} iterations, {variant}, {backend}): kappa={kappa:.3g} "
+         f"err_vs_oracle={err:.3e} dmma_permutation_floor={floor:.3e} tol={tol:.1e}")
+    if variant == "reference-horner" or backend == "ozaki":
         assert err <= max(FACTOR * floor, 64 * np.finfo(np.float64).eps)

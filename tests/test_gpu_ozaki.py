@@ -49,17 +49,26 @@ def _dmma(a, b):
         return P.mat_mul(a, b, P.MulCounter())
 
 
+@pytest.mark.parametrize("kernel", ["pair", "single"])
 @pytest.mark.parametrize("planes,m,n,kp", [(1, 128, 256, 128), (3, 300, 520, 256),
                                            (2, 1000, 777, 1024), (16, 513, 300, 2048),
-                                           (5, 129, 1000, 4096)])
-def test_int8_kernel_exact(planes, m, n, kp):
+                                           (5, 129, 1000, 4096), (2, 1, 1, 128),
+                                           (3, 1200, 257, 384)])
+def test_int8_kernel_exact(planes, m, n, kp, kernel):
+    """Both INT8 kernels (CTA pairs / single CTAs) reproduce the exact integer
+    products mod m_l, ragged tiles (rows / columns past the 256 x 256 pair tile
+    or the 128 x 256 tile, one-row / one-column products) included."""
     import paper_2008_11480_b200 as P
 
     mods = P.ozaki_moduli(16)
     g = torch.Generator(device="cuda").manual_seed(planes * 1000 + m)
     a = torch.randint(-128, 128, (planes, m, kp), dtype=torch.int8, device="cuda", generator=g)
     bt = torch.randint(-128, 128, (planes, n, kp), dtype=torch.int8, device="cuda", generator=g)
-    r = P.i8_gemm_mod(a, bt)
+    P.set_ozaki_kernel(kernel)
+    try:
+        r = P.i8_gemm_mod(a, bt)
+    finally:
+        P.set_ozaki_kernel("auto")
     for l in range(planes):
         # |sum| <= kp * 2^14 < 2^53: the FP64 product of these integers is exact
         ref = torch.remainder(a[l].double() @ bt[l].double().T, mods[l]).to(torch.uint8)
@@ -74,10 +83,34 @@ def test_int8_kernel_extreme_residues():
     a = torch.full((4, 256, 8192), -128, dtype=torch.int8, device="cuda")
     bt = torch.full((4, 256, 8192), -128, dtype=torch.int8, device="cuda")
     bt[:, ::2] = 127
-    r = P.i8_gemm_mod(a, bt)
-    for l in range(4):
-        ref = torch.remainder(a[l].double() @ bt[l].double().T, mods[l]).to(torch.uint8)
-        assert torch.equal(ref, r[l])
+    for kernel in ("pair", "single"):
+        P.set_ozaki_kernel(kernel)
+        try:
+            r = P.i8_gemm_mod(a, bt)
+        finally:
+            P.set_ozaki_kernel("auto")
+        for l in range(4):
+            ref = torch.remainder(a[l].double() @ bt[l].double().T, mods[l]).to(torch.uint8)
+            assert torch.equal(ref, r[l])
+
+
+def test_kernels_bitwise_on_emulated_products():
+    """The emulated FP64 product is the same bits with either INT8 kernel."""
+    import paper_2008_11480_b200 as P
+
+    rng = np.random.default_rng(31)
+    a = torch.from_numpy(rng.standard_normal((1500, 1300))).cuda()
+    b = torch.from_numpy(rng.standard_normal((1300, 1700))).cuda()
+    outs = []
+    for kernel in ("pair", "single"):
+        P.set_ozaki_kernel(kernel)
+        try:
+            outs.append(_ozaki(a, b))
+        finally:
+            P.set_ozaki_kernel("auto")
+    assert torch.equal(outs[0], outs[1])
+    with pytest.raises(ValueError):
+        P.set_ozaki_kernel("quad")
 
 
 def _cases(rng, n):
@@ -259,3 +292,39 @@ def test_c4_recipe_emulated_vs_oracle():
         et = np.linalg.norm(theta.cpu().numpy() - oth) / np.linalg.norm(oth)
         assert ep <= tol and et <= tol, (k, ep, et)
     assert (st.ctr.mmm, st.ctr.mvm) == (ost.ctr.mmm, ost.ctr.mvm)
+
+
+def test_chunks_bitwise():
+    """Chunking D (bounded workspace, si_set_ozaki_chunks) changes nothing: every
+    row's and column's scale and residues are its own; the epilogue's C and the
+    shifted diagonal follow the chunk offsets; B-side planes are rebuilt per row
+    chunk when several column chunks are needed."""
+    import ctypes
+
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import _lib
+
+    rng = np.random.default_rng(21)
+    m, k, n, doff = 1300, 1100, 1300, 37
+    a_np, b_np, c_np = (rng.standard_normal(s) for s in ((m, k), (k, n), (m, n)))
+    a, b, c = (torch.from_numpy(x).cuda() for x in (a_np, b_np, c_np))
+    P.set_gemm_backend("ozaki", 16, 128)
+    outs = []
+    try:
+        for rows, cols in ((0, 0), (0, 256), (0, 768), (512, 0), (256, 512), (768, 256)):
+            P.set_ozaki_chunks(rows, cols)
+            d = torch.empty(m, n, dtype=torch.float64, device="cuda")
+            ctr = (ctypes.c_int64 * 2)()
+            _lib.call("si_gemm_ex", _lib.handle(), m, n, k, -1.0, a.data_ptr(), k, b.data_ptr(), n,
+                      1.0, c.data_ptr(), n, 3.0, doff, d.data_ptr(), n, 0, ctr, _lib.stream_ptr())
+            outs.append(d)
+    finally:
+        P.set_ozaki_chunks(0, 0)
+    for d in outs[1:]:
+        assert torch.equal(d, outs[0])
+    ref = -(a_np.astype(np.longdouble) @ b_np) + c_np
+    idx = np.arange(m - doff)
+    ref[idx, idx + doff] += 3.0
+    assert np.abs(outs[0].cpu().numpy() - ref).max() <= 1e-13 * np.abs(ref).max()
+    with pytest.raises(ValueError):
+        P.set_ozaki_chunks(-1, 0)
