@@ -188,6 +188,48 @@ def resident_roofline(w, tflops_per_gpu: float, step_s: float, peak: float) -> d
             "peak_source": "measured live: DMMA m8n8k4 register-only probe (si_dmma_peak)"}
 
 
+def dmma_side_run(w, args, h, flops: float, peak: float) -> dict:
+    """The same workload with every product on FP64 DMMA (the library default),
+    timed right after the emulated run in the same process: a few steps, CUDA
+    events, clocks sampled -- the FP64-tensor-core reference point of the line."""
+    import ctypes
+
+    import torch
+
+    from paper_2008_11480_b200 import _lib
+
+    k = max(1, min(args.steps, 3))
+    with w.P.gemm_backend("dmma"):
+        w.step()  # warm (kernels, workspace)
+        torch.cuda.synchronize()
+        sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+        sampler.start()
+        _lib.call("si_profile_begin", h)
+        stream = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            w.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        g_ms, g_fl = ctypes.c_double(), ctypes.c_double()
+        g_n, launches = ctypes.c_int64(), ctypes.c_int64()
+        _lib.call("si_profile_end", h, ctypes.byref(g_ms), ctypes.byref(g_fl), ctypes.byref(g_n),
+                  ctypes.byref(launches))
+        clocks = sampler.stop()
+    step_s = e0.elapsed_time(e1) / 1e3 / k
+    ach = g_fl.value / (g_ms.value / 1e3) / 1e12 if g_ms.value > 0 else None
+    return {"what": "same workload, every product on FP64 DMMA (gemm_f64_tma_kernel), timed after "
+                    "the emulated run in this process",
+            "value": w.iters_per_step / step_s, "unit": "iters/s", "steps": k,
+            "ms_per_step": step_s * 1e3, "tflops": flops / step_s / 1e12,
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                         "frac": ach / peak if ach else None, "kernel": "gemm_f64_tma_kernel",
+                         "launches": g_n.value,
+                         "peak_source": "measured live: DMMA register-only probe (si_dmma_peak)"},
+            "clocks": clocks}
+
+
 def int8_peak_tops() -> tuple[float, str]:
     """Measured INT8 tensor-core yardstick: cuBLASLt int8 GEMM 8192^3
     (torch._int_mm, int8 x int8 -> int32), best of 10 launches (burst, like
@@ -210,16 +252,16 @@ def int8_peak_tops() -> tuple[float, str]:
         best = min(best, e0.elapsed_time(e1))
     del a, b
     return 2.0 * n**3 / (best * 1e-3) / 1e12, (
-        "measured live: cuBLASLt int8 GEMM 8192^3 (torch._int_mm), best of 10; "
-        "MEASURED_PEAKS.json has no INT8 entry (nominal dense INT8: 4500 TOPS)")
+        "measured live before the timed region: cuBLASLt int8 GEMM 8192^3 (torch._int_mm), "
+        "best of 10 (burst); MEASURED_PEAKS.json has no INT8 entry (nominal dense INT8: 4500 TOPS)")
 
 
 def ozaki_roofline(w, i8_ms: float, i8_ops: float, i8_launches: int, fp64_achieved, fp64_launches,
-                   dmma_peak: float, moduli: int) -> dict:
+                   dmma_peak: float, moduli: int, i8_peak: tuple) -> dict:
     """Roofline of the Ozaki-II products: the dominant kernel is the INT8
     tcgen05 GEMM (i8_gemm_mod_kernel); achieved = its algorithmic int8 ops
     (2 M N Kp per modulus plane) / its CUDA-event time on the launching stream."""
-    peak, src = int8_peak_tops()
+    peak, src = i8_peak
     ach = i8_ops / (i8_ms * 1e-3) / 1e12 if i8_ms > 0 else None
     traffic = None
     try:
@@ -230,7 +272,8 @@ def ozaki_roofline(w, i8_ms: float, i8_ops: float, i8_launches: int, fp64_achiev
         pass
     return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOPS (int8)",
             "frac": ach / peak if ach else None, "traffic": traffic,
-            "kernel": "i8_gemm_mod_kernel", "launches": i8_launches, "moduli": moduli,
+            "kernel": ("i8_gemm_mod_kernel" if getattr(w, "i8_kernel", "auto") == "single"
+                       else "i8_gemm_mod_pair_kernel"), "launches": i8_launches, "moduli": moduli,
             "peak_source": src,
             "fp64_equivalent": {
                 "what": "whole emulated products (scaling, residues, INT8 GEMM, CRT + epilogue): "
@@ -322,6 +365,7 @@ class Workload:
         self.native = None
         self.split_batch = False
         self.iters_per_step = 1
+        self.executor = None  # composite parts on concurrent streams (--streams)
 
     # FLOPs of the executed reference DAG per step (2 M N K summed)
     def flops(self) -> float:
@@ -594,7 +638,7 @@ class Workload:
         self.theta = P.plain_richardson(self.theta, self.st.estimate, self.sp.matrix, self.b, self.st.ctr)
         if cfg == "c4":
             self.st = P.composite_step(self.st, self.sp.matrix, self.sp, self.spec, 2,
-                                       parts=self.parts)
+                                       executor=self.executor, parts=self.parts)
         elif cfg == "c3":
             self.st = P.ns_step(self.st, self.sp.matrix, plan=self.plan8)
         else:
@@ -684,7 +728,7 @@ class Workload:
         if self.cfg == "c4":
             sp = P.Splitting(precond=d["precond"], residual=d["residual"], matrix=d["a"],
                              kind="scalar", verify=False)
-            new = P.composite_step(st, sp.matrix, sp, self.spec, 2,
+            new = P.composite_step(st, sp.matrix, sp, self.spec, 2, executor=self.executor,
                                    input_panels=(flags, epoch, npanels), residual_chunks=chunks,
                                    estimate_done=g_done)
         else:
@@ -1276,10 +1320,22 @@ def run_ours(args):
     w.setup()
     flops = w.flops()
     h = _lib.handle()
-    ozaki = args.gemm == "ozaki" and w.cfg in ("c3", "c4", "c5")
+    if args.streams and w.cfg == "c4":
+        w.executor = "streams"  # any non-None executor: parts on the library's side streams
+    ozaki = (args.gemm == "ozaki" and w.cfg in ("c3", "c4", "c5")) or (
+        args.gemm == "auto" and w.cfg in ("c3", "c4"))
     if ozaki:
         # after setup (the PD check / verification products stay on DMMA)
         w.P.set_gemm_backend("ozaki", moduli=args.moduli, min_dim=1024)
+        w.P.set_ozaki_kernel(args.i8_kernel)
+        w.i8_kernel = args.i8_kernel
+    # roofline denominators, probed before any timed work (a GPU held at its
+    # power cap by a long INT8 run reads far lower)
+    import ctypes
+
+    peak = ctypes.c_double()
+    _lib.call("si_dmma_peak", h, 20000, ctypes.byref(peak))
+    i8_peak = int8_peak_tops() if ozaki else None
     for _ in range(args.warmup):
         w.step()
     torch.cuda.synchronize()
@@ -1320,10 +1376,11 @@ def run_ours(args):
     value = (1 if strong else world) * args.steps * w.iters_per_step / (ms_max / 1e3)
     tflops = (1 if strong else world) * flops / step_s / 1e12
 
-    peak = ctypes.c_double()
-    _lib.call("si_dmma_peak", h, 20000, ctypes.byref(peak))
     achieved = (g_fl.value / (g_ms.value / 1e3) / 1e12) if g_ms.value > 0 else None
 
+    fp64_dmma = None
+    if ozaki and world == 1 and not args.no_dmma_side:
+        fp64_dmma = dmma_side_run(w, args, h, flops, peak.value)
     e2e = None
     if w.sharded is not None and w.sharded.get("native"):
         e2e = {"unavailable": "--comm native: e2e is measured on the peer / nccl paths"}
@@ -1399,6 +1456,7 @@ def run_ours(args):
             "dtype": (f"int8 tensor cores -> f64 (Ozaki-II FP64 emulation, {args.moduli} moduli)"
                       if ozaki else "f64"),
             "gemm_backend": "ozaki" if ozaki else "dmma",
+            "parts_on_streams": w.executor is not None,
             "data": "synthetic (seeded PCG64 draws, SURVEY Appendix A recipe)",
             "config": config_of(w),
             "parallelism": layout_note(w) + (f"composite parts on GPU groups x{world} (NCCL p2p tree)"
@@ -1412,12 +1470,13 @@ def run_ours(args):
             "tflops_frac_of_dmma_peak": tflops / (world * peak.value),
             "roofline": resident_roofline(w, tflops / world, step_s, peak.value) if w.cfg in ("c1", "c2") else
                         ozaki_roofline(w, i8_ms.value, i8_ops.value, i8_n.value, achieved, g_n.value,
-                                       peak.value, args.moduli) if ozaki else
+                                       peak.value, args.moduli, i8_peak) if ozaki else
                         {"bound": "tensor", "achieved": achieved, "peak": peak.value,
                          "unit": "TFLOP/s", "frac": (achieved / peak.value) if achieved else None,
                          "traffic": ncu_traffic(w), "kernel": "gemm_f64_tma_kernel",
                          "launches": g_n.value,
-                         "peak_source": "measured live: DMMA m8n8k4 register-only probe (si_dmma_peak); MEASURED_PEAKS.json has no FP64 entry"},
+                         "peak_source": "measured live before the timed region: DMMA m8n8k4 register-only probe (si_dmma_peak); MEASURED_PEAKS.json has no FP64 entry"},
+            "fp64_dmma": fp64_dmma,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches.value,
@@ -1452,11 +1511,20 @@ def main():
     ap.add_argument("--shard", choices=["rows", "parts"], default="rows",
                     help="c4 at N > 1: block-row sharding of every product (rows) or the "
                          "composite parts on GPU groups + one tree reduction (parts)")
-    ap.add_argument("--gemm", choices=["dmma", "ozaki"], default="dmma",
-                    help="FP64 product backend of the dense configs (c3/c4/c5): FP64 DMMA, "
-                         "or Ozaki-II emulation on the INT8 tensor cores (si_set_gemm_backend)")
+    ap.add_argument("--gemm", choices=["auto", "dmma", "ozaki"], default="auto",
+                    help="FP64 product backend of the dense configs: FP64 DMMA, or Ozaki-II "
+                         "emulation on the INT8 tensor cores (si_set_gemm_backend); auto = "
+                         "ozaki for c3/c4, dmma for c5 (its n=32768 state leaves no room for "
+                         "the emulation's workspace on one GPU)")
     ap.add_argument("--moduli", type=int, default=16,
                     help="--gemm ozaki: number of moduli (16 = at least DGEMM's accuracy)")
+    ap.add_argument("--i8-kernel", choices=["auto", "pair", "single"], default="auto",
+                    help="--gemm ozaki: INT8 tensor-core kernel (CTA pairs or single CTAs)")
+    ap.add_argument("--no-dmma-side", action="store_true",
+                    help="--gemm ozaki: skip the FP64 DMMA reference point timed after the run")
+    ap.add_argument("--streams", action="store_true",
+                    help="c4: evaluate the composite parts on concurrent CUDA streams (the "
+                         "paper's simultaneously evaluated parts, on one GPU; bitwise equal)")
     ap.add_argument("--ref-budget", type=float, default=300.0,
                     help="--impl reference, c4/c5: wall-clock budget (s) for the executed "
                          "full-size CPU steps (at least one is always executed)")

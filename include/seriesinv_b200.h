@@ -452,6 +452,10 @@ SI_API int si_set_ozaki_chunks(si_handle h, int64_t max_rows, int64_t max_cols);
  * 1 = CTA pairs (tcgen05.mma.cta_group::2, 256 x 256 tiles), 2 = single CTAs
  * (cta_group::1, 128 x 256 tiles).  Results are identical (exact integers). */
 SI_API int si_set_ozaki_kernel(si_handle h, int variant);
+/* Tuning hook of the CTA-pair INT8 kernel (process-wide; measurement tools):
+ * rasterisation group in 256-row pair tiles (0 keeps), L2 policy of the A /
+ * B operand loads (0 evict_normal, 1 evict_last, 2 evict_first; -1 keeps). */
+SI_API int si_ozaki_tune(int group_m, int l2_a, int l2_b);
 /* The first n moduli of the emulation. */
 SI_API int si_ozaki_moduli(int n, uint32_t* moduli);
 /* The INT8 tensor-core kernel alone (test hook): r[l] = (a[l] @ bt[l]^T) mod

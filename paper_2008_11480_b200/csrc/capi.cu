@@ -1239,6 +1239,13 @@ int si_set_ozaki_kernel(si_handle h, int variant) {
   });
 }
 
+int si_ozaki_tune(int group_m, int l2_a, int l2_b) {
+  return guard([&] {
+    need(group_m >= 0 && l2_a >= -1 && l2_a <= 2 && l2_b >= -1 && l2_b <= 2, "bad tuning values");
+    oz::tune_pair(group_m, l2_a, l2_b);
+  });
+}
+
 int si_ozaki_moduli(int n, uint32_t* moduli) {
   return guard([&] {
     need(moduli != nullptr && n >= 1 && n <= oz::kMaxModuli, "bad arguments");

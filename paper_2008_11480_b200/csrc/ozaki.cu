@@ -101,14 +101,25 @@ __device__ __forceinline__ Chunks chunks_of(long long x) {
   const unsigned long long u = (unsigned long long)(x + (1ll << 57));
   return Chunks{(uint32_t)u & 0xFFFFFu, (uint32_t)(u >> 20) & 0xFFFFFu, (uint32_t)(u >> 40)};
 }
+// (x + h) mod m with h = m / 2, i.e. the symmetric residue plus h, in [0, m)
 template <int L>
-__device__ __forceinline__ int res_sym(const Chunks& c) {
+__device__ __forceinline__ uint32_t res_shifted(const Chunks& c) {
   constexpr unsigned m = kmod(L);
   constexpr unsigned r40 = pow2mod(40, m);
   constexpr unsigned r20 = pow2mod(20, m);
-  constexpr unsigned k = m - pow2mod(57, m);
-  const unsigned r = (c.c2 * r40 + c.c1 * r20 + c.c0 + k) % m;
-  return (int)r - (r >= (m + 1) / 2 ? (int)m : 0);
+  constexpr unsigned kh = (m - pow2mod(57, m) + m / 2) % m;
+  return (c.c2 * r40 + c.c1 * r20 + c.c0 + kh) % m;
+}
+
+// four shifted residues r_j in [0, m) -> one word of the int8 values r_j - h
+// (two's complement bytes): byte packing by PRMT, then a carry-free per-byte
+// subtraction of h
+template <int L>
+__device__ __forceinline__ uint32_t pack_sym4(uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  constexpr unsigned h = kmod(L) / 2;
+  const uint32_t w = __byte_perm(__byte_perm(r0, r1, 0x0040), __byte_perm(r2, r3, 0x0040), 0x5410);
+  constexpr uint32_t H = (uint32_t)((256u - h) & 0xFFu) * 0x01010101u;  // + (256 - h) per byte
+  return ((w & 0x7F7F7F7Fu) + (H & 0x7F7F7F7Fu)) ^ ((w ^ H) & 0x80808080u);
 }
 
 // integer image rint(a * 2^sh) of a (sh not the sentinel)
@@ -120,10 +131,6 @@ __device__ __forceinline__ long long int_image(double a, int sh) {
   return __double2ll_rn(a * pow2(sh));
 }
 
-__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
-  return (uint32_t)(a & 0xff) | ((uint32_t)(b & 0xff) << 8) | ((uint32_t)(c & 0xff) << 16) |
-         ((uint32_t)(d & 0xff) << 24);
-}
 
 // ------------------------------------------------------------- scaling --
 // max |a_ij| over each row (as the bit pattern of |a|: ordered like the value,
@@ -180,14 +187,14 @@ template <int L>
 __device__ __forceinline__ void emit16(int nmod, const Chunks (&x)[16], int8_t* dst, int64_t plane) {
   if constexpr (L < kMaxModuli) {
     if (L >= nmod) return;
-    int r[16];
+    uint32_t r[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) r[j] = res_sym<L>(x[j]);
+    for (int j = 0; j < 16; ++j) r[j] = res_shifted<L>(x[j]);
     uint4 w;
-    w.x = pack4(r[0], r[1], r[2], r[3]);
-    w.y = pack4(r[4], r[5], r[6], r[7]);
-    w.z = pack4(r[8], r[9], r[10], r[11]);
-    w.w = pack4(r[12], r[13], r[14], r[15]);
+    w.x = pack_sym4<L>(r[0], r[1], r[2], r[3]);
+    w.y = pack_sym4<L>(r[4], r[5], r[6], r[7]);
+    w.z = pack_sym4<L>(r[8], r[9], r[10], r[11]);
+    w.w = pack_sym4<L>(r[12], r[13], r[14], r[15]);
     *reinterpret_cast<uint4*>(dst + L * plane) = w;
     emit16<L + 1>(nmod, x, dst, plane);
   }
@@ -353,14 +360,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int& plane, int& tm, int& tn) {
+__device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int& plane, int& tm, int& tn,
+                                        int group_m = GROUP_M) {
   const int per_plane = num_m * num_n;
   plane = t / per_plane;
   const int r = t - plane * per_plane;
-  const int per_group = GROUP_M * num_n;
+  const int per_group = group_m * num_n;
   const int group = r / per_group;
-  const int first_m = group * GROUP_M;
-  const int gsize = min(num_m - first_m, GROUP_M);
+  const int first_m = group * group_m;
+  const int gsize = min(num_m - first_m, group_m);
   const int q = r - group * per_group;
   tm = first_m + q % gsize;
   tn = q / gsize;
@@ -563,12 +571,23 @@ __device__ __forceinline__ void cluster_sync() {
                    "memory");
 }
 __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
-                                                 int c0, int c1, int c2) {
+                                                 int c0, int c1, int c2, uint64_t policy) {
   asm volatile(
       "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
       : "memory");
+}
+// L2 policies of the operand loads: 0 evict_normal, 1 evict_last, 2 evict_first
+__device__ __forceinline__ uint64_t l2_policy(int kind) {
+  uint64_t p;
+  if (kind == 1)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else if (kind == 2)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                             uint32_t accumulate) {
@@ -593,7 +612,8 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar) {
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GTHREADS, 1)
     i8_gemm_mod_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                             const __grid_constant__ CUtensorMap tmB, uint8_t* __restrict__ R,
-                            int M, int N, int Kp, int nplanes, const __grid_constant__ ModTab mt) {
+                            int M, int N, int Kp, int nplanes, const __grid_constant__ ModTab mt,
+                            int group_m, int l2a, int l2b) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -642,11 +662,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GTHREADS, 1)
       // ---------------- TMA producer (both CTAs: own A rows, own half of Bt) ----
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      const uint64_t pol_a = l2_policy(l2a), pol_b = l2_policy(l2b);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cid; t < total; t += nclusters) {
         int plane, tm, tn;
-        tile_of(t, num_m, num_n, plane, tm, tn);
+        tile_of(t, num_m, num_n, plane, tm, tn, group_m);
         const int arow = tm * PBM + (int)rank * (PBM / 2);
         const int brow = tn * PBN + (int)rank * (PBN / 2);
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -654,8 +675,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GTHREADS, 1)
           const uint32_t sa = base + stage * PSTAGE_BYTES;
           const uint32_t fb = leader_addr(full_bar(stage));
           if (rank == 0) mbar_expect_tx(full_bar(stage), 2 * PSTAGE_BYTES);
-          tma_load_3d_pair(sa, &tmA, fb, kb * GBK, arow, plane);
-          tma_load_3d_pair(sa + PA_BYTES, &tmB, fb, kb * GBK, brow, plane);
+          tma_load_3d_pair(sa, &tmA, fb, kb * GBK, arow, plane, pol_a);
+          tma_load_3d_pair(sa + PA_BYTES, &tmB, fb, kb * GBK, brow, plane, pol_b);
           if (++stage == PSTAGES) {
             stage = 0;
             phase ^= 1u;
@@ -702,7 +723,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GTHREADS, 1)
     uint32_t aphase = 0;
     for (int t = cid; t < total; t += nclusters) {
       int plane, tm, tn;
-      tile_of(t, num_m, num_n, plane, tm, tn);
+      tile_of(t, num_m, num_n, plane, tm, tn, group_m);
       const unsigned m = mt.m[plane], magic = mt.magic[plane], off = mt.off[plane];
       mbar_wait(tfull_bar(acc), aphase);
       tc_fence_after();
@@ -769,29 +790,48 @@ struct CrtTab {
   int nmod;
 };
 
+// alpha * acc + beta * c with one rounding for the sum (alpha = +-1, beta = 1:
+// the exactly rounded acc +- c)
 __device__ __forceinline__ double apply_epi(double acc, double alpha, double beta, double cval) {
-  double v = (alpha == 1.0) ? acc : (alpha == -1.0 ? -acc : __dmul_rn(alpha, acc));
-  if (beta != 0.0) v = __dadd_rn(v, beta == 1.0 ? cval : __dmul_rn(beta, cval));
-  return v;
+  const double v = __dmul_rn(alpha, acc);
+  return beta != 0.0 ? __fma_rn(beta, cval, v) : v;
 }
 
-__device__ __forceinline__ double crt_value(const uint32_t (&w)[kMaxModuli], int j, const CrtTab& t) {
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+// byte j of w as a double: the bits of 2^52 + byte, minus 2^52 (one DADD on the
+// FP64 pipe instead of an I2F conversion)
+__device__ __forceinline__ double byte_f64(uint32_t w, int j) {
+  return __hiloint2double(0x43300000, (int)((w >> (8 * j)) & 0xFFu)) - 0x1p52;
+}
+
+// the CRT sums of the 4 entries packed in w[l] (byte j = entry j), planes
+// outermost so each CRT constant is loaded once per 4 entries
+template <int NMOD>
+__device__ __forceinline__ void crt_values4(const uint32_t (&w)[NMOD], const CrtTab& t,
+                                            double (&out)[4]) {
+  double sum[4][4];
 #pragma unroll
-  for (int l = 0; l < kMaxModuli; ++l) {
-    if (l < t.nmod) {
-      const double cl = (double)((w[l] >> (8 * j)) & 0xFFu);
-      s0 = fma(cl, t.w[l][0], s0);
-      s1 = fma(cl, t.w[l][1], s1);
-      s2 = fma(cl, t.w[l][2], s2);
-      s3 = fma(cl, t.w[l][3], s3);
+  for (int j = 0; j < 4; ++j) sum[j][0] = sum[j][1] = sum[j][2] = sum[j][3] = 0.0;
+#pragma unroll
+  for (int l = 0; l < NMOD; ++l) {
+    const double w0 = t.w[l][0], w1 = t.w[l][1], w2 = t.w[l][2], w3 = t.w[l][3];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double cl = byte_f64(w[l], j);
+      sum[j][0] = fma(cl, w0, sum[j][0]);
+      sum[j][1] = fma(cl, w1, sum[j][1]);
+      sum[j][2] = fma(cl, w2, sum[j][2]);
+      sum[j][3] = fma(cl, w3, sum[j][3]);
     }
   }
-  const double x = fma(s3, 0x1p96, fma(s2, 0x1p64, s1 * 0x1p32));
-  const double q = rint(x * t.inv_m);
-  const double t3 = fma(-q, t.mp[3], s3), t2 = fma(-q, t.mp[2], s2);
-  const double t1 = fma(-q, t.mp[1], s1), t0 = fma(-q, t.mp[0], s0);
-  return fma(fma(fma(t3, 0x1p32, t2), 0x1p32, t1), 0x1p32, t0);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double s0 = sum[j][0], s1 = sum[j][1], s2 = sum[j][2], s3 = sum[j][3];
+    const double x = fma(s3, 0x1p96, fma(s2, 0x1p64, s1 * 0x1p32));
+    const double q = rint(x * t.inv_m);
+    const double t3 = fma(-q, t.mp[3], s3), t2 = fma(-q, t.mp[2], s2);
+    const double t1 = fma(-q, t.mp[1], s1), t0 = fma(-q, t.mp[0], s0);
+    out[j] = fma(fma(fma(t3, 0x1p32, t2), 0x1p32, t1), 0x1p32, t0);
+  }
 }
 
 // v * 2^e, one rounding
@@ -799,7 +839,9 @@ __device__ __forceinline__ double scale2(double v, int e) {
   return (e >= -1022 && e <= 1023) ? v * pow2(e) : ldexp(v, e);
 }
 
-// one thread per 4 consecutive columns of a row (one 32-bit load per plane)
+// one thread per 4 consecutive columns of a row (one 32-bit load per plane);
+// the moduli count is a template parameter (no per-plane branches)
+template <int NMOD>
 __global__ void __launch_bounds__(256) crt_kernel(
     const uint8_t* __restrict__ R, int M, int N, const unsigned long long* __restrict__ rmax,
     const unsigned long long* __restrict__ cmax, int pa, int pb, const __grid_constant__ CrtTab tab,
@@ -808,6 +850,8 @@ __global__ void __launch_bounds__(256) crt_kernel(
   const int chunks = (N + 3) >> 2;
   const int64_t total = (int64_t)M * chunks;
   const int64_t plane = (int64_t)M * N;
+  const bool vec_cd = ((ldd & 1) == 0) && ((reinterpret_cast<uintptr_t>(D) & 15u) == 0) &&
+                      (beta == 0.0 || (((ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15u) == 0)));
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int row = (int)(idx / chunks);
@@ -815,34 +859,76 @@ __global__ void __launch_bounds__(256) crt_kernel(
     const int sa = shift_of(rmax[row], pa);
     const int64_t off = (int64_t)row * N + j0;
     const bool full = (j0 + 4 <= N) && ((N & 3) == 0);
-    uint32_t w[kMaxModuli];
+    uint32_t w[NMOD];
+    if (full) {
 #pragma unroll
-    for (int l = 0; l < kMaxModuli; ++l) {
-      w[l] = 0u;
-      if (l < tab.nmod) {
-        if (full) {
-          w[l] = __ldcs(reinterpret_cast<const unsigned*>(R + l * plane + off));
-        } else {
-          for (int j = 0; j < 4 && j0 + j < N; ++j) w[l] |= (uint32_t)R[l * plane + off + j] << (8 * j);
-        }
+      for (int l = 0; l < NMOD; ++l) w[l] = __ldcs(reinterpret_cast<const unsigned*>(R + l * plane + off));
+    } else {
+#pragma unroll
+      for (int l = 0; l < NMOD; ++l) {
+        w[l] = 0u;
+        for (int j = 0; j < 4 && j0 + j < N; ++j) w[l] |= (uint32_t)R[l * plane + off + j] << (8 * j);
       }
     }
+    double v[4];
+    crt_values4<NMOD>(w, tab, v);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int col = j0 + j;
-      if (col >= N) break;
-      const int sb = shift_of(cmax[col], pb);
-      double v;
-      if (sa == kNonFinite || sb == kNonFinite) {
-        v = __longlong_as_double(0x7FF8000000000000ll);
-      } else {
-        v = scale2(crt_value(w, j, tab), -(sa + sb));
-      }
-      const double cv = beta != 0.0 ? C[(int64_t)row * ldc + col] : 0.0;
-      v = apply_epi(v, alpha, beta, cv);
-      if (diag != 0.0 && (int64_t)row + doff == (int64_t)col) v = __dadd_rn(v, diag);
-      D[(int64_t)row * ldd + col] = v;
+      const int sb = col < N ? shift_of(cmax[col], pb) : 0;
+      v[j] = (sa == kNonFinite || sb == kNonFinite) ? __longlong_as_double(0x7FF8000000000000ll)
+                                                    : scale2(v[j], -(sa + sb));
     }
+    double* drow = D + (int64_t)row * ldd + j0;
+    const double* crow = beta != 0.0 ? C + (int64_t)row * ldc + j0 : nullptr;
+    if (full && vec_cd) {
+      double cv[4] = {0.0, 0.0, 0.0, 0.0};
+      if (crow) {
+        const double2 c01 = *reinterpret_cast<const double2*>(crow);
+        const double2 c23 = *reinterpret_cast<const double2*>(crow + 2);
+        cv[0] = c01.x, cv[1] = c01.y, cv[2] = c23.x, cv[3] = c23.y;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[j] = apply_epi(v[j], alpha, beta, cv[j]);
+        if (diag != 0.0 && (int64_t)row + doff == (int64_t)(j0 + j)) v[j] = __dadd_rn(v[j], diag);
+      }
+      *reinterpret_cast<double2*>(drow) = make_double2(v[0], v[1]);
+      *reinterpret_cast<double2*>(drow + 2) = make_double2(v[2], v[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = j0 + j;
+        if (col >= N) break;
+        double x = apply_epi(v[j], alpha, beta, crow ? crow[j] : 0.0);
+        if (diag != 0.0 && (int64_t)row + doff == (int64_t)col) x = __dadd_rn(x, diag);
+        drow[j] = x;
+      }
+    }
+  }
+}
+
+template <int NMOD>
+void launch_crt_n(int blocks, cudaStream_t s, const uint8_t* R, int M, int N,
+                  const unsigned long long* rmax, const unsigned long long* cmax, int pa, int pb,
+                  const CrtTab& tab, double* D, int64_t ldd, const double* C, int64_t ldc,
+                  double alpha, double beta, double diag, int64_t doff) {
+  crt_kernel<NMOD><<<blocks, 256, 0, s>>>(R, M, N, rmax, cmax, pa, pb, tab, D, ldd, C, ldc, alpha,
+                                          beta, diag, doff);
+}
+
+template <int NMOD = kMinModuli>
+void launch_crt(int nmod, int blocks, cudaStream_t s, const uint8_t* R, int M, int N,
+                const unsigned long long* rmax, const unsigned long long* cmax, int pa, int pb,
+                const CrtTab& tab, double* D, int64_t ldd, const double* C, int64_t ldc,
+                double alpha, double beta, double diag, int64_t doff) {
+  if constexpr (NMOD <= kMaxModuli) {
+    if (nmod == NMOD)
+      launch_crt_n<NMOD>(blocks, s, R, M, N, rmax, cmax, pa, pb, tab, D, ldd, C, ldc, alpha, beta,
+                         diag, doff);
+    else
+      launch_crt<NMOD + 1>(nmod, blocks, s, R, M, N, rmax, cmax, pa, pb, tab, D, ldd, C, ldc,
+                           alpha, beta, diag, doff);
   }
 }
 
@@ -925,6 +1011,9 @@ const Consts& consts() {
   return c;
 }
 
+// rasterisation group and L2 policies of the pair kernel (tuning hook: si_ozaki_tune)
+int g_pair_group_m = GROUP_M, g_pair_l2a = 0, g_pair_l2b = 0;
+
 int num_sms() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -952,6 +1041,12 @@ inline int64_t kpad(int64_t K) { return (K + GBK - 1) / GBK * GBK; }
 }  // namespace
 
 unsigned modulus(int l) { return kmod(l); }
+
+void tune_pair(int group_m, int l2a, int l2b) {
+  if (group_m > 0) g_pair_group_m = group_m;
+  if (l2a >= 0 && l2a <= 2) g_pair_l2a = l2a;
+  if (l2b >= 0 && l2b <= 2) g_pair_l2b = l2b;
+}
 
 namespace {
 // columns of D per chunk: B-side planes (nmod x Nc x Kp) + result planes
@@ -1002,7 +1097,8 @@ cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, in
     const int64_t tiles = ((M + PBM - 1) / PBM) * ((N + PBN - 1) / PBN) * nplanes;
     const int grid = (int)std::min<int64_t>(2 * tiles, sms & ~1);
     i8_gemm_mod_pair_kernel<<<grid, GTHREADS, PSMEM, s>>>(ta, tb, R, (int)M, (int)N, (int)Kp,
-                                                          nplanes, consts().mt);
+                                                          nplanes, consts().mt, g_pair_group_m,
+                                                          g_pair_l2a, g_pair_l2b);
   } else {
     const int64_t tiles = ((M + GBM - 1) / GBM) * ((N + GBN - 1) / GBN) * nplanes;
     const int grid = (int)(tiles < sms ? tiles : sms);
@@ -1076,10 +1172,9 @@ cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, i
       ++n;
       const int64_t thr = mc * ((nc + 3) / 4);
       const int blocks = (int)std::min<int64_t>((thr + 255) / 256, 64 * sms);
-      crt_kernel<<<blocks, 256, 0, s>>>(
-          res, (int)mc, (int)nc, rmax, cmax, pa, pb, cs.crt[nmod], D.p + i0 * D.ld + j0, D.ld,
-          e.beta != 0.0 ? e.c + i0 * e.ldc + j0 : nullptr, e.ldc, e.alpha, e.beta, e.diag,
-          e.doff + i0 - j0);
+      launch_crt(nmod, blocks, s, res, (int)mc, (int)nc, rmax, cmax, pa, pb, cs.crt[nmod],
+                 D.p + i0 * D.ld + j0, D.ld, e.beta != 0.0 ? e.c + i0 * e.ldc + j0 : nullptr,
+                 e.ldc, e.alpha, e.beta, e.diag, e.doff + i0 - j0);
       ++n;
     }
   }

@@ -60,6 +60,11 @@ cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, i
 cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, int64_t M, int64_t N,
                                int64_t Kp, int nplanes, cudaStream_t s, int variant = kI8Auto);
 
+// Tuning hook of the CTA-pair INT8 kernel (process-wide): rasterisation group
+// (pair-tile rows per group) and the L2 policies of the A / B operand loads
+// (0 evict_normal, 1 evict_last, 2 evict_first); negative / zero keeps a value.
+void tune_pair(int group_m, int l2a, int l2b);
+
 // Moduli (pairwise coprime, <= 256) in the order the planes use them.
 unsigned modulus(int l);
 

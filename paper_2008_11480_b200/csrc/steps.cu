@@ -1,6 +1,7 @@
 // Step bodies of newton_schulz.py and richardson.py on the native engine.
 // Outputs are caller-owned device buffers; inputs are never written (the
 // reference's purity contract: states are immutable, matrix_core.py:52).
+#include <functional>
 #include "steps.hpp"
 
 namespace si {
@@ -273,12 +274,16 @@ void richardson_recursive_step(Ctx& c, const MV& A, const MV& b, const MV& theta
   }
   MV s = doubling_sum ? power_sum_doubling(c, R, n) : power_sum(c, R, n);
   MV nsn;
-  auto estimate = [&](Ctx& cc) {
-    MV diff = lincomb(cc, 0.0, {{1.0, &om_prev}, {-1.0, &ns_prev}}, G.v.rows, G.v.cols);
-    gemm(cc, Gout, s, diff, 1.0, &ns_prev, 1.0);  // S (om - ns) + ns
+  auto estimate_then = [&](Ctx& cc, const std::function<void(Ctx&)>& after_g) {
+    {
+      MV diff = lincomb(cc, 0.0, {{1.0, &om_prev}, {-1.0, &ns_prev}}, G.v.rows, G.v.cols);
+      gemm(cc, Gout, s, diff, 1.0, &ns_prev, 1.0);  // S (om - ns) + ns
+    }
+    if (after_g) after_g(cc);
     residual_into(cc, Fout, Gout, A);
     nsn = factor_plan ? eval_node(cc, *factor_plan, Fout, Gout, A) : horner(cc, Fout, Gout, n);
   };
+  auto estimate = [&](Ctx& cc) { estimate_then(cc, nullptr); };
   auto accel = [&](Ctx& cc) {
     gemm(cc, Lout, s, L);
     residual_into(cc, Rout, Lout, A);
@@ -291,8 +296,16 @@ void richardson_recursive_step(Ctx& c, const MV& A, const MV& b, const MV& theta
     fk.join(c1);
     fk.join(c2);
   } else {
-    estimate(c);
+    // the independent accel half first: S is then last read by G' = S (om - ns)
+    // + ns and released before F' and N' are formed (one n x n matrix less at
+    // the step's peak; the emulated products' workspace needs it at n = 32768)
     accel(c);
+    auto release_s = [&](Ctx&) {
+      s = MV();
+      ns_prev = MV();
+      om_prev = MV();
+    };
+    estimate_then(c, release_s);
   }
   copy_into(c, ns_out, nsn);
   gemm(c, omega_out, Rout, ns_out, 1.0, &Lout, 1.0);              // L' + R' N'

@@ -328,3 +328,29 @@ def test_chunks_bitwise():
     assert np.abs(outs[0].cpu().numpy() - ref).max() <= 1e-13 * np.abs(ref).max()
     with pytest.raises(ValueError):
         P.set_ozaki_chunks(-1, 0)
+
+
+def test_workspace_retry_under_memory_cap():
+    """With the allocator capped below a product's full workspace (3 x 1 GiB of
+    residue / result planes at n=8192), the library retries with smaller row x
+    column chunks instead of failing, and the result is bitwise the uncapped one."""
+    import paper_2008_11480_b200 as P
+
+    n = 8192
+    g = torch.Generator(device="cuda").manual_seed(4)
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    full = _ozaki(a, b)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    total = torch.cuda.get_device_properties(0).total_memory
+    used = torch.cuda.memory_allocated()
+    # room for the output (0.5 GiB) and ~1.5 GiB of workspace, not the 3.2 GiB of one chunk
+    torch.cuda.set_per_process_memory_fraction((used + (2 << 30)) / total)
+    try:
+        capped = _ozaki(a, b)
+        torch.cuda.synchronize()
+    finally:
+        torch.cuda.set_per_process_memory_fraction(1.0)
+        torch.cuda.empty_cache()
+    assert torch.equal(capped, full)
