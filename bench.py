@@ -198,7 +198,7 @@ def dmma_side_run(w, args, h, flops: float, peak: float) -> dict:
 
     from paper_2008_11480_b200 import _lib
 
-    k = max(1, min(args.steps, 3))
+    k = 1 if w.cfg == "c5" else max(1, min(args.steps, 3))  # c5: ~35 s per DMMA step
     with w.P.gemm_backend("dmma"):
         w.step()  # warm (kernels, workspace)
         torch.cuda.synchronize()
@@ -272,8 +272,8 @@ def ozaki_roofline(w, i8_ms: float, i8_ops: float, i8_launches: int, fp64_achiev
         pass
     return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOPS (int8)",
             "frac": ach / peak if ach else None, "traffic": traffic,
-            "kernel": ("i8_gemm_mod_kernel" if getattr(w, "i8_kernel", "auto") == "single"
-                       else "i8_gemm_mod_pair_kernel"), "launches": i8_launches, "moduli": moduli,
+            "kernel": ("i8_gemm_mod_pair_kernel" if getattr(w, "i8_kernel", "auto") == "pair"
+                       else "i8_gemm_mod_kernel"), "launches": i8_launches, "moduli": moduli,
             "peak_source": src,
             "fp64_equivalent": {
                 "what": "whole emulated products (scaling, residues, INT8 GEMM, CRT + epilogue): "
@@ -1322,8 +1322,7 @@ def run_ours(args):
     h = _lib.handle()
     if args.streams and w.cfg == "c4":
         w.executor = "streams"  # any non-None executor: parts on the library's side streams
-    ozaki = (args.gemm == "ozaki" and w.cfg in ("c3", "c4", "c5")) or (
-        args.gemm == "auto" and w.cfg in ("c3", "c4"))
+    ozaki = args.gemm in ("ozaki", "auto") and w.cfg in ("c3", "c4", "c5")
     if ozaki:
         # after setup (the PD check / verification products stay on DMMA)
         w.P.set_gemm_backend("ozaki", moduli=args.moduli, min_dim=1024)
@@ -1512,10 +1511,9 @@ def main():
                     help="c4 at N > 1: block-row sharding of every product (rows) or the "
                          "composite parts on GPU groups + one tree reduction (parts)")
     ap.add_argument("--gemm", choices=["auto", "dmma", "ozaki"], default="auto",
-                    help="FP64 product backend of the dense configs: FP64 DMMA, or Ozaki-II "
-                         "emulation on the INT8 tensor cores (si_set_gemm_backend); auto = "
-                         "ozaki for c3/c4, dmma for c5 (its n=32768 state leaves no room for "
-                         "the emulation's workspace on one GPU)")
+                    help="FP64 product backend of the dense configs c3/c4/c5: FP64 DMMA, or "
+                         "Ozaki-II emulation on the INT8 tensor cores (si_set_gemm_backend); "
+                         "auto = ozaki")
     ap.add_argument("--moduli", type=int, default=16,
                     help="--gemm ozaki: number of moduli (16 = at least DGEMM's accuracy)")
     ap.add_argument("--i8-kernel", choices=["auto", "pair", "single"], default="auto",

@@ -448,13 +448,16 @@ SI_API int si_get_gemm_backend(si_handle h, int* backend, int* nmoduli, int64_t*
  * the allocator cannot serve a product's workspace the library retries with
  * halved chunks.  Results do not depend on the chunking (bitwise). */
 SI_API int si_set_ozaki_chunks(si_handle h, int64_t max_rows, int64_t max_cols);
-/* INT8 tensor-core kernel of the emulated products: 0 = automatic (CTA pairs),
- * 1 = CTA pairs (tcgen05.mma.cta_group::2, 256 x 256 tiles), 2 = single CTAs
- * (cta_group::1, 128 x 256 tiles).  Results are identical (exact integers). */
+/* INT8 tensor-core kernel of the emulated products: 0 = automatic (single
+ * CTAs), 1 = CTA pairs (tcgen05.mma.cta_group::2, 256 x 256 tiles), 2 = single
+ * CTAs (cta_group::1, 128 x 256 tiles).  Results are identical (exact
+ * integers); at the power cap the single-CTA kernel is faster (fewer DRAM bytes). */
 SI_API int si_set_ozaki_kernel(si_handle h, int variant);
-/* Tuning hook of the CTA-pair INT8 kernel (process-wide; measurement tools):
- * rasterisation group in 256-row pair tiles (0 keeps), L2 policy of the A /
- * B operand loads (0 evict_normal, 1 evict_last, 2 evict_first; -1 keeps). */
+/* Tuning hook of the INT8 kernels (process-wide; measurement tools):
+ * rasterisation group in 256-row pair tiles (0 keeps; >= 2^20: a probe in
+ * which every tile reads and writes tile (0, 0) of plane 0 -- operands served
+ * from L2, results meaningless), L2 policy of the A / B operand loads
+ * (0 evict_normal, 1 evict_last, 2 evict_first; -1 keeps). */
 SI_API int si_ozaki_tune(int group_m, int l2_a, int l2_b);
 /* The first n moduli of the emulation. */
 SI_API int si_ozaki_moduli(int n, uint32_t* moduli);

@@ -70,9 +70,9 @@ _KERNELS = {"auto": 0, "pair": 1, "single": 2}
 
 
 def set_ozaki_kernel(name: str, device: int | None = None) -> None:
-    """INT8 tensor-core kernel of the emulated products: ``"pair"`` (2-CTA
-    clusters, tcgen05.mma.cta_group::2, 256 x 256 tiles; what ``"auto"``
-    picks) or ``"single"`` (one CTA per 128 x 256 tile).  Results are identical."""
+    """INT8 tensor-core kernel of the emulated products: ``"single"`` (one CTA
+    per 128 x 256 tile; what ``"auto"`` picks) or ``"pair"`` (2-CTA clusters,
+    tcgen05.mma.cta_group::2, 256 x 256 tiles).  Results are identical."""
     if name not in _KERNELS:
         raise ValueError(f"unknown INT8 kernel {name!r} (expected one of {sorted(_KERNELS)})")
     _lib.call("si_set_ozaki_kernel", _lib.handle(device), _KERNELS[name])

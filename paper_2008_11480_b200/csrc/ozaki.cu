@@ -360,8 +360,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+constexpr int kL2OnlyProbe = 1 << 20;  // tuning probe: every tile reads tile (0, 0) of plane 0
+
 __device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int& plane, int& tm, int& tn,
                                         int group_m = GROUP_M) {
+  if (group_m >= kL2OnlyProbe) {  // measurement only (si_ozaki_tune): operands stay in L2
+    plane = tm = tn = 0;
+    return;
+  }
   const int per_plane = num_m * num_n;
   plane = t / per_plane;
   const int r = t - plane * per_plane;
@@ -378,7 +384,7 @@ __device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int& plane,
 __global__ void __launch_bounds__(GTHREADS, 1)
     i8_gemm_mod_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, uint8_t* __restrict__ R, int M,
-                       int N, int Kp, int nplanes, const __grid_constant__ ModTab mt) {
+                       int N, int Kp, int nplanes, const __grid_constant__ ModTab mt, int group_m) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -429,7 +435,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int plane, tm, tn;
-        tile_of(t, num_m, num_n, plane, tm, tn);
+        tile_of(t, num_m, num_n, plane, tm, tn, group_m);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1u);
           const uint32_t sa = base + stage * GSTAGE_BYTES;
@@ -482,7 +488,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     uint32_t aphase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int plane, tm, tn;
-      tile_of(t, num_m, num_n, plane, tm, tn);
+      tile_of(t, num_m, num_n, plane, tm, tn, group_m);
       const unsigned m = mt.m[plane], magic = mt.magic[plane], off = mt.off[plane];
       mbar_wait(tfull_bar(acc), aphase);
       tc_fence_after();
@@ -1013,6 +1019,7 @@ const Consts& consts() {
 
 // rasterisation group and L2 policies of the pair kernel (tuning hook: si_ozaki_tune)
 int g_pair_group_m = GROUP_M, g_pair_l2a = 0, g_pair_l2b = 0;
+int g_single_group_m = GROUP_M;
 
 int num_sms() {
   int dev = 0, n = 0;
@@ -1043,7 +1050,7 @@ inline int64_t kpad(int64_t K) { return (K + GBK - 1) / GBK * GBK; }
 unsigned modulus(int l) { return kmod(l); }
 
 void tune_pair(int group_m, int l2a, int l2b) {
-  if (group_m > 0) g_pair_group_m = group_m;
+  if (group_m > 0) g_pair_group_m = g_single_group_m = group_m;
   if (l2a >= 0 && l2a <= 2) g_pair_l2a = l2a;
   if (l2b >= 0 && l2b <= 2) g_pair_l2b = l2b;
 }
@@ -1083,7 +1090,7 @@ cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, in
   if (M <= 0 || N <= 0 || Kp <= 0 || Kp % GBK || nplanes < 1 || nplanes > kMaxModuli ||
       M > INT32_MAX || N > INT32_MAX || Kp > kMaxK + GBK || variant < 0 || variant > 2)
     return cudaErrorInvalidValue;
-  const bool pair = variant != kI8Single;
+  const bool pair = variant == kI8Pair;  // auto: single CTAs (fewer DRAM bytes; faster at the power cap)
   CUtensorMap ta, tb;
   if (!make_map_i8(&ta, A, Kp, M, nplanes, pair ? PBM / 2 : GBM) ||
       !make_map_i8(&tb, Bt, Kp, N, nplanes, pair ? PBN / 2 : GBN)) {
@@ -1103,7 +1110,7 @@ cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, in
     const int64_t tiles = ((M + GBM - 1) / GBM) * ((N + GBN - 1) / GBN) * nplanes;
     const int grid = (int)(tiles < sms ? tiles : sms);
     i8_gemm_mod_kernel<<<grid, GTHREADS, GSMEM, s>>>(ta, tb, R, (int)M, (int)N, (int)Kp, nplanes,
-                                                     consts().mt);
+                                                     consts().mt, g_single_group_m);
   }
   return cudaGetLastError();
 }

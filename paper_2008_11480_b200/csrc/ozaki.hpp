@@ -16,8 +16,10 @@ constexpr int64_t kMaxK = 65536;  // |sum of K products of int8 residues| < 2^30
 
 // Device workspace of one emulated product, carved by the caller (engine.cu)
 // from one allocation of workspace_bytes().
-// INT8 tensor-core kernel: CTA pairs (cta_group::2, 256 x 256 tiles; default)
-// or single CTAs (128 x 256 tiles).  Results are identical (exact integers).
+// INT8 tensor-core kernel: single CTAs (cta_group::1, 128 x 256 tiles; the
+// default) or CTA pairs (cta_group::2, 256 x 256 tiles: more work per clock,
+// but twice the DRAM bytes, which costs more at the 1000 W cap -- 10% slower
+// in the C4 step, profiles/ozaki_kernel_ab_r02.txt).  Identical results.
 constexpr int kI8Auto = 0, kI8Pair = 1, kI8Single = 2;
 
 struct Work {
@@ -60,7 +62,7 @@ cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, i
 cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, int64_t M, int64_t N,
                                int64_t Kp, int nplanes, cudaStream_t s, int variant = kI8Auto);
 
-// Tuning hook of the CTA-pair INT8 kernel (process-wide): rasterisation group
+// Tuning hook of the INT8 kernels (process-wide): rasterisation group
 // (pair-tile rows per group) and the L2 policies of the A / B operand loads
 // (0 evict_normal, 1 evict_last, 2 evict_first); negative / zero keeps a value.
 void tune_pair(int group_m, int l2a, int l2b);

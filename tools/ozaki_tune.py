@@ -20,6 +20,7 @@ from int8_yardstick import Clocks, timed  # noqa: E402
 
 SETTINGS = [(16, 0, 0), (8, 0, 0), (4, 0, 0), (32, 0, 0), (16, 1, 2), (8, 1, 2), (4, 1, 2),
             (8, 1, 0), (8, 0, 2)]
+L2_PROBE = (1 << 20, 0, 0)  # every tile on the same operands: no DRAM traffic (timing probe)
 
 
 def main():
@@ -27,13 +28,16 @@ def main():
     ap.add_argument("--once", nargs=3, type=int, default=None)
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--planes", type=int, default=16)
+    ap.add_argument("--kernel", default="pair", choices=["pair", "single"])
+    ap.add_argument("--probe", action="store_true",
+                    help="A/B of the default raster against the L2-only probe, alternating")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     n, planes = args.n, args.planes
     g = torch.Generator(device="cuda").manual_seed(0)
     a = torch.randint(-128, 128, (planes, n, n), dtype=torch.int8, device="cuda", generator=g)
     b = torch.randint(-128, 128, (planes, n, n), dtype=torch.int8, device="cuda", generator=g)
-    P.set_ozaki_kernel("pair")
+    P.set_ozaki_kernel(args.kernel)
     ops = 2.0 * n ** 3 * planes
     if args.once:
         for s in (SETTINGS if args.once[0] == 0 else [tuple(args.once)]):
@@ -42,7 +46,10 @@ def main():
             torch.cuda.synchronize()
         return
     res = {}
-    for s in SETTINGS:
+    settings = SETTINGS
+    if args.probe:
+        settings = [(16, 0, 0), L2_PROBE, (16, 0, 0), L2_PROBE]
+    for i, s in enumerate(settings):
         _lib.call("si_ozaki_tune", *s)
         fn = lambda: P.i8_gemm_mod(a, b)  # noqa: E731
         fn()
@@ -52,10 +59,11 @@ def main():
         clk = Clocks()
         sus = timed(fn, reps)
         c = clk.stop()
-        res[str(s)] = {"burst_tops": ops / burst / 1e9, "sustained_tops": ops / sus / 1e9,
+        res[f"{i}:{s}"] = {"burst_tops": ops / burst / 1e9, "sustained_tops": ops / sus / 1e9,
                        "burst_ms": burst, "sustained_ms": sus, "clocks": c}
-        print(s, json.dumps(res[str(s)]), flush=True)
-    json.dump(res, open("gpurun_out/ozaki_tune.json", "w"), indent=1)
+        print(s, json.dumps(res[f"{i}:{s}"]), flush=True)
+    json.dump(res, open(f"gpurun_out/ozaki_tune_{args.kernel}{'_probe' if args.probe else ''}.json",
+                        "w"), indent=1)
 
 
 if __name__ == "__main__":
