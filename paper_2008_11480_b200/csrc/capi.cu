@@ -76,6 +76,22 @@ struct Call {
   ~Call() { add_counters(counters, c); }
 };
 
+// A step's n x n inputs that no output of the call overlaps: the emulated
+// products may keep their operand images across the call (engine.cu oz_side).
+void mark_stable(Ctx& c, int64_t n, std::initializer_list<const double*> ins,
+                 std::initializer_list<const double*> outs) {
+  const size_t bytes = (size_t)n * (size_t)n * sizeof(double);
+  for (const double* in : ins) {
+    const char* a = reinterpret_cast<const char*>(in);
+    bool clash = false;
+    for (const double* out : outs) {
+      const char* b = reinterpret_cast<const char*>(out);
+      if (a < b + bytes && b < a + bytes) clash = true;
+    }
+    if (!clash) c.stable.push_back(in);
+  }
+}
+
 // One sharded C-ABI call: Call + this call's Shard (row split, gather cache).
 struct ShardCall {
   Call call;
@@ -576,6 +592,7 @@ int si_ns_step(si_handle h, int64_t n, const double* a, const double* g, const d
     need(h && a && g && f && g_out && f_out, "null pointer");
     PlanPtr pl = opt_plan(plan, plan_len, consts, nconsts);
     Call call(h, stream, counters);
+    mark_stable(call.c, n, {a, g, f}, {g_out, f_out});
     ns_step(call.c, sq(a, n), sq(g, n), sq(f, n), order, pl.get(), sq(g_out, n), sq(f_out, n));
   });
 }
@@ -588,6 +605,7 @@ int si_ns_step_ex(si_handle h, int64_t n, const double* a, const double* g, cons
     need(h && a && g && f && g_out && f_out, "null pointer");
     PlanPtr pl = opt_plan(plan, plan_len, consts, nconsts);
     Call call(h, stream, counters);
+    mark_stable(call.c, n, {a, g, f}, {g_out, f_out});
     if (input_ready_events) {
       const double* bases[3] = {a, g, f};
       for (int i = 0; i < 3; ++i)
@@ -613,6 +631,7 @@ int si_ns_step_gated(si_handle h, int64_t n, const double* a, const double* g, c
     std::vector<cudaEvent_t> chunks(f_chunks);
     for (int k = 0; k < f_chunks; ++k) chunks[k] = reinterpret_cast<cudaEvent_t>(f_chunk_events[k]);
     Call call(h, stream, counters);
+    mark_stable(call.c, n, {a, g, f}, {g_out, f_out});
     if (input_flags) {
       const double* bases[3] = {a, g, f};
       for (int i = 0; i < 3; ++i) {
@@ -672,6 +691,7 @@ int si_composite_step_ex(si_handle h, int64_t n, const double* a, const double* 
         ev.ready[i] = reinterpret_cast<cudaEvent_t>(input_ready_events[i]);
     ev.g_done = reinterpret_cast<cudaEvent_t>(g_done_event);
     Call call(h, stream, counters);
+    mark_stable(call.c, n, {a, g, f, precond, residual, split_matrix}, {g_out, f_out});
     composite_step(call.c, sq(a, n), sq(g, n), sq(f, n), sq(precond, n), sq(residual, n),
                    sq(split_matrix, n), rv, pv, order_n, concurrent != 0, sq(g_out, n),
                    sq(f_out, n), &ev);
@@ -711,6 +731,7 @@ int si_composite_step_gated(si_handle h, int64_t n, const double* a, const doubl
     ev.f_chunk = f_chunks ? chunks.data() : nullptr;
     ev.f_chunks = f_chunks;
     Call call(h, stream, counters);
+    mark_stable(call.c, n, {a, g, f, precond, residual, split_matrix}, {g_out, f_out});
     if (input_flags) {
       const double* bases[6] = {a, g, f, precond, residual, split_matrix};
       for (int i = 0; i < 6; ++i) {

@@ -96,6 +96,55 @@ void Ctx::gate_stream(const void* p) {
     }
 }
 
+struct Ctx::OzSide {
+  const void* ptr;
+  int64_t rows, cols, ld, k;
+  int nmod;
+  bool b_side;
+  MV buf;
+  oz::Side side;
+};
+
+namespace {
+constexpr size_t kOzSideMaxBytes = (size_t)8 << 30;  // keep sides up to n = 16384 x 16384
+
+// The kept scales + planes of operand `m` (A side: rows of A; B side: columns
+// of B) of an emulated product with inner dimension k, or nullptr when `m` is
+// not a stable input of this call (or its side does not fit the budget).
+oz::Side* oz_side(Ctx& c, const Mat& m, bool b_side, int64_t k, int nmod) {
+  if (c.s != c.root || c.stable.empty()) return nullptr;
+  if (std::find(c.stable.begin(), c.stable.end(), (const void*)m.p) == c.stable.end())
+    return nullptr;
+  for (auto& e : c.oz_sides)
+    if (e->ptr == m.p && e->rows == m.rows && e->cols == m.cols && e->ld == m.ld && e->k == k &&
+        e->nmod == nmod && e->b_side == b_side)
+      return &e->side;
+  const int64_t n = b_side ? m.cols : m.rows;
+  const size_t bytes = oz::side_bytes(n, k, nmod);
+  if (bytes > kOzSideMaxBytes) return nullptr;
+  auto e = std::make_shared<Ctx::OzSide>();
+  try {
+    e->buf = alloc(c, 1, (int64_t)((bytes + 7) / 8));
+  } catch (const Error& ex) {
+    if (ex.code == kENoMem) return nullptr;  // no room: compute per product
+    throw;
+  }
+  e->ptr = m.p;
+  e->rows = m.rows;
+  e->cols = m.cols;
+  e->ld = m.ld;
+  e->k = k;
+  e->nmod = nmod;
+  e->b_side = b_side;
+  auto* base = reinterpret_cast<uint8_t*>(e->buf.v.p);
+  e->side.scale = reinterpret_cast<unsigned long long*>(base);
+  e->side.planes = reinterpret_cast<int8_t*>(base + ((n * 8 + 255) & ~(int64_t)255));
+  e->side.ready = false;
+  c.oz_sides.push_back(e);
+  return &e->side;
+}
+}  // namespace
+
 void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV* C, double beta,
           double diag, bool mv, int64_t doff, const PanelWait* pw) {
   if (c.shard) {
@@ -189,11 +238,23 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
     w.max_cols = h->oz_max_cols;
     w.max_rows = h->oz_max_rows;
     w.variant = h->oz_variant;
+    // A branch context keeps every buffer it allocates until its join, so its
+    // products share one workspace (stream-ordered on the branch stream); on
+    // the root stream each product's workspace is released right after it.
+    const bool reuse_ws = c.s != c.root;
     MV ws;
     for (int level = 0;; ++level) {
       w.bytes = oz::workspace_bytes(d.rows, d.cols, A.v.cols, h->oz_nmod, w.max_cols, w.max_rows);
+      if (reuse_ws && c.oz_ws.own && c.oz_ws_bytes >= w.bytes) {
+        ws = c.oz_ws;
+        break;
+      }
       try {
         ws = alloc(c, 1, (int64_t)((w.bytes + 7) / 8));
+        if (reuse_ws) {
+          c.oz_ws = ws;
+          c.oz_ws_bytes = w.bytes;
+        }
         break;
       } catch (const Error& ex) {
         if (ex.code != kENoMem || level == 4 || (w.max_rows > 0 && w.max_rows <= 1024)) throw;
@@ -222,7 +283,9 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
         }
       };
     }
-    err = oz::launch_gemm(A.v, B.v, d, e, h->oz_nmod, w, c.s, &nl, hook);
+    oz::Side* as = oz_side(c, A.v, false, A.v.cols, h->oz_nmod);
+    oz::Side* bs = oz_side(c, B.v, true, A.v.cols, h->oz_nmod);
+    err = oz::launch_gemm(A.v, B.v, d, e, h->oz_nmod, w, c.s, &nl, hook, as, bs);
     h->launches += nl;
     if (h->profiling && err == cudaSuccess) {
       check(cudaEventRecord(rec.stop, c.s), "cudaEventRecord");

@@ -123,6 +123,16 @@ struct Ctx {
   // this rank's rows; a replicated left / epilogue operand is read through its
   // row view, a sharded right operand is all-gathered first.
   Shard* shard = nullptr;
+  // workspace of the emulated (Ozaki-II) products on a branch context, reused
+  // by every product on its stream (they are stream-ordered)
+  MV oz_ws;
+  size_t oz_ws_bytes = 0;
+  // Caller buffers this call only reads (a step's inputs, not aliased by an
+  // output): the emulated products keep their operand scales + residue
+  // planes across the call's products (root stream only; released with the call).
+  std::vector<const void*> stable;
+  struct OzSide;
+  std::vector<std::shared_ptr<OzSide>> oz_sides;
   Ctx(Handle* hh, cudaStream_t st) : h(hh), root(st), s(st) {}
 };
 

@@ -1076,6 +1076,10 @@ int64_t chunk_rows(int64_t M, int64_t max_rows) {
   return std::min(M, ((M + nch - 1) / nch + PBM - 1) / PBM * PBM);  // balanced chunks
 }
 
+size_t side_bytes(int64_t rows, int64_t K, int nmod) {
+  return align256(rows * 8) + align256((size_t)nmod * rows * kpad(K));
+}
+
 size_t workspace_bytes(int64_t M, int64_t N, int64_t K, int nmod, int64_t max_cols,
                        int64_t max_rows) {
   const int64_t Kp = kpad(K);
@@ -1116,7 +1120,8 @@ cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, in
 }
 
 cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, int nmod,
-                        const Work& w, cudaStream_t s, int64_t* launches, const I8Hook& hook) {
+                        const Work& w, cudaStream_t s, int64_t* launches, const I8Hook& hook,
+                        Side* a_side, Side* b_side) {
   const int64_t M = D.rows, N = D.cols, K = A.cols;
   if (nmod < kMinModuli || nmod > kMaxModuli || K < 1 || K > kMaxK || M > INT32_MAX ||
       N > INT32_MAX || w.bytes < workspace_bytes(M, N, K, nmod, w.max_cols, w.max_rows))
@@ -1142,25 +1147,37 @@ cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, i
   int64_t n = 0;
   cudaError_t err;
   const int sms = num_sms();
+  // operand sides kept by the caller (unchunked sides only)
+  const bool a_ext = a_side && a_side->scale && a_side->planes && MC == M;
+  const bool b_ext = b_side && b_side->scale && b_side->planes && NC == N;
+  if (a_ext) {
+    rmax = a_side->scale;
+    ares = a_side->planes;
+  }
+  if (b_ext) {
+    cmax = b_side->scale;
+    bres = b_side->planes;
+  }
   for (int64_t i0 = 0; i0 < M; i0 += MC) {
     const int64_t mc = std::min(MC, M - i0);
     const double* ap = A.p + i0 * A.ld;
     // A side of this row chunk: row scales and residue planes
-    row_absmax_kernel<<<(int)std::min<int64_t>((mc + 7) / 8, 16 * sms), 256, 0, s>>>(
-        ap, A.ld, (int)mc, (int)K, rmax);
-    ++n;
-    {
+    if (!(a_ext && a_side->ready)) {
+      row_absmax_kernel<<<(int)std::min<int64_t>((mc + 7) / 8, 16 * sms), 256, 0, s>>>(
+          ap, A.ld, (int)mc, (int)K, rmax);
+      ++n;
       const int64_t thr = mc * (Kp / 16);
       const int blocks = (int)std::min<int64_t>((thr + 255) / 256, 64 * sms);
       residues_rows_kernel<<<blocks, 256, 0, s>>>(ap, A.ld, (int)mc, (int)K, (int)Kp, rmax, pa,
                                                    nmod, ares);
       ++n;
+      if (a_ext) a_side->ready = true;
     }
     // B side (kept across row chunks when one column chunk covers N), the
     // tensor-core products and the reconstruction per column chunk
     for (int64_t j0 = 0; j0 < N; j0 += NC) {
       const int64_t nc = std::min(NC, N - j0);
-      if (i0 == 0 || NC < N) {
+      if ((i0 == 0 || NC < N) && !(b_ext && b_side->ready)) {
         const double* bp = B.p + j0;
         if ((err = cudaMemsetAsync(cmax, 0, nc * 8, s)) != cudaSuccess) return err;
         col_absmax_kernel<<<dim3((unsigned)((nc + 31) / 32), (unsigned)((K + 255) / 256)), 256, 0,
@@ -1169,6 +1186,7 @@ cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, i
         residues_cols_kernel<<<dim3((unsigned)((nc + 63) / 64), (unsigned)(Kp / 64)), 256, 0, s>>>(
             bp, B.ld, (int)K, (int)nc, (int)Kp, cmax, pb, nmod, bres);
         ++n;
+        if (b_ext) b_side->ready = true;
       }
       if ((err = cudaGetLastError()) != cudaSuccess) return err;
       if (hook) hook(true, 2.0 * (double)mc * (double)nc * (double)Kp * (double)nmod);

@@ -42,6 +42,18 @@ constexpr size_t kChunkBudget = (size_t)10 << 30;
 size_t workspace_bytes(int64_t M, int64_t N, int64_t K, int nmod, int64_t max_cols = 0,
                        int64_t max_rows = 0);
 
+// Scales + residue planes of one operand side, kept by the caller across
+// products that share the operand (engine.cu: a step's immutable inputs).
+// `ready` = already filled (stream-ordered before this launch); otherwise
+// launch_gemm fills them.  Used only when the product is not chunked on that
+// side (rows of A / columns of B).
+struct Side {
+  unsigned long long* scale = nullptr;  // max |entry| bits per row (A) / column (B)
+  int8_t* planes = nullptr;             // nmod x rows x Kp (A) / nmod x cols x Kp (B)
+  bool ready = false;
+};
+size_t side_bytes(int64_t rows, int64_t K, int nmod);  // scale + planes, 256-aligned parts
+
 // Called on the stream right before (begin = true) and after (false) every
 // INT8 tensor-core launch of a product, with that launch's int8 op count
 // (2 M Nc Kp per plane, summed over planes) -- the profiling hook.
@@ -54,7 +66,8 @@ using I8Hook = std::function<void(bool begin, double ops)>;
 // Returns the number of kernels launched through *launches.
 cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, int nmod,
                         const Work& w, cudaStream_t s, int64_t* launches,
-                        const I8Hook& hook = nullptr);
+                        const I8Hook& hook = nullptr, Side* a_side = nullptr,
+                        Side* b_side = nullptr);
 
 // Test hook for the tensor-core kernel alone: R[l] = (A[l] @ Bt[l]^T) mod m_l
 // for l < nplanes, A[l]: M x Kp int8 rows, Bt[l]: N x Kp int8 rows (K-major,

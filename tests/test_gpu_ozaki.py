@@ -354,3 +354,36 @@ def test_workspace_retry_under_memory_cap():
         torch.cuda.set_per_process_memory_fraction(1.0)
         torch.cuda.empty_cache()
     assert torch.equal(capped, full)
+
+
+def test_step_operand_images_kept_bitwise():
+    """A composite step keeps the scales / residue planes of its immutable
+    inputs (A, S^-1, B, G, F) across its emulated products; the parts on
+    concurrent streams recompute them per product.  Both give the same bits,
+    and the kept images save residue launches."""
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import _lib, configs
+
+    a, _ = configs.c4_householder(n=2048, rhs=1)
+    P.set_gemm_backend("ozaki", 16, 1024)
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False)
+    st = P.initial_series(sp, 0, 1, order=2)
+    spec = P.CompositeSpec((2, 3, 4, 5))
+    h = _lib.handle()
+    import ctypes
+
+    def run(executor):
+        _lib.call("si_profile_begin", h)
+        out = P.composite_step(st, sp.matrix, sp, spec, 2, executor=executor)
+        torch.cuda.synchronize()
+        ms, fl, ng, nl = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.call("si_profile_end", h, ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(ng),
+                  ctypes.byref(nl))
+        return out, nl.value
+
+    serial, n_serial = run(None)
+    conc, n_conc = run("streams")
+    assert torch.equal(serial.estimate, conc.estimate)
+    assert torch.equal(serial.residual, conc.residual)
+    assert serial.ctr.mmm == conc.ctr.mmm
+    assert n_serial < n_conc, (n_serial, n_conc)
