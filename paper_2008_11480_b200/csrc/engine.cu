@@ -197,13 +197,16 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
   // inputs still arriving in row panels: in-kernel gates for A rows / B k-slabs
   // of the DMMA GEMM, stream waits for everything else
   const PanelWait* pwa = nullptr;
+  const PanelWait* oz_rows = nullptr;  // emulated product: rows of A waited per row chunk
   if (!c.gates.empty()) {
     if (in_kernel_gates) {
       pwa = c.gate_of(A.v.p);
       if (!pw) pw = c.gate_of(B.v.p);
       if (C && C->v.p != B.v.p) c.gate_stream(C->v.p);  // C == B: its panels gate the k-loop
     } else {
-      c.gate_stream(A.v.p);
+      if (use_oz && A.v.p != B.v.p && (!C || C->v.p != A.v.p) && A.v.rows == d.rows)
+        oz_rows = c.gate_of(A.v.p);
+      if (!oz_rows) c.gate_stream(A.v.p);
       c.gate_stream(B.v.p);
       if (C) c.gate_stream(C->v.p);
     }
@@ -238,6 +241,21 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
     w.max_cols = h->oz_max_cols;
     w.max_rows = h->oz_max_rows;
     w.variant = h->oz_variant;
+    oz::RowHook row_hook;
+    if (oz_rows) {
+      // A's rows still arriving in panels: one row chunk per panel, each
+      // waiting for its own panels only, so the product runs behind the copy
+      const PanelWait gate = *oz_rows;
+      int64_t prow = d.rows;
+      for (int p = 0; p < gate.npanels; ++p)
+        prow = std::min<int64_t>(prow, gate.bounds[p + 1] - gate.bounds[p]);
+      w.max_rows = w.max_rows > 0 ? std::min(w.max_rows, prow) : prow;
+      row_hook = [&c, gate](int64_t r0, int64_t r1) {
+        for (int p = 0; p < gate.npanels; ++p)
+          if (gate.bounds[p] < r1 && gate.bounds[p + 1] > r0)
+            check(stream_wait_u32(gate.ready + p, gate.epoch, c.s), "panel wait");
+      };
+    }
     // A branch context keeps every buffer it allocates until its join, so its
     // products share one workspace (stream-ordered on the branch stream); on
     // the root stream each product's workspace is released right after it.
@@ -285,7 +303,8 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
     }
     oz::Side* as = oz_side(c, A.v, false, A.v.cols, h->oz_nmod);
     oz::Side* bs = oz_side(c, B.v, true, A.v.cols, h->oz_nmod);
-    err = oz::launch_gemm(A.v, B.v, d, e, h->oz_nmod, w, c.s, &nl, hook, as, bs);
+    err = oz::launch_gemm(A.v, B.v, d, e, h->oz_nmod, w, c.s, &nl, hook, as, bs, row_hook);
+    if (oz_rows) c.gate_stream(A.v.p);  // every panel waited (no-ops by now): later readers
     h->launches += nl;
     if (h->profiling && err == cudaSuccess) {
       check(cudaEventRecord(rec.stop, c.s), "cudaEventRecord");

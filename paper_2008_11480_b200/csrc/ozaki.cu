@@ -1121,7 +1121,7 @@ cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, in
 
 cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, int nmod,
                         const Work& w, cudaStream_t s, int64_t* launches, const I8Hook& hook,
-                        Side* a_side, Side* b_side) {
+                        Side* a_side, Side* b_side, const RowHook& row_hook) {
   const int64_t M = D.rows, N = D.cols, K = A.cols;
   if (nmod < kMinModuli || nmod > kMaxModuli || K < 1 || K > kMaxK || M > INT32_MAX ||
       N > INT32_MAX || w.bytes < workspace_bytes(M, N, K, nmod, w.max_cols, w.max_rows))
@@ -1161,6 +1161,7 @@ cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, i
   for (int64_t i0 = 0; i0 < M; i0 += MC) {
     const int64_t mc = std::min(MC, M - i0);
     const double* ap = A.p + i0 * A.ld;
+    if (row_hook) row_hook(i0, i0 + mc);
     // A side of this row chunk: row scales and residue planes
     if (!(a_ext && a_side->ready)) {
       row_absmax_kernel<<<(int)std::min<int64_t>((mc + 7) / 8, 16 * sms), 256, 0, s>>>(

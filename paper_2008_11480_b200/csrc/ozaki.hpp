@@ -59,6 +59,10 @@ size_t side_bytes(int64_t rows, int64_t K, int nmod);  // scale + planes, 256-al
 // (2 M Nc Kp per plane, summed over planes) -- the profiling hook.
 using I8Hook = std::function<void(bool begin, double ops)>;
 
+// Called on the stream before the A-side work of each row chunk [r0, r1) of D
+// (e.g. waits for the rows of A still being copied in).
+using RowHook = std::function<void(int64_t r0, int64_t r1)>;
+
 // D = alpha * (A @ B) + beta * C + diag * I (diag at (i, i + doff)), A @ B
 // computed exactly from integer images of A and B on the INT8 tensor cores
 // (tcgen05.mma kind::i8, one GEMM per modulus) and reconstructed by the
@@ -67,7 +71,7 @@ using I8Hook = std::function<void(bool begin, double ops)>;
 cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, int nmod,
                         const Work& w, cudaStream_t s, int64_t* launches,
                         const I8Hook& hook = nullptr, Side* a_side = nullptr,
-                        Side* b_side = nullptr);
+                        Side* b_side = nullptr, const RowHook& row_hook = nullptr);
 
 // Test hook for the tensor-core kernel alone: R[l] = (A[l] @ Bt[l]^T) mod m_l
 // for l < nplanes, A[l]: M x Kp int8 rows, Bt[l]: N x Kp int8 rows (K-major,

@@ -150,14 +150,27 @@ def test_composite_step_with_inputs_in_flight():
         P.composite_step(st, sp.matrix, sp, spec, 2, inputs_ready={"bogus": done})
 
 
-@pytest.mark.parametrize("concurrent", [False, True])
-def test_composite_step_with_inputs_in_row_panels(concurrent):
+@pytest.mark.parametrize("backend,concurrent", [("dmma", False), ("dmma", True),
+                                                ("ozaki", False), ("ozaki", True)])
+def test_composite_step_with_inputs_in_row_panels(backend, concurrent):
     """Inputs copied host->device panel by panel (out of order, a delaying copy
-    first) with flags; the DMMA products gate their loads per panel and F' comes
-    out in row blocks: bitwise the resident-input result, same product count."""
+    first) with flags; the DMMA products gate their loads per panel (the
+    emulated products wait per row chunk of A and for whole B / C operands) and
+    F' comes out in row blocks: bitwise the resident-input result, same product
+    count."""
     import paper_2008_11480_b200 as P
     from paper_2008_11480_b200 import _lib, configs
 
+    if backend == "ozaki":
+        # every product emulated, the F' row blocks (192 rows) included
+        P.set_gemm_backend("ozaki", 16, 128)
+    try:
+        _inputs_in_row_panels(P, _lib, configs, concurrent)
+    finally:
+        P.set_gemm_backend("dmma", 16, 1024)
+
+
+def _inputs_in_row_panels(P, _lib, configs, concurrent):
     n, npanels = 768, 6
     a, _ = configs.c4_householder(n=n, rhs=1)
     sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False)
