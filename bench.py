@@ -272,8 +272,9 @@ def ozaki_roofline(w, i8_ms: float, i8_ops: float, i8_launches: int, fp64_achiev
         pass
     return {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOPS (int8)",
             "frac": ach / peak if ach else None, "traffic": traffic,
-            "kernel": ("i8_gemm_mod_pair_kernel" if getattr(w, "i8_kernel", "auto") == "pair"
-                       else "i8_gemm_mod_kernel"), "launches": i8_launches, "moduli": moduli,
+            "kernel": {"pair": "i8_gemm_mod_pair_kernel", "multicast": "i8_gemm_mod_mc_kernel"}.get(
+                getattr(w, "i8_kernel", "auto"), "i8_gemm_mod_kernel"),
+            "launches": i8_launches, "moduli": moduli,
             "peak_source": src,
             "fp64_equivalent": {
                 "what": "whole emulated products (scaling, residues, INT8 GEMM, CRT + epilogue): "
@@ -1516,7 +1517,7 @@ def main():
                          "auto = ozaki")
     ap.add_argument("--moduli", type=int, default=16,
                     help="--gemm ozaki: number of moduli (16 = at least DGEMM's accuracy)")
-    ap.add_argument("--i8-kernel", choices=["auto", "pair", "single"], default="auto",
+    ap.add_argument("--i8-kernel", choices=["auto", "pair", "single", "multicast"], default="auto",
                     help="--gemm ozaki: INT8 tensor-core kernel (CTA pairs or single CTAs)")
     ap.add_argument("--no-dmma-side", action="store_true",
                     help="--gemm ozaki: skip the FP64 DMMA reference point timed after the run")

@@ -448,10 +448,10 @@ SI_API int si_get_gemm_backend(si_handle h, int* backend, int* nmoduli, int64_t*
  * the allocator cannot serve a product's workspace the library retries with
  * halved chunks.  Results do not depend on the chunking (bitwise). */
 SI_API int si_set_ozaki_chunks(si_handle h, int64_t max_rows, int64_t max_cols);
-/* INT8 tensor-core kernel of the emulated products: 0 = automatic (single
- * CTAs), 1 = CTA pairs (tcgen05.mma.cta_group::2, 256 x 256 tiles), 2 = single
- * CTAs (cta_group::1, 128 x 256 tiles).  Results are identical (exact
- * integers); at the power cap the single-CTA kernel is faster (fewer DRAM bytes). */
+/* INT8 tensor-core kernel of the emulated products: 0 = automatic, 1 = CTA
+ * pairs (tcgen05.mma.cta_group::2, 256 x 256 tiles), 2 = single CTAs
+ * (cta_group::1, 128 x 256 tiles), 3 = single-CTA MMAs on 2-CTA clusters that
+ * multicast the shared B tile.  Results are identical (exact integers). */
 SI_API int si_set_ozaki_kernel(si_handle h, int variant);
 /* Tuning hook of the INT8 kernels (process-wide; measurement tools):
  * rasterisation group in 256-row pair tiles (0 keeps; >= 2^20: a probe in

@@ -66,7 +66,7 @@ def set_ozaki_chunks(max_rows: int = 0, max_cols: int = 0, device: int | None = 
     _lib.call("si_set_ozaki_chunks", _lib.handle(device), int(max_rows), int(max_cols))
 
 
-_KERNELS = {"auto": 0, "pair": 1, "single": 2}
+_KERNELS = {"auto": 0, "pair": 1, "single": 2, "multicast": 3}
 
 
 def set_ozaki_kernel(name: str, device: int | None = None) -> None:

@@ -1253,7 +1253,8 @@ int si_set_ozaki_chunks(si_handle h, int64_t max_rows, int64_t max_cols) {
 int si_set_ozaki_kernel(si_handle h, int variant) {
   return guard([&] {
     need(h != nullptr, "null handle");
-    need(variant == oz::kI8Auto || variant == oz::kI8Pair || variant == oz::kI8Single,
+    need(variant == oz::kI8Auto || variant == oz::kI8Pair || variant == oz::kI8Single ||
+             variant == oz::kI8Multicast,
          "unknown INT8 kernel variant");
     std::lock_guard<std::recursive_mutex> lock(h->h.mu);
     h->h.oz_variant = variant;

@@ -784,6 +784,209 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GTHREADS, 1)
   }
 }
 
+// ------------------------------- INT8 GEMM, B tiles multicast in CTA pairs --
+// Single-CTA MMAs (cta_group::1, 128 x 256 per CTA) on 2-CTA clusters whose
+// CTAs take adjacent 128-row tiles of the same 256-column tile: each CTA loads
+// its own A rows and HALF of the Bt tile with `.multicast::cluster`, which
+// lands in both CTAs' shared memory -- per SM 32 KB of L2 reads per k-block
+// instead of 48 KB, with the single-CTA kernel's accumulators and epilogue.
+// A stage is refilled only when both CTAs' MMAs have read it (each MMA commit
+// arrives on both CTAs' empty barrier, count 2).
+__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                               int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_both(uint32_t bar) {  // this CTA's MMAs -> both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GTHREADS, 1)
+    i8_gemm_mod_mc_kernel(const __grid_constant__ CUtensorMap tmA,
+                          const __grid_constant__ CUtensorMap tmB, uint8_t* __restrict__ R, int M,
+                          int N, int Kp, int nplanes, const __grid_constant__ ModTab mt,
+                          int group_m) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t bars = base + GSTAGES * GSTAGE_BYTES;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (GSTAGES + s); };
+  auto tfull_bar = [&](int a) { return bars + 8u * (2 * GSTAGES + a); };
+  auto tempty_bar = [&](int a) { return bars + 8u * (2 * GSTAGES + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * GSTAGES + 4);
+  uint8_t* smem_gen = smem_raw + (tmem_slot - raw);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int rank = (int)cta_rank();
+  const int num_m = (M + 2 * GBM - 1) / (2 * GBM);  // 256-row tile pairs
+  const int num_n = (N + GBN - 1) / GBN;
+  const int total = num_m * num_n * nplanes;
+  const int kblocks = Kp / GBK;
+  const int cid = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  constexpr int kHalfB = GB_BYTES / 2;  // 128 rows of Bt per CTA
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < GSTAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 2);  // both CTAs' MMAs
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tmem_slot),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();  // the peer's barriers are initialised before any multicast reaches them
+  tc_fence_after();
+  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(smem_gen);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer: own A rows, half of Bt to both CTAs ----
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < total; t += nclusters) {
+        int plane, tm, tn;
+        tile_of(t, num_m, num_n, plane, tm, tn, group_m);
+        const int arow = tm * 2 * GBM + rank * GBM;
+        const int brow = tn * GBN + rank * (GBN / 2);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1u);  // both CTAs are done with this stage
+          const uint32_t sa = base + stage * GSTAGE_BYTES;
+          mbar_expect_tx(full_bar(stage), GSTAGE_BYTES);
+          tma_load_3d(sa, &tmA, full_bar(stage), kb * GBK, arow, plane);
+          tma_load_3d_mc(sa + GA_BYTES + rank * kHalfB, &tmB, full_bar(stage), kb * GBK, brow,
+                         plane);
+          if (++stage == GSTAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+      // drain: every commit of both CTAs' MMAs has reached this CTA's empty
+      // barriers before the cluster may exit
+      for (int i = 0; i < GSTAGES; ++i) {
+        mbar_wait(empty_bar(stage), phase ^ 1u);
+        if (++stage == GSTAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (one thread per CTA) ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      for (int t = cid; t < total; t += nclusters) {
+        mbar_wait(tempty_bar(acc), aphase ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * GBN);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(full_bar(stage), phase);
+          tc_fence_after();
+          const uint32_t sa = base + stage * GSTAGE_BYTES;
+          const uint64_t adesc = sdesc(sa), bdesc = sdesc(sa + GA_BYTES);
+#pragma unroll
+          for (int k = 0; k < GBK / 32; ++k)
+            mma_i8(d, adesc + 2 * k, bdesc + 2 * k, (kb | k) != 0 ? 1u : 0u);
+          mma_commit_both(empty_bar(stage));
+          if (++stage == GSTAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        mma_commit(tfull_bar(acc));
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue: own 128 rows ----------------
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int t = cid; t < total; t += nclusters) {
+      int plane, tm, tn;
+      tile_of(t, num_m, num_n, plane, tm, tn, group_m);
+      const unsigned m = mt.m[plane], magic = mt.magic[plane], off = mt.off[plane];
+      mbar_wait(tfull_bar(acc), aphase);
+      tc_fence_after();
+      const int row = tm * 2 * GBM + rank * GBM + q * 32 + lane;
+      const int col0 = tn * GBN;
+      uint8_t* rp = R + (int64_t)plane * M * N + (int64_t)row * N + col0;
+      const bool vec = ((N & 15) == 0);
+#pragma unroll 1
+      for (int c = 0; c < GBN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * GBN + c * 32), v);
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          uint32_t b[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t u = v[i + j] + (1u << 30);
+            const uint32_t qq = __umulhi(u, magic) >> 7;
+            uint32_t r = u - qq * m;
+            r = r >= off ? r - off : r + m - off;
+            b[j] = r;
+          }
+          w[i >> 2] = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+        }
+        const int cc = col0 + c * 32;
+        if (row < M && cc < N) {
+          if (vec && cc + 32 <= N) {
+            uint4* dst = reinterpret_cast<uint4*>(rp + c * 32);
+            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          } else {
+            for (int i = 0; i < 32 && cc + i < N; ++i) rp[c * 32 + i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty_bar(acc));
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1u;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(kTmemCols)
+                 : "memory");
+  }
+}
+
 // ------------------------------------------------------------------ CRT --
 // X = sum_l c_l W_l (W_l the CRT weights, c_l in [0, m_l)) is held exactly as
 // four partial sums S_k of 32-bit pieces (c_l * piece < 2^40, 16 terms < 2^44);
@@ -1038,6 +1241,9 @@ cudaError_t set_gemm_attr() {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(i8_gemm_mod_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              PSMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(i8_gemm_mod_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             GSMEM);
   if (e == cudaSuccess && dev < 64) done.fetch_or(1ull << dev);
   return e;
 }
@@ -1092,12 +1298,13 @@ size_t workspace_bytes(int64_t M, int64_t N, int64_t K, int nmod, int64_t max_co
 cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, int64_t M, int64_t N,
                                int64_t Kp, int nplanes, cudaStream_t s, int variant) {
   if (M <= 0 || N <= 0 || Kp <= 0 || Kp % GBK || nplanes < 1 || nplanes > kMaxModuli ||
-      M > INT32_MAX || N > INT32_MAX || Kp > kMaxK + GBK || variant < 0 || variant > 2)
+      M > INT32_MAX || N > INT32_MAX || Kp > kMaxK + GBK || variant < 0 || variant > 3)
     return cudaErrorInvalidValue;
   const bool pair = variant == kI8Pair;  // auto: single CTAs (fewer DRAM bytes; faster at the power cap)
+  const bool mc = variant == kI8Multicast;
   CUtensorMap ta, tb;
   if (!make_map_i8(&ta, A, Kp, M, nplanes, pair ? PBM / 2 : GBM) ||
-      !make_map_i8(&tb, Bt, Kp, N, nplanes, pair ? PBN / 2 : GBN)) {
+      !make_map_i8(&tb, Bt, Kp, N, nplanes, (pair || mc) ? PBN / 2 : GBN)) {
     set_error("cuTensorMapEncodeTiled failed (int8 planes)");
     return cudaErrorInvalidValue;
   }
@@ -1110,6 +1317,11 @@ cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, in
     i8_gemm_mod_pair_kernel<<<grid, GTHREADS, PSMEM, s>>>(ta, tb, R, (int)M, (int)N, (int)Kp,
                                                           nplanes, consts().mt, g_pair_group_m,
                                                           g_pair_l2a, g_pair_l2b);
+  } else if (mc) {
+    const int64_t tiles = ((M + 2 * GBM - 1) / (2 * GBM)) * ((N + GBN - 1) / GBN) * nplanes;
+    const int grid = (int)std::min<int64_t>(2 * tiles, sms & ~1);
+    i8_gemm_mod_mc_kernel<<<grid, GTHREADS, GSMEM, s>>>(ta, tb, R, (int)M, (int)N, (int)Kp,
+                                                        nplanes, consts().mt, g_single_group_m);
   } else {
     const int64_t tiles = ((M + GBM - 1) / GBM) * ((N + GBN - 1) / GBN) * nplanes;
     const int grid = (int)(tiles < sms ? tiles : sms);

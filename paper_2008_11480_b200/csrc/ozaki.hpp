@@ -21,6 +21,8 @@ constexpr int64_t kMaxK = 65536;  // |sum of K products of int8 residues| < 2^30
 // but twice the DRAM bytes, which costs more at the 1000 W cap -- 10% slower
 // in the C4 step, profiles/ozaki_kernel_ab_r02.txt).  Identical results.
 constexpr int kI8Auto = 0, kI8Pair = 1, kI8Single = 2;
+// single-CTA MMAs on 2-CTA clusters sharing (multicasting) the B tile
+constexpr int kI8Multicast = 3;
 
 struct Work {
   uint8_t* base = nullptr;

@@ -49,7 +49,7 @@ def _dmma(a, b):
         return P.mat_mul(a, b, P.MulCounter())
 
 
-@pytest.mark.parametrize("kernel", ["pair", "single"])
+@pytest.mark.parametrize("kernel", ["pair", "single", "multicast"])
 @pytest.mark.parametrize("planes,m,n,kp", [(1, 128, 256, 128), (3, 300, 520, 256),
                                            (2, 1000, 777, 1024), (16, 513, 300, 2048),
                                            (5, 129, 1000, 4096), (2, 1, 1, 128),
@@ -83,7 +83,7 @@ def test_int8_kernel_extreme_residues():
     a = torch.full((4, 256, 8192), -128, dtype=torch.int8, device="cuda")
     bt = torch.full((4, 256, 8192), -128, dtype=torch.int8, device="cuda")
     bt[:, ::2] = 127
-    for kernel in ("pair", "single"):
+    for kernel in ("pair", "single", "multicast"):
         P.set_ozaki_kernel(kernel)
         try:
             r = P.i8_gemm_mod(a, bt)
@@ -102,13 +102,13 @@ def test_kernels_bitwise_on_emulated_products():
     a = torch.from_numpy(rng.standard_normal((1500, 1300))).cuda()
     b = torch.from_numpy(rng.standard_normal((1300, 1700))).cuda()
     outs = []
-    for kernel in ("pair", "single"):
+    for kernel in ("pair", "single", "multicast"):
         P.set_ozaki_kernel(kernel)
         try:
             outs.append(_ozaki(a, b))
         finally:
             P.set_ozaki_kernel("auto")
-    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
     with pytest.raises(ValueError):
         P.set_ozaki_kernel("quad")
 

@@ -83,7 +83,7 @@ def main():
         planes = 16 if n == 8192 else 4
         a3 = torch.randint(-128, 128, (planes, n, n), dtype=torch.int8, device="cuda", generator=g)
         b3 = torch.randint(-128, 128, (planes, n, n), dtype=torch.int8, device="cuda", generator=g)
-        for kernel in ("pair", "single"):
+        for kernel in ("pair", "single", "multicast"):
             P.set_ozaki_kernel(kernel)
             r = measure(lambda: P.i8_gemm_mod(a3, b3), 2.0 * n ** 3 * planes)
             res[f"si_i8_gemm_mod_{kernel}_{planes}x{n}"] = r

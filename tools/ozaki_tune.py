@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--once", nargs=3, type=int, default=None)
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--planes", type=int, default=16)
-    ap.add_argument("--kernel", default="pair", choices=["pair", "single"])
+    ap.add_argument("--kernel", default="pair", choices=["pair", "single", "multicast"])
     ap.add_argument("--probe", action="store_true",
                     help="A/B of the default raster against the L2-only probe, alternating")
     args = ap.parse_args()
