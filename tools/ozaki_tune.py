@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--planes", type=int, default=16)
     ap.add_argument("--kernel", default="pair", choices=["pair", "single", "multicast"])
+    ap.add_argument("--groups", type=str, default=None,
+                    help="comma-separated rasterisation groups to sweep (no L2 hints)")
     ap.add_argument("--probe", action="store_true",
                     help="A/B of the default raster against the L2-only probe, alternating")
     args = ap.parse_args()
@@ -39,14 +41,17 @@ def main():
     b = torch.randint(-128, 128, (planes, n, n), dtype=torch.int8, device="cuda", generator=g)
     P.set_ozaki_kernel(args.kernel)
     ops = 2.0 * n ** 3 * planes
+    settings_once = SETTINGS
+    if args.groups:
+        settings_once = [(int(g), 0, 0) for g in args.groups.split(",")]
     if args.once:
-        for s in (SETTINGS if args.once[0] == 0 else [tuple(args.once)]):
+        for s in (settings_once if args.once[0] == 0 else [tuple(args.once)]):
             _lib.call("si_ozaki_tune", *s)
             P.i8_gemm_mod(a, b)
             torch.cuda.synchronize()
         return
     res = {}
-    settings = SETTINGS
+    settings = settings_once
     if args.probe:
         settings = [(16, 0, 0), L2_PROBE, (16, 0, 0), L2_PROBE]
     for i, s in enumerate(settings):
