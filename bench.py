@@ -735,16 +735,21 @@ class Workload:
         else:
             new = P.ns_step(st, d["a"], plan=self.plan8, input_panels=(flags, epoch, npanels),
                             residual_chunks=chunks, estimate_done=g_done)
-        down.wait_event(g_done)
+        interleaved = self.cfg == "c4"  # composite_step: G' and F' final per row block
         with torch.cuda.stream(down):
-            host["out"]["g"].copy_(new.estimate, non_blocking=True)
             new.estimate.record_stream(down)
             new.residual.record_stream(down)
-        if chunks:  # F' row block by row block, while the next blocks are computed
+        if not interleaved:
+            down.wait_event(g_done)
+            with torch.cuda.stream(down):
+                host["out"]["g"].copy_(new.estimate, non_blocking=True)
+        if chunks:  # row block by row block, while the next blocks are computed
             for p, e in enumerate(chunks):
                 down.wait_event(e)
                 with torch.cuda.stream(down):
                     r0, r1 = bounds[p], bounds[p + 1]
+                    if interleaved:
+                        host["out"]["g"][r0:r1].copy_(new.estimate[r0:r1], non_blocking=True)
                     host["out"]["f"][r0:r1].copy_(new.residual[r0:r1], non_blocking=True)
         else:
             f_done = torch.cuda.Event()

@@ -341,9 +341,12 @@ SI_API int si_composite_step_ex(si_handle h, int64_t n, const double* a, const d
  * The DMMA products gate their A-tile / B-slab loads on those flags, so the
  * first product starts while later panels are still copying.  The flags must
  * be raised by work that needs no SM (copy engines, stream memory operations):
- * gated products may occupy every SM while they wait.  f_chunks > 0:
- * F' = I - G'A is produced in f_chunks row blocks, f_chunk_events[k] recorded
- * after block k (one product in the counters). */
+ * gated products may occupy every SM while they wait.  f_chunks > 0: the last
+ * two products, G' = t + r N and F' = I - G'A, are produced in f_chunks row
+ * blocks, interleaved; f_chunk_events[k] is recorded once G' and F' rows of
+ * block k are final, g_done_event after the last G' block (two products in
+ * the counters).  The emulated products wait per row chunk for the first
+ * product's A rows and for whole B / C operands. */
 SI_API int si_composite_step_gated(si_handle h, int64_t n, const double* a, const double* g,
                                    const double* f, const double* precond,
                                    const double* residual, const double* split_matrix,
@@ -454,10 +457,9 @@ SI_API int si_set_ozaki_chunks(si_handle h, int64_t max_rows, int64_t max_cols);
  * multicast the shared B tile.  Results are identical (exact integers). */
 SI_API int si_set_ozaki_kernel(si_handle h, int variant);
 /* Tuning hook of the INT8 kernels (process-wide; measurement tools):
- * rasterisation group in 256-row pair tiles (0 keeps; >= 2^20: a probe in
- * which every tile reads and writes tile (0, 0) of plane 0 -- operands served
- * from L2, results meaningless), L2 policy of the A / B operand loads
- * (0 evict_normal, 1 evict_last, 2 evict_first; -1 keeps). */
+ * rasterisation group in row tiles (0 keeps), L2 policy of the CTA-pair
+ * kernel's A / B operand loads (0 evict_normal, 1 evict_last, 2 evict_first;
+ * -1 keeps). */
 SI_API int si_ozaki_tune(int group_m, int l2_a, int l2_b);
 /* The first n moduli of the emulation. */
 SI_API int si_ozaki_moduli(int n, uint32_t* moduli);

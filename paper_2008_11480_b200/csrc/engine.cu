@@ -105,6 +105,12 @@ struct Ctx::OzSide {
   oz::Side side;
 };
 
+void keep_stable(Ctx& c, const MV& v) {
+  if (c.s != c.root || !v.v.p) return;
+  c.stable.push_back(v.v.p);
+  c.stable_keep.push_back(v);
+}
+
 namespace {
 constexpr size_t kOzSideMaxBytes = (size_t)8 << 30;  // keep sides up to n = 16384 x 16384
 

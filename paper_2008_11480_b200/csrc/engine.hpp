@@ -131,12 +131,17 @@ struct Ctx {
   // output): the emulated products keep their operand scales + residue
   // planes across the call's products (root stream only; released with the call).
   std::vector<const void*> stable;
+  std::vector<MV> stable_keep;  // engine values marked stable (kept alive for the call)
   struct OzSide;
   std::vector<std::shared_ptr<OzSide>> oz_sides;
   Ctx(Handle* hh, cudaStream_t st) : h(hh), root(st), s(st) {}
 };
 
 void check(cudaError_t e, const char* what);
+// Mark an engine value that is never written again in this call as stable (its
+// emulated-product operand images may be kept); it stays allocated until the
+// call ends.  Root context only (no-op on branches).
+void keep_stable(Ctx& c, const MV& v);
 MV view(double* p, int64_t rows, int64_t cols, int64_t ld);
 MV alloc(Ctx& c, int64_t rows, int64_t cols);
 

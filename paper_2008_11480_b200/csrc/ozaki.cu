@@ -360,14 +360,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-constexpr int kL2OnlyProbe = 1 << 20;  // tuning probe: every tile reads tile (0, 0) of plane 0
 
 __device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int& plane, int& tm, int& tn,
                                         int group_m = GROUP_M) {
-  if (group_m >= kL2OnlyProbe) {  // measurement only (si_ozaki_tune): operands stay in L2
-    plane = tm = tn = 0;
-    return;
-  }
   const int per_plane = num_m * num_n;
   plane = t / per_plane;
   const int r = t - plane * per_plane;

@@ -119,6 +119,28 @@ void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, 
     e.wait(c, StepEvents::kG);
     nsp = horner(c, F, G, order_n);
   }
+  if (e.f_chunks > 0 && e.f_chunk && !c.shard) {
+    // G' = t + r ns and F' = I - G' A in row blocks, interleaved: block k of
+    // both is final at event k, so both go device->host while the next block
+    // is computed (ns's operand image is built once: a stable value); two
+    // counted products, as in the reference DAG
+    keep_stable(c, nsp);
+    const int64_t n = Gout.v.rows;
+    const int chunks = e.f_chunks;
+    auto rows = [](const MV& m, int64_t r0, int64_t r1) {
+      return view(m.v.p + r0 * m.v.ld, r1 - r0, m.v.cols, m.v.ld);
+    };
+    for (int k = 0; k < chunks; ++k) {
+      const int64_t r0 = n * k / chunks, r1 = n * (k + 1) / chunks;
+      const MV gr = rows(Gout, r0, r1), tr = rows(t, r0, r1);
+      gemm(c, gr, rows(r, r0, r1), nsp, 1.0, &tr, 1.0);          // rows of t + r ns
+      if (k == chunks - 1 && e.g_done) check(cudaEventRecord(e.g_done, c.s), "cudaEventRecord");
+      gemm(c, rows(Fout, r0, r1), gr, A, -1.0, nullptr, 0.0, 1.0, false, r0);  // rows of I - G'A
+      if (e.f_chunk[k]) check(cudaEventRecord(e.f_chunk[k], c.s), "cudaEventRecord");
+    }
+    c.ctr.mmm -= 2 * (chunks - 1);
+    return;
+  }
   gemm(c, Gout, r, nsp, 1.0, &t, 1.0);  // G = t + r ns
   if (e.g_done) check(cudaEventRecord(e.g_done, c.s), "cudaEventRecord");  // G' may go D2H now
   if (e.f_chunks > 0 && e.f_chunk) {

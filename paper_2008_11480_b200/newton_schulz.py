@@ -248,8 +248,11 @@ def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_
     panel's copy -- the products gate their loads per panel.  The flags must be
     raised by work that needs no SM (copy-engine copies, stream memory
     operations): the gated products may hold every SM while they wait.
-    ``residual_chunks`` (list of ``torch.cuda.Event``): F' is produced in that
-    many row blocks, each event recorded after its block."""
+    ``residual_chunks`` (list of ``torch.cuda.Event``): G' and F' are produced
+    in that many row blocks, interleaved (G' block k, then F' block k), each
+    event recorded once both blocks are final -- both may go device->host
+    while the next blocks are computed; ``estimate_done`` then fires when the
+    last G' block is final."""
     if order_n < 1:
         raise ValueError("order_n must be >= 1")
     a = as_device(a)

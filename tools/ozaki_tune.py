@@ -20,7 +20,6 @@ from int8_yardstick import Clocks, timed  # noqa: E402
 
 SETTINGS = [(16, 0, 0), (8, 0, 0), (4, 0, 0), (32, 0, 0), (16, 1, 2), (8, 1, 2), (4, 1, 2),
             (8, 1, 0), (8, 0, 2)]
-L2_PROBE = (1 << 20, 0, 0)  # every tile on the same operands: no DRAM traffic (timing probe)
 
 
 def main():
@@ -31,8 +30,6 @@ def main():
     ap.add_argument("--kernel", default="pair", choices=["pair", "single", "multicast"])
     ap.add_argument("--groups", type=str, default=None,
                     help="comma-separated rasterisation groups to sweep (no L2 hints)")
-    ap.add_argument("--probe", action="store_true",
-                    help="A/B of the default raster against the L2-only probe, alternating")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     n, planes = args.n, args.planes
@@ -52,8 +49,6 @@ def main():
         return
     res = {}
     settings = settings_once
-    if args.probe:
-        settings = [(16, 0, 0), L2_PROBE, (16, 0, 0), L2_PROBE]
     for i, s in enumerate(settings):
         _lib.call("si_ozaki_tune", *s)
         fn = lambda: P.i8_gemm_mod(a, b)  # noqa: E731
@@ -67,7 +62,7 @@ def main():
         res[f"{i}:{s}"] = {"burst_tops": ops / burst / 1e9, "sustained_tops": ops / sus / 1e9,
                        "burst_ms": burst, "sustained_ms": sus, "clocks": c}
         print(s, json.dumps(res[f"{i}:{s}"]), flush=True)
-    json.dump(res, open(f"gpurun_out/ozaki_tune_{args.kernel}{'_probe' if args.probe else ''}.json",
+    json.dump(res, open(f"gpurun_out/ozaki_tune_{args.kernel}.json",
                         "w"), indent=1)
 
 
