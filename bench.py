@@ -1413,7 +1413,8 @@ def run_ours(args):
     if not args.no_e2e and args.config in ("c4", "c3") and w.sharded is None and not args.hoist:
         host = w.pinned_inputs()
         h2d = d2h = 0
-        ksteps = max(1, min(args.steps, 3))
+        # at least ~1 s of e2e steps (3 for c4; ~100 for c3), at most --steps
+        ksteps = max(1, min(args.steps, max(3, int(1.0 / max(step_s, 1e-3)))))
         w.e2e_step(host)  # warm
         torch.cuda.synchronize()
         f0 = torch.cuda.Event(enable_timing=True)

@@ -210,8 +210,13 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
       if (!pw) pw = c.gate_of(B.v.p);
       if (C && C->v.p != B.v.p) c.gate_stream(C->v.p);  // C == B: its panels gate the k-loop
     } else {
-      if (use_oz && A.v.p != B.v.p && (!C || C->v.p != A.v.p) && A.v.rows == d.rows)
+      // (only for panels of >= 2048 rows: smaller row chunks cost more in
+      // partial INT8 waves than the copy they hide)
+      if (use_oz && A.v.p != B.v.p && (!C || C->v.p != A.v.p) && A.v.rows == d.rows) {
         oz_rows = c.gate_of(A.v.p);
+        for (int p = 0; oz_rows && p < oz_rows->npanels; ++p)
+          if (oz_rows->bounds[p + 1] - oz_rows->bounds[p] < 2048) oz_rows = nullptr;
+      }
       if (!oz_rows) c.gate_stream(A.v.p);
       c.gate_stream(B.v.p);
       if (C) c.gate_stream(C->v.p);

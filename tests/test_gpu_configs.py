@@ -150,14 +150,16 @@ def test_composite_step_with_inputs_in_flight():
         P.composite_step(st, sp.matrix, sp, spec, 2, inputs_ready={"bogus": done})
 
 
-@pytest.mark.parametrize("backend,concurrent", [("dmma", False), ("dmma", True),
-                                                ("ozaki", False), ("ozaki", True)])
-def test_composite_step_with_inputs_in_row_panels(backend, concurrent):
+@pytest.mark.parametrize("backend,concurrent,n,npanels", [
+    ("dmma", False, 768, 6), ("dmma", True, 768, 6), ("ozaki", False, 768, 6),
+    ("ozaki", True, 768, 6), ("ozaki", False, 4096, 2)])
+def test_composite_step_with_inputs_in_row_panels(backend, concurrent, n, npanels):
     """Inputs copied host->device panel by panel (out of order, a delaying copy
     first) with flags; the DMMA products gate their loads per panel (the
     emulated products wait per row chunk of A and for whole B / C operands) and
     F' comes out in row blocks: bitwise the resident-input result, same product
-    count."""
+    count.  n=4096 with 2048-row panels: the emulated first product runs in row
+    chunks behind the copy of its left operand."""
     import paper_2008_11480_b200 as P
     from paper_2008_11480_b200 import _lib, configs
 
@@ -165,13 +167,12 @@ def test_composite_step_with_inputs_in_row_panels(backend, concurrent):
         # every product emulated, the F' row blocks (192 rows) included
         P.set_gemm_backend("ozaki", 16, 128)
     try:
-        _inputs_in_row_panels(P, _lib, configs, concurrent)
+        _inputs_in_row_panels(P, _lib, configs, concurrent, n, npanels)
     finally:
         P.set_gemm_backend("dmma", 16, 1024)
 
 
-def _inputs_in_row_panels(P, _lib, configs, concurrent):
-    n, npanels = 768, 6
+def _inputs_in_row_panels(P, _lib, configs, concurrent, n, npanels):
     a, _ = configs.c4_householder(n=n, rhs=1)
     sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False)
     spec = P.CompositeSpec((2, 3, 4, 5))
