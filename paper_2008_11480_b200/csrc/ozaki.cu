@@ -361,6 +361,46 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 }
 
 
+// Epilogue of one accumulator: this thread's TMEM lane holds row `row` of a
+// 256-column tile (from column `taddr`); the int32 sums are reduced exactly
+// mod m (u = v + 2^30 < 2^31, q = floor(u magic / 2^39)) and stored as one
+// byte per entry into row `row`, columns col0.. of the plane.
+__device__ __forceinline__ void store_mod_row(uint32_t taddr, uint8_t* __restrict__ plane_base,
+                                              int row, int col0, int M, int N, unsigned m,
+                                              unsigned magic, unsigned off) {
+  uint8_t* rp = plane_base + (int64_t)row * N + col0;
+  const bool vec = ((N & 15) == 0);
+#pragma unroll 1
+  for (int c = 0; c < 256 / 32; ++c) {
+    uint32_t v[32];
+    tmem_ld32(taddr + (uint32_t)(c * 32), v);
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      uint32_t b[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t u = v[i + j] + (1u << 30);
+        const uint32_t qq = __umulhi(u, magic) >> 7;
+        uint32_t r = u - qq * m;
+        r = r >= off ? r - off : r + m - off;
+        b[j] = r;
+      }
+      w[i >> 2] = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+    }
+    const int cc = col0 + c * 32;
+    if (row < M && cc < N) {
+      if (vec && cc + 32 <= N) {
+        uint4* dst = reinterpret_cast<uint4*>(rp + c * 32);
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      } else {
+        for (int i = 0; i < 32 && cc + i < N; ++i) rp[c * 32 + i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int& plane, int& tm, int& tn,
                                         int group_m = GROUP_M) {
   const int per_plane = num_m * num_n;
@@ -489,37 +529,8 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       tc_fence_after();
       const int row = tm * GBM + q * 32 + lane;
       const int col0 = tn * GBN;
-      uint8_t* rp = R + (int64_t)plane * M * N + (int64_t)row * N + col0;
-      const bool vec = ((N & 15) == 0);
-#pragma unroll 1
-      for (int c = 0; c < GBN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * GBN + c * 32), v);
-        uint32_t w[8];
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          uint32_t b[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t u = v[i + j] + (1u << 30);
-            const uint32_t qq = __umulhi(u, magic) >> 7;
-            uint32_t r = u - qq * m;
-            r = r >= off ? r - off : r + m - off;
-            b[j] = r;
-          }
-          w[i >> 2] = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
-        }
-        const int cc = col0 + c * 32;
-        if (row < M && cc < N) {
-          if (vec && cc + 32 <= N) {
-            uint4* dst = reinterpret_cast<uint4*>(rp + c * 32);
-            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-          } else {
-            for (int i = 0; i < 32 && cc + i < N; ++i) rp[c * 32 + i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
-          }
-        }
-      }
+      store_mod_row(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * GBN),
+                    R + (int64_t)plane * M * N, row, col0, M, N, m, magic, off);
       tc_fence_before();
       mbar_arrive(tempty_bar(acc));
       if (++acc == 2) {
@@ -730,37 +741,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GTHREADS, 1)
       tc_fence_after();
       const int row = tm * PBM + (int)rank * (PBM / 2) + q * 32 + lane;
       const int col0 = tn * PBN;
-      uint8_t* rp = R + (int64_t)plane * M * N + (int64_t)row * N + col0;
-      const bool vec = ((N & 15) == 0);
-#pragma unroll 1
-      for (int c = 0; c < PBN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * PBN + c * 32), v);
-        uint32_t w[8];
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          uint32_t b[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t u = v[i + j] + (1u << 30);
-            const uint32_t qq = __umulhi(u, magic) >> 7;
-            uint32_t r = u - qq * m;
-            r = r >= off ? r - off : r + m - off;
-            b[j] = r;
-          }
-          w[i >> 2] = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
-        }
-        const int cc = col0 + c * 32;
-        if (row < M && cc < N) {
-          if (vec && cc + 32 <= N) {
-            uint4* dst = reinterpret_cast<uint4*>(rp + c * 32);
-            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-          } else {
-            for (int i = 0; i < 32 && cc + i < N; ++i) rp[c * 32 + i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
-          }
-        }
-      }
+      store_mod_row(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * PBN),
+                    R + (int64_t)plane * M * N, row, col0, M, N, m, magic, off);
       tc_fence_before();
       mbar_arrive_cluster(leader_addr(tempty_bar(acc)));
       if (++acc == 2) {
@@ -933,37 +915,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GTHREADS, 1)
       tc_fence_after();
       const int row = tm * 2 * GBM + rank * GBM + q * 32 + lane;
       const int col0 = tn * GBN;
-      uint8_t* rp = R + (int64_t)plane * M * N + (int64_t)row * N + col0;
-      const bool vec = ((N & 15) == 0);
-#pragma unroll 1
-      for (int c = 0; c < GBN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * GBN + c * 32), v);
-        uint32_t w[8];
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          uint32_t b[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t u = v[i + j] + (1u << 30);
-            const uint32_t qq = __umulhi(u, magic) >> 7;
-            uint32_t r = u - qq * m;
-            r = r >= off ? r - off : r + m - off;
-            b[j] = r;
-          }
-          w[i >> 2] = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
-        }
-        const int cc = col0 + c * 32;
-        if (row < M && cc < N) {
-          if (vec && cc + 32 <= N) {
-            uint4* dst = reinterpret_cast<uint4*>(rp + c * 32);
-            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-          } else {
-            for (int i = 0; i < 32 && cc + i < N; ++i) rp[c * 32 + i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
-          }
-        }
-      }
+      store_mod_row(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * GBN),
+                    R + (int64_t)plane * M * N, row, col0, M, N, m, magic, off);
       tc_fence_before();
       mbar_arrive(tempty_bar(acc));
       if (++acc == 2) {
