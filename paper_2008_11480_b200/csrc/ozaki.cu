@@ -1169,8 +1169,8 @@ const Consts& consts() {
 }
 
 // rasterisation group and L2 policies of the pair kernel (tuning hook: si_ozaki_tune)
-int g_pair_group_m = GROUP_M, g_pair_l2a = 0, g_pair_l2b = 0;
-int g_single_group_m = GROUP_M;
+std::atomic<int> g_pair_group_m{GROUP_M}, g_pair_l2a{0}, g_pair_l2b{0};
+std::atomic<int> g_single_group_m{GROUP_M};
 
 int num_sms() {
   int dev = 0, n = 0;
@@ -1204,7 +1204,10 @@ inline int64_t kpad(int64_t K) { return (K + GBK - 1) / GBK * GBK; }
 unsigned modulus(int l) { return kmod(l); }
 
 void tune_pair(int group_m, int l2a, int l2b) {
-  if (group_m > 0) g_pair_group_m = g_single_group_m = group_m;
+  if (group_m > 0) {
+    g_pair_group_m = group_m;
+    g_single_group_m = group_m;
+  }
   if (l2a >= 0 && l2a <= 2) g_pair_l2a = l2a;
   if (l2b >= 0 && l2b <= 2) g_pair_l2b = l2b;
 }
@@ -1263,18 +1266,19 @@ cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, in
     const int64_t tiles = ((M + PBM - 1) / PBM) * ((N + PBN - 1) / PBN) * nplanes;
     const int grid = (int)std::min<int64_t>(2 * tiles, sms & ~1);
     i8_gemm_mod_pair_kernel<<<grid, GTHREADS, PSMEM, s>>>(ta, tb, R, (int)M, (int)N, (int)Kp,
-                                                          nplanes, consts().mt, g_pair_group_m,
-                                                          g_pair_l2a, g_pair_l2b);
+                                                          nplanes, consts().mt, g_pair_group_m.load(),
+                                                          g_pair_l2a.load(), g_pair_l2b.load());
   } else if (mc) {
     const int64_t tiles = ((M + 2 * GBM - 1) / (2 * GBM)) * ((N + GBN - 1) / GBN) * nplanes;
     const int grid = (int)std::min<int64_t>(2 * tiles, sms & ~1);
     i8_gemm_mod_mc_kernel<<<grid, GTHREADS, GSMEM, s>>>(ta, tb, R, (int)M, (int)N, (int)Kp,
-                                                        nplanes, consts().mt, g_single_group_m);
+                                                        nplanes, consts().mt,
+                                                        g_single_group_m.load());
   } else {
     const int64_t tiles = ((M + GBM - 1) / GBM) * ((N + GBN - 1) / GBN) * nplanes;
     const int grid = (int)(tiles < sms ? tiles : sms);
     i8_gemm_mod_kernel<<<grid, GTHREADS, GSMEM, s>>>(ta, tb, R, (int)M, (int)N, (int)Kp, nplanes,
-                                                     consts().mt, g_single_group_m);
+                                                     consts().mt, g_single_group_m.load());
   }
   return cudaGetLastError();
 }

@@ -387,3 +387,35 @@ def test_step_operand_images_kept_bitwise():
     assert torch.equal(serial.residual, conc.residual)
     assert serial.ctr.mmm == conc.ctr.mmm
     assert n_serial < n_conc, (n_serial, n_conc)
+
+
+def test_strided_operands_through_the_abi():
+    """Operands and outputs with leading dimensions larger than their widths
+    (sub-blocks of bigger buffers), odd K: the emulated si_gemm_ex equals the
+    same product on contiguous copies, bitwise, and meets the accuracy bound."""
+    import ctypes
+
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import _lib
+
+    rng = np.random.default_rng(41)
+    m, k, n = 700, 1031, 900
+    big_a = torch.from_numpy(rng.standard_normal((m, k + 77))).cuda()
+    big_b = torch.from_numpy(rng.standard_normal((k, n + 33))).cuda()
+    big_c = torch.from_numpy(rng.standard_normal((m, n + 5))).cuda()
+    a, b, c = big_a[:, 3:3 + k], big_b[:, :n], big_c[:, 2:2 + n]
+    P.set_gemm_backend("ozaki", 16, 128)
+    ctr = (ctypes.c_int64 * 2)()
+    big_d = torch.full((m, n + 11), 7.0, dtype=torch.float64, device="cuda")
+    d = big_d[:, 4:4 + n]
+    _lib.call("si_gemm_ex", _lib.handle(), m, n, k, 1.0, a.data_ptr(), a.stride(0), b.data_ptr(),
+              b.stride(0), 1.0, c.data_ptr(), c.stride(0), 0.0, 0, d.data_ptr(), d.stride(0), 0,
+              ctr, _lib.stream_ptr())
+    ac, bc, cc = a.contiguous(), b.contiguous(), c.contiguous()
+    dc = torch.empty(m, n, dtype=torch.float64, device="cuda")
+    _lib.call("si_gemm_ex", _lib.handle(), m, n, k, 1.0, ac.data_ptr(), k, bc.data_ptr(), n, 1.0,
+              cc.data_ptr(), n, 0.0, 0, dc.data_ptr(), n, 0, ctr, _lib.stream_ptr())
+    assert torch.equal(d, dc)
+    assert bool((big_d[:, :4] == 7.0).all()) and bool((big_d[:, 4 + n:] == 7.0).all())
+    ref = a.cpu().numpy().astype(np.longdouble) @ b.cpu().numpy() + c.cpu().numpy()
+    assert np.abs(d.cpu().numpy() - ref).max() <= 1e-13 * np.abs(ref).max()
