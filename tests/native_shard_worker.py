@@ -23,6 +23,9 @@ def main():
     from paper_2008_11480_b200 import configs
     from paper_2008_11480_b200 import native_sharded as NS
 
+    if len(sys.argv) > 6 and sys.argv[6] == "ozaki":
+        P.set_gemm_backend("ozaki", 16, 128)
+
     a_np, b_np = configs.c4_householder(n=n, rhs=3)
     a = P.as_device(a_np)
     b = P.as_device(b_np)

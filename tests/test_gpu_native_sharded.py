@@ -78,8 +78,14 @@ def test_nccl_world_one_bitwise():
     comm.close()
 
 
+@pytest.mark.parametrize("backend", ["dmma", "ozaki"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_processes_share_gpu_host_exchange(world, tmp_path):
+def test_processes_share_gpu_host_exchange(world, backend, tmp_path):
+    """Block-row steps through si_sharded_* in `world` processes: bitwise the
+    single-GPU steps -- also with every product emulated on the INT8 tensor
+    cores (row splits change no bit: each row's scale and the integer
+    products are its own)."""
+    import paper_2008_11480_b200 as P
     from conftest import release_gpu_memory
 
     release_gpu_memory()
@@ -89,7 +95,7 @@ def test_processes_share_gpu_host_exchange(world, tmp_path):
         port = str(s.getsockname()[1])
     worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "native_shard_worker.py")
     procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), port, str(tmp_path),
-                               str(n)]) for r in range(world)]
+                               str(n), backend]) for r in range(world)]
     try:
         codes = [p.wait(timeout=300) for p in procs]
     finally:
@@ -97,7 +103,8 @@ def test_processes_share_gpu_host_exchange(world, tmp_path):
             if p.poll() is None:
                 p.kill()
     assert codes == [0] * world
-    ref = _single_gpu(n)
+    with P.gemm_backend(backend, moduli=16, min_dim=128):
+        ref = _single_gpu(n)
     from paper_2008_11480_b200.sharded import row_splits
 
     parts = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
