@@ -183,53 +183,63 @@ __global__ void col_absmax_kernel(const double* __restrict__ B, int64_t ldb, int
 // ------------------------------------------------------------ residues --
 // residues of 16 consecutive integers modulo kmod(L), kmod(L+1), ... (L < nmod),
 // one 16-byte store into each plane
-template <int L>
-__device__ __forceinline__ void emit16(int nmod, const Chunks (&x)[16], int8_t* dst, int64_t plane) {
+template <int L, int E>
+__device__ __forceinline__ void emit(int nmod, const Chunks (&x)[E], int8_t* dst, int64_t plane) {
+  static_assert(E == 8 || E == 16, "8 or 16 residues per store");
   if constexpr (L < kMaxModuli) {
     if (L >= nmod) return;
-    uint32_t r[16];
+    uint32_t r[E];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) r[j] = res_shifted<L>(x[j]);
-    uint4 w;
-    w.x = pack_sym4<L>(r[0], r[1], r[2], r[3]);
-    w.y = pack_sym4<L>(r[4], r[5], r[6], r[7]);
-    w.z = pack_sym4<L>(r[8], r[9], r[10], r[11]);
-    w.w = pack_sym4<L>(r[12], r[13], r[14], r[15]);
-    *reinterpret_cast<uint4*>(dst + L * plane) = w;
-    emit16<L + 1>(nmod, x, dst, plane);
+    for (int j = 0; j < E; ++j) r[j] = res_shifted<L>(x[j]);
+    if constexpr (E == 16) {
+      uint4 w;
+      w.x = pack_sym4<L>(r[0], r[1], r[2], r[3]);
+      w.y = pack_sym4<L>(r[4], r[5], r[6], r[7]);
+      w.z = pack_sym4<L>(r[8], r[9], r[10], r[11]);
+      w.w = pack_sym4<L>(r[12], r[13], r[14], r[15]);
+      *reinterpret_cast<uint4*>(dst + L * plane) = w;
+    } else {
+      uint2 w;
+      w.x = pack_sym4<L>(r[0], r[1], r[2], r[3]);
+      w.y = pack_sym4<L>(r[4], r[5], r[6], r[7]);
+      *reinterpret_cast<uint2*>(dst + L * plane) = w;
+    }
+    emit<L + 1, E>(nmod, x, dst, plane);
   }
 }
 
 // A (M x K, row-major) -> nmod planes of M x Kp int8 (columns >= K zero):
-// one thread per 16 consecutive k of a row, one 16-byte store per plane.
+// one thread per RE consecutive k of a row, one RE-byte store per plane (8:
+// fewer registers per thread, twice the resident warps of 16)
+constexpr int RE = 8;
 __global__ void residues_rows_kernel(const double* __restrict__ A, int64_t lda, int M, int K,
                                      int Kp, const unsigned long long* __restrict__ rmax, int p,
                                      int nmod, int8_t* __restrict__ out) {
-  const int chunks = Kp >> 4;
+  const int chunks = Kp / RE;
   const int64_t total = (int64_t)M * chunks;
   const int64_t plane = (int64_t)M * Kp;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int row = (int)(idx / chunks);
-    const int k0 = (int)(idx - (int64_t)row * chunks) << 4;
+    const int k0 = (int)(idx - (int64_t)row * chunks) * RE;
     const int sh = shift_of(rmax[row], p);
-    Chunks x[16];
+    Chunks x[RE];
     const double* src = A + (int64_t)row * lda + k0;
     if (sh == kNonFinite) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) x[j] = chunks_of(0);
-    } else if (k0 + 16 <= K && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)) {
+      for (int j = 0; j < RE; ++j) x[j] = chunks_of(0);
+    } else if (k0 + RE <= K && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)) {
 #pragma unroll
-      for (int j = 0; j < 16; j += 2) {
+      for (int j = 0; j < RE; j += 2) {
         const double2 v = *reinterpret_cast<const double2*>(src + j);
         x[j] = chunks_of(int_image(v.x, sh));
         x[j + 1] = chunks_of(int_image(v.y, sh));
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) x[j] = chunks_of(k0 + j < K ? int_image(src[j], sh) : 0);
+      for (int j = 0; j < RE; ++j) x[j] = chunks_of(k0 + j < K ? int_image(src[j], sh) : 0);
     }
-    emit16<0>(nmod, x, out + (int64_t)row * Kp + k0, plane);
+    emit<0, RE>(nmod, x, out + (int64_t)row * Kp + k0, plane);
   }
 }
 
@@ -261,7 +271,7 @@ __global__ void __launch_bounds__(256) residues_cols_kernel(
   Chunks x[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) x[i] = chunks_of(xs[kc + i][jl]);
-  emit16<0>(nmod, x, out + (int64_t)(j0 + jl) * Kp + k0 + kc, (int64_t)N * Kp);
+  emit<0, 16>(nmod, x, out + (int64_t)(j0 + jl) * Kp + k0 + kc, (int64_t)N * Kp);
 }
 
 // -------------------------------------------------- INT8 tensor-core GEMM --
@@ -1331,7 +1341,7 @@ cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, i
       row_absmax_kernel<<<(int)std::min<int64_t>((mc + 7) / 8, 16 * sms), 256, 0, s>>>(
           ap, A.ld, (int)mc, (int)K, rmax);
       ++n;
-      const int64_t thr = mc * (Kp / 16);
+      const int64_t thr = mc * (Kp / RE);
       const int blocks = (int)std::min<int64_t>((thr + 255) / 256, 64 * sms);
       residues_rows_kernel<<<blocks, 256, 0, s>>>(ap, A.ld, (int)mc, (int)K, (int)Kp, rmax, pa,
                                                    nmod, ares);
