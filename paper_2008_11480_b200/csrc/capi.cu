@@ -78,17 +78,19 @@ struct Call {
 
 // A step's n x n inputs that no output of the call overlaps: the emulated
 // products may keep their operand images across the call (engine.cu oz_side).
+// (`out_rows`: rows of each output, e.g. a rank's row block in a sharded call)
 void mark_stable(Ctx& c, int64_t n, std::initializer_list<const double*> ins,
-                 std::initializer_list<const double*> outs) {
+                 std::initializer_list<const double*> outs, int64_t out_rows = -1) {
   const size_t bytes = (size_t)n * (size_t)n * sizeof(double);
+  const size_t obytes = (size_t)(out_rows < 0 ? n : out_rows) * (size_t)n * sizeof(double);
   for (const double* in : ins) {
     const char* a = reinterpret_cast<const char*>(in);
     bool clash = false;
     for (const double* out : outs) {
       const char* b = reinterpret_cast<const char*>(out);
-      if (a < b + bytes && b < a + bytes) clash = true;
+      if (a < b + obytes && b < a + bytes) clash = true;
     }
-    if (!clash) c.stable.push_back(in);
+    if (!clash) c.stable.push_back({a, bytes});
   }
 }
 
@@ -941,6 +943,7 @@ int si_sharded_ns_step(si_handle h, si_comm comm, int64_t n, const double* a, co
     need(h && a && g_rows && f_rows && g_out_rows && f_out_rows, "null pointer");
     PlanPtr pl = opt_plan(plan, plan_len, consts, nconsts);
     ShardCall sc(h, comm, n, stream, counters);
+    mark_stable(sc.call.c, n, {a}, {g_out_rows, f_out_rows}, sc.rows());
     ns_step(sc.call.c, sq(a, n), sc.loc(g_rows, n), sc.loc(f_rows, n), order, pl.get(),
             sc.loc(g_out_rows, n), sc.loc(f_out_rows, n));
   });
@@ -971,6 +974,9 @@ int si_sharded_composite_step(si_handle h, si_comm comm, int64_t n, const double
       }
     }
     ShardCall sc(h, comm, n, stream, counters);
+    // the replicated inputs (and their row blocks) may keep their operand images
+    mark_stable(sc.call.c, n, {a, precond, residual, split_matrix}, {g_out_rows, f_out_rows},
+                sc.rows());
     // serial order only: every rank must issue its exchanges in the same order
     composite_step(sc.call.c, sq(a, n), sc.loc(g_rows, n), sc.loc(f_rows, n), sq(precond, n),
                    sq(residual, n), sq(split_matrix, n), rv, pv, order_n, false,
@@ -995,6 +1001,8 @@ int si_sharded_richardson_recursive_step(
     PlanPtr pl = opt_plan(factor_plan, plan_len, consts, nconsts);
     if (pl) need(plan_order_of(*pl) == order, "factor plan order != iteration order");
     ShardCall sc(h, comm, n, stream, counters);
+    mark_stable(sc.call.c, n, {a}, {g_out_rows, f_out_rows, l_out_rows, r_out_rows},
+                sc.rows());
     MV om = omega_rows ? sc.loc(omega_rows, n) : MV{};
     MV nsp = ns_rows ? sc.loc(ns_rows, n) : MV{};
     richardson_recursive_step(sc.call.c, sq(a, n), rect(b, n, nrhs), rect(theta, n, nrhs),

@@ -107,7 +107,8 @@ struct Ctx::OzSide {
 
 void keep_stable(Ctx& c, const MV& v) {
   if (c.s != c.root || !v.v.p) return;
-  c.stable.push_back(v.v.p);
+  const size_t bytes = sizeof(double) * (size_t)(v.v.rows > 0 ? (v.v.rows - 1) * v.v.ld + v.v.cols : 0);
+  c.stable.push_back({reinterpret_cast<const char*>(v.v.p), bytes});
   c.stable_keep.push_back(v);
 }
 
@@ -118,9 +119,14 @@ constexpr size_t kOzSideMaxBytes = (size_t)8 << 30;  // keep sides up to n = 163
 // of B) of an emulated product with inner dimension k, or nullptr when `m` is
 // not a stable input of this call (or its side does not fit the budget).
 oz::Side* oz_side(Ctx& c, const Mat& m, bool b_side, int64_t k, int nmod) {
-  if (c.s != c.root || c.stable.empty()) return nullptr;
-  if (std::find(c.stable.begin(), c.stable.end(), (const void*)m.p) == c.stable.end())
-    return nullptr;
+  if (c.s != c.root || c.stable.empty() || m.rows <= 0) return nullptr;
+  // the whole matrix (rows x cols at ld) inside one stable range
+  const char* lo = reinterpret_cast<const char*>(m.p);
+  const char* hi = lo + sizeof(double) * (size_t)((m.rows - 1) * m.ld + m.cols);
+  bool inside = false;
+  for (const auto& r : c.stable)
+    if (lo >= r.base && hi <= r.base + r.bytes) inside = true;
+  if (!inside) return nullptr;
   for (auto& e : c.oz_sides)
     if (e->ptr == m.p && e->rows == m.rows && e->cols == m.cols && e->ld == m.ld && e->k == k &&
         e->nmod == nmod && e->b_side == b_side)

@@ -130,7 +130,11 @@ struct Ctx {
   // Caller buffers this call only reads (a step's inputs, not aliased by an
   // output): the emulated products keep their operand scales + residue
   // planes across the call's products (root stream only; released with the call).
-  std::vector<const void*> stable;
+  struct Range {
+    const char* base;
+    size_t bytes;
+  };
+  std::vector<Range> stable;    // a matrix inside one of these ranges may keep its images
   std::vector<MV> stable_keep;  // engine values marked stable (kept alive for the call)
   struct OzSide;
   std::vector<std::shared_ptr<OzSide>> oz_sides;
