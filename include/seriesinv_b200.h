@@ -461,6 +461,8 @@ SI_API int si_set_ozaki_kernel(si_handle h, int variant);
  * kernel's A / B operand loads (0 evict_normal, 1 evict_last, 2 evict_first;
  * -1 keeps). */
 SI_API int si_ozaki_tune(int group_m, int l2_a, int l2_b);
+/* Tuning hook: shared-memory ring depth of the CTA-pair kernel (3..6). */
+SI_API int si_ozaki_tune_stages(int stages);
 /* The first n moduli of the emulation. */
 SI_API int si_ozaki_moduli(int n, uint32_t* moduli);
 /* The INT8 tensor-core kernel alone (test hook): r[l] = (a[l] @ bt[l]^T) mod

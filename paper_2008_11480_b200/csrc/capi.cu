@@ -1276,6 +1276,13 @@ int si_ozaki_tune(int group_m, int l2_a, int l2_b) {
   });
 }
 
+int si_ozaki_tune_stages(int stages) {
+  return guard([&] {
+    need(stages >= 3 && stages <= 6, "stages out of range");
+    oz::tune_pair_stages(stages);
+  });
+}
+
 int si_ozaki_moduli(int n, uint32_t* moduli) {
   return guard([&] {
     need(moduli != nullptr && n >= 1 && n <= oz::kMaxModuli, "bad arguments");

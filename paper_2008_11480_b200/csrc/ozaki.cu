@@ -570,11 +570,10 @@ __global__ void __launch_bounds__(GTHREADS, 1)
 // epilogue drains its own TMEM rows and arrives on the leader's TMEM-empty
 // barrier.
 constexpr int PBM = 256, PBN = 256;  // pair tile (each CTA: 128 rows of A, 128 rows of Bt)
-constexpr int PSTAGES = 6;
 constexpr int PA_BYTES = (PBM / 2) * GBK;  // 16 KB
 constexpr int PB_BYTES = (PBN / 2) * GBK;  // 16 KB
 constexpr int PSTAGE_BYTES = PA_BYTES + PB_BYTES;
-constexpr int PSMEM = PSTAGES * PSTAGE_BYTES + 1024 + 256;
+constexpr int psmem(int stages) { return stages * PSTAGE_BYTES + 1024 + 256; }
 constexpr uint32_t kIdescPair = (2u << 4) | (1u << 7) | (1u << 10) |
                                 ((uint32_t)(PBN >> 3) << 17) | ((uint32_t)(PBM >> 4) << 24);
 
@@ -631,6 +630,7 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+template <int PSTAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GTHREADS, 1)
     i8_gemm_mod_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                             const __grid_constant__ CUtensorMap tmB, uint8_t* __restrict__ R,
@@ -1179,8 +1179,9 @@ const Consts& consts() {
 }
 
 // rasterisation group and L2 policies of the pair kernel (tuning hook: si_ozaki_tune)
-std::atomic<int> g_pair_group_m{GROUP_M}, g_pair_l2a{0}, g_pair_l2b{0};
+std::atomic<int> g_pair_group_m{8}, g_pair_l2a{0}, g_pair_l2b{0};  // pair: 2048-row groups
 std::atomic<int> g_single_group_m{GROUP_M};
+std::atomic<int> g_pair_stages{4};  // smem ring depth of the pair kernel (3..6; tuning hook)
 
 int num_sms() {
   int dev = 0, n = 0;
@@ -1197,8 +1198,17 @@ cudaError_t set_gemm_attr() {
   cudaError_t e =
       cudaFuncSetAttribute(i8_gemm_mod_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GSMEM);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(i8_gemm_mod_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             PSMEM);
+    e = cudaFuncSetAttribute(i8_gemm_mod_pair_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             psmem(3));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(i8_gemm_mod_pair_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             psmem(4));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(i8_gemm_mod_pair_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             psmem(5));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(i8_gemm_mod_pair_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             psmem(6));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(i8_gemm_mod_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              GSMEM);
@@ -1212,6 +1222,10 @@ inline int64_t kpad(int64_t K) { return (K + GBK - 1) / GBK * GBK; }
 }  // namespace
 
 unsigned modulus(int l) { return kmod(l); }
+
+void tune_pair_stages(int stages) {
+  if (stages >= 3 && stages <= 6) g_pair_stages = stages;
+}
 
 void tune_pair(int group_m, int l2a, int l2b) {
   if (group_m > 0) {
@@ -1275,9 +1289,13 @@ cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, in
   if (pair) {
     const int64_t tiles = ((M + PBM - 1) / PBM) * ((N + PBN - 1) / PBN) * nplanes;
     const int grid = (int)std::min<int64_t>(2 * tiles, sms & ~1);
-    i8_gemm_mod_pair_kernel<<<grid, GTHREADS, PSMEM, s>>>(ta, tb, R, (int)M, (int)N, (int)Kp,
-                                                          nplanes, consts().mt, g_pair_group_m.load(),
-                                                          g_pair_l2a.load(), g_pair_l2b.load());
+    const int st = g_pair_stages.load();
+    auto kern = st == 3 ? i8_gemm_mod_pair_kernel<3>
+                : st == 5 ? i8_gemm_mod_pair_kernel<5>
+                : st == 6 ? i8_gemm_mod_pair_kernel<6> : i8_gemm_mod_pair_kernel<4>;
+    kern<<<grid, GTHREADS, psmem(st == 3 || st == 5 || st == 6 ? st : 4), s>>>(
+        ta, tb, R, (int)M, (int)N, (int)Kp, nplanes, consts().mt, g_pair_group_m.load(),
+        g_pair_l2a.load(), g_pair_l2b.load());
   } else if (mc) {
     const int64_t tiles = ((M + 2 * GBM - 1) / (2 * GBM)) * ((N + GBN - 1) / GBN) * nplanes;
     const int grid = (int)std::min<int64_t>(2 * tiles, sms & ~1);

@@ -85,6 +85,7 @@ cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, in
 // (pair-tile rows per group) and the L2 policies of the A / B operand loads
 // (0 evict_normal, 1 evict_last, 2 evict_first); negative / zero keeps a value.
 void tune_pair(int group_m, int l2a, int l2b);
+void tune_pair_stages(int stages);
 
 // Moduli (pairwise coprime, <= 256) in the order the planes use them.
 unsigned modulus(int l);

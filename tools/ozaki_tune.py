@@ -27,7 +27,8 @@ def main():
     ap.add_argument("--once", nargs=3, type=int, default=None)
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--planes", type=int, default=16)
-    ap.add_argument("--kernel", default="pair", choices=["pair", "single", "multicast"])
+    ap.add_argument("--kernel", default="pair")
+    ap.add_argument("--stages", type=int, default=0, help="pair kernel ring depth (3..6)")
     ap.add_argument("--groups", type=str, default=None,
                     help="comma-separated rasterisation groups to sweep (no L2 hints)")
     args = ap.parse_args()
@@ -37,6 +38,8 @@ def main():
     a = torch.randint(-128, 128, (planes, n, n), dtype=torch.int8, device="cuda", generator=g)
     b = torch.randint(-128, 128, (planes, n, n), dtype=torch.int8, device="cuda", generator=g)
     P.set_ozaki_kernel(args.kernel)
+    if args.stages:
+        _lib.call("si_ozaki_tune_stages", args.stages)
     ops = 2.0 * n ** 3 * planes
     settings_once = SETTINGS
     if args.groups:
