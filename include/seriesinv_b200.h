@@ -433,12 +433,15 @@ SI_API int si_dmma_peak(si_handle h, int iters, double* tflops);
  *                     power-of-two-scaled integer images of A and B, one INT8
  *                     tcgen05 GEMM per modulus (nmoduli of 256, 255, 253, ...),
  *                     recombined by the Chinese remainder theorem; used for
- *                     products whose dimensions are all >= min_dim (and K <=
- *                     32768; smaller or gated products stay on DMMA).
+ *                     products whose dimensions are all >= min_dim and K <=
+ *                     65536 (smaller products and GEMVs stay on DMMA; inputs
+ *                     still being copied are awaited on the stream, per row
+ *                     chunk for the rows of A).
  * nmoduli = 0 / min_dim = 0 keep the current value (defaults 16 / 1024).
- * The emulated result is not bitwise the DMMA result; its error is bounded by
- * 2^-(pa) relative to the largest entry of each row of A / column of B, with
- * pa ~ 54 at K = 16384 and 16 moduli (ozaki.cu). */
+ * The emulated result is deterministic but not bitwise the DMMA result; each
+ * entry of A (B) is kept to 2^-pa (2^-pb) relative to the largest entry of its
+ * row (column), pa = 55 and pb = 54 at K = 16384 with 16 moduli, and the
+ * integer product is exact (ozaki.cu). */
 #define SI_GEMM_DMMA 0
 #define SI_GEMM_OZAKI_I8 1
 SI_API int si_set_gemm_backend(si_handle h, int backend, int nmoduli, int64_t min_dim);
