@@ -9,6 +9,7 @@
  *
  * Checks on the host: the Richardson mismatch ||A theta - b|| contracts, the
  * residual ||F||_F (si_fro_norm) falls as F_k = F_{k-1}^3, F = I - G A holds,
+ * the step with the products emulated on the INT8 tensor cores matches FP64 DMMA,
  * the counters tick like MulCounter (3 mmm + 2 mvm per step after the init),
  * and a bad argument returns SI_EINVAL with a message.  Exit status 0 = pass. */
 #include <cuda_runtime.h>
@@ -142,6 +143,30 @@ int main(void) {
       sharded_ok = 1;  /* no libnccl on this host: nothing to compare */
     }
   }
+  /* the same NS step with every product emulated on the INT8 tensor cores
+   * (si_set_gemm_backend: Ozaki-II, 16 moduli; min_dim 128 so n = 256 qualifies):
+   * within 1e-13 (relative Frobenius) of the FP64 DMMA step */
+  double emul_diff = 1.0;
+  {
+    double *dGe, *dFe;
+    cudaMalloc((void**)&dGe, mat);
+    cudaMalloc((void**)&dFe, mat);
+    CK(si_ns_step(h, n, dA, dG, dF, 3, NULL, 0, NULL, 0, dG2, dF2, NULL, NULL));
+    CK(si_set_gemm_backend(h, SI_GEMM_OZAKI_I8, 16, 128));
+    CK(si_ns_step(h, n, dA, dG, dF, 3, NULL, 0, NULL, 0, dGe, dFe, NULL, NULL));
+    CK(si_set_gemm_backend(h, SI_GEMM_DMMA, 0, 0));
+    cudaMemcpy(hG, dG2, mat, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hF, dGe, mat, cudaMemcpyDeviceToHost);
+    double num = 0.0, den = 0.0;
+    for (int64_t i = 0; i < n * n; ++i) {
+      num += (hF[i] - hG[i]) * (hF[i] - hG[i]);
+      den += hG[i] * hG[i];
+    }
+    emul_diff = sqrt(num / den);
+    cudaFree(dGe);
+    cudaFree(dFe);
+  }
+  printf("ns_step emulated on the INT8 tensor cores vs FP64 DMMA: rel diff %.2e\n", emul_diff);
   /* a bad argument: negative dimension */
   const int bad = si_gemm(h, -1, n, n, 1.0, dA, n, dA, n, 0.0, NULL, n, 0.0, dG2, n, 0, NULL, NULL);
   printf("||F_0||_F=%.3e ||F_%d||_F=%.3e mismatch=%.3e |F - (I - G A)|max=%.2e "
@@ -153,7 +178,7 @@ int main(void) {
   cudaFree(dG2); cudaFree(dF2); cudaFree(db); cudaFree(dx); cudaFree(dx2);
   free(hA); free(hM); free(hb); free(hx); free(hG); free(hF);
   printf("sharded ns_step (NCCL, 1 rank) bitwise equal: %s\n", sharded_ok ? "yes" : "NO");
-  if (bad != SI_EINVAL || !sharded_ok) return 1;
+  if (bad != SI_EINVAL || !sharded_ok || !(emul_diff <= 1e-13)) return 1;
   if (!(fk < f0) || worst > 1e-12) return 1;
   return 0;
 }

@@ -95,7 +95,8 @@ def test_exact_inverse_is_reproduced():
 
 def test_c_host_demo():
     """A non-Python host of the C ABI (examples/c_host_demo.c: split, initial
-    series, plain Richardson + NS steps, norms, error status) built by build()."""
+    series, plain Richardson + NS steps, norms, error status, the INT8-emulated
+    backend, the sharded entry point) built by build()."""
     import os
     import subprocess
 
@@ -106,6 +107,7 @@ def test_c_host_demo():
     assert out.returncode == 0, out.stdout + out.stderr
     assert "bad-call status=-1" in out.stdout
     assert "sharded ns_step (NCCL, 1 rank) bitwise equal: yes" in out.stdout
+    assert "ns_step emulated on the INT8 tensor cores vs FP64 DMMA: rel diff" in out.stdout
 
 
 def test_batched_ns_richardson_into_packed_outputs():
