@@ -85,7 +85,7 @@ void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, 
   e.wait(c, StepEvents::kPrecond);
   e.wait(c, StepEvents::kResidual);
   e.wait(c, StepEvents::kSplitMatrix);
-  auto part = [&](Ctx& cc, size_t i) {
+  auto series = [&](Ctx& cc, size_t i) {  // T_i: products with B and S^-1 only
     if (rates[i] < 1) throw Error(kEInval, "rates must be positive integers");
     if (rates[i] == 1) {
       ts[i] = alloc_like(cc, P);
@@ -93,6 +93,9 @@ void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, 
     } else {
       ts[i] = geometric(cc, B, P, rates[i], Sm, plans[i]);
     }
+  };
+  auto part = [&](Ctx& cc, size_t i) {
+    series(cc, i);
     e.wait(cc, StepEvents::kA);
     gs[i] = residual(cc, ts[i], A);
   };
@@ -107,7 +110,13 @@ void composite_step(Ctx& c, const MV& A, const MV& G, const MV& F, const MV& P, 
     for (auto& kd : kids) fk.join(kd);
     fk.join(nsc);
   } else {
-    for (size_t i = 0; i < k; ++i) part(c, i);
+    // every part's series first (they read only B and S^-1), then the
+    // residuals Gamma_i = I - T_i A: with A still in flight (the e2e path)
+    // its copy overlaps ten products instead of stalling the second; the
+    // products are the same, so the results are bitwise unchanged
+    for (size_t i = 0; i < k; ++i) series(c, i);
+    e.wait(c, StepEvents::kA);
+    for (size_t i = 0; i < k; ++i) gs[i] = residual(c, ts[i], A);
   }
   MV t = ts[0], r = gs[0];
   for (size_t i = 1; i < k; ++i) {
