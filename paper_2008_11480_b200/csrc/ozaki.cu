@@ -14,7 +14,7 @@
 //     largest entries themselves.
 //  2. For each modulus m_l (pairwise coprime, <= 256): residues of A' and B'
 //     in [-128, 127] (int8), and C_l = A'_l @ B'_l on the tensor cores.  The
-//     int32 sums are exact (|C_l| <= K * 2^14 < 2^30 for K <= 32768), reduced
+//     int32 sums are exact (|C_l| <= K * 2^14 <= 2^30 for K <= 65536), reduced
 //     mod m_l in the TMEM epilogue and stored as one byte per entry.
 //  3. C' = A' B' is the unique integer in (-M/4, M/4] with those residues
 //     (Chinese remainder theorem), rebuilt in FP64 from exact partial sums
@@ -22,19 +22,26 @@
 //     the seriesinv epilogue (alpha, beta * C, diag * I) is fused there.
 //
 // The integer product is exact and order-free, so results do not depend on
-// tiling, concurrency or on how rows are split across ranks (the block-row
-// sharded path stays bitwise equal to the single-GPU call, as with DMMA).
+// tiling, chunking, concurrency or on how rows are split across ranks (the
+// block-row sharded path stays bitwise equal to the single-GPU call, as with
+// DMMA).
 //
-// Kernels (one emulated product = 6 launches):
+// Kernels (one emulated product = 6 launches per row x column chunk):
 //   row_absmax / col_absmax      max |a| per row of A, per column of B (HBM)
 //   residues_rows / residues_cols A -> nmod int8 planes (K-major), B -> nmod
-//                                int8 planes transposed to K-major (HBM)
+//                                int8 planes transposed to K-major (INT pipe)
 //   i8_gemm_mod_kernel           nmod int8 GEMMs, tcgen05.mma kind::i8 with
 //                                TMA (128B swizzle) -> 4-stage smem ring ->
 //                                single-thread MMA issue -> double-buffered
 //                                TMEM accumulators -> 4 epilogue warps
-//                                (tcgen05.ld, mod m_l, byte stores)
-//   crt_kernel                   CRT + scale + fused epilogue (HBM)
+//                                (tcgen05.ld, mod m_l, byte stores); the
+//                                default.  Variants: i8_gemm_mod_pair_kernel
+//                                (cta_group::2 CTA pairs) and
+//                                i8_gemm_mod_mc_kernel (B tiles multicast in
+//                                2-CTA clusters), measured and kept selectable
+//   crt_kernel<NMOD>             CRT + scale + fused epilogue (FP64 pipe)
+// The scales + residue planes of a step's immutable operands are kept across
+// the step's products by the caller (engine.cu, `Side`).
 #include "ozaki.hpp"
 
 #include <cuda.h>
