@@ -111,3 +111,26 @@ def test_baked_resident_programs_are_current():
     buf = ctypes.create_string_buffer(n.value + 1)
     assert lib.si_resident_program_source_ns(64, 3, 8, buf, n.value + 1, ctypes.byref(n)) == 0
     assert buf.value.decode() == body(os.path.join(csrc, "resident_fixed_c1.inc"))
+
+
+def test_backend_entry_points_validate_without_gpu():
+    """The FP64-product backend entry points (si_set_gemm_backend & co.) reject
+    bad arguments with SI_EINVAL before touching a device."""
+    from paper_2008_11480_b200 import _lib
+
+    lib = _lib.load_library()
+    E = _lib.SI_EINVAL
+    assert lib.si_set_gemm_backend(None, 1, 16, 1024) == E  # null handle
+    assert lib.si_get_gemm_backend(None, None, None, None) == E
+    assert lib.si_set_ozaki_chunks(None, 0, 0) == E
+    assert lib.si_set_ozaki_kernel(None, 0) == E
+    assert lib.si_ozaki_tune(-1, 0, 0) == E
+    assert lib.si_ozaki_tune(0, 3, 0) == E
+    assert lib.si_ozaki_tune_stages(2) == E and lib.si_ozaki_tune_stages(7) == E
+    assert lib.si_ozaki_moduli(0, None) == E
+    mods = (ctypes.c_uint32 * 17)()
+    assert lib.si_ozaki_moduli(17, mods) == E
+    assert lib.si_ozaki_moduli(16, mods) == _lib.SI_OK
+    assert list(mods)[:3] == [256, 255, 253]
+    assert lib.si_i8_gemm_mod(None, None, None, None, 1, 1, 128, 1, None) == E
+    assert lib.si_profile_i8(None, None, None, None) == E
