@@ -419,3 +419,35 @@ def test_strided_operands_through_the_abi():
     assert bool((big_d[:, :4] == 7.0).all()) and bool((big_d[:, 4 + n:] == 7.0).all())
     ref = a.cpu().numpy().astype(np.longdouble) @ b.cpu().numpy() + c.cpu().numpy()
     assert np.abs(d.cpu().numpy() - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_largest_inner_dimension():
+    """K = 65536 (kMaxK): all -128 residues give the largest int32 sum the
+    epilogue reduces, 2^30 (u = 2^31), exactly; an emulated product with that K
+    meets the a-priori bound."""
+    import paper_2008_11480_b200 as P
+
+    kp = 65536
+    mods = P.ozaki_moduli(2)
+    a = torch.full((2, 128, kp), -128, dtype=torch.int8, device="cuda")
+    bt = torch.full((2, 128, kp), -128, dtype=torch.int8, device="cuda")
+    for kernel in ("single", "pair"):
+        P.set_ozaki_kernel(kernel)
+        try:
+            r = P.i8_gemm_mod(a, bt)
+        finally:
+            P.set_ozaki_kernel("auto")
+        for l in range(2):
+            assert bool((r[l] == (kp * 16384) % mods[l]).all()), (kernel, l)
+    rng = np.random.default_rng(13)
+    a_np, b_np = rng.standard_normal((256, kp)), rng.standard_normal((kp, 256))
+    c = _ozaki(torch.from_numpy(a_np).cuda(), torch.from_numpy(b_np).cuda()).cpu().numpy()
+    ref = a_np.astype(np.longdouble) @ b_np.astype(np.longdouble)
+    pa, pb = _pa_pb(kp, 16)
+    amax = np.abs(a_np).max(1, keepdims=True)
+    bmax = np.abs(b_np).max(0, keepdims=True)
+    bound = (2.0 ** -pa * amax * np.abs(b_np).sum(0, keepdims=True)
+             + 2.0 ** -pb * bmax * np.abs(a_np).sum(1, keepdims=True)
+             + 2.0 ** -(pa + pb) * kp * amax * bmax)
+    bound = 1.01 * bound + 4 * 2.0 ** -53 * np.abs(ref).astype(np.float64)
+    assert np.all(np.abs(c - ref).astype(np.float64) <= bound)
