@@ -284,6 +284,18 @@ SI_API int si_mat_pow_counted(si_handle h, int64_t n, const double* y, int e, do
 
 /* ---------------- Newton-Schulz steps (newton_schulz.py) ---------------- */
 
+/* Fused stop-rule norm (converged, newton_schulz.py:328-331 over fro_norm,
+ * matrix_core.py:167-168): the NEXT step call on this handle (si_initial_series,
+ * si_ns_step*, si_composite_step*, si_composite_apply, si_initial_double,
+ * si_double_ns_step) writes ||F'||_F^2 of its residual output into the device
+ * double `fro2` (stream-ordered).  The products that write F' emit per-warp
+ * partial sums of squares from their epilogues (FP64 GEMM, CRT of the
+ * emulated products; small-n kernels one partial pass), reduced in a fixed
+ * order -- deterministic, no extra pass over F'.  One-shot: the step call
+ * consumes it; NULL cancels.  Not used by the si_sharded_* calls
+ * (si_sharded_fro_norm). */
+SI_API int si_set_step_norm(si_handle h, double* fro2);
+
 /* initial_series (newton_schulz.py:127-147) */
 SI_API int si_initial_series(si_handle h, int64_t n, const double* precond, const double* residual,
                       const double* a, int p, int w, double* g_out, double* f_out,

@@ -46,6 +46,7 @@ SIGNATURES: dict[str, list] = {
     "si_lincomb": [_P, _I64, _I64, _D, _I, _P, _P, _P, _P, _I64, _P],
     "si_lincomb_ex": [_P, _I64, _I64, _D, _I64, _I, _P, _P, _P, _P, _I64, _P],
     "si_fro_norm": [_P, _I64, _I64, _P, _I64, POINTER(c_double), _P],
+    "si_set_step_norm": [_P, _P],
     "si_inf_norm": [_P, _I64, _I64, _P, _I64, POINTER(c_double), _P],
     "si_split_scalar": [_P, _I64, _P, _D, _P, _P, _P],
     "si_split_diagonal": [_P, _I64, _P, _P, _P, _P],

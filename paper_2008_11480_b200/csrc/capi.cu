@@ -94,6 +94,41 @@ void mark_stable(Ctx& c, int64_t n, std::initializer_list<const double*> ins,
   }
 }
 
+// si_set_step_norm: ||F'||_F^2 of this step call's residual output F' (n x n
+// at f_out), fused into the epilogues of the products that write F'
+// (newton_schulz.py:328-331 reads it back as converged()); consumes the
+// handle's one-shot target.  finish() after the step body.
+struct StepNorm {
+  Ctx& c;
+  const double* f;
+  int64_t n;
+  double* out;
+  Ctx::SqAcc acc;
+  StepNorm(Call& call, const double* f_out, int64_t nn, double* target)
+      : c(call.c), f(f_out), n(nn), out(target) {
+    if (out) {
+      c.sq = &acc;
+      c.sq_lo = f;
+      c.sq_hi = f + n * n;
+    }
+  }
+  void finish() {
+    c.sq = nullptr;
+    if (out) finish_sq(c, acc, view(const_cast<double*>(f), n, n, n).v, out);
+  }
+  ~StepNorm() { c.sq = nullptr; }
+};
+
+// the handle's one-shot si_set_step_norm target, consumed first thing by
+// every step call (also by one that then fails its argument checks)
+double* take_step_norm(si_handle h) {
+  if (!h) return nullptr;
+  std::lock_guard<std::recursive_mutex> lock(h->h.mu);
+  double* t = h->h.step_norm;
+  h->h.step_norm = nullptr;
+  return t;
+}
+
 // One sharded C-ABI call: Call + this call's Shard (row split, gather cache).
 struct ShardCall {
   Call call;
@@ -194,6 +229,14 @@ int si_destroy(si_handle h) {
     for (auto& kv : h->h.programs) cudaFree(kv.second);
     if (h->h.pool) cudaMemPoolDestroy(h->h.pool);
     delete h;
+  });
+}
+
+int si_set_step_norm(si_handle h, double* fro2) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    std::lock_guard<std::recursive_mutex> lock(h->h.mu);
+    h->h.step_norm = fro2;
   });
 }
 
@@ -580,10 +623,13 @@ int si_initial_series(si_handle h, int64_t n, const double* precond, const doubl
                       const double* a, int p, int w, double* g_out, double* f_out,
                       int64_t* counters, void* stream) {
   return guard([&] {
+    double* fro2 = take_step_norm(h);
     need(h && precond && residual && a && g_out && f_out, "null pointer");
     Call call(h, stream, counters);
+    StepNorm norm(call, f_out, n, fro2);
     initial_series(call.c, sq(precond, n), sq(residual, n), sq(a, n), p, w, sq(g_out, n),
                    sq(f_out, n));
+    norm.finish();
   });
 }
 
@@ -591,11 +637,14 @@ int si_ns_step(si_handle h, int64_t n, const double* a, const double* g, const d
                int order, const int32_t* plan, int64_t plan_len, const double* consts,
                int64_t nconsts, double* g_out, double* f_out, int64_t* counters, void* stream) {
   return guard([&] {
+    double* fro2 = take_step_norm(h);
     need(h && a && g && f && g_out && f_out, "null pointer");
     PlanPtr pl = opt_plan(plan, plan_len, consts, nconsts);
     Call call(h, stream, counters);
+    StepNorm norm(call, f_out, n, fro2);
     mark_stable(call.c, n, {a, g, f}, {g_out, f_out});
     ns_step(call.c, sq(a, n), sq(g, n), sq(f, n), order, pl.get(), sq(g_out, n), sq(f_out, n));
+    norm.finish();
   });
 }
 
@@ -604,9 +653,11 @@ int si_ns_step_ex(si_handle h, int64_t n, const double* a, const double* g, cons
                   int64_t nconsts, void* const* input_ready_events, void* g_done_event,
                   double* g_out, double* f_out, int64_t* counters, void* stream) {
   return guard([&] {
+    double* fro2 = take_step_norm(h);
     need(h && a && g && f && g_out && f_out, "null pointer");
     PlanPtr pl = opt_plan(plan, plan_len, consts, nconsts);
     Call call(h, stream, counters);
+    StepNorm norm(call, f_out, n, fro2);
     mark_stable(call.c, n, {a, g, f}, {g_out, f_out});
     if (input_ready_events) {
       const double* bases[3] = {a, g, f};
@@ -617,6 +668,7 @@ int si_ns_step_ex(si_handle h, int64_t n, const double* a, const double* g, cons
     }
     ns_step(call.c, sq(a, n), sq(g, n), sq(f, n), order, pl.get(), sq(g_out, n), sq(f_out, n),
             reinterpret_cast<cudaEvent_t>(g_done_event));
+    norm.finish();
   });
 }
 
@@ -626,6 +678,7 @@ int si_ns_step_gated(si_handle h, int64_t n, const double* a, const double* g, c
                      void* g_done_event, void* const* f_chunk_events, int f_chunks,
                      double* g_out, double* f_out, int64_t* counters, void* stream) {
   return guard([&] {
+    double* fro2 = take_step_norm(h);
     need(h && a && g && f && g_out && f_out, "null pointer");
     need(!input_flags || (npanels >= 1 && npanels <= kMaxPanels), "npanels out of range");
     need(f_chunks >= 0 && (f_chunks == 0 || f_chunk_events), "bad f_chunks");
@@ -633,6 +686,7 @@ int si_ns_step_gated(si_handle h, int64_t n, const double* a, const double* g, c
     std::vector<cudaEvent_t> chunks(f_chunks);
     for (int k = 0; k < f_chunks; ++k) chunks[k] = reinterpret_cast<cudaEvent_t>(f_chunk_events[k]);
     Call call(h, stream, counters);
+    StepNorm norm(call, f_out, n, fro2);
     mark_stable(call.c, n, {a, g, f}, {g_out, f_out});
     if (input_flags) {
       const double* bases[3] = {a, g, f};
@@ -650,6 +704,7 @@ int si_ns_step_gated(si_handle h, int64_t n, const double* a, const double* g, c
     ns_step(call.c, sq(a, n), sq(g, n), sq(f, n), order, pl.get(), sq(g_out, n), sq(f_out, n),
             reinterpret_cast<cudaEvent_t>(g_done_event), f_chunks,
             f_chunks ? chunks.data() : nullptr);
+    norm.finish();
   });
 }
 
@@ -672,6 +727,7 @@ int si_composite_step_ex(si_handle h, int64_t n, const double* a, const double* 
                          void* const* input_ready_events, void* g_done_event, double* g_out,
                          double* f_out, int64_t* counters, void* stream) {
   return guard([&] {
+    double* fro2 = take_step_norm(h);
     need(h && a && g && f && precond && residual && split_matrix && g_out && f_out,
          "null pointer");
     need(nrates >= 1 && rates, "composite spec needs at least one rate");
@@ -693,10 +749,12 @@ int si_composite_step_ex(si_handle h, int64_t n, const double* a, const double* 
         ev.ready[i] = reinterpret_cast<cudaEvent_t>(input_ready_events[i]);
     ev.g_done = reinterpret_cast<cudaEvent_t>(g_done_event);
     Call call(h, stream, counters);
+    StepNorm norm(call, f_out, n, fro2);
     mark_stable(call.c, n, {a, g, f, precond, residual, split_matrix}, {g_out, f_out});
     composite_step(call.c, sq(a, n), sq(g, n), sq(f, n), sq(precond, n), sq(residual, n),
                    sq(split_matrix, n), rv, pv, order_n, concurrent != 0, sq(g_out, n),
                    sq(f_out, n), &ev);
+    norm.finish();
   });
 }
 
@@ -709,6 +767,7 @@ int si_composite_step_gated(si_handle h, int64_t n, const double* a, const doubl
                             void* g_done_event, void* const* f_chunk_events, int f_chunks,
                             double* g_out, double* f_out, int64_t* counters, void* stream) {
   return guard([&] {
+    double* fro2 = take_step_norm(h);
     need(h && a && g && f && precond && residual && split_matrix && g_out && f_out,
          "null pointer");
     need(nrates >= 1 && rates, "composite spec needs at least one rate");
@@ -733,6 +792,7 @@ int si_composite_step_gated(si_handle h, int64_t n, const double* a, const doubl
     ev.f_chunk = f_chunks ? chunks.data() : nullptr;
     ev.f_chunks = f_chunks;
     Call call(h, stream, counters);
+    StepNorm norm(call, f_out, n, fro2);
     mark_stable(call.c, n, {a, g, f, precond, residual, split_matrix}, {g_out, f_out});
     if (input_flags) {
       const double* bases[6] = {a, g, f, precond, residual, split_matrix};
@@ -750,6 +810,7 @@ int si_composite_step_gated(si_handle h, int64_t n, const double* a, const doubl
     composite_step(call.c, sq(a, n), sq(g, n), sq(f, n), sq(precond, n), sq(residual, n),
                    sq(split_matrix, n), rv, pv, order_n, concurrent != 0, sq(g_out, n),
                    sq(f_out, n), &ev);
+    norm.finish();
   });
 }
 
@@ -782,11 +843,14 @@ int si_composite_apply(si_handle h, int64_t n, const double* a, const double* g,
                        const double* t, const double* r, int order_n, double* g_out,
                        double* f_out, int64_t* counters, void* stream) {
   return guard([&] {
+    double* fro2 = take_step_norm(h);
     need(h && a && g && f && t && r && g_out && f_out, "null pointer");
     need(order_n >= 1, "order_n must be >= 1");
     Call call(h, stream, counters);
+    StepNorm norm(call, f_out, n, fro2);
     composite_apply(call.c, sq(a, n), sq(g, n), sq(f, n), sq(t, n), sq(r, n), order_n,
                     sq(g_out, n), sq(f_out, n));
+    norm.finish();
   });
 }
 
@@ -794,11 +858,14 @@ int si_initial_double(si_handle h, int64_t n, const double* precond, const doubl
                       const double* a, int p, int w, int order, double* g_out, double* f_out,
                       double* l_out, double* r_out, int64_t* counters, void* stream) {
   return guard([&] {
+    double* fro2 = take_step_norm(h);
     need(h && precond && residual && a && g_out && f_out && l_out && r_out, "null pointer");
     need(order >= 1, "order must be >= 1");
     Call call(h, stream, counters);
+    StepNorm norm(call, f_out, n, fro2);
     initial_double(call.c, sq(precond, n), sq(residual, n), sq(a, n), p, w, order, sq(g_out, n),
                    sq(f_out, n), sq(l_out, n), sq(r_out, n));
+    norm.finish();
   });
 }
 
@@ -807,10 +874,13 @@ int si_double_ns_step(si_handle h, int64_t n, const double* a, const double* g, 
                       double* f_out, double* l_out, double* r_out, int64_t* counters,
                       void* stream) {
   return guard([&] {
+    double* fro2 = take_step_norm(h);
     need(h && a && g && f && l && r && g_out && f_out && l_out && r_out, "null pointer");
     Call call(h, stream, counters);
+    StepNorm norm(call, f_out, n, fro2);
     double_ns_step(call.c, sq(a, n), sq(g, n), sq(f, n), sq(l, n), sq(r, n), order,
                    concurrent != 0, sq(g_out, n), sq(f_out, n), sq(l_out, n), sq(r_out, n));
+    norm.finish();
   });
 }
 

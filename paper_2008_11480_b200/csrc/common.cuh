@@ -24,6 +24,10 @@ struct Epilogue {
   int64_t doff = 0;  // diag*I sits at (i, i + doff): row blocks of a sharded matrix
   const double* c = nullptr;
   int64_t ldc = 0;
+  // optional: per-CTA-warp partial sums of squares of the stored values (the
+  // fused ||D||_F^2 of newton_schulz.py:328-331); the kernel writes exactly
+  // the slots its *_sq_slots() function counts
+  double* sq = nullptr;
 };
 
 // Panel gate of a product whose right operand B is being gathered row panel
@@ -47,6 +51,7 @@ cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& 
 cudaError_t launch_gemm_generic(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, cudaStream_t s);
 cudaError_t launch_gemv(const Mat& A, const Mat& X, Mat& D, const Epilogue& e, cudaStream_t s);
 bool tma_eligible(const Mat& A, const Mat& B, const Mat& D, const Epilogue& e);
+int64_t gemm_tma_sq_slots(int64_t M, int64_t N);
 
 // D = cdiag * I + sum_i coef[i] * X[i], accumulated in argument order with one
 // rounding per term (series_toolkit.py:375-378, numpy temporaries).
@@ -68,6 +73,9 @@ size_t reduce_work_elems(const Mat& X);
 // per-block partial sums of squares only (sumsq_partials() of them, fixed order)
 cudaError_t launch_sumsq_partials(const Mat& X, double* part, cudaStream_t s);
 int sumsq_partials();
+// *out = (accumulate ? *out : 0) + fixed-order sum of part[0..n) (fused-norm slots)
+cudaError_t launch_sum_slots(const double* part, int64_t n, double* out, bool accumulate,
+                             cudaStream_t s);
 // Stream memory operations (driver entry points; executed by the stream's
 // front end, no SM involved): *addr = value after prior work, and wait until
 // (int32)(*addr - value) >= 0.  Either address may be a peer (IPC) mapping.

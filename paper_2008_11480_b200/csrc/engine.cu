@@ -157,6 +157,35 @@ oz::Side* oz_side(Ctx& c, const Mat& m, bool b_side, int64_t k, int nmod) {
 }
 }  // namespace
 
+// fused-norm slots of one product (Ctx::sq): a fresh slot buffer, appended
+static double* sq_slots_for(Ctx& c, int64_t slots) {
+  MV part = alloc(c, 1, slots);
+  c.sq->parts.emplace_back(part, slots);
+  return part.v.p;
+}
+
+// products without a fused epilogue partial (GEMV, small-n generic kernel):
+// one partial pass over the stored values
+static cudaError_t unfused_sq(Ctx& c, const Mat& d) {
+  double* part = sq_slots_for(c, sumsq_partials());
+  c.h->launches += 1;
+  return launch_sumsq_partials(d, part, c.s);
+}
+
+void finish_sq(Ctx& c, const Ctx::SqAcc& acc, const Mat& F, double* out) {
+  if (acc.parts.empty()) {
+    MV work = alloc(c, 1, (int64_t)reduce_work_elems(F));
+    check(launch_sumsq(F, out, work.v.p, c.s), "sumsq");
+    c.h->launches += 2;
+    return;
+  }
+  for (size_t i = 0; i < acc.parts.size(); ++i) {
+    check(launch_sum_slots(acc.parts[i].first.v.p, acc.parts[i].second, out, i > 0, c.s),
+          "sum slots");
+    c.h->launches += 1;
+  }
+}
+
 void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV* C, double beta,
           double diag, bool mv, int64_t doff, const PanelWait* pw) {
   if (c.shard) {
@@ -193,6 +222,7 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
   Mat d = D.v;
   cudaError_t err;
   Handle* h = c.h;
+  const bool collect_sq = c.sq && d.p >= c.sq_lo && d.p < c.sq_hi && d.rows > 0 && d.cols > 0;
   if (!c.awaits.empty()) {
     c.await_ptr(A.v.p);
     c.await_ptr(B.v.p);
@@ -320,6 +350,7 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
     }
     oz::Side* as = oz_side(c, A.v, false, A.v.cols, h->oz_nmod);
     oz::Side* bs = oz_side(c, B.v, true, A.v.cols, h->oz_nmod);
+    if (collect_sq) e.sq = sq_slots_for(c, oz::sq_slots(d.rows, d.cols, A.v.cols, h->oz_nmod, w));
     err = oz::launch_gemm(A.v, B.v, d, e, h->oz_nmod, w, c.s, &nl, hook, as, bs, row_hook);
     if (oz_rows) c.gate_stream(A.v.p);  // every panel waited (no-ops by now): later readers
     h->launches += nl;
@@ -330,7 +361,9 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
   } else if (d.cols <= 4) {
     err = launch_gemv(A.v, B.v, d, e, c.s);
     h->launches += 1;
+    if (collect_sq && err == cudaSuccess) err = unfused_sq(c, d);
   } else if (use_tma) {
+    if (collect_sq) e.sq = sq_slots_for(c, gemm_tma_sq_slots(d.rows, d.cols));
     Handle::ProfRec rec{};
     if (h->profiling) {
       for (cudaEvent_t* ev : {&rec.start, &rec.stop}) {
@@ -353,6 +386,7 @@ void gemm(Ctx& c, const MV& D, const MV& A, const MV& B, double alpha, const MV*
   } else {
     err = launch_gemm_generic(A.v, B.v, d, e, c.s);
     h->launches += 1;
+    if (collect_sq && err == cudaSuccess) err = unfused_sq(c, d);
   }
   check(err, "gemm launch");
   if (mv)

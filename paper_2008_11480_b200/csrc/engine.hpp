@@ -40,6 +40,9 @@ struct Handle {
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> prof_pool;
   int64_t launches = 0;  // kernels launched by this handle
+  // si_set_step_norm: device double receiving ||F'||_F^2 of the next step
+  // call's residual output (one-shot: the step call consumes it)
+  double* step_norm = nullptr;
   // FP64 product backend (si_set_gemm_backend): 0 = DMMA (gemm_tma.cu, the
   // default), 1 = Ozaki-II emulation on the INT8 tensor cores (ozaki.cu) for
   // products whose three dimensions are all >= oz_min_dim.
@@ -138,10 +141,26 @@ struct Ctx {
   std::vector<MV> stable_keep;  // engine values marked stable (kept alive for the call)
   struct OzSide;
   std::vector<std::shared_ptr<OzSide>> oz_sides;
+  // Fused ||F||_F^2 of a step's residual output (si_set_step_norm,
+  // newton_schulz.py:328-331): while `sq` is set, every product whose output
+  // lies in [sq_lo, sq_hi) (the step's F' buffer) writes the sum-of-squares
+  // slots of the values it stores (GEMM / CRT epilogue; a separate partial
+  // pass on the small-n kernels) into a buffer appended here; finish_sq()
+  // reduces them in product order into one device double.
+  struct SqAcc {
+    std::vector<std::pair<MV, int64_t>> parts;  // slot buffer, slot count
+  };
+  SqAcc* sq = nullptr;
+  const double* sq_lo = nullptr;
+  const double* sq_hi = nullptr;
   Ctx(Handle* hh, cudaStream_t st) : h(hh), root(st), s(st) {}
 };
 
 void check(cudaError_t e, const char* what);
+// *out = ||F||_F^2 of the step output F: the fixed-order sum of the slots `acc`
+// collected from the products that wrote F, or (no product wrote it, e.g. a
+// copied F) one reduction pass over F (stream-ordered)
+void finish_sq(Ctx& c, const Ctx::SqAcc& acc, const Mat& F, double* out);
 // Mark an engine value that is never written again in this call as stable (its
 // emulated-product operand images may be kept); it stays allocated until the
 // call ends.  Root context only (no-op on branches).

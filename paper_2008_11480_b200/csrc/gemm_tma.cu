@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         int K, double alpha, double beta, double diag, int64_t doff,
                         const __grid_constant__ PanelWait pw,
                         const __grid_constant__ PanelWait pwa, SyncSet* __restrict__ sync,
-                        int group_m) {
+                        int group_m, double* __restrict__ sq) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -403,6 +403,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------- fused epilogue ----------------
     const int row0 = tm * BM + wm * 64 + g;
     const int col0 = tn * BN + wn * 32 + 2 * t;
+    // sum of squares of the stored values (sq != null): one slot per (tile,
+    // consumer warp), written by that warp alone -- a fixed-order reduction
+    // of the slots later gives ||D||_F^2 deterministically
+    double ss = 0.0;
+    auto flush_sq = [&]() {
+      if (sq == nullptr) return;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) sq[(int64_t)tile * NUM_CONSUMER_WARPS + warp] = ss;
+    };
     if (EPI == 1 && beta != 0.0) {
       // C loads issued a pair of fragment rows ahead of the stores that use them
       // (each thread reads its own elements before writing them, so D == C is fine)
@@ -445,12 +455,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             if (col + 1 < N) {
               *reinterpret_cast<double2*>(D + (int64_t)row * ldd + col) = make_double2(v0, v1);
+              ss = fma(v1, v1, fma(v0, v0, ss));
             } else {
               D[(int64_t)row * ldd + col] = v0;
+              ss = fma(v0, v0, ss);
             }
           }
         }
       }
+      flush_sq();
       continue;
     }
 #pragma unroll
@@ -480,11 +493,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (two) {
           *reinterpret_cast<double2*>(D + (int64_t)row * ldd + col) = make_double2(v0, v1);
+          ss = fma(v1, v1, fma(v0, v0, ss));
         } else {
           D[(int64_t)row * ldd + col] = v0;
+          ss = fma(v0, v0, ss);
         }
       }
     }
+    flush_sq();
   }
 }
 
@@ -625,8 +641,12 @@ cudaError_t launch_gemm_tma(const Mat& A, const Mat& B, Mat& D, const Epilogue& 
   auto kern = epi == 1 ? gemm_f64_tma_kernel<1> : gemm_f64_tma_kernel<0>;
   kern<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, D.p, D.ld, e.c, e.ldc, M, N, K,
                                                         e.alpha, e.beta, e.diag, e.doff, gate,
-                                                        gate_a, sync, group_m());
+                                                        gate_a, sync, group_m(), e.sq);
   return cudaGetLastError();
+}
+
+int64_t gemm_tma_sq_slots(int64_t M, int64_t N) {
+  return ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * NUM_CONSUMER_WARPS;
 }
 
 }  // namespace si

@@ -473,6 +473,22 @@ cudaError_t launch_sumsq(const Mat& X, double* out_dev, double* work, cudaStream
 
 int sumsq_partials() { return RED_BLOCKS; }
 
+// *out = (accumulate ? *out : 0) + sum of part[0..n) in a fixed order
+__global__ void __launch_bounds__(RED_THREADS) sum_slots_kernel(const double* __restrict__ part,
+                                                               int64_t n, double* __restrict__ out,
+                                                               int accumulate) {
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) *out = accumulate ? *out + s : s;
+}
+
+cudaError_t launch_sum_slots(const double* part, int64_t n, double* out, bool accumulate,
+                             cudaStream_t s) {
+  sum_slots_kernel<<<1, RED_THREADS, 0, s>>>(part, n, out, accumulate ? 1 : 0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sumsq_partials(const Mat& X, double* part, cudaStream_t s) {
   sumsq_partial<<<RED_BLOCKS, RED_THREADS, 0, s>>>(X.p, X.ld, X.rows, X.cols, part);
   return cudaGetLastError();

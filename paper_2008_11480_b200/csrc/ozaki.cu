@@ -1020,7 +1020,8 @@ __global__ void __launch_bounds__(256) crt_kernel(
     const uint8_t* __restrict__ R, int M, int N, const unsigned long long* __restrict__ rmax,
     const unsigned long long* __restrict__ cmax, int pa, int pb, const __grid_constant__ CrtTab tab,
     double* D, int64_t ldd, const double* C, int64_t ldc, double alpha, double beta, double diag,
-    int64_t doff) {
+    int64_t doff, double* __restrict__ sq) {
+  double ss = 0.0;  // sum of squares of this thread's stored values (sq != null)
   const int chunks = (N + 3) >> 2;
   const int64_t total = (int64_t)M * chunks;
   const int64_t plane = (int64_t)M * N;
@@ -1069,6 +1070,7 @@ __global__ void __launch_bounds__(256) crt_kernel(
       }
       *reinterpret_cast<double2*>(drow) = make_double2(v[0], v[1]);
       *reinterpret_cast<double2*>(drow + 2) = make_double2(v[2], v[3]);
+      if (sq) ss = fma(v[3], v[3], fma(v[2], v[2], fma(v[1], v[1], fma(v[0], v[0], ss))));
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -1077,8 +1079,14 @@ __global__ void __launch_bounds__(256) crt_kernel(
         double x = apply_epi(v[j], alpha, beta, crow ? crow[j] : 0.0);
         if (diag != 0.0 && (int64_t)row + doff == (int64_t)col) x = __dadd_rn(x, diag);
         drow[j] = x;
+        ss = fma(x, x, ss);
       }
     }
+  }
+  if (sq) {  // one slot per warp of the (fixed-size) grid: a deterministic partial
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) sq[blockIdx.x * 8 + (threadIdx.x >> 5)] = ss;
   }
 }
 
@@ -1086,24 +1094,30 @@ template <int NMOD>
 void launch_crt_n(int blocks, cudaStream_t s, const uint8_t* R, int M, int N,
                   const unsigned long long* rmax, const unsigned long long* cmax, int pa, int pb,
                   const CrtTab& tab, double* D, int64_t ldd, const double* C, int64_t ldc,
-                  double alpha, double beta, double diag, int64_t doff) {
+                  double alpha, double beta, double diag, int64_t doff, double* sq) {
   crt_kernel<NMOD><<<blocks, 256, 0, s>>>(R, M, N, rmax, cmax, pa, pb, tab, D, ldd, C, ldc, alpha,
-                                          beta, diag, doff);
+                                          beta, diag, doff, sq);
 }
 
 template <int NMOD = kMinModuli>
 void launch_crt(int nmod, int blocks, cudaStream_t s, const uint8_t* R, int M, int N,
                 const unsigned long long* rmax, const unsigned long long* cmax, int pa, int pb,
                 const CrtTab& tab, double* D, int64_t ldd, const double* C, int64_t ldc,
-                double alpha, double beta, double diag, int64_t doff) {
+                double alpha, double beta, double diag, int64_t doff, double* sq) {
   if constexpr (NMOD <= kMaxModuli) {
     if (nmod == NMOD)
       launch_crt_n<NMOD>(blocks, s, R, M, N, rmax, cmax, pa, pb, tab, D, ldd, C, ldc, alpha, beta,
-                         diag, doff);
+                         diag, doff, sq);
     else
       launch_crt<NMOD + 1>(nmod, blocks, s, R, M, N, rmax, cmax, pa, pb, tab, D, ldd, C, ldc,
-                           alpha, beta, diag, doff);
+                           alpha, beta, diag, doff, sq);
   }
+}
+
+// grid of the CRT kernel for an mc x nc chunk (its sum-of-squares slots: 8 per block)
+int crt_blocks(int64_t mc, int64_t nc, int sms) {
+  const int64_t thr = mc * ((nc + 3) / 4);
+  return (int)std::min<int64_t>((thr + 255) / 256, 64 * sms);
 }
 
 // ----------------------------------------------------------------- host --
@@ -1343,7 +1357,7 @@ cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, i
   auto* bres = reinterpret_cast<int8_t*>(p);
   p += align256((size_t)nmod * NC * Kp);
   auto* res = p;
-  int64_t n = 0;
+  int64_t n = 0, sq_off = 0;
   cudaError_t err;
   const int sms = num_sms();
   // operand sides kept by the caller (unchunked sides only)
@@ -1395,16 +1409,27 @@ cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, i
         return err;
       if (hook) hook(false, 0.0);
       ++n;
-      const int64_t thr = mc * ((nc + 3) / 4);
-      const int blocks = (int)std::min<int64_t>((thr + 255) / 256, 64 * sms);
+      const int blocks = crt_blocks(mc, nc, sms);
       launch_crt(nmod, blocks, s, res, (int)mc, (int)nc, rmax, cmax, pa, pb, cs.crt[nmod],
                  D.p + i0 * D.ld + j0, D.ld, e.beta != 0.0 ? e.c + i0 * e.ldc + j0 : nullptr,
-                 e.ldc, e.alpha, e.beta, e.diag, e.doff + i0 - j0);
+                 e.ldc, e.alpha, e.beta, e.diag, e.doff + i0 - j0, e.sq ? e.sq + sq_off : nullptr);
+      sq_off += 8 * (int64_t)blocks;
       ++n;
     }
   }
   if (launches) *launches += n;
   return cudaGetLastError();
+}
+
+int64_t sq_slots(int64_t M, int64_t N, int64_t K, int nmod, const Work& w) {
+  const int64_t MC = chunk_rows(M, w.max_rows);
+  const int64_t NC = chunk_cols(MC, N, kpad(K), nmod, w.max_cols);
+  const int sms = num_sms();
+  int64_t slots = 0;
+  for (int64_t i0 = 0; i0 < M; i0 += MC)
+    for (int64_t j0 = 0; j0 < N; j0 += NC)
+      slots += 8 * (int64_t)crt_blocks(std::min(MC, M - i0), std::min(NC, N - j0), sms);
+  return slots;
 }
 
 }  // namespace oz

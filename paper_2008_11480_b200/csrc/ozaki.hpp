@@ -75,6 +75,10 @@ cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, i
                         const I8Hook& hook = nullptr, Side* a_side = nullptr,
                         Side* b_side = nullptr, const RowHook& row_hook = nullptr);
 
+// Sum-of-squares slots launch_gemm writes when e.sq is set (D's ||.||_F^2 =
+// the fixed-order sum of these; one slot per warp of each CRT launch).
+int64_t sq_slots(int64_t M, int64_t N, int64_t K, int nmod, const Work& w);
+
 // Test hook for the tensor-core kernel alone: R[l] = (A[l] @ Bt[l]^T) mod m_l
 // for l < nplanes, A[l]: M x Kp int8 rows, Bt[l]: N x Kp int8 rows (K-major,
 // Kp a multiple of 128, columns >= K zero), R[l]: M x N uint8.

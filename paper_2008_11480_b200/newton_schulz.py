@@ -11,7 +11,7 @@ here unchanged in meaning.
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from math import sqrt
 
 import torch
@@ -47,6 +47,20 @@ __all__ = [
 DEFAULT_MAX_STEPS = 30
 
 
+def _step_call(name: str, h, like: torch.Tensor, *args) -> torch.Tensor:
+    """One step call with its residual's ||F'||_F^2 fused into the products
+    that write F' (si_set_step_norm, a one-shot target); returns that device
+    double."""
+    fro2 = torch.empty(1, dtype=torch.float64, device=like.device)
+    _lib.call("si_set_step_norm", h, fro2.data_ptr())
+    try:
+        _lib.call(name, h, *args)
+    except BaseException:
+        _lib.call("si_set_step_norm", h, None)
+        raise
+    return fro2
+
+
 @dataclass
 class NsState:
     """G_k (estimate), F_k = I - G_k A (residual) (newton_schulz.py:58-72)."""
@@ -57,6 +71,9 @@ class NsState:
     order: int
     series_order: int
     ctr: MulCounter
+    # ||F_k||_F^2 as a device double, fused into the epilogues of the products
+    # that wrote F_k (si_set_step_norm); read by converged()
+    residual_fro2: torch.Tensor | None = field(default=None, compare=False, repr=False)
 
 
 @dataclass
@@ -71,6 +88,7 @@ class DoubleNsState:
     order: int
     series_order: int
     ctr: MulCounter
+    residual_fro2: torch.Tensor | None = field(default=None, compare=False, repr=False)
 
 
 @dataclass(frozen=True)
@@ -121,10 +139,12 @@ def initial_series(split: Splitting, p: int, w: int, order: int = 2) -> NsState:
     f = torch.empty_like(split.matrix)
     h, s = _ctx(g)
     buf = _lib.counter_buf()
-    _lib.call("si_initial_series", h, n, split.precond.data_ptr(), split.residual.data_ptr(),
-              split.matrix.data_ptr(), p, w, g.data_ptr(), f.data_ptr(), buf, s)
+    nrm = _step_call("si_initial_series", h, g, n, split.precond.data_ptr(),
+                     split.residual.data_ptr(), split.matrix.data_ptr(), p, w, g.data_ptr(),
+                     f.data_ptr(), buf, s)
     ctr.absorb(buf)
-    return NsState(estimate=g, residual=f, step=0, order=order, series_order=w * (p + 1), ctr=ctr)
+    return NsState(estimate=g, residual=f, step=0, order=order, series_order=w * (p + 1), ctr=ctr,
+                   residual_fro2=nrm)
 
 
 def ns_step(st: NsState, a, plan: FactorPlan | None = None, *, inputs_ready: dict | None = None,
@@ -155,14 +175,15 @@ def ns_step(st: NsState, a, plan: FactorPlan | None = None, *, inputs_ready: dic
         flags_ptr, epoch, npanels = _panel_args(input_panels, 48)
         chunks = list(residual_chunks or [])
         evs = (ctypes.c_void_p * max(len(chunks), 1))(*[e.cuda_event for e in chunks])
-        _lib.call("si_ns_step_gated", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
-                  st.residual.data_ptr(), n, _lib.i32_array(code) if code else None, len(code),
-                  _lib.f64_array(consts) if consts else None, len(consts), flags_ptr, epoch,
-                  npanels, estimate_done.cuda_event if estimate_done is not None else None,
-                  evs if chunks else None, len(chunks), g.data_ptr(), f.data_ptr(), buf, s)
+        nrm = _step_call("si_ns_step_gated", h, g, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
+                         st.residual.data_ptr(), n, _lib.i32_array(code) if code else None,
+                         len(code), _lib.f64_array(consts) if consts else None, len(consts),
+                         flags_ptr, epoch, npanels,
+                         estimate_done.cuda_event if estimate_done is not None else None,
+                         evs if chunks else None, len(chunks), g.data_ptr(), f.data_ptr(), buf, s)
         st.ctr.absorb(buf)
         return NsState(estimate=g, residual=f, step=st.step + 1, order=n,
-                       series_order=st.series_order, ctr=st.ctr)
+                       series_order=st.series_order, ctr=st.ctr, residual_fro2=nrm)
     ready = None
     if inputs_ready:
         order3 = ("a", "estimate", "residual")
@@ -171,14 +192,14 @@ def ns_step(st: NsState, a, plan: FactorPlan | None = None, *, inputs_ready: dic
             raise ValueError(f"unknown inputs in inputs_ready: {sorted(unknown)}")
         ready = (ctypes.c_void_p * 3)(
             *[inputs_ready[k].cuda_event if k in inputs_ready else None for k in order3])
-    _lib.call("si_ns_step_ex", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
-              st.residual.data_ptr(), n, _lib.i32_array(code) if code else None, len(code),
-              _lib.f64_array(consts) if consts else None, len(consts), ready,
-              estimate_done.cuda_event if estimate_done is not None else None, g.data_ptr(),
-              f.data_ptr(), buf, s)
+    nrm = _step_call("si_ns_step_ex", h, g, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
+                     st.residual.data_ptr(), n, _lib.i32_array(code) if code else None, len(code),
+                     _lib.f64_array(consts) if consts else None, len(consts), ready,
+                     estimate_done.cuda_event if estimate_done is not None else None, g.data_ptr(),
+                     f.data_ptr(), buf, s)
     st.ctr.absorb(buf)
     return NsState(estimate=g, residual=f, step=st.step + 1, order=n,
-                   series_order=st.series_order, ctr=st.ctr)
+                   series_order=st.series_order, ctr=st.ctr, residual_fro2=nrm)
 
 
 def _panel_args(input_panels, words: int):
@@ -265,12 +286,12 @@ def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_
         f = torch.empty_like(st.estimate)
         h, s = _ctx(g)
         buf = _lib.counter_buf()
-        _lib.call("si_composite_apply", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
-                  st.residual.data_ptr(), parts.t_comp.data_ptr(), parts.r_comp.data_ptr(),
-                  order_n, g.data_ptr(), f.data_ptr(), buf, s)
+        nrm = _step_call("si_composite_apply", h, g, a.shape[0], a.data_ptr(),
+                         st.estimate.data_ptr(), st.residual.data_ptr(), parts.t_comp.data_ptr(),
+                         parts.r_comp.data_ptr(), order_n, g.data_ptr(), f.data_ptr(), buf, s)
         st.ctr.absorb(buf)
         return NsState(estimate=g, residual=f, step=st.step + 1, order=order_n,
-                       series_order=st.series_order, ctr=st.ctr)
+                       series_order=st.series_order, ctr=st.ctr, residual_fro2=nrm)
     plans = [geometric_base_plan(x) if x > 1 else None for x in spec.rates]
     code, offsets, consts = encode_many(plans)
     g = torch.empty_like(st.estimate)
@@ -283,16 +304,17 @@ def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_
         flags_ptr, epoch, npanels = _panel_args(input_panels, 96)
         chunks = list(residual_chunks or [])
         evs = (ctypes.c_void_p * max(len(chunks), 1))(*[e.cuda_event for e in chunks])
-        _lib.call("si_composite_step_gated", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
-                  st.residual.data_ptr(), split.precond.data_ptr(), split.residual.data_ptr(),
-                  split.matrix.data_ptr(), len(spec.rates), _lib.i32_array(list(spec.rates)),
-                  _lib.i32_array(code), _lib.i64_array(offsets), _lib.f64_array(consts),
-                  len(consts), order_n, int(executor is not None), flags_ptr, epoch, npanels,
-                  estimate_done.cuda_event if estimate_done is not None else None,
-                  evs if chunks else None, len(chunks), g.data_ptr(), f.data_ptr(), buf, s)
+        nrm = _step_call("si_composite_step_gated", h, g, a.shape[0], a.data_ptr(),
+                         st.estimate.data_ptr(), st.residual.data_ptr(), split.precond.data_ptr(),
+                         split.residual.data_ptr(), split.matrix.data_ptr(), len(spec.rates),
+                         _lib.i32_array(list(spec.rates)), _lib.i32_array(code),
+                         _lib.i64_array(offsets), _lib.f64_array(consts), len(consts), order_n,
+                         int(executor is not None), flags_ptr, epoch, npanels,
+                         estimate_done.cuda_event if estimate_done is not None else None,
+                         evs if chunks else None, len(chunks), g.data_ptr(), f.data_ptr(), buf, s)
         st.ctr.absorb(buf)
         return NsState(estimate=g, residual=f, step=st.step + 1, order=order_n,
-                       series_order=st.series_order, ctr=st.ctr)
+                       series_order=st.series_order, ctr=st.ctr, residual_fro2=nrm)
     ready = None
     if inputs_ready:
         unknown = set(inputs_ready) - set(_READY_ORDER)
@@ -300,16 +322,16 @@ def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_
             raise ValueError(f"unknown inputs in inputs_ready: {sorted(unknown)}")
         ready = (ctypes.c_void_p * len(_READY_ORDER))(
             *[inputs_ready[k].cuda_event if k in inputs_ready else None for k in _READY_ORDER])
-    _lib.call("si_composite_step_ex", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
-              st.residual.data_ptr(), split.precond.data_ptr(), split.residual.data_ptr(),
-              split.matrix.data_ptr(), len(spec.rates), _lib.i32_array(list(spec.rates)),
-              _lib.i32_array(code), _lib.i64_array(offsets), _lib.f64_array(consts), len(consts),
-              order_n, int(executor is not None), ready,
-              estimate_done.cuda_event if estimate_done is not None else None, g.data_ptr(),
-              f.data_ptr(), buf, s)
+    nrm = _step_call("si_composite_step_ex", h, g, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
+                     st.residual.data_ptr(), split.precond.data_ptr(), split.residual.data_ptr(),
+                     split.matrix.data_ptr(), len(spec.rates), _lib.i32_array(list(spec.rates)),
+                     _lib.i32_array(code), _lib.i64_array(offsets), _lib.f64_array(consts),
+                     len(consts), order_n, int(executor is not None), ready,
+                     estimate_done.cuda_event if estimate_done is not None else None, g.data_ptr(),
+                     f.data_ptr(), buf, s)
     st.ctr.absorb(buf)
     return NsState(estimate=g, residual=f, step=st.step + 1, order=order_n,
-                   series_order=st.series_order, ctr=st.ctr)
+                   series_order=st.series_order, ctr=st.ctr, residual_fro2=nrm)
 
 
 def initial_double(split: Splitting, p: int, w: int, order: int = 2) -> DoubleNsState:
@@ -323,12 +345,12 @@ def initial_double(split: Splitting, p: int, w: int, order: int = 2) -> DoubleNs
     g, f, l, r = (torch.empty_like(m) for _ in range(4))
     h, s = _ctx(m)
     buf = _lib.counter_buf()
-    _lib.call("si_initial_double", h, m.shape[0], split.precond.data_ptr(), split.residual.data_ptr(),
-              m.data_ptr(), p, w, order, g.data_ptr(), f.data_ptr(), l.data_ptr(), r.data_ptr(),
-              buf, s)
+    nrm = _step_call("si_initial_double", h, m, m.shape[0], split.precond.data_ptr(),
+                     split.residual.data_ptr(), m.data_ptr(), p, w, order, g.data_ptr(),
+                     f.data_ptr(), l.data_ptr(), r.data_ptr(), buf, s)
     ctr.absorb(buf)
     return DoubleNsState(estimate=g, residual=f, accel_estimate=l, accel_residual=r, step=0,
-                         order=order, series_order=w * (p + 1), ctr=ctr)
+                         order=order, series_order=w * (p + 1), ctr=ctr, residual_fro2=nrm)
 
 
 def double_ns_step(st: DoubleNsState, a, executor=None) -> DoubleNsState:
@@ -339,13 +361,14 @@ def double_ns_step(st: DoubleNsState, a, executor=None) -> DoubleNsState:
     g, f, l, r = (torch.empty_like(st.estimate) for _ in range(4))
     h, s = _ctx(g)
     buf = _lib.counter_buf()
-    _lib.call("si_double_ns_step", h, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
-              st.residual.data_ptr(), st.accel_estimate.data_ptr(), st.accel_residual.data_ptr(),
-              st.order, int(executor is not None), g.data_ptr(), f.data_ptr(), l.data_ptr(),
-              r.data_ptr(), buf, s)
+    nrm = _step_call("si_double_ns_step", h, g, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
+                     st.residual.data_ptr(), st.accel_estimate.data_ptr(),
+                     st.accel_residual.data_ptr(), st.order, int(executor is not None),
+                     g.data_ptr(), f.data_ptr(), l.data_ptr(), r.data_ptr(), buf, s)
     st.ctr.absorb(buf)
     return DoubleNsState(estimate=g, residual=f, accel_estimate=l, accel_residual=r,
-                         step=st.step + 1, order=st.order, series_order=st.series_order, ctr=st.ctr)
+                         step=st.step + 1, order=st.order, series_order=st.series_order,
+                         ctr=st.ctr, residual_fro2=nrm)
 
 
 def additive_correction_step(z, g, a, p: int, ctr: MulCounter):
@@ -366,7 +389,9 @@ def additive_correction_step(z, g, a, p: int, ctr: MulCounter):
 def converged(st) -> bool:
     """||F_k||_F <= 1e-13 sqrt(n) (newton_schulz.py:328-331)."""
     dim = st.residual.shape[0]
-    return fro_norm(st.residual) <= 1e-13 * sqrt(dim)
+    fro2 = getattr(st, "residual_fro2", None)
+    norm = sqrt(float(fro2.item())) if fro2 is not None else fro_norm(st.residual)
+    return norm <= 1e-13 * sqrt(dim)
 
 
 def run_until_converged(st: NsState, a, max_steps: int = DEFAULT_MAX_STEPS) -> NsState:

@@ -134,3 +134,15 @@ def test_backend_entry_points_validate_without_gpu():
     assert list(mods)[:3] == [256, 255, 253]
     assert lib.si_i8_gemm_mod(None, None, None, None, 1, 1, 128, 1, None) == E
     assert lib.si_profile_i8(None, None, None, None) == E
+
+
+def test_step_norm_entry_point_validates_without_gpu():
+    """si_set_step_norm (the fused ||F'||_F^2 target of the next step call)
+    rejects a null handle; a step call with a null handle still returns
+    SI_EINVAL (it consumes a target before its argument checks)."""
+    from paper_2008_11480_b200 import _lib
+
+    lib = _lib.load_library()
+    assert lib.si_set_step_norm(None, None) == _lib.SI_EINVAL
+    assert lib.si_ns_step(None, 4, None, None, None, 2, None, 0, None, 0, None, None, None,
+                          None) == _lib.SI_EINVAL
