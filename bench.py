@@ -324,7 +324,28 @@ def make_comm(n: int, kind: str):
     if SHARE_GPU:
         # ranks sharing one GPU must not spin in kernels on each other's panels
         kind = "peer-stream"
-    return PeerComm(n, IpcFabric(dev), mode="fused" if kind == "peer" else "stream")
+    # The peer exchange needs CUDA IPC mappings and peer access between every
+    # pair of GPUs.  If any rank cannot set it up (no P2P between two devices,
+    # IPC disabled in a container), every rank falls back to the NCCL
+    # all-gather together and the JSON line says so (``comm_fallback``).
+    import torch.distributed as dist
+
+    comm, why = None, ""
+    try:
+        comm = PeerComm(n, IpcFabric(dev), mode="fused" if kind == "peer" else "stream")
+    except Exception as exc:  # noqa: BLE001 -- any set-up failure takes the fallback
+        why = f"{type(exc).__name__}: {exc}"[:200]
+    ok = torch.tensor([1 if comm is not None else 0], dtype=torch.int32,
+                      device="cpu" if SHARE_GPU else dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if int(ok.item()) == 1:
+        return comm
+    COMM_FALLBACK["reason"] = why or "peer exchange set-up failed on another rank"
+    del comm
+    return RowComm(n)
+
+
+COMM_FALLBACK: dict = {}
 
 
 _COMM_LABEL = {"peer": "copy-engine panel exchange, panel-gated products",
@@ -946,13 +967,35 @@ class Workload:
 
     def e2e_step_c5(self, host):
         """One steady-state recursive step (factorised order 16, the bench DAG)
-        through the public API from host buffers: H2D of the inputs, the step,
-        D2H of the new state and theta."""
+        through the public API from host buffers, copies overlapped with the
+        step: the inputs go H2D on a copy stream in the order the DAG first
+        reads them (R for the power sum, L, A, omega, N, b, theta; G and F,
+        which the steady-state DAG does not read, last), each behind an event
+        the step waits on right before that input's first use; every field of
+        the new state goes D2H on a second copy stream as soon as the step
+        records it final (L', R', G', F', N', omega', theta')."""
         import torch
 
         P = self.P
         dev = torch.device("cuda", torch.cuda.current_device())
-        d = {k: v.to(dev, non_blocking=True) for k, v in host["in"].items()}
+        main = torch.cuda.current_stream(dev)
+        if not hasattr(self, "_copy_streams"):
+            self._copy_streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+        up, down = self._copy_streams
+        names = {"a": "a", "b": "b", "theta": "theta", "g": "estimate", "f": "residual",
+                 "l": "accel_estimate", "r": "accel_residual", "omega": "omega", "ns": "ns_part"}
+        order = ("r", "l", "a", "omega", "ns", "b", "theta", "g", "f")
+        # buffers from the step's own (main-stream) pool, as the unoverlapped
+        # call had them: at n = 32768 the step runs at the edge of the 180 GB
+        d = {k: torch.empty(host["in"][k].shape, dtype=torch.float64, device=dev) for k in order}
+        up.wait_stream(main)
+        ready = {}
+        with torch.cuda.stream(up):
+            for k in order:
+                d[k].record_stream(up)
+                d[k].copy_(host["in"][k], non_blocking=True)
+                ready[names[k]] = torch.cuda.Event()
+                ready[names[k]].record(up)
         inner = P.DoubleNsState(estimate=d["g"], residual=d["f"], accel_estimate=d["l"],
                                 accel_residual=d["r"], step=1, order=16, series_order=1,
                                 ctr=P.MulCounter())
@@ -960,13 +1003,25 @@ class Workload:
                                ns_part=d["ns"], step=1, ctr=inner.ctr)
         a, b = d.pop("a"), d.pop("b")
         del d
-        new = P.richardson_recursive_step(st, a, b, factor_plan=self.plan16, doubling_sum=True)
+        outs = ("accel_estimate", "accel_residual", "estimate", "residual", "ns_part", "omega",
+                "theta")
+        done = {k: torch.cuda.Event() for k in outs}
+        new = P.richardson_recursive_step(st, a, b, factor_plan=self.plan16, doubling_sum=True,
+                                          inputs_ready=ready, outputs_done=done)
         del st, inner
         out = host["out"]
-        for k, v in (("theta", new.theta), ("g", new.inner.estimate), ("f", new.inner.residual),
-                     ("l", new.inner.accel_estimate), ("r", new.inner.accel_residual),
-                     ("omega", new.omega), ("ns", new.ns_part)):
-            out[k].copy_(v, non_blocking=True)
+        fields = {"accel_estimate": ("l", new.inner.accel_estimate),
+                  "accel_residual": ("r", new.inner.accel_residual),
+                  "estimate": ("g", new.inner.estimate), "residual": ("f", new.inner.residual),
+                  "ns_part": ("ns", new.ns_part), "omega": ("omega", new.omega),
+                  "theta": ("theta", new.theta)}
+        for k in outs:  # the order the step finishes them in
+            hk, v = fields[k]
+            down.wait_event(done[k])
+            v.record_stream(down)
+            with torch.cuda.stream(down):
+                out[hk].copy_(v, non_blocking=True)
+        main.wait_stream(down)
         h2d = sum(v.numel() * 8 for v in host["in"].values())
         d2h = sum(v.numel() * 8 for v in out.values())
         return h2d, d2h
@@ -1442,8 +1497,9 @@ def run_ours(args):
             e_ms = max_over_ranks(f0.elapsed_time(f1), world)
             e2e = {"value": world / (e_ms / 1e3), "unit": "iters/s",
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": 1,
-                   "note": "copies not overlapped with the step (A, b, theta and the six "
-                           "carried n x n matrices in, the new state and theta out)"}
+                   "note": "A, b, theta and the six carried n x n matrices in, the new state "
+                           "and theta out; copies overlapped with the step per input / "
+                           "output (si_richardson_recursive_step_ex)"}
             del host
         except (RuntimeError, MemoryError) as exc:  # pinned host memory exhausted, ...
             e2e = {"unavailable": f"c5 e2e failed: {exc}"[:200]}
@@ -1471,7 +1527,7 @@ def run_ours(args):
             "config": config_of(w),
             "parallelism": layout_note(w) + (f"composite parts on GPU groups x{world} (NCCL p2p tree)"
                             if w.sharded is not None and "gc" in w.sharded
-                            else f"block-row x{world} ({_COMM_LABEL[args.comm]})"
+                            else f"block-row x{world} ({_COMM_LABEL['nccl' if COMM_FALLBACK else args.comm]})"
                             if w.sharded is not None
                             else f"batch split x{world} (no communication)" if w.split_batch
                             else (f"replicas x{world}" if world > 1 else "single-gpu")),
@@ -1494,6 +1550,9 @@ def run_ours(args):
             "hbm_peak_gb": torch.cuda.max_memory_allocated() / 1e9,
             "clocks": clocks,
         }
+        if COMM_FALLBACK:
+            line["comm_fallback"] = ("peer exchange unavailable, NCCL all-gather used: "
+                                     + COMM_FALLBACK["reason"])
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -416,6 +416,28 @@ SI_API int si_richardson_recursive_step(si_handle h, int64_t n, int64_t nrhs, co
                                  int concurrent, double* g_out, double* f_out, double* l_out,
                                  double* r_out, double* omega_out, double* ns_out,
                                  double* theta_out, int64_t* counters, void* stream);
+/* si_richardson_recursive_step with host-copy overlap (the numpy-facing call
+ * at n = 32768 moves 69 GB in and 60 GB out per step).  input_ready_events
+ * (may be NULL) = 9 cudaEvent_t, each may be NULL, for {a, b, theta, g, f, l,
+ * r, omega, ns_part}: the step makes its stream wait on an input's event right
+ * before the first kernel that reads it (inputs the DAG does not read -- g
+ * and f in the steady state -- are waited for at the end of the call).
+ * output_done_events (may be NULL) = 7 cudaEvent_t, each may be NULL, for
+ * {l_out, r_out, g_out, f_out, ns_out, omega_out, theta_out}, recorded once
+ * that output is final (in this order on the serial path), so it can be read
+ * back while the remaining products run.  Same products, bitwise the plain
+ * call. */
+SI_API int si_richardson_recursive_step_ex(si_handle h, int64_t n, int64_t nrhs, const double* a,
+                                    const double* b, const double* theta, const double* g,
+                                    const double* f, const double* l, const double* r,
+                                    const double* omega, const double* ns_part, int order,
+                                    const int32_t* factor_plan, int64_t plan_len,
+                                    const double* consts, int64_t nconsts, int doubling_sum,
+                                    int concurrent, void* const* input_ready_events,
+                                    void* const* output_done_events, double* g_out,
+                                    double* f_out, double* l_out, double* r_out,
+                                    double* omega_out, double* ns_out, double* theta_out,
+                                    int64_t* counters, void* stream);
 /* Plain update theta' = theta - P (A theta - b)  (ordering as
  * richardson.py:88-89). */
 SI_API int si_plain_richardson(si_handle h, int64_t n, int64_t nrhs, const double* a, const double* b,

@@ -97,6 +97,10 @@ SIGNATURES: dict[str, list] = {
         _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I64, _P, _I64, _I, _I,
         _P, _P, _P, _P, _P, _P, _P, _PI64, _P,
     ],
+    "si_richardson_recursive_step_ex": [
+        _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _I64, _P, _I64, _I, _I,
+        _P, _P, _P, _P, _P, _P, _P, _P, _P, _PI64, _P,
+    ],
     "si_plain_richardson": [_P, _I64, _I64, _P, _P, _P, _P, _P, _PI64, _P],
     "si_profile_begin": [_P],
     "si_profile_end": [_P, POINTER(c_double), POINTER(c_double), _PI64, _PI64],
@@ -245,6 +249,25 @@ def ptr(t: torch.Tensor | None) -> int | None:
     if t is None:
         return None
     return t.data_ptr()
+
+
+def event_ptr(ev, recorded: bool = False) -> int | None:
+    """The ``cudaEvent_t`` of a ``torch.cuda.Event`` for the C ABI (None -> NULL).
+
+    torch creates the underlying CUDA event lazily, at its first ``record``:
+    a fresh ``Event()`` has ``cuda_event == 0``, and passing that would make
+    the library skip the record and every later ``wait_event`` a no-op.  An
+    event the LIBRARY is to record (``recorded=False``) is therefore recorded
+    once here on the current stream to create it (the library's record
+    replaces that one); an event the CALLER recorded (``recorded=True``, the
+    inputs-ready events) must exist already."""
+    if ev is None:
+        return None
+    if not ev.cuda_event:
+        if recorded:
+            raise ValueError("an input-ready event must be recorded before the call")
+        ev.record(torch.cuda.current_stream())
+    return ev.cuda_event
 
 
 def i32_array(values) -> ctypes.Array:

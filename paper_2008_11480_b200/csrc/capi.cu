@@ -912,6 +912,54 @@ int si_richardson_step(si_handle h, int64_t n, int64_t nrhs, const double* a, co
   });
 }
 
+namespace {
+int recursive_step_impl(si_handle h, int64_t n, int64_t nrhs, const double* a, const double* b,
+                        const double* theta, const double* g, const double* f, const double* l,
+                        const double* r, const double* omega, const double* ns_part, int order,
+                        const int32_t* factor_plan, int64_t plan_len, const double* consts,
+                        int64_t nconsts, int doubling_sum, int concurrent,
+                        void* const* input_ready_events, void* const* output_done_events,
+                        double* g_out, double* f_out, double* l_out, double* r_out,
+                        double* omega_out, double* ns_out, double* theta_out, int64_t* counters,
+                        void* stream) {
+  return guard([&] {
+    need(h && a && b && theta && g && f && l && r && g_out && f_out && l_out && r_out &&
+             omega_out && ns_out && theta_out,
+         "null pointer");
+    need(nrhs >= 1, "nrhs must be >= 1");
+    PlanPtr pl = opt_plan(factor_plan, plan_len, consts, nconsts);
+    if (pl) need(plan_order_of(*pl) == order, "factor plan order != iteration order");
+    Call call(h, stream, counters);
+    if (input_ready_events) {
+      const double* bases[9] = {a, b, theta, g, f, l, r, omega, ns_part};
+      for (int i = 0; i < 9; ++i)
+        if (input_ready_events[i] && bases[i])
+          call.c.awaits.push_back({bases[i], reinterpret_cast<cudaEvent_t>(input_ready_events[i]),
+                                   false});
+    }
+    cudaEvent_t done[kRecOutputs] = {};
+    if (output_done_events)
+      for (int i = 0; i < kRecOutputs; ++i)
+        done[i] = reinterpret_cast<cudaEvent_t>(output_done_events[i]);
+    MV om = omega ? sq(omega, n) : MV{}, nsp = ns_part ? sq(ns_part, n) : MV{};
+    richardson_recursive_step(call.c, sq(a, n), rect(b, n, nrhs), rect(theta, n, nrhs), sq(g, n),
+                              sq(f, n), sq(l, n), sq(r, n), omega ? &om : nullptr,
+                              ns_part ? &nsp : nullptr, order, concurrent != 0, pl.get(),
+                              doubling_sum != 0, sq(g_out, n), sq(f_out, n), sq(l_out, n),
+                              sq(r_out, n), sq(omega_out, n), sq(ns_out, n),
+                              rect(theta_out, n, nrhs), output_done_events ? done : nullptr);
+    // inputs the DAG did not read (g, f in the steady state) are part of the
+    // call's state all the same: the stream does not leave the call before
+    // their copies have landed
+    for (auto& aw : call.c.awaits)
+      if (!aw.done) {
+        check(cudaStreamWaitEvent(call.c.s, aw.ev, 0), "cudaStreamWaitEvent");
+        aw.done = true;
+      }
+  });
+}
+}  // namespace
+
 int si_richardson_recursive_step(si_handle h, int64_t n, int64_t nrhs, const double* a,
                                  const double* b, const double* theta, const double* g,
                                  const double* f, const double* l, const double* r,
@@ -921,22 +969,27 @@ int si_richardson_recursive_step(si_handle h, int64_t n, int64_t nrhs, const dou
                                  int concurrent, double* g_out, double* f_out, double* l_out,
                                  double* r_out, double* omega_out, double* ns_out,
                                  double* theta_out, int64_t* counters, void* stream) {
-  return guard([&] {
-    need(h && a && b && theta && g && f && l && r && g_out && f_out && l_out && r_out &&
-             omega_out && ns_out && theta_out,
-         "null pointer");
-    need(nrhs >= 1, "nrhs must be >= 1");
-    PlanPtr pl = opt_plan(factor_plan, plan_len, consts, nconsts);
-    if (pl) need(plan_order_of(*pl) == order, "factor plan order != iteration order");
-    Call call(h, stream, counters);
-    MV om = omega ? sq(omega, n) : MV{}, nsp = ns_part ? sq(ns_part, n) : MV{};
-    richardson_recursive_step(call.c, sq(a, n), rect(b, n, nrhs), rect(theta, n, nrhs), sq(g, n),
-                              sq(f, n), sq(l, n), sq(r, n), omega ? &om : nullptr,
-                              ns_part ? &nsp : nullptr, order, concurrent != 0, pl.get(),
-                              doubling_sum != 0, sq(g_out, n), sq(f_out, n), sq(l_out, n),
-                              sq(r_out, n), sq(omega_out, n), sq(ns_out, n),
-                              rect(theta_out, n, nrhs));
-  });
+  return recursive_step_impl(h, n, nrhs, a, b, theta, g, f, l, r, omega, ns_part, order,
+                             factor_plan, plan_len, consts, nconsts, doubling_sum, concurrent,
+                             nullptr, nullptr, g_out, f_out, l_out, r_out, omega_out, ns_out,
+                             theta_out, counters, stream);
+}
+
+int si_richardson_recursive_step_ex(si_handle h, int64_t n, int64_t nrhs, const double* a,
+                                    const double* b, const double* theta, const double* g,
+                                    const double* f, const double* l, const double* r,
+                                    const double* omega, const double* ns_part, int order,
+                                    const int32_t* factor_plan, int64_t plan_len,
+                                    const double* consts, int64_t nconsts, int doubling_sum,
+                                    int concurrent, void* const* input_ready_events,
+                                    void* const* output_done_events, double* g_out,
+                                    double* f_out, double* l_out, double* r_out,
+                                    double* omega_out, double* ns_out, double* theta_out,
+                                    int64_t* counters, void* stream) {
+  return recursive_step_impl(h, n, nrhs, a, b, theta, g, f, l, r, omega, ns_part, order,
+                             factor_plan, plan_len, consts, nconsts, doubling_sum, concurrent,
+                             input_ready_events, output_done_events, g_out, f_out, l_out, r_out,
+                             omega_out, ns_out, theta_out, counters, stream);
 }
 
 int si_plain_richardson(si_handle h, int64_t n, int64_t nrhs, const double* a, const double* b,

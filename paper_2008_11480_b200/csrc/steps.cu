@@ -292,9 +292,16 @@ void richardson_recursive_step(Ctx& c, const MV& A, const MV& b, const MV& theta
                                const MV* ns_part, int order, bool concurrent,
                                const PlanNode* factor_plan, bool doubling_sum,
                                const MV& Gout, const MV& Fout, const MV& Lout, const MV& Rout,
-                               const MV& omega_out, const MV& ns_out, const MV& theta_out) {
+                               const MV& omega_out, const MV& ns_out, const MV& theta_out,
+                               const cudaEvent_t* out_done) {
   const int n = order;
   if (n < 1) throw Error(kEInval, "order must be >= 1");
+  // an output may go device->host as soon as it is final (its event fires on
+  // the stream that wrote it; later products only read it)
+  auto done = [&](Ctx& cc, int which) {
+    if (out_done && out_done[which])
+      check(cudaEventRecord(out_done[which], cc.s), "cudaEventRecord");
+  };
   MV ns_prev, om_prev;
   if (!omega || !ns_part) {
     ns_prev = horner(c, F, G, n);
@@ -310,14 +317,18 @@ void richardson_recursive_step(Ctx& c, const MV& A, const MV& b, const MV& theta
       MV diff = lincomb(cc, 0.0, {{1.0, &om_prev}, {-1.0, &ns_prev}}, G.v.rows, G.v.cols);
       gemm(cc, Gout, s, diff, 1.0, &ns_prev, 1.0);  // S (om - ns) + ns
     }
+    done(cc, kRecG);
     if (after_g) after_g(cc);
     residual_into(cc, Fout, Gout, A);
+    done(cc, kRecF);
     nsn = factor_plan ? eval_node(cc, *factor_plan, Fout, Gout, A) : horner(cc, Fout, Gout, n);
   };
   auto estimate = [&](Ctx& cc) { estimate_then(cc, nullptr); };
   auto accel = [&](Ctx& cc) {
     gemm(cc, Lout, s, L);
+    done(cc, kRecL);
     residual_into(cc, Rout, Lout, A);
+    done(cc, kRecR);
   };
   if (concurrent) {
     Fork fk(c);
@@ -339,9 +350,12 @@ void richardson_recursive_step(Ctx& c, const MV& A, const MV& b, const MV& theta
     estimate_then(c, release_s);
   }
   copy_into(c, ns_out, nsn);
+  done(c, kRecNs);
   gemm(c, omega_out, Rout, ns_out, 1.0, &Lout, 1.0);              // L' + R' N'
+  done(c, kRecOmega);
   MV resid = gemm_new(c, A, theta, 1.0, &b, -1.0, 0.0, true);     // A theta - b
   gemm(c, theta_out, omega_out, resid, -1.0, &theta, 1.0, 0.0, true);
+  done(c, kRecTheta);
 }
 
 // theta + P (b - A theta), evaluated as ri:88-89 does.

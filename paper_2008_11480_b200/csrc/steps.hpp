@@ -53,7 +53,10 @@ void richardson_recursive_step(Ctx& c, const MV& A, const MV& b, const MV& theta
                                const MV* ns_part, int order, bool concurrent,
                                const PlanNode* factor_plan, bool doubling_sum,
                                const MV& Gout, const MV& Fout, const MV& Lout, const MV& Rout,
-                               const MV& omega_out, const MV& ns_out, const MV& theta_out);
+                               const MV& omega_out, const MV& ns_out, const MV& theta_out,
+                               const cudaEvent_t* out_done = nullptr);
+// indices of `out_done` (each may be null): recorded once that output is final
+enum { kRecL = 0, kRecR, kRecG, kRecF, kRecNs, kRecOmega, kRecTheta, kRecOutputs };
 void plain_richardson(Ctx& c, const MV& A, const MV& b, const MV& theta, const MV& P,
                       const MV& theta_out);
 

@@ -174,12 +174,12 @@ def ns_step(st: NsState, a, plan: FactorPlan | None = None, *, inputs_ready: dic
             raise ValueError("inputs_ready and input_panels are exclusive")
         flags_ptr, epoch, npanels = _panel_args(input_panels, 48)
         chunks = list(residual_chunks or [])
-        evs = (ctypes.c_void_p * max(len(chunks), 1))(*[e.cuda_event for e in chunks])
+        evs = (ctypes.c_void_p * max(len(chunks), 1))(*[_lib.event_ptr(e) for e in chunks])
         nrm = _step_call("si_ns_step_gated", h, g, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
                          st.residual.data_ptr(), n, _lib.i32_array(code) if code else None,
                          len(code), _lib.f64_array(consts) if consts else None, len(consts),
                          flags_ptr, epoch, npanels,
-                         estimate_done.cuda_event if estimate_done is not None else None,
+                         _lib.event_ptr(estimate_done),
                          evs if chunks else None, len(chunks), g.data_ptr(), f.data_ptr(), buf, s)
         st.ctr.absorb(buf)
         return NsState(estimate=g, residual=f, step=st.step + 1, order=n,
@@ -191,11 +191,11 @@ def ns_step(st: NsState, a, plan: FactorPlan | None = None, *, inputs_ready: dic
         if unknown:
             raise ValueError(f"unknown inputs in inputs_ready: {sorted(unknown)}")
         ready = (ctypes.c_void_p * 3)(
-            *[inputs_ready[k].cuda_event if k in inputs_ready else None for k in order3])
+            *[_lib.event_ptr(inputs_ready.get(k), recorded=True) for k in order3])
     nrm = _step_call("si_ns_step_ex", h, g, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
                      st.residual.data_ptr(), n, _lib.i32_array(code) if code else None, len(code),
                      _lib.f64_array(consts) if consts else None, len(consts), ready,
-                     estimate_done.cuda_event if estimate_done is not None else None, g.data_ptr(),
+                     _lib.event_ptr(estimate_done), g.data_ptr(),
                      f.data_ptr(), buf, s)
     st.ctr.absorb(buf)
     return NsState(estimate=g, residual=f, step=st.step + 1, order=n,
@@ -303,14 +303,14 @@ def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_
             raise ValueError("inputs_ready and input_panels are exclusive")
         flags_ptr, epoch, npanels = _panel_args(input_panels, 96)
         chunks = list(residual_chunks or [])
-        evs = (ctypes.c_void_p * max(len(chunks), 1))(*[e.cuda_event for e in chunks])
+        evs = (ctypes.c_void_p * max(len(chunks), 1))(*[_lib.event_ptr(e) for e in chunks])
         nrm = _step_call("si_composite_step_gated", h, g, a.shape[0], a.data_ptr(),
                          st.estimate.data_ptr(), st.residual.data_ptr(), split.precond.data_ptr(),
                          split.residual.data_ptr(), split.matrix.data_ptr(), len(spec.rates),
                          _lib.i32_array(list(spec.rates)), _lib.i32_array(code),
                          _lib.i64_array(offsets), _lib.f64_array(consts), len(consts), order_n,
                          int(executor is not None), flags_ptr, epoch, npanels,
-                         estimate_done.cuda_event if estimate_done is not None else None,
+                         _lib.event_ptr(estimate_done),
                          evs if chunks else None, len(chunks), g.data_ptr(), f.data_ptr(), buf, s)
         st.ctr.absorb(buf)
         return NsState(estimate=g, residual=f, step=st.step + 1, order=order_n,
@@ -321,13 +321,13 @@ def composite_step(st: NsState, a, split: Splitting, spec: CompositeSpec, order_
         if unknown:
             raise ValueError(f"unknown inputs in inputs_ready: {sorted(unknown)}")
         ready = (ctypes.c_void_p * len(_READY_ORDER))(
-            *[inputs_ready[k].cuda_event if k in inputs_ready else None for k in _READY_ORDER])
+            *[_lib.event_ptr(inputs_ready.get(k), recorded=True) for k in _READY_ORDER])
     nrm = _step_call("si_composite_step_ex", h, g, a.shape[0], a.data_ptr(), st.estimate.data_ptr(),
                      st.residual.data_ptr(), split.precond.data_ptr(), split.residual.data_ptr(),
                      split.matrix.data_ptr(), len(spec.rates), _lib.i32_array(list(spec.rates)),
                      _lib.i32_array(code), _lib.i64_array(offsets), _lib.f64_array(consts),
                      len(consts), order_n, int(executor is not None), ready,
-                     estimate_done.cuda_event if estimate_done is not None else None, g.data_ptr(),
+                     _lib.event_ptr(estimate_done), g.data_ptr(),
                      f.data_ptr(), buf, s)
     st.ctr.absorb(buf)
     return NsState(estimate=g, residual=f, step=st.step + 1, order=order_n,

@@ -8,6 +8,7 @@ theta + P (b - A theta) with products ordered as richardson.py:88-89.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
@@ -100,14 +101,37 @@ def richardson_step(st: RichardsonState, a, b) -> RichardsonState:
                            ns_part=None, step=st.step + 1, ctr=st.ctr)
 
 
+_RECURSIVE_INPUTS = ("a", "b", "theta", "estimate", "residual", "accel_estimate",
+                     "accel_residual", "omega", "ns_part")
+_RECURSIVE_OUTPUTS = ("accel_estimate", "accel_residual", "estimate", "residual", "ns_part",
+                      "omega", "theta")
+
+
+def _event_array(events: dict | None, names: tuple, what: str, recorded: bool):
+    if not events:
+        return None
+    unknown = set(events) - set(names)
+    if unknown:
+        raise ValueError(f"unknown names in {what}: {sorted(unknown)}")
+    return (ctypes.c_void_p * len(names))(
+        *[_lib.event_ptr(events.get(k), recorded=recorded) for k in names])
+
+
 def richardson_recursive_step(st: RichardsonState, a, b, executor=None, *,
                               factor_plan: FactorPlan | None = None,
-                              doubling_sum: bool = False) -> RichardsonState:
+                              doubling_sum: bool = False, inputs_ready: dict | None = None,
+                              outputs_done: dict | None = None) -> RichardsonState:
     """Recursive form, q == n only (richardson.py:111-189).
 
     Opt-in (not in the reference; changes the GEMM count): ``factor_plan`` of
     order n evaluates N' through a factorised plan and ``doubling_sum``
-    builds S = prod (I + Gamma^(2^j)) for power-of-two n."""
+    builds S = prod (I + Gamma^(2^j)) for power-of-two n.
+
+    Host-copy overlap (``si_richardson_recursive_step_ex``): ``inputs_ready``
+    maps input names (``a``, ``b``, ``theta`` and the state fields) to CUDA
+    events recorded behind their host->device copies -- the step waits for an
+    input right before its first use; ``outputs_done`` maps the new state's
+    field names to events the step records once that field is final."""
     n = st.inner.order
     if st.q != n:
         raise ValueError("the recursive form requires q == n")
@@ -124,14 +148,17 @@ def richardson_recursive_step(st: RichardsonState, a, b, executor=None, *,
     g, f, l, rr, om, nsp = (torch.empty_like(prev.estimate) for _ in range(6))
     theta = torch.empty_like(th2)
     buf = _lib.counter_buf()
-    _lib.call("si_richardson_recursive_step", _lib.handle(a.device.index), a.shape[0], r,
+    ready = _event_array(inputs_ready, _RECURSIVE_INPUTS, "inputs_ready", True)
+    done = _event_array(outputs_done, _RECURSIVE_OUTPUTS, "outputs_done", False)
+    _lib.call("si_richardson_recursive_step_ex", _lib.handle(a.device.index), a.shape[0], r,
               a.data_ptr(), b2.data_ptr(), th2.data_ptr(), prev.estimate.data_ptr(),
               prev.residual.data_ptr(), prev.accel_estimate.data_ptr(),
               prev.accel_residual.data_ptr(), _lib.ptr(st.omega), _lib.ptr(st.ns_part), n,
               _lib.i32_array(code) if code else None, len(code),
               _lib.f64_array(consts) if consts else None, len(consts), int(doubling_sum),
-              int(executor is not None), g.data_ptr(), f.data_ptr(), l.data_ptr(), rr.data_ptr(),
-              om.data_ptr(), nsp.data_ptr(), theta.data_ptr(), buf, _lib.stream_ptr(a.device))
+              int(executor is not None), ready, done, g.data_ptr(), f.data_ptr(), l.data_ptr(),
+              rr.data_ptr(), om.data_ptr(), nsp.data_ptr(), theta.data_ptr(), buf,
+              _lib.stream_ptr(a.device))
     st.ctr.absorb(buf)
     inner = DoubleNsState(estimate=g, residual=f, accel_estimate=l, accel_residual=rr,
                           step=prev.step + 1, order=n, series_order=prev.series_order, ctr=st.ctr)

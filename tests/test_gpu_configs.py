@@ -199,9 +199,22 @@ def _inputs_in_row_panels(P, _lib, configs, concurrent, n, npanels):
     sp2 = P.Splitting(precond=d["p"], residual=d["b"], matrix=d["a"], kind="scalar", verify=False)
     chunks = [torch.cuda.Event() for _ in range(4)]
     done = torch.cuda.Event()
+    # G' / F' read back row block by row block behind the events the step
+    # records (the host buffers exist before the call: pinned allocation
+    # synchronises the device and would hide an ungated read-back)
+    back_g = torch.zeros(n, n, dtype=torch.float64).pin_memory()
+    back_f = torch.zeros(n, n, dtype=torch.float64).pin_memory()
+    down = torch.cuda.Stream()
     out = P.composite_step(st2, sp2.matrix, sp2, spec, 2, object() if concurrent else None,
                            input_panels=(flags, 3, npanels), residual_chunks=chunks,
                            estimate_done=done)
+    assert all(e.cuda_event for e in chunks) and done.cuda_event  # created, not lazy nulls
+    cb = [n * k // len(chunks) for k in range(len(chunks) + 1)]
+    for k, e in enumerate(chunks):
+        down.wait_event(e)
+        with torch.cuda.stream(down):
+            back_g[cb[k]:cb[k + 1]].copy_(out.estimate[cb[k]:cb[k + 1]], non_blocking=True)
+            back_f[cb[k]:cb[k + 1]].copy_(out.residual[cb[k]:cb[k + 1]], non_blocking=True)
     with torch.cuda.stream(up):
         big2.copy_(big, non_blocking=True)  # the step is already waiting on the flags
         for k in ("b", "p", "a", "g", "f"):
@@ -216,6 +229,7 @@ def _inputs_in_row_panels(P, _lib, configs, concurrent, n, npanels):
     assert torch.equal(out.residual, ref.residual)
     assert out.ctr.mmm == n_ref
     assert all(e.query() for e in chunks)
+    assert torch.equal(back_g, ref.estimate.cpu()) and torch.equal(back_f, ref.residual.cpu())
 
 
 def test_ns_step_with_inputs_in_flight():

@@ -146,3 +146,83 @@ def test_recursive_executor_bitwise_and_acceleration():
         plain = P.ns_step(plain, a)
     theta_plain = P.mat_vec(plain.estimate, b, plain.ctr)
     assert np.linalg.norm(_np(rich.theta) - ts) <= np.linalg.norm(_np(theta_plain) - ts)
+
+
+@pytest.mark.parametrize("backend,concurrent,factorised", [
+    ("dmma", False, False), ("dmma", True, True), ("ozaki", False, True)])
+def test_recursive_step_with_copies_in_flight(backend, concurrent, factorised):
+    """si_richardson_recursive_step_ex: every input copied host->device on another
+    stream behind its own event, every field of the new state read back behind
+    the event the step records for it -- bitwise the plain call (first call and
+    steady state), same product counts."""
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import configs
+
+    n, rhs = 1024, 4
+    a, _ = configs.c3_gram(n=n, shift=1e-3)
+    b = np.random.default_rng(5).standard_normal((n, rhs))
+    sp = P.split_scalar(a, P.inf_norm(a) / 2.0, check_pd=False)
+    bd = P.as_device(b)
+    kw = dict(factor_plan=P.plan_order(16), doubling_sum=True) if factorised else {}
+    ex = True if concurrent else None
+    names = {"a": "a", "b": "b", "theta": "theta", "g": "estimate", "f": "residual",
+             "l": "accel_estimate", "r": "accel_residual", "omega": "omega", "ns": "ns_part"}
+
+    def fields(st):
+        return {"theta": st.theta, "g": st.inner.estimate, "f": st.inner.residual,
+                "l": st.inner.accel_estimate, "r": st.inner.accel_residual,
+                "omega": st.omega, "ns": st.ns_part}
+
+    def in_flight(st):
+        host = {k: v.cpu().pin_memory() for k, v in fields(st).items() if v is not None}
+        host["a"], host["b"] = sp.matrix.cpu().pin_memory(), bd.cpu().pin_memory()
+        up, down = torch.cuda.Stream(), torch.cuda.Stream()
+        main = torch.cuda.current_stream()
+        up.wait_stream(main)
+        d, ready = {}, {}
+        with torch.cuda.stream(up):
+            torch.cuda._sleep(20_000_000)  # the step must wait, not race
+            for k in ("f", "g", "ns", "omega", "theta", "b", "a", "l", "r"):
+                if k not in host:
+                    continue
+                d[k] = host[k].to("cuda", non_blocking=True)
+                d[k].record_stream(main)
+                ready[names[k]] = torch.cuda.Event()
+                ready[names[k]].record(up)
+        inner = P.DoubleNsState(estimate=d["g"], residual=d["f"], accel_estimate=d["l"],
+                                accel_residual=d["r"], step=st.inner.step, order=16,
+                                series_order=st.inner.series_order, ctr=P.MulCounter())
+        st2 = P.RichardsonState(theta=d["theta"], inner=inner, q=16, omega=d.get("omega"),
+                                ns_part=d.get("ns"), step=st.step, ctr=inner.ctr)
+        outs = ("accel_estimate", "accel_residual", "estimate", "residual", "ns_part", "omega",
+                "theta")
+        done = {k: torch.cuda.Event() for k in outs}
+        new = P.richardson_recursive_step(st2, d["a"], d["b"], executor=ex, inputs_ready=ready,
+                                          outputs_done=done, **kw)
+        back = {}
+        rev = {v: k for k, v in names.items()}
+        for k in outs:
+            v = fields(new)[rev[k]]
+            down.wait_event(done[k])
+            v.record_stream(down)
+            with torch.cuda.stream(down):
+                back[rev[k]] = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+                back[rev[k]].copy_(v, non_blocking=True)
+        down.synchronize()
+        return new, back
+
+    with P.gemm_backend(backend, moduli=16, min_dim=1024) if backend == "ozaki" \
+            else P.gemm_backend("dmma"):
+        st = P.initial_richardson(sp, bd, order=16, q=16)
+        for _ in range(2):  # the first call (no omega / ns_part yet), then the steady state
+            before = st.ctr.mmm
+            ref = P.richardson_recursive_step(st, sp.matrix, bd, executor=ex, **kw)
+            new, back = in_flight(st)
+            torch.cuda.synchronize()
+            for k, v in fields(ref).items():
+                assert torch.equal(v, fields(new)[k]), k
+                assert torch.equal(v.cpu(), back[k]), k
+            assert new.ctr.mmm == ref.ctr.mmm - before
+            st = ref
+    with pytest.raises(ValueError):
+        P.richardson_recursive_step(st, sp.matrix, bd, inputs_ready={"bogus": None})
