@@ -500,6 +500,11 @@ SI_API int si_set_ozaki_kernel(si_handle h, int variant);
 SI_API int si_ozaki_tune(int group_m, int l2_a, int l2_b);
 /* Tuning hook: shared-memory ring depth of the CTA-pair kernel (3..6). */
 SI_API int si_ozaki_tune_stages(int stages);
+/* Tuning hook: the longest K range one launch of the single-CTA INT8 kernel
+ * covers; longer products run as several launches that accumulate the
+ * residues (bitwise the unsplit result).  0 = never split (the default: the
+ * split was measured at K = 32768 and lost); a multiple of 128. */
+SI_API int si_ozaki_tune_ksplit(int64_t kmax);
 /* The first n moduli of the emulation. */
 SI_API int si_ozaki_moduli(int n, uint32_t* moduli);
 /* The INT8 tensor-core kernel alone (test hook): r[l] = (a[l] @ bt[l]^T) mod

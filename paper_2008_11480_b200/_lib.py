@@ -112,6 +112,7 @@ SIGNATURES: dict[str, list] = {
     "si_set_ozaki_kernel": [_P, _I],
     "si_ozaki_tune": [_I, _I, _I],
     "si_ozaki_tune_stages": [_I],
+    "si_ozaki_tune_ksplit": [_I64],
     "si_i8_gemm_mod": [_P, _P, _P, _P, _I64, _I64, _I64, _I, _P],
     "si_profile_i8": [_P, POINTER(c_double), POINTER(c_double), _PI64],
     "si_batched_ns_richardson": [_P, _I64, _I64, _P, _P, _I, _P, _I64, _P, _I64, _I, _P, _P, _P, _PI64, _P],

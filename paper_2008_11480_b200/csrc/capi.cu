@@ -1406,6 +1406,13 @@ int si_ozaki_tune_stages(int stages) {
   });
 }
 
+int si_ozaki_tune_ksplit(int64_t kmax) {
+  return guard([&] {
+    need(kmax >= 0 && kmax % 128 == 0, "kmax must be a non-negative multiple of 128");
+    oz::tune_ksplit(kmax);
+  });
+}
+
 int si_ozaki_moduli(int n, uint32_t* moduli) {
   return guard([&] {
     need(moduli != nullptr && n >= 1 && n <= oz::kMaxModuli, "bad arguments");

@@ -382,15 +382,29 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 // 256-column tile (from column `taddr`); the int32 sums are reduced exactly
 // mod m (u = v + 2^30 < 2^31, q = floor(u magic / 2^39)) and stored as one
 // byte per entry into row `row`, columns col0.. of the plane.
+// `accum`: the plane already holds the residues of an earlier K range of the
+// same product (launch_i8_gemm_mod's K split); they are added before the
+// reduction (|v| <= 2^29 per range, + 255: still below 2^31 after the shift).
 __device__ __forceinline__ void store_mod_row(uint32_t taddr, uint8_t* __restrict__ plane_base,
                                               int row, int col0, int M, int N, unsigned m,
-                                              unsigned magic, unsigned off) {
+                                              unsigned magic, unsigned off, bool accum = false) {
   uint8_t* rp = plane_base + (int64_t)row * N + col0;
   const bool vec = ((N & 15) == 0);
 #pragma unroll 1
   for (int c = 0; c < 256 / 32; ++c) {
     uint32_t v[32];
     tmem_ld32(taddr + (uint32_t)(c * 32), v);
+    if (accum && row < M && col0 + c * 32 < N) {
+      if (vec && col0 + c * 32 + 32 <= N) {
+        const uint4* src = reinterpret_cast<const uint4*>(rp + c * 32);
+        const uint4 p0 = src[0], p1 = src[1];
+        const uint32_t pw[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] += (pw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+      } else {
+        for (int i = 0; i < 32 && col0 + c * 32 + i < N; ++i) v[i] += rp[c * 32 + i];
+      }
+    }
     uint32_t w[8];
 #pragma unroll
     for (int i = 0; i < 32; i += 4) {
@@ -435,8 +449,9 @@ __device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int& plane,
 // R[l] = (A[l] @ Bt[l]^T) mod m_l, persistent over (plane, row tile, column tile)
 __global__ void __launch_bounds__(GTHREADS, 1)
     i8_gemm_mod_kernel(const __grid_constant__ CUtensorMap tmA,
-                       const __grid_constant__ CUtensorMap tmB, uint8_t* __restrict__ R, int M,
-                       int N, int Kp, int nplanes, const __grid_constant__ ModTab mt, int group_m) {
+                       const __grid_constant__ CUtensorMap tmB, uint8_t* R, int M,
+                       int N, int kb0, int kblocks, int accum, int nplanes,
+                       const __grid_constant__ ModTab mt, int group_m) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -452,8 +467,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
   const int lane = threadIdx.x & 31;
   const int num_m = (M + GBM - 1) / GBM;
   const int num_n = (N + GBN - 1) / GBN;
-  const int total = num_m * num_n * nplanes;
-  const int kblocks = Kp / GBK;
+  const int total = num_m * num_n * nplanes;  // k-blocks [kb0, kb0 + kblocks) of every tile
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < GSTAGES; ++s) {
@@ -492,8 +506,8 @@ __global__ void __launch_bounds__(GTHREADS, 1)
           mbar_wait(empty_bar(stage), phase ^ 1u);
           const uint32_t sa = base + stage * GSTAGE_BYTES;
           mbar_expect_tx(full_bar(stage), GSTAGE_BYTES);
-          tma_load_3d(sa, &tmA, full_bar(stage), kb * GBK, tm * GBM, plane);
-          tma_load_3d(sa + GA_BYTES, &tmB, full_bar(stage), kb * GBK, tn * GBN, plane);
+          tma_load_3d(sa, &tmA, full_bar(stage), (kb0 + kb) * GBK, tm * GBM, plane);
+          tma_load_3d(sa + GA_BYTES, &tmB, full_bar(stage), (kb0 + kb) * GBK, tn * GBN, plane);
           if (++stage == GSTAGES) {
             stage = 0;
             phase ^= 1u;
@@ -547,7 +561,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       const int row = tm * GBM + q * 32 + lane;
       const int col0 = tn * GBN;
       store_mod_row(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * GBN),
-                    R + (int64_t)plane * M * N, row, col0, M, N, m, magic, off);
+                    R + (int64_t)plane * M * N, row, col0, M, N, m, magic, off, accum != 0);
       tc_fence_before();
       mbar_arrive(tempty_bar(acc));
       if (++acc == 2) {
@@ -1203,6 +1217,7 @@ const Consts& consts() {
 std::atomic<int> g_pair_group_m{8}, g_pair_l2a{0}, g_pair_l2b{0};  // pair: 2048-row groups
 std::atomic<int> g_single_group_m{GROUP_M};
 std::atomic<int> g_pair_stages{4};  // smem ring depth of the pair kernel (3..6; tuning hook)
+std::atomic<int64_t> g_ksplit{0};  // longest K range of one single-CTA launch (0: no split)
 
 int num_sms() {
   int dev = 0, n = 0;
@@ -1243,6 +1258,8 @@ inline int64_t kpad(int64_t K) { return (K + GBK - 1) / GBK * GBK; }
 }  // namespace
 
 unsigned modulus(int l) { return kmod(l); }
+
+void tune_ksplit(int64_t kmax) { g_ksplit = kmax > 0 ? kmax : 0; }
 
 void tune_pair_stages(int stages) {
   if (stages >= 3 && stages <= 6) g_pair_stages = stages;
@@ -1291,6 +1308,17 @@ size_t workspace_bytes(int64_t M, int64_t N, int64_t K, int nmod, int64_t max_co
          align256((size_t)nmod * nc * Kp) + align256((size_t)nmod * mc * nc);
 }
 
+// kernel launches launch_i8_gemm_mod makes for one call (the K ranges)
+static int i8_launch_count(int64_t Kp, int variant) {
+  if (variant == kI8Pair || variant == kI8Multicast) return 1;
+  const int kblocks = (int)(Kp / GBK);
+  const int64_t ks = g_ksplit.load();
+  const int maxb = ks > 0 ? (int)std::max<int64_t>(1, ks / GBK) : kblocks;
+  const int nranges = (kblocks + maxb - 1) / maxb;
+  const int per = (kblocks + nranges - 1) / nranges;
+  return (kblocks + per - 1) / per;
+}
+
 cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, int64_t M, int64_t N,
                                int64_t Kp, int nplanes, cudaStream_t s, int variant) {
   if (M <= 0 || N <= 0 || Kp <= 0 || Kp % GBK || nplanes < 1 || nplanes > kMaxModuli ||
@@ -1326,8 +1354,22 @@ cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, in
   } else {
     const int64_t tiles = ((M + GBM - 1) / GBM) * ((N + GBN - 1) / GBN) * nplanes;
     const int grid = (int)(tiles < sms ? tiles : sms);
-    i8_gemm_mod_kernel<<<grid, GTHREADS, GSMEM, s>>>(ta, tb, R, (int)M, (int)N, (int)Kp, nplanes,
-                                                     consts().mt, g_single_group_m.load());
+    // K split (tuning hook, off by default): K can run as ranges of <= g_ksplit,
+    // each later range adding the residues already in R before its reduction
+    // -- the same integers mod m_l, bitwise.  Measured at config 5 (K = 32768,
+    // where one launch moves 153 GB of DRAM bytes) it did not pay: two ranges
+    // of 16384 moved 2 x 118 GB and the step was 3% slower
+    // (profiles/ozaki_ksplit_r02.txt).
+    const int kblocks = (int)(Kp / GBK);
+    const int64_t ks = g_ksplit.load();
+    const int maxb = ks > 0 ? (int)std::max<int64_t>(1, ks / GBK) : kblocks;
+    const int nranges = (kblocks + maxb - 1) / maxb;
+    const int per = (kblocks + nranges - 1) / nranges;  // balanced ranges
+    for (int kb0 = 0; kb0 < kblocks; kb0 += per)
+      i8_gemm_mod_kernel<<<grid, GTHREADS, GSMEM, s>>>(ta, tb, R, (int)M, (int)N, kb0,
+                                                       std::min(per, kblocks - kb0), kb0 > 0,
+                                                       nplanes, consts().mt,
+                                                       g_single_group_m.load());
   }
   return cudaGetLastError();
 }
@@ -1408,7 +1450,7 @@ cudaError_t launch_gemm(const Mat& A, const Mat& B, Mat& D, const Epilogue& e, i
           cudaSuccess)
         return err;
       if (hook) hook(false, 0.0);
-      ++n;
+      n += i8_launch_count(Kp, w.variant);
       const int blocks = crt_blocks(mc, nc, sms);
       launch_crt(nmod, blocks, s, res, (int)mc, (int)nc, rmax, cmax, pa, pb, cs.crt[nmod],
                  D.p + i0 * D.ld + j0, D.ld, e.beta != 0.0 ? e.c + i0 * e.ldc + j0 : nullptr,

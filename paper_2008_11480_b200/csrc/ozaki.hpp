@@ -90,6 +90,10 @@ cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, in
 // (0 evict_normal, 1 evict_last, 2 evict_first); negative / zero keeps a value.
 void tune_pair(int group_m, int l2a, int l2b);
 void tune_pair_stages(int stages);
+// Longest K range one launch of the single-CTA kernel covers (longer products
+// run as several launches accumulating residues in R; 0 = never split, the
+// default).
+void tune_ksplit(int64_t kmax);
 
 // Moduli (pairwise coprime, <= 256) in the order the planes use them.
 unsigned modulus(int l);

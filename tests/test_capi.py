@@ -127,6 +127,7 @@ def test_backend_entry_points_validate_without_gpu():
     assert lib.si_ozaki_tune(-1, 0, 0) == E
     assert lib.si_ozaki_tune(0, 3, 0) == E
     assert lib.si_ozaki_tune_stages(2) == E and lib.si_ozaki_tune_stages(7) == E
+    assert lib.si_ozaki_tune_ksplit(-128) == E and lib.si_ozaki_tune_ksplit(100) == E
     assert lib.si_ozaki_moduli(0, None) == E
     mods = (ctypes.c_uint32 * 17)()
     assert lib.si_ozaki_moduli(17, mods) == E

@@ -75,6 +75,45 @@ def test_int8_kernel_exact(planes, m, n, kp, kernel):
         assert torch.equal(ref, r[l]), (l, int((ref != r[l]).sum()))
 
 
+@pytest.mark.parametrize("planes,m,n,kp", [(3, 300, 512, 4096), (2, 257, 777, 2048),
+                                           (16, 128, 256, 1024)])
+def test_int8_kernel_k_ranges(planes, m, n, kp):
+    """A long K runs as several launches of the single-CTA kernel, each later one
+    adding the residues already stored before its reduction (si_ozaki_tune_ksplit,
+    a tuning hook that is off by default): the same integers mod m_l for any
+    range length, ragged column counts (byte path) included."""
+    import paper_2008_11480_b200 as P
+    from paper_2008_11480_b200 import _lib
+
+    mods = P.ozaki_moduli(16)
+    g = torch.Generator(device="cuda").manual_seed(planes * 77 + kp)
+    a = torch.randint(-128, 128, (planes, m, kp), dtype=torch.int8, device="cuda", generator=g)
+    bt = torch.randint(-128, 128, (planes, n, kp), dtype=torch.int8, device="cuda", generator=g)
+    P.set_ozaki_kernel("single")
+    outs = []
+    try:
+        for ks in (0, 128, 512, 1536, 16384):
+            _lib.call("si_ozaki_tune_ksplit", ks)
+            outs.append(P.i8_gemm_mod(a, bt).clone())
+    finally:
+        _lib.call("si_ozaki_tune_ksplit", 0)
+        P.set_ozaki_kernel("auto")
+    for l in range(planes):
+        ref = torch.remainder(a[l].double() @ bt[l].double().T, mods[l]).to(torch.uint8)
+        for r in outs:
+            assert torch.equal(ref, r[l]), l
+    # and through a whole emulated product (K = 2048 in ranges of 512)
+    rng = np.random.default_rng(3)
+    x, y = (torch.from_numpy(rng.standard_normal((600, 2048))).cuda(),
+            torch.from_numpy(rng.standard_normal((2048, 520))).cuda())
+    whole = _ozaki(x, y)
+    try:
+        _lib.call("si_ozaki_tune_ksplit", 512)
+        assert torch.equal(_ozaki(x, y), whole)
+    finally:
+        _lib.call("si_ozaki_tune_ksplit", 0)
+
+
 def test_int8_kernel_extreme_residues():
     """All-(-128) operands: the largest int32 sums the kernel's reduction sees."""
     import paper_2008_11480_b200 as P
