@@ -1564,7 +1564,9 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 5; our arm's c1 / c2 / c3 default to 15000 / "
+                         "120 / 300 so the timed region is >= 2 s and the clock sampler sees it)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c4")
@@ -1599,6 +1601,11 @@ def main():
     args = ap.parse_args()
     if args.gpus < 1:
         ap.error("--gpus must be >= 1")
+    if args.steps is None:
+        short = {"c1": 15000, "c2": 120, "c3": 300}  # sub-20-ms steps: a >= 2 s timed region
+        args.steps = short.get(args.config, 5) if args.impl == "ours" else 5
+    if args.steps < 1:
+        ap.error("--steps must be >= 1")
     env_world = os.environ.get("WORLD_SIZE")
     if env_world is None and args.gpus > 1:
         # not launched by torchrun: start the N ranks ourselves (one per GPU)
