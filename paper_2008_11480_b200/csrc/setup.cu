@@ -336,11 +336,21 @@ bool cholesky_pd(Ctx& c, const MV& a, double pivot_tol, bool default_tol, int64_
       transpose_kernel<<<tg, 256, 0, c.s>>>(wpanel.v.p, m, NB, wt.v.p, ldt, status);
       h->launches += 2;
       check(cudaGetLastError(), "cholesky panel");
-      // trailing update A22 -= W W^T on the DMMA GEMM (in place: D == C)
-      MV a22 = view(w.v.p + (k0 + NB) * ld + k0 + NB, m, m, ld);
-      MV wl = view(wpanel.v.p, m, NB, NB);
-      MV wr = view(wt.v.p, NB, m, ldt);
-      gemm(c, a22, wl, wr, -1.0, &a22, 1.0, 0.0, false);
+      // trailing update A22 -= W W^T on the DMMA GEMM (in place: D == C).  Only
+      // the lower triangle is ever read again (the diagonal blocks and the
+      // panels below them), so large trailing matrices are updated in row
+      // strips, each up to its own last column: ~(1 + 1/strips)/2 of the
+      // product (the k order per entry is unchanged: same pivots, bitwise).
+      double* a22p = w.v.p + (k0 + NB) * ld + k0 + NB;
+      const int64_t strips = m >= 4096 ? std::min<int64_t>(8, m / 2048) : 1;
+      const int64_t sr = ((m + strips - 1) / strips + NB - 1) / NB * NB;
+      for (int64_t i0 = 0; i0 < m; i0 += sr) {
+        const int64_t i1 = std::min(m, i0 + sr);
+        MV a22 = view(a22p + i0 * ld, i1 - i0, i1, ld);
+        MV wl = view(wpanel.v.p + i0 * NB, i1 - i0, NB, NB);
+        MV wr = view(wt.v.p, NB, i1, ldt);
+        gemm(c, a22, wl, wr, -1.0, &a22, 1.0, 0.0, false);
+      }
     }
     check(cudaGetLastError(), "cholesky diag");
     // early exit: look at the status every 16 panels
