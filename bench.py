@@ -666,6 +666,30 @@ class Workload:
         else:
             self.st = P.ns_step(self.st, self.sp.matrix)
 
+    def e2e_outputs_match(self, host) -> bool:
+        """The outputs an e2e step left in ``host["out"]`` against the device-resident
+        step from the same state (c4 / c3): bitwise, since the gated / row-block
+        step computes the same products in the same order.  Untimed."""
+        import torch
+
+        P = self.P
+        if self.cfg == "c4":
+            ref = P.composite_step(self.st, self.sp.matrix, self.sp, self.spec, 2,
+                                   executor=self.executor)
+        else:
+            ref = P.ns_step(self.st, self.sp.matrix, plan=self.plan8)
+        theta = P.plain_richardson(self.theta, self.st.estimate, self.sp.matrix, self.b,
+                                   P.MulCounter())
+        ok = True
+        for key, dev in (("g", ref.estimate), ("f", ref.residual), ("theta", theta)):
+            back = host["out"][key].to(dev.device, non_blocking=True).reshape(dev.shape)
+            if not torch.equal(back, dev):
+                ok = False
+                print(f"bench: e2e output {key!r} differs from the device-resident step: "
+                      f"max |diff| {(back - dev).abs().max().item():.3e}", file=sys.stderr)
+            del back
+        return ok
+
     def e2e_step(self, host):
         """The public API called with HOST inputs: H2D of the step's inputs from pinned
         memory, the step, D2H of its result; returns (h2d_bytes, d2h_bytes)."""
@@ -696,7 +720,9 @@ class Workload:
         up.wait_stream(main)
         d, ev = {}, {}
         n = self.n
-        npanels = 8
+        # row panels of the inputs = row blocks of G' / F'; at least 1024 rows each,
+        # so every block product stays on the emulated backend (its min_dim)
+        npanels = int(os.environ.get("SI_BENCH_E2E_PANELS", "0")) or max(1, min(8, n // 1024))
         bounds = [n * p // npanels for p in range(npanels + 1)]
         h = _lib.handle(dev.index)
         self._e2e_epoch += 1
@@ -1483,6 +1509,15 @@ def run_ours(args):
         e_ms = max_over_ranks(f0.elapsed_time(f1), world)
         e2e = {"value": world * ksteps / (e_ms / 1e3), "unit": "iters/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": ksteps}
+        # what the last timed e2e step read back is the device-resident step's
+        # result (every step starts from the same host state)
+        if w.e2e_outputs_match(host):
+            e2e["outputs"] = "bitwise equal to the device-resident step from the same state"
+        else:
+            print("bench: the e2e step's outputs differ from the device-resident step", file=sys.stderr)
+            e2e = {"invalid": "e2e outputs differ from the device-resident step", **e2e}
+            e2e["value"] = None
+        torch.cuda.synchronize()
         del host
 
     if not args.no_e2e and args.config == "c5" and w.sharded is None:
