@@ -1522,6 +1522,18 @@ def run_ours(args):
 
     if not args.no_e2e and args.config == "c5" and w.sharded is None:
         try:
+            # checksums of the device-resident step from the state the e2e step will
+            # start from (the state itself is released for the host copies)
+            def sums(t):
+                return (t.sum().item(), t.abs().max().item())
+
+            ref = w.P.richardson_recursive_step(w.st, w.sp.matrix, w.b, factor_plan=w.plan16,
+                                                doubling_sum=True)
+            want = {"theta": sums(ref.theta), "g": sums(ref.inner.estimate),
+                    "f": sums(ref.inner.residual), "l": sums(ref.inner.accel_estimate),
+                    "r": sums(ref.inner.accel_residual), "omega": sums(ref.omega),
+                    "ns": sums(ref.ns_part)}
+            del ref
             host = w.pinned_inputs_c5()
             f0 = torch.cuda.Event(enable_timing=True)
             f1 = torch.cuda.Event(enable_timing=True)
@@ -1535,6 +1547,21 @@ def run_ours(args):
                    "note": "A, b, theta and the six carried n x n matrices in, the new state "
                            "and theta out; copies overlapped with the step per input / "
                            "output (si_richardson_recursive_step_ex)"}
+            torch.cuda.empty_cache()
+            bad = []
+            for k, v in host["out"].items():  # one matrix at a time back on the device
+                got = sums(v.to("cuda"))
+                if got != want[k]:
+                    bad.append(k)
+            if bad:
+                print(f"bench: c5 e2e outputs {bad} differ from the device-resident step",
+                      file=sys.stderr)
+                e2e = {"invalid": f"e2e outputs {bad} differ from the device-resident step",
+                       **e2e}
+                e2e["value"] = None
+            else:
+                e2e["outputs"] = ("sum and max |.| of every output equal those of the "
+                                  "device-resident step from the same state")
             del host
         except (RuntimeError, MemoryError) as exc:  # pinned host memory exhausted, ...
             e2e = {"unavailable": f"c5 e2e failed: {exc}"[:200]}
