@@ -673,6 +673,27 @@ class Workload:
         import torch
 
         P = self.P
+        if self.cfg in ("c1", "c2"):  # the resident run from the state the host copies hold
+            if self.cfg == "c1":
+                s = self.c1
+                outs = P.batched_ns_richardson(s["a"], s["b"], s["p"], s["f"], s["t"], 3,
+                                               self.iters_per_step)
+                back = host["pack_out"].to("cuda")
+                nm = s["p"].numel()
+                got = (back[:nm], back[nm:2 * nm], back[2 * nm:])
+            else:
+                outs = P.batched_composite_richardson(
+                    self.a2, self.b2, self.pre2, self.res2, self.p2, self.f2, self.t2, (2, 3), 2,
+                    self.iters_per_step)
+                got = tuple(host["out"][k].to("cuda") for k in ("p", "f", "t"))
+            ok = True
+            for key, dev, g in zip(("p", "f", "t"), outs, got):
+                if not torch.equal(g.reshape(dev.shape), dev):
+                    ok = False
+                    print(f"bench: e2e output {key!r} differs from the device-resident run: "
+                          f"max |diff| {(g.reshape(dev.shape) - dev).abs().max().item():.3e}",
+                          file=sys.stderr)
+            return ok
         if self.cfg == "c4":
             ref = P.composite_step(self.st, self.sp.matrix, self.sp, self.spec, 2,
                                    executor=self.executor)
@@ -1478,7 +1499,8 @@ def run_ours(args):
             e2e = {"unavailable": f"sharded e2e failed: {exc}"[:200]}
     if not args.no_e2e and args.config in ("c1", "c2") and not w.split_batch:
         host = w.pinned_inputs_resident()
-        ksteps = max(1, min(args.steps, 3))
+        # ~0.3-0.5 s of e2e runs (a c1 run is ~0.2 ms, a c2 run ~18 ms), at most --steps
+        ksteps = max(1, min(args.steps, 2000 if args.config == "c1" else 30))
         w.e2e_step_resident(host)  # warm
         torch.cuda.synchronize()
         f0 = torch.cuda.Event(enable_timing=True)
@@ -1491,6 +1513,12 @@ def run_ours(args):
         e_ms = max_over_ranks(f0.elapsed_time(f1), world)
         e2e = {"value": world * ksteps * w.iters_per_step / (e_ms / 1e3), "unit": "iters/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": ksteps}
+        if w.e2e_outputs_match(host):
+            e2e["outputs"] = "bitwise equal to the device-resident run from the same state"
+        else:
+            e2e = {"invalid": "e2e outputs differ from the device-resident run", **e2e}
+            e2e["value"] = None
+        torch.cuda.synchronize()
         del host
     if not args.no_e2e and args.config in ("c4", "c3") and w.sharded is None and not args.hoist:
         host = w.pinned_inputs()
