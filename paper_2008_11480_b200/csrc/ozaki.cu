@@ -385,24 +385,32 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 // `accum`: the plane already holds the residues of an earlier K range of the
 // same product (launch_i8_gemm_mod's K split); they are added before the
 // reduction (|v| <= 2^29 per range, + 255: still below 2^31 after the shift).
+// (a template parameter: the default instantiation is the plain epilogue, and
+// every index into v[] stays a compile-time constant -- a dynamically indexed
+// v[] would live in local memory and slow the epilogue of every launch)
+template <bool ACCUM = false>
 __device__ __forceinline__ void store_mod_row(uint32_t taddr, uint8_t* __restrict__ plane_base,
                                               int row, int col0, int M, int N, unsigned m,
-                                              unsigned magic, unsigned off, bool accum = false) {
+                                              unsigned magic, unsigned off) {
   uint8_t* rp = plane_base + (int64_t)row * N + col0;
   const bool vec = ((N & 15) == 0);
 #pragma unroll 1
   for (int c = 0; c < 256 / 32; ++c) {
     uint32_t v[32];
     tmem_ld32(taddr + (uint32_t)(c * 32), v);
-    if (accum && row < M && col0 + c * 32 < N) {
-      if (vec && col0 + c * 32 + 32 <= N) {
-        const uint4* src = reinterpret_cast<const uint4*>(rp + c * 32);
-        const uint4 p0 = src[0], p1 = src[1];
-        const uint32_t pw[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+    if constexpr (ACCUM) {
+      if (row < M && col0 + c * 32 < N) {
+        if (vec && col0 + c * 32 + 32 <= N) {
+          const uint4* src = reinterpret_cast<const uint4*>(rp + c * 32);
+          const uint4 p0 = src[0], p1 = src[1];
+          const uint32_t pw[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] += (pw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-      } else {
-        for (int i = 0; i < 32 && col0 + c * 32 + i < N; ++i) v[i] += rp[c * 32 + i];
+          for (int i = 0; i < 32; ++i) v[i] += (pw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (col0 + c * 32 + i < N) v[i] += rp[c * 32 + i];
+        }
       }
     }
     uint32_t w[8];
@@ -447,10 +455,11 @@ __device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int& plane,
 }
 
 // R[l] = (A[l] @ Bt[l]^T) mod m_l, persistent over (plane, row tile, column tile)
+template <bool ACCUM>
 __global__ void __launch_bounds__(GTHREADS, 1)
     i8_gemm_mod_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, uint8_t* R, int M,
-                       int N, int kb0, int kblocks, int accum, int nplanes,
+                       int N, int kb0, int kblocks, int nplanes,
                        const __grid_constant__ ModTab mt, int group_m) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -560,8 +569,8 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       tc_fence_after();
       const int row = tm * GBM + q * 32 + lane;
       const int col0 = tn * GBN;
-      store_mod_row(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * GBN),
-                    R + (int64_t)plane * M * N, row, col0, M, N, m, magic, off, accum != 0);
+      store_mod_row<ACCUM>(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * GBN),
+                           R + (int64_t)plane * M * N, row, col0, M, N, m, magic, off);
       tc_fence_before();
       mbar_arrive(tempty_bar(acc));
       if (++acc == 2) {
@@ -1232,7 +1241,11 @@ cudaError_t set_gemm_attr() {
   cudaGetDevice(&dev);
   if (dev < 64 && (done.load() & (1ull << dev))) return cudaSuccess;
   cudaError_t e =
-      cudaFuncSetAttribute(i8_gemm_mod_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GSMEM);
+      cudaFuncSetAttribute(i8_gemm_mod_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           GSMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(i8_gemm_mod_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             GSMEM);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(i8_gemm_mod_pair_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              psmem(3));
@@ -1365,11 +1378,12 @@ cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, in
     const int maxb = ks > 0 ? (int)std::max<int64_t>(1, ks / GBK) : kblocks;
     const int nranges = (kblocks + maxb - 1) / maxb;
     const int per = (kblocks + nranges - 1) / nranges;  // balanced ranges
-    for (int kb0 = 0; kb0 < kblocks; kb0 += per)
-      i8_gemm_mod_kernel<<<grid, GTHREADS, GSMEM, s>>>(ta, tb, R, (int)M, (int)N, kb0,
-                                                       std::min(per, kblocks - kb0), kb0 > 0,
-                                                       nplanes, consts().mt,
-                                                       g_single_group_m.load());
+    for (int kb0 = 0; kb0 < kblocks; kb0 += per) {
+      auto kern = kb0 > 0 ? i8_gemm_mod_kernel<true> : i8_gemm_mod_kernel<false>;
+      kern<<<grid, GTHREADS, GSMEM, s>>>(ta, tb, R, (int)M, (int)N, kb0,
+                                         std::min(per, kblocks - kb0), nplanes, consts().mt,
+                                         g_single_group_m.load());
+    }
   }
   return cudaGetLastError();
 }
