@@ -1371,7 +1371,7 @@ cudaError_t launch_i8_gemm_mod(const int8_t* A, const int8_t* Bt, uint8_t* R, in
     // each later range adding the residues already in R before its reduction
     // -- the same integers mod m_l, bitwise.  Measured at config 5 (K = 32768,
     // where one launch moves 153 GB of DRAM bytes) it did not pay: two ranges
-    // of 16384 moved 2 x 118 GB and the step was 3% slower
+    // of 16384 moved 2 x 118 GB and the step was 1% slower
     // (profiles/ozaki_ksplit_r02.txt).
     const int kblocks = (int)(Kp / GBK);
     const int64_t ks = g_ksplit.load();

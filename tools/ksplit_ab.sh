@@ -1,6 +1,6 @@
 #!/bin/bash
-# A/B of the INT8 kernel's K split at config 5 (n = 32768), same box: the
-# default (ranges of 16384) against no split; then the kernel's DRAM bytes.
+# A/B of the INT8 kernel's K split at config 5 (n = 32768), same box: ranges
+# of 16384 against no split (the default).
 set -e
 mkdir -p gpurun_out
 run() {  # $1 = kmax, $2 = tag
@@ -18,10 +18,7 @@ d = json.loads(open('gpurun_out/ksplit_$2.json').read().strip().splitlines()[-1]
 print('$2', d['value'], d['ms_per_step'], d['roofline']['achieved'], d['roofline']['frac'], d['clocks'])
 "
 }
-run 16384 split
 run 0 nosplit
-run 16384 split2
+run 16384 split
 run 0 nosplit2
-M="dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,lts__t_sector_hit_rate.pct"
-ncu --metrics $M --clock-control none -k regex:i8_gemm_mod -s 2 -c 4 --csv \
-    --log-file gpurun_out/ncu_i8_dram_32768_ksplit.csv python tools/ozaki_one.py 32768 16 > /dev/null
+run 16384 split2
